@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""Benchmark: FD preconditioner application DOF/s (complex FP64) on B200.
+
+Headline workload (BASELINE.json configs[2], "c3"): d=3 space + time on
+[0,1]^3 x [0,1], p=2, maximal regularity, 64 elements per direction,
+reduced dims (65, 64, 64, 64) = 17,039,360 complex DOF; RHS re/im i.i.d.
+U[-1,1] from seed 1234. configs[1] (d=2, 279K DOF) is latency-bound and is
+reported as the full-solve leg ("solve_c2"); c3 is the largest single-GPU
+config the metric's roofline target is quoted on.
+
+A "step" is one FD preconditioner application over the whole c3 tensor with
+the input resident in HBM. `value` = DOF/s over all ranks; `e2e` = the same
+through the public host-pointer API (H2D of r and D2H of z inside the timed
+region, pinned host memory). The tensor (272 MB) is larger than L2 (126 MB),
+so no explicit flush is needed between steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (d, p, n_el, n_el_time)
+    "c1": (1, 3, 64, 64),
+    "c2": (2, 3, 64, 64),
+    "c3": (3, 2, 64, 64),
+    "c5": (3, 4, 128, 128),
+}
+
+
+def fd_flops_per_dof(dims, p):
+    # F_alg = 8 * sum_l n_l + 24 p + 8 (dense transforms + pivoted banded solve)
+    return 8 * sum(dims[1:]) + 24 * p + 8
+
+
+def matvec_flops_per_dof(d, p):
+    return 24 * d * (2 * p + 1)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+        return rank, ws, local, dist
+    return rank, ws, local, None
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def max_over_ranks(dist, v):
+    if dist is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def rhs(n, seed=1234):
+    """RHS re/im i.i.d. U[-1,1] (bench-side generator; the oracle has its own MT19937-64)."""
+    g = np.random.default_rng(seed)
+    v = np.empty(n, dtype=np.complex128)
+    v.real = g.uniform(-1.0, 1.0, n)
+    v.imag = g.uniform(-1.0, 1.0, n)
+    return v
+
+
+def cpu_baseline_fd(cfg, r, steps=1):
+    """Reference CPU path on the host cores: oracle/_ref (reference sources) if built,
+    else the C restatement (port). Single-threaded like the reference."""
+    from oracle import oracle as O
+    import paper_2311_18461_b200 as ks
+    d, p, n_el, n_el_t = CONFIGS[cfg]
+    kind = "port"
+    ref = None
+    try:
+        from oracle import refdrv
+        if refdrv.available():
+            ref = refdrv.RefProblem(d, p, n_el, n_el_t)
+            kind = "reference"
+    except Exception:
+        ref = None
+    if ref is None:
+        O.build_oracle()
+        prob = ks.SpaceTimeProblem.uniform(d, p, n_el, n_el_t)
+        Lt, Mt, Wt = prob.time_bands()
+        U, lam = zip(*[prob.eig(l) for l in range(d)])
+        fd = O.OracleFD(prob.reduced_dims(), 1.0, p, U, lam, Lt, Mt, Wt)
+        apply = fd.apply
+    else:
+        apply = ref.fd_apply
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        apply(r)
+        times.append(time.perf_counter() - t0)
+    return kind, float(np.median(times)), len(times)
+
+
+def run_reference_arm(args, rank, ws, dist):
+    if rank != 0:
+        return
+    cfg = args.config
+    d, p, n_el, n_el_t = CONFIGS[cfg]
+    n = 1
+    import paper_2311_18461_b200 as ks
+    prob = ks.SpaceTimeProblem.uniform(d, p, n_el, n_el_t)
+    n = prob.N_dof
+    r = rhs(n)
+    # bounded: one warm-up at most, steps capped so the arm ends within minutes
+    kind, _, _ = cpu_baseline_fd(cfg, r, steps=min(args.warmup, 1))
+    steps = max(1, min(args.steps, 4))
+    kind, med, used = cpu_baseline_fd(cfg, r, steps=steps)
+    val = n / med
+    line = {
+        "metric": "fd_apply_dof_per_s", "value": val, "unit": "DOF/s", "n_gpus": ws,
+        "steps": used, "warmup": min(args.warmup, 1), "ms_per_step": med * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"{cfg}: d={d} p={p} n_el={n_el} FD apply", "dofs": n},
+        "cpu_baseline": {"value": val, "unit": "DOF/s", "cores": 1, "kind": kind,
+                         "sample": f"{used} full {cfg} FD applications (median), single thread"},
+        "e2e": {"value": val, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-solve", action="store_true")
+    args = ap.parse_args()
+    rank, ws, local, dist = dist_init()
+    if args.impl == "reference":
+        run_reference_arm(args, rank, ws, dist)
+        return
+    import paper_2311_18461_b200 as ks
+    ks.lib()
+    if ks.device_count() < 1:
+        raise SystemExit("no CUDA device: libks has no CPU fallback")
+    ks.lib().ks_set_device(local)
+    d, p, n_el, n_el_t = CONFIGS[args.config]
+    W = max(args.warmup, 3)
+    K = args.steps
+
+    t_setup = time.perf_counter()
+    prob = ks.SpaceTimeProblem.uniform(d, p, n_el, n_el_t)
+    P = ks.FDPreconditioner(prob, device=local)
+    A = ks.assemble_system_operator(prob, device=local)
+    setup_s = time.perf_counter() - t_setup
+    dims = prob.reduced_dims()
+    n = prob.N_dof
+    r_host = rhs(n)
+    r = ks.DeviceVector.from_host(r_host)
+    z = ks.DeviceVector(n)
+    y = ks.DeviceVector(n)
+    dfma, dmma = ks.fp64_peaks()
+    fp64_peak = max(dfma, dmma)
+
+    # ---- device-resident FD apply (the headline) ----
+    P.time(r, z, W, flush=False)
+    barrier(dist)
+    ks.lib().ks_synchronize()
+    ks.reset_launch_count()
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        ms_fd, ms_gemm = P.time(r, z, K, flush=False)
+        ks.lib().ks_synchronize()
+        wall_fd = time.perf_counter() - t0
+    launches = ks.launch_count()
+    barrier(dist)
+    ms_fd = max_over_ranks(dist, ms_fd)
+    value = ws * n / (ms_fd * 1e-3)
+
+    # ---- matvec ----
+    A.time(r, y, W, flush=False)
+    ms_mv = max_over_ranks(dist, A.time(r, y, K, flush=False))
+
+    # ---- e2e through the public host-pointer API (pinned host buffers) ----
+    import ctypes as C
+    hp, hz = C.c_void_p(), C.c_void_p()
+    ks._check(ks.lib().ks_host_alloc(C.byref(hp), n * 16))
+    ks._check(ks.lib().ks_host_alloc(C.byref(hz), n * 16))
+    rin = np.ctypeslib.as_array(C.cast(hp, C.POINTER(C.c_double)), (2 * n,)).view(np.complex128)
+    zout = np.ctypeslib.as_array(C.cast(hz, C.POINTER(C.c_double)), (2 * n,)).view(np.complex128)
+    rin[:] = r_host
+    for _ in range(2):
+        P.apply(rin, zout)
+    barrier(dist)
+    t0 = time.perf_counter()
+    for _ in range(K):
+        P.apply(rin, zout)
+    e2e_s = (time.perf_counter() - t0) / K
+    e2e_s = max_over_ranks(dist, e2e_s)
+    e2e_val = ws * n / e2e_s
+    check = float(np.abs(zout).sum())  # the step's result was read back on the host
+
+    # ---- full solves (device-resident PCG) ----
+    solves = {}
+    if not args.no_solve:
+        b = ks.DeviceVector.from_host(r_host)
+        rep = ks.pcg(A, P, b, ks.PcgOptions(1e-8, 200))
+        solves[f"solve_{args.config}"] = {"iterations": rep.iterations, "converged": rep.converged,
+                                          "seconds": rep.solve_seconds,
+                                          "final_relres": rep.res_history[-1] if rep.res_history else None}
+        if args.config == "c3":
+            p2 = ks.SpaceTimeProblem.uniform(*CONFIGS["c2"])
+            P2, A2 = ks.FDPreconditioner(p2, device=local), ks.assemble_system_operator(p2, device=local)
+            b2 = ks.DeviceVector.from_host(rhs(p2.N_dof))
+            ks.pcg(A2, P2, b2)
+            rep2 = ks.pcg(A2, P2, b2, ks.PcgOptions(1e-8, 200))
+            solves["solve_c2_random_rhs"] = {"iterations": rep2.iterations,
+                                             "converged": rep2.converged,
+                                             "seconds": rep2.solve_seconds,
+                                             "dofs": p2.N_dof}
+
+    # ---- roofline: dominant kernel = the spatial transform GEMM ----
+    gemm_flops = 2 * sum(4.0 * dims[l] * n for l in range(1, d + 1))  # fwd + inv, per apply
+    achieved = gemm_flops / (ms_gemm * 1e-3) / 1e12
+    pk = peaks()
+    fd_f = fd_flops_per_dof(dims, p) * n
+    fd_roof_s = max(fd_f / (fp64_peak * 1e12), 32.0 * n / (pk["hbm_gbs"] * 1e9))
+    mv_roof_s = max(matvec_flops_per_dof(d, p) * n / (fp64_peak * 1e12),
+                    32.0 * n / (pk["hbm_gbs"] * 1e9))
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        kind, sec, used = cpu_baseline_fd(args.config, r_host, steps=1)
+        cpu = {"value": n / sec, "unit": "DOF/s", "cores": 1, "kind": kind,
+               "sample": f"{used} full {args.config} FD application ({n} DOF), single thread, "
+                         "setup (block factorisation) excluded"}
+
+    if rank == 0:
+        line = {
+            "metric": "fd_apply_dof_per_s", "value": value, "unit": "DOF/s", "n_gpus": ws,
+            "steps": K, "warmup": W, "ms_per_step": ms_fd, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128 (complex FP64)",
+            "data": "synthetic (seeded U[-1,1] RHS, SURVEY 8(d))",
+            "config": {"workload": f"{args.config}: d={d} p={p} n_el={n_el} n_el_t={n_el_t}, "
+                                   "one FD preconditioner application per step",
+                       "dims": dims, "dofs": n,
+                       "parallelism": "replicas" if ws > 1 else "single",
+                       "l2": "inputs (272 MB/vector) larger than L2; no flush",
+                       "transform_engine": ["dfma", "dmma"][ks.lib().ks_transform_engine()]},
+            "e2e": {"value": e2e_val, "unit": "DOF/s", "h2d_bytes_per_step": n * 16,
+                    "d2h_bytes_per_step": n * 16, "ms_per_step": e2e_s * 1e3},
+            "gpu_launches": launches,
+            "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak,
+                         "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": None,
+                         "kernel": "k_mode_gemm (spatial transform)",
+                         "peak_source": "measured live: DFMA %.2f / DMMA %.2f TFLOP/s microbenchmarks"
+                                        % (dfma, dmma),
+                         "gemm_ms_per_apply": ms_gemm},
+            "fd_apply": {"ms": ms_fd, "roofline_ms": fd_roof_s * 1e3,
+                         "frac_of_roofline": fd_roof_s * 1e3 / ms_fd,
+                         "flops_per_dof": fd_flops_per_dof(dims, p), "wall_s": wall_fd},
+            "matvec": {"ms": ms_mv, "dof_per_s": ws * n / (ms_mv * 1e-3),
+                       "roofline_ms": mv_roof_s * 1e3, "frac_of_roofline": mv_roof_s * 1e3 / ms_mv,
+                       "plan": A.plan_info(),
+                       "hbm_gbs_effective": 32.0 * n / (ms_mv * 1e-3) / 1e9},
+            "solves": solves,
+            "setup_s": setup_s,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+            "checksum": check,
+        }
+        print(json.dumps(line), flush=True)
+    ks.lib().ks_host_free(hp)
+    ks.lib().ks_host_free(hz)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

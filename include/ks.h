@@ -1,0 +1,230 @@
+/*
+ * ks.h — C-ABI of the B200 (sm_100a) hot path of the space-time least-squares
+ * isogeometric Schroedinger solver (arXiv 2311.18461, reference "kronschro").
+ *
+ * This is the drop-in boundary. Every entry point replaces one reference C++
+ * interface; the reference file:line it stands in for is cited beside it
+ * (paths relative to the reference's proj/ directory). Only plain pointers,
+ * sizes and POD structs cross it: no torch or C++ types.
+ *
+ * Conventions shared with the reference:
+ *   - complex FP64 is interleaved (re, im): ks_c64 is layout-compatible with
+ *     std::complex<double> (include/kronschro/tensorops.hpp:15, kernels_avx2.cpp:10);
+ *   - tensors are linearised with axis 0 (time) fastest:
+ *     vec index = i_0 + n_0*(i_1 + n_1*(i_2 + ...)) (include/kronschro/tensorops.hpp:15-16);
+ *   - banded matrices use the LAPACK-style layout of BandedMatrix<T>: entry
+ *     (i,j), |i-j| <= bw, lives at data[bw + i - j + j*(2*bw+1)]
+ *     (include/kronschro/banded.hpp:11-13, :91-94);
+ *   - dense eigenvector matrices U_l are column-major n_l x n_l, as Eigen's
+ *     MatrixXd (include/kronschro/eigensolve.hpp:16-19).
+ *
+ * Errors: every int-returning call returns KS_OK or a KS_E* code and leaves a
+ * thread-local message in ks_last_error(). The C++ wrappers in
+ * kronschro_gpu.hpp rethrow the std exception the reference throws
+ * (invalid_argument / runtime_error / length_error).
+ *
+ * There is no CPU fallback: without a CUDA device every compute call returns
+ * KS_ECUDA.
+ */
+#ifndef KS_H_
+#define KS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct { double re, im; } ks_c64;
+
+enum ks_status {
+    KS_OK = 0,
+    KS_EINVAL = 1,     /* std::invalid_argument in the reference */
+    KS_ESINGULAR = 2,  /* std::runtime_error("factor_banded: numerically singular pivot"), eigensolve.cpp:105-106 */
+    KS_ECUDA = 3,      /* CUDA runtime failure / no device */
+    KS_ENOMEM = 4,     /* device allocation failed */
+    KS_ENCCL = 5,      /* collective failure (multi-GPU) */
+    KS_ELENGTH = 6     /* std::length_error (dense caps), tensorops.cpp:279, fdsolver.cpp:138-139 */
+};
+
+/* Where the vectors passed to an apply/solve call live. HOST means the call
+ * copies in and out (the reference-facing parity path); DEVICE means the
+ * pointers are device pointers on the handle's device (the HBM-resident path). */
+enum ks_mem { KS_MEM_HOST = 0, KS_MEM_DEVICE = 1 };
+
+const char* ks_last_error(void);
+int ks_version(void);
+/* Number of visible CUDA devices (0 on a CPU-only host; never throws). */
+int ks_device_count(void);
+
+/* ---------------------------------------------------------------------------
+ * Fast-diagonalisation preconditioner (Algorithm 1)
+ *
+ * Replaces  FDPreconditioner(const SpaceTimeProblem&, const UnivariateSet&)
+ *           (include/kronschro/fdsolver.hpp:58, src/fdsolver.cpp:124-126)
+ * The host keeps the reference's setup: build_univariate (assembly.cpp:146-160)
+ * and spatial_eigenbasis/generalized_sym_eig (fdsolver.cpp:23-44,
+ * eigensolve.cpp:8-29) produce the inputs below; the N_s block factorisations
+ * (fdsolver.cpp:46-51, eigensolve.cpp:77-121) run on the GPU inside create.
+ *
+ *   d        number of spatial axes (1..3)
+ *   dims     d+1 ints: (n_t, n_1, ..., n_d) = SpaceTimeProblem::reduced_dims()
+ *   nu       the problem's nu (> 0)
+ *   p_t      time bandwidth (= time degree) of Lt, Mt, Wt
+ *   U        d pointers, U[l] column-major n_{l+1} x n_{l+1} (M-orthonormal eigenvectors)
+ *   lambda   d pointers, lambda[l] of length n_{l+1} (ascending eigenvalues)
+ *   Lt, Mt   real time bands, (2*p_t+1) x n_t, BandedMatrix<double> layout
+ *   Wt       complex time band (not yet symmetrised), same layout
+ * The composite eigenvalues lambda_i = sum_l lambda_l[i_l] (fdsolver.cpp:30-42)
+ * and the blocks H_i = Lt + nu^2 lambda_i^2 Mt + nu lambda_i (Wt + Wt^H)
+ * (fdsolver.cpp:95-120) are formed on the device.
+ * ------------------------------------------------------------------------- */
+typedef struct ks_fd ks_fd;
+
+int ks_fd_create(int d, const int* dims, double nu, int p_t,
+                 const double* const* U, const double* const* lambda,
+                 const double* Lt, const double* Mt, const ks_c64* Wt,
+                 int device, ks_fd** out);
+/* z = P^-1 r. Replaces FDPreconditioner::apply(const cplx* r, cplx* z) const
+ * (fdsolver.hpp:61 -> FastDiagSolver::solve, fdsolver.cpp:53-63). r and z may
+ * alias. stream is a cudaStream_t (NULL = the handle's own stream). */
+int ks_fd_apply(ks_fd* fd, const ks_c64* r, ks_c64* z, int mem, void* stream);
+/* Same as apply but with the adjoint block solves (FastDiagSolver::solve_adjoint,
+ * fdsolver.cpp:65-75, eigensolve.cpp:148-170). */
+int ks_fd_apply_adjoint(ks_fd* fd, const ks_c64* r, ks_c64* z, int mem, void* stream);
+size_t ks_fd_vec_size(const ks_fd* fd);                 /* fdsolver.hpp:63 */
+/* Composite eigenvalues in spatial vec order (fdsolver.hpp:64-66); out has N_s entries. */
+int ks_fd_eigenvalues(const ks_fd* fd, double* out);
+/* Copy the device-factored block of spatial eigen-index i back to the host in
+ * the BandedFactorization layout (eigensolve.hpp:36-42): ab is (3p+1) x n_t
+ * complex with ldab = 3p+1, piv has n_t ints. For parity tests. */
+int ks_fd_block(const ks_fd* fd, size_t i, ks_c64* ab, int* piv);
+int ks_fd_destroy(ks_fd* fd);
+
+/* ---------------------------------------------------------------------------
+ * Kronecker-sum operator (include/kronschro/tensorops.hpp:57-87)
+ *
+ * Replaces KroneckerOperator(dims) + add_term(coeff, factors) (tensorops.cpp:219-234).
+ * A term is coeff * (F_D x ... x F_1 x F_0); factor k acts on tensor axis k;
+ * a NULL factor is the identity. Factors are complex square bands of size
+ * dims[k] and bandwidth bw[k] (BandedMatrix<cplx> layout).
+ * ------------------------------------------------------------------------- */
+typedef struct {
+    ks_c64 coeff;
+    const ks_c64* const* factors; /* ndim pointers, NULL = identity */
+    const int* bw;                /* ndim bandwidths (ignored for NULL factors) */
+} ks_term;
+
+typedef struct ks_kron ks_kron;
+
+int ks_kron_create(int ndim, const int* dims, int nterms, const ks_term* terms,
+                   int device, ks_kron** out);
+/* y = K x (tensorops.cpp:236-254). x and y must not alias. */
+int ks_kron_apply(ks_kron* k, const ks_c64* x, ks_c64* y, int mem, void* stream);
+size_t ks_kron_vec_size(const ks_kron* k);
+/* Planner diagnostics: number of fused level passes and intermediate tensors. */
+int ks_kron_plan_info(const ks_kron* k, int* npasses, int* nnodes, int* nproducts);
+int ks_kron_destroy(ks_kron* k);
+
+/* ---------------------------------------------------------------------------
+ * Preconditioned CG (include/kronschro/krylov.hpp:11-38, src/krylov.cpp:24-114)
+ * Device-resident loop with the reference's control flow: zero initial guess,
+ * b = 0 -> converged in 0 iterations, breakdown on Re<p,Ap> <= 0, recurrence
+ * residual confirmed by a true residual at exit with <= 2 restarts, strict mode.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+    double tol;           /* PcgOptions::tol (default 1e-8) */
+    int maxit;            /* PcgOptions::maxit (default 200) */
+    int strict_residual;  /* PcgOptions::strict_residual */
+} ks_pcg_opts;
+
+typedef struct {
+    int iterations;
+    int converged;
+    int breakdown;
+    int restarts;
+    int hist_len;          /* entries written to res_hist (<= hist_cap) */
+    double matvec_seconds; /* device time (CUDA events) per component */
+    double precond_seconds;
+    double solve_seconds;
+} ks_pcg_report;
+
+/* P may be NULL (unpreconditioned, krylov.hpp:36). b and x are host or device
+ * per mem. res_hist (host, may be NULL) receives up to hist_cap relative
+ * residuals, one per iteration (SolveReport::res_history). */
+int ks_pcg(ks_kron* A, ks_fd* P, const ks_c64* b, ks_c64* x, int mem,
+           const ks_pcg_opts* opts, double* res_hist, int hist_cap,
+           ks_pcg_report* report);
+
+/* ---------------------------------------------------------------------------
+ * BLAS-1 (include/kronschro/kernels.hpp:13-48) on device vectors. Reductions
+ * are deterministic (fixed two-stage tree, no atomics).
+ * ------------------------------------------------------------------------- */
+int ks_axpy_real(double a, const ks_c64* x, ks_c64* y, size_t n, void* stream);
+int ks_axpy(ks_c64 a, const ks_c64* x, ks_c64* y, size_t n, void* stream);
+int ks_dotc(const ks_c64* x, const ks_c64* y, size_t n, ks_c64* out, void* stream);
+int ks_norm2sq(const ks_c64* x, size_t n, double* out, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Device memory / timing helpers (plumbing for the bench and tests)
+ * ------------------------------------------------------------------------- */
+int ks_set_device(int device);
+int ks_malloc(void** ptr, size_t bytes);
+int ks_free(void* ptr);
+/* kind: 0 = host->device, 1 = device->host, 2 = device->device */
+int ks_memcpy(void* dst, const void* src, size_t bytes, int kind);
+int ks_host_alloc(void** ptr, size_t bytes); /* pinned host memory */
+int ks_host_free(void* ptr);
+int ks_synchronize(void);
+/* Overwrite `bytes` of a device scratch buffer (L2 flush between timed runs). */
+int ks_flush_l2(size_t bytes);
+/* Time `iters` back-to-back launches of the FD apply / Kron apply on device
+ * pointers with CUDA events on the handle's stream; optional per-iteration
+ * L2 flush. ms_out receives the average ms per call and ms_kernel the
+ * average device time of the dominant kernel per call. */
+int ks_fd_time(ks_fd* fd, const ks_c64* r, ks_c64* z, int iters, int flush,
+               double* ms_out, double* ms_kernel);
+int ks_kron_time(ks_kron* k, const ks_c64* x, ks_c64* y, int iters, int flush,
+                 double* ms_out);
+/* Measured FP64 FMA peak (TFLOP/s) of this device, from a DFMA microbenchmark. */
+int ks_fp64_peak(double* tflops);
+/* Both FP64 peaks: CUDA-core DFMA and tensor-core DMMA (mma.sync m8n8k4 f64). */
+int ks_fp64_peaks(double* dfma_tflops, double* dmma_tflops);
+/* Which engine the spatial transforms use: 0 = DFMA, 1 = DMMA (env KS_GEMM). */
+int ks_transform_engine(void);
+/* Number of kernels the library launched since the last reset. */
+uint64_t ks_launch_count(void);
+void ks_launch_count_reset(void);
+
+/* ---------------------------------------------------------------------------
+ * Host setup (product-side mirror of the reference's shared setup; used when
+ * no reference process hands over its own setup products)
+ *   SpaceTimeProblem::uniform  (assembly.cpp:110-117)
+ *   build_univariate           (assembly.cpp:146-160)
+ *   generalized_sym_eig        (eigensolve.cpp:8-29)
+ *   assemble_system_operator   (assembly.cpp:202-257)
+ * ------------------------------------------------------------------------- */
+typedef struct ks_setup ks_setup;
+
+/* trial: 0 = initial-condition space (time drops first), 1 = final-condition. */
+int ks_setup_create(int d, int p, int n_el, int n_el_time, double T, double nu,
+                    int trial, ks_setup** out);
+int ks_setup_dims(const ks_setup* s, int* d, int* dims /* d+1 */, int* p);
+/* Copy the time bands (Lt, Mt real; Wt complex), each (2p+1) x n_t. */
+int ks_setup_time_bands(const ks_setup* s, double* Lt, double* Mt, ks_c64* Wt);
+/* Spatial axis l (0-based): M, L, G, V real bands (2p+1) x n_l (any may be NULL). */
+int ks_setup_space_bands(const ks_setup* s, int l, double* M, double* L,
+                         double* G, double* V);
+/* Eigenpairs of (L_l, M_l): U column-major n_l x n_l, lambda ascending. */
+int ks_setup_eig(const ks_setup* s, int l, double* U, double* lambda);
+int ks_setup_create_fd(const ks_setup* s, int device, ks_fd** out);
+/* The system operator A as the reference's term list (assembly.cpp:202-251). */
+int ks_setup_create_system(const ks_setup* s, int device, ks_kron** out);
+int ks_setup_destroy(ks_setup* s);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KS_H_ */

@@ -1,0 +1,746 @@
+// C-ABI implementation (include/ks.h): FD preconditioner, Kronecker operator,
+// device-resident PCG, BLAS-1 entry points, device plumbing and timing.
+#include "ks_internal.hpp"
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+
+namespace ks {
+
+std::atomic<uint64_t> g_launches{0};
+static thread_local std::string t_last_error;
+void set_last_error(const std::string& msg) { t_last_error = msg; }
+
+void ensure_device(int device) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        throw Error(KS_ECUDA, "no CUDA device available (libks has no CPU fallback)");
+    KS_REQUIRE(device >= 0 && device < n, KS_EINVAL, "device index out of range");
+    KS_CUDA(cudaSetDevice(device));
+}
+
+int transform_engine();
+
+// kron engine (ks_kron.cu)
+struct KronPlan;
+KronPlan* kron_plan(const std::vector<int>& dims,
+                                    const std::vector<std::vector<double2>>& bands,
+                                    const std::vector<int>& band_n, const std::vector<int>& band_bw,
+                                    const std::vector<double2>& coeffs,
+                                    const std::vector<std::vector<int>>& fids);
+void kron_apply(KronPlan& P, const double2* x, double2* y, cudaStream_t st,
+                std::vector<void*>& host_ptrs);
+void kron_plan_info(const KronPlan& P, int* npasses, int* nnodes, int* nproducts);
+void kron_plan_free(KronPlan* p);
+struct KronPlanDeleter {
+    void operator()(KronPlan* p) const { kron_plan_free(p); }
+};
+
+} // namespace ks
+
+using namespace ks;
+
+#define API_BEGIN try {
+#define API_END                                                                \
+    }                                                                          \
+    catch (const ks::Error& e) {                                               \
+        ks::set_last_error(e.what());                                          \
+        return e.code;                                                         \
+    }                                                                          \
+    catch (const std::bad_alloc&) {                                            \
+        ks::set_last_error("host allocation failed");                          \
+        return KS_ENOMEM;                                                      \
+    }                                                                          \
+    catch (const std::exception& e) {                                          \
+        ks::set_last_error(e.what());                                          \
+        return KS_EINVAL;                                                      \
+    }                                                                          \
+    return KS_OK;
+
+// ---------------------------------------------------------------------------
+// handles
+// ---------------------------------------------------------------------------
+struct ks_fd {
+    int device = 0;
+    int d = 0, p = 0;
+    double nu = 1.0;
+    std::vector<int> dims;
+    size_t N = 0, Ns = 0;
+    std::vector<DevBuf> At_fwd, At_inv, lam;
+    std::vector<std::vector<double>> lam_host;
+    DevBuf Lt, Mt, Wsym;
+    FdBlocks blocks;
+    DevBuf s0, s1, io;
+    cudaStream_t stream = nullptr;
+    std::mutex mu;
+    ~ks_fd() {
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+struct ks_kron {
+    int device = 0;
+    std::vector<int> dims;
+    size_t N = 0;
+    std::unique_ptr<KronPlan, KronPlanDeleter> plan;
+    DevBuf io_x, io_y;
+    std::vector<void*> hptrs;
+    cudaStream_t stream = nullptr;
+    std::mutex mu;
+    ~ks_kron() {
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+namespace {
+
+inline cudaStream_t pick(void* user, cudaStream_t own) {
+    return user ? static_cast<cudaStream_t>(user) : own;
+}
+
+// FD apply on device pointers (Algorithm 1 steps 2-4; fdsolver.cpp:53-63).
+// ev (optional): start/stop event pairs recorded around each transform kernel.
+void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStream_t st,
+                  std::vector<cudaEvent_t>* ev) {
+    const int d = f->d;
+    const double* cur = reinterpret_cast<const double*>(r);
+    double* bufs[2] = {f->s0.as<double>(), f->s1.as<double>()};
+    int nb = 0;
+    size_t s = f->dims[0];
+    auto gemm = [&](const DevBuf& At, int l, const double* in, double* out) {
+        const int n = f->dims[l];
+        size_t stride = 1;
+        for (int k = 0; k < l; ++k) stride *= (size_t)f->dims[k];
+        const size_t outer = f->N / (stride * (size_t)n);
+        if (ev) {
+            cudaEvent_t a, b;
+            KS_CUDA(cudaEventCreate(&a));
+            KS_CUDA(cudaEventCreate(&b));
+            KS_CUDA(cudaEventRecord(a, st));
+            launch_mode_gemm(At.as<double>(), n, in, out, stride, outer, st);
+            KS_CUDA(cudaEventRecord(b, st));
+            ev->push_back(a);
+            ev->push_back(b);
+        } else {
+            launch_mode_gemm(At.as<double>(), n, in, out, stride, outer, st);
+        }
+    };
+    (void)s;
+    // to_eigen: axes 1..d with U_l^T (fdsolver.cpp:7-14)
+    for (int l = 1; l <= d; ++l) {
+        double* out = bufs[nb];
+        nb ^= 1;
+        gemm(f->At_fwd[l - 1], l, cur, out);
+        cur = out;
+    }
+    // N_s block solves (fdsolver.cpp:58-60)
+    launch_fd_solve(f->blocks, reinterpret_cast<double2*>(const_cast<double*>(cur)), adjoint, st);
+    // from_eigen: axes 1..d with U_l (fdsolver.cpp:16-21)
+    for (int l = 1; l <= d; ++l) {
+        double* out = (l == d) ? reinterpret_cast<double*>(z) : bufs[nb];
+        if (l != d) nb ^= 1;
+        gemm(f->At_inv[l - 1], l, cur, out);
+        cur = out;
+    }
+}
+
+void fd_apply_any(ks_fd* f, const ks_c64* r, ks_c64* z, int mem, void* stream, bool adjoint) {
+    KS_REQUIRE(f, KS_EINVAL, "ks_fd_apply: NULL handle");
+    std::lock_guard<std::mutex> lk(f->mu);
+    ensure_device(f->device);
+    cudaStream_t st = pick(stream, f->stream);
+    const size_t bytes = f->N * sizeof(double2);
+    if (mem == KS_MEM_DEVICE) {
+        fd_apply_dev(f, reinterpret_cast<const double2*>(r), reinterpret_cast<double2*>(z), adjoint,
+                     st, nullptr);
+    } else {
+        if (!f->io.p) f->io.alloc(bytes);
+        KS_CUDA(cudaMemcpyAsync(f->io.p, r, bytes, cudaMemcpyHostToDevice, st));
+        fd_apply_dev(f, f->io.as<double2>(), f->io.as<double2>(), adjoint, st, nullptr);
+        KS_CUDA(cudaMemcpyAsync(z, f->io.p, bytes, cudaMemcpyDeviceToHost, st));
+        KS_CUDA(cudaStreamSynchronize(st));
+    }
+}
+
+void kron_apply_any(ks_kron* k, const ks_c64* x, ks_c64* y, int mem, void* stream) {
+    KS_REQUIRE(k, KS_EINVAL, "ks_kron_apply: NULL handle");
+    std::lock_guard<std::mutex> lk(k->mu);
+    ensure_device(k->device);
+    cudaStream_t st = pick(stream, k->stream);
+    const size_t bytes = k->N * sizeof(double2);
+    if (mem == KS_MEM_DEVICE) {
+        KS_REQUIRE(x != y, KS_EINVAL, "ks_kron_apply: x and y must not alias");
+        kron_apply(*k->plan, reinterpret_cast<const double2*>(x), reinterpret_cast<double2*>(y), st,
+                   k->hptrs);
+    } else {
+        if (!k->io_x.p) {
+            k->io_x.alloc(bytes);
+            k->io_y.alloc(bytes);
+        }
+        KS_CUDA(cudaMemcpyAsync(k->io_x.p, x, bytes, cudaMemcpyHostToDevice, st));
+        kron_apply(*k->plan, k->io_x.as<double2>(), k->io_y.as<double2>(), st, k->hptrs);
+        KS_CUDA(cudaMemcpyAsync(y, k->io_y.p, bytes, cudaMemcpyDeviceToHost, st));
+        KS_CUDA(cudaStreamSynchronize(st));
+    }
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.f;
+    KS_CUDA(cudaEventElapsedTime(&ms, a, b));
+    return ms;
+}
+
+} // namespace
+
+extern "C" {
+
+const char* ks_last_error(void) { return t_last_error.c_str(); }
+int ks_version(void) { return 1; }
+int ks_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+uint64_t ks_launch_count(void) { return g_launches.load(); }
+void ks_launch_count_reset(void) { g_launches.store(0); }
+
+// ---------------------------------------------------------------------------
+// FD preconditioner
+// ---------------------------------------------------------------------------
+int ks_fd_create(int d, const int* dims, double nu, int p_t, const double* const* U,
+                 const double* const* lambda, const double* Lt, const double* Mt, const ks_c64* Wt,
+                 int device, ks_fd** out) {
+    API_BEGIN
+    KS_REQUIRE(out && dims && U && lambda && Lt && Mt && Wt, KS_EINVAL, "ks_fd_create: NULL argument");
+    KS_REQUIRE(d >= 1 && d <= 3, KS_EINVAL, "ks_fd_create: d must be 1, 2 or 3");
+    KS_REQUIRE(nu > 0, KS_EINVAL, "ks_fd_create: nu must be positive");
+    KS_REQUIRE(p_t >= 1 && p_t <= 8, KS_EINVAL, "ks_fd_create: time degree must be 1..8");
+    for (int a = 0; a <= d; ++a) KS_REQUIRE(dims[a] >= 1, KS_EINVAL, "CoeffTensor: dims must be positive");
+    for (int l = 0; l < d; ++l) KS_REQUIRE(U[l] && lambda[l], KS_EINVAL, "ks_fd_create: NULL U/lambda");
+    ensure_device(device);
+    std::unique_ptr<ks_fd> f(new ks_fd());
+    f->device = device;
+    f->d = d;
+    f->p = p_t;
+    f->nu = nu;
+    f->dims.assign(dims, dims + d + 1);
+    f->Ns = 1;
+    for (int l = 1; l <= d; ++l) f->Ns *= (size_t)dims[l];
+    f->N = f->Ns * (size_t)dims[0];
+    KS_CUDA(cudaStreamCreateWithFlags(&f->stream, cudaStreamNonBlocking));
+    std::vector<const double*> lam_dev;
+    for (int l = 0; l < d; ++l) {
+        const int n = dims[l + 1];
+        for (int i = 0; i < n; ++i)
+            KS_REQUIRE(lambda[l][i] > 0, KS_EINVAL, "ks_fd_create: eigenvalues must be positive");
+        std::vector<double> af((size_t)n * n), ai((size_t)n * n);
+        // kernel wants At[j*n + r] = A[r][j]
+        // forward A = U^T: A[r][j] = U(j,r) = U[j + r*n]
+        // inverse A = U:   A[r][j] = U(r,j) = U[r + j*n]
+        for (int j = 0; j < n; ++j)
+            for (int r = 0; r < n; ++r) {
+                af[(size_t)j * n + r] = U[l][j + (size_t)r * n];
+                ai[(size_t)j * n + r] = U[l][r + (size_t)j * n];
+            }
+        f->At_fwd.emplace_back(af.size() * sizeof(double));
+        f->At_inv.emplace_back(ai.size() * sizeof(double));
+        KS_CUDA(cudaMemcpy(f->At_fwd.back().p, af.data(), af.size() * sizeof(double), cudaMemcpyHostToDevice));
+        KS_CUDA(cudaMemcpy(f->At_inv.back().p, ai.data(), ai.size() * sizeof(double), cudaMemcpyHostToDevice));
+        f->lam.emplace_back(n * sizeof(double));
+        KS_CUDA(cudaMemcpy(f->lam.back().p, lambda[l], n * sizeof(double), cudaMemcpyHostToDevice));
+        f->lam_host.emplace_back(lambda[l], lambda[l] + n);
+        lam_dev.push_back(f->lam.back().as<double>());
+    }
+    const int nt = dims[0], ld = 2 * p_t + 1;
+    // W + W^H (fdsolver.cpp:95-103)
+    std::vector<double2> ws((size_t)ld * nt, make_double2(0, 0));
+    auto wget = [&](int i, int j) -> double2 {
+        if (i < 0 || j < 0 || i >= nt || j >= nt || std::abs(i - j) > p_t) return make_double2(0, 0);
+        const ks_c64 v = Wt[p_t + i - j + (size_t)j * ld];
+        return make_double2(v.re, v.im);
+    };
+    for (int i = 0; i < nt; ++i)
+        for (int j = std::max(0, i - p_t); j <= std::min(nt - 1, i + p_t); ++j) {
+            const double2 a = wget(i, j), b = wget(j, i);
+            ws[p_t + i - j + (size_t)j * ld] = make_double2(a.x + b.x, a.y - b.y);
+        }
+    f->Lt.alloc((size_t)ld * nt * sizeof(double));
+    f->Mt.alloc((size_t)ld * nt * sizeof(double));
+    f->Wsym.alloc(ws.size() * sizeof(double2));
+    KS_CUDA(cudaMemcpy(f->Lt.p, Lt, (size_t)ld * nt * sizeof(double), cudaMemcpyHostToDevice));
+    KS_CUDA(cudaMemcpy(f->Mt.p, Mt, (size_t)ld * nt * sizeof(double), cudaMemcpyHostToDevice));
+    KS_CUDA(cudaMemcpy(f->Wsym.p, ws.data(), ws.size() * sizeof(double2), cudaMemcpyHostToDevice));
+    // factor all N_s blocks on the device (fdsolver.cpp:46-51)
+    FdBlocks& B = f->blocks;
+    B.nt = nt;
+    B.p = p_t;
+    B.ldab = 3 * p_t + 1;
+    B.ns = f->Ns;
+    B.ab.alloc((size_t)nt * B.ldab * B.ns * sizeof(double2));
+    B.piv.alloc((size_t)nt * B.ns);
+    B.flag.alloc(sizeof(int));
+    launch_fd_factor(B, d, dims + 1, lam_dev.data(), nu, f->Lt.as<double>(), f->Mt.as<double>(),
+                     f->Wsym.as<double2>(), f->stream);
+    f->s0.alloc(f->N * sizeof(double2));
+    f->s1.alloc(f->N * sizeof(double2));
+    KS_CUDA(cudaStreamSynchronize(f->stream));
+    *out = f.release();
+    API_END
+}
+
+int ks_fd_apply(ks_fd* fd, const ks_c64* r, ks_c64* z, int mem, void* stream) {
+    API_BEGIN
+    fd_apply_any(fd, r, z, mem, stream, false);
+    API_END
+}
+
+int ks_fd_apply_adjoint(ks_fd* fd, const ks_c64* r, ks_c64* z, int mem, void* stream) {
+    API_BEGIN
+    fd_apply_any(fd, r, z, mem, stream, true);
+    API_END
+}
+
+size_t ks_fd_vec_size(const ks_fd* fd) { return fd ? fd->N : 0; }
+
+int ks_fd_eigenvalues(const ks_fd* fd, double* out) {
+    API_BEGIN
+    KS_REQUIRE(fd && out, KS_EINVAL, "ks_fd_eigenvalues: NULL argument");
+    std::vector<int> idx(fd->d, 0);
+    for (size_t i = 0; i < fd->Ns; ++i) {
+        double s = 0;
+        for (int l = 0; l < fd->d; ++l) s += fd->lam_host[l][idx[l]];
+        out[i] = s;
+        for (int l = 0; l < fd->d; ++l) {
+            if (++idx[l] < fd->dims[l + 1]) break;
+            idx[l] = 0;
+        }
+    }
+    API_END
+}
+
+int ks_fd_block(const ks_fd* fd, size_t i, ks_c64* ab, int* piv) {
+    API_BEGIN
+    KS_REQUIRE(fd && ab && piv, KS_EINVAL, "ks_fd_block: NULL argument");
+    KS_REQUIRE(i < fd->Ns, KS_EINVAL, "ks_fd_block: index out of range");
+    ensure_device(fd->device);
+    const FdBlocks& B = fd->blocks;
+    for (int k = 0; k < B.nt; ++k) {
+        for (int e = 0; e < B.ldab; ++e)
+            KS_CUDA(cudaMemcpy(ab + (size_t)k * B.ldab + e,
+                               B.ab.as<double2>() + ((size_t)k * B.ldab + e) * B.ns + i,
+                               sizeof(double2), cudaMemcpyDeviceToHost));
+        unsigned char po = 0;
+        KS_CUDA(cudaMemcpy(&po, B.piv.as<unsigned char>() + (size_t)k * B.ns + i, 1,
+                           cudaMemcpyDeviceToHost));
+        piv[k] = k + po;
+    }
+    API_END
+}
+
+int ks_fd_destroy(ks_fd* fd) {
+    if (fd) {
+        cudaSetDevice(fd->device);
+        delete fd;
+    }
+    return KS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Kronecker operator
+// ---------------------------------------------------------------------------
+int ks_kron_create(int ndim, const int* dims, int nterms, const ks_term* terms, int device,
+                   ks_kron** out) {
+    API_BEGIN
+    KS_REQUIRE(out && dims && ndim >= 1, KS_EINVAL, "ks_kron_create: bad arguments");
+    KS_REQUIRE(nterms >= 0 && (nterms == 0 || terms), KS_EINVAL, "ks_kron_create: bad term list");
+    for (int a = 0; a < ndim; ++a) KS_REQUIRE(dims[a] >= 1, KS_EINVAL, "CoeffTensor: dims must be positive");
+    // factor dedup by content (shared prefixes need equal factors to share ids)
+    std::vector<std::vector<double2>> bands;
+    std::vector<int> bn, bbw;
+    std::vector<double2> coeffs;
+    std::vector<std::vector<int>> fids;
+    for (int t = 0; t < nterms; ++t) {
+        KS_REQUIRE(terms[t].factors, KS_EINVAL, "KroneckerOperator: wrong factor count");
+        std::vector<int> ids(ndim, -1);
+        for (int a = 0; a < ndim; ++a) {
+            const ks_c64* f = terms[t].factors[a];
+            if (!f) continue;
+            KS_REQUIRE(terms[t].bw, KS_EINVAL, "KroneckerOperator: missing bandwidths");
+            const int bw = terms[t].bw[a];
+            KS_REQUIRE(bw >= 0, KS_EINVAL, "BandedMatrix: invalid dimensions");
+            const int n = dims[a];
+            std::vector<double2> b((size_t)(2 * bw + 1) * n);
+            for (size_t i = 0; i < b.size(); ++i) b[i] = make_double2(f[i].re, f[i].im);
+            int id = -1;
+            for (size_t e = 0; e < bands.size(); ++e)
+                if (bn[e] == n && bbw[e] == bw &&
+                    std::memcmp(bands[e].data(), b.data(), b.size() * sizeof(double2)) == 0) {
+                    id = (int)e;
+                    break;
+                }
+            if (id < 0) {
+                id = (int)bands.size();
+                bands.push_back(std::move(b));
+                bn.push_back(n);
+                bbw.push_back(bw);
+            }
+            ids[a] = id;
+        }
+        coeffs.push_back(make_double2(terms[t].coeff.re, terms[t].coeff.im));
+        fids.push_back(ids);
+    }
+    ensure_device(device);
+    std::unique_ptr<ks_kron> k(new ks_kron());
+    k->device = device;
+    k->dims.assign(dims, dims + ndim);
+    k->N = 1;
+    for (int a = 0; a < ndim; ++a) k->N *= (size_t)dims[a];
+    KS_CUDA(cudaStreamCreateWithFlags(&k->stream, cudaStreamNonBlocking));
+    k->plan.reset(kron_plan(k->dims, bands, bn, bbw, coeffs, fids));
+    *out = k.release();
+    API_END
+}
+
+int ks_kron_apply(ks_kron* k, const ks_c64* x, ks_c64* y, int mem, void* stream) {
+    API_BEGIN
+    kron_apply_any(k, x, y, mem, stream);
+    API_END
+}
+
+size_t ks_kron_vec_size(const ks_kron* k) { return k ? k->N : 0; }
+
+int ks_kron_plan_info(const ks_kron* k, int* npasses, int* nnodes, int* nproducts) {
+    API_BEGIN
+    KS_REQUIRE(k, KS_EINVAL, "NULL handle");
+    kron_plan_info(*k->plan, npasses, nnodes, nproducts);
+    API_END
+}
+
+int ks_kron_destroy(ks_kron* k) {
+    if (k) {
+        cudaSetDevice(k->device);
+        delete k;
+    }
+    return KS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// PCG (krylov.cpp:24-114)
+// ---------------------------------------------------------------------------
+int ks_pcg(ks_kron* A, ks_fd* P, const ks_c64* b, ks_c64* x, int mem, const ks_pcg_opts* opts,
+           double* res_hist, int hist_cap, ks_pcg_report* report) {
+    API_BEGIN
+    KS_REQUIRE(A && b && x && opts && report, KS_EINVAL, "ks_pcg: NULL argument");
+    KS_REQUIRE(opts->tol > 0 && opts->maxit >= 0, KS_EINVAL, "pcg: bad options");
+    KS_REQUIRE(!P || P->N == A->N, KS_EINVAL, "pcg: operator sizes differ");
+    KS_REQUIRE(!P || P->device == A->device, KS_EINVAL, "pcg: operators on different devices");
+    std::lock_guard<std::mutex> lka(A->mu);
+    std::unique_ptr<std::lock_guard<std::mutex>> lkp;
+    if (P) lkp.reset(new std::lock_guard<std::mutex>(P->mu));
+    ensure_device(A->device);
+    std::memset(report, 0, sizeof(*report));
+    cudaStream_t st = A->stream;
+    const size_t n = A->N, bytes = n * sizeof(double2);
+    const auto t_start = std::chrono::steady_clock::now();
+
+    DevBuf bb, xv(bytes), r(bytes), z(bytes), p(bytes), q(bytes), scratch(bytes);
+    const double2* bd;
+    if (mem == KS_MEM_DEVICE) {
+        bd = reinterpret_cast<const double2*>(b);
+    } else {
+        bb.alloc(bytes);
+        KS_CUDA(cudaMemcpyAsync(bb.p, b, bytes, cudaMemcpyHostToDevice, st));
+        bd = bb.as<double2>();
+    }
+    KS_CUDA(cudaMemsetAsync(xv.p, 0, bytes, st));
+    Reducer red;
+    cudaEvent_t e0, e1;
+    KS_CUDA(cudaEventCreate(&e0));
+    KS_CUDA(cudaEventCreate(&e1));
+    struct EvGuard {
+        cudaEvent_t a, b;
+        ~EvGuard() { cudaEventDestroy(a); cudaEventDestroy(b); }
+    } evg{e0, e1};
+    double t_mv = 0, t_pc = 0;
+    auto matvec = [&](const double2* in, double2* outv) {
+        KS_CUDA(cudaEventRecord(e0, st));
+        kron_apply(*A->plan, in, outv, st, A->hptrs);
+        KS_CUDA(cudaEventRecord(e1, st));
+        KS_CUDA(cudaEventSynchronize(e1));
+        t_mv += elapsed(e0, e1) * 1e-3;
+    };
+    auto precond = [&](const double2* rin, double2* zout) {
+        if (P) {
+            KS_CUDA(cudaEventRecord(e0, st));
+            fd_apply_dev(P, rin, zout, false, st, nullptr);
+            KS_CUDA(cudaEventRecord(e1, st));
+            KS_CUDA(cudaEventSynchronize(e1));
+            t_pc += elapsed(e0, e1) * 1e-3;
+        } else {
+            KS_CUDA(cudaMemcpyAsync(zout, rin, bytes, cudaMemcpyDeviceToDevice, st));
+        }
+    };
+    auto dotc_re = [&](const double2* a, const double2* c) {
+        launch_dotc(red, a, c, n, st);
+        fetch(red, st, 2);
+        return red.host[0];
+    };
+    auto norm2 = [&](const double2* a) {
+        launch_norm2sq(red, a, n, st);
+        fetch(red, st, 1);
+        return red.host[0];
+    };
+    auto finish_out = [&]() {
+        KS_CUDA(cudaMemcpyAsync(x, xv.p, bytes,
+                                mem == KS_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                                st));
+        KS_CUDA(cudaStreamSynchronize(st));
+        report->matvec_seconds = t_mv;
+        report->precond_seconds = t_pc;
+        report->solve_seconds =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    };
+    int hist_len = 0;
+    auto push_hist = [&](double v) {
+        if (res_hist && hist_len < hist_cap) res_hist[hist_len] = v;
+        ++hist_len;
+    };
+    auto set_last_hist = [&](double v) {
+        if (res_hist && hist_len - 1 < hist_cap && hist_len > 0) res_hist[hist_len - 1] = v;
+    };
+
+    const double bnorm = std::sqrt(norm2(bd));
+    if (bnorm == 0.0) {
+        report->converged = 1;
+        finish_out();
+        return KS_OK;
+    }
+    auto true_relres = [&]() {
+        matvec(xv.as<double2>(), scratch.as<double2>());
+        launch_axpy_real(-1.0, bd, scratch.as<double2>(), n, st); // Ax - b
+        return std::sqrt(norm2(scratch.as<double2>())) / bnorm;
+    };
+    KS_CUDA(cudaMemcpyAsync(r.p, bd, bytes, cudaMemcpyDeviceToDevice, st));
+    precond(r.as<double2>(), z.as<double2>());
+    KS_CUDA(cudaMemcpyAsync(p.p, z.p, bytes, cudaMemcpyDeviceToDevice, st));
+    double rho = dotc_re(r.as<double2>(), z.as<double2>());
+    int restarts = 0;
+    for (int k = 0; k < opts->maxit; ++k) {
+        matvec(p.as<double2>(), q.as<double2>());
+        const double curvature = dotc_re(p.as<double2>(), q.as<double2>());
+        if (curvature <= 0.0) {
+            report->breakdown = 1;
+            break;
+        }
+        const double alpha = rho / curvature;
+        launch_cg_update(red, alpha, p.as<double2>(), q.as<double2>(), xv.as<double2>(),
+                         r.as<double2>(), n, st);
+        fetch(red, st, 1);
+        report->iterations++;
+        double relres = std::sqrt(red.host[0]) / bnorm;
+        if (opts->strict_residual) relres = true_relres();
+        push_hist(relres);
+        if (relres <= opts->tol) {
+            if (!opts->strict_residual) {
+                const double tr = true_relres();
+                set_last_hist(tr);
+                if (tr > opts->tol) {
+                    if (++restarts > 2) break;
+                    launch_neg_copy(scratch.as<double2>(), r.as<double2>(), n, st);
+                    precond(r.as<double2>(), z.as<double2>());
+                    KS_CUDA(cudaMemcpyAsync(p.p, z.p, bytes, cudaMemcpyDeviceToDevice, st));
+                    rho = dotc_re(r.as<double2>(), z.as<double2>());
+                    continue;
+                }
+            }
+            report->converged = 1;
+            break;
+        }
+        precond(r.as<double2>(), z.as<double2>());
+        const double rho_new = dotc_re(r.as<double2>(), z.as<double2>());
+        const double beta = rho_new / rho;
+        rho = rho_new;
+        launch_xpby(z.as<double2>(), beta, p.as<double2>(), n, st);
+    }
+    report->restarts = restarts;
+    report->hist_len = hist_len < hist_cap ? hist_len : hist_cap;
+    if (!res_hist) report->hist_len = 0;
+    finish_out();
+    API_END
+}
+
+// ---------------------------------------------------------------------------
+// BLAS-1 on device vectors
+// ---------------------------------------------------------------------------
+int ks_axpy_real(double a, const ks_c64* x, ks_c64* y, size_t n, void* stream) {
+    API_BEGIN
+    launch_axpy_real(a, reinterpret_cast<const double2*>(x), reinterpret_cast<double2*>(y), n,
+                     static_cast<cudaStream_t>(stream));
+    KS_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    API_END
+}
+int ks_axpy(ks_c64 a, const ks_c64* x, ks_c64* y, size_t n, void* stream) {
+    API_BEGIN
+    launch_axpy(make_double2(a.re, a.im), reinterpret_cast<const double2*>(x),
+                reinterpret_cast<double2*>(y), n, static_cast<cudaStream_t>(stream));
+    KS_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    API_END
+}
+int ks_dotc(const ks_c64* x, const ks_c64* y, size_t n, ks_c64* out, void* stream) {
+    API_BEGIN
+    KS_REQUIRE(out, KS_EINVAL, "ks_dotc: NULL out");
+    Reducer red;
+    launch_dotc(red, reinterpret_cast<const double2*>(x), reinterpret_cast<const double2*>(y), n,
+                static_cast<cudaStream_t>(stream));
+    fetch(red, static_cast<cudaStream_t>(stream), 2);
+    out->re = red.host[0];
+    out->im = red.host[1];
+    API_END
+}
+int ks_norm2sq(const ks_c64* x, size_t n, double* out, void* stream) {
+    API_BEGIN
+    KS_REQUIRE(out, KS_EINVAL, "ks_norm2sq: NULL out");
+    Reducer red;
+    launch_norm2sq(red, reinterpret_cast<const double2*>(x), n, static_cast<cudaStream_t>(stream));
+    fetch(red, static_cast<cudaStream_t>(stream), 1);
+    *out = red.host[0];
+    API_END
+}
+
+// ---------------------------------------------------------------------------
+// plumbing
+// ---------------------------------------------------------------------------
+int ks_set_device(int device) {
+    API_BEGIN
+    ensure_device(device);
+    API_END
+}
+int ks_malloc(void** ptr, size_t bytes) {
+    API_BEGIN
+    KS_REQUIRE(ptr, KS_EINVAL, "ks_malloc: NULL");
+    KS_CUDA(cudaMalloc(ptr, bytes));
+    API_END
+}
+int ks_free(void* ptr) {
+    API_BEGIN
+    KS_CUDA(cudaFree(ptr));
+    API_END
+}
+int ks_memcpy(void* dst, const void* src, size_t bytes, int kind) {
+    API_BEGIN
+    const cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice
+                                       : (kind == 1 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice);
+    KS_CUDA(cudaMemcpy(dst, src, bytes, k));
+    API_END
+}
+int ks_host_alloc(void** ptr, size_t bytes) {
+    API_BEGIN
+    KS_CUDA(cudaMallocHost(ptr, bytes));
+    API_END
+}
+int ks_host_free(void* ptr) {
+    API_BEGIN
+    KS_CUDA(cudaFreeHost(ptr));
+    API_END
+}
+int ks_synchronize(void) {
+    API_BEGIN
+    KS_CUDA(cudaDeviceSynchronize());
+    API_END
+}
+
+static DevBuf& flush_buf() {
+    static DevBuf b;
+    return b;
+}
+int ks_flush_l2(size_t bytes) {
+    API_BEGIN
+    DevBuf& b = flush_buf();
+    if (b.bytes < bytes) b.alloc(bytes);
+    launch_fill_bytes(b.p, bytes, nullptr);
+    API_END
+}
+
+int ks_fd_time(ks_fd* fd, const ks_c64* r, ks_c64* z, int iters, int flush, double* ms_out,
+               double* ms_kernel) {
+    API_BEGIN
+    KS_REQUIRE(fd && r && z && iters > 0, KS_EINVAL, "ks_fd_time: bad arguments");
+    std::lock_guard<std::mutex> lk(fd->mu);
+    ensure_device(fd->device);
+    cudaStream_t st = fd->stream;
+    DevBuf& fb = flush_buf();
+    const size_t fbytes = (size_t)256 << 20;
+    if (flush && fb.bytes < fbytes) fb.alloc(fbytes);
+    cudaEvent_t a, b;
+    KS_CUDA(cudaEventCreate(&a));
+    KS_CUDA(cudaEventCreate(&b));
+    double tot = 0, ker = 0;
+    for (int it = 0; it < iters; ++it) {
+        if (flush) launch_fill_bytes(fb.p, fbytes, st);
+        std::vector<cudaEvent_t> ev;
+        KS_CUDA(cudaEventRecord(a, st));
+        fd_apply_dev(fd, reinterpret_cast<const double2*>(r), reinterpret_cast<double2*>(z), false, st,
+                     ms_kernel ? &ev : nullptr);
+        KS_CUDA(cudaEventRecord(b, st));
+        KS_CUDA(cudaEventSynchronize(b));
+        tot += elapsed(a, b);
+        for (size_t e = 0; e + 1 < ev.size(); e += 2) {
+            ker += elapsed(ev[e], ev[e + 1]);
+            cudaEventDestroy(ev[e]);
+            cudaEventDestroy(ev[e + 1]);
+        }
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    if (ms_out) *ms_out = tot / iters;
+    if (ms_kernel) *ms_kernel = ker / iters;
+    API_END
+}
+
+int ks_kron_time(ks_kron* k, const ks_c64* x, ks_c64* y, int iters, int flush, double* ms_out) {
+    API_BEGIN
+    KS_REQUIRE(k && x && y && iters > 0, KS_EINVAL, "ks_kron_time: bad arguments");
+    std::lock_guard<std::mutex> lk(k->mu);
+    ensure_device(k->device);
+    cudaStream_t st = k->stream;
+    DevBuf& fb = flush_buf();
+    const size_t fbytes = (size_t)256 << 20;
+    if (flush && fb.bytes < fbytes) fb.alloc(fbytes);
+    cudaEvent_t a, b;
+    KS_CUDA(cudaEventCreate(&a));
+    KS_CUDA(cudaEventCreate(&b));
+    double tot = 0;
+    for (int it = 0; it < iters; ++it) {
+        if (flush) launch_fill_bytes(fb.p, fbytes, st);
+        KS_CUDA(cudaEventRecord(a, st));
+        kron_apply(*k->plan, reinterpret_cast<const double2*>(x), reinterpret_cast<double2*>(y), st,
+                   k->hptrs);
+        KS_CUDA(cudaEventRecord(b, st));
+        KS_CUDA(cudaEventSynchronize(b));
+        tot += elapsed(a, b);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    if (ms_out) *ms_out = tot / iters;
+    API_END
+}
+
+int ks_fp64_peak(double* tflops) {
+    API_BEGIN
+    KS_REQUIRE(tflops, KS_EINVAL, "ks_fp64_peak: NULL");
+    int dev = 0;
+    KS_CUDA(cudaGetDevice(&dev));
+    ensure_device(dev);
+    fp64_peak_bench(tflops);
+    API_END
+}
+
+int ks_transform_engine(void) { return transform_engine(); }
+
+} // extern "C"

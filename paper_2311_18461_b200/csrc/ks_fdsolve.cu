@@ -1,0 +1,304 @@
+// Per-spatial-eigenvalue time blocks of the FD preconditioner: build,
+// factor (partial-pivot banded LU) and solve, one time fiber per thread.
+//
+// Reference:
+//   composite eigenvalue   lambda_i = sum_l lambda_l[i_l], axis 1 fastest
+//                          (src/fdsolver.cpp:30-42)
+//   block                  H_i = Lt + nu^2 lambda_i^2 Mt + nu lambda_i (W + W^H)
+//                          (src/fdsolver.cpp:95-120; exact expression :115-116)
+//   factor                 factor_banded (src/eigensolve.cpp:77-121):
+//                          kl = p, ku_f = 2p, ldab = 3p+1, pivot = first argmax |a(i,k)|
+//                          over i in [k, k+kl], singular if max == 0, row swap over
+//                          [k, k+ku_f], multipliers stored in place
+//   solve                  solve_banded (src/eigensolve.cpp:123-140)
+//   adjoint solve          solve_banded_adjoint (src/eigensolve.cpp:148-170)
+//
+// Device layout ("fiber-interleaved"): band column k, band row e, fiber i at
+// ab[(k*ldab + e)*ns + i], pivots piv[k*ns + i] as the offset piv[k]-k in
+// [0, p]. Consecutive threads own consecutive fibers, so every band access of
+// a warp is one coalesced 512 B transaction. The solve keeps the (p+1)-wide
+// forward and (2p+1)-wide backward elimination windows in registers
+// (compile-time p), so each tensor entry is read and written once per sweep.
+//
+// Complex arithmetic follows the reference's std::complex<double> operations:
+// products (ac-bd, ad+bc), Smith-style division as in libgcc's __divdc3, and
+// |z| = hypot(re, im) for the pivot search.
+#include "ks_internal.hpp"
+
+namespace ks {
+
+namespace {
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cconjmul(double2 a, double2 b) { // conj(a) * b
+    return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+__device__ __forceinline__ double2 csub(double2 a, double2 b) {
+    return make_double2(a.x - b.x, a.y - b.y);
+}
+// (a + ib) / (c + id), Smith's algorithm as in libgcc __divdc3
+__device__ __forceinline__ double2 cdiv(double2 num, double2 den) {
+    const double a = num.x, b = num.y, c = den.x, d = den.y;
+    double x, y;
+    if (fabs(c) < fabs(d)) {
+        const double ratio = c / d;
+        const double denom = (c * ratio) + d;
+        x = ((a * ratio) + b) / denom;
+        y = ((b * ratio) - a) / denom;
+    } else {
+        const double ratio = d / c;
+        const double denom = (d * ratio) + c;
+        x = ((b * ratio) + a) / denom;
+        y = (b - (a * ratio)) / denom;
+    }
+    return make_double2(x, y);
+}
+__device__ __forceinline__ double cabs_(double2 a) { return hypot(a.x, a.y); }
+
+struct LamAxes {
+    const double* lam[3];
+    int n[3];
+    int d;
+};
+
+// ---------------------------------------------------------------------------
+// factor: one thread per fiber; builds H(lambda_i) into the interleaved band
+// and eliminates in place.
+// ---------------------------------------------------------------------------
+__global__ void k_fd_factor(double2* __restrict__ ab, unsigned char* __restrict__ piv,
+                            int* __restrict__ flag, size_t ns, int nt, int p, LamAxes la,
+                            double nu, const double* __restrict__ Lt,
+                            const double* __restrict__ Mt, const double2* __restrict__ Wsym) {
+    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (i >= ns) return;
+    const int ldab = 3 * p + 1, kuf = 2 * p, bwld = 2 * p + 1;
+    // composite eigenvalue, summed in axis order 1..d from 0 (fdsolver.cpp:33-35)
+    double lam = 0.0;
+    {
+        size_t rem = i;
+        for (int l = 0; l < la.d; ++l) {
+            const size_t il = rem % (size_t)la.n[l];
+            rem /= (size_t)la.n[l];
+            lam += la.lam[l][il];
+        }
+    }
+    auto A = [&](int r, int c) -> double2& {
+        return ab[((size_t)c * ldab + (size_t)(kuf + r - c)) * ns + i];
+    };
+    // fill: zero band, then H(r, c) for |r - c| <= p
+    for (int c = 0; c < nt; ++c)
+        for (int e = 0; e < ldab; ++e) ab[((size_t)c * ldab + e) * ns + i] = make_double2(0.0, 0.0);
+    const double s2 = nu * nu * lam * lam; // nu*nu*lam*lam (left to right)
+    const double s1 = nu * lam;
+    for (int c = 0; c < nt; ++c) {
+        const int r0 = c - p < 0 ? 0 : c - p, r1 = c + p > nt - 1 ? nt - 1 : c + p;
+        for (int r = r0; r <= r1; ++r) {
+            const int bi = p + r - c + c * bwld;
+            const double2 w = Wsym[bi];
+            // Lt(i,j) + nu*nu*lam*lam*Mt(i,j) + nu*lam*Wsym(i,j), complex
+            double re = __dadd_rn(Lt[bi], __dmul_rn(s2, Mt[bi]));
+            double im = 0.0; // Lt, Mt have zero imaginary parts (to_complex)
+            re = __dadd_rn(re, __dmul_rn(s1, w.x));
+            im = __dadd_rn(im, __dmul_rn(s1, w.y));
+            A(r, c) = make_double2(re, im);
+        }
+    }
+    // partial-pivot banded LU (eigensolve.cpp:93-119)
+    for (int k = 0; k < nt; ++k) {
+        const int imax = k + p < nt - 1 ? k + p : nt - 1;
+        int pr = k;
+        double best = cabs_(A(k, k));
+        for (int r = k + 1; r <= imax; ++r) {
+            const double v = cabs_(A(r, k));
+            if (v > best) {
+                best = v;
+                pr = r;
+            }
+        }
+        piv[(size_t)k * ns + i] = (unsigned char)(pr - k);
+        if (best == 0.0) {
+            atomicExch(flag, 1);
+            return;
+        }
+        const int jmax = k + kuf < nt - 1 ? k + kuf : nt - 1;
+        if (pr != k)
+            for (int c = k; c <= jmax; ++c) {
+                const double2 t = A(k, c);
+                A(k, c) = A(pr, c);
+                A(pr, c) = t;
+            }
+        const double2 pivval = A(k, k);
+        for (int r = k + 1; r <= imax; ++r) {
+            const double2 m = cdiv(A(r, k), pivval);
+            A(r, k) = m;
+            if (m.x != 0.0 || m.y != 0.0)
+                for (int c = k + 1; c <= jmax; ++c) A(r, c) = csub(A(r, c), cmul(m, A(k, c)));
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// solve: x <- H_i^{-1} x on fiber i (contiguous nt complex at X + i*nt)
+// ---------------------------------------------------------------------------
+template <int P>
+__global__ void __launch_bounds__(128) k_fd_solve(const double2* __restrict__ ab,
+                                                  const unsigned char* __restrict__ piv,
+                                                  double2* __restrict__ X, size_t ns, int nt) {
+    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (i >= ns) return;
+    constexpr int ldab = 3 * P + 1, kuf = 2 * P;
+    double2* x = X + i * (size_t)nt;
+    auto band = [&](int k, int e) -> double2 {
+        return __ldg(ab + ((size_t)k * ldab + e) * ns + i);
+    };
+    // forward: L with row interchanges (eigensolve.cpp:127-133); w[m] = x[k+m]
+    double2 w[P + 1];
+#pragma unroll
+    for (int m = 0; m <= P; ++m) w[m] = m < nt ? x[m] : make_double2(0.0, 0.0);
+    for (int k = 0; k < nt; ++k) {
+        const int po = piv[(size_t)k * ns + i];
+#pragma unroll
+        for (int m = 1; m <= P; ++m)
+            if (po == m) {
+                const double2 t = w[0];
+                w[0] = w[m];
+                w[m] = t;
+            }
+#pragma unroll
+        for (int m = 1; m <= P; ++m)
+            if (k + m < nt) w[m] = csub(w[m], cmul(band(k, kuf + m), w[0]));
+        x[k] = w[0];
+#pragma unroll
+        for (int m = 0; m < P; ++m) w[m] = w[m + 1];
+        w[P] = (k + P + 1 < nt) ? x[k + P + 1] : make_double2(0.0, 0.0);
+    }
+    // backward: U, column oriented (eigensolve.cpp:134-139); u[j] = x[k-j]
+    double2 u[2 * P + 1];
+#pragma unroll
+    for (int j = 0; j <= 2 * P; ++j) u[j] = (nt - 1 - j >= 0) ? x[nt - 1 - j] : make_double2(0.0, 0.0);
+    for (int k = nt - 1; k >= 0; --k) {
+        u[0] = cdiv(u[0], band(k, kuf));
+#pragma unroll
+        for (int j = 1; j <= 2 * P; ++j)
+            if (k - j >= 0) u[j] = csub(u[j], cmul(band(k, kuf - j), u[0]));
+        x[k] = u[0];
+#pragma unroll
+        for (int j = 0; j < 2 * P; ++j) u[j] = u[j + 1];
+        u[2 * P] = (k - 2 * P - 1 >= 0) ? x[k - 2 * P - 1] : make_double2(0.0, 0.0);
+    }
+}
+
+// adjoint: H_i^{-H} x (eigensolve.cpp:148-170)
+template <int P>
+__global__ void __launch_bounds__(128) k_fd_solve_adj(const double2* __restrict__ ab,
+                                                      const unsigned char* __restrict__ piv,
+                                                      double2* __restrict__ X, size_t ns, int nt) {
+    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (i >= ns) return;
+    constexpr int ldab = 3 * P + 1, kuf = 2 * P;
+    double2* x = X + i * (size_t)nt;
+    auto band = [&](int k, int e) -> double2 {
+        return __ldg(ab + ((size_t)k * ldab + e) * ns + i);
+    };
+    // U^H z = y, forward; h[j] = x[k - 2P + j] (finalised values)
+    double2 h[2 * P];
+#pragma unroll
+    for (int j = 0; j < 2 * P; ++j) h[j] = make_double2(0.0, 0.0);
+    for (int k = 0; k < nt; ++k) {
+        double2 s = x[k];
+#pragma unroll
+        for (int j = 0; j < 2 * P; ++j) {
+            const int r = k - 2 * P + j; // row index i, ascending
+            if (r >= 0) s = csub(s, cconjmul(band(k, kuf + r - k), h[j]));
+        }
+        const double2 dk = band(k, kuf);
+        s = cdiv(s, make_double2(dk.x, -dk.y));
+        x[k] = s;
+#pragma unroll
+        for (int j = 0; j < 2 * P - 1; ++j) h[j] = h[j + 1];
+        h[2 * P - 1] = s;
+    }
+    // L^H w = z with swaps in reverse; g[m] = x[k+m]
+    double2 g[P + 1];
+#pragma unroll
+    for (int m = 0; m <= P; ++m) {
+        const int r = nt - 1 + m;
+        g[m] = r < nt ? x[r] : make_double2(0.0, 0.0);
+    }
+    for (int k = nt - 1; k >= 0; --k) {
+        double2 s = g[0];
+#pragma unroll
+        for (int m = 1; m <= P; ++m)
+            if (k + m < nt) s = csub(s, cconjmul(band(k, kuf + m), g[m]));
+        g[0] = s;
+        const int po = piv[(size_t)k * ns + i];
+#pragma unroll
+        for (int m = 1; m <= P; ++m)
+            if (po == m) {
+                const double2 t = g[0];
+                g[0] = g[m];
+                g[m] = t;
+            }
+        if (k + P < nt) x[k + P] = g[P];
+#pragma unroll
+        for (int m = P; m > 0; --m) g[m] = g[m - 1];
+        g[0] = k - 1 >= 0 ? x[k - 1] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int m = 1; m <= P; ++m)
+        if (m - 1 < nt) x[m - 1] = g[m];
+}
+
+template <int P>
+void launch_solve_p(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t st) {
+    const unsigned grid = (unsigned)((B.ns + 127) / 128);
+    if (adjoint) {
+        k_fd_solve_adj<P><<<grid, 128, 0, st>>>(B.ab.as<double2>(), B.piv.as<unsigned char>(), X,
+                                                B.ns, B.nt);
+        check_launch("k_fd_solve_adj");
+    } else {
+        k_fd_solve<P><<<grid, 128, 0, st>>>(B.ab.as<double2>(), B.piv.as<unsigned char>(), X,
+                                            B.ns, B.nt);
+        check_launch("k_fd_solve");
+    }
+}
+
+} // namespace
+
+void launch_fd_factor(FdBlocks& B, int d, const int* ns_axes, const double* const* lam_axes_dev,
+                      double nu, const double* Lt, const double* Mt, const double2* Wsym,
+                      cudaStream_t st) {
+    LamAxes la{};
+    la.d = d;
+    for (int l = 0; l < d; ++l) {
+        la.lam[l] = lam_axes_dev[l];
+        la.n[l] = ns_axes[l];
+    }
+    KS_CUDA(cudaMemsetAsync(B.flag.p, 0, sizeof(int), st));
+    const unsigned grid = (unsigned)((B.ns + 127) / 128);
+    k_fd_factor<<<grid, 128, 0, st>>>(B.ab.as<double2>(), B.piv.as<unsigned char>(),
+                                      B.flag.as<int>(), B.ns, B.nt, B.p, la, nu, Lt, Mt, Wsym);
+    check_launch("k_fd_factor");
+    int h = 0;
+    KS_CUDA(cudaMemcpyAsync(&h, B.flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    KS_CUDA(cudaStreamSynchronize(st));
+    KS_REQUIRE(h == 0, KS_ESINGULAR, "factor_banded: numerically singular pivot");
+}
+
+void launch_fd_solve(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t st) {
+    switch (B.p) {
+    case 1: launch_solve_p<1>(B, X, adjoint, st); break;
+    case 2: launch_solve_p<2>(B, X, adjoint, st); break;
+    case 3: launch_solve_p<3>(B, X, adjoint, st); break;
+    case 4: launch_solve_p<4>(B, X, adjoint, st); break;
+    case 5: launch_solve_p<5>(B, X, adjoint, st); break;
+    case 6: launch_solve_p<6>(B, X, adjoint, st); break;
+    case 7: launch_solve_p<7>(B, X, adjoint, st); break;
+    case 8: launch_solve_p<8>(B, X, adjoint, st); break;
+    default: throw Error(KS_EINVAL, "FD solve: time degree must be 1..8");
+    }
+}
+
+} // namespace ks

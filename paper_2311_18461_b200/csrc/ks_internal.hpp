@@ -1,0 +1,147 @@
+// Internal declarations shared by the libks translation units.
+// Nothing here crosses the C-ABI (include/ks.h).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/ks.h"
+
+namespace ks {
+
+// ---------------------------------------------------------------------------
+// errors: one exception type carrying a ks_status; the API wrappers turn it
+// into a return code + thread-local message.
+// ---------------------------------------------------------------------------
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void set_last_error(const std::string& msg);
+
+#define KS_CUDA(expr)                                                          \
+    do {                                                                       \
+        cudaError_t e_ = (expr);                                               \
+        if (e_ != cudaSuccess)                                                 \
+            throw ::ks::Error(e_ == cudaErrorMemoryAllocation ? KS_ENOMEM      \
+                                                              : KS_ECUDA,      \
+                              std::string(#expr) + ": " +                      \
+                                  cudaGetErrorString(e_));                     \
+    } while (0)
+
+#define KS_REQUIRE(cond, code, msg)                                            \
+    do {                                                                       \
+        if (!(cond))                                                           \
+            throw ::ks::Error((code), (msg));                                  \
+    } while (0)
+
+// counts every kernel this library launches (ks_launch_count)
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+inline void check_launch(const char* what) {
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+        throw Error(KS_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// RAII device buffer
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    explicit DevBuf(size_t b) { alloc(b); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) { release(); p = o.p; bytes = o.bytes; o.p = nullptr; o.bytes = 0; }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void alloc(size_t b) {
+        release();
+        if (b == 0) return;
+        KS_CUDA(cudaMalloc(&p, b));
+        bytes = b;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <typename T> T* as() const { return static_cast<T*>(p); }
+};
+
+void ensure_device(int device);
+
+// ---------------------------------------------------------------------------
+// reductions / BLAS-1 (ks_blas.cu). Deterministic: fixed grid, fixed tree.
+// ---------------------------------------------------------------------------
+struct Reducer {
+    static constexpr int kBlocks = 592;   // 4 x 148 SMs
+    static constexpr int kThreads = 256;
+    DevBuf partial;   // kBlocks x 3 doubles
+    DevBuf counter;   // unsigned int, last-block detection
+    DevBuf result;    // 3 doubles
+    double* host = nullptr; // pinned, 3 doubles
+    Reducer();
+    ~Reducer();
+    Reducer(const Reducer&) = delete;
+    Reducer& operator=(const Reducer&) = delete;
+};
+
+// device-side reductions; results land in r.result (device) and, after
+// fetch(), in r.host.
+void launch_dotc(Reducer& r, const double2* x, const double2* y, size_t n, cudaStream_t s);
+void launch_norm2sq(Reducer& r, const double2* x, size_t n, cudaStream_t s);
+// x += a p ; r -= a q ; result[0] = ||r||^2   (krylov.cpp:73-78)
+void launch_cg_update(Reducer& red, double alpha, const double2* p, const double2* q,
+                      double2* x, double2* r, size_t n, cudaStream_t s);
+// p = z + beta p   (krylov.cpp:109-110)
+void launch_xpby(const double2* z, double beta, double2* p, size_t n, cudaStream_t s);
+// y = a*x + y (real a)
+void launch_axpy_real(double a, const double2* x, double2* y, size_t n, cudaStream_t s);
+void launch_axpy(double2 a, const double2* x, double2* y, size_t n, cudaStream_t s);
+// y = -x
+void launch_neg_copy(const double2* x, double2* y, size_t n, cudaStream_t s);
+void fetch(Reducer& r, cudaStream_t s, int count);
+void launch_fill_bytes(void* p, size_t bytes, cudaStream_t s);
+
+// ---------------------------------------------------------------------------
+// dense mode product with a real n x n matrix (ks_transform.cu)
+//   Y[o][r][q] = sum_j A[r][j] X[o][j][q],  q over 2*s doubles
+// At is A stored k-major: At[j*n + r] = A[r][j].
+// ---------------------------------------------------------------------------
+void launch_mode_gemm(const double* At, int n, const double* X, double* Y,
+                      size_t s_complex, size_t outer, cudaStream_t st);
+
+// ---------------------------------------------------------------------------
+// banded block factor / solve (ks_fdsolve.cu)
+// ---------------------------------------------------------------------------
+struct FdBlocks {
+    int nt = 0, p = 0, ldab = 0;
+    size_t ns = 0;
+    DevBuf ab;   // complex [nt][ldab][ns]  (fiber-interleaved band columns)
+    DevBuf piv;  // uint8 [nt][ns]  pivot offset piv[k]-k in 0..p
+    DevBuf flag; // int: singular-pivot flag set by the factor kernel
+};
+// lam_axes: d device arrays; time bands on device: Lt, Mt real (2p+1)xnt, Wsym complex
+void launch_fd_factor(FdBlocks& B, int d, const int* ns_axes, const double* const* lam_axes_dev,
+                      double nu, const double* Lt, const double* Mt, const double2* Wsym,
+                      cudaStream_t st);
+void launch_fd_solve(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t st);
+
+// ---------------------------------------------------------------------------
+// level-pass Kronecker engine (ks_kron.cu)
+// ---------------------------------------------------------------------------
+void fp64_peak_bench(double* tflops);
+
+} // namespace ks

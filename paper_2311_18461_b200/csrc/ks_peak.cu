@@ -1,0 +1,93 @@
+// FP64 peak microbenchmarks: the roofline denominator for the FP64-bound
+// transforms. MEASURED_PEAKS.json carries only HBM and bf16 figures, so the
+// bench measures the DFMA (CUDA-core) and DMMA (mma.sync f64) issue peaks
+// live on the same device, at the clocks the device runs under load.
+#include "ks_internal.hpp"
+
+namespace ks {
+
+namespace {
+
+constexpr int kIters = 2048;
+
+__global__ void __launch_bounds__(256) k_dfma_peak(double* out, double seed) {
+    double a[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = seed + threadIdx.x * 1e-9 + i;
+    const double b = 0.999999, c = 1e-7;
+    for (int it = 0; it < kIters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = fma(a[i], b, c);
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += a[i];
+    if (s == 12345.678) out[threadIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(256) k_dmma_peak(double* out, double seed) {
+    double c[8][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = seed + i;
+    const double a = 0.999 + threadIdx.x * 1e-9, b = 1e-3;
+    for (int it = 0; it < kIters / 4; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                         : "+d"(c[i][0]), "+d"(c[i][1])
+                         : "d"(a), "d"(b));
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+    if (s == 12345.678) out[threadIdx.x] = s;
+}
+
+} // namespace
+
+static void run_peak(bool mma, double* tflops) {
+    int sms = 148;
+    int dev = 0;
+    KS_CUDA(cudaGetDevice(&dev));
+    KS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    DevBuf out(256 * sizeof(double));
+    const unsigned grid = sms * 8;
+    cudaEvent_t a, b;
+    KS_CUDA(cudaEventCreate(&a));
+    KS_CUDA(cudaEventCreate(&b));
+    float best = 1e30f;
+    for (int rep = 0; rep < 6; ++rep) {
+        KS_CUDA(cudaEventRecord(a));
+        if (mma) k_dmma_peak<<<grid, 256>>>(out.as<double>(), 1.0);
+        else k_dfma_peak<<<grid, 256>>>(out.as<double>(), 1.0);
+        check_launch("k_fp64_peak");
+        KS_CUDA(cudaEventRecord(b));
+        KS_CUDA(cudaEventSynchronize(b));
+        float ms = 0;
+        KS_CUDA(cudaEventElapsedTime(&ms, a, b));
+        if (rep > 0 && ms < best) best = ms;
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    // flops: DFMA 2 per lane-op; DMMA m8n8k4 = 256 FMA per warp-op = 512 flops
+    const double threads = (double)grid * 256;
+    const double flops = mma ? (double)grid * 8 /*warps*/ * (kIters / 4) * 8 * 512.0
+                             : threads * kIters * 8 * 2.0;
+    *tflops = flops / (best * 1e-3) / 1e12;
+}
+
+void fp64_peak_bench(double* tflops) { run_peak(false, tflops); }
+void fp64_peak_bench_mma(double* tflops) { run_peak(true, tflops); }
+
+} // namespace ks
+
+extern "C" int ks_fp64_peaks(double* dfma, double* dmma) {
+    try {
+        if (dfma) ks::fp64_peak_bench(dfma);
+        if (dmma) ks::fp64_peak_bench_mma(dmma);
+    } catch (const ks::Error& e) {
+        ks::set_last_error(e.what());
+        return e.code;
+    }
+    return KS_OK;
+}

@@ -1,0 +1,356 @@
+// Dense spatial eigen-transform: the mode-l product of the complex FP64
+// coefficient tensor with a dense real n x n matrix (U_l^T forward, U_l
+// inverse).
+//
+// Reference: mode_product(const CoeffTensor&, const Eigen::MatrixXd&, axis)
+// (src/tensorops.cpp:125-156), called from SpatialEigenbasis::to_eigen /
+// from_eigen (src/fdsolver.cpp:7-21). The reference walks slabs and does
+// one axpy of length s per (row, column) pair (:145-153).
+//
+// B200 formulation: with the tensor viewed as X[o][j][q] (o over the axes
+// after l, j over axis l, q over 2*s interleaved doubles of the axes before
+// l), the product is a real GEMM  Y(n x C) = A(n x n) * X(n x C)  over the
+// flattened column index c = o*2s + q, C = outer*2s. Real x complex is exact
+// in this view: the re and im parts are independent columns.
+//
+// Roofline: per complex DOF 4n flops (2n FMA) and 32 B compulsory (read X,
+// write Y) -> n/8 flop/B, above the FP64 ridge (~5.7 flop/B at 37 TF /
+// 6.5 TB/s) for every n >= 48: FP64-pipe bound. A stays in shared memory,
+// X tiles stream through shared memory once (double-buffered), each output
+// is written once.
+//
+// Two inner engines over the same tiling:
+//   * DFMA: 8 x TM register micro-tile per thread (CUDA cores);
+//   * DMMA: mma.sync.aligned.m8n8k4.row.col.f64 (FP64 tensor-core path).
+// ks_transform_engine() picks one (env KS_GEMM=dfma|dmma, default below);
+// both are exact FP64 with identical accumulation order per output
+// (k ascending in 16-wide chunks), differing only in FMA rounding.
+#include "ks_internal.hpp"
+
+#include <cstdlib>
+#include <cstring>
+
+namespace ks {
+
+namespace {
+
+constexpr int kThreads = 256; // 8 warps
+constexpr int kBK = 16;       // k-chunk
+constexpr int kBN = 128;      // columns (doubles) per CTA
+
+// ---------------------------------------------------------------------------
+// DFMA engine. Warp lanes: tx = lane % 8 (columns), ty = lane / 8 (rows).
+// Warps: wr = warp % 4 (rows), wc = warp / 4 (columns).
+// Thread rows:  r = (wr*4 + ty)*TM + i, i < TM      -> BM = 16*TM
+// Thread cols:  c = wc*64 + m*16 + 2*tx + {0,1}, m < 4
+// ---------------------------------------------------------------------------
+template <int TM>
+__global__ void __launch_bounds__(kThreads, 1)
+k_mode_gemm_dfma(const double* __restrict__ At, int n, const double* __restrict__ X,
+                 double* __restrict__ Y, long long W2, long long C) {
+    constexpr int BM = 16 * TM;
+    constexpr int BMP = BM + 2; // pad (keeps 16 B alignment, breaks row conflicts)
+    extern __shared__ double smem[];
+    double* As = smem;                       // [2][kBK][BMP]
+    double* Bs = smem + 2 * kBK * BMP;       // [2][kBK][kBN]
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tx = lane & 7, ty = lane >> 3, wr = warp & 3, wc = warp >> 2;
+    const long long c0 = (long long)blockIdx.x * kBN;
+
+    // loader mapping for X: thread owns column pair cp = tid % 64, rows tid/64 + 4k
+    const int lcp = tid & 63;
+    const long long lc = c0 + 2 * lcp;
+    const bool lvalid = lc < C;
+    long long loff = 0;
+    if (lvalid) {
+        const long long o = lc / W2, q = lc - o * W2;
+        loff = o * (long long)n * W2 + q;
+    }
+    const int lrow0 = tid >> 6;
+
+    double2 breg[4];
+    double areg[(kBK * BM + kThreads - 1) / kThreads];
+
+    auto gload = [&](int j0) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int j = j0 + lrow0 + 4 * k;
+            breg[k] = (lvalid && j < n)
+                          ? __ldg(reinterpret_cast<const double2*>(X + loff + (long long)j * W2))
+                          : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int k = 0; k < (kBK * BM + kThreads - 1) / kThreads; ++k) {
+            const int e = tid + k * kThreads;
+            const int jj = e / BM, r = e - jj * BM;
+            const int j = j0 + jj;
+            areg[k] = (e < kBK * BM && j < n && r < n) ? __ldg(At + (long long)j * n + r) : 0.0;
+        }
+    };
+    auto sstore = [&](int buf) {
+        double* as = As + buf * kBK * BMP;
+        double* bs = Bs + buf * kBK * kBN;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            *reinterpret_cast<double2*>(bs + (lrow0 + 4 * k) * kBN + 2 * lcp) = breg[k];
+#pragma unroll
+        for (int k = 0; k < (kBK * BM + kThreads - 1) / kThreads; ++k) {
+            const int e = tid + k * kThreads;
+            if (e < kBK * BM) {
+                const int jj = e / BM, r = e - jj * BM;
+                as[jj * BMP + r] = areg[k];
+            }
+        }
+    };
+
+    double acc[TM][8];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int m = 0; m < 8; ++m) acc[i][m] = 0.0;
+
+    const int nk = (n + kBK - 1) / kBK;
+    gload(0);
+    sstore(0);
+    __syncthreads();
+    const int rbase = (wr * 4 + ty) * TM;
+    const int cbase = wc * 64 + 2 * tx;
+    for (int kc = 0; kc < nk; ++kc) {
+        const int buf = kc & 1;
+        if (kc + 1 < nk) gload((kc + 1) * kBK);
+        const double* as = As + buf * kBK * BMP;
+        const double* bs = Bs + buf * kBK * kBN;
+#pragma unroll
+        for (int jj = 0; jj < kBK; ++jj) {
+            double a[TM];
+#pragma unroll
+            for (int i = 0; i < TM; ++i) a[i] = as[jj * BMP + rbase + i];
+            double b[8];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const double2 v = *reinterpret_cast<const double2*>(bs + jj * kBN + cbase + 16 * m);
+                b[2 * m] = v.x;
+                b[2 * m + 1] = v.y;
+            }
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int m = 0; m < 8; ++m) acc[i][m] = fma(a[i], b[m], acc[i][m]);
+        }
+        if (kc + 1 < nk) {
+            sstore(buf ^ 1);
+        }
+        __syncthreads();
+    }
+
+    // epilogue: write Y rows r < n, column pairs
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        const long long c = c0 + cbase + 16 * m;
+        if (c >= C) continue;
+        const long long o = c / W2, q = c - o * W2;
+        double* yb = Y + o * (long long)n * W2 + q;
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+            const int r = rbase + i;
+            if (r < n)
+                *reinterpret_cast<double2*>(yb + (long long)r * W2) =
+                    make_double2(acc[i][2 * m], acc[i][2 * m + 1]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// DMMA engine: FP64 mma.sync m8n8k4 (A row-major 8x4, B col-major 4x8).
+// Fragment ownership (PTX ISA, mma.m8n8k4 .f64):
+//   A: lane holds A[lane/4][lane%4]      B: lane holds B[lane%4][lane/4]
+//   C: lane holds C[lane/4][2*(lane%4) + {0,1}]
+// CTA tile: BM = 16*TM rows, kBN = 128 columns.
+// Warps: wr = warp % 2 -> rows [wr*BM/2, +BM/2), wc = warp / 2 -> cols [wc*32, +32)
+// Each warp: (BM/2/8) x 4 mma tiles.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void dmma_m8n8k4(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+template <int TM>
+__global__ void __launch_bounds__(kThreads, 1)
+k_mode_gemm_dmma(const double* __restrict__ At, int n, const double* __restrict__ X,
+                 double* __restrict__ Y, long long W2, long long C) {
+    constexpr int BM = 16 * TM;
+    constexpr int MT = BM / 2 / 8; // mma row tiles per warp
+    constexpr int BMP = BM + 4;
+    constexpr int BNP = kBN + 4;
+    extern __shared__ double smem[];
+    double* As = smem;                 // [2][kBK][BMP]  (k-major: As[k][r])
+    double* Bs = smem + 2 * kBK * BMP; // [2][kBK][BNP]  (Bs[k][c])
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wr = warp & 1, wc = warp >> 1;
+    const long long c0 = (long long)blockIdx.x * kBN;
+
+    const int lcp = tid & 63;
+    const long long lc = c0 + 2 * lcp;
+    const bool lvalid = lc < C;
+    long long loff = 0;
+    if (lvalid) {
+        const long long o = lc / W2, q = lc - o * W2;
+        loff = o * (long long)n * W2 + q;
+    }
+    const int lrow0 = tid >> 6;
+    double2 breg[4];
+    double areg[(kBK * BM + kThreads - 1) / kThreads];
+
+    auto gload = [&](int j0) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int j = j0 + lrow0 + 4 * k;
+            breg[k] = (lvalid && j < n)
+                          ? __ldg(reinterpret_cast<const double2*>(X + loff + (long long)j * W2))
+                          : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int k = 0; k < (kBK * BM + kThreads - 1) / kThreads; ++k) {
+            const int e = tid + k * kThreads;
+            const int jj = e / BM, r = e - jj * BM;
+            const int j = j0 + jj;
+            areg[k] = (e < kBK * BM && j < n && r < n) ? __ldg(At + (long long)j * n + r) : 0.0;
+        }
+    };
+    auto sstore = [&](int buf) {
+        double* as = As + buf * kBK * BMP;
+        double* bs = Bs + buf * kBK * BNP;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            *reinterpret_cast<double2*>(bs + (lrow0 + 4 * k) * BNP + 2 * lcp) = breg[k];
+#pragma unroll
+        for (int k = 0; k < (kBK * BM + kThreads - 1) / kThreads; ++k) {
+            const int e = tid + k * kThreads;
+            if (e < kBK * BM) {
+                const int jj = e / BM, r = e - jj * BM;
+                as[jj * BMP + r] = areg[k];
+            }
+        }
+    };
+
+    double acc[MT][4][2];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int m = 0; m < 4; ++m) acc[i][m][0] = acc[i][m][1] = 0.0;
+
+    const int nk = (n + kBK - 1) / kBK;
+    gload(0);
+    sstore(0);
+    __syncthreads();
+    const int r_warp = wr * (BM / 2);
+    const int c_warp = wc * 32;
+    const int ar = lane >> 2, ak = lane & 3; // A frag: row ar, k ak
+    const int bk = lane & 3, bn = lane >> 2; // B frag: k bk, col bn
+    for (int kc = 0; kc < nk; ++kc) {
+        const int buf = kc & 1;
+        if (kc + 1 < nk) gload((kc + 1) * kBK);
+        const double* as = As + buf * kBK * BMP;
+        const double* bs = Bs + buf * kBK * BNP;
+#pragma unroll
+        for (int k4 = 0; k4 < kBK; k4 += 4) {
+            double a[MT], b[4];
+#pragma unroll
+            for (int i = 0; i < MT; ++i) a[i] = as[(k4 + ak) * BMP + r_warp + i * 8 + ar];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) b[m] = bs[(k4 + bk) * BNP + c_warp + m * 8 + bn];
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int m = 0; m < 4; ++m) dmma_m8n8k4(acc[i][m][0], acc[i][m][1], a[i], b[m]);
+        }
+        if (kc + 1 < nk) sstore(buf ^ 1);
+        __syncthreads();
+    }
+
+    // epilogue: C[lane/4][2*(lane%4)+{0,1}] of each tile
+    const int cr = lane >> 2, cc = 2 * (lane & 3);
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        const long long c = c0 + c_warp + m * 8 + cc;
+        if (c >= C) continue;
+        const long long o = c / W2, q = c - o * W2;
+        double* yb = Y + o * (long long)n * W2 + q;
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+            const int r = r_warp + i * 8 + cr;
+            if (r < n)
+                *reinterpret_cast<double2*>(yb + (long long)r * W2) =
+                    make_double2(acc[i][m][0], acc[i][m][1]);
+        }
+    }
+}
+
+int engine_choice() {
+    static int e = [] {
+        const char* v = std::getenv("KS_GEMM");
+        if (v && std::strcmp(v, "dfma") == 0) return 0;
+        if (v && std::strcmp(v, "dmma") == 0) return 1;
+        return 1; // default: DMMA (profiles/ for the measurement)
+    }();
+    return e;
+}
+
+template <int TM>
+void launch_tm(int engine, const double* At, int n, const double* X, double* Y, long long W2,
+               long long C, cudaStream_t st) {
+    const unsigned grid = (unsigned)((C + kBN - 1) / kBN);
+    if (engine == 0) {
+        const size_t sm = (size_t)2 * kBK * (16 * TM + 2 + kBN) * sizeof(double);
+        static bool attr = false;
+        if (!attr) {
+            KS_CUDA(cudaFuncSetAttribute(k_mode_gemm_dfma<TM>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            attr = true;
+        }
+        k_mode_gemm_dfma<TM><<<grid, kThreads, sm, st>>>(At, n, X, Y, W2, C);
+        check_launch("k_mode_gemm_dfma");
+    } else {
+        const size_t sm = (size_t)2 * kBK * (16 * TM + 4 + kBN + 4) * sizeof(double);
+        static bool attr = false;
+        if (!attr) {
+            KS_CUDA(cudaFuncSetAttribute(k_mode_gemm_dmma<TM>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            attr = true;
+        }
+        k_mode_gemm_dmma<TM><<<grid, kThreads, sm, st>>>(At, n, X, Y, W2, C);
+        check_launch("k_mode_gemm_dmma");
+    }
+}
+
+} // namespace
+
+int transform_engine() { return engine_choice(); }
+
+void launch_mode_gemm(const double* At, int n, const double* X, double* Y, size_t s_complex,
+                      size_t outer, cudaStream_t st) {
+    const long long W2 = 2 * (long long)s_complex;
+    const long long C = W2 * (long long)outer;
+    if (C == 0 || n == 0) return;
+    const int eng = engine_choice();
+    // rows per CTA: 16*TM >= n
+    const int tm = (n + 15) / 16;
+    KS_REQUIRE(tm <= 10, KS_EINVAL, "mode product: axis length > 160 not supported");
+    switch (tm) {
+    case 1: launch_tm<1>(eng, At, n, X, Y, W2, C, st); break;
+    case 2: launch_tm<2>(eng, At, n, X, Y, W2, C, st); break;
+    case 3: launch_tm<3>(eng, At, n, X, Y, W2, C, st); break;
+    case 4: launch_tm<4>(eng, At, n, X, Y, W2, C, st); break;
+    case 5: launch_tm<5>(eng, At, n, X, Y, W2, C, st); break;
+    case 6: launch_tm<6>(eng, At, n, X, Y, W2, C, st); break;
+    case 7: launch_tm<7>(eng, At, n, X, Y, W2, C, st); break;
+    case 8: launch_tm<8>(eng, At, n, X, Y, W2, C, st); break;
+    case 9: launch_tm<9>(eng, At, n, X, Y, W2, C, st); break;
+    case 10: launch_tm<10>(eng, At, n, X, Y, W2, C, st); break;
+    }
+}
+
+} // namespace ks
