@@ -200,7 +200,7 @@ def run_reference_arm(args, rank, ws, dist):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
@@ -235,15 +235,15 @@ def main():
     fp64_peak = max(dfma, dmma)
 
     # ---- device-resident FD apply (the headline) ----
+    clk = ClockSampler(local).__enter__()
     P.time(r, z, W, flush=False)
     barrier(dist)
     ks.lib().ks_synchronize()
     ks.reset_launch_count()
-    with ClockSampler(local) as clk:
-        t0 = time.perf_counter()
-        ms_fd, ms_gemm = P.time(r, z, K, flush=False)
-        ks.lib().ks_synchronize()
-        wall_fd = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ms_fd, ms_gemm = P.time(r, z, K, flush=False)
+    ks.lib().ks_synchronize()
+    wall_fd = time.perf_counter() - t0
     launches = ks.launch_count()
     barrier(dist)
     ms_fd = max_over_ranks(dist, ms_fd)
@@ -271,6 +271,7 @@ def main():
     e2e_s = max_over_ranks(dist, e2e_s)
     e2e_val = ws * n / e2e_s
     check = float(np.abs(zout).sum())  # the step's result was read back on the host
+    clk.__exit__(None, None, None)
 
     # ---- full solves (device-resident PCG) ----
     solves = {}

@@ -156,6 +156,8 @@ void fd_apply_any(ks_fd* f, const ks_c64* r, ks_c64* z, int mem, void* stream, b
     if (mem == KS_MEM_DEVICE) {
         fd_apply_dev(f, reinterpret_cast<const double2*>(r), reinterpret_cast<double2*>(z), adjoint,
                      st, nullptr);
+        // no caller stream: behave like the reference's blocking call
+        if (!stream) KS_CUDA(cudaStreamSynchronize(st));
     } else {
         if (!f->io.p) f->io.alloc(bytes);
         KS_CUDA(cudaMemcpyAsync(f->io.p, r, bytes, cudaMemcpyHostToDevice, st));
@@ -175,6 +177,7 @@ void kron_apply_any(ks_kron* k, const ks_c64* x, ks_c64* y, int mem, void* strea
         KS_REQUIRE(x != y, KS_EINVAL, "ks_kron_apply: x and y must not alias");
         kron_apply(*k->plan, reinterpret_cast<const double2*>(x), reinterpret_cast<double2*>(y), st,
                    k->hptrs);
+        if (!stream) KS_CUDA(cudaStreamSynchronize(st));
     } else {
         if (!k->io_x.p) {
             k->io_x.alloc(bytes);
