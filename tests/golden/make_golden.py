@@ -1,0 +1,88 @@
+"""Generate the golden fixtures in tests/golden/ from the REFERENCE itself:
+/root/reference/proj/src/*.cpp compiled unmodified into oracle/_ref
+(oracle/build_ref.sh), driven through oracle/ref_driver.cpp.
+
+Run here (the reference tree exists only in the build container):
+    bash oracle/build_ref.sh && python tests/golden/make_golden.py
+
+Each case_*.npz holds the reference's setup products (reduced dims, time and
+space bands, eigenpairs, composite eigenvalues), a seeded input r
+(std::mt19937_64(1234), re/im = 2u-1), and the reference's outputs:
+FD apply z = P^-1 r, matvec y = A r, one factored block (ab, piv), and a
+PCG solve (iterations, residual history, x). Outputs are produced twice:
+with the reference's scalar backend (bit-exact target for the C oracle) and
+with its default AVX2 backend ("_avx2" keys, the reference as shipped).
+tw_*.npz hold the 2-D traveling-wave right-hand sides of the paper's Table 2
+(lift_nonhomogeneous) and the reference's FD-PCG counts.
+"""
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+from oracle import oracle as O  # noqa: E402
+from oracle import refdrv  # noqa: E402
+
+CASES = [  # (d, p, n_el, n_el_t) -- reference unit-test shapes + config 1 + 3-D
+    (1, 2, 5, 4), (2, 2, 3, 4), (1, 2, 1, 1), (1, 3, 6, 6), (1, 3, 64, 64),
+    (2, 3, 10, 9), (2, 4, 6, 5), (2, 6, 5, 5), (3, 2, 6, 6), (3, 4, 4, 4),
+]
+TW = [(2, 8), (3, 8), (4, 8), (2, 16), (3, 16), (4, 16)]  # Table 2: 7 / 9 / 10 +- 2
+
+
+def case(d, p, n_el, n_el_t):
+    out = {}
+    R = refdrv.RefProblem(d, p, n_el, n_el_t)
+    Lt, Mt, Wt = R.time_bands()
+    out.update(dims=np.array(R.dims), d=d, p=p, nu=1.0, Lt=Lt, Mt=Mt, Wt=Wt,
+               lam_composite=R.composite_lambda())
+    for l in range(d):
+        U, lam = R.eig(l)
+        M, L, G, V = R.space_bands(l)
+        out.update({f"U{l}": U, f"lam{l}": lam, f"M{l}": M, f"L{l}": L, f"G{l}": G, f"V{l}": V})
+    r = O.random_vec(R.N, 1234)
+    out["r"] = r
+    ns = R.N // R.dims[0]
+    ab, piv = R.fd_block(ns // 2)
+    out.update(block_index=ns // 2, block_ab=ab, block_piv=piv)
+    for tag, be in (("", "scalar"), ("_avx2", "auto")):
+        refdrv.force_backend(be)
+        out["z" + tag] = R.fd_apply(r)
+        out["y" + tag] = R.kron_apply(r)
+        s = R.pcg(r, 1e-8, 200)
+        out["pcg_iters" + tag] = s["iterations"]
+        out["pcg_hist" + tag] = np.array(s["res_history"])
+        out["pcg_x" + tag] = s["x"]
+    refdrv.force_backend("scalar")
+    return out
+
+
+def main():
+    for c in CASES:
+        name = "case_d%d_p%d_n%d_t%d.npz" % c
+        np.savez_compressed(os.path.join(HERE, name), **case(*c))
+        print("wrote", name)
+    for p, n_el in TW:
+        R = refdrv.RefProblem(2, p, n_el, n_el)
+        refdrv.force_backend("auto")
+        b = R.named_rhs("traveling_wave_2d")
+        s = R.pcg(b, 1e-8, 200)
+        Lt, Mt, Wt = R.time_bands()
+        d = {"dims": np.array(R.dims), "p": p, "b": b, "pcg_iters": s["iterations"],
+             "Lt": Lt, "Mt": Mt, "Wt": Wt}
+        for l in range(2):
+            U, lam = R.eig(l)
+            M, L, G, V = R.space_bands(l)
+            d.update({f"U{l}": U, f"lam{l}": lam, f"M{l}": M, f"L{l}": L, f"G{l}": G, f"V{l}": V})
+        name = "tw_p%d_n%d.npz" % (p, n_el)
+        np.savez_compressed(os.path.join(HERE, name), **d)
+        print("wrote", name, "iters", s["iterations"])
+    refdrv.force_backend("scalar")
+
+
+if __name__ == "__main__":
+    main()
