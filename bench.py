@@ -319,7 +319,7 @@ def main():
                        "dims": dims, "dofs": n,
                        "parallelism": "replicas" if ws > 1 else "single",
                        "l2": "inputs (272 MB/vector) larger than L2; no flush",
-                       "transform_engine": ["dfma", "dmma"][ks.lib().ks_transform_engine()]},
+                       "transform_engine": {0: "dfma", 1: "dmma_v1", 2: "dmma_v2"}[ks.lib().ks_transform_engine()]},
             "e2e": {"value": e2e_val, "unit": "DOF/s", "h2d_bytes_per_step": n * 16,
                     "d2h_bytes_per_step": n * 16, "ms_per_step": e2e_s * 1e3},
             "gpu_launches": launches,

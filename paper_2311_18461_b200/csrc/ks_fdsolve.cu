@@ -190,6 +190,107 @@ __global__ void __launch_bounds__(128) k_fd_solve(const double2* __restrict__ ab
     }
 }
 
+// ---------------------------------------------------------------------------
+// solve v2 (default): a CTA owns kFib consecutive fibers = one contiguous block
+// of kFib*nt complex, staged through shared memory with fully coalesced loads
+// and stores (sm[k][fiber], row pitch kFib+1 keeps 16 B accesses conflict-free).
+// Each thread then runs its fiber's forward/backward sweeps out of shared
+// memory, with the next step's band column prefetched into registers so the
+// factor loads (the dominant HBM traffic, 16(3p+1) B/DOF) overlap the
+// recurrence.
+// ---------------------------------------------------------------------------
+constexpr int kFib = 64;
+
+template <int P>
+__global__ void __launch_bounds__(kFib) k_fd_solve2(const double2* __restrict__ ab,
+                                                    const unsigned char* __restrict__ piv,
+                                                    double2* __restrict__ X, size_t ns, int nt) {
+    constexpr int ldab = 3 * P + 1, kuf = 2 * P;
+    constexpr int PITCH = kFib + 1;
+    extern __shared__ double2 sx[]; // [nt][PITCH]
+    const size_t f0 = (size_t)blockIdx.x * kFib;
+    const int nf = (int)min((size_t)kFib, ns - f0);
+    const int tid = threadIdx.x;
+    double2* xb = X + f0 * (size_t)nt;
+    const int tot = nf * nt;
+    for (int e = tid; e < tot; e += kFib) {
+        const int f = e / nt, k = e - f * nt;
+        sx[k * PITCH + f] = xb[e];
+    }
+    __syncthreads();
+    if (tid < nf) {
+        const size_t i = f0 + tid;
+        auto band = [&](int k, int e) -> double2 {
+            return __ldg(ab + ((size_t)k * ldab + e) * ns + i);
+        };
+        double2* x = sx + tid;
+        // forward: L with interchanges; w[m] = x[k+m]
+        double2 w[P + 1];
+#pragma unroll
+        for (int m = 0; m <= P; ++m) w[m] = m < nt ? x[m * PITCH] : make_double2(0.0, 0.0);
+        double2 lnext[P];
+        int pnext = piv[i];
+#pragma unroll
+        for (int m = 1; m <= P; ++m) lnext[m - 1] = m < nt ? band(0, kuf + m) : make_double2(0, 0);
+        for (int k = 0; k < nt; ++k) {
+            double2 l[P];
+#pragma unroll
+            for (int m = 0; m < P; ++m) l[m] = lnext[m];
+            const int po = pnext;
+            if (k + 1 < nt) {
+                pnext = piv[(size_t)(k + 1) * ns + i];
+#pragma unroll
+                for (int m = 1; m <= P; ++m)
+                    lnext[m - 1] = (k + 1 + m < nt) ? band(k + 1, kuf + m) : make_double2(0, 0);
+            }
+#pragma unroll
+            for (int m = 1; m <= P; ++m)
+                if (po == m) {
+                    const double2 t = w[0];
+                    w[0] = w[m];
+                    w[m] = t;
+                }
+#pragma unroll
+            for (int m = 1; m <= P; ++m)
+                if (k + m < nt) w[m] = csub(w[m], cmul(l[m - 1], w[0]));
+            x[k * PITCH] = w[0];
+#pragma unroll
+            for (int m = 0; m < P; ++m) w[m] = w[m + 1];
+            w[P] = (k + P + 1 < nt) ? x[(k + P + 1) * PITCH] : make_double2(0.0, 0.0);
+        }
+        // backward: U column oriented; u[j] = x[k-j]
+        double2 u[2 * P + 1];
+#pragma unroll
+        for (int j = 0; j <= 2 * P; ++j)
+            u[j] = (nt - 1 - j >= 0) ? x[(nt - 1 - j) * PITCH] : make_double2(0.0, 0.0);
+        double2 unext[2 * P + 1];
+#pragma unroll
+        for (int j = 0; j <= 2 * P; ++j) unext[j] = band(nt - 1, kuf - j);
+        for (int k = nt - 1; k >= 0; --k) {
+            double2 uc[2 * P + 1];
+#pragma unroll
+            for (int j = 0; j <= 2 * P; ++j) uc[j] = unext[j];
+            if (k > 0) {
+#pragma unroll
+                for (int j = 0; j <= 2 * P; ++j) unext[j] = band(k - 1, kuf - j);
+            }
+            u[0] = cdiv(u[0], uc[0]);
+#pragma unroll
+            for (int j = 1; j <= 2 * P; ++j)
+                if (k - j >= 0) u[j] = csub(u[j], cmul(uc[j], u[0]));
+            x[k * PITCH] = u[0];
+#pragma unroll
+            for (int j = 0; j < 2 * P; ++j) u[j] = u[j + 1];
+            u[2 * P] = (k - 2 * P - 1 >= 0) ? x[(k - 2 * P - 1) * PITCH] : make_double2(0.0, 0.0);
+        }
+    }
+    __syncthreads();
+    for (int e = tid; e < tot; e += kFib) {
+        const int f = e / nt, k = e - f * nt;
+        xb[e] = sx[k * PITCH + f];
+    }
+}
+
 // adjoint: H_i^{-H} x (eigensolve.cpp:148-170)
 template <int P>
 __global__ void __launch_bounds__(128) k_fd_solve_adj(const double2* __restrict__ ab,
@@ -259,9 +360,23 @@ void launch_solve_p(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t st
                                                 B.ns, B.nt);
         check_launch("k_fd_solve_adj");
     } else {
-        k_fd_solve<P><<<grid, 128, 0, st>>>(B.ab.as<double2>(), B.piv.as<unsigned char>(), X,
-                                            B.ns, B.nt);
-        check_launch("k_fd_solve");
+        const size_t sm = (size_t)B.nt * (kFib + 1) * sizeof(double2);
+        if (sm <= 200 * 1024) {
+            static bool attr = false;
+            if (!attr) {
+                KS_CUDA(cudaFuncSetAttribute(k_fd_solve2<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             200 * 1024));
+                attr = true;
+            }
+            const unsigned g2 = (unsigned)((B.ns + kFib - 1) / kFib);
+            k_fd_solve2<P><<<g2, kFib, sm, st>>>(B.ab.as<double2>(), B.piv.as<unsigned char>(), X,
+                                                 B.ns, B.nt);
+            check_launch("k_fd_solve2");
+        } else {
+            k_fd_solve<P><<<grid, 128, 0, st>>>(B.ab.as<double2>(), B.piv.as<unsigned char>(), X,
+                                                B.ns, B.nt);
+            check_launch("k_fd_solve");
+        }
     }
 }
 

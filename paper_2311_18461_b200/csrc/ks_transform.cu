@@ -28,6 +28,7 @@
 #include "ks_internal.hpp"
 
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 
 namespace ks {
@@ -289,12 +290,134 @@ k_mode_gemm_dmma(const double* __restrict__ At, int n, const double* __restrict_
     }
 }
 
+// ---------------------------------------------------------------------------
+// DMMA engine v2 (default): persistent CTAs, the whole n x n matrix resident in
+// shared memory (loaded once per CTA), and a continuous S-stage cp.async ring
+// over (column tile, k-chunk) work items, so the loads of the next tile are in
+// flight while the current tile's DMMAs run. Same warp/fragment layout as
+// k_mode_gemm_dmma. <=128 registers for TM <= 5 so two CTAs share an SM.
+// ---------------------------------------------------------------------------
+constexpr int kStages = 4;
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, bool valid) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    const int sz = valid ? 16 : 0; // src-size 0 -> zero fill
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gsrc), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N> __device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <int TM>
+__global__ void __launch_bounds__(kThreads, (TM <= 5 ? 2 : 1))
+k_mode_gemm_dmma2(const double* __restrict__ At, int n, const double* __restrict__ X,
+                  double* __restrict__ Y, long long W2, long long C, int ntiles) {
+    constexpr int BM = 16 * TM;
+    constexpr int MT = TM;
+    constexpr int BMP = BM + 4; // == 4 (mod 16): conflict-free fragment loads
+    constexpr int BNP = kBN + 4;
+    extern __shared__ __align__(16) double smem[];
+    const int nk = (n + kBK - 1) / kBK;
+    double* As = smem;                      // [nk*kBK][BMP]
+    double* Bs = smem + (size_t)nk * kBK * BMP; // [kStages][kBK][BNP]
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wr = warp & 1, wc = warp >> 1;
+
+    // A once: As[j][r] = At[j*n + r] (zero padded)
+    for (int e = tid; e < nk * kBK * BM; e += kThreads) {
+        const int j = e / BM, r = e - j * BM;
+        As[j * BMP + r] = (j < n && r < n) ? __ldg(At + (long long)j * n + r) : 0.0;
+    }
+
+    const int lcp = tid & 63, lrow0 = tid >> 6;
+    const int my_tiles = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    const int nwork = my_tiles * nk;
+
+    auto issue = [&](int w) {
+        if (w < nwork) {
+            const int t = (int)blockIdx.x + (w / nk) * (int)gridDim.x;
+            const int kc = w - (w / nk) * nk;
+            const long long c = (long long)t * kBN + 2 * lcp;
+            const bool cv = c < C;
+            long long off = 0;
+            if (cv) {
+                const long long o = c / W2, q = c - o * W2;
+                off = o * (long long)n * W2 + q;
+            }
+            double* bs = Bs + (size_t)(w % kStages) * kBK * BNP;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int jj = lrow0 + 4 * k, j = kc * kBK + jj;
+                const bool v = cv && j < n;
+                cp_async16(bs + jj * BNP + 2 * lcp, v ? (const void*)(X + off + (long long)j * W2) : (const void*)X, v);
+            }
+        }
+        cp_async_commit();
+    };
+
+    double acc[MT][4][2];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int m = 0; m < 4; ++m) acc[i][m][0] = acc[i][m][1] = 0.0;
+
+#pragma unroll
+    for (int s = 0; s < kStages - 1; ++s) issue(s);
+
+    const int r_warp = wr * (BM / 2), c_warp = wc * 32;
+    const int ar = lane >> 2, ak = lane & 3;
+    const int cr = lane >> 2, cc = 2 * (lane & 3);
+    for (int w = 0; w < nwork; ++w) {
+        cp_async_wait<kStages - 2>();
+        __syncthreads();
+        issue(w + kStages - 1);
+        const int kc = w % nk;
+        const double* bs = Bs + (size_t)(w % kStages) * kBK * BNP;
+        const double* as = As + (size_t)kc * kBK * BMP;
+#pragma unroll
+        for (int k4 = 0; k4 < kBK; k4 += 4) {
+            double a[MT], b[4];
+#pragma unroll
+            for (int i = 0; i < MT; ++i) a[i] = as[(k4 + ak) * BMP + r_warp + i * 8 + ar];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) b[m] = bs[(k4 + ak) * BNP + c_warp + m * 8 + ar];
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int m = 0; m < 4; ++m) dmma_m8n8k4(acc[i][m][0], acc[i][m][1], a[i], b[m]);
+        }
+        if (kc == nk - 1) {
+            const int t = (int)blockIdx.x + (w / nk) * (int)gridDim.x;
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const long long c = (long long)t * kBN + c_warp + m * 8 + cc;
+                if (c < C) {
+                    const long long o = c / W2, q = c - o * W2;
+                    double* yb = Y + o * (long long)n * W2 + q;
+#pragma unroll
+                    for (int i = 0; i < MT; ++i) {
+                        const int r = r_warp + i * 8 + cr;
+                        if (r < n)
+                            *reinterpret_cast<double2*>(yb + (long long)r * W2) =
+                                make_double2(acc[i][m][0], acc[i][m][1]);
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < MT; ++i) acc[i][m][0] = acc[i][m][1] = 0.0;
+            }
+        }
+    }
+    cp_async_wait<0>();
+}
+
 int engine_choice() {
     static int e = [] {
         const char* v = std::getenv("KS_GEMM");
         if (v && std::strcmp(v, "dfma") == 0) return 0;
-        if (v && std::strcmp(v, "dmma") == 0) return 1;
-        return 1; // default: DMMA (profiles/ for the measurement)
+        if (v && std::strcmp(v, "dmma1") == 0) return 1;
+        return 2; // default: DMMA v2 (profiles/ for the measurement)
     }();
     return e;
 }
@@ -313,6 +436,24 @@ void launch_tm(int engine, const double* At, int n, const double* X, double* Y, 
         }
         k_mode_gemm_dfma<TM><<<grid, kThreads, sm, st>>>(At, n, X, Y, W2, C);
         check_launch("k_mode_gemm_dfma");
+    } else if (engine == 2) {
+        const int nk = (n + kBK - 1) / kBK;
+        const size_t sm = ((size_t)nk * kBK * (16 * TM + 4) + (size_t)kStages * kBK * (kBN + 4)) *
+                          sizeof(double);
+        static int sms = 0;
+        if (!sms) {
+            int dev = 0;
+            KS_CUDA(cudaGetDevice(&dev));
+            KS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            KS_CUDA(cudaFuncSetAttribute(k_mode_gemm_dmma2<TM>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        }
+        KS_REQUIRE(sm <= 227 * 1024, KS_EINVAL, "mode product: axis too long for the resident-A kernel");
+        const int per_sm = (TM <= 5 && 2 * sm <= 227 * 1024) ? 2 : 1;
+        const int ntiles = (int)grid;
+        const unsigned g2 = (unsigned)std::min<long long>(ntiles, (long long)sms * per_sm);
+        k_mode_gemm_dmma2<TM><<<g2, kThreads, sm, st>>>(At, n, X, Y, W2, C, ntiles);
+        check_launch("k_mode_gemm_dmma2");
     } else {
         const size_t sm = (size_t)2 * kBK * (16 * TM + 4 + kBN + 4) * sizeof(double);
         static bool attr = false;
