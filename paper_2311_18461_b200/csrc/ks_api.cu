@@ -2,7 +2,9 @@
 // device-resident PCG, BLAS-1 entry points, device plumbing and timing.
 #include "ks_internal.hpp"
 
+#include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -71,6 +73,7 @@ struct ks_fd {
     size_t N = 0, Ns = 0;
     std::vector<DevBuf> At_fwd, At_inv, lam;
     std::vector<std::vector<double>> lam_host;
+    std::vector<int> fiber_block; // host copy of the block map (empty = identity)
     DevBuf Lt, Mt, Wsym;
     FdBlocks blocks;
     DevBuf s0, s1, io;
@@ -237,7 +240,6 @@ int ks_fd_create(int d, const int* dims, double nu, int p_t, const double* const
     for (int l = 1; l <= d; ++l) f->Ns *= (size_t)dims[l];
     f->N = f->Ns * (size_t)dims[0];
     KS_CUDA(cudaStreamCreateWithFlags(&f->stream, cudaStreamNonBlocking));
-    std::vector<const double*> lam_dev;
     for (int l = 0; l < d; ++l) {
         const int n = dims[l + 1];
         for (int i = 0; i < n; ++i)
@@ -258,7 +260,6 @@ int ks_fd_create(int d, const int* dims, double nu, int p_t, const double* const
         f->lam.emplace_back(n * sizeof(double));
         KS_CUDA(cudaMemcpy(f->lam.back().p, lambda[l], n * sizeof(double), cudaMemcpyHostToDevice));
         f->lam_host.emplace_back(lambda[l], lambda[l] + n);
-        lam_dev.push_back(f->lam.back().as<double>());
     }
     const int nt = dims[0], ld = 2 * p_t + 1;
     // W + W^H (fdsolver.cpp:95-103)
@@ -279,17 +280,69 @@ int ks_fd_create(int d, const int* dims, double nu, int p_t, const double* const
     KS_CUDA(cudaMemcpy(f->Lt.p, Lt, (size_t)ld * nt * sizeof(double), cudaMemcpyHostToDevice));
     KS_CUDA(cudaMemcpy(f->Mt.p, Mt, (size_t)ld * nt * sizeof(double), cudaMemcpyHostToDevice));
     KS_CUDA(cudaMemcpy(f->Wsym.p, ws.data(), ws.size() * sizeof(double2), cudaMemcpyHostToDevice));
-    // factor all N_s blocks on the device (fdsolver.cpp:46-51)
+    // factored blocks (fdsolver.cpp:46-51): one per composite eigenvalue, or one
+    // per distinct eigenvalue when all axes carry identical 1-D spectra.
     FdBlocks& B = f->blocks;
     B.nt = nt;
     B.p = p_t;
     B.ldab = 3 * p_t + 1;
     B.ns = f->Ns;
-    B.ab.alloc((size_t)nt * B.ldab * B.ns * sizeof(double2));
-    B.piv.alloc((size_t)nt * B.ns);
+    bool dedup = d >= 2;
+    for (int l = 1; l < d && dedup; ++l)
+        dedup = dims[l + 1] == dims[1] &&
+                std::memcmp(lambda[l], lambda[0], sizeof(double) * dims[1]) == 0;
+    if (const char* e = std::getenv("KS_FD_DEDUP")) dedup = dedup && std::strcmp(e, "0") != 0;
+    std::vector<double> lam_blk;
+    f->fiber_block.clear();
+    auto ref_sum = [&](const int* idx) { // fdsolver.cpp:33-35 order
+        double sum = 0;
+        for (int l = 0; l < d; ++l) sum += lambda[l][idx[l]];
+        return sum;
+    };
+    int idx[3] = {0, 0, 0};
+    if (!dedup) {
+        lam_blk.resize(f->Ns);
+        for (size_t i = 0; i < f->Ns; ++i) {
+            lam_blk[i] = ref_sum(idx);
+            for (int l = 0; l < d; ++l) {
+                if (++idx[l] < dims[l + 1]) break;
+                idx[l] = 0;
+            }
+        }
+    } else {
+        const size_t n = (size_t)dims[1];
+        std::vector<int> id_of(f->Ns, -1);
+        f->fiber_block.resize(f->Ns);
+        // blocks are numbered by the spatial index of their sorted multi-index
+        for (size_t i = 0; i < f->Ns; ++i) {
+            bool sorted = true;
+            for (int l = 1; l < d; ++l) sorted &= idx[l - 1] <= idx[l];
+            if (sorted) {
+                id_of[i] = (int)lam_blk.size();
+                lam_blk.push_back(ref_sum(idx));
+            }
+            int srt[3] = {idx[0], idx[1], idx[2]};
+            std::sort(srt, srt + d);
+            size_t key = 0;
+            for (int l = d - 1; l >= 0; --l) key = key * n + (size_t)srt[l];
+            f->fiber_block[i] = key; // resolved below (key <= i)
+            for (int l = 0; l < d; ++l) {
+                if (++idx[l] < dims[l + 1]) break;
+                idx[l] = 0;
+            }
+        }
+        for (size_t i = 0; i < f->Ns; ++i) f->fiber_block[i] = id_of[f->fiber_block[i]];
+        B.fiber_block.alloc(f->Ns * sizeof(int));
+        KS_CUDA(cudaMemcpy(B.fiber_block.p, f->fiber_block.data(), f->Ns * sizeof(int),
+                           cudaMemcpyHostToDevice));
+    }
+    B.nblk = lam_blk.size();
+    B.lam_blk.alloc(B.nblk * sizeof(double));
+    KS_CUDA(cudaMemcpy(B.lam_blk.p, lam_blk.data(), B.nblk * sizeof(double), cudaMemcpyHostToDevice));
+    B.ab.alloc((size_t)nt * B.ldab * B.nblk * sizeof(double2));
+    B.piv.alloc((size_t)nt * B.nblk);
     B.flag.alloc(sizeof(int));
-    launch_fd_factor(B, d, dims + 1, lam_dev.data(), nu, f->Lt.as<double>(), f->Mt.as<double>(),
-                     f->Wsym.as<double2>(), f->stream);
+    launch_fd_factor(B, nu, f->Lt.as<double>(), f->Mt.as<double>(), f->Wsym.as<double2>(), f->stream);
     f->s0.alloc(f->N * sizeof(double2));
     f->s1.alloc(f->N * sizeof(double2));
     KS_CUDA(cudaStreamSynchronize(f->stream));
@@ -333,13 +386,14 @@ int ks_fd_block(const ks_fd* fd, size_t i, ks_c64* ab, int* piv) {
     KS_REQUIRE(i < fd->Ns, KS_EINVAL, "ks_fd_block: index out of range");
     ensure_device(fd->device);
     const FdBlocks& B = fd->blocks;
+    const size_t b = fd->fiber_block.empty() ? i : (size_t)fd->fiber_block[i];
     for (int k = 0; k < B.nt; ++k) {
         for (int e = 0; e < B.ldab; ++e)
             KS_CUDA(cudaMemcpy(ab + (size_t)k * B.ldab + e,
-                               B.ab.as<double2>() + ((size_t)k * B.ldab + e) * B.ns + i,
+                               B.ab.as<double2>() + ((size_t)k * B.ldab + e) * B.nblk + b,
                                sizeof(double2), cudaMemcpyDeviceToHost));
         unsigned char po = 0;
-        KS_CUDA(cudaMemcpy(&po, B.piv.as<unsigned char>() + (size_t)k * B.ns + i, 1,
+        KS_CUDA(cudaMemcpy(&po, B.piv.as<unsigned char>() + (size_t)k * B.nblk + b, 1,
                            cudaMemcpyDeviceToHost));
         piv[k] = k + po;
     }

@@ -128,15 +128,17 @@ void launch_mode_gemm(const double* At, int n, const double* X, double* Y,
 // ---------------------------------------------------------------------------
 struct FdBlocks {
     int nt = 0, p = 0, ldab = 0;
-    size_t ns = 0;
-    DevBuf ab;   // complex [nt][ldab][ns]  (fiber-interleaved band columns)
-    DevBuf piv;  // uint8 [nt][ns]  pivot offset piv[k]-k in 0..p
-    DevBuf flag; // int: singular-pivot flag set by the factor kernel
+    size_t ns = 0;      // fibers (= N_s)
+    size_t nblk = 0;    // factored blocks (N_s, or fewer when deduplicated)
+    DevBuf ab;          // complex [nt][ldab][nblk]  (block-interleaved band columns)
+    DevBuf piv;         // uint8 [nt][nblk]  pivot offset piv[k]-k in 0..p
+    DevBuf flag;        // int: singular-pivot flag set by the factor kernel
+    DevBuf lam_blk;     // double [nblk] composite eigenvalue of each block
+    DevBuf fiber_block; // int [ns] block of each fiber (empty = identity)
 };
-// lam_axes: d device arrays; time bands on device: Lt, Mt real (2p+1)xnt, Wsym complex
-void launch_fd_factor(FdBlocks& B, int d, const int* ns_axes, const double* const* lam_axes_dev,
-                      double nu, const double* Lt, const double* Mt, const double2* Wsym,
-                      cudaStream_t st);
+// time bands on device: Lt, Mt real (2p+1)xnt, Wsym complex
+void launch_fd_factor(FdBlocks& B, double nu, const double* Lt, const double* Mt,
+                      const double2* Wsym, cudaStream_t st);
 void launch_fd_solve(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t st);
 
 // ---------------------------------------------------------------------------

@@ -131,6 +131,131 @@ __global__ void __launch_bounds__(256) k_kron_level(
     }
 }
 
+// ---------------------------------------------------------------------------
+// Level pass v2: a CTA owns TQ consecutive "columns" (o, q) and the FULL axis
+// extent r = 0..n-1 of each, so every band product is local (no halo). The
+// input nodes are staged through shared memory one at a time (coalesced:
+// along q for s > 1, along r for the contiguous time axis s = 1), and every
+// output node accumulates in registers; each input element is read from HBM
+// once and each output written once per pass.
+// Thread layout: column cc = tid % TQ, rows r = tid / TQ + k * (256 / TQ).
+// ---------------------------------------------------------------------------
+constexpr int kLvThreads = 256;
+constexpr int kMaxOut = 8;
+constexpr int kRPT = 5; // rows per thread (n <= kRPT * 256 / TQ)
+
+template <int NOUT>
+__global__ void __launch_bounds__(kLvThreads) k_kron_level2(
+    const double2* const* __restrict__ in_ptrs, int n_in, double2* const* __restrict__ out_ptrs,
+    const int* __restrict__ out_begin, const KronContrib* __restrict__ contribs,
+    const DevFactor* __restrict__ factors, const double2* __restrict__ bands, size_t ncols,
+    size_t s, int n, int TQ) {
+    extern __shared__ double2 tile[]; // [n][TQ + 1]
+    const int tid = threadIdx.x;
+    const int pitch = TQ + 1;
+    const int rstep = kLvThreads / TQ;
+    const int cc = tid % TQ, r0 = tid / TQ;
+    const size_t c0 = (size_t)blockIdx.x * TQ;
+    const int ncol = (int)min((size_t)TQ, ncols - c0);
+    // this thread's column -> base address
+    const size_t cme = c0 + cc;
+    const size_t o = cme / s, q = cme - o * s;
+    const size_t base = o * (size_t)n * s + q;
+    const bool cvalid = cc < ncol;
+
+    double2 acc[NOUT][kRPT];
+#pragma unroll
+    for (int a = 0; a < NOUT; ++a)
+#pragma unroll
+        for (int k = 0; k < kRPT; ++k) acc[a][k] = make_double2(0.0, 0.0);
+
+    for (int j = 0; j < n_in; ++j) {
+        const double2* __restrict__ in = in_ptrs[j];
+        __syncthreads();
+        const int tot = n * TQ;
+        if (s == 1) { // contiguous fibers: consecutive threads walk r
+            for (int e = tid; e < tot; e += kLvThreads) {
+                const int c = e / n, r = e - c * n;
+                tile[r * pitch + c] = c < ncol ? __ldg(in + (c0 + c) * (size_t)n + r) : make_double2(0, 0);
+            }
+        } else {      // consecutive threads walk the contiguous q
+            for (int e = tid; e < tot; e += kLvThreads) {
+                const int r = e / TQ, c = e - r * TQ;
+                const size_t cm = c0 + c;
+                double2 v = make_double2(0, 0);
+                if (c < ncol) {
+                    const size_t oo = cm / s, qq = cm - oo * s;
+                    v = __ldg(in + oo * (size_t)n * s + (size_t)r * s + qq);
+                }
+                tile[r * pitch + c] = v;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int oi = 0; oi < NOUT; ++oi) {
+            const int cb = out_begin[oi], ce = out_begin[oi + 1];
+            for (int ci = cb; ci < ce; ++ci) {
+                const KronContrib c = contribs[ci];
+                if (c.in != j) continue;
+#pragma unroll
+                for (int k = 0; k < kRPT; ++k) {
+                    const int r = r0 + k * rstep;
+                    if (r >= n) break;
+                    double vr, vi;
+                    if (c.factor < 0) {
+                        const double2 v = tile[r * pitch + cc];
+                        vr = v.x;
+                        vi = v.y;
+                    } else {
+                        const DevFactor f = factors[c.factor];
+                        const int bw = f.bw, ld = 2 * bw + 1;
+                        const int j0 = r - bw < 0 ? 0 : r - bw;
+                        const int j1 = r + bw > n - 1 ? n - 1 : r + bw;
+                        const double2* band = bands + f.off;
+                        vr = 0.0;
+                        vi = 0.0;
+                        if (f.is_real) {
+                            for (int jj = j0; jj <= j1; ++jj) {
+                                const double a = __ldg(&band[bw + r - jj + jj * ld].x);
+                                const double2 v = tile[jj * pitch + cc];
+                                vr = fma(a, v.x, vr);
+                                vi = fma(a, v.y, vi);
+                            }
+                        } else {
+                            for (int jj = j0; jj <= j1; ++jj) {
+                                const double2 a = __ldg(&band[bw + r - jj + jj * ld]);
+                                const double2 v = tile[jj * pitch + cc];
+                                vr = fma(a.x, v.x, fma(-a.y, v.y, vr));
+                                vi = fma(a.x, v.y, fma(a.y, v.x, vi));
+                            }
+                        }
+                    }
+                    double2& A = acc[oi][k];
+                    if (c.coeff.y == 0.0) {
+                        A.x = fma(c.coeff.x, vr, A.x);
+                        A.y = fma(c.coeff.x, vi, A.y);
+                    } else {
+                        A.x = fma(c.coeff.x, vr, fma(-c.coeff.y, vi, A.x));
+                        A.y = fma(c.coeff.x, vi, fma(c.coeff.y, vr, A.y));
+                    }
+                }
+            }
+        }
+    }
+    // write outputs (thread-per-(r, column): coalesced along q for s > 1)
+    if (!cvalid) return;
+#pragma unroll
+    for (int oi = 0; oi < NOUT; ++oi) {
+        double2* __restrict__ out = out_ptrs[oi];
+#pragma unroll
+        for (int k = 0; k < kRPT; ++k) {
+            const int r = r0 + k * rstep;
+            if (r >= n) break;
+            out[base + (size_t)r * s] = acc[oi][k];
+        }
+    }
+}
+
 } // namespace
 
 // Build the plan. terms: coeff + per-axis factor id (-1 identity).
@@ -318,6 +443,30 @@ void kron_apply(KronPlan& P, const double2* x, double2* y, cudaStream_t st,
         size_t s = 1;
         for (int a = 0; a < ps.axis; ++a) s *= (size_t)P.dims[a];
         const int n = P.dims[ps.axis];
+        // v2 (smem-tiled) when the level fits its register budget
+        int TQ = 16;
+        while (TQ > 1 && (n + kLvThreads / TQ - 1) / (kLvThreads / TQ) > kRPT) TQ /= 2;
+        const bool v2 = ps.n_out <= kMaxOut && (n + kLvThreads / TQ - 1) / (kLvThreads / TQ) <= kRPT;
+        if (v2) {
+            const size_t ncols = P.N / (size_t)n;
+            const size_t sm = (size_t)n * (TQ + 1) * sizeof(double2);
+            const unsigned g2 = (unsigned)((ncols + TQ - 1) / TQ);
+            auto ip = reinterpret_cast<const double2* const*>(dp + P.ptr_off[k]);
+            auto op = reinterpret_cast<double2* const*>(const_cast<void**>(dp + P.ptr_off[k] + ps.n_in));
+#define KS_LV2(NO)                                                                              \
+    case NO:                                                                                    \
+        k_kron_level2<NO><<<g2, kLvThreads, sm, st>>>(ip, ps.n_in, op, ps.d_begin.as<int>(),    \
+                                                      ps.d_contribs.as<KronContrib>(),         \
+                                                      P.d_factors.as<DevFactor>(),             \
+                                                      P.d_bands.as<double2>(), ncols, s, n, TQ); \
+        break;
+            switch (ps.n_out) {
+                KS_LV2(1) KS_LV2(2) KS_LV2(3) KS_LV2(4) KS_LV2(5) KS_LV2(6) KS_LV2(7) KS_LV2(8)
+            }
+#undef KS_LV2
+            check_launch("k_kron_level2");
+            continue;
+        }
         const unsigned grid = (unsigned)((P.N + 255) / 256);
         k_kron_level<<<grid, 256, 0, st>>>(
             reinterpret_cast<const double2* const*>(dp + P.ptr_off[k]),
