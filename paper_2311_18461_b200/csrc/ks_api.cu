@@ -113,7 +113,7 @@ void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStre
     double* bufs[2] = {f->s0.as<double>(), f->s1.as<double>()};
     int nb = 0;
     size_t s = f->dims[0];
-    auto gemm = [&](const DevBuf& At, int l, const double* in, double* out) {
+    auto gemm = [&](const DevBuf& At, int l, const double* in, double* out, int layout) {
         const int n = f->dims[l];
         size_t stride = 1;
         for (int k = 0; k < l; ++k) stride *= (size_t)f->dims[k];
@@ -123,29 +123,34 @@ void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStre
             KS_CUDA(cudaEventCreate(&a));
             KS_CUDA(cudaEventCreate(&b));
             KS_CUDA(cudaEventRecord(a, st));
-            launch_mode_gemm(At.as<double>(), n, in, out, stride, outer, st);
+            launch_mode_gemm(At.as<double>(), n, in, out, stride, outer, st, layout, f->dims[0]);
             KS_CUDA(cudaEventRecord(b, st));
             ev->push_back(a);
             ev->push_back(b);
         } else {
-            launch_mode_gemm(At.as<double>(), n, in, out, stride, outer, st);
+            launch_mode_gemm(At.as<double>(), n, in, out, stride, outer, st, layout, f->dims[0]);
         }
     };
     (void)s;
-    // to_eigen: axes 1..d with U_l^T (fdsolver.cpp:7-14)
+    // to_eigen: axes 1..d with U_l^T (fdsolver.cpp:7-14). The last one (the
+    // outermost axis d) writes the time-major layout T[t][fiber] so that the
+    // block solves read and write coalesced.
     for (int l = 1; l <= d; ++l) {
         double* out = bufs[nb];
         nb ^= 1;
-        gemm(f->At_fwd[l - 1], l, cur, out);
+        gemm(f->At_fwd[l - 1], l, cur, out, l == d ? 1 : 0);
         cur = out;
     }
-    // N_s block solves (fdsolver.cpp:58-60)
-    launch_fd_solve(f->blocks, reinterpret_cast<double2*>(const_cast<double*>(cur)), adjoint, st);
-    // from_eigen: axes 1..d with U_l (fdsolver.cpp:16-21)
-    for (int l = 1; l <= d; ++l) {
-        double* out = (l == d) ? reinterpret_cast<double*>(z) : bufs[nb];
-        if (l != d) nb ^= 1;
-        gemm(f->At_inv[l - 1], l, cur, out);
+    // N_s block solves (fdsolver.cpp:58-60), time-major
+    launch_fd_solve(f->blocks, reinterpret_cast<double2*>(const_cast<double*>(cur)), adjoint, st, true);
+    // from_eigen with U_l (fdsolver.cpp:16-21): axis d first (it consumes the
+    // time-major layout), then axes 1..d-1. Mode products on distinct axes
+    // commute, so only the rounding order differs.
+    for (int k = 0; k < d; ++k) {
+        const int l = k == 0 ? d : k;
+        double* out = (k == d - 1) ? reinterpret_cast<double*>(z) : bufs[nb];
+        if (k != d - 1) nb ^= 1;
+        gemm(f->At_inv[l - 1], l, cur, out, k == 0 ? 2 : 0);
         cur = out;
     }
 }

@@ -142,11 +142,19 @@ template <int P>
 __global__ void __launch_bounds__(128) k_fd_solve(const double2* __restrict__ ab,
                                                   const unsigned char* __restrict__ piv,
                                                   double2* __restrict__ X, size_t ns, int nt,
-                                                  size_t nblk, const int* __restrict__ fblk) {
+                                                  size_t nblk, const int* __restrict__ fblk,
+                                                  int tmajor) {
     const size_t f = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     if (f >= ns) return;
     constexpr int ldab = 3 * P + 1, kuf = 2 * P;
-    double2* x = X + f * (size_t)nt;
+    // fiber f: contiguous (X[f][t]) or time-major (X[t][f], coalesced across threads)
+    double2* x0 = tmajor ? X + f : X + f * (size_t)nt;
+    const size_t xs = tmajor ? ns : 1;
+    struct XA {
+        double2* p;
+        size_t s;
+        __device__ double2& operator[](int k) const { return p[(size_t)k * s]; }
+    } x{x0, xs};
     const size_t i = fblk ? (size_t)__ldg(fblk + f) : f; // factored block of this fiber
     auto band = [&](int k, int e) -> double2 {
         return __ldg(ab + ((size_t)k * ldab + e) * nblk + i);
@@ -193,11 +201,19 @@ template <int P>
 __global__ void __launch_bounds__(128) k_fd_solve_adj(const double2* __restrict__ ab,
                                                       const unsigned char* __restrict__ piv,
                                                       double2* __restrict__ X, size_t ns, int nt,
-                                                      size_t nblk, const int* __restrict__ fblk) {
+                                                      size_t nblk, const int* __restrict__ fblk,
+                                                  int tmajor) {
     const size_t f = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     if (f >= ns) return;
     constexpr int ldab = 3 * P + 1, kuf = 2 * P;
-    double2* x = X + f * (size_t)nt;
+    // fiber f: contiguous (X[f][t]) or time-major (X[t][f], coalesced across threads)
+    double2* x0 = tmajor ? X + f : X + f * (size_t)nt;
+    const size_t xs = tmajor ? ns : 1;
+    struct XA {
+        double2* p;
+        size_t s;
+        __device__ double2& operator[](int k) const { return p[(size_t)k * s]; }
+    } x{x0, xs};
     const size_t i = fblk ? (size_t)__ldg(fblk + f) : f;
     auto band = [&](int k, int e) -> double2 {
         return __ldg(ab + ((size_t)k * ldab + e) * nblk + i);
@@ -252,15 +268,15 @@ __global__ void __launch_bounds__(128) k_fd_solve_adj(const double2* __restrict_
 }
 
 template <int P>
-void launch_solve_p(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t st) {
+void launch_solve_p(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t st, int tm) {
     const unsigned grid = (unsigned)((B.ns + 127) / 128);
     if (adjoint) {
         k_fd_solve_adj<P><<<grid, 128, 0, st>>>(B.ab.as<double2>(), B.piv.as<unsigned char>(), X,
-                                                B.ns, B.nt, B.nblk, B.fiber_block.as<int>());
+                                                B.ns, B.nt, B.nblk, B.fiber_block.as<int>(), tm);
         check_launch("k_fd_solve_adj");
     } else {
         k_fd_solve<P><<<grid, 128, 0, st>>>(B.ab.as<double2>(), B.piv.as<unsigned char>(), X,
-                                            B.ns, B.nt, B.nblk, B.fiber_block.as<int>());
+                                            B.ns, B.nt, B.nblk, B.fiber_block.as<int>(), tm);
         check_launch("k_fd_solve");
     }
 }
@@ -281,16 +297,17 @@ void launch_fd_factor(FdBlocks& B, double nu, const double* Lt, const double* Mt
     KS_REQUIRE(h == 0, KS_ESINGULAR, "factor_banded: numerically singular pivot");
 }
 
-void launch_fd_solve(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t st) {
+void launch_fd_solve(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t st, bool time_major) {
+    const int tm = time_major ? 1 : 0;
     switch (B.p) {
-    case 1: launch_solve_p<1>(B, X, adjoint, st); break;
-    case 2: launch_solve_p<2>(B, X, adjoint, st); break;
-    case 3: launch_solve_p<3>(B, X, adjoint, st); break;
-    case 4: launch_solve_p<4>(B, X, adjoint, st); break;
-    case 5: launch_solve_p<5>(B, X, adjoint, st); break;
-    case 6: launch_solve_p<6>(B, X, adjoint, st); break;
-    case 7: launch_solve_p<7>(B, X, adjoint, st); break;
-    case 8: launch_solve_p<8>(B, X, adjoint, st); break;
+    case 1: launch_solve_p<1>(B, X, adjoint, st, tm); break;
+    case 2: launch_solve_p<2>(B, X, adjoint, st, tm); break;
+    case 3: launch_solve_p<3>(B, X, adjoint, st, tm); break;
+    case 4: launch_solve_p<4>(B, X, adjoint, st, tm); break;
+    case 5: launch_solve_p<5>(B, X, adjoint, st, tm); break;
+    case 6: launch_solve_p<6>(B, X, adjoint, st, tm); break;
+    case 7: launch_solve_p<7>(B, X, adjoint, st, tm); break;
+    case 8: launch_solve_p<8>(B, X, adjoint, st, tm); break;
     default: throw Error(KS_EINVAL, "FD solve: time degree must be 1..8");
     }
 }

@@ -120,8 +120,10 @@ void launch_fill_bytes(void* p, size_t bytes, cudaStream_t s);
 //   Y[o][r][q] = sum_j A[r][j] X[o][j][q],  q over 2*s doubles
 // At is A stored k-major: At[j*n + r] = A[r][j].
 // ---------------------------------------------------------------------------
+// layout: 0 natural in/out; 1 natural in -> time-major out T[t][i];
+//         2 time-major in -> natural out (1/2 need outer == 1; nt = time extent)
 void launch_mode_gemm(const double* At, int n, const double* X, double* Y,
-                      size_t s_complex, size_t outer, cudaStream_t st);
+                      size_t s_complex, size_t outer, cudaStream_t st, int layout = 0, int nt = 0);
 
 // ---------------------------------------------------------------------------
 // banded block factor / solve (ks_fdsolve.cu)
@@ -139,7 +141,10 @@ struct FdBlocks {
 // time bands on device: Lt, Mt real (2p+1)xnt, Wsym complex
 void launch_fd_factor(FdBlocks& B, double nu, const double* Lt, const double* Mt,
                       const double2* Wsym, cudaStream_t st);
-void launch_fd_solve(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t st);
+// time_major: X is T[t][fiber] (stride ns between time steps) instead of
+// contiguous fibers X[fiber][t]
+void launch_fd_solve(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t st,
+                     bool time_major = false);
 
 // ---------------------------------------------------------------------------
 // level-pass Kronecker engine (ks_kron.cu)

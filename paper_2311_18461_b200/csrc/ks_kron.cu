@@ -47,6 +47,7 @@ struct KronPass {
     std::vector<int> out_begin; // n_out + 1
     std::vector<KronContrib> contribs;
     DevBuf d_begin, d_contribs;
+    DevBuf d_in_begin, d_entries; // v3: contributions grouped by input
     int in_pool = -1, out_pool = -1; // -1 = x / y
 };
 
@@ -61,6 +62,8 @@ struct KronPlan {
     DevBuf d_ptrs; // per pass: in pointers then out pointers (device table)
     std::vector<size_t> ptr_off;
     int nnodes = 0, nproducts = 0;
+    int bwmax = 0, nmax = 1;
+    DevBuf d_rowband, d_freal; // v3: rb[f][r][dj] (width 2*bwmax+1), is_real[f]
 };
 
 namespace {
@@ -132,127 +135,121 @@ __global__ void __launch_bounds__(256) k_kron_level(
 }
 
 // ---------------------------------------------------------------------------
-// Level pass v2: a CTA owns TQ consecutive "columns" (o, q) and the FULL axis
-// extent r = 0..n-1 of each, so every band product is local (no halo). The
-// input nodes are staged through shared memory one at a time (coalesced:
-// along q for s > 1, along r for the contiguous time axis s = 1), and every
-// output node accumulates in registers; each input element is read from HBM
-// once and each output written once per pass.
-// Thread layout: column cc = tid % TQ, rows r = tid / TQ + k * (256 / TQ).
+// Level pass v3 ("row-chunk sweep"): a thread owns one column (o, q) and a
+// chunk of kR consecutive rows r along the pass axis. For each input node it
+// loads the kR + 2*BW window once into registers, applies every factor that
+// reads this input (contributions grouped by input on the host) and adds the
+// results into the per-output accumulators through a uniform switch, so all
+// register indices are static. Threads are ordered column-fastest for s > 1
+// (coalesced along q) and chunk-fastest for the contiguous time axis s = 1.
+// Bands are pre-expanded row-major: rb[f][r][dj] = F(r, r + dj - BW).
 // ---------------------------------------------------------------------------
-constexpr int kLvThreads = 256;
+constexpr int kR = 4;
 constexpr int kMaxOut = 8;
-constexpr int kRPT = 5; // rows per thread (n <= kRPT * 256 / TQ)
 
-template <int NOUT>
-__global__ void __launch_bounds__(kLvThreads) k_kron_level2(
+struct SweepEntry {
+    int out;    // output node
+    int factor; // -1 = identity
+    double2 coeff;
+};
+
+template <int NOUT, int BW>
+__global__ void __launch_bounds__(256) k_kron_sweep(
     const double2* const* __restrict__ in_ptrs, int n_in, double2* const* __restrict__ out_ptrs,
-    const int* __restrict__ out_begin, const KronContrib* __restrict__ contribs,
-    const DevFactor* __restrict__ factors, const double2* __restrict__ bands, size_t ncols,
-    size_t s, int n, int TQ) {
-    extern __shared__ double2 tile[]; // [n][TQ + 1]
-    const int tid = threadIdx.x;
-    const int pitch = TQ + 1;
-    const int rstep = kLvThreads / TQ;
-    const int cc = tid % TQ, r0 = tid / TQ;
-    const size_t c0 = (size_t)blockIdx.x * TQ;
-    const int ncol = (int)min((size_t)TQ, ncols - c0);
-    // this thread's column -> base address
-    const size_t cme = c0 + cc;
-    const size_t o = cme / s, q = cme - o * s;
+    const int* __restrict__ in_begin, const SweepEntry* __restrict__ entries,
+    const double2* __restrict__ rb, const int* __restrict__ freal, size_t ncols, size_t s, int n,
+    int nmax) {
+    constexpr int W = kR + 2 * BW, TAPS = 2 * BW + 1;
+    const int nch = (n + kR - 1) / kR;
+    const size_t gid = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (gid >= ncols * (size_t)nch) return;
+    size_t col;
+    int ch;
+    if (s == 1) {
+        col = gid / nch;
+        ch = (int)(gid - col * nch);
+    } else {
+        ch = (int)(gid / ncols);
+        col = gid - (size_t)ch * ncols;
+    }
+    const int r0 = ch * kR;
+    const size_t o = col / s, q = col - o * s;
     const size_t base = o * (size_t)n * s + q;
-    const bool cvalid = cc < ncol;
 
-    double2 acc[NOUT][kRPT];
+    double2 acc[NOUT][kR];
 #pragma unroll
     for (int a = 0; a < NOUT; ++a)
 #pragma unroll
-        for (int k = 0; k < kRPT; ++k) acc[a][k] = make_double2(0.0, 0.0);
+        for (int k = 0; k < kR; ++k) acc[a][k] = make_double2(0.0, 0.0);
 
-    for (int j = 0; j < n_in; ++j) {
-        const double2* __restrict__ in = in_ptrs[j];
-        __syncthreads();
-        const int tot = n * TQ;
-        if (s == 1) { // contiguous fibers: consecutive threads walk r
-            for (int e = tid; e < tot; e += kLvThreads) {
-                const int c = e / n, r = e - c * n;
-                tile[r * pitch + c] = c < ncol ? __ldg(in + (c0 + c) * (size_t)n + r) : make_double2(0, 0);
-            }
-        } else {      // consecutive threads walk the contiguous q
-            for (int e = tid; e < tot; e += kLvThreads) {
-                const int r = e / TQ, c = e - r * TQ;
-                const size_t cm = c0 + c;
-                double2 v = make_double2(0, 0);
-                if (c < ncol) {
-                    const size_t oo = cm / s, qq = cm - oo * s;
-                    v = __ldg(in + oo * (size_t)n * s + (size_t)r * s + qq);
-                }
-                tile[r * pitch + c] = v;
-            }
+    for (int ii = 0; ii < n_in; ++ii) {
+        const double2* __restrict__ in = in_ptrs[ii];
+        double2 w[W];
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+            const int r = r0 - BW + k;
+            w[k] = (r >= 0 && r < n) ? __ldg(in + base + (size_t)r * s) : make_double2(0.0, 0.0);
         }
-        __syncthreads();
+        const int eb = in_begin[ii], ee = in_begin[ii + 1];
+        for (int e = eb; e < ee; ++e) {
+            const SweepEntry en = entries[e];
+            double2 v[kR];
+            if (en.factor < 0) {
 #pragma unroll
-        for (int oi = 0; oi < NOUT; ++oi) {
-            const int cb = out_begin[oi], ce = out_begin[oi + 1];
-            for (int ci = cb; ci < ce; ++ci) {
-                const KronContrib c = contribs[ci];
-                if (c.in != j) continue;
+                for (int k = 0; k < kR; ++k) v[k] = w[k + BW];
+            } else {
+                const double2* band = rb + (size_t)en.factor * nmax * TAPS;
+                if (freal[en.factor]) {
 #pragma unroll
-                for (int k = 0; k < kRPT; ++k) {
-                    const int r = r0 + k * rstep;
-                    if (r >= n) break;
-                    double vr, vi;
-                    if (c.factor < 0) {
-                        const double2 v = tile[r * pitch + cc];
-                        vr = v.x;
-                        vi = v.y;
-                    } else {
-                        const DevFactor f = factors[c.factor];
-                        const int bw = f.bw, ld = 2 * bw + 1;
-                        const int j0 = r - bw < 0 ? 0 : r - bw;
-                        const int j1 = r + bw > n - 1 ? n - 1 : r + bw;
-                        const double2* band = bands + f.off;
-                        vr = 0.0;
-                        vi = 0.0;
-                        if (f.is_real) {
-                            for (int jj = j0; jj <= j1; ++jj) {
-                                const double a = __ldg(&band[bw + r - jj + jj * ld].x);
-                                const double2 v = tile[jj * pitch + cc];
-                                vr = fma(a, v.x, vr);
-                                vi = fma(a, v.y, vi);
-                            }
-                        } else {
-                            for (int jj = j0; jj <= j1; ++jj) {
-                                const double2 a = __ldg(&band[bw + r - jj + jj * ld]);
-                                const double2 v = tile[jj * pitch + cc];
-                                vr = fma(a.x, v.x, fma(-a.y, v.y, vr));
-                                vi = fma(a.x, v.y, fma(a.y, v.x, vi));
-                            }
+                    for (int k = 0; k < kR; ++k) {
+                        const int r = min(r0 + k, n - 1);
+                        double vr = 0.0, vi = 0.0;
+#pragma unroll
+                        for (int t = 0; t < TAPS; ++t) {
+                            const double a = __ldg(&band[(size_t)r * TAPS + t].x);
+                            vr = fma(a, w[k + t].x, vr);
+                            vi = fma(a, w[k + t].y, vi);
                         }
+                        v[k] = make_double2(vr, vi);
                     }
-                    double2& A = acc[oi][k];
-                    if (c.coeff.y == 0.0) {
-                        A.x = fma(c.coeff.x, vr, A.x);
-                        A.y = fma(c.coeff.x, vi, A.y);
-                    } else {
-                        A.x = fma(c.coeff.x, vr, fma(-c.coeff.y, vi, A.x));
-                        A.y = fma(c.coeff.x, vi, fma(c.coeff.y, vr, A.y));
+                } else {
+#pragma unroll
+                    for (int k = 0; k < kR; ++k) {
+                        const int r = min(r0 + k, n - 1);
+                        double vr = 0.0, vi = 0.0;
+#pragma unroll
+                        for (int t = 0; t < TAPS; ++t) {
+                            const double2 a = __ldg(&band[(size_t)r * TAPS + t]);
+                            vr = fma(a.x, w[k + t].x, fma(-a.y, w[k + t].y, vr));
+                            vi = fma(a.x, w[k + t].y, fma(a.y, w[k + t].x, vi));
+                        }
+                        v[k] = make_double2(vr, vi);
                     }
                 }
+            }
+            const double cr = en.coeff.x, ci = en.coeff.y;
+            switch (en.out) {
+#define KS_ACC(OO)                                                                 \
+    case OO:                                                                       \
+        if (OO < NOUT) {                                                           \
+            _Pragma("unroll") for (int k = 0; k < kR; ++k) {                       \
+                double2& A = acc[OO < NOUT ? OO : 0][k];                           \
+                A.x = fma(cr, v[k].x, fma(-ci, v[k].y, A.x));                      \
+                A.y = fma(cr, v[k].y, fma(ci, v[k].x, A.y));                       \
+            }                                                                      \
+        }                                                                          \
+        break;
+                KS_ACC(0) KS_ACC(1) KS_ACC(2) KS_ACC(3) KS_ACC(4) KS_ACC(5) KS_ACC(6) KS_ACC(7)
+#undef KS_ACC
             }
         }
     }
-    // write outputs (thread-per-(r, column): coalesced along q for s > 1)
-    if (!cvalid) return;
 #pragma unroll
-    for (int oi = 0; oi < NOUT; ++oi) {
-        double2* __restrict__ out = out_ptrs[oi];
+    for (int a = 0; a < NOUT; ++a) {
+        double2* __restrict__ out = out_ptrs[a];
 #pragma unroll
-        for (int k = 0; k < kRPT; ++k) {
-            const int r = r0 + k * rstep;
-            if (r >= n) break;
-            out[base + (size_t)r * s] = acc[oi][k];
-        }
+        for (int k = 0; k < kR; ++k)
+            if (r0 + k < n) out[base + (size_t)(r0 + k) * s] = acc[a][k];
     }
 }
 
@@ -401,6 +398,59 @@ KronPlan* kron_plan(const std::vector<int>& dims,
         }
         P->passes.push_back(std::move(ps));
     }
+    // v3 tables: row-major bands padded to the widest bandwidth
+    for (auto& f : P->factors) P->bwmax = std::max(P->bwmax, f.bw);
+    {
+        const int taps = 2 * P->bwmax + 1;
+        size_t tot = 0;
+        std::vector<size_t> foff;
+        for (auto& f : P->factors) {
+            foff.push_back(tot);
+            tot += (size_t)f.n * taps;
+        }
+        // all factors of one axis share n, but pool offsets are per factor: store
+        // each factor at f * nmax * taps so the kernel indexes by factor id
+        int nmax = 1;
+        for (auto& f : P->factors) nmax = std::max(nmax, f.n);
+        std::vector<double2> rb((size_t)std::max<size_t>(P->factors.size(), 1) * nmax * taps,
+                                make_double2(0, 0));
+        std::vector<int> freal(std::max<size_t>(P->factors.size(), 1), 1);
+        for (size_t fi = 0; fi < P->factors.size(); ++fi) {
+            const KronFactor& f = P->factors[fi];
+            freal[fi] = f.is_real ? 1 : 0;
+            for (int r = 0; r < f.n; ++r)
+                for (int dj = -f.bw; dj <= f.bw; ++dj) {
+                    const int j = r + dj;
+                    if (j < 0 || j >= f.n) continue;
+                    rb[(fi * nmax + r) * taps + (dj + P->bwmax)] =
+                        pool[f.off + (size_t)(f.bw + r - j) + (size_t)j * (2 * f.bw + 1)];
+                }
+        }
+        P->nmax = nmax;
+        P->d_rowband.alloc(rb.size() * sizeof(double2));
+        KS_CUDA(cudaMemcpy(P->d_rowband.p, rb.data(), rb.size() * sizeof(double2), cudaMemcpyHostToDevice));
+        P->d_freal.alloc(freal.size() * sizeof(int));
+        KS_CUDA(cudaMemcpy(P->d_freal.p, freal.data(), freal.size() * sizeof(int), cudaMemcpyHostToDevice));
+    }
+    for (auto& ps : P->passes) {
+        std::vector<int> ib(ps.n_in + 1, 0);
+        for (auto& c : ps.contribs) ib[c.in + 1]++;
+        for (int i = 0; i < ps.n_in; ++i) ib[i + 1] += ib[i];
+        std::vector<SweepEntry> ent(ps.contribs.size());
+        std::vector<int> fill(ib.begin(), ib.end() - 1);
+        for (int o = 0; o < ps.n_out; ++o)
+            for (int ci = ps.out_begin[o]; ci < ps.out_begin[o + 1]; ++ci) {
+                const KronContrib& c = ps.contribs[ci];
+                ent[fill[c.in]++] = SweepEntry{o, c.factor, c.coeff};
+            }
+        ps.d_in_begin.alloc(ib.size() * sizeof(int));
+        KS_CUDA(cudaMemcpy(ps.d_in_begin.p, ib.data(), ib.size() * sizeof(int), cudaMemcpyHostToDevice));
+        if (!ent.empty()) {
+            ps.d_entries.alloc(ent.size() * sizeof(SweepEntry));
+            KS_CUDA(cudaMemcpy(ps.d_entries.p, ent.data(), ent.size() * sizeof(SweepEntry),
+                               cudaMemcpyHostToDevice));
+        }
+    }
     for (int pl = 0; pl < 2; ++pl)
         if (P->pool_nodes[pl] > 0) P->pool[pl].alloc((size_t)P->pool_nodes[pl] * P->N * sizeof(double2));
     // pointer tables: filled per apply (x / y change); reserve device space
@@ -443,28 +493,33 @@ void kron_apply(KronPlan& P, const double2* x, double2* y, cudaStream_t st,
         size_t s = 1;
         for (int a = 0; a < ps.axis; ++a) s *= (size_t)P.dims[a];
         const int n = P.dims[ps.axis];
-        // v2 (smem-tiled) when the level fits its register budget
-        int TQ = 16;
-        while (TQ > 1 && (n + kLvThreads / TQ - 1) / (kLvThreads / TQ) > kRPT) TQ /= 2;
-        const bool v2 = ps.n_out <= kMaxOut && (n + kLvThreads / TQ - 1) / (kLvThreads / TQ) <= kRPT;
-        if (v2) {
+        // v3 sweep when the level fits its register budget (NOUT <= 8, bw <= 4)
+        if (ps.n_out <= kMaxOut && P.bwmax >= 1 && P.bwmax <= 4) {
             const size_t ncols = P.N / (size_t)n;
-            const size_t sm = (size_t)n * (TQ + 1) * sizeof(double2);
-            const unsigned g2 = (unsigned)((ncols + TQ - 1) / TQ);
+            const size_t nth = ncols * (size_t)((n + kR - 1) / kR);
+            const unsigned g3 = (unsigned)((nth + 255) / 256);
             auto ip = reinterpret_cast<const double2* const*>(dp + P.ptr_off[k]);
             auto op = reinterpret_cast<double2* const*>(const_cast<void**>(dp + P.ptr_off[k] + ps.n_in));
-#define KS_LV2(NO)                                                                              \
-    case NO:                                                                                    \
-        k_kron_level2<NO><<<g2, kLvThreads, sm, st>>>(ip, ps.n_in, op, ps.d_begin.as<int>(),    \
-                                                      ps.d_contribs.as<KronContrib>(),         \
-                                                      P.d_factors.as<DevFactor>(),             \
-                                                      P.d_bands.as<double2>(), ncols, s, n, TQ); \
+#define KS_SW(NO, BWV)                                                                         \
+    k_kron_sweep<NO, BWV><<<g3, 256, 0, st>>>(ip, ps.n_in, op, ps.d_in_begin.as<int>(),        \
+                                               ps.d_entries.as<SweepEntry>(),                  \
+                                               P.d_rowband.as<double2>(), P.d_freal.as<int>(), \
+                                               ncols, s, n, P.nmax)
+#define KS_SWB(NO)                                                                             \
+    case NO:                                                                                   \
+        switch (P.bwmax) {                                                                     \
+        case 1: KS_SW(NO, 1); break;                                                           \
+        case 2: KS_SW(NO, 2); break;                                                           \
+        case 3: KS_SW(NO, 3); break;                                                           \
+        default: KS_SW(NO, 4); break;                                                          \
+        }                                                                                      \
         break;
             switch (ps.n_out) {
-                KS_LV2(1) KS_LV2(2) KS_LV2(3) KS_LV2(4) KS_LV2(5) KS_LV2(6) KS_LV2(7) KS_LV2(8)
+                KS_SWB(1) KS_SWB(2) KS_SWB(3) KS_SWB(4) KS_SWB(5) KS_SWB(6) KS_SWB(7) KS_SWB(8)
             }
-#undef KS_LV2
-            check_launch("k_kron_level2");
+#undef KS_SWB
+#undef KS_SW
+            check_launch("k_kron_sweep");
             continue;
         }
         const unsigned grid = (unsigned)((P.N + 255) / 256);

@@ -309,49 +309,100 @@ template <int N> __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// Column maps: the GEMM's N dimension is a set of complex columns q (re/im =
+// 2 adjacent doubles). MAP_STD walks the natural layout X[o][j][q']. For the
+// outermost axis (outer = 1) the FD apply can instead hand the block solves a
+// time-major layout T[t][i] (i = spatial index, axis 1 fastest): MAP_TOUT
+// reads natural and writes time-major, MAP_TIN the reverse. Their column
+// tiles are tbt (time) x tbr (lower spatial index) blocks of 64 columns, so
+// both the natural side (consecutive t) and the time-major side (consecutive
+// i) move 64-128 B segments.
+enum { MAP_STD = 0, MAP_TOUT = 1, MAP_TIN = 2 };
+struct ColMap {
+    int mode;
+    int nt;            // time extent (T modes)
+    int tbt, tbr;      // tile blocking (T modes), tbt * tbr = 64
+    long long Q;       // complex columns
+    long long s;       // complex stride of the axis in the natural layout
+    long long Np;      // product of the spatial dims before the axis (T modes)
+    long long Ns;      // spatial size (T modes)
+    long long ntb;     // number of time blocks (T modes)
+    long long ntiles;
+};
+
+// offsets (doubles) and row strides of complex column j of tile tile
+__device__ __forceinline__ bool colmap(const ColMap& M, int n, long long tile, int j,
+                                       long long& in_off, long long& out_off) {
+    if (M.mode == MAP_STD) {
+        const long long q = tile * 64 + j;
+        if (q >= M.Q) return false;
+        const long long o = q / M.s, qq = q - o * M.s;
+        in_off = out_off = 2 * (o * (long long)n * M.s + qq);
+        return true;
+    }
+    const long long tb = tile % M.ntb, rb = tile / M.ntb;
+    // in-tile order: the time-major side's contiguous index fastest on the
+    // store side (TOUT: spatial i fastest) / load side (TIN: t fastest); with
+    // the m8n8k4 C fragment (4 consecutive columns per lane quad) both sides
+    // then move >= 64 B contiguous segments
+    const int jt = M.mode == MAP_TOUT ? j / M.tbr : j % M.tbt;
+    const int jr = M.mode == MAP_TOUT ? j % M.tbr : j / M.tbt;
+    const long long t = tb * M.tbt + jt, rest = rb * M.tbr + jr;
+    if (t >= M.nt || rest >= M.Np) return false;
+    const long long nat = 2 * (t + (long long)M.nt * rest);
+    const long long tm = 2 * (t * M.Ns + rest);
+    in_off = M.mode == MAP_TOUT ? nat : tm;
+    out_off = M.mode == MAP_TOUT ? tm : nat;
+    return true;
+}
+
 template <int TM>
 __global__ void __launch_bounds__(kThreads, (TM <= 5 ? 2 : 1))
 k_mode_gemm_dmma2(const double* __restrict__ At, int n, const double* __restrict__ X,
-                  double* __restrict__ Y, long long W2, long long C, int ntiles) {
+                  double* __restrict__ Y, ColMap M) {
     constexpr int BM = 16 * TM;
     constexpr int MT = TM;
     constexpr int BMP = BM + 4; // == 4 (mod 16): conflict-free fragment loads
     constexpr int BNP = kBN + 4;
     extern __shared__ __align__(16) double smem[];
     const int nk = (n + kBK - 1) / kBK;
-    double* As = smem;                      // [nk*kBK][BMP]
+    double* As = smem;                          // [nk*kBK][BMP]
     double* Bs = smem + (size_t)nk * kBK * BMP; // [kStages][kBK][BNP]
+    const long long in_rs = M.mode == MAP_TIN ? 2 * M.Np : 2 * M.s;
+    const long long out_rs = M.mode == MAP_TOUT ? 2 * M.Np : 2 * M.s;
+    const long long ntiles = M.ntiles;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wr = warp & 1, wc = warp >> 1;
 
-    // A once: As[j][r] = At[j*n + r] (zero padded)
     for (int e = tid; e < nk * kBK * BM; e += kThreads) {
         const int j = e / BM, r = e - j * BM;
         As[j * BMP + r] = (j < n && r < n) ? __ldg(At + (long long)j * n + r) : 0.0;
     }
 
     const int lcp = tid & 63, lrow0 = tid >> 6;
-    const int my_tiles = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-    const int nwork = my_tiles * nk;
+    const long long my_tiles =
+        ntiles > (long long)blockIdx.x ? (ntiles - 1 - (long long)blockIdx.x) / gridDim.x + 1 : 0;
+    const long long nwork = my_tiles * nk;
+    long long cur_tile = -1, cur_in = 0;
+    bool cur_valid = false;
 
-    auto issue = [&](int w) {
+    auto issue = [&](long long w) {
         if (w < nwork) {
-            const int t = (int)blockIdx.x + (w / nk) * (int)gridDim.x;
-            const int kc = w - (w / nk) * nk;
-            const long long c = (long long)t * kBN + 2 * lcp;
-            const bool cv = c < C;
-            long long off = 0;
-            if (cv) {
-                const long long o = c / W2, q = c - o * W2;
-                off = o * (long long)n * W2 + q;
+            const long long tile = (long long)blockIdx.x + (w / nk) * gridDim.x;
+            const int kc = (int)(w - (w / nk) * nk);
+            if (tile != cur_tile) {
+                long long dummy;
+                cur_valid = colmap(M, n, tile, lcp, cur_in, dummy);
+                cur_tile = tile;
             }
             double* bs = Bs + (size_t)(w % kStages) * kBK * BNP;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int jj = lrow0 + 4 * k, j = kc * kBK + jj;
-                const bool v = cv && j < n;
-                cp_async16(bs + jj * BNP + 2 * lcp, v ? (const void*)(X + off + (long long)j * W2) : (const void*)X, v);
+                const bool v = cur_valid && j < n;
+                cp_async16(bs + jj * BNP + 2 * lcp,
+                           v ? (const void*)(X + cur_in + (long long)j * in_rs) : (const void*)X, v);
             }
         }
         cp_async_commit();
@@ -368,12 +419,12 @@ k_mode_gemm_dmma2(const double* __restrict__ At, int n, const double* __restrict
 
     const int r_warp = wr * (BM / 2), c_warp = wc * 32;
     const int ar = lane >> 2, ak = lane & 3;
-    const int cr = lane >> 2, cc = 2 * (lane & 3);
-    for (int w = 0; w < nwork; ++w) {
+    const int cr = lane >> 2;
+    for (long long w = 0; w < nwork; ++w) {
         cp_async_wait<kStages - 2>();
         __syncthreads();
         issue(w + kStages - 1);
-        const int kc = w % nk;
+        const int kc = (int)(w % nk);
         const double* bs = Bs + (size_t)(w % kStages) * kBK * BNP;
         const double* as = As + (size_t)kc * kBK * BMP;
 #pragma unroll
@@ -389,18 +440,18 @@ k_mode_gemm_dmma2(const double* __restrict__ At, int n, const double* __restrict
                 for (int m = 0; m < 4; ++m) dmma_m8n8k4(acc[i][m][0], acc[i][m][1], a[i], b[m]);
         }
         if (kc == nk - 1) {
-            const int t = (int)blockIdx.x + (w / nk) * (int)gridDim.x;
+            const long long tile = (long long)blockIdx.x + (w / nk) * gridDim.x;
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
-                const long long c = (long long)t * kBN + c_warp + m * 8 + cc;
-                if (c < C) {
-                    const long long o = c / W2, q = c - o * W2;
-                    double* yb = Y + o * (long long)n * W2 + q;
+                const int jcol = (c_warp >> 1) + m * 4 + (lane & 3); // complex column in tile
+                long long io, oo;
+                if (colmap(M, n, tile, jcol, io, oo)) {
+                    double* yb = Y + oo;
 #pragma unroll
                     for (int i = 0; i < MT; ++i) {
                         const int r = r_warp + i * 8 + cr;
                         if (r < n)
-                            *reinterpret_cast<double2*>(yb + (long long)r * W2) =
+                            *reinterpret_cast<double2*>(yb + (long long)r * out_rs) =
                                 make_double2(acc[i][m][0], acc[i][m][1]);
                     }
                 }
@@ -424,7 +475,7 @@ int engine_choice() {
 
 template <int TM>
 void launch_tm(int engine, const double* At, int n, const double* X, double* Y, long long W2,
-               long long C, cudaStream_t st) {
+               long long C, cudaStream_t st, const ColMap* map) {
     const unsigned grid = (unsigned)((C + kBN - 1) / kBN);
     if (engine == 0) {
         const size_t sm = (size_t)2 * kBK * (16 * TM + 2 + kBN) * sizeof(double);
@@ -450,9 +501,9 @@ void launch_tm(int engine, const double* At, int n, const double* X, double* Y, 
         }
         KS_REQUIRE(sm <= 227 * 1024, KS_EINVAL, "mode product: axis too long for the resident-A kernel");
         const int per_sm = (TM <= 5 && 2 * sm <= 227 * 1024) ? 2 : 1;
-        const int ntiles = (int)grid;
-        const unsigned g2 = (unsigned)std::min<long long>(ntiles, (long long)sms * per_sm);
-        k_mode_gemm_dmma2<TM><<<g2, kThreads, sm, st>>>(At, n, X, Y, W2, C, ntiles);
+        ColMap M = *map;
+        const unsigned g2 = (unsigned)std::min<long long>(M.ntiles, (long long)sms * per_sm);
+        k_mode_gemm_dmma2<TM><<<g2, kThreads, sm, st>>>(At, n, X, Y, M);
         check_launch("k_mode_gemm_dmma2");
     } else {
         const size_t sm = (size_t)2 * kBK * (16 * TM + 4 + kBN + 4) * sizeof(double);
@@ -472,25 +523,44 @@ void launch_tm(int engine, const double* At, int n, const double* X, double* Y, 
 int transform_engine() { return engine_choice(); }
 
 void launch_mode_gemm(const double* At, int n, const double* X, double* Y, size_t s_complex,
-                      size_t outer, cudaStream_t st) {
+                      size_t outer, cudaStream_t st, int layout, int nt) {
     const long long W2 = 2 * (long long)s_complex;
     const long long C = W2 * (long long)outer;
     if (C == 0 || n == 0) return;
-    const int eng = engine_choice();
-    // rows per CTA: 16*TM >= n
+    int eng = engine_choice();
+    if (layout != MAP_STD) {
+        KS_REQUIRE(outer == 1 && nt > 0 && s_complex % (size_t)nt == 0, KS_EINVAL,
+                   "time-major transform needs the outermost axis");
+        eng = 2; // only the v2 engine implements the time-major maps
+    }
+    ColMap M{};
+    M.mode = layout;
+    M.s = (long long)s_complex;
+    M.Q = (long long)s_complex * (long long)outer;
+    if (layout == MAP_STD) {
+        M.ntiles = (M.Q + 63) / 64;
+    } else {
+        M.nt = nt;
+        M.Np = (long long)s_complex / nt;
+        M.Ns = M.Np * n;
+        M.tbr = M.Np >= 8 ? 8 : (M.Np >= 4 ? 4 : (M.Np >= 2 ? 2 : 1));
+        M.tbt = 64 / M.tbr;
+        M.ntb = (nt + M.tbt - 1) / M.tbt;
+        M.ntiles = M.ntb * ((M.Np + M.tbr - 1) / M.tbr);
+    }
     const int tm = (n + 15) / 16;
     KS_REQUIRE(tm <= 10, KS_EINVAL, "mode product: axis length > 160 not supported");
     switch (tm) {
-    case 1: launch_tm<1>(eng, At, n, X, Y, W2, C, st); break;
-    case 2: launch_tm<2>(eng, At, n, X, Y, W2, C, st); break;
-    case 3: launch_tm<3>(eng, At, n, X, Y, W2, C, st); break;
-    case 4: launch_tm<4>(eng, At, n, X, Y, W2, C, st); break;
-    case 5: launch_tm<5>(eng, At, n, X, Y, W2, C, st); break;
-    case 6: launch_tm<6>(eng, At, n, X, Y, W2, C, st); break;
-    case 7: launch_tm<7>(eng, At, n, X, Y, W2, C, st); break;
-    case 8: launch_tm<8>(eng, At, n, X, Y, W2, C, st); break;
-    case 9: launch_tm<9>(eng, At, n, X, Y, W2, C, st); break;
-    case 10: launch_tm<10>(eng, At, n, X, Y, W2, C, st); break;
+    case 1: launch_tm<1>(eng, At, n, X, Y, W2, C, st, &M); break;
+    case 2: launch_tm<2>(eng, At, n, X, Y, W2, C, st, &M); break;
+    case 3: launch_tm<3>(eng, At, n, X, Y, W2, C, st, &M); break;
+    case 4: launch_tm<4>(eng, At, n, X, Y, W2, C, st, &M); break;
+    case 5: launch_tm<5>(eng, At, n, X, Y, W2, C, st, &M); break;
+    case 6: launch_tm<6>(eng, At, n, X, Y, W2, C, st, &M); break;
+    case 7: launch_tm<7>(eng, At, n, X, Y, W2, C, st, &M); break;
+    case 8: launch_tm<8>(eng, At, n, X, Y, W2, C, st, &M); break;
+    case 9: launch_tm<9>(eng, At, n, X, Y, W2, C, st, &M); break;
+    case 10: launch_tm<10>(eng, At, n, X, Y, W2, C, st, &M); break;
     }
 }
 
