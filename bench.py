@@ -232,6 +232,7 @@ def main():
     z = ks.DeviceVector(n)
     y = ks.DeviceVector(n)
     dfma, dmma = ks.fp64_peaks()
+    mixed = ks.fp64_peak_mixed()
     fp64_peak = max(dfma, dmma)
 
     # ---- device-resident FD apply (the headline) ----
@@ -328,6 +329,7 @@ def main():
                          "kernel": "k_mode_gemm (spatial transform)",
                          "peak_source": "measured live: DFMA %.2f / DMMA %.2f TFLOP/s microbenchmarks"
                                         % (dfma, dmma),
+                         "mixed_dfma_dmma_tflops": mixed,
                          "gemm_ms_per_apply": ms_gemm},
             "fd_apply": {"ms": ms_fd, "roofline_ms": fd_roof_s * 1e3,
                          "frac_of_roofline": fd_roof_s * 1e3 / ms_fd,

@@ -191,6 +191,8 @@ int ks_kron_time(ks_kron* k, const ks_c64* x, ks_c64* y, int iters, int flush,
 int ks_fp64_peak(double* tflops);
 /* Both FP64 peaks: CUDA-core DFMA and tensor-core DMMA (mma.sync m8n8k4 f64). */
 int ks_fp64_peaks(double* dfma_tflops, double* dmma_tflops);
+/* Combined FP64 throughput with half the warps on DMMA and half on DFMA. */
+int ks_fp64_peak_mixed(double* tflops);
 /* Which engine the spatial transforms use: 0 = DFMA, 1 = DMMA (env KS_GEMM). */
 int ks_transform_engine(void);
 /* Number of kernels the library launched since the last reset. */

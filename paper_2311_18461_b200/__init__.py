@@ -122,6 +122,7 @@ _SIGS = {
     "ks_kron_time": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "ks_fp64_peak": (C.c_int, [C.POINTER(C.c_double)]),
     "ks_fp64_peaks": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "ks_fp64_peak_mixed": (C.c_int, [C.POINTER(C.c_double)]),
     "ks_transform_engine": (C.c_int, []),
     "ks_launch_count": (C.c_uint64, []),
     "ks_launch_count_reset": (None, []),
@@ -566,6 +567,12 @@ def fp64_peaks():
     a, b = C.c_double(), C.c_double()
     _check(lib().ks_fp64_peaks(C.byref(a), C.byref(b)))
     return a.value, b.value
+
+
+def fp64_peak_mixed():
+    a = C.c_double()
+    _check(lib().ks_fp64_peak_mixed(C.byref(a)))
+    return a.value
 
 
 def launch_count() -> int:

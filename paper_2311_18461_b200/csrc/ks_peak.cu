@@ -43,7 +43,71 @@ __global__ void __launch_bounds__(256) k_dmma_peak(double* out, double seed) {
     if (s == 12345.678) out[threadIdx.x] = s;
 }
 
+// warps 0-3 issue DMMA, warps 4-7 DFMA: does the FP64 tensor path run
+// concurrently with the CUDA-core FP64 pipe?
+__global__ void __launch_bounds__(256) k_mixed_peak(double* out, double seed) {
+    const int warp = threadIdx.x >> 5;
+    double s = 0;
+    if (warp < 4) {
+        double c[8][2];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = seed + i;
+        const double a = 0.999 + threadIdx.x * 1e-9, b = 1e-3;
+        for (int it = 0; it < kIters / 4; ++it) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                             : "+d"(c[i][0]), "+d"(c[i][1])
+                             : "d"(a), "d"(b));
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+    } else {
+        double a[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = seed + threadIdx.x * 1e-9 + i;
+        const double b = 0.999999, cc = 1e-7;
+        for (int it = 0; it < kIters; ++it) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] = fma(a[i], b, cc);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s += a[i];
+    }
+    if (s == 12345.678) out[threadIdx.x] = s;
+}
+
 } // namespace
+
+// flops of one mixed launch: 4 DMMA warps + 4 DFMA warps per block
+static double mixed_flops(unsigned grid) {
+    return (double)grid * 4 * (kIters / 4) * 8 * 512.0 + (double)grid * 128 * kIters * 8 * 2.0;
+}
+
+static void run_mixed(double* tflops) {
+    int sms = 148, dev = 0;
+    KS_CUDA(cudaGetDevice(&dev));
+    KS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    DevBuf out(256 * sizeof(double));
+    const unsigned grid = sms * 8;
+    cudaEvent_t a, b;
+    KS_CUDA(cudaEventCreate(&a));
+    KS_CUDA(cudaEventCreate(&b));
+    float best = 1e30f;
+    for (int rep = 0; rep < 6; ++rep) {
+        KS_CUDA(cudaEventRecord(a));
+        k_mixed_peak<<<grid, 256>>>(out.as<double>(), 1.0);
+        check_launch("k_mixed_peak");
+        KS_CUDA(cudaEventRecord(b));
+        KS_CUDA(cudaEventSynchronize(b));
+        float ms = 0;
+        KS_CUDA(cudaEventElapsedTime(&ms, a, b));
+        if (rep > 0 && ms < best) best = ms;
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *tflops = mixed_flops(grid) / (best * 1e-3) / 1e12;
+}
 
 static void run_peak(bool mma, double* tflops) {
     int sms = 148;
@@ -77,9 +141,20 @@ static void run_peak(bool mma, double* tflops) {
 }
 
 void fp64_peak_bench(double* tflops) { run_peak(false, tflops); }
+void fp64_peak_bench_mixed(double* tflops) { run_mixed(tflops); }
 void fp64_peak_bench_mma(double* tflops) { run_peak(true, tflops); }
 
 } // namespace ks
+
+extern "C" int ks_fp64_peak_mixed(double* tflops) {
+    try {
+        ks::fp64_peak_bench_mixed(tflops);
+    } catch (const ks::Error& e) {
+        ks::set_last_error(e.what());
+        return e.code;
+    }
+    return KS_OK;
+}
 
 extern "C" int ks_fp64_peaks(double* dfma, double* dmma) {
     try {

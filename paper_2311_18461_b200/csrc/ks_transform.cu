@@ -331,16 +331,38 @@ struct ColMap {
 };
 
 // offsets (doubles) and row strides of complex column j of tile tile
-__device__ __forceinline__ bool colmap(const ColMap& M, int n, long long tile, int j,
+// per-tile state: one division per tile, none per column
+struct TileBase {
+    long long q0, o0, r0; // STD: first column, its slab o0 and offset r0 = q0 - o0*s
+    long long tb, rb;     // T modes
+};
+__device__ __forceinline__ TileBase tile_base(const ColMap& M, long long tile) {
+    TileBase b;
+    if (M.mode == MAP_STD) {
+        b.q0 = tile * 64;
+        b.o0 = b.q0 / M.s;
+        b.r0 = b.q0 - b.o0 * M.s;
+        b.tb = b.rb = 0;
+    } else {
+        b.rb = tile / M.ntb;
+        b.tb = tile - b.rb * M.ntb;
+        b.q0 = b.o0 = b.r0 = 0;
+    }
+    return b;
+}
+__device__ __forceinline__ bool colmap(const ColMap& M, int n, const TileBase& B, int j,
                                        long long& in_off, long long& out_off) {
     if (M.mode == MAP_STD) {
-        const long long q = tile * 64 + j;
-        if (q >= M.Q) return false;
-        const long long o = q / M.s, qq = q - o * M.s;
+        if (B.q0 + j >= M.Q) return false;
+        long long o = B.o0, qq = B.r0 + j;
+        while (qq >= M.s) { // s >= 1; a 64-column tile crosses at most ceil(64/s) slabs
+            qq -= M.s;
+            ++o;
+        }
         in_off = out_off = 2 * (o * (long long)n * M.s + qq);
         return true;
     }
-    const long long tb = tile % M.ntb, rb = tile / M.ntb;
+    const long long tb = B.tb, rb = B.rb;
     // in-tile order: the time-major side's contiguous index fastest on the
     // store side (TOUT: spatial i fastest) / load side (TIN: t fastest); with
     // the m8n8k4 C fragment (4 consecutive columns per lane quad) both sides
@@ -381,19 +403,20 @@ k_mode_gemm_dmma2(const double* __restrict__ At, int n, const double* __restrict
     }
 
     const int lcp = tid & 63, lrow0 = tid >> 6;
-    const long long my_tiles =
-        ntiles > (long long)blockIdx.x ? (ntiles - 1 - (long long)blockIdx.x) / gridDim.x + 1 : 0;
-    const long long nwork = my_tiles * nk;
+    const int my_tiles =
+        ntiles > (long long)blockIdx.x ? (int)((ntiles - 1 - (long long)blockIdx.x) / gridDim.x + 1) : 0;
+    const int nwork = my_tiles * nk;
     long long cur_tile = -1, cur_in = 0;
     bool cur_valid = false;
 
-    auto issue = [&](long long w) {
+    auto issue = [&](int w) {
         if (w < nwork) {
-            const long long tile = (long long)blockIdx.x + (w / nk) * gridDim.x;
-            const int kc = (int)(w - (w / nk) * nk);
+            const int wt = w / nk;
+            const long long tile = (long long)blockIdx.x + (long long)wt * gridDim.x;
+            const int kc = w - wt * nk;
             if (tile != cur_tile) {
                 long long dummy;
-                cur_valid = colmap(M, n, tile, lcp, cur_in, dummy);
+                cur_valid = colmap(M, n, tile_base(M, tile), lcp, cur_in, dummy);
                 cur_tile = tile;
             }
             double* bs = Bs + (size_t)(w % kStages) * kBK * BNP;
@@ -420,11 +443,11 @@ k_mode_gemm_dmma2(const double* __restrict__ At, int n, const double* __restrict
     const int r_warp = wr * (BM / 2), c_warp = wc * 32;
     const int ar = lane >> 2, ak = lane & 3;
     const int cr = lane >> 2;
-    for (long long w = 0; w < nwork; ++w) {
+    for (int w = 0; w < nwork; ++w) {
         cp_async_wait<kStages - 2>();
         __syncthreads();
         issue(w + kStages - 1);
-        const int kc = (int)(w % nk);
+        const int kc = w % nk;
         const double* bs = Bs + (size_t)(w % kStages) * kBK * BNP;
         const double* as = As + (size_t)kc * kBK * BMP;
 #pragma unroll
@@ -440,12 +463,13 @@ k_mode_gemm_dmma2(const double* __restrict__ At, int n, const double* __restrict
                 for (int m = 0; m < 4; ++m) dmma_m8n8k4(acc[i][m][0], acc[i][m][1], a[i], b[m]);
         }
         if (kc == nk - 1) {
-            const long long tile = (long long)blockIdx.x + (w / nk) * gridDim.x;
+            const long long tile = (long long)blockIdx.x + (long long)(w / nk) * gridDim.x;
+            const TileBase tbase = tile_base(M, tile);
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
                 const int jcol = (c_warp >> 1) + m * 4 + (lane & 3); // complex column in tile
                 long long io, oo;
-                if (colmap(M, n, tile, jcol, io, oo)) {
+                if (colmap(M, n, tbase, jcol, io, oo)) {
                     double* yb = Y + oo;
 #pragma unroll
                     for (int i = 0; i < MT; ++i) {
