@@ -159,84 +159,40 @@ __global__ void __launch_bounds__(128) k_fd_solve(const double2* __restrict__ ab
     auto band = [&](int k, int e) -> double2 {
         return __ldg(ab + ((size_t)k * ldab + e) * nblk + i);
     };
-    // Loads for step k are issued kD steps ahead into register rings (static
-    // slot c = k mod kD after unrolling by kD), so the factor / window loads
-    // overlap the dependent elimination chain.
-    constexpr int kD = 4;
-    const double2 Z = make_double2(0.0, 0.0);
     // forward: L with row interchanges (eigensolve.cpp:127-133); w[m] = x[k+m]
     double2 w[P + 1];
 #pragma unroll
-    for (int m = 0; m <= P; ++m) w[m] = m < nt ? x[m] : Z;
-    double2 LR[kD][P];
-    double2 XR[kD];
-    int PR[kD];
+    for (int m = 0; m <= P; ++m) w[m] = m < nt ? x[m] : make_double2(0.0, 0.0);
+    for (int k = 0; k < nt; ++k) {
+        const int po = piv[(size_t)k * nblk + i];
 #pragma unroll
-    for (int c = 0; c < kD; ++c) {
-        const int k = c;
-        PR[c] = k < nt ? piv[(size_t)k * nblk + i] : 0;
-#pragma unroll
-        for (int m = 1; m <= P; ++m) LR[c][m - 1] = (k + m < nt) ? band(k, kuf + m) : Z;
-        XR[c] = (k + P + 1 < nt) ? x[k + P + 1] : Z;
-    }
-    for (int kb = 0; kb < nt; kb += kD) {
-#pragma unroll
-        for (int c = 0; c < kD; ++c) {
-            const int k = kb + c;
-            if (k < nt) {
-                const int po = PR[c];
-#pragma unroll
-                for (int m = 1; m <= P; ++m)
-                    if (po == m) {
-                        const double2 t = w[0];
-                        w[0] = w[m];
-                        w[m] = t;
-                    }
-#pragma unroll
-                for (int m = 1; m <= P; ++m) w[m] = csub(w[m], cmul(LR[c][m - 1], w[0]));
-                x[k] = w[0];
-#pragma unroll
-                for (int m = 0; m < P; ++m) w[m] = w[m + 1];
-                w[P] = XR[c];
-                const int kn = k + kD; // refill this slot
-                PR[c] = kn < nt ? piv[(size_t)kn * nblk + i] : 0;
-#pragma unroll
-                for (int m = 1; m <= P; ++m) LR[c][m - 1] = (kn + m < nt) ? band(kn, kuf + m) : Z;
-                XR[c] = (kn + P + 1 < nt) ? x[kn + P + 1] : Z;
+        for (int m = 1; m <= P; ++m)
+            if (po == m) {
+                const double2 t = w[0];
+                w[0] = w[m];
+                w[m] = t;
             }
-        }
+#pragma unroll
+        for (int m = 1; m <= P; ++m)
+            if (k + m < nt) w[m] = csub(w[m], cmul(band(k, kuf + m), w[0]));
+        x[k] = w[0];
+#pragma unroll
+        for (int m = 0; m < P; ++m) w[m] = w[m + 1];
+        w[P] = (k + P + 1 < nt) ? x[k + P + 1] : make_double2(0.0, 0.0);
     }
     // backward: U, column oriented (eigensolve.cpp:134-139); u[j] = x[k-j]
     double2 u[2 * P + 1];
 #pragma unroll
-    for (int j = 0; j <= 2 * P; ++j) u[j] = (nt - 1 - j >= 0) ? x[nt - 1 - j] : Z;
-    double2 UR[kD][2 * P + 1];
-    double2 YR[kD];
+    for (int j = 0; j <= 2 * P; ++j) u[j] = (nt - 1 - j >= 0) ? x[nt - 1 - j] : make_double2(0.0, 0.0);
+    for (int k = nt - 1; k >= 0; --k) {
+        u[0] = cdiv(u[0], band(k, kuf));
 #pragma unroll
-    for (int c = 0; c < kD; ++c) {
-        const int k = nt - 1 - c;
+        for (int j = 1; j <= 2 * P; ++j)
+            if (k - j >= 0) u[j] = csub(u[j], cmul(band(k, kuf - j), u[0]));
+        x[k] = u[0];
 #pragma unroll
-        for (int j = 0; j <= 2 * P; ++j) UR[c][j] = k >= 0 ? band(k, kuf - j) : Z;
-        YR[c] = (k - 2 * P - 1 >= 0) ? x[k - 2 * P - 1] : Z;
-    }
-    for (int kb = nt - 1; kb >= 0; kb -= kD) {
-#pragma unroll
-        for (int c = 0; c < kD; ++c) {
-            const int k = kb - c;
-            if (k >= 0) {
-                u[0] = cdiv(u[0], UR[c][0]);
-#pragma unroll
-                for (int j = 1; j <= 2 * P; ++j) u[j] = csub(u[j], cmul(UR[c][j], u[0]));
-                x[k] = u[0];
-#pragma unroll
-                for (int j = 0; j < 2 * P; ++j) u[j] = u[j + 1];
-                u[2 * P] = YR[c];
-                const int kn = k - kD;
-#pragma unroll
-                for (int j = 0; j <= 2 * P; ++j) UR[c][j] = kn >= 0 ? band(kn, kuf - j) : Z;
-                YR[c] = (kn - 2 * P - 1 >= 0) ? x[kn - 2 * P - 1] : Z;
-            }
-        }
+        for (int j = 0; j < 2 * P; ++j) u[j] = u[j + 1];
+        u[2 * P] = (k - 2 * P - 1 >= 0) ? x[k - 2 * P - 1] : make_double2(0.0, 0.0);
     }
 }
 

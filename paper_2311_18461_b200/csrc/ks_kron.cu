@@ -31,6 +31,15 @@
 
 namespace ks {
 
+struct SweepEntry {
+    int out;    // output node
+    int factor; // -1 = identity
+    double2 coeff;
+};
+bool launch_colsweep(int nin, int nout, int bw, const double2* const* ip, double2* const* op,
+                     const int* in_begin, const SweepEntry* entries, const double2* rb,
+                     const int* freal, size_t ncols, size_t s, int n, int nmax, cudaStream_t st);
+
 struct KronFactor {
     int n = 0, bw = 0;
     bool is_real = false;
@@ -146,12 +155,6 @@ __global__ void __launch_bounds__(256) k_kron_level(
 // ---------------------------------------------------------------------------
 constexpr int kR = 4;
 constexpr int kMaxOut = 8;
-
-struct SweepEntry {
-    int out;    // output node
-    int factor; // -1 = identity
-    double2 coeff;
-};
 
 template <int NOUT, int BW>
 __global__ void __launch_bounds__(256) k_kron_sweep(
@@ -493,7 +496,16 @@ void kron_apply(KronPlan& P, const double2* x, double2* y, cudaStream_t st,
         size_t s = 1;
         for (int a = 0; a < ps.axis; ++a) s *= (size_t)P.dims[a];
         const int n = P.dims[ps.axis];
-        // v3 sweep when the level fits its register budget (NOUT <= 8, bw <= 4)
+        // spatial axes: full-column sliding-window sweep
+        if (s > 1 && ps.n_in <= 8 && ps.n_out <= 8 && P.bwmax >= 1 && P.bwmax <= 4) {
+            auto ip = reinterpret_cast<const double2* const*>(dp + P.ptr_off[k]);
+            auto op = reinterpret_cast<double2* const*>(const_cast<void**>(dp + P.ptr_off[k] + ps.n_in));
+            if (launch_colsweep(ps.n_in, ps.n_out, P.bwmax, ip, op, ps.d_in_begin.as<int>(),
+                                ps.d_entries.as<SweepEntry>(), P.d_rowband.as<double2>(),
+                                P.d_freal.as<int>(), P.N / (size_t)n, s, n, P.nmax, st))
+                continue;
+        }
+        // time axis (and any other shape): row-chunk sweep
         if (ps.n_out <= kMaxOut && P.bwmax >= 1 && P.bwmax <= 4) {
             const size_t ncols = P.N / (size_t)n;
             const size_t nth = ncols * (size_t)((n + kR - 1) / kR);
