@@ -496,8 +496,8 @@ void kron_apply(KronPlan& P, const double2* x, double2* y, cudaStream_t st,
         size_t s = 1;
         for (int a = 0; a < ps.axis; ++a) s *= (size_t)P.dims[a];
         const int n = P.dims[ps.axis];
-        // spatial axes: full-column sliding-window sweep
-        if (s > 1 && ps.n_in <= 8 && ps.n_out <= 8 && P.bwmax >= 1 && P.bwmax <= 4) {
+        // smem column-tile kernel (all axes)
+        if (ps.n_out <= 8 && P.bwmax >= 1 && P.bwmax <= 4) {
             auto ip = reinterpret_cast<const double2* const*>(dp + P.ptr_off[k]);
             auto op = reinterpret_cast<double2* const*>(const_cast<void**>(dp + P.ptr_off[k] + ps.n_in));
             if (launch_colsweep(ps.n_in, ps.n_out, P.bwmax, ip, op, ps.d_in_begin.as<int>(),
