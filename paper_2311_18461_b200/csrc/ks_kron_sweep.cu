@@ -33,13 +33,28 @@ __global__ void __launch_bounds__(kTileThreads) k_kron_elem(
     const double2* const* __restrict__ in_ptrs, int n_in, double2* const* __restrict__ out_ptrs,
     const int* __restrict__ in_begin, const SweepEntry* __restrict__ entries,
     const double2* __restrict__ rb, const int* __restrict__ freal, size_t N, size_t s, int n,
-    int nmax) {
+    int nmax, size_t nqt) {
     constexpr int TAPS = 2 * BW + 1;
-    const size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-    if (idx >= N) return;
-    const size_t q = idx % s, t = idx / s;
-    const int r = (int)(t % (size_t)n);
-    const size_t o = t / (size_t)n;
+    size_t idx, q, o;
+    int r;
+    if (nqt == 0) { // natural order: q fastest, then r
+        idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+        if (idx >= N) return;
+        q = idx % s;
+        const size_t t = idx / s;
+        r = (int)(t % (size_t)n);
+        o = t / (size_t)n;
+    } else {        // long strides: CTA = (o, q-tile, r), r fastest across CTAs so the
+                    // +-BW neighbour rows of a q-tile are still in L2
+        const size_t b = blockIdx.x;
+        r = (int)(b % (size_t)n);
+        const size_t rest = b / (size_t)n;
+        const size_t qt = rest % nqt;
+        o = rest / nqt;
+        q = qt * blockDim.x + threadIdx.x;
+        if (q >= s) return;
+        idx = (o * (size_t)n + r) * s + q;
+    }
     const size_t base = o * (size_t)n * s + q;
     const double2 Z = make_double2(0.0, 0.0);
     double2 acc[NOUT];
@@ -102,12 +117,12 @@ __global__ void __launch_bounds__(kTileThreads) k_kron_elem(
 template <int NOUT>
 void launch_bw(int bw, unsigned grid, cudaStream_t st, const double2* const* ip, int nin,
                double2* const* op, const int* ib, const SweepEntry* en, const double2* rb,
-               const int* fr, size_t N, size_t s, int n, int nmax) {
+               const int* fr, size_t N, size_t s, int n, int nmax, size_t nqt) {
     switch (bw) {
-    case 1: k_kron_elem<NOUT, 1><<<grid, kTileThreads, 0, st>>>(ip, nin, op, ib, en, rb, fr, N, s, n, nmax); break;
-    case 2: k_kron_elem<NOUT, 2><<<grid, kTileThreads, 0, st>>>(ip, nin, op, ib, en, rb, fr, N, s, n, nmax); break;
-    case 3: k_kron_elem<NOUT, 3><<<grid, kTileThreads, 0, st>>>(ip, nin, op, ib, en, rb, fr, N, s, n, nmax); break;
-    default: k_kron_elem<NOUT, 4><<<grid, kTileThreads, 0, st>>>(ip, nin, op, ib, en, rb, fr, N, s, n, nmax); break;
+    case 1: k_kron_elem<NOUT, 1><<<grid, kTileThreads, 0, st>>>(ip, nin, op, ib, en, rb, fr, N, s, n, nmax, nqt); break;
+    case 2: k_kron_elem<NOUT, 2><<<grid, kTileThreads, 0, st>>>(ip, nin, op, ib, en, rb, fr, N, s, n, nmax, nqt); break;
+    case 3: k_kron_elem<NOUT, 3><<<grid, kTileThreads, 0, st>>>(ip, nin, op, ib, en, rb, fr, N, s, n, nmax, nqt); break;
+    default: k_kron_elem<NOUT, 4><<<grid, kTileThreads, 0, st>>>(ip, nin, op, ib, en, rb, fr, N, s, n, nmax, nqt); break;
     }
 }
 
@@ -119,16 +134,22 @@ bool launch_colsweep(int nin, int nout, int bw, const double2* const* ip, double
                      const int* freal, size_t ncols, size_t s, int n, int nmax, cudaStream_t st) {
     if (nout < 1 || nout > 8 || bw < 1 || bw > 4) return false;
     const size_t N = ncols * (size_t)n;
-    const unsigned grid = (unsigned)((N + kTileThreads - 1) / kTileThreads);
+    size_t nqt = 0;
+    unsigned grid = (unsigned)((N + kTileThreads - 1) / kTileThreads);
+    if (s >= 4 * kTileThreads) {
+        nqt = (s + kTileThreads - 1) / kTileThreads;
+        const size_t outer = ncols / s;
+        grid = (unsigned)(outer * nqt * (size_t)n);
+    }
     switch (nout) {
-    case 1: launch_bw<1>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax); break;
-    case 2: launch_bw<2>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax); break;
-    case 3: launch_bw<3>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax); break;
-    case 4: launch_bw<4>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax); break;
-    case 5: launch_bw<5>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax); break;
-    case 6: launch_bw<6>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax); break;
-    case 7: launch_bw<7>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax); break;
-    case 8: launch_bw<8>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax); break;
+    case 1: launch_bw<1>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax, nqt); break;
+    case 2: launch_bw<2>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax, nqt); break;
+    case 3: launch_bw<3>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax, nqt); break;
+    case 4: launch_bw<4>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax, nqt); break;
+    case 5: launch_bw<5>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax, nqt); break;
+    case 6: launch_bw<6>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax, nqt); break;
+    case 7: launch_bw<7>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax, nqt); break;
+    case 8: launch_bw<8>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax, nqt); break;
     }
     check_launch("k_kron_elem");
     return true;
