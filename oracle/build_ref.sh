@@ -26,3 +26,11 @@ wait
 $CXX $FLAGS -c "$HERE/ref_driver.cpp" -o "$OUT/ref_driver.o"
 $CXX -shared -o "$OUT/libkronschro_ref.so" "${objs[@]}" "$OUT/ref_driver.o"
 echo "built $OUT/libkronschro_ref.so"
+# the reference-side binding as a runnable drop-in demo,
+# linked against the reference objects and libks.so (rpath = repo-relative)
+KS="$HERE/../paper_2311_18461_b200"
+if [ -f "$KS/libks.so" ]; then
+  $CXX $FLAGS -I"$HERE/../include" "$HERE/integration_demo.cpp" "${objs[@]}" -o "$OUT/integration_demo" \
+      -L"$KS" -lks -Wl,-rpath,'$ORIGIN/../../paper_2311_18461_b200'
+  echo "built $OUT/integration_demo"
+fi
