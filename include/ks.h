@@ -200,6 +200,32 @@ uint64_t ks_launch_count(void);
 void ks_launch_count_reset(void);
 
 /* ---------------------------------------------------------------------------
+ * Slab-sharded FD preconditioner (multi-GPU); one rank per GPU.
+ * Axis d (outermost spatial) is split in contiguous slabs, so every rank owns
+ * a contiguous chunk of each vector. The caller runs two all-to-alls
+ * (counts from ks_shard_plan, in complex elements; the way back swaps the
+ * send/recv roles):
+ *   forward(r_slab -> send) ; all_to_all(send -> work) ; middle(work) ;
+ *   all_to_all(work -> back) ; backward(back -> z_slab)
+ * ks_shard_plan is host-only (no device needed).
+ * ------------------------------------------------------------------------- */
+typedef struct ks_fdshard ks_fdshard;
+
+int ks_shard_plan(int d, const int* dims, int nranks, int rank, long long* slab_lo,
+                  long long* slab_hi, long long* send_counts, long long* send_displs,
+                  long long* recv_counts, long long* recv_displs);
+int ks_fdshard_create(int d, const int* dims, double nu, int p_t,
+                      const double* const* U, const double* const* lambda,
+                      const double* Lt, const double* Mt, const ks_c64* Wt,
+                      int nranks, int rank, int device, ks_fdshard** out);
+/* complex elements of the local slab and of the re-sharded work tensor */
+int ks_fdshard_sizes(const ks_fdshard* h, size_t* slab_n, size_t* work_n);
+int ks_fdshard_forward(ks_fdshard* h, const ks_c64* r_slab, ks_c64* sendbuf, void* stream);
+int ks_fdshard_middle(ks_fdshard* h, ks_c64* work, void* stream);
+int ks_fdshard_backward(ks_fdshard* h, const ks_c64* recvbuf, ks_c64* z_slab, void* stream);
+int ks_fdshard_destroy(ks_fdshard* h);
+
+/* ---------------------------------------------------------------------------
  * Host setup (product-side mirror of the reference's shared setup; used when
  * no reference process hands over its own setup products)
  *   SpaceTimeProblem::uniform  (assembly.cpp:110-117)

@@ -126,6 +126,18 @@ _SIGS = {
     "ks_transform_engine": (C.c_int, []),
     "ks_launch_count": (C.c_uint64, []),
     "ks_launch_count_reset": (None, []),
+    "ks_shard_plan": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.c_int, C.c_int,
+                                C.POINTER(C.c_longlong), C.POINTER(C.c_longlong),
+                                C.POINTER(C.c_longlong), C.POINTER(C.c_longlong),
+                                C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),
+    "ks_fdshard_create": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.c_double, C.c_int,
+                                    C.POINTER(_P), C.POINTER(_P), _P, _P, _P, C.c_int, C.c_int,
+                                    C.c_int, C.POINTER(_P)]),
+    "ks_fdshard_sizes": (C.c_int, [_P, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
+    "ks_fdshard_forward": (C.c_int, [_P, _P, _P, _P]),
+    "ks_fdshard_middle": (C.c_int, [_P, _P, _P]),
+    "ks_fdshard_backward": (C.c_int, [_P, _P, _P, _P]),
+    "ks_fdshard_destroy": (C.c_int, [_P]),
     "ks_setup_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                   C.c_int, C.POINTER(_P)]),
     "ks_setup_dims": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
