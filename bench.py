@@ -273,10 +273,13 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
     args = ap.parse_args()
-    rank, ws, local, dist = dist_init()
     if args.impl == "reference":
-        run_reference_arm(args, rank, ws, dist)
+        # CPU arm: rank 0 alone runs the reference; other ranks exit without work
+        rank = int(os.environ.get("RANK", "0"))
+        ws = int(os.environ.get("WORLD_SIZE", "1"))
+        run_reference_arm(args, rank, ws, None)
         return
+    rank, ws, local, dist = dist_init()
     if ws > 1:
         run_sharded(args, rank, ws, local, dist)
         return

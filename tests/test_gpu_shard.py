@@ -71,3 +71,30 @@ def test_virtual_ranks_match_single_gpu(gpu, oracle, P, d, p, n_el, n_el_t):
     if N <= 400000:
         F = oracle.OracleFD(dims, 1.0, p, a["U"], a["lam"], a["Lt"], a["Mt"], a["Wt"])
         assert rel(z, F.apply(r)) < 1e-10
+
+
+def test_sharded_class_single_rank_nccl(gpu, oracle):
+    """dist.ShardedFDPreconditioner end to end over a 1-rank NCCL group."""
+    import os
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_2311_18461_b200.dist import ShardedFDPreconditioner
+    ks = gpu
+    a = setup_arrays(ks, 3, 2, 10, 9)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        S = ShardedFDPreconditioner(a["dims"], 1.0, 2, a["U"], a["lam"], a["Lt"], a["Mt"], a["Wt"])
+        r = oracle.random_vec(int(np.prod(a["dims"])), 7)
+        z = S.apply(torch.from_numpy(r).cuda()).cpu().numpy()
+        torch.cuda.synchronize()
+        single = ks.FDPreconditioner.from_arrays(a["dims"], 1.0, 2, a["U"], a["lam"], a["Lt"],
+                                                 a["Mt"], a["Wt"])
+        assert rel(z, single.apply(r)) < 1e-12
+    finally:
+        dist.destroy_process_group()
