@@ -487,6 +487,97 @@ k_mode_gemm_dmma2(const double* __restrict__ At, int n, const double* __restrict
     cp_async_wait<0>();
 }
 
+// ---------------------------------------------------------------------------
+// DMMA engine v3 (small axes, n <= 80): the whole K extent of a column tile is
+// one cp.async group (two tile buffers), so per synchronisation a warp issues
+// TM*4*nk*4 DMMAs (256 at n = 64) and the per-work-item integer work of v2
+// (which left the SMSP issue slots, not the tensor pipe, as the limit) is paid
+// once per tile. Column maps as in v2. One CTA (8 warps) per SM.
+// ---------------------------------------------------------------------------
+template <int TM>
+__global__ void __launch_bounds__(kThreads, 1)
+k_mode_gemm_dmma3(const double* __restrict__ At, int n, const double* __restrict__ X,
+                  double* __restrict__ Y, ColMap M) {
+    constexpr int BM = 16 * TM;
+    constexpr int MT = TM;
+    constexpr int BMP = BM + 4;
+    constexpr int BNP = kBN + 4;
+    constexpr int KMAX = BM; // K padded to the row padding (n <= BM)
+    extern __shared__ __align__(16) double smem[];
+    const int nk = (n + kBK - 1) / kBK;
+    const int kpad = nk * kBK;
+    double* As = smem;                           // [KMAX][BMP]
+    double* Bs = smem + (size_t)KMAX * BMP;      // [2][KMAX][BNP]
+    const long long in_rs = M.mode == MAP_TIN ? 2 * M.Np : 2 * M.s;
+    const long long out_rs = M.mode == MAP_TOUT ? 2 * M.Np : 2 * M.s;
+    const long long ntiles = M.ntiles;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wr = warp & 1, wc = warp >> 1;
+    for (int e = tid; e < kpad * BM; e += kThreads) {
+        const int j = e / BM, r = e - j * BM;
+        As[j * BMP + r] = (j < n && r < n) ? __ldg(At + (long long)j * n + r) : 0.0;
+    }
+    const int lcp = tid & 63, lrow0 = tid >> 6;
+    auto issue = [&](long long tile, int buf) {
+        if (tile < ntiles) {
+            long long in_off, dummy;
+            const bool cv = colmap(M, n, tile_base(M, tile), lcp, in_off, dummy);
+            double* bs = Bs + (size_t)buf * KMAX * BNP;
+            const double* src = X + in_off;
+            for (int j = lrow0; j < kpad; j += 4) {
+                const bool v = cv && j < n;
+                cp_async16(bs + j * BNP + 2 * lcp, v ? (const void*)(src + (long long)j * in_rs) : (const void*)X, v);
+            }
+        }
+        cp_async_commit();
+    };
+    const int r_warp = wr * (BM / 2), c_warp = wc * 32;
+    const int ar = lane >> 2, ak = lane & 3, cr = lane >> 2;
+    long long tile = blockIdx.x;
+    int buf = 0;
+    issue(tile, 0);
+    for (; tile < ntiles; tile += gridDim.x, buf ^= 1) {
+        issue(tile + gridDim.x, buf ^ 1);
+        cp_async_wait<1>();
+        __syncthreads();
+        double acc[MT][4][2];
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+            for (int m = 0; m < 4; ++m) acc[i][m][0] = acc[i][m][1] = 0.0;
+        const double* bs = Bs + (size_t)buf * KMAX * BNP;
+        for (int k4 = 0; k4 < kpad; k4 += 4) {
+            double a[MT], b[4];
+#pragma unroll
+            for (int i = 0; i < MT; ++i) a[i] = As[(k4 + ak) * BMP + r_warp + i * 8 + ar];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) b[m] = bs[(k4 + ak) * BNP + c_warp + m * 8 + ar];
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int m = 0; m < 4; ++m) dmma_m8n8k4(acc[i][m][0], acc[i][m][1], a[i], b[m]);
+        }
+        const TileBase tb = tile_base(M, tile);
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const int jcol = (c_warp >> 1) + m * 4 + (lane & 3);
+            long long io, oo;
+            if (colmap(M, n, tb, jcol, io, oo)) {
+                double* yb = Y + oo;
+#pragma unroll
+                for (int i = 0; i < MT; ++i) {
+                    const int r = r_warp + i * 8 + cr;
+                    if (r < n)
+                        *reinterpret_cast<double2*>(yb + (long long)r * out_rs) =
+                            make_double2(acc[i][m][0], acc[i][m][1]);
+                }
+            }
+        }
+        __syncthreads(); // the next iteration's issue overwrites this buffer
+    }
+    cp_async_wait<0>();
+}
+
 int engine_choice() {
     static int e = [] {
         const char* v = std::getenv("KS_GEMM");
@@ -511,6 +602,21 @@ void launch_tm(int engine, const double* At, int n, const double* X, double* Y, 
         }
         k_mode_gemm_dfma<TM><<<grid, kThreads, sm, st>>>(At, n, X, Y, W2, C);
         check_launch("k_mode_gemm_dfma");
+    } else if (engine == 2 && TM <= 5 && !std::getenv("KS_GEMM_V2")) {
+        constexpr int BM = 16 * TM;
+        const size_t sm = ((size_t)BM * (BM + 4) + (size_t)2 * BM * (kBN + 4)) * sizeof(double);
+        static int sms = 0;
+        if (!sms) {
+            int dev = 0;
+            KS_CUDA(cudaGetDevice(&dev));
+            KS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            KS_CUDA(cudaFuncSetAttribute(k_mode_gemm_dmma3<TM>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        }
+        ColMap Mm = *map;
+        const unsigned g3 = (unsigned)std::min<long long>(Mm.ntiles, (long long)sms);
+        k_mode_gemm_dmma3<TM><<<g3, kThreads, sm, st>>>(At, n, X, Y, Mm);
+        check_launch("k_mode_gemm_dmma3");
     } else if (engine == 2) {
         const int nk = (n + kBK - 1) / kBK;
         const size_t sm = ((size_t)nk * kBK * (16 * TM + 4) + (size_t)kStages * kBK * (kBN + 4)) *
