@@ -546,6 +546,7 @@ k_mode_gemm_dmma3(const double* __restrict__ At, int n, const double* __restrict
 #pragma unroll
             for (int m = 0; m < 4; ++m) acc[i][m][0] = acc[i][m][1] = 0.0;
         const double* bs = Bs + (size_t)buf * KMAX * BNP;
+#pragma unroll 4
         for (int k4 = 0; k4 < kpad; k4 += 4) {
             double a[MT], b[4];
 #pragma unroll
