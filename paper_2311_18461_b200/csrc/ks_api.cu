@@ -74,6 +74,7 @@ struct ks_fd {
     std::vector<DevBuf> At_fwd, At_inv, lam;
     std::vector<std::vector<double>> lam_host;
     std::vector<int> fiber_block; // host copy of the block map (empty = identity)
+    bool fused = false;           // outermost axis via k_fd_fused
     DevBuf Lt, Mt, Wsym;
     FdBlocks blocks;
     DevBuf s0, s1, io;
@@ -132,6 +133,42 @@ void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStre
         }
     };
     (void)s;
+    if (f->fused && !adjoint) {
+        // axes 1..d-1 forward, fused [axis d forward, solves, axis d inverse],
+        // axes 1..d-1 inverse
+        for (int l = 1; l < d; ++l) {
+            double* out = bufs[nb];
+            nb ^= 1;
+            gemm(f->At_fwd[l - 1], l, cur, out, 0);
+            cur = out;
+        }
+        double* mid = (d == 1) ? reinterpret_cast<double*>(z) : bufs[nb];
+        if (d != 1) nb ^= 1;
+        if (ev) {
+            cudaEvent_t a, b;
+            KS_CUDA(cudaEventCreate(&a));
+            KS_CUDA(cudaEventCreate(&b));
+            KS_CUDA(cudaEventRecord(a, st));
+            launch_fd_fused(f->At_fwd[d - 1].as<double>(), f->At_inv[d - 1].as<double>(), f->blocks,
+                            f->dims[d], (long long)(f->Ns / (size_t)f->dims[d]),
+                            reinterpret_cast<const double2*>(cur), reinterpret_cast<double2*>(mid), st);
+            KS_CUDA(cudaEventRecord(b, st));
+            ev->push_back(a);
+            ev->push_back(b);
+        } else {
+            launch_fd_fused(f->At_fwd[d - 1].as<double>(), f->At_inv[d - 1].as<double>(), f->blocks,
+                            f->dims[d], (long long)(f->Ns / (size_t)f->dims[d]),
+                            reinterpret_cast<const double2*>(cur), reinterpret_cast<double2*>(mid), st);
+        }
+        cur = mid;
+        for (int l = 1; l < d; ++l) {
+            double* out = (l == d - 1) ? reinterpret_cast<double*>(z) : bufs[nb];
+            if (l != d - 1) nb ^= 1;
+            gemm(f->At_inv[l - 1], l, cur, out, 0);
+            cur = out;
+        }
+        return;
+    }
     // to_eigen: axes 1..d with U_l^T (fdsolver.cpp:7-14). The last one (the
     // outermost axis d) writes the time-major layout T[t][fiber] so that the
     // block solves read and write coalesced.
@@ -292,7 +329,17 @@ int ks_fd_create(int d, const int* dims, double nu, int p_t, const double* const
     B.p = p_t;
     B.ldab = 3 * p_t + 1;
     B.ns = f->Ns;
-    bool dedup = d >= 2;
+    // fused outermost-axis kernel (ks_fdfused.cu) when the slab fits shared memory;
+    // it streams per-column factors, so it factors every fiber (no dedup)
+    const long long Np_all = (long long)(f->Ns / (size_t)dims[d]);
+    bool fused = fd_fused_supported(nt, dims[d], p_t);
+    if (const char* e = std::getenv("KS_FD_FUSED")) fused = fused && std::strcmp(e, "0") != 0;
+    f->fused = fused;
+    if (fused) {
+        B.fused_nd = dims[d];
+        B.fused_np = Np_all;
+    }
+    bool dedup = d >= 2 && !fused;
     for (int l = 1; l < d && dedup; ++l)
         dedup = dims[l + 1] == dims[1] &&
                 std::memcmp(lambda[l], lambda[0], sizeof(double) * dims[1]) == 0;
@@ -392,13 +439,21 @@ int ks_fd_block(const ks_fd* fd, size_t i, ks_c64* ab, int* piv) {
     ensure_device(fd->device);
     const FdBlocks& B = fd->blocks;
     const size_t b = fd->fiber_block.empty() ? i : (size_t)fd->fiber_block[i];
+    size_t fb = b, fe = B.nblk, pbi = b, pst = B.nblk;
+    if (B.fused_nd > 0) {
+        const size_t rho = b % (size_t)B.fused_np, r = b / (size_t)B.fused_np;
+        fb = rho * (size_t)B.nt * B.ldab * B.fused_nd + r;
+        fe = B.fused_nd;
+        pbi = rho * (size_t)B.nt * B.fused_nd + r;
+        pst = B.fused_nd;
+    }
     for (int k = 0; k < B.nt; ++k) {
         for (int e = 0; e < B.ldab; ++e)
             KS_CUDA(cudaMemcpy(ab + (size_t)k * B.ldab + e,
-                               B.ab.as<double2>() + ((size_t)k * B.ldab + e) * B.nblk + b,
+                               B.ab.as<double2>() + fb + ((size_t)k * B.ldab + e) * fe,
                                sizeof(double2), cudaMemcpyDeviceToHost));
         unsigned char po = 0;
-        KS_CUDA(cudaMemcpy(&po, B.piv.as<unsigned char>() + (size_t)k * B.nblk + b, 1,
+        KS_CUDA(cudaMemcpy(&po, B.piv.as<unsigned char>() + pbi + (size_t)k * pst, 1,
                            cudaMemcpyDeviceToHost));
         piv[k] = k + po;
     }

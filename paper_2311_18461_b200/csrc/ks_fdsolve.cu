@@ -73,19 +73,31 @@ __global__ void k_fd_factor(double2* __restrict__ ab, unsigned char* __restrict_
                             int* __restrict__ flag, size_t ns, int nt, int p,
                             const double* __restrict__ lam_blk, double nu,
                             const double* __restrict__ Lt, const double* __restrict__ Mt,
-                            const double2* __restrict__ Wsym) {
+                            const double2* __restrict__ Wsym, int fused_nd, long long fused_np) {
     const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     if (i >= ns) return; // here ns = number of factored blocks
     const int ldab = 3 * p + 1, kuf = 2 * p, bwld = 2 * p + 1;
+    // layout: block-interleaved [k][e][block], or (fused_nd > 0) per rest column
+    // [rho][k][e][r] for block i = rho + Np * r (the fused axis-d kernel's fibers)
+    size_t base = i, estr = ns, kstr = (size_t)ldab * ns;
+    size_t pbase = i, pstr = ns;
+    if (fused_nd > 0) {
+        const size_t rho = i % (size_t)fused_np, r = i / (size_t)fused_np;
+        base = rho * (size_t)nt * ldab * fused_nd + r;
+        estr = fused_nd;
+        kstr = (size_t)ldab * fused_nd;
+        pbase = rho * (size_t)nt * fused_nd + r;
+        pstr = fused_nd;
+    }
     // composite eigenvalue lambda_i = sum_l lambda_l[i_l], formed on the host in
     // the reference's summation order (fdsolver.cpp:30-42)
     const double lam = lam_blk[i];
     auto A = [&](int r, int c) -> double2& {
-        return ab[((size_t)c * ldab + (size_t)(kuf + r - c)) * ns + i];
+        return ab[base + (size_t)c * kstr + (size_t)(kuf + r - c) * estr];
     };
     // fill: zero band, then H(r, c) for |r - c| <= p
     for (int c = 0; c < nt; ++c)
-        for (int e = 0; e < ldab; ++e) ab[((size_t)c * ldab + e) * ns + i] = make_double2(0.0, 0.0);
+        for (int e = 0; e < ldab; ++e) ab[base + (size_t)c * kstr + (size_t)e * estr] = make_double2(0.0, 0.0);
     const double s2 = nu * nu * lam * lam; // nu*nu*lam*lam (left to right)
     const double s1 = nu * lam;
     for (int c = 0; c < nt; ++c) {
@@ -113,7 +125,7 @@ __global__ void k_fd_factor(double2* __restrict__ ab, unsigned char* __restrict_
                 pr = r;
             }
         }
-        piv[(size_t)k * ns + i] = (unsigned char)(pr - k);
+        piv[pbase + (size_t)k * pstr] = (unsigned char)(pr - k);
         if (best == 0.0) {
             atomicExch(flag, 1);
             return;
@@ -143,7 +155,7 @@ __global__ void __launch_bounds__(128) k_fd_solve(const double2* __restrict__ ab
                                                   const unsigned char* __restrict__ piv,
                                                   double2* __restrict__ X, size_t ns, int nt,
                                                   size_t nblk, const int* __restrict__ fblk,
-                                                  int tmajor) {
+                                                  int tmajor, int fnd, long long fnp) {
     const size_t f = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     if (f >= ns) return;
     constexpr int ldab = 3 * P + 1, kuf = 2 * P;
@@ -156,15 +168,24 @@ __global__ void __launch_bounds__(128) k_fd_solve(const double2* __restrict__ ab
         __device__ double2& operator[](int k) const { return p[(size_t)k * s]; }
     } x{x0, xs};
     const size_t i = fblk ? (size_t)__ldg(fblk + f) : f; // factored block of this fiber
+    // factor address: block-interleaved, or per-rest-column (fused layout)
+    size_t fb = i, fe = nblk, pbi = i, pst = nblk;
+    if (fnd > 0) {
+        const size_t rho = i % (size_t)fnp, r = i / (size_t)fnp;
+        fb = rho * (size_t)nt * ldab * fnd + r;
+        fe = fnd;
+        pbi = rho * (size_t)nt * fnd + r;
+        pst = fnd;
+    }
     auto band = [&](int k, int e) -> double2 {
-        return __ldg(ab + ((size_t)k * ldab + e) * nblk + i);
+        return __ldg(ab + fb + ((size_t)k * ldab + e) * fe);
     };
     // forward: L with row interchanges (eigensolve.cpp:127-133); w[m] = x[k+m]
     double2 w[P + 1];
 #pragma unroll
     for (int m = 0; m <= P; ++m) w[m] = m < nt ? x[m] : make_double2(0.0, 0.0);
     for (int k = 0; k < nt; ++k) {
-        const int po = piv[(size_t)k * nblk + i];
+        const int po = piv[pbi + (size_t)k * pst];
 #pragma unroll
         for (int m = 1; m <= P; ++m)
             if (po == m) {
@@ -202,7 +223,7 @@ __global__ void __launch_bounds__(128) k_fd_solve_adj(const double2* __restrict_
                                                       const unsigned char* __restrict__ piv,
                                                       double2* __restrict__ X, size_t ns, int nt,
                                                       size_t nblk, const int* __restrict__ fblk,
-                                                  int tmajor) {
+                                                  int tmajor, int fnd, long long fnp) {
     const size_t f = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     if (f >= ns) return;
     constexpr int ldab = 3 * P + 1, kuf = 2 * P;
@@ -215,8 +236,17 @@ __global__ void __launch_bounds__(128) k_fd_solve_adj(const double2* __restrict_
         __device__ double2& operator[](int k) const { return p[(size_t)k * s]; }
     } x{x0, xs};
     const size_t i = fblk ? (size_t)__ldg(fblk + f) : f;
+    // factor address: block-interleaved, or per-rest-column (fused layout)
+    size_t fb = i, fe = nblk, pbi = i, pst = nblk;
+    if (fnd > 0) {
+        const size_t rho = i % (size_t)fnp, r = i / (size_t)fnp;
+        fb = rho * (size_t)nt * ldab * fnd + r;
+        fe = fnd;
+        pbi = rho * (size_t)nt * fnd + r;
+        pst = fnd;
+    }
     auto band = [&](int k, int e) -> double2 {
-        return __ldg(ab + ((size_t)k * ldab + e) * nblk + i);
+        return __ldg(ab + fb + ((size_t)k * ldab + e) * fe);
     };
     // U^H z = y, forward; h[j] = x[k - 2P + j] (finalised values)
     double2 h[2 * P];
@@ -249,7 +279,7 @@ __global__ void __launch_bounds__(128) k_fd_solve_adj(const double2* __restrict_
         for (int m = 1; m <= P; ++m)
             if (k + m < nt) s = csub(s, cconjmul(band(k, kuf + m), g[m]));
         g[0] = s;
-        const int po = piv[(size_t)k * nblk + i];
+        const int po = piv[pbi + (size_t)k * pst];
 #pragma unroll
         for (int m = 1; m <= P; ++m)
             if (po == m) {
@@ -272,11 +302,11 @@ void launch_solve_p(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t st
     const unsigned grid = (unsigned)((B.ns + 127) / 128);
     if (adjoint) {
         k_fd_solve_adj<P><<<grid, 128, 0, st>>>(B.ab.as<double2>(), B.piv.as<unsigned char>(), X,
-                                                B.ns, B.nt, B.nblk, B.fiber_block.as<int>(), tm);
+                                                B.ns, B.nt, B.nblk, B.fiber_block.as<int>(), tm, B.fused_nd, B.fused_np);
         check_launch("k_fd_solve_adj");
     } else {
         k_fd_solve<P><<<grid, 128, 0, st>>>(B.ab.as<double2>(), B.piv.as<unsigned char>(), X,
-                                            B.ns, B.nt, B.nblk, B.fiber_block.as<int>(), tm);
+                                            B.ns, B.nt, B.nblk, B.fiber_block.as<int>(), tm, B.fused_nd, B.fused_np);
         check_launch("k_fd_solve");
     }
 }
@@ -289,7 +319,7 @@ void launch_fd_factor(FdBlocks& B, double nu, const double* Lt, const double* Mt
     const unsigned grid = (unsigned)((B.nblk + 127) / 128);
     k_fd_factor<<<grid, 128, 0, st>>>(B.ab.as<double2>(), B.piv.as<unsigned char>(),
                                       B.flag.as<int>(), B.nblk, B.nt, B.p, B.lam_blk.as<double>(), nu,
-                                      Lt, Mt, Wsym);
+                                      Lt, Mt, Wsym, B.fused_nd, B.fused_np);
     check_launch("k_fd_factor");
     int h = 0;
     KS_CUDA(cudaMemcpyAsync(&h, B.flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));

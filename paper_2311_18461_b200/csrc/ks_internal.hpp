@@ -137,6 +137,8 @@ struct FdBlocks {
     DevBuf flag;        // int: singular-pivot flag set by the factor kernel
     DevBuf lam_blk;     // double [nblk] composite eigenvalue of each block
     DevBuf fiber_block; // int [ns] block of each fiber (empty = identity)
+    int fused_nd = 0;        // > 0: per-rest-column layout for the fused axis-d kernel
+    long long fused_np = 0;  //      (block i = rho + fused_np * r, r < fused_nd)
 };
 // time bands on device: Lt, Mt real (2p+1)xnt, Wsym complex
 void launch_fd_factor(FdBlocks& B, double nu, const double* Lt, const double* Mt,
@@ -145,6 +147,13 @@ void launch_fd_factor(FdBlocks& B, double nu, const double* Lt, const double* Mt
 // contiguous fibers X[fiber][t]
 void launch_fd_solve(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t st,
                      bool time_major = false);
+
+// fused outermost-axis step of the FD apply (ks_fdfused.cu): X natural
+// (n_t, Np, n_d) -> forward transform with At_fwd, block solves, inverse with
+// At_inv -> Z natural. Returns false when the shape is not supported.
+bool fd_fused_supported(int nt, int nd, int p);
+void launch_fd_fused(const double* At_fwd, const double* At_inv, const FdBlocks& B, int nd,
+                     long long Np, const double2* X, double2* Z, cudaStream_t st);
 
 // ---------------------------------------------------------------------------
 // level-pass Kronecker engine (ks_kron.cu)
