@@ -332,8 +332,12 @@ int ks_fd_create(int d, const int* dims, double nu, int p_t, const double* const
     // fused outermost-axis kernel (ks_fdfused.cu) when the slab fits shared memory;
     // it streams per-column factors, so it factors every fiber (no dedup)
     const long long Np_all = (long long)(f->Ns / (size_t)dims[d]);
-    bool fused = fd_fused_supported(nt, dims[d], p_t);
-    if (const char* e = std::getenv("KS_FD_FUSED")) fused = fused && std::strcmp(e, "0") != 0;
+    // opt-in (KS_FD_FUSED=1): measured slower than the unfused path at c3 (1.39 ms
+    // vs 0.98 ms for the same work; the serial block solves of one slab leave
+    // 6 of 8 warps at the barrier) -- see profiles/round1_summary.md
+    bool fused = false;
+    if (const char* e = std::getenv("KS_FD_FUSED"))
+        fused = std::strcmp(e, "1") == 0 && fd_fused_supported(nt, dims[d], p_t);
     f->fused = fused;
     if (fused) {
         B.fused_nd = dims[d];

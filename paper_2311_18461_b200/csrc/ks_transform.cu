@@ -603,7 +603,8 @@ void launch_tm(int engine, const double* At, int n, const double* X, double* Y, 
         }
         k_mode_gemm_dfma<TM><<<grid, kThreads, sm, st>>>(At, n, X, Y, W2, C);
         check_launch("k_mode_gemm_dfma");
-    } else if (engine == 2 && TM <= 5 && !std::getenv("KS_GEMM_V2")) {
+    } else if (engine == 2 && TM <= 5 && std::getenv("KS_GEMM_V3")) {
+        // opt-in: measured slower than v2 at c3 (193-265 us vs 189-241 us per launch)
         constexpr int BM = 16 * TM;
         const size_t sm = ((size_t)BM * (BM + 4) + (size_t)2 * BM * (kBN + 4)) * sizeof(double);
         static int sms = 0;
