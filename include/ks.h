@@ -193,6 +193,8 @@ int ks_fp64_peak(double* tflops);
 int ks_fp64_peaks(double* dfma_tflops, double* dmma_tflops);
 /* Combined FP64 throughput with half the warps on DMMA and half on DFMA. */
 int ks_fp64_peak_mixed(double* tflops);
+/* FP64 tensor-core throughput with the sm_90+ mma.sync m16n8k16 shape. */
+int ks_fp64_peak_mma16(double* tflops);
 /* Which engine the spatial transforms use: 0 = DFMA, 1 = DMMA (env KS_GEMM). */
 int ks_transform_engine(void);
 /* Number of kernels the library launched since the last reset. */

@@ -123,6 +123,7 @@ _SIGS = {
     "ks_fp64_peak": (C.c_int, [C.POINTER(C.c_double)]),
     "ks_fp64_peaks": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "ks_fp64_peak_mixed": (C.c_int, [C.POINTER(C.c_double)]),
+    "ks_fp64_peak_mma16": (C.c_int, [C.POINTER(C.c_double)]),
     "ks_transform_engine": (C.c_int, []),
     "ks_launch_count": (C.c_uint64, []),
     "ks_launch_count_reset": (None, []),
@@ -579,6 +580,12 @@ def fp64_peaks():
     a, b = C.c_double(), C.c_double()
     _check(lib().ks_fp64_peaks(C.byref(a), C.byref(b)))
     return a.value, b.value
+
+
+def fp64_peak_mma16():
+    a = C.c_double()
+    _check(lib().ks_fp64_peak_mma16(C.byref(a)))
+    return a.value
 
 
 def fp64_peak_mixed():

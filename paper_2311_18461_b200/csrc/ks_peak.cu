@@ -43,6 +43,33 @@ __global__ void __launch_bounds__(256) k_dmma_peak(double* out, double seed) {
     if (s == 12345.678) out[threadIdx.x] = s;
 }
 
+// m16n8k16 f64 (sm_90+ shape): 2048 FMA per warp instruction
+__global__ void __launch_bounds__(256) k_dmma16_peak(double* out, double seed) {
+    double c[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c[i][j] = seed + i + j;
+    double a[8], b[4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = 0.999 + threadIdx.x * 1e-9 + i * 1e-6;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) b[i] = 1e-3 + i * 1e-7;
+    for (int it = 0; it < kIters / 32; ++it) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            asm volatile("mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, "
+                         "{%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};\n"
+                         : "+d"(c[i][0]), "+d"(c[i][1]), "+d"(c[i][2]), "+d"(c[i][3])
+                         : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]),
+                           "d"(a[7]), "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s += c[i][0] + c[i][1] + c[i][2] + c[i][3];
+    if (s == 12345.678) out[threadIdx.x] = s;
+}
+
 // warps 0-3 issue DMMA, warps 4-7 DFMA: does the FP64 tensor path run
 // concurrently with the CUDA-core FP64 pipe?
 __global__ void __launch_bounds__(256) k_mixed_peak(double* out, double seed) {
@@ -109,6 +136,32 @@ static void run_mixed(double* tflops) {
     *tflops = mixed_flops(grid) / (best * 1e-3) / 1e12;
 }
 
+static void run_mma16(double* tflops) {
+    int sms = 148, dev = 0;
+    KS_CUDA(cudaGetDevice(&dev));
+    KS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    DevBuf out(256 * sizeof(double));
+    const unsigned grid = sms * 8;
+    cudaEvent_t a, b;
+    KS_CUDA(cudaEventCreate(&a));
+    KS_CUDA(cudaEventCreate(&b));
+    float best = 1e30f;
+    for (int rep = 0; rep < 6; ++rep) {
+        KS_CUDA(cudaEventRecord(a));
+        k_dmma16_peak<<<grid, 256>>>(out.as<double>(), 1.0);
+        check_launch("k_dmma16_peak");
+        KS_CUDA(cudaEventRecord(b));
+        KS_CUDA(cudaEventSynchronize(b));
+        float ms = 0;
+        KS_CUDA(cudaEventElapsedTime(&ms, a, b));
+        if (rep > 0 && ms < best) best = ms;
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    const double flops = (double)grid * 8 * (kIters / 32) * 4 * 4096.0;
+    *tflops = flops / (best * 1e-3) / 1e12;
+}
+
 static void run_peak(bool mma, double* tflops) {
     int sms = 148;
     int dev = 0;
@@ -142,9 +195,20 @@ static void run_peak(bool mma, double* tflops) {
 
 void fp64_peak_bench(double* tflops) { run_peak(false, tflops); }
 void fp64_peak_bench_mixed(double* tflops) { run_mixed(tflops); }
+void fp64_peak_bench_mma16(double* tflops) { run_mma16(tflops); }
 void fp64_peak_bench_mma(double* tflops) { run_peak(true, tflops); }
 
 } // namespace ks
+
+extern "C" int ks_fp64_peak_mma16(double* tflops) {
+    try {
+        ks::fp64_peak_bench_mma16(tflops);
+    } catch (const ks::Error& e) {
+        ks::set_last_error(e.what());
+        return e.code;
+    }
+    return KS_OK;
+}
 
 extern "C" int ks_fp64_peak_mixed(double* tflops) {
     try {
