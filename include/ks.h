@@ -195,6 +195,8 @@ int ks_fp64_peaks(double* dfma_tflops, double* dmma_tflops);
 int ks_fp64_peak_mixed(double* tflops);
 /* FP64 tensor-core throughput with the sm_90+ mma.sync m16n8k16 shape. */
 int ks_fp64_peak_mma16(double* tflops);
+/* DMMA (m8n8k4) throughput with `ctas_per_sm` CTAs of `threads` threads per SM. */
+int ks_fp64_dmma_occupancy(int ctas_per_sm, int threads, double* tflops);
 /* Which engine the spatial transforms use: 0 = DFMA, 1 = DMMA (env KS_GEMM). */
 int ks_transform_engine(void);
 /* Number of kernels the library launched since the last reset. */
@@ -227,6 +229,24 @@ int ks_fdshard_middle(ks_fdshard* h, ks_c64* work, void* stream);
 int ks_fdshard_backward(ks_fdshard* h, const ks_c64* recvbuf, ks_c64* z_slab, void* stream);
 int ks_fdshard_destroy(ks_fdshard* h);
 
+/* Sharded Kronecker operator: same slabs of the outermost axis; the input is
+ * the slab plus a halo of bw planes on each side (bw = widest band on that
+ * axis; the caller exchanges the halos with the neighbouring ranks):
+ * x_ext = x[ext_lo .. ext_hi) planes, y_slab = (K x)[lo .. hi). Destroy with
+ * ks_kron_destroy. */
+int ks_kronshard_create(int ndim, const int* dims, int nterms, const ks_term* terms,
+                        int nranks, int rank, int device, ks_kron** out);
+int ks_kronshard_plan(long long nd, int bw, int nranks, int rank, long long* lo, long long* hi,
+                      long long* ext_lo, long long* ext_hi); /* host-only */
+int ks_kronshard_sizes(const ks_kron* k, long long* lo, long long* hi, long long* ext_lo,
+                       long long* ext_hi, size_t* plane_elems);
+int ks_kronshard_apply(ks_kron* k, const ks_c64* x_ext, ks_c64* y_slab, void* stream);
+/* PCG building blocks on device vectors (sharded PCG): x += a p, r -= a q,
+ * *rr = local ||r||^2; and p = z + beta p. Both synchronise the stream. */
+int ks_cg_update(double alpha, const ks_c64* p, const ks_c64* q, ks_c64* x, ks_c64* r, size_t n,
+                 double* rr, void* stream);
+int ks_xpby(const ks_c64* z, double beta, ks_c64* p, size_t n, void* stream);
+
 /* ---------------------------------------------------------------------------
  * Host setup (product-side mirror of the reference's shared setup; used when
  * no reference process hands over its own setup products)
@@ -251,6 +271,9 @@ int ks_setup_eig(const ks_setup* s, int l, double* U, double* lambda);
 int ks_setup_create_fd(const ks_setup* s, int device, ks_fd** out);
 /* The system operator A as the reference's term list (assembly.cpp:202-251). */
 int ks_setup_create_system(const ks_setup* s, int device, ks_kron** out);
+/* The same operator sharded over nranks (ks_kronshard_*). */
+int ks_setup_create_system_sharded(const ks_setup* s, int nranks, int rank, int device,
+                                   ks_kron** out);
 int ks_setup_destroy(ks_setup* s);
 
 #ifdef __cplusplus

@@ -124,6 +124,7 @@ _SIGS = {
     "ks_fp64_peaks": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "ks_fp64_peak_mixed": (C.c_int, [C.POINTER(C.c_double)]),
     "ks_fp64_peak_mma16": (C.c_int, [C.POINTER(C.c_double)]),
+    "ks_fp64_dmma_occupancy": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "ks_transform_engine": (C.c_int, []),
     "ks_launch_count": (C.c_uint64, []),
     "ks_launch_count_reset": (None, []),
@@ -139,6 +140,17 @@ _SIGS = {
     "ks_fdshard_middle": (C.c_int, [_P, _P, _P]),
     "ks_fdshard_backward": (C.c_int, [_P, _P, _P, _P]),
     "ks_fdshard_destroy": (C.c_int, [_P]),
+    "ks_kronshard_create": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.c_int, C.POINTER(ks_term),
+                                      C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),
+    "ks_kronshard_sizes": (C.c_int, [_P, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong),
+                                     C.POINTER(C.c_longlong), C.POINTER(C.c_longlong),
+                                     C.POINTER(C.c_size_t)]),
+    "ks_kronshard_apply": (C.c_int, [_P, _P, _P, _P]),
+    "ks_kronshard_plan": (C.c_int, [C.c_longlong, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_longlong),
+                                    C.POINTER(C.c_longlong), C.POINTER(C.c_longlong),
+                                    C.POINTER(C.c_longlong)]),
+    "ks_cg_update": (C.c_int, [C.c_double, _P, _P, _P, _P, C.c_size_t, C.POINTER(C.c_double), _P]),
+    "ks_xpby": (C.c_int, [_P, C.c_double, _P, C.c_size_t, _P]),
     "ks_setup_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                   C.c_int, C.POINTER(_P)]),
     "ks_setup_dims": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
@@ -147,6 +159,7 @@ _SIGS = {
     "ks_setup_eig": (C.c_int, [_P, C.c_int, _P, _P]),
     "ks_setup_create_fd": (C.c_int, [_P, C.c_int, C.POINTER(_P)]),
     "ks_setup_create_system": (C.c_int, [_P, C.c_int, C.POINTER(_P)]),
+    "ks_setup_create_system_sharded": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),
     "ks_setup_destroy": (C.c_int, [_P]),
 }
 

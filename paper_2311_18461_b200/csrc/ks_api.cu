@@ -37,6 +37,7 @@ void kron_apply(KronPlan& P, const double2* x, double2* y, cudaStream_t st,
                 std::vector<void*>& host_ptrs);
 void kron_plan_info(const KronPlan& P, int* npasses, int* nnodes, int* nproducts);
 void kron_plan_free(KronPlan* p);
+void kron_plan_set_shard(KronPlan& P, int rows, int in_off, int band_off);
 struct KronPlanDeleter {
     void operator()(KronPlan* p) const { kron_plan_free(p); }
 };
@@ -89,6 +90,10 @@ struct ks_kron {
     int device = 0;
     std::vector<int> dims;
     size_t N = 0;
+    // sharded outermost axis: owned planes [lo, hi), haloed input [ext_lo, ext_hi)
+    bool sharded = false;
+    long long lo = 0, hi = 0, ext_lo = 0, ext_hi = 0;
+    size_t plane = 0;
     std::unique_ptr<KronPlan, KronPlanDeleter> plan;
     DevBuf io_x, io_y;
     std::vector<void*> hptrs;
@@ -475,9 +480,8 @@ int ks_fd_destroy(ks_fd* fd) {
 // ---------------------------------------------------------------------------
 // Kronecker operator
 // ---------------------------------------------------------------------------
-int ks_kron_create(int ndim, const int* dims, int nterms, const ks_term* terms, int device,
-                   ks_kron** out) {
-    API_BEGIN
+static void kron_create_impl(int ndim, const int* dims, int nterms, const ks_term* terms, int device,
+                             int nranks, int rank, ks_kron** out) {
     KS_REQUIRE(out && dims && ndim >= 1, KS_EINVAL, "ks_kron_create: bad arguments");
     KS_REQUIRE(nterms >= 0 && (nterms == 0 || terms), KS_EINVAL, "ks_kron_create: bad term list");
     for (int a = 0; a < ndim; ++a) KS_REQUIRE(dims[a] >= 1, KS_EINVAL, "CoeffTensor: dims must be positive");
@@ -520,11 +524,92 @@ int ks_kron_create(int ndim, const int* dims, int nterms, const ks_term* terms, 
     std::unique_ptr<ks_kron> k(new ks_kron());
     k->device = device;
     k->dims.assign(dims, dims + ndim);
+    std::vector<int> pdims = k->dims;
+    if (nranks > 0) {
+        // outermost axis split in slabs (same split as ks_shard_plan); halo = widest band on it
+        const int D = ndim - 1;
+        const long long nd = dims[D];
+        KS_REQUIRE(nranks <= nd && rank >= 0 && rank < nranks, KS_EINVAL, "bad rank / nranks");
+        const long long base = nd / nranks, rem = nd % nranks;
+        k->lo = rank * base + std::min<long long>(rank, rem);
+        k->hi = k->lo + base + (rank < rem ? 1 : 0);
+        int bwd = 0;
+        for (auto& t : fids)
+            if (t[D] >= 0) bwd = std::max(bwd, bbw[t[D]]);
+        KS_REQUIRE(nranks == 1 || k->hi - k->lo >= bwd, KS_EINVAL,
+                   "sharded matvec: slab thinner than the band (halo would span ranks)");
+        k->ext_lo = std::max<long long>(k->lo - bwd, 0);
+        k->ext_hi = std::min<long long>(k->hi + bwd, nd);
+        k->plane = 1;
+        for (int a = 0; a < D; ++a) k->plane *= (size_t)dims[a];
+        pdims[D] = (int)(k->ext_hi - k->ext_lo);
+        k->sharded = true;
+    }
     k->N = 1;
-    for (int a = 0; a < ndim; ++a) k->N *= (size_t)dims[a];
+    for (int a = 0; a < ndim; ++a) k->N *= (size_t)(k->sharded && a == ndim - 1 ? k->hi - k->lo : dims[a]);
     KS_CUDA(cudaStreamCreateWithFlags(&k->stream, cudaStreamNonBlocking));
-    k->plan.reset(kron_plan(k->dims, bands, bn, bbw, coeffs, fids));
+    k->plan.reset(kron_plan(pdims, bands, bn, bbw, coeffs, fids));
+    if (k->sharded && bbw.size() && pdims.back() != (int)(k->hi - k->lo))
+        kron_plan_set_shard(*k->plan, (int)(k->hi - k->lo), (int)(k->lo - k->ext_lo), (int)k->lo);
+    else if (k->sharded)
+        kron_plan_set_shard(*k->plan, (int)(k->hi - k->lo), 0, (int)k->lo);
     *out = k.release();
+}
+
+int ks_kron_create(int ndim, const int* dims, int nterms, const ks_term* terms, int device,
+                   ks_kron** out) {
+    API_BEGIN
+    kron_create_impl(ndim, dims, nterms, terms, device, 0, 0, out);
+    API_END
+}
+
+int ks_kronshard_create(int ndim, const int* dims, int nterms, const ks_term* terms, int nranks,
+                        int rank, int device, ks_kron** out) {
+    API_BEGIN
+    KS_REQUIRE(nranks >= 1, KS_EINVAL, "ks_kronshard_create: nranks >= 1");
+    kron_create_impl(ndim, dims, nterms, terms, device, nranks, rank, out);
+    API_END
+}
+
+// host-only slab + halo extents (same split as kron_create_impl)
+int ks_kronshard_plan(long long nd, int bw, int nranks, int rank, long long* lo, long long* hi,
+                      long long* ext_lo, long long* ext_hi) {
+    API_BEGIN
+    KS_REQUIRE(nranks >= 1 && nranks <= nd && rank >= 0 && rank < nranks && bw >= 0, KS_EINVAL,
+               "ks_kronshard_plan: bad arguments");
+    const long long base = nd / nranks, rem = nd % nranks;
+    const long long l = rank * base + std::min<long long>(rank, rem);
+    const long long h = l + base + (rank < rem ? 1 : 0);
+    KS_REQUIRE(nranks == 1 || h - l >= bw, KS_EINVAL, "sharded matvec: slab thinner than the band");
+    if (lo) *lo = l;
+    if (hi) *hi = h;
+    if (ext_lo) *ext_lo = std::max<long long>(l - bw, 0);
+    if (ext_hi) *ext_hi = std::min<long long>(h + bw, nd);
+    API_END
+}
+
+int ks_kronshard_sizes(const ks_kron* k, long long* lo, long long* hi, long long* ext_lo,
+                       long long* ext_hi, size_t* plane) {
+    API_BEGIN
+    KS_REQUIRE(k && k->sharded, KS_EINVAL, "ks_kronshard_sizes: not a sharded operator");
+    if (lo) *lo = k->lo;
+    if (hi) *hi = k->hi;
+    if (ext_lo) *ext_lo = k->ext_lo;
+    if (ext_hi) *ext_hi = k->ext_hi;
+    if (plane) *plane = k->plane;
+    API_END
+}
+
+// y_slab = (K x)[slab] from the haloed input x_ext = x[ext_lo .. ext_hi) (device pointers)
+int ks_kronshard_apply(ks_kron* k, const ks_c64* x_ext, ks_c64* y_slab, void* stream) {
+    API_BEGIN
+    KS_REQUIRE(k && k->sharded && x_ext && y_slab, KS_EINVAL, "ks_kronshard_apply: bad arguments");
+    std::lock_guard<std::mutex> lk(k->mu);
+    ensure_device(k->device);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : k->stream;
+    kron_apply(*k->plan, reinterpret_cast<const double2*>(x_ext), reinterpret_cast<double2*>(y_slab), st,
+               k->hptrs);
+    if (!stream) KS_CUDA(cudaStreamSynchronize(st));
     API_END
 }
 
@@ -731,6 +816,27 @@ int ks_norm2sq(const ks_c64* x, size_t n, double* out, void* stream) {
     launch_norm2sq(red, reinterpret_cast<const double2*>(x), n, static_cast<cudaStream_t>(stream));
     fetch(red, static_cast<cudaStream_t>(stream), 1);
     *out = red.host[0];
+    API_END
+}
+
+// PCG building blocks on device vectors (for the sharded PCG, dist.py)
+int ks_cg_update(double alpha, const ks_c64* p, const ks_c64* q, ks_c64* x, ks_c64* r, size_t n,
+                 double* rr, void* stream) {
+    API_BEGIN
+    KS_REQUIRE(rr, KS_EINVAL, "ks_cg_update: NULL rr");
+    Reducer red;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    launch_cg_update(red, alpha, reinterpret_cast<const double2*>(p), reinterpret_cast<const double2*>(q),
+                     reinterpret_cast<double2*>(x), reinterpret_cast<double2*>(r), n, st);
+    fetch(red, st, 1);
+    *rr = red.host[0];
+    API_END
+}
+int ks_xpby(const ks_c64* z, double beta, ks_c64* p, size_t n, void* stream) {
+    API_BEGIN
+    launch_xpby(reinterpret_cast<const double2*>(z), beta, reinterpret_cast<double2*>(p), n,
+                static_cast<cudaStream_t>(stream));
+    KS_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
     API_END
 }
 

@@ -38,7 +38,8 @@ struct SweepEntry {
 };
 bool launch_colsweep(int nin, int nout, int bw, const double2* const* ip, double2* const* op,
                      const int* in_begin, const SweepEntry* entries, const double2* rb,
-                     const int* freal, size_t ncols, size_t s, int n, int nmax, cudaStream_t st);
+                     const int* freal, size_t ncols, size_t s, int n, int nmax, cudaStream_t st,
+                     int nir = 0, int ioff = 0, int boff = 0);
 
 struct KronFactor {
     int n = 0, bw = 0;
@@ -72,6 +73,9 @@ struct KronPlan {
     std::vector<size_t> ptr_off;
     int nnodes = 0, nproducts = 0;
     int bwmax = 0, nmax = 1;
+    // sharded outermost axis (ks_kronshard_*): the last pass reads the haloed
+    // slab (dims.back() rows) and writes shard_rows owned planes
+    int shard_rows = 0, shard_in_off = 0, shard_band_off = 0;
     DevBuf d_rowband, d_freal; // v3: rb[f][r][dj] (width 2*bwmax+1), is_real[f]
 };
 
@@ -496,15 +500,23 @@ void kron_apply(KronPlan& P, const double2* x, double2* y, cudaStream_t st,
         size_t s = 1;
         for (int a = 0; a < ps.axis; ++a) s *= (size_t)P.dims[a];
         const int n = P.dims[ps.axis];
-        // smem column-tile kernel (all axes)
+        const bool shard_last = P.shard_rows > 0 && k + 1 == P.passes.size() &&
+                                ps.axis == (int)P.dims.size() - 1;
+        // element-parallel level kernel (all axes)
         if (ps.n_out <= 8 && P.bwmax >= 1 && P.bwmax <= 4) {
             auto ip = reinterpret_cast<const double2* const*>(dp + P.ptr_off[k]);
             auto op = reinterpret_cast<double2* const*>(const_cast<void**>(dp + P.ptr_off[k] + ps.n_in));
-            if (launch_colsweep(ps.n_in, ps.n_out, P.bwmax, ip, op, ps.d_in_begin.as<int>(),
-                                ps.d_entries.as<SweepEntry>(), P.d_rowband.as<double2>(),
-                                P.d_freal.as<int>(), P.N / (size_t)n, s, n, P.nmax, st))
-                continue;
+            const bool ok = shard_last
+                                ? launch_colsweep(ps.n_in, ps.n_out, P.bwmax, ip, op, ps.d_in_begin.as<int>(),
+                                                  ps.d_entries.as<SweepEntry>(), P.d_rowband.as<double2>(),
+                                                  P.d_freal.as<int>(), P.N / (size_t)n, s, P.shard_rows,
+                                                  P.nmax, st, n, P.shard_in_off, P.shard_band_off)
+                                : launch_colsweep(ps.n_in, ps.n_out, P.bwmax, ip, op, ps.d_in_begin.as<int>(),
+                                                  ps.d_entries.as<SweepEntry>(), P.d_rowband.as<double2>(),
+                                                  P.d_freal.as<int>(), P.N / (size_t)n, s, n, P.nmax, st);
+            if (ok) continue;
         }
+        KS_REQUIRE(!shard_last, KS_EINVAL, "sharded matvec: level shape not supported");
         // time axis (and any other shape): row-chunk sweep
         if (ps.n_out <= kMaxOut && P.bwmax >= 1 && P.bwmax <= 4) {
             const size_t ncols = P.N / (size_t)n;
@@ -545,5 +557,11 @@ void kron_apply(KronPlan& P, const double2* x, double2* y, cudaStream_t st,
 }
 
 void kron_plan_free(KronPlan* p) { delete p; }
+
+void kron_plan_set_shard(KronPlan& P, int rows, int in_off, int band_off) {
+    P.shard_rows = rows;
+    P.shard_in_off = in_off;
+    P.shard_band_off = band_off;
+}
 
 } // namespace ks

@@ -33,7 +33,10 @@ __global__ void __launch_bounds__(kTileThreads) k_kron_elem(
     const double2* const* __restrict__ in_ptrs, int n_in, double2* const* __restrict__ out_ptrs,
     const int* __restrict__ in_begin, const SweepEntry* __restrict__ entries,
     const double2* __restrict__ rb, const int* __restrict__ freal, size_t N, size_t s, int n,
-    int nmax, size_t nqt) {
+    int nmax, size_t nqt, int n_in_rows, int in_off, int band_off) {
+    // n = output rows of the pass axis; the input has n_in_rows rows and output
+    // row r reads input rows r + in_off - BW .. r + in_off + BW with band row
+    // band_off + r (sharded outermost axis: haloed slab in, owned planes out)
     constexpr int TAPS = 2 * BW + 1;
     size_t idx, q, o;
     int r;
@@ -55,7 +58,7 @@ __global__ void __launch_bounds__(kTileThreads) k_kron_elem(
         if (q >= s) return;
         idx = (o * (size_t)n + r) * s + q;
     }
-    const size_t base = o * (size_t)n * s + q;
+    const size_t base = o * (size_t)n_in_rows * s + q;
     const double2 Z = make_double2(0.0, 0.0);
     double2 acc[NOUT];
 #pragma unroll
@@ -65,8 +68,8 @@ __global__ void __launch_bounds__(kTileThreads) k_kron_elem(
         double2 w[TAPS];
 #pragma unroll
         for (int tp = 0; tp < TAPS; ++tp) {
-            const int rr = r - BW + tp;
-            w[tp] = (rr >= 0 && rr < n) ? __ldg(in + (size_t)rr * s) : Z;
+            const int rr = r + in_off - BW + tp;
+            w[tp] = (rr >= 0 && rr < n_in_rows) ? __ldg(in + (size_t)rr * s) : Z;
         }
         const int eb = __ldg(in_begin + j), ee = __ldg(in_begin + j + 1);
         for (int e = eb; e < ee; ++e) {
@@ -77,7 +80,7 @@ __global__ void __launch_bounds__(kTileThreads) k_kron_elem(
                 vr = w[BW].x;
                 vi = w[BW].y;
             } else {
-                const double2* band = rb + ((size_t)ef * nmax + r) * TAPS;
+                const double2* band = rb + ((size_t)ef * nmax + band_off + r) * TAPS;
                 vr = 0.0;
                 vi = 0.0;
                 if (__ldg(freal + ef)) {
@@ -117,12 +120,13 @@ __global__ void __launch_bounds__(kTileThreads) k_kron_elem(
 template <int NOUT>
 void launch_bw(int bw, unsigned grid, cudaStream_t st, const double2* const* ip, int nin,
                double2* const* op, const int* ib, const SweepEntry* en, const double2* rb,
-               const int* fr, size_t N, size_t s, int n, int nmax, size_t nqt) {
+               const int* fr, size_t N, size_t s, int n, int nmax, size_t nqt, int nir, int ioff,
+               int boff) {
     switch (bw) {
-    case 1: k_kron_elem<NOUT, 1><<<grid, kTileThreads, 0, st>>>(ip, nin, op, ib, en, rb, fr, N, s, n, nmax, nqt); break;
-    case 2: k_kron_elem<NOUT, 2><<<grid, kTileThreads, 0, st>>>(ip, nin, op, ib, en, rb, fr, N, s, n, nmax, nqt); break;
-    case 3: k_kron_elem<NOUT, 3><<<grid, kTileThreads, 0, st>>>(ip, nin, op, ib, en, rb, fr, N, s, n, nmax, nqt); break;
-    default: k_kron_elem<NOUT, 4><<<grid, kTileThreads, 0, st>>>(ip, nin, op, ib, en, rb, fr, N, s, n, nmax, nqt); break;
+    case 1: k_kron_elem<NOUT, 1><<<grid, kTileThreads, 0, st>>>(ip, nin, op, ib, en, rb, fr, N, s, n, nmax, nqt, nir, ioff, boff); break;
+    case 2: k_kron_elem<NOUT, 2><<<grid, kTileThreads, 0, st>>>(ip, nin, op, ib, en, rb, fr, N, s, n, nmax, nqt, nir, ioff, boff); break;
+    case 3: k_kron_elem<NOUT, 3><<<grid, kTileThreads, 0, st>>>(ip, nin, op, ib, en, rb, fr, N, s, n, nmax, nqt, nir, ioff, boff); break;
+    default: k_kron_elem<NOUT, 4><<<grid, kTileThreads, 0, st>>>(ip, nin, op, ib, en, rb, fr, N, s, n, nmax, nqt, nir, ioff, boff); break;
     }
 }
 
@@ -131,7 +135,9 @@ void launch_bw(int bw, unsigned grid, cudaStream_t st, const double2* const* ip,
 // returns false when the level's shape is outside the instantiated range
 bool launch_colsweep(int nin, int nout, int bw, const double2* const* ip, double2* const* op,
                      const int* in_begin, const SweepEntry* entries, const double2* rb,
-                     const int* freal, size_t ncols, size_t s, int n, int nmax, cudaStream_t st) {
+                     const int* freal, size_t ncols, size_t s, int n, int nmax, cudaStream_t st,
+                     int nir, int ioff, int boff) {
+    if (nir <= 0) nir = n;
     if (nout < 1 || nout > 8 || bw < 1 || bw > 4) return false;
     const size_t N = ncols * (size_t)n;
     size_t nqt = 0;
@@ -142,14 +148,14 @@ bool launch_colsweep(int nin, int nout, int bw, const double2* const* ip, double
         grid = (unsigned)(outer * nqt * (size_t)n);
     }
     switch (nout) {
-    case 1: launch_bw<1>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax, nqt); break;
-    case 2: launch_bw<2>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax, nqt); break;
-    case 3: launch_bw<3>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax, nqt); break;
-    case 4: launch_bw<4>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax, nqt); break;
-    case 5: launch_bw<5>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax, nqt); break;
-    case 6: launch_bw<6>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax, nqt); break;
-    case 7: launch_bw<7>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax, nqt); break;
-    case 8: launch_bw<8>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax, nqt); break;
+    case 1: launch_bw<1>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax, nqt, nir, ioff, boff); break;
+    case 2: launch_bw<2>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax, nqt, nir, ioff, boff); break;
+    case 3: launch_bw<3>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax, nqt, nir, ioff, boff); break;
+    case 4: launch_bw<4>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax, nqt, nir, ioff, boff); break;
+    case 5: launch_bw<5>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax, nqt, nir, ioff, boff); break;
+    case 6: launch_bw<6>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax, nqt, nir, ioff, boff); break;
+    case 7: launch_bw<7>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax, nqt, nir, ioff, boff); break;
+    case 8: launch_bw<8>(bw, grid, st, ip, nin, op, in_begin, entries, rb, freal, N, s, n, nmax, nqt, nir, ioff, boff); break;
     }
     check_launch("k_kron_elem");
     return true;

@@ -43,7 +43,26 @@ __global__ void __launch_bounds__(256) k_dmma_peak(double* out, double seed) {
     if (s == 12345.678) out[threadIdx.x] = s;
 }
 
-// m16n8k16 f64 (sm_90+ shape): 2048 FMA per warp instruction
+} // namespace
+__global__ void k_dmma_peak_pub(double* out, double seed) {
+    double c[8][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = seed + i;
+    const double a = 0.999 + threadIdx.x * 1e-9, b = 1e-3;
+    for (int it = 0; it < 2048 / 4; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                         : "+d"(c[i][0]), "+d"(c[i][1])
+                         : "d"(a), "d"(b));
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+    if (s == 12345.678) out[threadIdx.x] = s;
+}
+namespace {
+// m16n8k16 f64 (sm_90+ shape; ptxas lowers it to 8x DMMA.8x8x4 on sm_100a)
 __global__ void __launch_bounds__(256) k_dmma16_peak(double* out, double seed) {
     double c[4][4];
 #pragma unroll
@@ -199,6 +218,39 @@ void fp64_peak_bench_mma16(double* tflops) { run_mma16(tflops); }
 void fp64_peak_bench_mma(double* tflops) { run_peak(true, tflops); }
 
 } // namespace ks
+
+// DMMA throughput at a given number of resident warps per SM (grid = SMs x ctas)
+extern "C" int ks_fp64_dmma_occupancy(int ctas_per_sm, int threads, double* tflops) {
+    try {
+        int sms = 148, dev = 0;
+        KS_CUDA(cudaGetDevice(&dev));
+        KS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        ks::DevBuf out(1024 * sizeof(double));
+        const unsigned grid = sms * ctas_per_sm;
+        cudaEvent_t a, b;
+        KS_CUDA(cudaEventCreate(&a));
+        KS_CUDA(cudaEventCreate(&b));
+        float best = 1e30f;
+        for (int rep = 0; rep < 5; ++rep) {
+            KS_CUDA(cudaEventRecord(a));
+            ks::k_dmma_peak_pub<<<grid, threads>>>(out.as<double>(), 1.0);
+            ks::check_launch("k_dmma_peak");
+            KS_CUDA(cudaEventRecord(b));
+            KS_CUDA(cudaEventSynchronize(b));
+            float ms = 0;
+            KS_CUDA(cudaEventElapsedTime(&ms, a, b));
+            if (rep > 0 && ms < best) best = ms;
+        }
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        const double flops = (double)grid * (threads / 32) * (2048 / 4) * 8 * 512.0;
+        *tflops = flops / (best * 1e-3) / 1e12;
+    } catch (const ks::Error& e) {
+        ks::set_last_error(e.what());
+        return e.code;
+    }
+    return KS_OK;
+}
 
 extern "C" int ks_fp64_peak_mma16(double* tflops) {
     try {

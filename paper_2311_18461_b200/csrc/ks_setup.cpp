@@ -421,8 +421,18 @@ extern "C" int ks_setup_create_fd(const ks_setup* s, int device, ks_fd** out) {
                         s->Mt.a.data(), reinterpret_cast<const ks_c64*>(s->Wt.a.data()), device, out);
 }
 
+static int create_system(const ks_setup* s, int device, int nranks, int rank, ks_kron** out);
+
 // assemble_system (assembly.cpp:202-251), restricted (rs = DropBoth) branch
 extern "C" int ks_setup_create_system(const ks_setup* s, int device, ks_kron** out) {
+    return create_system(s, device, 0, 0, out);
+}
+extern "C" int ks_setup_create_system_sharded(const ks_setup* s, int nranks, int rank, int device,
+                                              ks_kron** out) {
+    return create_system(s, device, nranks, rank, out);
+}
+
+static int create_system(const ks_setup* s, int device, int nranks, int rank, ks_kron** out) {
     if (!s) return KS_EINVAL;
     const int d = s->d, D = d + 1;
     const double nu = s->nu;
@@ -501,6 +511,8 @@ extern "C" int ks_setup_create_system(const ks_setup* s, int device, ks_kron** o
         kt[t].factors = fp[t].data();
         kt[t].bw = bw[t].data();
     }
+    if (nranks > 0)
+        return ks_kronshard_create(D, s->dims.data(), (int)kt.size(), kt.data(), nranks, rank, device, out);
     return ks_kron_create(D, s->dims.data(), (int)kt.size(), kt.data(), device, out);
 }
 

@@ -487,132 +487,6 @@ k_mode_gemm_dmma2(const double* __restrict__ At, int n, const double* __restrict
     cp_async_wait<0>();
 }
 
-// m16n8k16 variant of v2 (TM even): acc[2i][m] holds C rows g, acc[2i+1][m] rows g+8
-template <int TM>
-__global__ void __launch_bounds__(kThreads, (TM <= 5 ? 2 : 1))
-k_mode_gemm_dmma4(const double* __restrict__ At, int n, const double* __restrict__ X,
-                  double* __restrict__ Y, ColMap M) {
-    constexpr int BM = 16 * TM;
-    constexpr int MT = TM;
-    constexpr int BMP = BM + 4; // == 4 (mod 16): conflict-free fragment loads
-    constexpr int BNP = kBN + 4;
-    extern __shared__ __align__(16) double smem[];
-    const int nk = (n + kBK - 1) / kBK;
-    double* As = smem;                          // [nk*kBK][BMP]
-    double* Bs = smem + (size_t)nk * kBK * BMP; // [kStages][kBK][BNP]
-    const long long in_rs = M.mode == MAP_TIN ? 2 * M.Np : 2 * M.s;
-    const long long out_rs = M.mode == MAP_TOUT ? 2 * M.Np : 2 * M.s;
-    const long long ntiles = M.ntiles;
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wr = warp & 1, wc = warp >> 1;
-
-    for (int e = tid; e < nk * kBK * BM; e += kThreads) {
-        const int j = e / BM, r = e - j * BM;
-        As[j * BMP + r] = (j < n && r < n) ? __ldg(At + (long long)j * n + r) : 0.0;
-    }
-
-    const int lcp = tid & 63, lrow0 = tid >> 6;
-    const int my_tiles =
-        ntiles > (long long)blockIdx.x ? (int)((ntiles - 1 - (long long)blockIdx.x) / gridDim.x + 1) : 0;
-    const int nwork = my_tiles * nk;
-    long long cur_tile = -1, cur_in = 0;
-    bool cur_valid = false;
-
-    auto issue = [&](int w) {
-        if (w < nwork) {
-            const int wt = w / nk;
-            const long long tile = (long long)blockIdx.x + (long long)wt * gridDim.x;
-            const int kc = w - wt * nk;
-            if (tile != cur_tile) {
-                long long dummy;
-                cur_valid = colmap(M, n, tile_base(M, tile), lcp, cur_in, dummy);
-                cur_tile = tile;
-            }
-            double* bs = Bs + (size_t)(w % kStages) * kBK * BNP;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int jj = lrow0 + 4 * k, j = kc * kBK + jj;
-                const bool v = cur_valid && j < n;
-                cp_async16(bs + jj * BNP + 2 * lcp,
-                           v ? (const void*)(X + cur_in + (long long)j * in_rs) : (const void*)X, v);
-            }
-        }
-        cp_async_commit();
-    };
-
-    double acc[MT][4][2];
-#pragma unroll
-    for (int i = 0; i < MT; ++i)
-#pragma unroll
-        for (int m = 0; m < 4; ++m) acc[i][m][0] = acc[i][m][1] = 0.0;
-
-#pragma unroll
-    for (int s = 0; s < kStages - 1; ++s) issue(s);
-
-    const int r_warp = wr * (BM / 2), c_warp = wc * 32;
-    const int ar = lane >> 2, ak = lane & 3;
-    const int cr = lane >> 2;
-    for (int w = 0; w < nwork; ++w) {
-        cp_async_wait<kStages - 2>();
-        __syncthreads();
-        issue(w + kStages - 1);
-        const int kc = w % nk;
-        const double* bs = Bs + (size_t)(w % kStages) * kBK * BNP;
-        const double* as = As + (size_t)kc * kBK * BMP;
-        if constexpr (TM % 2 == 0) {
-            // one m16n8k16 step per k-chunk: A frag a_q = A[g (+8)][t + 4q'], B frag b_q = B[t + 4q][g]
-            constexpr int M16 = MT / 2; // m16 tiles per warp
-            double a[M16][8], b[4][4];
-#pragma unroll
-            for (int i = 0; i < M16; ++i)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    a[i][2 * q] = as[(ak + 4 * q) * BMP + r_warp + i * 16 + ar];
-                    a[i][2 * q + 1] = as[(ak + 4 * q) * BMP + r_warp + i * 16 + 8 + ar];
-                }
-#pragma unroll
-            for (int m = 0; m < 4; ++m)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) b[m][q] = bs[(ak + 4 * q) * BNP + c_warp + m * 8 + ar];
-#pragma unroll
-            for (int i = 0; i < M16; ++i)
-#pragma unroll
-                for (int m = 0; m < 4; ++m)
-                    asm volatile(
-                        "mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, "
-                        "{%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};\n"
-                        : "+d"(acc[2 * i][m][0]), "+d"(acc[2 * i][m][1]), "+d"(acc[2 * i + 1][m][0]),
-                          "+d"(acc[2 * i + 1][m][1])
-                        : "d"(a[i][0]), "d"(a[i][1]), "d"(a[i][2]), "d"(a[i][3]), "d"(a[i][4]),
-                          "d"(a[i][5]), "d"(a[i][6]), "d"(a[i][7]), "d"(b[m][0]), "d"(b[m][1]),
-                          "d"(b[m][2]), "d"(b[m][3]));
-        }
-        if (kc == nk - 1) {
-            const long long tile = (long long)blockIdx.x + (long long)(w / nk) * gridDim.x;
-            const TileBase tbase = tile_base(M, tile);
-#pragma unroll
-            for (int m = 0; m < 4; ++m) {
-                const int jcol = (c_warp >> 1) + m * 4 + (lane & 3); // complex column in tile
-                long long io, oo;
-                if (colmap(M, n, tbase, jcol, io, oo)) {
-                    double* yb = Y + oo;
-#pragma unroll
-                    for (int i = 0; i < MT; ++i) {
-                        const int r = r_warp + i * 8 + cr;
-                        if (r < n)
-                            *reinterpret_cast<double2*>(yb + (long long)r * out_rs) =
-                                make_double2(acc[i][m][0], acc[i][m][1]);
-                    }
-                }
-#pragma unroll
-                for (int i = 0; i < MT; ++i) acc[i][m][0] = acc[i][m][1] = 0.0;
-            }
-        }
-    }
-    cp_async_wait<0>();
-}
-
 // ---------------------------------------------------------------------------
 // DMMA engine v3 (small axes, n <= 80): the whole K extent of a column tile is
 // one cp.async group (two tile buffers), so per synchronisation a warp issues
@@ -745,24 +619,6 @@ void launch_tm(int engine, const double* At, int n, const double* X, double* Y, 
         const unsigned g3 = (unsigned)std::min<long long>(Mm.ntiles, (long long)sms);
         k_mode_gemm_dmma3<TM><<<g3, kThreads, sm, st>>>(At, n, X, Y, Mm);
         check_launch("k_mode_gemm_dmma3");
-    } else if (engine == 2 && (TM % 2 == 0) && !std::getenv("KS_GEMM_V2")) {
-        const int nk = (n + kBK - 1) / kBK;
-        const size_t sm = ((size_t)nk * kBK * (16 * TM + 4) + (size_t)kStages * kBK * (kBN + 4)) *
-                          sizeof(double);
-        static int sms = 0;
-        if (!sms) {
-            int dev = 0;
-            KS_CUDA(cudaGetDevice(&dev));
-            KS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-            KS_CUDA(cudaFuncSetAttribute(k_mode_gemm_dmma4<TM>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        }
-        KS_REQUIRE(sm <= 227 * 1024, KS_EINVAL, "mode product: axis too long for the resident-A kernel");
-        const int per_sm = (TM <= 5 && 2 * sm <= 227 * 1024) ? 2 : 1;
-        ColMap M = *map;
-        const unsigned g2 = (unsigned)std::min<long long>(M.ntiles, (long long)sms * per_sm);
-        k_mode_gemm_dmma4<TM><<<g2, kThreads, sm, st>>>(At, n, X, Y, M);
-        check_launch("k_mode_gemm_dmma4");
     } else if (engine == 2) {
         const int nk = (n + kBK - 1) / kBK;
         const size_t sm = ((size_t)nk * kBK * (16 * TM + 4) + (size_t)kStages * kBK * (kBN + 4)) *

@@ -21,6 +21,7 @@ from typing import Callable, List, Optional, Sequence
 import numpy as np
 
 from . import _check, _cvec, _ptr, lib
+from . import ks_c64 as _C64
 
 
 def shard_plan(d: int, dims: Sequence[int], nranks: int, rank: int) -> dict:
@@ -100,3 +101,179 @@ class ShardedFDPreconditioner:
                 self._h = None
         except Exception:
             pass
+
+
+# ---------------------------------------------------------------------------
+# sharded Kronecker-sum matvec: halo exchange of bw planes with the neighbours
+# ---------------------------------------------------------------------------
+def kron_shard_plan(n_d: int, bw: int, nranks: int, rank: int):
+    """Host-only: owned planes [lo, hi) and haloed input [ext_lo, ext_hi) of a rank."""
+    LL = C.c_longlong
+    v = [LL() for _ in range(4)]
+    _check(lib().ks_kronshard_plan(n_d, bw, nranks, rank, *[C.byref(x) for x in v]))
+    return tuple(x.value for x in v)
+
+
+def halo_exchange(ext, slab, plane, lo, hi, ext_lo, ext_hi, rank, nranks, send, recv):
+    """Fill ext = [halo_lo | slab | halo_hi] from the neighbours: rank-1 sends its
+    last (lo - ext_lo) planes, rank+1 its first (ext_hi - hi) planes; we send
+    them the planes their halos need (bw each, the same width on both sides of
+    an interior boundary). send/recv are point-to-point callables
+    (tensor, peer) -> request-like; the default is NCCL via torch.distributed."""
+    n_lo, n_hi = lo - ext_lo, ext_hi - hi
+    bw = max(n_lo, n_hi)
+    reqs = []
+    if rank > 0:
+        reqs.append(recv(ext[:n_lo * plane], rank - 1))
+        reqs.append(send(slab[:bw * plane].contiguous(), rank - 1))
+    if rank < nranks - 1:
+        reqs.append(recv(ext[ext.numel() - n_hi * plane:], rank + 1))
+        reqs.append(send(slab[slab.numel() - bw * plane:].contiguous(), rank + 1))
+    for r in reqs:
+        if r is not None:
+            r.wait()
+
+
+def _nccl_p2p():
+    import torch.distributed as dist
+    return (lambda t, peer: dist.isend(t, peer)), (lambda t, peer: dist.irecv(t, peer))
+
+
+class ShardedKroneckerOperator:
+    """The system operator A (assembly.cpp:202-251) slab-sharded like the FD
+    preconditioner: apply(x_slab) -> y_slab after a halo exchange."""
+
+    def __init__(self, prob, nranks: Optional[int] = None, rank: Optional[int] = None,
+                 device: int = 0, halo: Optional[Callable] = None):
+        import torch
+        if nranks is None or rank is None:
+            import torch.distributed as dist
+            nranks, rank = dist.get_world_size(), dist.get_rank()
+        self.nranks, self.rank, self.device = nranks, rank, device
+        h = C.c_void_p()
+        _check(lib().ks_setup_create_system_sharded(prob._h, nranks, rank, device, C.byref(h)))
+        self._h = h
+        lo, hi, elo, ehi = (C.c_longlong() for _ in range(4))
+        plane = C.c_size_t()
+        _check(lib().ks_kronshard_sizes(h, C.byref(lo), C.byref(hi), C.byref(elo), C.byref(ehi),
+                                        C.byref(plane)))
+        self.lo, self.hi, self.ext_lo, self.ext_hi = lo.value, hi.value, elo.value, ehi.value
+        self.plane = plane.value
+        self.n_lo, self.n_hi = self.lo - self.ext_lo, self.ext_hi - self.hi
+        self._ext = torch.empty((self.ext_hi - self.ext_lo) * self.plane, dtype=torch.complex128,
+                                device=torch.device("cuda", device))
+        self._halo = halo
+
+    def apply(self, x_slab, y_slab=None):
+        import torch
+        if y_slab is None:
+            y_slab = torch.empty_like(x_slab)
+        a, b = self.n_lo * self.plane, self.n_lo * self.plane + x_slab.numel()
+        self._ext[a:b].copy_(x_slab)
+        send, recv = self._halo if self._halo is not None else _nccl_p2p()
+        halo_exchange(self._ext, x_slab, self.plane, self.lo, self.hi, self.ext_lo, self.ext_hi,
+                      self.rank, self.nranks, send, recv)
+        st = C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+        _check(lib().ks_kronshard_apply(self._h, C.c_void_p(self._ext.data_ptr()),
+                                        C.c_void_p(y_slab.data_ptr()), st))
+        return y_slab
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().ks_kron_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------------------
+# sharded PCG: krylov.cpp:24-114 control flow, local BLAS-1 in libks, global
+# sums by all-reduce
+# ---------------------------------------------------------------------------
+def sharded_pcg(apply_a, apply_p, b_slab, tol=1e-8, maxit=200, strict=False, allreduce=None):
+    """PCG over slab-sharded vectors. apply_a / apply_p map a torch slab to a
+    torch slab (the sharded operators); allreduce sums a python float over ranks
+    (default: torch.distributed NCCL)."""
+    import torch
+    if allreduce is None:
+        import torch.distributed as dist
+
+        def allreduce(v):
+            t = torch.tensor([v], dtype=torch.float64, device=b_slab.device)
+            dist.all_reduce(t)
+            return float(t.item())
+    if not (tol > 0) or maxit < 0:
+        raise ValueError("pcg: bad options")
+    L = lib()
+    n = b_slab.numel()
+    st = C.c_void_p(torch.cuda.current_stream(b_slab.device).cuda_stream)
+    ptr = lambda t: C.c_void_p(t.data_ptr())
+
+    def dot_re(x, y):
+        out = _C64()
+        torch.cuda.synchronize(b_slab.device)
+        _check(L.ks_dotc(ptr(x), ptr(y), n, C.byref(out), st))
+        return allreduce(out.re)
+
+    def norm2(x):
+        v = C.c_double()
+        torch.cuda.synchronize(b_slab.device)
+        _check(L.ks_norm2sq(ptr(x), n, C.byref(v), st))
+        return allreduce(v.value)
+
+    x = torch.zeros_like(b_slab)
+    hist = []
+    bnorm = norm2(b_slab) ** 0.5
+    rep = {"x": x, "iterations": 0, "res_history": hist, "converged": False, "breakdown": False}
+    if bnorm == 0.0:
+        rep["converged"] = True
+        return rep
+
+    def true_relres():
+        s = apply_a(x)
+        s.sub_(b_slab)
+        return norm2(s) ** 0.5 / bnorm, s
+
+    r = b_slab.clone()
+    z = apply_p(r) if apply_p else r.clone()
+    p = z.clone()
+    rho = dot_re(r, z)
+    restarts = 0
+    for _ in range(maxit):
+        q = apply_a(p)
+        curv = dot_re(p, q)
+        if curv <= 0.0:
+            rep["breakdown"] = True
+            break
+        alpha = rho / curv
+        rr = C.c_double()
+        torch.cuda.synchronize(b_slab.device)
+        _check(L.ks_cg_update(alpha, ptr(p), ptr(q), ptr(x), ptr(r), n, C.byref(rr), st))
+        rep["iterations"] += 1
+        relres = allreduce(rr.value) ** 0.5 / bnorm
+        if strict:
+            relres, _ = true_relres()
+        hist.append(relres)
+        if relres <= tol:
+            if not strict:
+                tr, s = true_relres()
+                hist[-1] = tr
+                if tr > tol:
+                    restarts += 1
+                    if restarts > 2:
+                        break
+                    r = -s
+                    z = apply_p(r) if apply_p else r.clone()
+                    p = z.clone()
+                    rho = dot_re(r, z)
+                    continue
+            rep["converged"] = True
+            break
+        z = apply_p(r) if apply_p else r.clone()
+        rho_new = dot_re(r, z)
+        beta = rho_new / rho
+        rho = rho_new
+        torch.cuda.synchronize(b_slab.device)
+        _check(L.ks_xpby(ptr(z), beta, ptr(p), n, st))
+    return rep

@@ -138,3 +138,75 @@ def test_shard_plan_counts(ks):
         assert tot_send == 131 * 130 ** 3
     with pytest.raises(ks.InvalidArgument):
         shard_plan(1, [66, 65], 2, 0)  # d = 1 cannot re-shard axes 1..d-1
+
+
+def _halo_worker(rank, ws, port, d, p, n_el, q):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import torch
+    import torch.distributed as dist
+    import paper_2311_18461_b200 as ks
+    from paper_2311_18461_b200.dist import kron_shard_plan, halo_exchange
+    from oracle import oracle as O
+    from helpers import setup_arrays
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=ws)
+        a = setup_arrays(ks, d, p, n_el, n_el)
+        dims = a["dims"]
+        plane = int(np.prod(dims[:d]))
+        lo, hi, elo, ehi = kron_shard_plan(dims[d], p, ws, rank)
+        K = O.OracleKron(dims, O.system_terms(a, d, 1.0))
+        x = O.random_vec(K.N, 99)
+        xs = torch.from_numpy(x[lo * plane: hi * plane].copy())
+        ext = torch.zeros((ehi - elo) * plane, dtype=torch.complex128)
+        ext[(lo - elo) * plane:(lo - elo) * plane + xs.numel()] = xs
+        send = lambda t, peer: dist.isend(torch.view_as_real(t).reshape(-1), peer)
+        recv = lambda t, peer: _Recv(t, peer)
+        halo_exchange(ext, xs, plane, lo, hi, elo, ehi, rank, ws, send, recv)
+        # y[lo:hi] depends only on x[ext_lo:ext_hi] (banded outermost factors): zero elsewhere
+        xg = np.zeros(K.N, dtype=np.complex128)
+        xg[elo * plane: ehi * plane] = ext.numpy()
+        y_slab = K.apply(xg)[lo * plane: hi * plane]
+        gathered = [None] * ws
+        dist.all_gather_object(gathered, y_slab)
+        if rank == 0:
+            y = np.concatenate(gathered)
+            yo = K.apply(x)
+            q.put(float(np.linalg.norm(y - yo) / np.linalg.norm(yo)))
+        dist.destroy_process_group()
+    except Exception as e:
+        q.put(repr(e))
+        raise
+
+
+class _Recv:
+    """gloo recv into a complex tensor view (irecv + copy back on wait)."""
+
+    def __init__(self, t, peer):
+        import torch.distributed as dist
+        self.t = t
+        self.buf = torch_view = __import__("torch").empty(t.numel() * 2, dtype=__import__("torch").float64)
+        self.req = dist.irecv(torch_view, peer)
+
+    def wait(self):
+        import torch
+        self.req.wait()
+        self.t.copy_(torch.view_as_complex(self.buf.view(-1, 2)))
+
+
+@pytest.mark.parametrize("ws,d,p,n_el", [(2, 2, 2, 8), (3, 3, 2, 6), (2, 3, 3, 6)])
+def test_sharded_matvec_halo_gloo(ws, d, p, n_el):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_halo_worker, args=(k, ws, port, d, p, n_el, q)) for k in range(ws)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(timeout=240)
+    res = q.get(timeout=10)
+    assert not isinstance(res, str), res
+    assert res < 1e-14

@@ -98,3 +98,58 @@ def test_sharded_class_single_rank_nccl(gpu, oracle):
         assert rel(z, single.apply(r)) < 1e-12
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("P,d,p,n_el", [(2, 2, 3, 10), (3, 3, 2, 8), (4, 3, 4, 16)])
+def test_sharded_matvec_virtual_ranks(gpu, oracle, P, d, p, n_el):
+    ks = gpu
+    L = ks.lib()
+    prob = ks.SpaceTimeProblem.uniform(d, p, n_el, n_el)
+    dims = prob.reduced_dims()
+    plane = int(np.prod(dims[:d]))
+    A = ks.assemble_system_operator(prob)
+    x = oracle.random_vec(prob.N_dof, 5)
+    y_ref = A.apply(x)
+    ys = []
+    for k in range(P):
+        h = C.c_void_p()
+        ks._check(L.ks_setup_create_system_sharded(prob._h, P, k, 0, C.byref(h)))
+        lo, hi, elo, ehi = (C.c_longlong() for _ in range(4))
+        pl = C.c_size_t()
+        ks._check(L.ks_kronshard_sizes(h, C.byref(lo), C.byref(hi), C.byref(elo), C.byref(ehi), C.byref(pl)))
+        assert pl.value == plane
+        xe = ks.DeviceVector.from_host(x[elo.value * plane: ehi.value * plane])  # emulated halo exchange
+        yk = ks.DeviceVector((hi.value - lo.value) * plane)
+        ks._check(L.ks_kronshard_apply(h, xe.ptr, yk.ptr, None))
+        ys.append(yk.to_host())
+        L.ks_kron_destroy(h)
+    assert rel(np.concatenate(ys), y_ref) < 1e-13
+
+
+def test_sharded_pcg_single_rank_nccl(gpu, oracle):
+    """dist.sharded_pcg with the sharded operators over a 1-rank NCCL group
+    matches the device-resident ks_pcg."""
+    import os
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_2311_18461_b200.dist import (ShardedFDPreconditioner, ShardedKroneckerOperator,
+                                            sharded_pcg)
+    ks = gpu
+    a = setup_arrays(ks, 3, 2, 12, 12)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        S = ShardedFDPreconditioner(a["dims"], 1.0, 2, a["U"], a["lam"], a["Lt"], a["Mt"], a["Wt"])
+        A = ShardedKroneckerOperator(a["prob"])
+        b = oracle.random_vec(int(np.prod(a["dims"])), 1234)
+        rep = sharded_pcg(A.apply, S.apply, torch.from_numpy(b).cuda())
+        ref = ks.pcg(ks.assemble_system_operator(a["prob"]), ks.FDPreconditioner(a["prob"]), b)
+        assert rep["converged"] and abs(rep["iterations"] - ref.iterations) <= 1
+        assert rel(rep["x"].cpu().numpy(), ref.x) < 1e-7
+    finally:
+        dist.destroy_process_group()
