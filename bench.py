@@ -248,6 +248,20 @@ def run_sharded(args, rank, ws, local, dist):
     clk.__exit__(None, None, None)
     ms = max_over_ranks(dist, ms)
     e2e = max_over_ranks(dist, e2e)
+    # full sharded solve to 1e-8 (sharded matvec with halo exchange + sharded FD + all-reduce dots)
+    solves = {}
+    if not args.no_solve:
+        from paper_2311_18461_b200.dist import ShardedKroneckerOperator, sharded_pcg
+        A = ShardedKroneckerOperator(prob, device=local)
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        rep = sharded_pcg(A.apply, S.apply, r, 1e-8, 200)
+        torch.cuda.synchronize()
+        sec = max_over_ranks(dist, time.perf_counter() - t0)
+        solves[f"solve_{args.config}"] = {"iterations": rep["iterations"], "converged": rep["converged"],
+                                          "seconds": sec,
+                                          "final_relres": rep["res_history"][-1] if rep["res_history"] else None}
     if rank == 0:
         print(json.dumps({
             "metric": "fd_apply_dof_per_s", "value": n / (ms * 1e-3), "unit": "DOF/s", "n_gpus": ws,
@@ -258,7 +272,8 @@ def run_sharded(args, rank, ws, local, dist):
                        "dims": dims, "dofs": n, "parallelism": f"slab{ws} (axis {d}) + 2x NCCL all-to-all"},
             "e2e": {"value": n / e2e, "unit": "DOF/s", "h2d_bytes_per_step": int(r_host.nbytes) * ws,
                     "d2h_bytes_per_step": int(r_host.nbytes) * ws, "ms_per_step": e2e * 1e3},
-            "gpu_launches": launches, "roofline": None, "clocks": clk.summary(), "cpu_baseline": None}),
+            "gpu_launches": launches, "roofline": None, "clocks": clk.summary(), "cpu_baseline": None,
+            "solves": solves}),
             flush=True)
     dist.destroy_process_group()
 
