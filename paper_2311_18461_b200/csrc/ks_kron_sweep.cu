@@ -15,6 +15,8 @@
 // algorithmic bytes but ran at 12-17% occupancy, 2-4x slower.)
 #include "ks_internal.hpp"
 
+#include <cstdlib>
+
 namespace ks {
 
 struct SweepEntry {
@@ -117,6 +119,161 @@ __global__ void __launch_bounds__(kTileThreads) k_kron_elem(
     for (int a = 0; a < NOUT; ++a) out_ptrs[a][idx] = acc[a];
 }
 
+// ---------------------------------------------------------------------------
+// Tile kernel: a CTA owns kTQ = 8 consecutive columns (o, q) and the FULL axis
+// (rows r = 0..n-1, RPT per thread, 32 row groups), so banded products are
+// local. Input nodes are staged in shared memory one after another through a
+// two-buffer cp.async pipeline (input j+1 loads while input j is consumed);
+// rows are padded with BW zero rows so the tap loops have no branches.
+// ---------------------------------------------------------------------------
+constexpr int kTQ = 8, kRG = 32;
+
+__device__ __forceinline__ void cpa16(void* dst, const void* src, bool v) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(v ? 16 : 0));
+}
+
+template <int NOUT, int BW, int RPT>
+__global__ void __launch_bounds__(kTileThreads) k_kron_tile2(
+    const double2* const* __restrict__ in_ptrs, int n_in, double2* const* __restrict__ out_ptrs,
+    const int* __restrict__ in_begin, const SweepEntry* __restrict__ entries,
+    const double2* __restrict__ rb, const int* __restrict__ freal, size_t ncols, size_t s, int n,
+    int nmax, int n_in_rows, int in_off, int band_off) {
+    constexpr int TAPS = 2 * BW + 1, PITCH = kTQ + 1;
+    extern __shared__ __align__(16) double2 tl[]; // [2][n_in_rows + 2BW][PITCH]
+    const int rows_p = n_in_rows + 2 * BW;
+    const int tid = threadIdx.x, cc = tid % kTQ, rg = tid / kTQ;
+    const size_t c0 = (size_t)blockIdx.x * kTQ;
+    const int ncol = (int)min((size_t)kTQ, ncols - c0);
+    const double2 Z = make_double2(0.0, 0.0);
+    for (int e = tid; e < BW * PITCH; e += kTileThreads) // zero halo rows of both buffers
+        for (int b = 0; b < 2; ++b) {
+            tl[b * rows_p * PITCH + e] = Z;
+            tl[b * rows_p * PITCH + (n_in_rows + BW) * PITCH + e] = Z;
+        }
+    auto issue = [&](int j, int b) {
+        if (j < n_in) {
+            const double2* __restrict__ in = in_ptrs[j];
+            double2* t = tl + (size_t)b * rows_p * PITCH + BW * PITCH;
+            const int tot = n_in_rows * kTQ;
+            for (int e = tid; e < tot; e += kTileThreads) {
+                int r, c;
+                if (s == 1) { c = e / n_in_rows; r = e - c * n_in_rows; } // fibers contiguous
+                else { r = e / kTQ; c = e - r * kTQ; }                    // q contiguous
+                const bool v = c < ncol;
+                const size_t cm = c0 + c;
+                const size_t oo = cm / s, qq = cm - oo * s;
+                const double2* src = in + oo * (size_t)n_in_rows * s + (size_t)r * s + qq;
+                cpa16(t + r * PITCH + c, v ? (const void*)src : (const void*)in, v);
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    };
+    double2 acc[NOUT][RPT];
+#pragma unroll
+    for (int a = 0; a < NOUT; ++a)
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) acc[a][k] = Z;
+    issue(0, 0);
+    for (int j = 0; j < n_in; ++j) {
+        issue(j + 1, (j + 1) & 1);
+        asm volatile("cp.async.wait_group 1;\n" ::);
+        __syncthreads();
+        const double2* t = tl + (size_t)(j & 1) * rows_p * PITCH + cc;
+        // window of the RPT rows' taps: input rows r + in_off - BW .. (padded index r + in_off)
+        const int eb = in_begin[j], ee = in_begin[j + 1];
+        for (int e = eb; e < ee; ++e) {
+            const SweepEntry en = entries[e];
+            double2 v[RPT];
+#pragma unroll
+            for (int k = 0; k < RPT; ++k) {
+                const int r = rg + k * kRG;
+                v[k] = Z;
+                if (r < n) {
+                    const double2* w = t + (r + in_off) * PITCH; // padded row r+in_off-BW+BW
+                    if (en.factor < 0) {
+                        v[k] = w[BW * PITCH];
+                    } else {
+                        const double2* band = rb + ((size_t)en.factor * nmax + band_off + r) * TAPS;
+                        double vr = 0.0, vi = 0.0;
+                        if (freal[en.factor]) {
+#pragma unroll
+                            for (int tp = 0; tp < TAPS; ++tp) {
+                                const double a = __ldg(&band[tp].x);
+                                const double2 x = w[tp * PITCH];
+                                vr = fma(a, x.x, vr);
+                                vi = fma(a, x.y, vi);
+                            }
+                        } else {
+#pragma unroll
+                            for (int tp = 0; tp < TAPS; ++tp) {
+                                const double2 a = __ldg(&band[tp]);
+                                const double2 x = w[tp * PITCH];
+                                vr = fma(a.x, x.x, fma(-a.y, x.y, vr));
+                                vi = fma(a.x, x.y, fma(a.y, x.x, vi));
+                            }
+                        }
+                        v[k] = make_double2(vr, vi);
+                    }
+                }
+            }
+            const double cr = en.coeff.x, ci = en.coeff.y;
+            switch (en.out) {
+#define KS_ACC(OO)                                                                 \
+    case OO:                                                                       \
+        if (OO < NOUT) {                                                           \
+            _Pragma("unroll") for (int k = 0; k < RPT; ++k) {                      \
+                double2& A = acc[OO < NOUT ? OO : 0][k];                           \
+                A.x = fma(cr, v[k].x, fma(-ci, v[k].y, A.x));                      \
+                A.y = fma(cr, v[k].y, fma(ci, v[k].x, A.y));                       \
+            }                                                                      \
+        }                                                                          \
+        break;
+                KS_ACC(0) KS_ACC(1) KS_ACC(2) KS_ACC(3) KS_ACC(4) KS_ACC(5) KS_ACC(6) KS_ACC(7)
+#undef KS_ACC
+            }
+        }
+        __syncthreads(); // buffer j&1 is refilled by the next iteration's issue
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    if (cc >= ncol) return;
+    const size_t cme = c0 + cc;
+    const size_t o = cme / s, q = cme - o * s;
+    const size_t base = o * (size_t)n * s + q;
+#pragma unroll
+    for (int a = 0; a < NOUT; ++a) {
+        double2* __restrict__ out = out_ptrs[a];
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) {
+            const int r = rg + k * kRG;
+            if (r < n) out[base + (size_t)r * s] = acc[a][k];
+        }
+    }
+}
+
+template <int NOUT, int BW>
+bool launch_tile2(int rpt, unsigned grid, size_t sm, cudaStream_t st, const double2* const* ip, int nin,
+                  double2* const* op, const int* ib, const SweepEntry* en, const double2* rb,
+                  const int* fr, size_t ncols, size_t s, int n, int nmax, int nir, int ioff, int boff) {
+#define KS_T2(R)                                                                                        \
+    case R: {                                                                                           \
+        static bool attr = false;                                                                       \
+        if (!attr) {                                                                                    \
+            KS_CUDA(cudaFuncSetAttribute(k_kron_tile2<NOUT, BW, R>,                                     \
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));     \
+            attr = true;                                                                                \
+        }                                                                                               \
+        k_kron_tile2<NOUT, BW, R><<<grid, kTileThreads, sm, st>>>(ip, nin, op, ib, en, rb, fr, ncols, s, \
+                                                                  n, nmax, nir, ioff, boff);            \
+        return true;                                                                                    \
+    }
+    switch (rpt) {
+        KS_T2(1) KS_T2(2) KS_T2(3) KS_T2(4) KS_T2(5)
+    }
+#undef KS_T2
+    return false;
+}
+
 template <int NOUT>
 void launch_bw(int bw, unsigned grid, cudaStream_t st, const double2* const* ip, int nin,
                double2* const* op, const int* ib, const SweepEntry* en, const double2* rb,
@@ -139,6 +296,27 @@ bool launch_colsweep(int nin, int nout, int bw, const double2* const* ip, double
                      int nir, int ioff, int boff) {
     if (nir <= 0) nir = n;
     if (nout < 1 || nout > 8 || bw < 1 || bw > 4) return false;
+    const int rpt = (n + kRG - 1) / kRG;
+    if (rpt <= 5 && !std::getenv("KS_KRON_ELEM")) {
+        const size_t sm = (size_t)2 * (nir + 2 * bw) * (kTQ + 1) * sizeof(double2);
+        const unsigned g = (unsigned)((ncols + kTQ - 1) / kTQ);
+        bool ok = false;
+#define KS_T2B(NO)                                                                               \
+    case NO:                                                                                     \
+        switch (bw) {                                                                            \
+        case 1: ok = launch_tile2<NO, 1>(rpt, g, sm, st, ip, nin, op, in_begin, entries, rb, freal, ncols, s, n, nmax, nir, ioff, boff); break; \
+        case 2: ok = launch_tile2<NO, 2>(rpt, g, sm, st, ip, nin, op, in_begin, entries, rb, freal, ncols, s, n, nmax, nir, ioff, boff); break; \
+        case 3: ok = launch_tile2<NO, 3>(rpt, g, sm, st, ip, nin, op, in_begin, entries, rb, freal, ncols, s, n, nmax, nir, ioff, boff); break; \
+        default: ok = launch_tile2<NO, 4>(rpt, g, sm, st, ip, nin, op, in_begin, entries, rb, freal, ncols, s, n, nmax, nir, ioff, boff); break; \
+        }                                                                                        \
+        break;
+        switch (nout) { KS_T2B(1) KS_T2B(2) KS_T2B(3) KS_T2B(4) KS_T2B(5) KS_T2B(6) KS_T2B(7) KS_T2B(8) }
+#undef KS_T2B
+        if (ok) {
+            check_launch("k_kron_tile2");
+            return true;
+        }
+    }
     const size_t N = ncols * (size_t)n;
     size_t nqt = 0;
     unsigned grid = (unsigned)((N + kTileThreads - 1) / kTileThreads);
