@@ -146,6 +146,12 @@ __global__ void __launch_bounds__(kTileThreads) k_kron_tile2(
     const size_t c0 = (size_t)blockIdx.x * kTQ;
     const int ncol = (int)min((size_t)kTQ, ncols - c0);
     const double2 Z = make_double2(0.0, 0.0);
+    __shared__ long long colbase[kTQ]; // natural offset of column c0 + c (row 0), input geometry
+    if (tid < kTQ) {
+        const size_t cm = c0 + tid;
+        const size_t oo = cm / s, qq = cm - oo * s;
+        colbase[tid] = (long long)(oo * (size_t)n_in_rows * s + qq);
+    }
     for (int e = tid; e < BW * PITCH; e += kTileThreads) // zero halo rows of both buffers
         for (int b = 0; b < 2; ++b) {
             tl[b * rows_p * PITCH + e] = Z;
@@ -159,11 +165,9 @@ __global__ void __launch_bounds__(kTileThreads) k_kron_tile2(
             for (int e = tid; e < tot; e += kTileThreads) {
                 int r, c;
                 if (s == 1) { c = e / n_in_rows; r = e - c * n_in_rows; } // fibers contiguous
-                else { r = e / kTQ; c = e - r * kTQ; }                    // q contiguous
+                else { r = e >> 3; c = e & (kTQ - 1); }                   // q contiguous
                 const bool v = c < ncol;
-                const size_t cm = c0 + c;
-                const size_t oo = cm / s, qq = cm - oo * s;
-                const double2* src = in + oo * (size_t)n_in_rows * s + (size_t)r * s + qq;
+                const double2* src = in + colbase[c] + (size_t)r * s;
                 cpa16(t + r * PITCH + c, v ? (const void*)src : (const void*)in, v);
             }
         }
@@ -174,6 +178,7 @@ __global__ void __launch_bounds__(kTileThreads) k_kron_tile2(
     for (int a = 0; a < NOUT; ++a)
 #pragma unroll
         for (int k = 0; k < RPT; ++k) acc[a][k] = Z;
+    __syncthreads(); // colbase visible
     issue(0, 0);
     for (int j = 0; j < n_in; ++j) {
         issue(j + 1, (j + 1) & 1);

@@ -4,6 +4,8 @@
 // live on the same device, at the clocks the device runs under load.
 #include "ks_internal.hpp"
 
+#include <vector>
+
 namespace ks {
 
 namespace {
@@ -218,6 +220,54 @@ void fp64_peak_bench_mma16(double* tflops) { run_mma16(tflops); }
 void fp64_peak_bench_mma(double* tflops) { run_peak(true, tflops); }
 
 } // namespace ks
+
+// HBM fan-in/fan-out bandwidth: read NIN arrays, write NOUT arrays (sum / copies)
+__global__ void k_fan(const double2* const* __restrict__ in, int nin, double2* const* __restrict__ out,
+                      int nout, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        double2 a = make_double2(0, 0);
+        for (int j = 0; j < nin; ++j) {
+            const double2 v = __ldg(in[j] + i);
+            a.x += v.x;
+            a.y += v.y;
+        }
+        for (int k = 0; k < nout; ++k) out[k][i] = make_double2(a.x * (k + 1), a.y);
+    }
+}
+extern "C" int ks_bw_fan(int nin, int nout, size_t n, double* gbs) {
+    try {
+        std::vector<ks::DevBuf> bufs;
+        std::vector<void*> ptr;
+        for (int j = 0; j < nin + nout; ++j) {
+            bufs.emplace_back(n * sizeof(double2));
+            KS_CUDA(cudaMemset(bufs.back().p, 0, n * sizeof(double2)));
+            ptr.push_back(bufs.back().p);
+        }
+        ks::DevBuf dp(ptr.size() * sizeof(void*));
+        KS_CUDA(cudaMemcpy(dp.p, ptr.data(), ptr.size() * sizeof(void*), cudaMemcpyHostToDevice));
+        const double2* const* ip = reinterpret_cast<const double2* const*>(dp.p);
+        double2* const* op = reinterpret_cast<double2* const*>(static_cast<void**>(dp.p) + nin);
+        cudaEvent_t a, b;
+        KS_CUDA(cudaEventCreate(&a));
+        KS_CUDA(cudaEventCreate(&b));
+        float best = 1e30f;
+        for (int rep = 0; rep < 5; ++rep) {
+            KS_CUDA(cudaEventRecord(a));
+            k_fan<<<148 * 16, 256>>>(ip, nin, op, nout, n);
+            ks::check_launch("k_fan");
+            KS_CUDA(cudaEventRecord(b));
+            KS_CUDA(cudaEventSynchronize(b));
+            float ms = 0;
+            KS_CUDA(cudaEventElapsedTime(&ms, a, b));
+            if (rep > 0 && ms < best) best = ms;
+        }
+        *gbs = (double)(nin + nout) * n * 16 / (best * 1e-3) / 1e9;
+    } catch (const ks::Error& e) {
+        ks::set_last_error(e.what());
+        return e.code;
+    }
+    return KS_OK;
+}
 
 // DMMA throughput at a given number of resident warps per SM (grid = SMs x ctas)
 extern "C" int ks_fp64_dmma_occupancy(int ctas_per_sm, int threads, double* tflops) {
