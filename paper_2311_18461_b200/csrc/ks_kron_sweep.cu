@@ -15,6 +15,7 @@
 // algorithmic bytes but ran at 12-17% occupancy, 2-4x slower.)
 #include "ks_internal.hpp"
 
+#include <algorithm>
 #include <cstdlib>
 
 namespace ks {
@@ -133,42 +134,63 @@ __device__ __forceinline__ void cpa16(void* dst, const void* src, bool v) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(v ? 16 : 0));
 }
 
+constexpr int kStg = 4; // ring stages over (column tile, input) work items
+
 template <int NOUT, int BW, int RPT>
 __global__ void __launch_bounds__(kTileThreads) k_kron_tile2(
     const double2* const* __restrict__ in_ptrs, int n_in, double2* const* __restrict__ out_ptrs,
     const int* __restrict__ in_begin, const SweepEntry* __restrict__ entries,
     const double2* __restrict__ rb, const int* __restrict__ freal, size_t ncols, size_t s, int n,
     int nmax, int n_in_rows, int in_off, int band_off) {
+    // persistent: CTA b owns column tiles b, b + grid, ...; work item w = (tile, input j)
     constexpr int TAPS = 2 * BW + 1, PITCH = kTQ + 1;
-    extern __shared__ __align__(16) double2 tl[]; // [2][n_in_rows + 2BW][PITCH]
+    extern __shared__ __align__(16) double2 tl[]; // [kStg][n_in_rows + 2BW][PITCH]
     const int rows_p = n_in_rows + 2 * BW;
+    const size_t stage_sz = (size_t)rows_p * PITCH;
     const int tid = threadIdx.x, cc = tid % kTQ, rg = tid / kTQ;
-    const size_t c0 = (size_t)blockIdx.x * kTQ;
-    const int ncol = (int)min((size_t)kTQ, ncols - c0);
+    const size_t ntiles = (ncols + kTQ - 1) / kTQ;
     const double2 Z = make_double2(0.0, 0.0);
-    __shared__ long long colbase[kTQ]; // natural offset of column c0 + c (row 0), input geometry
-    if (tid < kTQ) {
-        const size_t cm = c0 + tid;
-        const size_t oo = cm / s, qq = cm - oo * s;
-        colbase[tid] = (long long)(oo * (size_t)n_in_rows * s + qq);
-    }
-    for (int e = tid; e < BW * PITCH; e += kTileThreads) // zero halo rows of both buffers
-        for (int b = 0; b < 2; ++b) {
-            tl[b * rows_p * PITCH + e] = Z;
-            tl[b * rows_p * PITCH + (n_in_rows + BW) * PITCH + e] = Z;
+    for (int e = tid; e < BW * PITCH; e += kTileThreads) // zero halo rows of every stage
+        for (int b = 0; b < kStg; ++b) {
+            tl[b * stage_sz + e] = Z;
+            tl[b * stage_sz + (n_in_rows + BW) * PITCH + e] = Z;
         }
-    auto issue = [&](int j, int b) {
-        if (j < n_in) {
+    const long long my_tiles =
+        ntiles > blockIdx.x ? (long long)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+    const long long nwork = my_tiles * n_in;
+    // issue side: column base of the item's tile (recomputed when the tile changes)
+    long long ibase_tile = -1;
+    long long ibase = 0;
+    int incol = 0;
+    auto issue = [&](long long w) {
+        if (w < nwork) {
+            const long long ti = w / n_in;
+            const int j = (int)(w - ti * n_in);
+            const size_t c0 = (size_t)(blockIdx.x + ti * gridDim.x) * kTQ;
+            const int ncol = (int)min((size_t)kTQ, ncols - c0);
+            double2* t = tl + (size_t)(w % kStg) * stage_sz + BW * PITCH;
             const double2* __restrict__ in = in_ptrs[j];
-            double2* t = tl + (size_t)b * rows_p * PITCH + BW * PITCH;
             const int tot = n_in_rows * kTQ;
-            for (int e = tid; e < tot; e += kTileThreads) {
-                int r, c;
-                if (s == 1) { c = e / n_in_rows; r = e - c * n_in_rows; } // fibers contiguous
-                else { r = e >> 3; c = e & (kTQ - 1); }                   // q contiguous
-                const bool v = c < ncol;
-                const double2* src = in + colbase[c] + (size_t)r * s;
-                cpa16(t + r * PITCH + c, v ? (const void*)src : (const void*)in, v);
+            if (s == 1) {
+                const double2* src0 = in + c0 * (size_t)n_in_rows; // fibers contiguous
+                for (int e = tid; e < tot; e += kTileThreads) {
+                    const int c = e / n_in_rows, r = e - c * n_in_rows;
+                    const bool v = c < ncol;
+                    cpa16(t + r * PITCH + c, v ? (const void*)(src0 + e) : (const void*)in, v);
+                }
+            } else {
+                if (ibase_tile != ti) { // this thread's column (tid & 7 fixed for all e)
+                    const size_t cm = c0 + (tid & (kTQ - 1));
+                    const size_t oo = cm / s, qq = cm - oo * s;
+                    ibase = (long long)(oo * (size_t)n_in_rows * s + qq);
+                    incol = (int)(tid & (kTQ - 1)) < ncol;
+                    ibase_tile = ti;
+                }
+                for (int e = tid; e < tot; e += kTileThreads) {
+                    const int r = e >> 3, c = e & (kTQ - 1);
+                    cpa16(t + r * PITCH + c, incol ? (const void*)(in + ibase + (size_t)r * s) : (const void*)in,
+                          incol != 0);
+                }
             }
         }
         asm volatile("cp.async.commit_group;\n" ::);
@@ -178,14 +200,16 @@ __global__ void __launch_bounds__(kTileThreads) k_kron_tile2(
     for (int a = 0; a < NOUT; ++a)
 #pragma unroll
         for (int k = 0; k < RPT; ++k) acc[a][k] = Z;
-    __syncthreads(); // colbase visible
-    issue(0, 0);
-    for (int j = 0; j < n_in; ++j) {
-        issue(j + 1, (j + 1) & 1);
-        asm volatile("cp.async.wait_group 1;\n" ::);
+    __syncthreads(); // halos visible before any stage is consumed
+#pragma unroll
+    for (int q = 0; q < kStg - 1; ++q) issue(q);
+    for (long long w = 0; w < nwork; ++w) {
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(kStg - 2));
         __syncthreads();
-        const double2* t = tl + (size_t)(j & 1) * rows_p * PITCH + cc;
-        // window of the RPT rows' taps: input rows r + in_off - BW .. (padded index r + in_off)
+        issue(w + kStg - 1);
+        const long long ti = w / n_in;
+        const int j = (int)(w - ti * n_in);
+        const double2* t = tl + (size_t)(w % kStg) * stage_sz + cc;
         const int eb = in_begin[j], ee = in_begin[j + 1];
         for (int e = eb; e < ee; ++e) {
             const SweepEntry en = entries[e];
@@ -195,9 +219,9 @@ __global__ void __launch_bounds__(kTileThreads) k_kron_tile2(
                 const int r = rg + k * kRG;
                 v[k] = Z;
                 if (r < n) {
-                    const double2* w = t + (r + in_off) * PITCH; // padded row r+in_off-BW+BW
+                    const double2* wv = t + (r + in_off) * PITCH;
                     if (en.factor < 0) {
-                        v[k] = w[BW * PITCH];
+                        v[k] = wv[BW * PITCH];
                     } else {
                         const double2* band = rb + ((size_t)en.factor * nmax + band_off + r) * TAPS;
                         double vr = 0.0, vi = 0.0;
@@ -205,7 +229,7 @@ __global__ void __launch_bounds__(kTileThreads) k_kron_tile2(
 #pragma unroll
                             for (int tp = 0; tp < TAPS; ++tp) {
                                 const double a = __ldg(&band[tp].x);
-                                const double2 x = w[tp * PITCH];
+                                const double2 x = wv[tp * PITCH];
                                 vr = fma(a, x.x, vr);
                                 vi = fma(a, x.y, vi);
                             }
@@ -213,7 +237,7 @@ __global__ void __launch_bounds__(kTileThreads) k_kron_tile2(
 #pragma unroll
                             for (int tp = 0; tp < TAPS; ++tp) {
                                 const double2 a = __ldg(&band[tp]);
-                                const double2 x = w[tp * PITCH];
+                                const double2 x = wv[tp * PITCH];
                                 vr = fma(a.x, x.x, fma(-a.y, x.y, vr));
                                 vi = fma(a.x, x.y, fma(a.y, x.x, vi));
                             }
@@ -238,22 +262,30 @@ __global__ void __launch_bounds__(kTileThreads) k_kron_tile2(
 #undef KS_ACC
             }
         }
-        __syncthreads(); // buffer j&1 is refilled by the next iteration's issue
-    }
-    asm volatile("cp.async.wait_group 0;\n" ::);
-    if (cc >= ncol) return;
-    const size_t cme = c0 + cc;
-    const size_t o = cme / s, q = cme - o * s;
-    const size_t base = o * (size_t)n * s + q;
+        if (j == n_in - 1) { // tile complete: store and reset
+            const size_t c0 = (size_t)(blockIdx.x + ti * gridDim.x) * kTQ;
+            const int ncol = (int)min((size_t)kTQ, ncols - c0);
+            if (cc < ncol) {
+                const size_t cme = c0 + cc;
+                const size_t o = cme / s, q = cme - o * s;
+                const size_t base = o * (size_t)n * s + q;
 #pragma unroll
-    for (int a = 0; a < NOUT; ++a) {
-        double2* __restrict__ out = out_ptrs[a];
+                for (int a = 0; a < NOUT; ++a) {
+                    double2* __restrict__ out = out_ptrs[a];
 #pragma unroll
-        for (int k = 0; k < RPT; ++k) {
-            const int r = rg + k * kRG;
-            if (r < n) out[base + (size_t)r * s] = acc[a][k];
+                    for (int k = 0; k < RPT; ++k) {
+                        const int r = rg + k * kRG;
+                        if (r < n) out[base + (size_t)r * s] = acc[a][k];
+                    }
+                }
+            }
+#pragma unroll
+            for (int a = 0; a < NOUT; ++a)
+#pragma unroll
+                for (int k = 0; k < RPT; ++k) acc[a][k] = Z;
         }
     }
+    asm volatile("cp.async.wait_group 0;\n" ::);
 }
 
 template <int NOUT, int BW>
@@ -303,8 +335,15 @@ bool launch_colsweep(int nin, int nout, int bw, const double2* const* ip, double
     if (nout < 1 || nout > 8 || bw < 1 || bw > 4) return false;
     const int rpt = (n + kRG - 1) / kRG;
     if (rpt <= 5 && !std::getenv("KS_KRON_ELEM")) {
-        const size_t sm = (size_t)2 * (nir + 2 * bw) * (kTQ + 1) * sizeof(double2);
-        const unsigned g = (unsigned)((ncols + kTQ - 1) / kTQ);
+        const size_t sm = (size_t)kStg * (nir + 2 * bw) * (kTQ + 1) * sizeof(double2);
+        static int sms = 0;
+        if (!sms) {
+            int dev = 0;
+            KS_CUDA(cudaGetDevice(&dev));
+            KS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        }
+        const size_t ntl = (ncols + kTQ - 1) / kTQ;
+        const unsigned g = (unsigned)std::min<size_t>(ntl, (size_t)sms * 4);
         bool ok = false;
 #define KS_T2B(NO)                                                                               \
     case NO:                                                                                     \
