@@ -334,7 +334,8 @@ bool launch_colsweep(int nin, int nout, int bw, const double2* const* ip, double
     if (nir <= 0) nir = n;
     if (nout < 1 || nout > 8 || bw < 1 || bw > 4) return false;
     const int rpt = (n + kRG - 1) / kRG;
-    if (rpt <= 5 && !std::getenv("KS_KRON_ELEM")) {
+    // opt-in: measured 3.70 ms vs 3.64 ms for the element kernel at c3
+    if (rpt <= 5 && std::getenv("KS_KRON_TILE")) {
         const size_t sm = (size_t)kStg * (nir + 2 * bw) * (kTQ + 1) * sizeof(double2);
         static int sms = 0;
         if (!sms) {
