@@ -39,7 +39,7 @@ struct SweepEntry {
 bool launch_colsweep(int nin, int nout, int bw, const double2* const* ip, double2* const* op,
                      const int* in_begin, const SweepEntry* entries, const double2* rb,
                      const int* freal, size_t ncols, size_t s, int n, int nmax, cudaStream_t st,
-                     int nir = 0, int ioff = 0, int boff = 0, int nent = 1 << 30, int nfac = 1 << 30);
+                     int nir = 0, int ioff = 0, int boff = 0);
 
 struct KronFactor {
     int n = 0, bw = 0;
@@ -510,12 +510,10 @@ void kron_apply(KronPlan& P, const double2* x, double2* y, cudaStream_t st,
                                 ? launch_colsweep(ps.n_in, ps.n_out, P.bwmax, ip, op, ps.d_in_begin.as<int>(),
                                                   ps.d_entries.as<SweepEntry>(), P.d_rowband.as<double2>(),
                                                   P.d_freal.as<int>(), P.N / (size_t)n, s, P.shard_rows,
-                                                  P.nmax, st, n, P.shard_in_off, P.shard_band_off,
-                                                  (int)ps.contribs.size(), (int)P.factors.size())
+                                                  P.nmax, st, n, P.shard_in_off, P.shard_band_off)
                                 : launch_colsweep(ps.n_in, ps.n_out, P.bwmax, ip, op, ps.d_in_begin.as<int>(),
                                                   ps.d_entries.as<SweepEntry>(), P.d_rowband.as<double2>(),
-                                                  P.d_freal.as<int>(), P.N / (size_t)n, s, n, P.nmax, st,
-                                                  0, 0, 0, (int)ps.contribs.size(), (int)P.factors.size());
+                                                  P.d_freal.as<int>(), P.N / (size_t)n, s, n, P.nmax, st);
             if (ok) continue;
         }
         KS_REQUIRE(!shard_last, KS_EINVAL, "sharded matvec: level shape not supported");

@@ -311,128 +311,6 @@ bool launch_tile2(int rpt, unsigned grid, size_t sm, cudaStream_t st, const doub
     return false;
 }
 
-// ---------------------------------------------------------------------------
-// Element kernel v2 (spatial axes, s >= 256): a CTA covers 256 consecutive q of
-// ONE row r, so every thread needs the same band rows. The CTA stages the
-// pass's contributions and the band rows F_f(r, r-BW..r+BW) of the factors it
-// uses into shared memory once; each thread then issues all NIN x (2BW+1)
-// window loads up front (independent, coalesced along q) and evaluates the
-// contributions with broadcast shared-memory coefficients.
-// ---------------------------------------------------------------------------
-constexpr int kMaxEnt = 64, kMaxFac = 16;
-
-template <int NIN, int NOUT, int BW>
-__global__ void __launch_bounds__(kTileThreads) k_kron_row(
-    const double2* const* __restrict__ in_ptrs, double2* const* __restrict__ out_ptrs,
-    const int* __restrict__ in_begin, const SweepEntry* __restrict__ entries, int n_ent,
-    const double2* __restrict__ rb, const int* __restrict__ freal, int nfac, size_t s, int n, int nmax,
-    size_t nqt, int n_in_rows, int in_off, int band_off) {
-    constexpr int TAPS = 2 * BW + 1;
-    __shared__ SweepEntry sent[kMaxEnt];
-    __shared__ int sib[NIN + 1];
-    __shared__ double2 sband[kMaxFac][TAPS];
-    __shared__ int sreal[kMaxFac];
-    const size_t b = blockIdx.x;
-    const int r = (int)(b % (size_t)n);
-    const size_t rest = b / (size_t)n;
-    const size_t qt = rest % nqt, o = rest / nqt;
-    const int tid = threadIdx.x;
-    for (int e = tid; e < n_ent; e += kTileThreads) sent[e] = entries[e];
-    if (tid <= NIN) sib[tid] = in_begin[tid];
-    for (int e = tid; e < nfac * TAPS; e += kTileThreads) {
-        const int f = e / TAPS, t = e - f * TAPS;
-        sband[f][t] = rb[((size_t)f * nmax + band_off + r) * TAPS + t];
-    }
-    if (tid < nfac) sreal[tid] = freal[tid];
-    __syncthreads();
-    const size_t q = qt * kTileThreads + tid;
-    if (q >= s) return;
-    const size_t base = o * (size_t)n_in_rows * s + q;
-    const double2 Z = make_double2(0.0, 0.0);
-    double2 w[NIN][TAPS];
-#pragma unroll
-    for (int j = 0; j < NIN; ++j) {
-        const double2* __restrict__ in = in_ptrs[j] + base;
-#pragma unroll
-        for (int tp = 0; tp < TAPS; ++tp) {
-            const int rr = r + in_off - BW + tp;
-            w[j][tp] = (rr >= 0 && rr < n_in_rows) ? __ldg(in + (size_t)rr * s) : Z;
-        }
-    }
-    double2 acc[NOUT];
-#pragma unroll
-    for (int a = 0; a < NOUT; ++a) acc[a] = Z;
-#pragma unroll
-    for (int j = 0; j < NIN; ++j) {
-        for (int e = sib[j]; e < sib[j + 1]; ++e) {
-            const SweepEntry en = sent[e];
-            double vr, vi;
-            if (en.factor < 0) {
-                vr = w[j][BW].x;
-                vi = w[j][BW].y;
-            } else {
-                vr = 0.0;
-                vi = 0.0;
-                if (sreal[en.factor]) {
-#pragma unroll
-                    for (int tp = 0; tp < TAPS; ++tp) {
-                        const double a = sband[en.factor][tp].x;
-                        vr = fma(a, w[j][tp].x, vr);
-                        vi = fma(a, w[j][tp].y, vi);
-                    }
-                } else {
-#pragma unroll
-                    for (int tp = 0; tp < TAPS; ++tp) {
-                        const double2 a = sband[en.factor][tp];
-                        vr = fma(a.x, w[j][tp].x, fma(-a.y, w[j][tp].y, vr));
-                        vi = fma(a.x, w[j][tp].y, fma(a.y, w[j][tp].x, vi));
-                    }
-                }
-            }
-            const double2 c = en.coeff;
-            switch (en.out) {
-#define KS_ACC(OO)                                                                 \
-    case OO:                                                                       \
-        if (OO < NOUT) {                                                           \
-            double2& A = acc[OO < NOUT ? OO : 0];                                  \
-            A.x = fma(c.x, vr, fma(-c.y, vi, A.x));                                \
-            A.y = fma(c.x, vi, fma(c.y, vr, A.y));                                 \
-        }                                                                          \
-        break;
-                KS_ACC(0) KS_ACC(1) KS_ACC(2) KS_ACC(3) KS_ACC(4) KS_ACC(5) KS_ACC(6) KS_ACC(7)
-#undef KS_ACC
-            }
-        }
-    }
-    const size_t obase = (o * (size_t)n + r) * s + q;
-#pragma unroll
-    for (int a = 0; a < NOUT; ++a) out_ptrs[a][obase] = acc[a];
-}
-
-template <int NIN, int NOUT>
-void launch_row_bw(int bw, unsigned grid, cudaStream_t st, const double2* const* ip, double2* const* op,
-                   const int* ib, const SweepEntry* en, int nent, const double2* rb, const int* fr, int nfac,
-                   size_t s, int n, int nmax, size_t nqt, int nir, int ioff, int boff) {
-    switch (bw) {
-    case 1: k_kron_row<NIN, NOUT, 1><<<grid, kTileThreads, 0, st>>>(ip, op, ib, en, nent, rb, fr, nfac, s, n, nmax, nqt, nir, ioff, boff); break;
-    case 2: k_kron_row<NIN, NOUT, 2><<<grid, kTileThreads, 0, st>>>(ip, op, ib, en, nent, rb, fr, nfac, s, n, nmax, nqt, nir, ioff, boff); break;
-    case 3: k_kron_row<NIN, NOUT, 3><<<grid, kTileThreads, 0, st>>>(ip, op, ib, en, nent, rb, fr, nfac, s, n, nmax, nqt, nir, ioff, boff); break;
-    default: k_kron_row<NIN, NOUT, 4><<<grid, kTileThreads, 0, st>>>(ip, op, ib, en, nent, rb, fr, nfac, s, n, nmax, nqt, nir, ioff, boff); break;
-    }
-}
-
-template <int NIN>
-void launch_row_out(int nout, int bw, unsigned grid, cudaStream_t st, const double2* const* ip,
-                    double2* const* op, const int* ib, const SweepEntry* en, int nent, const double2* rb,
-                    const int* fr, int nfac, size_t s, int n, int nmax, size_t nqt, int nir, int ioff,
-                    int boff) {
-    switch (nout) {
-#define KS_RO(NO) case NO: launch_row_bw<NIN, NO>(bw, grid, st, ip, op, ib, en, nent, rb, fr, nfac, s, n, nmax, nqt, nir, ioff, boff); break;
-        KS_RO(1) KS_RO(2) KS_RO(3) KS_RO(4) KS_RO(5) KS_RO(6) KS_RO(7) KS_RO(8)
-#undef KS_RO
-    }
-}
-
 template <int NOUT>
 void launch_bw(int bw, unsigned grid, cudaStream_t st, const double2* const* ip, int nin,
                double2* const* op, const int* ib, const SweepEntry* en, const double2* rb,
@@ -452,22 +330,9 @@ void launch_bw(int bw, unsigned grid, cudaStream_t st, const double2* const* ip,
 bool launch_colsweep(int nin, int nout, int bw, const double2* const* ip, double2* const* op,
                      const int* in_begin, const SweepEntry* entries, const double2* rb,
                      const int* freal, size_t ncols, size_t s, int n, int nmax, cudaStream_t st,
-                     int nir, int ioff, int boff, int nent_g, int nfac_g) {
+                     int nir, int ioff, int boff) {
     if (nir <= 0) nir = n;
     if (nout < 1 || nout > 8 || bw < 1 || bw > 4) return false;
-    if (s >= (size_t)kTileThreads && nin >= 1 && nin <= 8 && nent_g <= kMaxEnt && nfac_g <= kMaxFac &&
-        !std::getenv("KS_KRON_ELEM")) {
-        const size_t nqt = (s + kTileThreads - 1) / kTileThreads;
-        const size_t outer = ncols / s;
-        const unsigned grid = (unsigned)(outer * nqt * (size_t)n);
-        switch (nin) {
-#define KS_RI(NI) case NI: launch_row_out<NI>(nout, bw, grid, st, ip, op, in_begin, entries, nent_g, rb, freal, nfac_g, s, n, nmax, nqt, nir, ioff, boff); break;
-            KS_RI(1) KS_RI(2) KS_RI(3) KS_RI(4) KS_RI(5) KS_RI(6) KS_RI(7) KS_RI(8)
-#undef KS_RI
-        }
-        check_launch("k_kron_row");
-        return true;
-    }
     const int rpt = (n + kRG - 1) / kRG;
     // opt-in: measured 3.70 ms vs 3.64 ms for the element kernel at c3
     if (rpt <= 5 && std::getenv("KS_KRON_TILE")) {
