@@ -378,7 +378,7 @@ __device__ __forceinline__ bool colmap(const ColMap& M, int n, const TileBase& B
     return true;
 }
 
-template <int TM>
+template <int TM, int STG = kStages>
 __global__ void __launch_bounds__(kThreads, (TM <= 5 ? 2 : 1))
 k_mode_gemm_dmma2(const double* __restrict__ At, int n, const double* __restrict__ X,
                   double* __restrict__ Y, ColMap M) {
@@ -389,7 +389,7 @@ k_mode_gemm_dmma2(const double* __restrict__ At, int n, const double* __restrict
     extern __shared__ __align__(16) double smem[];
     const int nk = (n + kBK - 1) / kBK;
     double* As = smem;                          // [nk*kBK][BMP]
-    double* Bs = smem + (size_t)nk * kBK * BMP; // [kStages][kBK][BNP]
+    double* Bs = smem + (size_t)nk * kBK * BMP; // [STG][kBK][BNP]
     const long long in_rs = M.mode == MAP_TIN ? 2 * M.Np : 2 * M.s;
     const long long out_rs = M.mode == MAP_TOUT ? 2 * M.Np : 2 * M.s;
     const long long ntiles = M.ntiles;
@@ -419,7 +419,7 @@ k_mode_gemm_dmma2(const double* __restrict__ At, int n, const double* __restrict
                 cur_valid = colmap(M, n, tile_base(M, tile), lcp, cur_in, dummy);
                 cur_tile = tile;
             }
-            double* bs = Bs + (size_t)(w % kStages) * kBK * BNP;
+            double* bs = Bs + (size_t)(w % STG) * kBK * BNP;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int jj = lrow0 + 4 * k, j = kc * kBK + jj;
@@ -438,17 +438,17 @@ k_mode_gemm_dmma2(const double* __restrict__ At, int n, const double* __restrict
         for (int m = 0; m < 4; ++m) acc[i][m][0] = acc[i][m][1] = 0.0;
 
 #pragma unroll
-    for (int s = 0; s < kStages - 1; ++s) issue(s);
+    for (int s = 0; s < STG - 1; ++s) issue(s);
 
     const int r_warp = wr * (BM / 2), c_warp = wc * 32;
     const int ar = lane >> 2, ak = lane & 3;
     const int cr = lane >> 2;
     for (int w = 0; w < nwork; ++w) {
-        cp_async_wait<kStages - 2>();
+        cp_async_wait<STG - 2>();
         __syncthreads();
-        issue(w + kStages - 1);
+        issue(w + STG - 1);
         const int kc = w % nk;
-        const double* bs = Bs + (size_t)(w % kStages) * kBK * BNP;
+        const double* bs = Bs + (size_t)(w % STG) * kBK * BNP;
         const double* as = As + (size_t)kc * kBK * BMP;
 #pragma unroll
         for (int k4 = 0; k4 < kBK; k4 += 4) {
@@ -621,8 +621,11 @@ void launch_tm(int engine, const double* At, int n, const double* X, double* Y, 
         check_launch("k_mode_gemm_dmma3");
     } else if (engine == 2) {
         const int nk = (n + kBK - 1) / kBK;
-        const size_t sm = ((size_t)nk * kBK * (16 * TM + 4) + (size_t)kStages * kBK * (kBN + 4)) *
-                          sizeof(double);
+        const size_t sm_a = (size_t)nk * kBK * (16 * TM + 4) * sizeof(double);
+        const size_t sm_s = (size_t)kBK * (kBN + 4) * sizeof(double);
+        // long axes (resident A large): fall back to a 2-stage ring
+        const bool two = sm_a + kStages * sm_s > 227 * 1024;
+        const size_t sm = sm_a + (two ? 2 : kStages) * sm_s;
         static int sms = 0;
         if (!sms) {
             int dev = 0;
@@ -630,12 +633,15 @@ void launch_tm(int engine, const double* At, int n, const double* X, double* Y, 
             KS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
             KS_CUDA(cudaFuncSetAttribute(k_mode_gemm_dmma2<TM>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+            KS_CUDA(cudaFuncSetAttribute(k_mode_gemm_dmma2<TM, 2>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         }
         KS_REQUIRE(sm <= 227 * 1024, KS_EINVAL, "mode product: axis too long for the resident-A kernel");
         const int per_sm = (TM <= 5 && 2 * sm <= 227 * 1024) ? 2 : 1;
         ColMap M = *map;
         const unsigned g2 = (unsigned)std::min<long long>(M.ntiles, (long long)sms * per_sm);
-        k_mode_gemm_dmma2<TM><<<g2, kThreads, sm, st>>>(At, n, X, Y, M);
+        if (two) k_mode_gemm_dmma2<TM, 2><<<g2, kThreads, sm, st>>>(At, n, X, Y, M);
+        else k_mode_gemm_dmma2<TM><<<g2, kThreads, sm, st>>>(At, n, X, Y, M);
         check_launch("k_mode_gemm_dmma2");
     } else {
         const size_t sm = (size_t)2 * kBK * (16 * TM + 4 + kBN + 4) * sizeof(double);
