@@ -36,6 +36,10 @@ struct SweepEntry {
     int factor; // -1 = identity
     double2 coeff;
 };
+struct RingCon {
+    int in, factor;
+    double2 coeff;
+};
 bool launch_colsweep(int nin, int nout, int bw, const double2* const* ip, double2* const* op,
                      const int* in_begin, const SweepEntry* entries, const double2* rb,
                      const int* freal, size_t ncols, size_t s, int n, int nmax, cudaStream_t st,
@@ -58,6 +62,7 @@ struct KronPass {
     std::vector<KronContrib> contribs;
     DevBuf d_begin, d_contribs;
     DevBuf d_in_begin, d_entries; // v3: contributions grouped by input
+    DevBuf d_ring;                // ring sweep: contributions grouped by output (RingCon)
     int in_pool = -1, out_pool = -1; // -1 = x / y
 };
 
@@ -450,6 +455,19 @@ KronPlan* kron_plan(const std::vector<int>& dims,
                 const KronContrib& c = ps.contribs[ci];
                 ent[fill[c.in]++] = SweepEntry{o, c.factor, c.coeff};
             }
+        {
+            std::vector<RingCon> rc;
+            bool fits = ps.n_out <= 8;
+            for (int o = 0; o < ps.n_out; ++o) {
+                if (ps.out_begin[o + 1] - ps.out_begin[o] > 12) fits = false;
+                for (int ci = ps.out_begin[o]; ci < ps.out_begin[o + 1]; ++ci)
+                    rc.push_back(RingCon{ps.contribs[ci].in, ps.contribs[ci].factor, ps.contribs[ci].coeff});
+            }
+            if (fits && !rc.empty()) {
+                ps.d_ring.alloc(rc.size() * sizeof(RingCon));
+                KS_CUDA(cudaMemcpy(ps.d_ring.p, rc.data(), rc.size() * sizeof(RingCon), cudaMemcpyHostToDevice));
+            }
+        }
         ps.d_in_begin.alloc(ib.size() * sizeof(int));
         KS_CUDA(cudaMemcpy(ps.d_in_begin.p, ib.data(), ib.size() * sizeof(int), cudaMemcpyHostToDevice));
         if (!ent.empty()) {

@@ -311,6 +311,129 @@ bool launch_tile2(int rpt, unsigned grid, size_t sm, cudaStream_t st, const doub
     return false;
 }
 
+// ---------------------------------------------------------------------------
+// Ring sweep (spatial axes, s > 1): a CTA owns 32 consecutive columns (o, q)
+// and walks the pass axis r = 0..n-1 once. Every input row enters a
+// shared-memory ring (RW = 2BW+1+kPre rows per input node) exactly once via
+// cp.async, kPre rows ahead, so L2 and HBM see each input element once (the
+// element kernel re-fetches each element 2BW+1 times through L2 on long
+// strides). Warp g computes output node g for the 32 columns: its
+// contributions are warp-uniform (staged in shared memory), band
+// coefficients are broadcast loads, the ring reads are conflict-free, and
+// the output row is one coalesced 512 B store. One barrier per row.
+// ---------------------------------------------------------------------------
+constexpr int kRC = 32, kPre = 4, kMaxCon = 12;
+
+struct RingCon {
+    int in, factor;
+    double2 coeff;
+};
+
+template <int BW>
+__global__ void __launch_bounds__(256) k_kron_ring(
+    const double2* const* __restrict__ in_ptrs, int n_in, double2* const* __restrict__ out_ptrs,
+    int n_out, const int* __restrict__ out_begin, const RingCon* __restrict__ cons,
+    const double2* __restrict__ rb, const int* __restrict__ freal, size_t ncols, size_t s, int n,
+    int nmax, int n_in_rows, int in_off, int band_off) {
+    constexpr int TAPS = 2 * BW + 1, RW = TAPS + kPre;
+    extern __shared__ __align__(16) double2 ring[]; // [n_in][RW][kRC]
+    __shared__ RingCon scon[8][kMaxCon];
+    __shared__ int sncon[8];
+    __shared__ long long scol[kRC];         // input offset of each column (row 0); -1 = invalid
+    __shared__ const double2* sin[8];
+    const int tid = threadIdx.x, lane = tid & 31, g = tid >> 5;
+    const size_t c0 = (size_t)blockIdx.x * kRC;
+    if (tid < kRC) {
+        const size_t cmc = c0 + tid;
+        if (cmc < ncols) {
+            const size_t oo = cmc / s, qq = cmc - oo * s;
+            scol[tid] = (long long)(oo * (size_t)n_in_rows * s + qq);
+        } else {
+            scol[tid] = -1;
+        }
+    }
+    if (tid < n_in && tid < 8) sin[tid] = in_ptrs[tid];
+    if (tid < 8) sncon[tid] = tid < n_out ? out_begin[tid + 1] - out_begin[tid] : 0;
+    for (int e = tid; e < 8 * kMaxCon; e += 256) {
+        const int o = e / kMaxCon, k = e - o * kMaxCon;
+        if (o < n_out && out_begin[o] + k < out_begin[o + 1]) scon[o][k] = cons[out_begin[o] + k];
+    }
+    // this lane's column (input geometry for loads, output geometry for stores)
+    const size_t cm = c0 + lane;
+    const bool cv = cm < ncols;
+    size_t ibase = 0, obase = 0;
+    if (cv) {
+        const size_t oo = cm / s, qq = cm - oo * s;
+        ibase = oo * (size_t)n_in_rows * s + qq;
+        obase = oo * (size_t)n * s + qq;
+    }
+    // row x of input j lands in slot x % RW; loads: thread t handles (j, lane) pairs
+    auto issue = [&](int x) { // input rows x (padded coordinate: x - BW is the true row)
+        const int row = x - BW + in_off; // input row index
+        const bool rv = row >= 0 && row < n_in_rows;
+        for (int e = tid; e < n_in * kRC; e += 256) {
+            const int j = e >> 5, c = e & (kRC - 1);
+            double2* dst = ring + ((size_t)j * RW + (x % RW)) * kRC + c;
+            const long long cb = scol[c];
+            const bool v = rv && cb >= 0;
+            const double2* src = sin[j];
+            if (v) src += cb + (long long)row * (long long)s;
+            const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(v ? 16 : 0));
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    };
+    __syncthreads(); // scol / sin / contributions visible
+    // prologue: padded rows 0 .. TAPS-2 + kPre (true rows -BW .. BW-1+kPre)
+    for (int x = 0; x < TAPS - 1 + kPre; ++x) issue(x);
+    __syncthreads();
+    const int nc = g < n_out ? sncon[g] : 0;
+    for (int r = 0; r < n; ++r) {
+        issue(r + TAPS - 1 + kPre); // keeps kPre rows in flight
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(kPre));
+        __syncthreads();
+        if (g < n_out) {
+            double ar = 0.0, ai = 0.0;
+            for (int k = 0; k < nc; ++k) {
+                const RingCon cn = scon[g][k];
+                const double2* rj = ring + (size_t)cn.in * RW * kRC + lane;
+                double vr, vi;
+                if (cn.factor < 0) {
+                    const double2 x = rj[((r + BW) % RW) * kRC];
+                    vr = x.x;
+                    vi = x.y;
+                } else {
+                    const double2* band = rb + ((size_t)cn.factor * nmax + band_off + r) * TAPS;
+                    vr = 0.0;
+                    vi = 0.0;
+                    if (__ldg(freal + cn.factor)) {
+#pragma unroll
+                        for (int tp = 0; tp < TAPS; ++tp) {
+                            const double a = __ldg(&band[tp].x);
+                            const double2 x = rj[((r + tp) % RW) * kRC];
+                            vr = fma(a, x.x, vr);
+                            vi = fma(a, x.y, vi);
+                        }
+                    } else {
+#pragma unroll
+                        for (int tp = 0; tp < TAPS; ++tp) {
+                            const double2 a = __ldg(&band[tp]);
+                            const double2 x = rj[((r + tp) % RW) * kRC];
+                            vr = fma(a.x, x.x, fma(-a.y, x.y, vr));
+                            vi = fma(a.x, x.y, fma(a.y, x.x, vi));
+                        }
+                    }
+                }
+                ar = fma(cn.coeff.x, vr, fma(-cn.coeff.y, vi, ar));
+                ai = fma(cn.coeff.x, vi, fma(cn.coeff.y, vr, ai));
+            }
+            if (cv) out_ptrs[g][obase + (size_t)r * s] = make_double2(ar, ai);
+        }
+        __syncthreads(); // slot (r % RW) is refilled by the next issue
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::);
+}
+
 template <int NOUT>
 void launch_bw(int bw, unsigned grid, cudaStream_t st, const double2* const* ip, int nin,
                double2* const* op, const int* ib, const SweepEntry* en, const double2* rb,
@@ -330,9 +453,32 @@ void launch_bw(int bw, unsigned grid, cudaStream_t st, const double2* const* ip,
 bool launch_colsweep(int nin, int nout, int bw, const double2* const* ip, double2* const* op,
                      const int* in_begin, const SweepEntry* entries, const double2* rb,
                      const int* freal, size_t ncols, size_t s, int n, int nmax, cudaStream_t st,
-                     int nir, int ioff, int boff) {
+                     int nir, int ioff, int boff, const int* ring_begin, const RingCon* ring_cons) {
     if (nir <= 0) nir = n;
     if (nout < 1 || nout > 8 || bw < 1 || bw > 4) return false;
+    if (s > 1 && ring_cons && nin >= 1 && !std::getenv("KS_KRON_ELEM")) {
+        const int RW = 2 * bw + 1 + kPre;
+        const size_t sm = (size_t)nin * RW * kRC * sizeof(double2);
+        if (sm <= 200 * 1024) {
+            const unsigned grid = (unsigned)((ncols + kRC - 1) / kRC);
+#define KS_RING(B)                                                                                    \
+    case B: {                                                                                         \
+        static bool attr = false;                                                                     \
+        if (!attr) {                                                                                  \
+            KS_CUDA(cudaFuncSetAttribute(k_kron_ring<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                         200 * 1024));                                                \
+            attr = true;                                                                              \
+        }                                                                                             \
+        k_kron_ring<B><<<grid, 256, sm, st>>>(ip, nin, op, nout, ring_begin, ring_cons, rb, freal,  \
+                                              ncols, s, n, nmax, nir, ioff, boff);                    \
+        break;                                                                                        \
+    }
+            switch (bw) { KS_RING(1) KS_RING(2) KS_RING(3) KS_RING(4) }
+#undef KS_RING
+            check_launch("k_kron_ring");
+            return true;
+        }
+    }
     const int rpt = (n + kRG - 1) / kRG;
     // opt-in: measured 3.70 ms vs 3.64 ms for the element kernel at c3
     if (rpt <= 5 && std::getenv("KS_KRON_TILE")) {
