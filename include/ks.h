@@ -100,6 +100,11 @@ int ks_fd_eigenvalues(const ks_fd* fd, double* out);
  * the BandedFactorization layout (eigensolve.hpp:36-42): ab is (3p+1) x n_t
  * complex with ldab = 3p+1, piv has n_t ints. For parity tests. */
 int ks_fd_block(const ks_fd* fd, size_t i, ks_c64* ab, int* piv);
+/* Execution plan of a handle (no reference counterpart; diagnostics):
+ * folded_axes bit l-1 set = axis l uses the even/odd folded transform
+ * (centro-symmetric pencil); blocks = factored time blocks
+ * (N_s, or fewer with permutation deduplication). Either pointer may be NULL. */
+int ks_fd_info(const ks_fd* fd, int* folded_axes, size_t* blocks);
 int ks_fd_destroy(ks_fd* fd);
 
 /* ---------------------------------------------------------------------------

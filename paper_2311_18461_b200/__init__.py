@@ -95,6 +95,7 @@ _SIGS = {
     "ks_fd_vec_size": (C.c_size_t, [_P]),
     "ks_fd_eigenvalues": (C.c_int, [_P, _P]),
     "ks_fd_block": (C.c_int, [_P, C.c_size_t, _P, _P]),
+    "ks_fd_info": (C.c_int, [_P, _P, _P]),
     "ks_fd_destroy": (C.c_int, [_P]),
     "ks_kron_create": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.c_int, C.POINTER(ks_term),
                                  C.c_int, C.POINTER(_P)]),
@@ -389,6 +390,13 @@ class FDPreconditioner:
         piv = np.zeros(nt, dtype=np.int32)
         _check(lib().ks_fd_block(self._h, int(i), _ptr(ab), _ptr(piv)))
         return ab, piv
+
+    def info(self) -> dict:
+        """Execution plan: axes on the folded (even/odd) transform, factored blocks."""
+        m, nb = C.c_int(), C.c_size_t()
+        _check(lib().ks_fd_info(self._h, C.byref(m), C.byref(nb)))
+        d = len(self.dims) - 1
+        return {"folded_axes": [l + 1 for l in range(d) if m.value >> l & 1], "blocks": nb.value}
 
     def time(self, r: DeviceVector, z: DeviceVector, iters: int, flush: bool = True):
         ms, mk = C.c_double(), C.c_double()

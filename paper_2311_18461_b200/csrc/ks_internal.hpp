@@ -125,6 +125,20 @@ void launch_fill_bytes(void* p, size_t bytes, cudaStream_t s);
 void launch_mode_gemm(const double* At, int n, const double* X, double* Y,
                       size_t s_complex, size_t outer, cudaStream_t st, int layout = 0, int nt = 0);
 
+// folded (even/odd) transform of one axis whose eigenvectors are all even or
+// odd to relative tolerance tol (centro-symmetric pencils): two half-size
+// GEMMs instead of one (ks_transform.cu)
+struct FoldAxis {
+    int n = 0, hc = 0, th = 0; // hc = ceil(n/2) even eigenvectors; tile height 16*th >= hc
+    DevBuf fwd, inv;           // [2][Kp][16*th] symmetrised half matrices (even, odd), k-major
+    DevBuf rmap;               // int [2][16*th]: even eigen-indices, odd eigen-indices
+};
+// U column-major (U[j + r*n] = U(j, r)); false (F untouched) if not foldable
+// or KS_FD_FOLD=0
+bool fold_axis_build(const double* U, int n, double tol, FoldAxis& F);
+void launch_mode_gemm_fold(const FoldAxis& F, bool inverse, const double* X, double* Y,
+                           size_t s_complex, size_t outer, cudaStream_t st, int layout = 0, int nt = 0);
+
 // ---------------------------------------------------------------------------
 // banded block factor / solve (ks_fdsolve.cu)
 // ---------------------------------------------------------------------------

@@ -43,7 +43,7 @@ struct RingCon {
 bool launch_colsweep(int nin, int nout, int bw, const double2* const* ip, double2* const* op,
                      const int* in_begin, const SweepEntry* entries, const double2* rb,
                      const int* freal, size_t ncols, size_t s, int n, int nmax, cudaStream_t st,
-                     int nir = 0, int ioff = 0, int boff = 0);
+                     int nir, int ioff, int boff, const int* ring_begin, const RingCon* ring_cons);
 
 struct KronFactor {
     int n = 0, bw = 0;
@@ -528,10 +528,12 @@ void kron_apply(KronPlan& P, const double2* x, double2* y, cudaStream_t st,
                                 ? launch_colsweep(ps.n_in, ps.n_out, P.bwmax, ip, op, ps.d_in_begin.as<int>(),
                                                   ps.d_entries.as<SweepEntry>(), P.d_rowband.as<double2>(),
                                                   P.d_freal.as<int>(), P.N / (size_t)n, s, P.shard_rows,
-                                                  P.nmax, st, n, P.shard_in_off, P.shard_band_off)
+                                                  P.nmax, st, n, P.shard_in_off, P.shard_band_off,
+                                                  ps.d_begin.as<int>(), ps.d_ring.as<RingCon>())
                                 : launch_colsweep(ps.n_in, ps.n_out, P.bwmax, ip, op, ps.d_in_begin.as<int>(),
                                                   ps.d_entries.as<SweepEntry>(), P.d_rowband.as<double2>(),
-                                                  P.d_freal.as<int>(), P.N / (size_t)n, s, n, P.nmax, st);
+                                                  P.d_freal.as<int>(), P.N / (size_t)n, s, n, P.nmax, st, n, 0, 0,
+                                                  ps.d_begin.as<int>(), ps.d_ring.as<RingCon>());
             if (ok) continue;
         }
         KS_REQUIRE(!shard_last, KS_EINVAL, "sharded matvec: level shape not supported");

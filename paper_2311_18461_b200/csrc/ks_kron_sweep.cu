@@ -25,6 +25,10 @@ struct SweepEntry {
     int factor; // -1 = identity
     double2 coeff;
 };
+struct RingCon {  // ring sweep: one contribution, grouped by output node
+    int in, factor;
+    double2 coeff;
+};
 
 namespace {
 
@@ -323,11 +327,6 @@ bool launch_tile2(int rpt, unsigned grid, size_t sm, cudaStream_t st, const doub
 // the output row is one coalesced 512 B store. One barrier per row.
 // ---------------------------------------------------------------------------
 constexpr int kRC = 32, kPre = 4, kMaxCon = 12;
-
-struct RingCon {
-    int in, factor;
-    double2 coeff;
-};
 
 template <int BW>
 __global__ void __launch_bounds__(256) k_kron_ring(

@@ -92,6 +92,7 @@ struct ks_fdshard {
     int device = 0;
     ks_fd* local_fd = nullptr;       // transforms on axes 1..d-1 only (dims of the slab)
     std::vector<DevBuf> At_fwd, At_inv; // per axis 1..d
+    std::vector<FoldAxis> fold;         // per axis; n == 0: dense transform
     FdBlocks blocks;                 // blocks of this rank's fibers
     DevBuf Lt, Mt, Wsym;
     DevBuf s0, s1, work2;
@@ -139,6 +140,17 @@ int ks_shard_plan(int d, const int* dims, int nranks, int rank, long long* slab_
     API_END
 }
 
+namespace {
+// transform of axis l (1-based): folded when the axis' eigenvectors are even/odd
+void shard_gemm(const ks_fdshard* h, int l, bool inv, const double* X, double* Y, size_t s, size_t outer,
+                cudaStream_t st, int layout, int nt) {
+    const FoldAxis& F = h->fold[l - 1];
+    if (F.n) launch_mode_gemm_fold(F, inv, X, Y, s, outer, st, layout, nt);
+    else launch_mode_gemm((inv ? h->At_inv : h->At_fwd)[l - 1].as<double>(), h->plan.dims[l], X, Y, s, outer, st,
+                          layout, nt);
+}
+} // namespace
+
 int ks_fdshard_create(int d, const int* dims, double nu, int p_t, const double* const* U,
                       const double* const* lambda, const double* Lt, const double* Mt,
                       const ks_c64* Wt, int nranks, int rank, int device, ks_fdshard** out) {
@@ -163,6 +175,8 @@ int ks_fdshard_create(int d, const int* dims, double nu, int p_t, const double* 
         h->At_inv.emplace_back(ai.size() * sizeof(double));
         KS_CUDA(cudaMemcpy(h->At_fwd.back().p, af.data(), af.size() * sizeof(double), cudaMemcpyHostToDevice));
         KS_CUDA(cudaMemcpy(h->At_inv.back().p, ai.data(), ai.size() * sizeof(double), cudaMemcpyHostToDevice));
+        h->fold.emplace_back();
+        fold_axis_build(U[l], n, 1e-9, h->fold.back());
     }
     // W + W^H and the time bands
     const int nt = dims[0], ld = 2 * p_t + 1;
@@ -270,7 +284,7 @@ int ks_fdshard_forward(ks_fdshard* h, const ks_c64* r_local, ks_c64* sendbuf, vo
         size_t stride = 1;
         for (int k = 0; k < l; ++k) stride *= (size_t)P.dims[k];
         const size_t outer = N / (stride * (size_t)P.dims[l]);
-        launch_mode_gemm(h->At_fwd[l - 1].as<double>(), P.dims[l], cur, bufs[nb], stride, outer, st, 0, 0);
+        shard_gemm(h, l, false, cur, bufs[nb], stride, outer, st, 0, 0);
         cur = bufs[nb];
         nb ^= 1;
     }
@@ -295,14 +309,11 @@ int ks_fdshard_middle(ks_fdshard* h, ks_c64* work, void* stream) {
     ensure_device(h->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : h->stream;
     const Plan& P = h->plan;
-    const int nd = (int)P.nd;
     const size_t s = (size_t)P.nt * P.rest[P.rank].n();
     double* tmp = h->s0.as<double>();
-    launch_mode_gemm(h->At_fwd[P.d - 1].as<double>(), nd, reinterpret_cast<double*>(work), tmp, s, 1, st,
-                     1, P.nt);
+    shard_gemm(h, P.d, false, reinterpret_cast<double*>(work), tmp, s, 1, st, 1, P.nt);
     launch_fd_solve(h->blocks, reinterpret_cast<double2*>(tmp), false, st, true);
-    launch_mode_gemm(h->At_inv[P.d - 1].as<double>(), nd, tmp, reinterpret_cast<double*>(work), s, 1, st,
-                     2, P.nt);
+    shard_gemm(h, P.d, true, tmp, reinterpret_cast<double*>(work), s, 1, st, 2, P.nt);
     if (!stream) KS_CUDA(cudaStreamSynchronize(st));
     API_END
 }
@@ -334,7 +345,7 @@ int ks_fdshard_backward(ks_fdshard* h, const ks_c64* recvbuf, ks_c64* z_local, v
         for (int k = 0; k < l; ++k) stride *= (size_t)P.dims[k];
         const size_t outer = N / (stride * (size_t)P.dims[l]);
         double* out = (l == d - 1) ? reinterpret_cast<double*>(z_local) : bufs[nb];
-        launch_mode_gemm(h->At_inv[l - 1].as<double>(), P.dims[l], cur, out, stride, outer, st, 0, 0);
+        shard_gemm(h, l, true, cur, out, stride, outer, st, 0, 0);
         cur = out;
         nb ^= 1;
     }

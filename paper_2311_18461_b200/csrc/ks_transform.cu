@@ -30,6 +30,8 @@
 #include <cstdlib>
 #include <algorithm>
 #include <cstring>
+#include <cmath>
+#include <vector>
 
 namespace ks {
 
@@ -656,7 +658,297 @@ void launch_tm(int engine, const double* At, int n, const double* X, double* Y, 
     }
 }
 
+// ---------------------------------------------------------------------------
+// Folded (even/odd) transform. On a uniform mesh the 1-D pencils are
+// centro-symmetric (J K J = K, J M J = M, J the flip), so every eigenvector is
+// even (u[n-1-j] = u[j]) or odd (u[n-1-j] = -u[j]); ceil(n/2) of them are even.
+// With E / O the even / odd eigen-indices, s_e / s_o the symmetrised half
+// columns (j < hc = ceil(n/2)):
+//   forward  Y[E_m] = sum_j s_e[j][E_m] (X[j] + X[n-1-j])
+//            Y[O_m] = sum_j s_o[j][O_m] (X[j] - X[n-1-j])
+//   inverse  e_j = sum_m s_e[j][E_m] X[E_m],  o_j = sum_m s_o[j][O_m] X[O_m]
+//            Y[j] = e_j + o_j,  Y[n-1-j] = e_j - o_j
+// i.e. two (n/2 x n/2) GEMMs instead of one n x n: half the FP64 work, same
+// HBM traffic. Stage chunk kc holds 16 rows: "top" rows 0-7 and "bottom" rows
+// 8-15 (forward: X[j], X[n-1-j] for j = 8kc..8kc+7; inverse: X[E_m], X[O_m]),
+// gathered by cp.async, so the fold is two FADDs per B fragment (forward) or
+// nothing (inverse). Each warp owns the same (half-row, column) block of both
+// GEMMs, so the inverse unfold happens in registers.
+// Resident matrices: Af[2][Kp][H] (k-major; [0] even, [1] odd), Kp = 8 * nkc.
+// ---------------------------------------------------------------------------
+template <int TH, bool INV, int STG = kStages>
+__global__ void __launch_bounds__(kThreads, (TH <= 2 ? 2 : 1))
+k_mode_gemm_fold(const double* __restrict__ Af, const int* __restrict__ rmap, int n, int hc, int nkc,
+                 const double* __restrict__ X, double* __restrict__ Y, ColMap M) {
+    constexpr int H = 16 * TH;
+    constexpr int MT = TH; // 8-row blocks per warp per GEMM (H/2 half-rows per warp)
+    constexpr int BMP = H + 4;
+    constexpr int BNP = kBN + 4;
+    extern __shared__ __align__(16) double smem[];
+    const int Kp = nkc * 8;
+    double* Ae = smem;                        // [Kp][BMP]
+    double* Ao = Ae + (size_t)Kp * BMP;       // [Kp][BMP]
+    double* Bs = Ao + (size_t)Kp * BMP;       // [STG][16][BNP]
+    int* rE = reinterpret_cast<int*>(Bs + (size_t)STG * 16 * BNP); // [H] even eigen-indices
+    int* rO = rE + H;                                               // [H] odd eigen-indices
+    const int no = n - hc;
+    const long long in_rs = M.mode == MAP_TIN ? 2 * M.Np : 2 * M.s;
+    const long long out_rs = M.mode == MAP_TOUT ? 2 * M.Np : 2 * M.s;
+    const long long ntiles = M.ntiles;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wr = warp & 1, wc = warp >> 1;
+
+    for (int e = tid; e < Kp * H; e += kThreads) {
+        const int k = e / H, r = e - k * H;
+        Ae[k * BMP + r] = __ldg(Af + e);
+        Ao[k * BMP + r] = __ldg(Af + (size_t)Kp * H + e);
+    }
+    for (int e = tid; e < 2 * H; e += kThreads) rE[e] = __ldg(rmap + e);
+    __syncthreads();
+
+    const int lcp = tid & 63, lrow0 = tid >> 6;
+    const int my_tiles =
+        ntiles > (long long)blockIdx.x ? (int)((ntiles - 1 - (long long)blockIdx.x) / gridDim.x + 1) : 0;
+    const int nwork = my_tiles * nkc;
+    long long cur_tile = -1, cur_in = 0;
+    bool cur_valid = false;
+
+    auto issue = [&](int w) {
+        if (w < nwork) {
+            const int wt = w / nkc;
+            const long long tile = (long long)blockIdx.x + (long long)wt * gridDim.x;
+            const int kc = w - wt * nkc;
+            if (tile != cur_tile) {
+                long long dummy;
+                cur_valid = colmap(M, n, tile_base(M, tile), lcp, cur_in, dummy);
+                cur_tile = tile;
+            }
+            double* bs = Bs + (size_t)(w % STG) * 16 * BNP;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int jj = lrow0 + 4 * k; // smem row 0..15
+                const int q = kc * 8 + (jj & 7);
+                int src;
+                bool v;
+                if (!INV) {
+                    src = jj < 8 ? q : n - 1 - q;
+                    v = jj < 8 ? q < hc : q < n - hc; // odd n: the middle row has no mirror
+                } else {
+                    v = jj < 8 ? q < hc : q < no;
+                    src = v ? (jj < 8 ? rE[q] : rO[q]) : 0;
+                }
+                v = v && cur_valid;
+                cp_async16(bs + jj * BNP + 2 * lcp,
+                           v ? (const void*)(X + cur_in + (long long)src * in_rs) : (const void*)X, v);
+            }
+        }
+        cp_async_commit();
+    };
+
+    double acc[2][MT][4][2];
+#pragma unroll
+    for (int g = 0; g < 2; ++g)
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+            for (int m = 0; m < 4; ++m) acc[g][i][m][0] = acc[g][i][m][1] = 0.0;
+
+#pragma unroll
+    for (int s = 0; s < STG - 1; ++s) issue(s);
+
+    const int r_warp = wr * (H / 2), c_warp = wc * 32;
+    const int ar = lane >> 2, ak = lane & 3;
+    const int cr = lane >> 2;
+    for (int w = 0; w < nwork; ++w) {
+        cp_async_wait<STG - 2>();
+        __syncthreads();
+        issue(w + STG - 1);
+        const int kc = w % nkc;
+        const double* bs = Bs + (size_t)(w % STG) * 16 * BNP;
+#pragma unroll
+        for (int k4 = 0; k4 < 8; k4 += 4) {
+            const int kr = kc * 8 + k4 + ak;
+            double ae[MT], ao[MT], be[4], bo[4];
+#pragma unroll
+            for (int i = 0; i < MT; ++i) {
+                ae[i] = Ae[kr * BMP + r_warp + i * 8 + ar];
+                ao[i] = Ao[kr * BMP + r_warp + i * 8 + ar];
+            }
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const double t = bs[(k4 + ak) * BNP + c_warp + m * 8 + ar];
+                const double b = bs[(8 + k4 + ak) * BNP + c_warp + m * 8 + ar];
+                be[m] = INV ? t : t + b;
+                bo[m] = INV ? b : t - b;
+            }
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    dmma_m8n8k4(acc[0][i][m][0], acc[0][i][m][1], ae[i], be[m]);
+                    dmma_m8n8k4(acc[1][i][m][0], acc[1][i][m][1], ao[i], bo[m]);
+                }
+        }
+        if (kc == nkc - 1) {
+            const long long tile = (long long)blockIdx.x + (long long)(w / nkc) * gridDim.x;
+            const TileBase tbase = tile_base(M, tile);
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const int jcol = (c_warp >> 1) + m * 4 + (lane & 3);
+                long long io, oo;
+                if (colmap(M, n, tbase, jcol, io, oo)) {
+                    double* yb = Y + oo;
+#pragma unroll
+                    for (int i = 0; i < MT; ++i) {
+                        const int h = r_warp + i * 8 + cr;
+                        const double2 e = make_double2(acc[0][i][m][0], acc[0][i][m][1]);
+                        const double2 o = make_double2(acc[1][i][m][0], acc[1][i][m][1]);
+                        if (!INV) {
+                            if (h < hc) *reinterpret_cast<double2*>(yb + (long long)rE[h] * out_rs) = e;
+                            if (h < no) *reinterpret_cast<double2*>(yb + (long long)rO[h] * out_rs) = o;
+                        } else if (h < hc) {
+                            *reinterpret_cast<double2*>(yb + (long long)h * out_rs) =
+                                make_double2(e.x + o.x, e.y + o.y);
+                            if (n - 1 - h != h)
+                                *reinterpret_cast<double2*>(yb + (long long)(n - 1 - h) * out_rs) =
+                                    make_double2(e.x - o.x, e.y - o.y);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < MT; ++i)
+                    acc[0][i][m][0] = acc[0][i][m][1] = acc[1][i][m][0] = acc[1][i][m][1] = 0.0;
+            }
+        }
+    }
+    cp_async_wait<0>();
+}
+
+template <int TH, bool INV>
+void launch_fold_th(const FoldAxis& F, const double* X, double* Y, const ColMap& M, cudaStream_t st) {
+    constexpr int H = 16 * TH;
+    const int nkc = (F.hc + 7) / 8;
+    const size_t sm_a = (size_t)2 * nkc * 8 * (H + 4) * sizeof(double) + (size_t)2 * H * sizeof(int);
+    const size_t sm_s = (size_t)16 * (kBN + 4) * sizeof(double);
+    const bool two = sm_a + kStages * sm_s > 227 * 1024;
+    const size_t sm = sm_a + (two ? 2 : kStages) * sm_s;
+    KS_REQUIRE(sm <= 227 * 1024, KS_EINVAL, "folded mode product: axis too long");
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        KS_CUDA(cudaGetDevice(&dev));
+        KS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        KS_CUDA(cudaFuncSetAttribute(k_mode_gemm_fold<TH, INV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     227 * 1024));
+        KS_CUDA(cudaFuncSetAttribute(k_mode_gemm_fold<TH, INV, 2>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    }
+    const int per_sm = (TH <= 2 && 2 * sm <= 227 * 1024) ? 2 : 1;
+    const unsigned g = (unsigned)std::min<long long>(M.ntiles, (long long)sms * per_sm);
+    const double* A = (INV ? F.inv : F.fwd).as<double>();
+    if (two)
+        k_mode_gemm_fold<TH, INV, 2><<<g, kThreads, sm, st>>>(A, F.rmap.as<int>(), F.n, F.hc, nkc, X, Y, M);
+    else
+        k_mode_gemm_fold<TH, INV><<<g, kThreads, sm, st>>>(A, F.rmap.as<int>(), F.n, F.hc, nkc, X, Y, M);
+    check_launch("k_mode_gemm_fold");
+}
+
+ColMap make_colmap(int n, size_t s_complex, size_t outer, int layout, int nt) {
+    ColMap M{};
+    M.mode = layout;
+    M.s = (long long)s_complex;
+    M.Q = (long long)s_complex * (long long)outer;
+    if (layout == MAP_STD) {
+        M.ntiles = (M.Q + 63) / 64;
+    } else {
+        KS_REQUIRE(outer == 1 && nt > 0 && s_complex % (size_t)nt == 0, KS_EINVAL,
+                   "time-major transform needs the outermost axis");
+        M.nt = nt;
+        M.Np = (long long)s_complex / nt;
+        M.Ns = M.Np * n;
+        M.tbr = M.Np >= 8 ? 8 : (M.Np >= 4 ? 4 : (M.Np >= 2 ? 2 : 1));
+        M.tbt = 64 / M.tbr;
+        M.ntb = (nt + M.tbt - 1) / M.tbt;
+        M.ntiles = M.ntb * ((M.Np + M.tbr - 1) / M.tbr);
+    }
+    return M;
+}
+
 } // namespace
+
+bool fold_axis_build(const double* U, int n, double tol, FoldAxis& F) {
+    // U column-major: U(j, r) = U[j + r*n]
+    if (n < 2) return false;
+    if (const char* e = std::getenv("KS_FD_FOLD"))
+        if (std::strcmp(e, "0") == 0) return false;
+    const int hc = (n + 1) / 2;
+    std::vector<int> E, O;
+    for (int r = 0; r < n; ++r) {
+        const double* u = U + (size_t)r * n;
+        double mx = 0, de = 0, dd = 0;
+        for (int j = 0; j < n; ++j) {
+            mx = std::max(mx, std::fabs(u[j]));
+            de = std::max(de, std::fabs(u[j] - u[n - 1 - j]));
+            dd = std::max(dd, std::fabs(u[j] + u[n - 1 - j]));
+        }
+        if (!(mx > 0) || std::min(de, dd) > tol * mx) return false;
+        (de <= dd ? E : O).push_back(r);
+    }
+    if ((int)E.size() != hc) return false;
+    const int th = (hc + 15) / 16;
+    if (th > 5) return false;
+    const int H = 16 * th, Kp = 8 * ((hc + 7) / 8);
+    std::vector<double> fwd((size_t)2 * Kp * H, 0.0), inv((size_t)2 * Kp * H, 0.0);
+    std::vector<int> rmap((size_t)2 * H, 0);
+    const int no = n - hc;
+    for (int m = 0; m < hc; ++m) rmap[m] = E[m];
+    for (int m = 0; m < no; ++m) rmap[H + m] = O[m];
+    for (int j = 0; j < hc; ++j) {
+        const int jm = n - 1 - j;
+        for (int m = 0; m < hc; ++m) { // even: s_e[j][E_m]
+            const double* u = U + (size_t)E[m] * n;
+            const double se = jm == j ? u[j] : 0.5 * (u[j] + u[jm]);
+            fwd[(size_t)j * H + m] = se;        // forward: k = j, row = m
+            inv[(size_t)m * H + j] = se;        // inverse: k = m, row = j
+        }
+        for (int m = 0; m < no; ++m) { // odd: s_o[j][O_m]
+            const double* u = U + (size_t)O[m] * n;
+            const double so = jm == j ? 0.0 : 0.5 * (u[j] - u[jm]);
+            fwd[(size_t)Kp * H + (size_t)j * H + m] = so;
+            inv[(size_t)Kp * H + (size_t)m * H + j] = so;
+        }
+    }
+    F.n = n;
+    F.hc = hc;
+    F.th = th;
+    F.fwd.alloc(fwd.size() * sizeof(double));
+    F.inv.alloc(inv.size() * sizeof(double));
+    F.rmap.alloc(rmap.size() * sizeof(int));
+    KS_CUDA(cudaMemcpy(F.fwd.p, fwd.data(), fwd.size() * sizeof(double), cudaMemcpyHostToDevice));
+    KS_CUDA(cudaMemcpy(F.inv.p, inv.data(), inv.size() * sizeof(double), cudaMemcpyHostToDevice));
+    KS_CUDA(cudaMemcpy(F.rmap.p, rmap.data(), rmap.size() * sizeof(int), cudaMemcpyHostToDevice));
+    return true;
+}
+
+void launch_mode_gemm_fold(const FoldAxis& F, bool inverse, const double* X, double* Y, size_t s_complex,
+                           size_t outer, cudaStream_t st, int layout, int nt) {
+    if (s_complex == 0 || outer == 0) return;
+    const ColMap M = make_colmap(F.n, s_complex, outer, layout, nt);
+#define KS_FOLD_CASE(T)                                                                            \
+    case T:                                                                                        \
+        if (inverse) launch_fold_th<T, true>(F, X, Y, M, st);                                      \
+        else launch_fold_th<T, false>(F, X, Y, M, st);                                             \
+        break;
+    switch (F.th) {
+        KS_FOLD_CASE(1)
+        KS_FOLD_CASE(2)
+        KS_FOLD_CASE(3)
+        KS_FOLD_CASE(4)
+        KS_FOLD_CASE(5)
+    default: throw Error(KS_EINVAL, "folded mode product: bad tile height");
+    }
+#undef KS_FOLD_CASE
+}
 
 int transform_engine() { return engine_choice(); }
 

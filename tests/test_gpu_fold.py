@@ -1,0 +1,73 @@
+"""Folded (even/odd) spatial transforms (csrc/ks_transform.cu k_mode_gemm_fold):
+on uniform meshes the 1-D pencils are centro-symmetric, every eigenvector is
+even or odd, and the FD apply runs two half-size GEMMs per transform. The
+result must still match the oracle's dense transforms (reference
+tensorops.cpp:125-156) within the north_star tolerance, forward and adjoint,
+for even and odd axis lengths and every tile height (hc = ceil(n/2) up to 80)."""
+import os
+
+import numpy as np
+import pytest
+
+from helpers import setup_arrays, rel, maxrel
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+def _pair(ks, oracle, d, p, n_el, n_el_t, fold=True):
+    a = setup_arrays(ks, d, p, n_el, n_el_t)
+    old = os.environ.get("KS_FD_FOLD")
+    os.environ["KS_FD_FOLD"] = "1" if fold else "0"
+    try:
+        g = ks.FDPreconditioner.from_arrays(a["dims"], a["nu"], a["p"], a["U"], a["lam"], a["Lt"],
+                                            a["Mt"], a["Wt"])
+    finally:
+        if old is None:
+            del os.environ["KS_FD_FOLD"]
+        else:
+            os.environ["KS_FD_FOLD"] = old
+    o = oracle.OracleFD(a["dims"], a["nu"], a["p"], a["U"], a["lam"], a["Lt"], a["Mt"], a["Wt"])
+    return a, g, o
+
+
+# n = n_el for p = 2 (Dirichlet): even and odd lengths, tile heights 1..5
+CASES = [(3, 2, 8, 8), (2, 2, 7, 6), (3, 2, 16, 8), (2, 2, 33, 5), (2, 2, 64, 9),
+         (2, 2, 70, 4), (2, 2, 97, 3), (2, 2, 128, 3), (2, 2, 130, 2), (1, 2, 64, 64)]
+
+
+@pytest.mark.parametrize("d,p,n_el,n_el_t", CASES)
+def test_folded_fd_matches_oracle(gpu, oracle, d, p, n_el, n_el_t):
+    a, g, o = _pair(gpu, oracle, d, p, n_el, n_el_t)
+    assert g.info()["folded_axes"] == list(range(1, d + 1))
+    r = oracle.random_vec(o.N, 99)
+    z = g.apply(r)
+    zo = o.apply(r)
+    assert rel(z, zo) <= TOL and maxrel(z, zo) <= TOL
+    za = g.apply_adjoint(r)
+    zao = o.apply_adjoint(r)
+    assert rel(za, zao) <= TOL and maxrel(za, zao) <= TOL
+
+
+@pytest.mark.parametrize("d,p,n_el,n_el_t", [(3, 2, 16, 8), (2, 2, 64, 9)])
+def test_folded_equals_dense_transform(gpu, oracle, d, p, n_el, n_el_t):
+    """The fold symmetrises the eigenvectors; the difference to the dense GEMM
+    path (KS_FD_FOLD=0) is rounding-level (measured ~1e-13 at n = 64)."""
+    _, gf, o = _pair(gpu, oracle, d, p, n_el, n_el_t, fold=True)
+    _, gd, _ = _pair(gpu, oracle, d, p, n_el, n_el_t, fold=False)
+    assert gd.info()["folded_axes"] == []
+    r = oracle.random_vec(o.N, 5)
+    assert rel(gf.apply(r), gd.apply(r)) <= 1e-12
+
+
+def test_non_symmetric_eigenvectors_stay_dense(gpu, oracle):
+    """Perturbed eigenvectors (not even/odd) must not be folded."""
+    a = setup_arrays(gpu, 2, 2, 10, 6)
+    U = [np.array(u, dtype=np.float64).ravel().copy() for u in a["U"]]
+    U[0][3] += 1e-3
+    g = gpu.FDPreconditioner.from_arrays(a["dims"], a["nu"], a["p"], U, a["lam"], a["Lt"], a["Mt"], a["Wt"])
+    assert g.info()["folded_axes"] == [2]
+    o = oracle.OracleFD(a["dims"], a["nu"], a["p"], U, a["lam"], a["Lt"], a["Mt"], a["Wt"])
+    r = oracle.random_vec(o.N, 3)
+    assert rel(g.apply(r), o.apply(r)) <= TOL
