@@ -412,9 +412,7 @@ int ks_fd_create(int d, const int* dims, double nu, int p_t, const double* const
     B.nblk = lam_blk.size();
     B.lam_blk.alloc(B.nblk * sizeof(double));
     KS_CUDA(cudaMemcpy(B.lam_blk.p, lam_blk.data(), B.nblk * sizeof(double), cudaMemcpyHostToDevice));
-    B.ab.alloc((size_t)nt * B.ldab * B.nblk * sizeof(double2));
-    B.piv.alloc((size_t)nt * B.nblk);
-    B.flag.alloc(sizeof(int));
+    fd_blocks_alloc(B);
     launch_fd_factor(B, nu, f->Lt.as<double>(), f->Mt.as<double>(), f->Wsym.as<double2>(), f->stream);
     f->s0.alloc(f->N * sizeof(double2));
     f->s1.alloc(f->N * sizeof(double2));
@@ -458,26 +456,8 @@ int ks_fd_block(const ks_fd* fd, size_t i, ks_c64* ab, int* piv) {
     KS_REQUIRE(fd && ab && piv, KS_EINVAL, "ks_fd_block: NULL argument");
     KS_REQUIRE(i < fd->Ns, KS_EINVAL, "ks_fd_block: index out of range");
     ensure_device(fd->device);
-    const FdBlocks& B = fd->blocks;
     const size_t b = fd->fiber_block.empty() ? i : (size_t)fd->fiber_block[i];
-    size_t fb = b, fe = B.nblk, pbi = b, pst = B.nblk;
-    if (B.fused_nd > 0) {
-        const size_t rho = b % (size_t)B.fused_np, r = b / (size_t)B.fused_np;
-        fb = rho * (size_t)B.nt * B.ldab * B.fused_nd + r;
-        fe = B.fused_nd;
-        pbi = rho * (size_t)B.nt * B.fused_nd + r;
-        pst = B.fused_nd;
-    }
-    for (int k = 0; k < B.nt; ++k) {
-        for (int e = 0; e < B.ldab; ++e)
-            KS_CUDA(cudaMemcpy(ab + (size_t)k * B.ldab + e,
-                               B.ab.as<double2>() + fb + ((size_t)k * B.ldab + e) * fe,
-                               sizeof(double2), cudaMemcpyDeviceToHost));
-        unsigned char po = 0;
-        KS_CUDA(cudaMemcpy(&po, B.piv.as<unsigned char>() + pbi + (size_t)k * pst, 1,
-                           cudaMemcpyDeviceToHost));
-        piv[k] = k + po;
-    }
+    fd_block_to_host(fd->blocks, b, ab, piv);
     API_END
 }
 

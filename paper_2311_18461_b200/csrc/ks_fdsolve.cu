@@ -13,10 +13,13 @@
 //   solve                  solve_banded (src/eigensolve.cpp:123-140)
 //   adjoint solve          solve_banded_adjoint (src/eigensolve.cpp:148-170)
 //
-// Device layout ("block-interleaved"): band column k, band row e, block b at
-// ab[(k*ldab + e)*nblk + b], pivots piv[k*nblk + b] as the offset piv[k]-k in
-// [0, p]. Consecutive threads own consecutive fibers, so band accesses of a
-// warp coalesce.
+// Device layout (fd_band_index, ks_internal.hpp): per-block records by
+// default -- band column k of block b is ab[(b*nt + k)*rec + e], e < ldab,
+// with the pivot offset piv[k]-k stored as a double in slot ldab -- so one
+// fiber's step reads one contiguous 128 B record (p = 2) whichever block its
+// fiber maps to (with deduplication a warp's 32 fibers hit scattered blocks;
+// the earlier block-interleaved layout ab[(k*ldab + e)*nblk + b] wasted half of
+// every 32 B sector there and is kept as KS_FD_REC=0).
 //
 // Block deduplication: when all spatial axes carry the
 // same 1-D eigenvalues (uniform identical meshes, every BASELINE config), the
@@ -32,6 +35,9 @@
 // products (ac-bd, ad+bc), Smith-style division as in libgcc's __divdc3, and
 // |z| = hypot(re, im) for the pivot search.
 #include "ks_internal.hpp"
+
+#include <cstdlib>
+#include <cstring>
 
 namespace ks {
 
@@ -73,22 +79,12 @@ __global__ void k_fd_factor(double2* __restrict__ ab, unsigned char* __restrict_
                             int* __restrict__ flag, size_t ns, int nt, int p,
                             const double* __restrict__ lam_blk, double nu,
                             const double* __restrict__ Lt, const double* __restrict__ Mt,
-                            const double2* __restrict__ Wsym, int fused_nd, long long fused_np) {
+                            const double2* __restrict__ Wsym, int rec, int fused_nd, long long fused_np) {
     const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     if (i >= ns) return; // here ns = number of factored blocks
     const int ldab = 3 * p + 1, kuf = 2 * p, bwld = 2 * p + 1;
-    // layout: block-interleaved [k][e][block], or (fused_nd > 0) per rest column
-    // [rho][k][e][r] for block i = rho + Np * r (the fused axis-d kernel's fibers)
-    size_t base = i, estr = ns, kstr = (size_t)ldab * ns;
-    size_t pbase = i, pstr = ns;
-    if (fused_nd > 0) {
-        const size_t rho = i % (size_t)fused_np, r = i / (size_t)fused_np;
-        base = rho * (size_t)nt * ldab * fused_nd + r;
-        estr = fused_nd;
-        kstr = (size_t)ldab * fused_nd;
-        pbase = rho * (size_t)nt * fused_nd + r;
-        pstr = fused_nd;
-    }
+    const BandIndex bx = fd_band_index(i, nt, ldab, ns, rec, fused_nd, fused_np);
+    const size_t base = bx.fb, estr = bx.fe, kstr = bx.fk;
     // composite eigenvalue lambda_i = sum_l lambda_l[i_l], formed on the host in
     // the reference's summation order (fdsolver.cpp:30-42)
     const double lam = lam_blk[i];
@@ -97,7 +93,8 @@ __global__ void k_fd_factor(double2* __restrict__ ab, unsigned char* __restrict_
     };
     // fill: zero band, then H(r, c) for |r - c| <= p
     for (int c = 0; c < nt; ++c)
-        for (int e = 0; e < ldab; ++e) ab[base + (size_t)c * kstr + (size_t)e * estr] = make_double2(0.0, 0.0);
+        for (int e = 0; e < (rec > 0 ? rec : ldab); ++e)
+            ab[base + (size_t)c * kstr + (size_t)e * estr] = make_double2(0.0, 0.0);
     const double s2 = nu * nu * lam * lam; // nu*nu*lam*lam (left to right)
     const double s1 = nu * lam;
     for (int c = 0; c < nt; ++c) {
@@ -125,7 +122,8 @@ __global__ void k_fd_factor(double2* __restrict__ ab, unsigned char* __restrict_
                 pr = r;
             }
         }
-        piv[pbase + (size_t)k * pstr] = (unsigned char)(pr - k);
+        if (rec > 0) ab[base + (size_t)k * kstr + ldab] = make_double2((double)(pr - k), 0.0);
+        else piv[bx.pb + (size_t)k * bx.pk] = (unsigned char)(pr - k);
         if (best == 0.0) {
             atomicExch(flag, 1);
             return;
@@ -155,7 +153,7 @@ __global__ void __launch_bounds__(128) k_fd_solve(const double2* __restrict__ ab
                                                   const unsigned char* __restrict__ piv,
                                                   double2* __restrict__ X, size_t ns, int nt,
                                                   size_t nblk, const int* __restrict__ fblk,
-                                                  int tmajor, int fnd, long long fnp) {
+                                                  int tmajor, int rec, int fnd, long long fnp) {
     const size_t f = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     if (f >= ns) return;
     constexpr int ldab = 3 * P + 1, kuf = 2 * P;
@@ -168,24 +166,17 @@ __global__ void __launch_bounds__(128) k_fd_solve(const double2* __restrict__ ab
         __device__ double2& operator[](int k) const { return p[(size_t)k * s]; }
     } x{x0, xs};
     const size_t i = fblk ? (size_t)__ldg(fblk + f) : f; // factored block of this fiber
-    // factor address: block-interleaved, or per-rest-column (fused layout)
-    size_t fb = i, fe = nblk, pbi = i, pst = nblk;
-    if (fnd > 0) {
-        const size_t rho = i % (size_t)fnp, r = i / (size_t)fnp;
-        fb = rho * (size_t)nt * ldab * fnd + r;
-        fe = fnd;
-        pbi = rho * (size_t)nt * fnd + r;
-        pst = fnd;
-    }
-    auto band = [&](int k, int e) -> double2 {
-        return __ldg(ab + fb + ((size_t)k * ldab + e) * fe);
+    const BandIndex bx = fd_band_index(i, nt, ldab, nblk, rec, fnd, fnp);
+    auto band = [&](int k, int e) -> double2 { return __ldg(ab + bx.fb + (size_t)k * bx.fk + (size_t)e * bx.fe); };
+    auto pivot = [&](int k) -> int {
+        return rec > 0 ? (int)__ldg(&ab[bx.fb + (size_t)k * bx.fk + ldab].x) : (int)piv[bx.pb + (size_t)k * bx.pk];
     };
     // forward: L with row interchanges (eigensolve.cpp:127-133); w[m] = x[k+m]
     double2 w[P + 1];
 #pragma unroll
     for (int m = 0; m <= P; ++m) w[m] = m < nt ? x[m] : make_double2(0.0, 0.0);
     for (int k = 0; k < nt; ++k) {
-        const int po = piv[pbi + (size_t)k * pst];
+        const int po = pivot(k);
 #pragma unroll
         for (int m = 1; m <= P; ++m)
             if (po == m) {
@@ -223,7 +214,7 @@ __global__ void __launch_bounds__(128) k_fd_solve_adj(const double2* __restrict_
                                                       const unsigned char* __restrict__ piv,
                                                       double2* __restrict__ X, size_t ns, int nt,
                                                       size_t nblk, const int* __restrict__ fblk,
-                                                  int tmajor, int fnd, long long fnp) {
+                                                  int tmajor, int rec, int fnd, long long fnp) {
     const size_t f = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     if (f >= ns) return;
     constexpr int ldab = 3 * P + 1, kuf = 2 * P;
@@ -236,17 +227,10 @@ __global__ void __launch_bounds__(128) k_fd_solve_adj(const double2* __restrict_
         __device__ double2& operator[](int k) const { return p[(size_t)k * s]; }
     } x{x0, xs};
     const size_t i = fblk ? (size_t)__ldg(fblk + f) : f;
-    // factor address: block-interleaved, or per-rest-column (fused layout)
-    size_t fb = i, fe = nblk, pbi = i, pst = nblk;
-    if (fnd > 0) {
-        const size_t rho = i % (size_t)fnp, r = i / (size_t)fnp;
-        fb = rho * (size_t)nt * ldab * fnd + r;
-        fe = fnd;
-        pbi = rho * (size_t)nt * fnd + r;
-        pst = fnd;
-    }
-    auto band = [&](int k, int e) -> double2 {
-        return __ldg(ab + fb + ((size_t)k * ldab + e) * fe);
+    const BandIndex bx = fd_band_index(i, nt, ldab, nblk, rec, fnd, fnp);
+    auto band = [&](int k, int e) -> double2 { return __ldg(ab + bx.fb + (size_t)k * bx.fk + (size_t)e * bx.fe); };
+    auto pivot = [&](int k) -> int {
+        return rec > 0 ? (int)__ldg(&ab[bx.fb + (size_t)k * bx.fk + ldab].x) : (int)piv[bx.pb + (size_t)k * bx.pk];
     };
     // U^H z = y, forward; h[j] = x[k - 2P + j] (finalised values)
     double2 h[2 * P];
@@ -279,7 +263,7 @@ __global__ void __launch_bounds__(128) k_fd_solve_adj(const double2* __restrict_
         for (int m = 1; m <= P; ++m)
             if (k + m < nt) s = csub(s, cconjmul(band(k, kuf + m), g[m]));
         g[0] = s;
-        const int po = piv[pbi + (size_t)k * pst];
+        const int po = pivot(k);
 #pragma unroll
         for (int m = 1; m <= P; ++m)
             if (po == m) {
@@ -302,16 +286,48 @@ void launch_solve_p(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t st
     const unsigned grid = (unsigned)((B.ns + 127) / 128);
     if (adjoint) {
         k_fd_solve_adj<P><<<grid, 128, 0, st>>>(B.ab.as<double2>(), B.piv.as<unsigned char>(), X,
-                                                B.ns, B.nt, B.nblk, B.fiber_block.as<int>(), tm, B.fused_nd, B.fused_np);
+                                                B.ns, B.nt, B.nblk, B.fiber_block.as<int>(), tm, B.rec, B.fused_nd, B.fused_np);
         check_launch("k_fd_solve_adj");
     } else {
         k_fd_solve<P><<<grid, 128, 0, st>>>(B.ab.as<double2>(), B.piv.as<unsigned char>(), X,
-                                            B.ns, B.nt, B.nblk, B.fiber_block.as<int>(), tm, B.fused_nd, B.fused_np);
+                                            B.ns, B.nt, B.nblk, B.fiber_block.as<int>(), tm, B.rec, B.fused_nd, B.fused_np);
         check_launch("k_fd_solve");
     }
 }
 
 } // namespace
+
+void fd_blocks_alloc(FdBlocks& B) {
+    B.rec = 0;
+    if (B.fused_nd == 0) {
+        B.rec = B.ldab + 1;
+        if (const char* e = std::getenv("KS_FD_REC"))
+            if (std::strcmp(e, "0") == 0) B.rec = 0;
+    }
+    const size_t per = B.rec > 0 ? (size_t)B.rec : (size_t)B.ldab;
+    B.ab.alloc((size_t)B.nt * per * B.nblk * sizeof(double2));
+    if (B.rec == 0) B.piv.alloc((size_t)B.nt * B.nblk);
+    B.flag.alloc(sizeof(int));
+}
+
+void fd_block_to_host(const FdBlocks& B, size_t b, ks_c64* ab, int* piv) {
+    const BandIndex bx = fd_band_index(b, B.nt, B.ldab, B.nblk, B.rec, B.fused_nd, B.fused_np);
+    for (int k = 0; k < B.nt; ++k) {
+        for (int e = 0; e < B.ldab; ++e)
+            KS_CUDA(cudaMemcpy(ab + (size_t)k * B.ldab + e, B.ab.as<double2>() + bx.fb + (size_t)k * bx.fk + (size_t)e * bx.fe,
+                               sizeof(double2), cudaMemcpyDeviceToHost));
+        if (B.rec > 0) {
+            double2 v;
+            KS_CUDA(cudaMemcpy(&v, B.ab.as<double2>() + bx.fb + (size_t)k * bx.fk + B.ldab, sizeof(v),
+                               cudaMemcpyDeviceToHost));
+            piv[k] = k + (int)v.x;
+        } else {
+            unsigned char po = 0;
+            KS_CUDA(cudaMemcpy(&po, B.piv.as<unsigned char>() + bx.pb + (size_t)k * bx.pk, 1, cudaMemcpyDeviceToHost));
+            piv[k] = k + po;
+        }
+    }
+}
 
 void launch_fd_factor(FdBlocks& B, double nu, const double* Lt, const double* Mt,
                       const double2* Wsym, cudaStream_t st) {
@@ -319,7 +335,7 @@ void launch_fd_factor(FdBlocks& B, double nu, const double* Lt, const double* Mt
     const unsigned grid = (unsigned)((B.nblk + 127) / 128);
     k_fd_factor<<<grid, 128, 0, st>>>(B.ab.as<double2>(), B.piv.as<unsigned char>(),
                                       B.flag.as<int>(), B.nblk, B.nt, B.p, B.lam_blk.as<double>(), nu,
-                                      Lt, Mt, Wsym, B.fused_nd, B.fused_np);
+                                      Lt, Mt, Wsym, B.rec, B.fused_nd, B.fused_np);
     check_launch("k_fd_factor");
     int h = 0;
     KS_CUDA(cudaMemcpyAsync(&h, B.flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));

@@ -146,14 +146,55 @@ struct FdBlocks {
     int nt = 0, p = 0, ldab = 0;
     size_t ns = 0;      // fibers (= N_s)
     size_t nblk = 0;    // factored blocks (N_s, or fewer when deduplicated)
-    DevBuf ab;          // complex [nt][ldab][nblk]  (block-interleaved band columns)
-    DevBuf piv;         // uint8 [nt][nblk]  pivot offset piv[k]-k in 0..p
+    // band storage, one of three layouts (fd_band_index):
+    //   rec > 0 (default): per-block records ab[(b*nt + k)*rec + e], e < ldab, and the
+    //                      pivot offset as a double in slot ldab (rec = ldab + 1);
+    //                      a fiber's step-k band column is one contiguous record
+    //   fused_nd > 0:      per-rest-column layout of the fused axis-d kernel
+    //   otherwise:         block-interleaved ab[(k*ldab + e)*nblk + b], piv[k*nblk + b]
+    DevBuf ab;
+    DevBuf piv;         // uint8 pivot offsets piv[k]-k in 0..p (not used with rec)
+    int rec = 0;
     DevBuf flag;        // int: singular-pivot flag set by the factor kernel
     DevBuf lam_blk;     // double [nblk] composite eigenvalue of each block
     DevBuf fiber_block; // int [ns] block of each fiber (empty = identity)
     int fused_nd = 0;        // > 0: per-rest-column layout for the fused axis-d kernel
     long long fused_np = 0;  //      (block i = rho + fused_np * r, r < fused_nd)
 };
+// address of band entry (k, e) of block b: fb + k*fk + e*fe; pivot offset
+// (non-rec layouts) at piv[pb + k*pk]
+struct BandIndex {
+    size_t fb, fk, fe, pb, pk;
+};
+__host__ __device__ inline BandIndex fd_band_index(size_t b, int nt, int ldab, size_t nblk, int rec,
+                                                   int fused_nd, long long fused_np) {
+    BandIndex x;
+    if (rec > 0) {
+        x.fb = b * (size_t)nt * rec;
+        x.fk = rec;
+        x.fe = 1;
+        x.pb = x.pk = 0;
+    } else if (fused_nd > 0) {
+        const size_t rho = b % (size_t)fused_np, r = b / (size_t)fused_np;
+        x.fb = rho * (size_t)nt * ldab * fused_nd + r;
+        x.fe = fused_nd;
+        x.fk = (size_t)ldab * fused_nd;
+        x.pb = rho * (size_t)nt * fused_nd + r;
+        x.pk = fused_nd;
+    } else {
+        x.fb = b;
+        x.fe = nblk;
+        x.fk = (size_t)ldab * nblk;
+        x.pb = b;
+        x.pk = nblk;
+    }
+    return x;
+}
+// allocate ab / piv / flag for B.nblk blocks in the layout chosen by B.fused_nd
+// and KS_FD_REC (records unless KS_FD_REC=0)
+void fd_blocks_alloc(FdBlocks& B);
+// copy block b back to the host in BandedFactorization layout (eigensolve.hpp:36-42)
+void fd_block_to_host(const FdBlocks& B, size_t b, ks_c64* ab, int* piv);
 // time bands on device: Lt, Mt real (2p+1)xnt, Wsym complex
 void launch_fd_factor(FdBlocks& B, double nu, const double* Lt, const double* Mt,
                       const double2* Wsym, cudaStream_t st);

@@ -455,7 +455,10 @@ bool launch_colsweep(int nin, int nout, int bw, const double2* const* ip, double
                      int nir, int ioff, int boff, const int* ring_begin, const RingCon* ring_cons) {
     if (nir <= 0) nir = n;
     if (nout < 1 || nout > 8 || bw < 1 || bw > 4) return false;
-    if (s > 1 && ring_cons && nin >= 1 && !std::getenv("KS_KRON_ELEM")) {
+    // ring sweep: opt-in (KS_KRON_RING=1). Exact DRAM bytes but shared-memory
+    // bandwidth bound (each tap re-read from the ring per contribution):
+    // 5.69 ms vs 3.64 ms for the element kernel at c3 (profiles/round1_summary.md)
+    if (s > 1 && ring_cons && nin >= 1 && std::getenv("KS_KRON_RING")) {
         const int RW = 2 * bw + 1 + kPre;
         const size_t sm = (size_t)nin * RW * kRC * sizeof(double2);
         if (sm <= 200 * 1024) {

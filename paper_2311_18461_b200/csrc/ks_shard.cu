@@ -242,9 +242,7 @@ int ks_fdshard_create(int d, const int* dims, double nu, int p_t, const double* 
     KS_CUDA(cudaMemcpy(B.lam_blk.p, lam_blk.data(), B.nblk * sizeof(double), cudaMemcpyHostToDevice));
     B.fiber_block.alloc(nf * sizeof(int));
     KS_CUDA(cudaMemcpy(B.fiber_block.p, fblk.data(), nf * sizeof(int), cudaMemcpyHostToDevice));
-    B.ab.alloc((size_t)nt * B.ldab * B.nblk * sizeof(double2));
-    B.piv.alloc((size_t)nt * B.nblk);
-    B.flag.alloc(sizeof(int));
+    fd_blocks_alloc(B);
     launch_fd_factor(B, nu, h->Lt.as<double>(), h->Mt.as<double>(), h->Wsym.as<double2>(), h->stream);
     // scratch: slab-sized for phases 1/3, rest-sized for phase 2
     const size_t slab_n = (size_t)nt * P.Np * P.slab[rank].n();
