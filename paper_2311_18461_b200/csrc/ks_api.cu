@@ -373,7 +373,38 @@ int ks_fd_create(int d, const int* dims, double nu, int p_t, const double* const
         return sum;
     };
     int idx[3] = {0, 0, 0};
-    if (!dedup) {
+    // pair mode (default for d = 3 with identical axes 2, 3; KS_FD_PAIR=0 off):
+    // coalesced two-fiber solves, half the blocks of the plain layout
+    bool pair = d == 3 && !fused && dims[2] == dims[3] &&
+                std::memcmp(lambda[1], lambda[2], sizeof(double) * dims[2]) == 0;
+    if (const char* e = std::getenv("KS_FD_PAIR")) pair = pair && std::strcmp(e, "0") != 0;
+    if (pair) {
+        const int n1 = dims[1], n2 = dims[2];
+        std::vector<int2> prs;
+        std::vector<int> pidx((size_t)n2 * n2);
+        for (int i3 = 0; i3 < n2; ++i3)
+            for (int i2 = 0; i2 <= i3; ++i2) {
+                pidx[(size_t)i2 * n2 + i3] = pidx[(size_t)i3 * n2 + i2] = (int)prs.size();
+                prs.push_back(make_int2(i2, i3));
+            }
+        lam_blk.resize((size_t)n1 * prs.size());
+        for (size_t pp = 0; pp < prs.size(); ++pp)
+            for (int i1 = 0; i1 < n1; ++i1) {
+                const int id[3] = {i1, prs[pp].x, prs[pp].y};
+                lam_blk[(size_t)i1 + (size_t)n1 * pp] = ref_sum(id);
+            }
+        f->fiber_block.resize(f->Ns);
+        for (size_t i = 0; i < f->Ns; ++i) {
+            const int i1 = (int)(i % n1), i2 = (int)((i / n1) % n2), i3 = (int)(i / ((size_t)n1 * n2));
+            f->fiber_block[i] = i1 + n1 * pidx[(size_t)i2 * n2 + i3];
+        }
+        B.fiber_block.alloc(f->Ns * sizeof(int)); // adjoint / non-time-major solves
+        KS_CUDA(cudaMemcpy(B.fiber_block.p, f->fiber_block.data(), f->Ns * sizeof(int), cudaMemcpyHostToDevice));
+        B.pair_n1 = n1;
+        B.pair_n2 = n2;
+        B.pairs.alloc(prs.size() * sizeof(int2));
+        KS_CUDA(cudaMemcpy(B.pairs.p, prs.data(), prs.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    } else if (!dedup) {
         lam_blk.resize(f->Ns);
         for (size_t i = 0; i < f->Ns; ++i) {
             lam_blk[i] = ref_sum(idx);

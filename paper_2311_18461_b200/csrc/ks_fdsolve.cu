@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(128) k_fd_solve(const double2* __restrict__ ab
                                                   const unsigned char* __restrict__ piv,
                                                   double2* __restrict__ X, size_t ns, int nt,
                                                   size_t nblk, const int* __restrict__ fblk,
-                                                  int tmajor, int rec, int fnd, long long fnp) {
+                                                  int tmajor, int rec, int fnd, long long fnp, int pfd) {
     const size_t f = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     if (f >= ns) return;
     constexpr int ldab = 3 * P + 1, kuf = 2 * P;
@@ -171,12 +171,37 @@ __global__ void __launch_bounds__(128) k_fd_solve(const double2* __restrict__ ab
     auto pivot = [&](int k) -> int {
         return rec > 0 ? (int)__ldg(&ab[bx.fb + (size_t)k * bx.fk + ldab].x) : (int)piv[bx.pb + (size_t)k * bx.pk];
     };
+    // Each step's band row, pivot and the x entry entering the window are
+    // loaded one step ahead into registers (the loads of step k+1 are in
+    // flight while step k computes), and pfd > 0 adds an L2 prefetch of step
+    // k+pfd (no registers).
+    auto pf = [&](const void* a) { asm volatile("prefetch.global.L2 [%0];" ::"l"(a)); };
     // forward: L with row interchanges (eigensolve.cpp:127-133); w[m] = x[k+m]
     double2 w[P + 1];
 #pragma unroll
     for (int m = 0; m <= P; ++m) w[m] = m < nt ? x[m] : make_double2(0.0, 0.0);
+    double2 lb[P], xn;
+    int po_n;
+    auto load_f = [&](int k) {
+#pragma unroll
+        for (int m = 1; m <= P; ++m) lb[m - 1] = (k + m < nt) ? band(k, kuf + m) : make_double2(0.0, 0.0);
+        po_n = pivot(k);
+        xn = (k + P + 1 < nt) ? x[k + P + 1] : make_double2(0.0, 0.0);
+    };
+    load_f(0);
     for (int k = 0; k < nt; ++k) {
-        const int po = pivot(k);
+        double2 l[P];
+#pragma unroll
+        for (int m = 0; m < P; ++m) l[m] = lb[m];
+        const int po = po_n;
+        const double2 xin = xn;
+        if (k + 1 < nt) load_f(k + 1);
+        if (pfd > 0 && k + pfd < nt) {
+            const int kp = k + pfd;
+            pf(ab + bx.fb + (size_t)kp * bx.fk + (size_t)(kuf + 1) * bx.fe);
+            if (rec == 0) pf(piv + bx.pb + (size_t)kp * bx.pk);
+            if (kp + P + 1 < nt) pf(&x[kp + P + 1]);
+        }
 #pragma unroll
         for (int m = 1; m <= P; ++m)
             if (po == m) {
@@ -186,25 +211,42 @@ __global__ void __launch_bounds__(128) k_fd_solve(const double2* __restrict__ ab
             }
 #pragma unroll
         for (int m = 1; m <= P; ++m)
-            if (k + m < nt) w[m] = csub(w[m], cmul(band(k, kuf + m), w[0]));
+            if (k + m < nt) w[m] = csub(w[m], cmul(l[m - 1], w[0]));
         x[k] = w[0];
 #pragma unroll
         for (int m = 0; m < P; ++m) w[m] = w[m + 1];
-        w[P] = (k + P + 1 < nt) ? x[k + P + 1] : make_double2(0.0, 0.0);
+        w[P] = xin;
     }
     // backward: U, column oriented (eigensolve.cpp:134-139); u[j] = x[k-j]
     double2 u[2 * P + 1];
 #pragma unroll
     for (int j = 0; j <= 2 * P; ++j) u[j] = (nt - 1 - j >= 0) ? x[nt - 1 - j] : make_double2(0.0, 0.0);
+    double2 ub[2 * P + 1];
+    auto load_b = [&](int k) {
+#pragma unroll
+        for (int j = 0; j <= 2 * P; ++j) ub[j] = (k - j >= 0) ? band(k, kuf - j) : make_double2(0.0, 0.0);
+        xn = (k - 2 * P - 1 >= 0) ? x[k - 2 * P - 1] : make_double2(0.0, 0.0);
+    };
+    load_b(nt - 1);
     for (int k = nt - 1; k >= 0; --k) {
-        u[0] = cdiv(u[0], band(k, kuf));
+        double2 ucol[2 * P + 1];
+#pragma unroll
+        for (int j = 0; j <= 2 * P; ++j) ucol[j] = ub[j];
+        const double2 xin = xn;
+        if (k > 0) load_b(k - 1);
+        if (pfd > 0 && k - pfd >= 0) {
+            const int kp = k - pfd;
+            pf(ab + bx.fb + (size_t)kp * bx.fk);
+            if (kp - 2 * P - 1 >= 0) pf(&x[kp - 2 * P - 1]);
+        }
+        u[0] = cdiv(u[0], ucol[0]);
 #pragma unroll
         for (int j = 1; j <= 2 * P; ++j)
-            if (k - j >= 0) u[j] = csub(u[j], cmul(band(k, kuf - j), u[0]));
+            if (k - j >= 0) u[j] = csub(u[j], cmul(ucol[j], u[0]));
         x[k] = u[0];
 #pragma unroll
         for (int j = 0; j < 2 * P; ++j) u[j] = u[j + 1];
-        u[2 * P] = (k - 2 * P - 1 >= 0) ? x[k - 2 * P - 1] : make_double2(0.0, 0.0);
+        u[2 * P] = xin;
     }
 }
 
@@ -281,6 +323,247 @@ __global__ void __launch_bounds__(128) k_fd_solve_adj(const double2* __restrict_
         if (m - 1 < nt) x[m - 1] = g[m];
 }
 
+// ---------------------------------------------------------------------------
+// ring solve (time-major fibers): the same sweeps as k_fd_solve, but each
+// thread streams its band entries, pivot words and incoming x entries through
+// a private D-step cp.async ring in shared memory ([slot][entry][thread], so a
+// warp's 16 B accesses are contiguous), keeping D-1 steps of loads in flight
+// without holding them in registers. Threads never share slots, so no
+// barriers: cp.async.wait_group orders each thread's own copies.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cpa16(void* sdst, const void* g, bool v) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(g), "r"(v ? 16 : 0));
+}
+__device__ __forceinline__ void cpa4(void* sdst, const void* g, bool v) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(g), "r"(v ? 4 : 0));
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N> __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <int P, int D>
+__global__ void __launch_bounds__(128) k_fd_solve_ring(const double2* __restrict__ ab,
+                                                       const unsigned char* __restrict__ piv,
+                                                       double2* __restrict__ X, size_t ns, int nt, size_t nblk,
+                                                       const int* __restrict__ fblk, int rec, int fnd,
+                                                       long long fnp) {
+    constexpr int ldab = 3 * P + 1, kuf = 2 * P, NE = 2 * P + 2;
+    extern __shared__ __align__(16) double2 ring[]; // [D][NE][128], then int [D][128]
+    unsigned* pr = reinterpret_cast<unsigned*>(ring + (size_t)D * NE * 128);
+    const int t = threadIdx.x;
+    const size_t f = blockIdx.x * (size_t)128 + t;
+    if (f >= ns) return;
+    double2* x = X + f; // x[k * ns]
+    const size_t i = fblk ? (size_t)__ldg(fblk + f) : f;
+    const BandIndex bx = fd_band_index(i, nt, ldab, nblk, rec, fnd, fnp);
+    auto slot = [&](int k, int e) -> double2* { return ring + ((size_t)((k % D) * NE + e) * 128 + t); };
+    auto baddr = [&](int k, int e) -> const double2* { return ab + bx.fb + (size_t)k * bx.fk + (size_t)e * bx.fe; };
+    // pivot of step k: byte (or record slot) -> 4 B word in the ring
+    auto issue_f = [&](int k) {
+        if (k < nt) {
+#pragma unroll
+            for (int m = 1; m <= P; ++m) cpa16(slot(k, m - 1), k + m < nt ? baddr(k, kuf + m) : ab, k + m < nt);
+            cpa16(slot(k, P), k + P + 1 < nt ? x + (size_t)(k + P + 1) * ns : X, k + P + 1 < nt);
+            if (rec > 0) {
+                cpa16(slot(k, P + 1), baddr(k, ldab), true);
+            } else {
+                const size_t o = bx.pb + (size_t)k * bx.pk;
+                cpa4(pr + (k % D) * 128 + t, piv + (o & ~(size_t)3), true);
+            }
+        }
+        cpa_commit();
+    };
+    auto pivot_of = [&](int k) -> int {
+        if (rec > 0) return (int)slot(k, P + 1)->x;
+        const size_t o = bx.pb + (size_t)k * bx.pk;
+        return (int)((pr[(k % D) * 128 + t] >> (8 * (unsigned)(o & 3))) & 0xffu);
+    };
+    // forward: L with row interchanges (eigensolve.cpp:127-133); w[m] = x[k+m]
+    double2 w[P + 1];
+#pragma unroll
+    for (int m = 0; m <= P; ++m) w[m] = m < nt ? x[(size_t)m * ns] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int k = 0; k < D - 1; ++k) issue_f(k);
+    for (int k = 0; k < nt; ++k) {
+        cpa_wait<D - 2>();
+        issue_f(k + D - 1);
+        const int po = pivot_of(k);
+#pragma unroll
+        for (int m = 1; m <= P; ++m)
+            if (po == m) {
+                const double2 tt = w[0];
+                w[0] = w[m];
+                w[m] = tt;
+            }
+#pragma unroll
+        for (int m = 1; m <= P; ++m)
+            if (k + m < nt) w[m] = csub(w[m], cmul(*slot(k, m - 1), w[0]));
+        x[(size_t)k * ns] = w[0];
+        const double2 xin = *slot(k, P);
+#pragma unroll
+        for (int m = 0; m < P; ++m) w[m] = w[m + 1];
+        w[P] = xin;
+    }
+    cpa_wait<0>();
+    // backward: U, column oriented (eigensolve.cpp:134-139); u[j] = x[k-j]
+    auto issue_b = [&](int k) {
+        if (k >= 0) {
+#pragma unroll
+            for (int j = 0; j <= 2 * P; ++j) cpa16(slot(k, j), k - j >= 0 ? baddr(k, kuf - j) : ab, k - j >= 0);
+            const int kx = k - 2 * P - 1;
+            cpa16(slot(k, 2 * P + 1), kx >= 0 ? x + (size_t)kx * ns : X, kx >= 0);
+        }
+        cpa_commit();
+    };
+    double2 u[2 * P + 1];
+#pragma unroll
+    for (int j = 0; j <= 2 * P; ++j) u[j] = (nt - 1 - j >= 0) ? x[(size_t)(nt - 1 - j) * ns] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int q = 0; q < D - 1; ++q) issue_b(nt - 1 - q);
+    for (int k = nt - 1; k >= 0; --k) {
+        cpa_wait<D - 2>();
+        issue_b(k - (D - 1));
+        // slot index of step k: use (nt-1-k) so the ring advances monotonically
+        u[0] = cdiv(u[0], *slot(k, 0));
+#pragma unroll
+        for (int j = 1; j <= 2 * P; ++j)
+            if (k - j >= 0) u[j] = csub(u[j], cmul(*slot(k, j), u[0]));
+        x[(size_t)k * ns] = u[0];
+        const double2 xin = *slot(k, 2 * P + 1);
+#pragma unroll
+        for (int j = 0; j < 2 * P; ++j) u[j] = u[j + 1];
+        u[2 * P] = xin;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// pair solve (d = 3, axes 2 and 3 identical): block b = i1 + n1 * pidx(i2 <= i3)
+// serves the fibers (i1, i2, i3) and (i1, i3, i2), which one thread solves
+// together (two right-hand sides, one factor read). Consecutive threads take
+// consecutive i1, so band reads (block-interleaved layout) and both fibers'
+// time-major x accesses coalesce. Loads go through the per-thread cp.async ring
+// as in k_fd_solve_ring.
+// ---------------------------------------------------------------------------
+template <int P, int D>
+__global__ void __launch_bounds__(128) k_fd_solve_pair(const double2* __restrict__ ab,
+                                                       const unsigned char* __restrict__ piv,
+                                                       double2* __restrict__ X, size_t ns, int nt, size_t nblk,
+                                                       int n1, int n2, const int2* __restrict__ pairs) {
+    constexpr int kuf = 2 * P, NE = 2 * P + 3;
+    extern __shared__ __align__(16) double2 ring[]; // [D][NE][128], then unsigned [D][128]
+    unsigned* pr = reinterpret_cast<unsigned*>(ring + (size_t)D * NE * 128);
+    const int t = threadIdx.x;
+    const size_t b = blockIdx.x * (size_t)128 + t;
+    if (b >= nblk) return;
+    const int i1 = (int)(b % (size_t)n1);
+    const int2 q = __ldg(pairs + b / (size_t)n1);
+    const bool hb = q.x != q.y;
+    double2* xa = X + (size_t)i1 + (size_t)n1 * ((size_t)q.x + (size_t)n2 * q.y);
+    double2* xb = X + (size_t)i1 + (size_t)n1 * ((size_t)q.y + (size_t)n2 * q.x);
+    auto slot = [&](int k, int e) -> double2* { return ring + ((size_t)((k % D) * NE + e) * 128 + t); };
+    auto baddr = [&](int k, int e) -> const double2* { return ab + b + ((size_t)k * (3 * P + 1) + e) * nblk; };
+    auto issue_f = [&](int k) {
+        if (k < nt) {
+#pragma unroll
+            for (int m = 1; m <= P; ++m) cpa16(slot(k, m - 1), k + m < nt ? baddr(k, kuf + m) : ab, k + m < nt);
+            const int kx = k + P + 1;
+            cpa16(slot(k, P), kx < nt ? xa + (size_t)kx * ns : X, kx < nt);
+            cpa16(slot(k, P + 1), kx < nt && hb ? xb + (size_t)kx * ns : X, kx < nt && hb);
+            const size_t o = (size_t)k * nblk + b;
+            cpa4(pr + (k % D) * 128 + t, piv + (o & ~(size_t)3), true);
+        }
+        cpa_commit();
+    };
+    // forward: L with row interchanges (eigensolve.cpp:127-133)
+    double2 wa[P + 1], wb[P + 1];
+#pragma unroll
+    for (int m = 0; m <= P; ++m) {
+        wa[m] = m < nt ? xa[(size_t)m * ns] : make_double2(0.0, 0.0);
+        wb[m] = m < nt && hb ? xb[(size_t)m * ns] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int k = 0; k < D - 1; ++k) issue_f(k);
+    for (int k = 0; k < nt; ++k) {
+        cpa_wait<D - 2>();
+        issue_f(k + D - 1);
+        const size_t o = (size_t)k * nblk + b;
+        const int po = (int)((pr[(k % D) * 128 + t] >> (8 * (unsigned)(o & 3))) & 0xffu);
+#pragma unroll
+        for (int m = 1; m <= P; ++m)
+            if (po == m) {
+                double2 tt = wa[0];
+                wa[0] = wa[m];
+                wa[m] = tt;
+                tt = wb[0];
+                wb[0] = wb[m];
+                wb[m] = tt;
+            }
+#pragma unroll
+        for (int m = 1; m <= P; ++m)
+            if (k + m < nt) {
+                const double2 l = *slot(k, m - 1);
+                wa[m] = csub(wa[m], cmul(l, wa[0]));
+                wb[m] = csub(wb[m], cmul(l, wb[0]));
+            }
+        xa[(size_t)k * ns] = wa[0];
+        if (hb) xb[(size_t)k * ns] = wb[0];
+        const double2 ina = *slot(k, P), inb = *slot(k, P + 1);
+#pragma unroll
+        for (int m = 0; m < P; ++m) {
+            wa[m] = wa[m + 1];
+            wb[m] = wb[m + 1];
+        }
+        wa[P] = ina;
+        wb[P] = inb;
+    }
+    cpa_wait<0>();
+    // backward: U, column oriented (eigensolve.cpp:134-139)
+    auto issue_b = [&](int k) {
+        if (k >= 0) {
+#pragma unroll
+            for (int j = 0; j <= 2 * P; ++j) cpa16(slot(k, j), k - j >= 0 ? baddr(k, kuf - j) : ab, k - j >= 0);
+            const int kx = k - 2 * P - 1;
+            cpa16(slot(k, 2 * P + 1), kx >= 0 ? xa + (size_t)kx * ns : X, kx >= 0);
+            cpa16(slot(k, 2 * P + 2), kx >= 0 && hb ? xb + (size_t)kx * ns : X, kx >= 0 && hb);
+        }
+        cpa_commit();
+    };
+    double2 ua[2 * P + 1], ub[2 * P + 1];
+#pragma unroll
+    for (int j = 0; j <= 2 * P; ++j) {
+        const bool v = nt - 1 - j >= 0;
+        ua[j] = v ? xa[(size_t)(nt - 1 - j) * ns] : make_double2(0.0, 0.0);
+        ub[j] = v && hb ? xb[(size_t)(nt - 1 - j) * ns] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int qq = 0; qq < D - 1; ++qq) issue_b(nt - 1 - qq);
+    for (int k = nt - 1; k >= 0; --k) {
+        cpa_wait<D - 2>();
+        issue_b(k - (D - 1));
+        const double2 dg = *slot(k, 0);
+        ua[0] = cdiv(ua[0], dg);
+        ub[0] = cdiv(ub[0], dg);
+#pragma unroll
+        for (int j = 1; j <= 2 * P; ++j)
+            if (k - j >= 0) {
+                const double2 uu = *slot(k, j);
+                ua[j] = csub(ua[j], cmul(uu, ua[0]));
+                ub[j] = csub(ub[j], cmul(uu, ub[0]));
+            }
+        xa[(size_t)k * ns] = ua[0];
+        if (hb) xb[(size_t)k * ns] = ub[0];
+        const double2 ina = *slot(k, 2 * P + 1), inb = *slot(k, 2 * P + 2);
+#pragma unroll
+        for (int j = 0; j < 2 * P; ++j) {
+            ua[j] = ua[j + 1];
+            ub[j] = ub[j + 1];
+        }
+        ua[2 * P] = ina;
+        ub[2 * P] = inb;
+    }
+}
+
 template <int P>
 void launch_solve_p(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t st, int tm) {
     const unsigned grid = (unsigned)((B.ns + 127) / 128);
@@ -289,8 +572,45 @@ void launch_solve_p(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t st
                                                 B.ns, B.nt, B.nblk, B.fiber_block.as<int>(), tm, B.rec, B.fused_nd, B.fused_np);
         check_launch("k_fd_solve_adj");
     } else {
+        static const int pfd = [] {
+            const char* e = std::getenv("KS_FD_PFD");
+            return e ? std::atoi(e) : 0;
+        }();
+        if (tm && B.pair_n1 > 0) {
+            constexpr int NE = 2 * P + 3, D = 4;
+            const size_t sm = (size_t)D * NE * 128 * sizeof(double2) + (size_t)D * 128 * sizeof(unsigned);
+            static bool attr = false;
+            if (!attr) {
+                KS_CUDA(cudaFuncSetAttribute(k_fd_solve_pair<P, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)sm));
+                attr = true;
+            }
+            const unsigned gp = (unsigned)((B.nblk + 127) / 128);
+            k_fd_solve_pair<P, D><<<gp, 128, sm, st>>>(B.ab.as<double2>(), B.piv.as<unsigned char>(), X, B.ns,
+                                                       B.nt, B.nblk, B.pair_n1, B.pair_n2, B.pairs.as<int2>());
+            check_launch("k_fd_solve_pair");
+            return;
+        }
+        static const int ring = [] {
+            const char* e = std::getenv("KS_FD_RING");
+            return e ? std::atoi(e) : 4;
+        }();
+        if (tm && (ring == 4 || ring == 8)) {
+            constexpr int NE = 2 * P + 2;
+            auto go = [&](auto kern, int D) {
+                const size_t sm = (size_t)D * NE * 128 * sizeof(double2) + (size_t)D * 128 * sizeof(unsigned);
+                KS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+                kern<<<grid, 128, sm, st>>>(B.ab.as<double2>(), B.piv.as<unsigned char>(), X, B.ns, B.nt, B.nblk,
+                                            B.fiber_block.as<int>(), B.rec, B.fused_nd, B.fused_np);
+            };
+            if (ring == 8) go(k_fd_solve_ring<P, 8>, 8);
+            else go(k_fd_solve_ring<P, 4>, 4);
+            check_launch("k_fd_solve_ring");
+            return;
+        }
         k_fd_solve<P><<<grid, 128, 0, st>>>(B.ab.as<double2>(), B.piv.as<unsigned char>(), X,
-                                            B.ns, B.nt, B.nblk, B.fiber_block.as<int>(), tm, B.rec, B.fused_nd, B.fused_np);
+                                            B.ns, B.nt, B.nblk, B.fiber_block.as<int>(), tm, B.rec, B.fused_nd,
+                                            B.fused_np, pfd);
         check_launch("k_fd_solve");
     }
 }
@@ -299,14 +619,16 @@ void launch_solve_p(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t st
 
 void fd_blocks_alloc(FdBlocks& B) {
     B.rec = 0;
-    if (B.fused_nd == 0) {
-        B.rec = B.ldab + 1;
+    if (B.fused_nd == 0 && B.pair_n1 == 0) {
+        // records are opt-in (KS_FD_REC=1): measured slower at c3 (0.84 vs 0.56 ms,
+        // 2.3 GB vs 1.05 GB DRAM read -- the interleaved layout's sectors are shared
+        // by neighbouring blocks that concurrently running fibers also read)
         if (const char* e = std::getenv("KS_FD_REC"))
-            if (std::strcmp(e, "0") == 0) B.rec = 0;
+            if (std::strcmp(e, "1") == 0) B.rec = B.ldab + 1;
     }
     const size_t per = B.rec > 0 ? (size_t)B.rec : (size_t)B.ldab;
     B.ab.alloc((size_t)B.nt * per * B.nblk * sizeof(double2));
-    if (B.rec == 0) B.piv.alloc((size_t)B.nt * B.nblk);
+    if (B.rec == 0) B.piv.alloc((size_t)B.nt * B.nblk + 4); // +4: 4 B cp.async words
     B.flag.alloc(sizeof(int));
 }
 

@@ -147,7 +147,7 @@ struct FdBlocks {
     size_t ns = 0;      // fibers (= N_s)
     size_t nblk = 0;    // factored blocks (N_s, or fewer when deduplicated)
     // band storage, one of three layouts (fd_band_index):
-    //   rec > 0 (default): per-block records ab[(b*nt + k)*rec + e], e < ldab, and the
+    //   rec > 0:           step-major records ab[(k*nblk + b)*rec + e], e < ldab, and the
     //                      pivot offset as a double in slot ldab (rec = ldab + 1);
     //                      a fiber's step-k band column is one contiguous record
     //   fused_nd > 0:      per-rest-column layout of the fused axis-d kernel
@@ -158,6 +158,10 @@ struct FdBlocks {
     DevBuf flag;        // int: singular-pivot flag set by the factor kernel
     DevBuf lam_blk;     // double [nblk] composite eigenvalue of each block
     DevBuf fiber_block; // int [ns] block of each fiber (empty = identity)
+    // pair mode (d = 3, axes 2 and 3 identical): block b = i1 + n1 * pidx over
+    // pairs (i2 <= i3), solved for fibers (i1, i2, i3) and (i1, i3, i2) together
+    int pair_n1 = 0, pair_n2 = 0;
+    DevBuf pairs;       // int2 [npairs] (i2, i3)
     int fused_nd = 0;        // > 0: per-rest-column layout for the fused axis-d kernel
     long long fused_np = 0;  //      (block i = rho + fused_np * r, r < fused_nd)
 };
@@ -170,8 +174,8 @@ __host__ __device__ inline BandIndex fd_band_index(size_t b, int nt, int ldab, s
                                                    int fused_nd, long long fused_np) {
     BandIndex x;
     if (rec > 0) {
-        x.fb = b * (size_t)nt * rec;
-        x.fk = rec;
+        x.fb = b * (size_t)rec;
+        x.fk = nblk * (size_t)rec;
         x.fe = 1;
         x.pb = x.pk = 0;
     } else if (fused_nd > 0) {
