@@ -43,6 +43,13 @@ def fd_flops_per_dof(dims, p):
     return 8 * sum(dims[1:]) + 24 * p + 8
 
 
+def fd_folded_flops_per_dof(dims, p, folded):
+    """Flops of the transforms as executed: a folded axis does two (n/2 x n/2)
+    products (4n flop/DOF for forward + inverse, plus 2 fold adds each way)."""
+    t = sum((4 * dims[l] + 4) if l in folded else 8 * dims[l] for l in range(1, len(dims)))
+    return t + 24 * p + 8
+
+
 def matvec_flops_per_dof(d, p):
     return 24 * d * (2 * p + 1)
 
@@ -380,14 +387,27 @@ def main():
                                              "seconds": rep2.solve_seconds,
                                              "dofs": p2.N_dof}
 
-    # ---- roofline: dominant kernel = the spatial transform GEMM ----
-    gemm_flops = 2 * sum(4.0 * dims[l] * n for l in range(1, d + 1))  # fwd + inv, per apply
-    achieved = gemm_flops / (ms_gemm * 1e-3) / 1e12
+    # ---- roofline: dominant kernel = the spatial transform (mode product) ----
+    info = P.info()
+    folded = set(info["folded_axes"])
+    nlaunch = 2 * d                                   # transform launches per apply
+    t_launch = ms_gemm * 1e-3 / nlaunch               # average transform launch (CUDA events)
+    bytes_launch = 32.0 * n                           # algorithmic: read X + write Y, 16 B each
+    flops_launch = sum((2 * dims[l] + 2) if l in folded else 4 * dims[l] for l in range(1, d + 1)) * n / d
     pk = peaks()
-    fd_f = fd_flops_per_dof(dims, p) * n
-    fd_roof_s = max(fd_f / (fp64_peak * 1e12), 32.0 * n / (pk["hbm_gbs"] * 1e9))
+    hbm_peak = pk.get("hbm_gbs", 6650.0)
+    gemm_hbm = bytes_launch / t_launch / 1e9
+    gemm_tf = flops_launch / t_launch / 1e12
+    hbm_bound = bytes_launch / (hbm_peak * 1e9) >= flops_launch / (fp64_peak * 1e12)
+    # whole FD apply: executed flops vs. this 2d+1 pass decomposition's HBM traffic
+    # (each pass reads and writes the 16 B/DOF tensor; the solve also streams its factors)
+    fd_f = fd_folded_flops_per_dof(dims, p, folded) * n
+    fac_bytes = info["blocks"] * dims[0] * (3 * p + 1) * 16 + info["blocks"] * dims[0]
+    fd_bytes = (2 * d + 1) * 32.0 * n + fac_bytes
+    fd_roof_s = max(fd_f / (fp64_peak * 1e12), fd_bytes / (hbm_peak * 1e9))
+    fd_roof_compulsory_s = max(fd_f / (fp64_peak * 1e12), (32.0 * n + fac_bytes) / (hbm_peak * 1e9))
     mv_roof_s = max(matvec_flops_per_dof(d, p) * n / (fp64_peak * 1e12),
-                    32.0 * n / (pk["hbm_gbs"] * 1e9))
+                    32.0 * n / (hbm_peak * 1e9))
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -407,20 +427,36 @@ def main():
                        "dims": dims, "dofs": n,
                        "parallelism": "replicas" if ws > 1 else "single",
                        "l2": "inputs (272 MB/vector) larger than L2; no flush",
-                       "transform_engine": {0: "dfma", 1: "dmma_v1", 2: "dmma_v2"}[ks.lib().ks_transform_engine()]},
+                       "transform_engine": {0: "dfma", 1: "dmma_v1", 2: "dmma_v2"}[ks.lib().ks_transform_engine()]
+                       + ("+fold" if P.info()["folded_axes"] else "")},
             "e2e": {"value": e2e_val, "unit": "DOF/s", "h2d_bytes_per_step": n * 16,
                     "d2h_bytes_per_step": n * 16, "ms_per_step": e2e_s * 1e3},
             "gpu_launches": launches,
-            "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak,
-                         "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": None,
-                         "kernel": "k_mode_gemm (spatial transform)",
-                         "peak_source": "measured live: DFMA %.2f / DMMA %.2f TFLOP/s microbenchmarks"
-                                        % (dfma, dmma),
+            "roofline": ({"bound": "hbm", "achieved": gemm_hbm, "peak": hbm_peak, "unit": "GB/s",
+                          "frac": gemm_hbm / hbm_peak} if hbm_bound else
+                         {"bound": "fp64", "achieved": gemm_tf, "peak": fp64_peak, "unit": "TFLOP/s",
+                          "frac": gemm_tf / fp64_peak}) | {
+                         "traffic": None,
+                         "kernel": "k_mode_gemm_fold" if folded else "k_mode_gemm_dmma2",
+                         "algorithmic_bytes_per_launch": bytes_launch,
+                         "flops_per_launch": flops_launch,
+                         "launch_ms": t_launch * 1e3,
+                         "fp64_tflops": gemm_tf, "fp64_frac": gemm_tf / fp64_peak,
+                         "hbm_gbs": gemm_hbm, "hbm_frac": gemm_hbm / hbm_peak,
+                         "peak_source": "HBM: MEASURED_PEAKS.json hbm_gbs; FP64: measured live "
+                                        "DFMA %.2f / DMMA %.2f TFLOP/s microbenchmarks" % (dfma, dmma),
                          "mixed_dfma_dmma_tflops": mixed,
                          "gemm_ms_per_apply": ms_gemm},
             "fd_apply": {"ms": ms_fd, "roofline_ms": fd_roof_s * 1e3,
                          "frac_of_roofline": fd_roof_s * 1e3 / ms_fd,
-                         "flops_per_dof": fd_flops_per_dof(dims, p), "wall_s": wall_fd},
+                         "roofline_basis": f"max(executed flops / FP64 peak, {2 * d + 1}-pass HBM traffic "
+                                           "(16 B/DOF in + out per pass, factors once) / HBM peak)",
+                         "roofline_compulsory_ms": fd_roof_compulsory_s * 1e3,
+                         "frac_of_compulsory_roofline": fd_roof_compulsory_s * 1e3 / ms_fd,
+                         "flops_per_dof_executed": fd_folded_flops_per_dof(dims, p, folded),
+                         "flops_per_dof_reference_algorithm": fd_flops_per_dof(dims, p),
+                         "folded_axes": sorted(folded), "factored_blocks": info["blocks"],
+                         "wall_s": wall_fd},
             "matvec": {"ms": ms_mv, "dof_per_s": ws * n / (ms_mv * 1e-3),
                        "roofline_ms": mv_roof_s * 1e3, "frac_of_roofline": mv_roof_s * 1e3 / ms_mv,
                        "plan": A.plan_info(),

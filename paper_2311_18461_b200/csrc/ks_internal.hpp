@@ -130,6 +130,7 @@ void launch_mode_gemm(const double* At, int n, const double* X, double* Y,
 // GEMMs instead of one (ks_transform.cu)
 struct FoldAxis {
     int n = 0, hc = 0, th = 0; // hc = ceil(n/2) even eigenvectors; tile height 16*th >= hc
+    int kst = 0;               // stored k rows of each half matrix (zero padded)
     DevBuf fwd, inv;           // [2][Kp][16*th] symmetrised half matrices (even, odd), k-major
     DevBuf rmap;               // int [2][16*th]: even eigen-indices, odd eigen-indices
 };

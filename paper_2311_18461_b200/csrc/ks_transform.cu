@@ -31,6 +31,7 @@
 #include <algorithm>
 #include <cstring>
 #include <cmath>
+#include <cstdio>
 #include <vector>
 
 namespace ks {
@@ -330,6 +331,7 @@ struct ColMap {
     long long Ns;      // spatial size (T modes)
     long long ntb;     // number of time blocks (T modes)
     long long ntiles;
+    int tw = 64;       // complex columns per tile
 };
 
 // offsets (doubles) and row strides of complex column j of tile tile
@@ -341,7 +343,7 @@ struct TileBase {
 __device__ __forceinline__ TileBase tile_base(const ColMap& M, long long tile) {
     TileBase b;
     if (M.mode == MAP_STD) {
-        b.q0 = tile * 64;
+        b.q0 = tile * M.tw;
         b.o0 = b.q0 / M.s;
         b.r0 = b.q0 - b.o0 * M.s;
         b.tb = b.rb = 0;
@@ -658,6 +660,30 @@ void launch_tm(int engine, const double* At, int n, const double* X, double* Y, 
     }
 }
 
+// TMA bulk copies (cp.async.bulk) completing on an mbarrier
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+    unsigned ok = 0;
+    do {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                     : "=r"(ok)
+                     : "r"(smem_u32(b)), "r"(parity)
+                     : "memory");
+    } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // Folded (even/odd) transform. On a uniform mesh the 1-D pencils are
 // centro-symmetric (J K J = K, J M J = M, J the flip), so every eigenvector is
@@ -674,23 +700,29 @@ void launch_tm(int engine, const double* At, int n, const double* X, double* Y, 
 // gathered by cp.async, so the fold is two FADDs per B fragment (forward) or
 // nothing (inverse). Each warp owns the same (half-row, column) block of both
 // GEMMs, so the inverse unfold happens in registers.
-// Resident matrices: Af[2][Kp][H] (k-major; [0] even, [1] odd), Kp = 8 * nkc.
+// Resident matrices: Af[2][kst][H] (k-major; [0] even, [1] odd, zero padded), staged as nkc*KC rows.
 // ---------------------------------------------------------------------------
-template <int TH, bool INV, int STG = kStages>
-__global__ void __launch_bounds__(kThreads, (TH <= 2 ? 2 : 1))
-k_mode_gemm_fold(const double* __restrict__ Af, const int* __restrict__ rmap, int n, int hc, int nkc,
-                 const double* __restrict__ X, double* __restrict__ Y, ColMap M) {
+template <int TH, bool INV, int KC, int STG, int MINB, int BNC, bool TMA>
+__global__ void __launch_bounds__(kThreads, MINB)
+k_mode_gemm_fold(const double* __restrict__ Af, int Kst, const int* __restrict__ rmap, int n, int hc, int nkc,
+                 const double* __restrict__ X, double* __restrict__ Y, ColMap M, int dry) {
     constexpr int H = 16 * TH;
     constexpr int MT = TH; // 8-row blocks per warp per GEMM (H/2 half-rows per warp)
     constexpr int BMP = H + 4;
-    constexpr int BNP = kBN + 4;
+    constexpr int BND = 2 * BNC;     // doubles per tile row
+    constexpr int BNP = BND + 4;     // == 4 (mod 16): conflict-free fragment loads
+    constexpr int NF = BND / 32;     // 8-column fragments per warp
+    constexpr int RPP = kThreads / BNC; // smem rows per loader pass
+    constexpr int SR = 2 * KC; // smem rows per stage: KC top + KC bottom
     extern __shared__ __align__(16) double smem[];
-    const int Kp = nkc * 8;
+    const int Kp = nkc * KC;
     double* Ae = smem;                        // [Kp][BMP]
     double* Ao = Ae + (size_t)Kp * BMP;       // [Kp][BMP]
-    double* Bs = Ao + (size_t)Kp * BMP;       // [STG][16][BNP]
-    int* rE = reinterpret_cast<int*>(Bs + (size_t)STG * 16 * BNP); // [H] even eigen-indices
+    double* Bs = Ao + (size_t)Kp * BMP;       // [STG][SR][BNP]
+    int* rE = reinterpret_cast<int*>(Bs + (size_t)STG * SR * BNP); // [H] even eigen-indices
     int* rO = rE + H;                                               // [H] odd eigen-indices
+    // TMA: one mbarrier per stage (8 B aligned: rE/rO hold 2H ints)
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(rO + H);
     const int no = n - hc;
     const long long in_rs = M.mode == MAP_TIN ? 2 * M.Np : 2 * M.s;
     const long long out_rs = M.mode == MAP_TOUT ? 2 * M.Np : 2 * M.s;
@@ -700,20 +732,66 @@ k_mode_gemm_fold(const double* __restrict__ Af, const int* __restrict__ rmap, in
 
     for (int e = tid; e < Kp * H; e += kThreads) {
         const int k = e / H, r = e - k * H;
-        Ae[k * BMP + r] = __ldg(Af + e);
-        Ao[k * BMP + r] = __ldg(Af + (size_t)Kp * H + e);
+        const bool v = k < Kst;
+        Ae[k * BMP + r] = v ? __ldg(Af + e) : 0.0;
+        Ao[k * BMP + r] = v ? __ldg(Af + (size_t)Kst * H + e) : 0.0;
     }
     for (int e = tid; e < 2 * H; e += kThreads) rE[e] = __ldg(rmap + e);
+    if (TMA) {
+        // rows that are never loaded (past hc / n-hc) must hold finite values
+        for (int e = tid; e < STG * SR * BNP; e += kThreads) Bs[e] = 0.0;
+        if (tid == 0) {
+            for (int q = 0; q < STG; ++q) mbar_init(bar + q, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+    }
     __syncthreads();
 
-    const int lcp = tid & 63, lrow0 = tid >> 6;
+    const int lcp = tid % BNC, lrow0 = tid / BNC;
     const int my_tiles =
         ntiles > (long long)blockIdx.x ? (int)((ntiles - 1 - (long long)blockIdx.x) / gridDim.x + 1) : 0;
     const int nwork = my_tiles * nkc;
     long long cur_tile = -1, cur_in = 0;
     bool cur_valid = false;
 
+    auto issue_tma = [&](int w) {
+        if (warp != 0 || w >= nwork) return;
+        const int wt = w / nkc;
+        const long long tile = (long long)blockIdx.x + (long long)wt * gridDim.x;
+        const int kc = w - wt * nkc;
+        const TileBase tb = tile_base(M, tile);
+        const long long ncol = M.Q - tb.q0 < BNC ? M.Q - tb.q0 : BNC;
+        const long long seg1 = M.s - tb.r0 < ncol ? M.s - tb.r0 : ncol;
+        const int jj = lane;
+        const int q = kc * KC + (jj % KC);
+        int src = 0;
+        bool v = jj < SR;
+        if (!INV) {
+            src = jj < KC ? q : n - 1 - q;
+            v = v && (jj < KC ? q < hc : q < n - hc);
+        } else {
+            v = v && (jj < KC ? q < hc : q < no);
+            if (v) src = jj < KC ? rE[q] : rO[q];
+        }
+        const unsigned mine = v ? (unsigned)(ncol * 16) : 0u;
+        const unsigned total = __reduce_add_sync(0xffffffffu, mine);
+        unsigned long long* b = bar + (w % STG);
+        if (lane == 0) mbar_arrive_tx(b, total);
+        __syncwarp();
+        if (v) {
+            double* dst = Bs + (size_t)(w % STG) * SR * BNP + jj * BNP;
+            const double* g = X + 2 * (tb.o0 * (long long)n * M.s + (long long)src * M.s + tb.r0);
+            bulk_g2s(dst, g, (unsigned)(seg1 * 16), b);
+            if (ncol > seg1)
+                bulk_g2s(dst + 2 * seg1, X + 2 * ((tb.o0 + 1) * (long long)n * M.s + (long long)src * M.s),
+                         (unsigned)((ncol - seg1) * 16), b);
+        }
+    };
     auto issue = [&](int w) {
+        if (TMA) {
+            issue_tma(w);
+            return;
+        }
         if (w < nwork) {
             const int wt = w / nkc;
             const long long tile = (long long)blockIdx.x + (long long)wt * gridDim.x;
@@ -723,21 +801,21 @@ k_mode_gemm_fold(const double* __restrict__ Af, const int* __restrict__ rmap, in
                 cur_valid = colmap(M, n, tile_base(M, tile), lcp, cur_in, dummy);
                 cur_tile = tile;
             }
-            double* bs = Bs + (size_t)(w % STG) * 16 * BNP;
+            double* bs = Bs + (size_t)(w % STG) * SR * BNP;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int jj = lrow0 + 4 * k; // smem row 0..15
-                const int q = kc * 8 + (jj & 7);
+            for (int k = 0; k < SR / RPP; ++k) {
+                const int jj = lrow0 + RPP * k; // smem row 0..SR-1
+                const int q = kc * KC + (jj % KC);
                 int src;
                 bool v;
                 if (!INV) {
-                    src = jj < 8 ? q : n - 1 - q;
-                    v = jj < 8 ? q < hc : q < n - hc; // odd n: the middle row has no mirror
+                    src = jj < KC ? q : n - 1 - q;
+                    v = jj < KC ? q < hc : q < n - hc; // odd n: the middle row has no mirror
                 } else {
-                    v = jj < 8 ? q < hc : q < no;
-                    src = v ? (jj < 8 ? rE[q] : rO[q]) : 0;
+                    v = jj < KC ? q < hc : q < no;
+                    src = v ? (jj < KC ? rE[q] : rO[q]) : 0;
                 }
-                v = v && cur_valid;
+                v = v && cur_valid && dry != 3;
                 cp_async16(bs + jj * BNP + 2 * lcp,
                            v ? (const void*)(X + cur_in + (long long)src * in_rs) : (const void*)X, v);
             }
@@ -745,55 +823,57 @@ k_mode_gemm_fold(const double* __restrict__ Af, const int* __restrict__ rmap, in
         cp_async_commit();
     };
 
-    double acc[2][MT][4][2];
+    double acc[2][MT][NF][2];
 #pragma unroll
     for (int g = 0; g < 2; ++g)
 #pragma unroll
         for (int i = 0; i < MT; ++i)
 #pragma unroll
-            for (int m = 0; m < 4; ++m) acc[g][i][m][0] = acc[g][i][m][1] = 0.0;
+            for (int m = 0; m < NF; ++m) acc[g][i][m][0] = acc[g][i][m][1] = 0.0;
 
 #pragma unroll
     for (int s = 0; s < STG - 1; ++s) issue(s);
 
-    const int r_warp = wr * (H / 2), c_warp = wc * 32;
+    const int r_warp = wr * (H / 2), c_warp = wc * (BND / 4);
     const int ar = lane >> 2, ak = lane & 3;
     const int cr = lane >> 2;
     for (int w = 0; w < nwork; ++w) {
-        cp_async_wait<STG - 2>();
+        if (TMA) mbar_wait(bar + (w % STG), (unsigned)((w / STG) & 1));
+        else cp_async_wait<STG - 2>();
         __syncthreads();
         issue(w + STG - 1);
         const int kc = w % nkc;
-        const double* bs = Bs + (size_t)(w % STG) * 16 * BNP;
+        const double* bs = Bs + (size_t)(w % STG) * SR * BNP;
+        if (!dry)
 #pragma unroll
-        for (int k4 = 0; k4 < 8; k4 += 4) {
-            const int kr = kc * 8 + k4 + ak;
-            double ae[MT], ao[MT], be[4], bo[4];
+        for (int k4 = 0; k4 < KC; k4 += 4) {
+            const int kr = kc * KC + k4 + ak;
+            double ae[MT], ao[MT], be[NF], bo[NF];
 #pragma unroll
             for (int i = 0; i < MT; ++i) {
                 ae[i] = Ae[kr * BMP + r_warp + i * 8 + ar];
                 ao[i] = Ao[kr * BMP + r_warp + i * 8 + ar];
             }
 #pragma unroll
-            for (int m = 0; m < 4; ++m) {
+            for (int m = 0; m < NF; ++m) {
                 const double t = bs[(k4 + ak) * BNP + c_warp + m * 8 + ar];
-                const double b = bs[(8 + k4 + ak) * BNP + c_warp + m * 8 + ar];
+                const double b = bs[(KC + k4 + ak) * BNP + c_warp + m * 8 + ar];
                 be[m] = INV ? t : t + b;
                 bo[m] = INV ? b : t - b;
             }
 #pragma unroll
             for (int i = 0; i < MT; ++i)
 #pragma unroll
-                for (int m = 0; m < 4; ++m) {
+                for (int m = 0; m < NF; ++m) {
                     dmma_m8n8k4(acc[0][i][m][0], acc[0][i][m][1], ae[i], be[m]);
                     dmma_m8n8k4(acc[1][i][m][0], acc[1][i][m][1], ao[i], bo[m]);
                 }
         }
-        if (kc == nkc - 1) {
+        if (kc == nkc - 1 && dry != 2) {
             const long long tile = (long long)blockIdx.x + (long long)(w / nkc) * gridDim.x;
             const TileBase tbase = tile_base(M, tile);
 #pragma unroll
-            for (int m = 0; m < 4; ++m) {
+            for (int m = 0; m < NF; ++m) {
                 const int jcol = (c_warp >> 1) + m * 4 + (lane & 3);
                 long long io, oo;
                 if (colmap(M, n, tbase, jcol, io, oo)) {
@@ -824,33 +904,77 @@ k_mode_gemm_fold(const double* __restrict__ Af, const int* __restrict__ rmap, in
     cp_async_wait<0>();
 }
 
-template <int TH, bool INV>
-void launch_fold_th(const FoldAxis& F, const double* X, double* Y, const ColMap& M, cudaStream_t st) {
+// fold kernel configuration: pair rows per stage (KC), ring stages, CTAs per SM
+// KS_FOLD_DRY=1: skip the MMAs (memory-pipeline ceiling experiment; wrong results)
+int dry_run() {
+    static const int d = std::getenv("KS_FOLD_DRY") ? std::atoi(std::getenv("KS_FOLD_DRY")) : 0;
+    return d;
+}
+
+// tile width (complex columns) of a column map; T modes block it as tbt x tbr
+void set_tile_width(ColMap& M, int tw) {
+    M.tw = tw;
+    if (M.mode == MAP_STD) {
+        M.ntiles = (M.Q + tw - 1) / tw;
+    } else {
+        M.tbr = M.Np >= 8 ? 8 : (M.Np >= 4 ? 4 : (M.Np >= 2 ? 2 : 1));
+        M.tbt = tw / M.tbr;
+        M.ntb = (M.nt + M.tbt - 1) / M.tbt;
+        M.ntiles = M.ntb * ((M.Np + M.tbr - 1) / M.tbr);
+    }
+}
+
+template <int TH, bool INV, int KC, int STG, int MINB, int BNC, bool TMA = false>
+void launch_fold_cfg(const FoldAxis& F, const double* X, double* Y, ColMap M, cudaStream_t st) {
     constexpr int H = 16 * TH;
-    const int nkc = (F.hc + 7) / 8;
-    const size_t sm_a = (size_t)2 * nkc * 8 * (H + 4) * sizeof(double) + (size_t)2 * H * sizeof(int);
-    const size_t sm_s = (size_t)16 * (kBN + 4) * sizeof(double);
-    const bool two = sm_a + kStages * sm_s > 227 * 1024;
-    const size_t sm = sm_a + (two ? 2 : kStages) * sm_s;
+    const int nkc = (F.hc + KC - 1) / KC;
+    const size_t sm = (size_t)2 * nkc * KC * (H + 4) * sizeof(double) + (size_t)2 * H * sizeof(int) +
+                      (size_t)STG * 2 * KC * (2 * BNC + 4) * sizeof(double) + (size_t)STG * 8;
     KS_REQUIRE(sm <= 227 * 1024, KS_EINVAL, "folded mode product: axis too long");
     static int sms = 0;
     if (!sms) {
         int dev = 0;
         KS_CUDA(cudaGetDevice(&dev));
         KS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        KS_CUDA(cudaFuncSetAttribute(k_mode_gemm_fold<TH, INV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     227 * 1024));
-        KS_CUDA(cudaFuncSetAttribute(k_mode_gemm_fold<TH, INV, 2>,
+        KS_CUDA(cudaFuncSetAttribute(k_mode_gemm_fold<TH, INV, KC, STG, MINB, BNC, TMA>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     }
-    const int per_sm = (TH <= 2 && 2 * sm <= 227 * 1024) ? 2 : 1;
+    set_tile_width(M, BNC);
+    const int per_sm = std::max(1, std::min(MINB, (int)((227 * 1024) / sm)));
     const unsigned g = (unsigned)std::min<long long>(M.ntiles, (long long)sms * per_sm);
     const double* A = (INV ? F.inv : F.fwd).as<double>();
-    if (two)
-        k_mode_gemm_fold<TH, INV, 2><<<g, kThreads, sm, st>>>(A, F.rmap.as<int>(), F.n, F.hc, nkc, X, Y, M);
-    else
-        k_mode_gemm_fold<TH, INV><<<g, kThreads, sm, st>>>(A, F.rmap.as<int>(), F.n, F.hc, nkc, X, Y, M);
+    k_mode_gemm_fold<TH, INV, KC, STG, MINB, BNC, TMA><<<g, kThreads, sm, st>>>(A, F.kst, F.rmap.as<int>(), F.n,
+                                                                                F.hc, nkc, X, Y, M, dry_run());
     check_launch("k_mode_gemm_fold");
+}
+
+template <int TH, bool INV>
+void launch_fold_th(const FoldAxis& F, const double* X, double* Y, const ColMap& M, cudaStream_t st) {
+    if (TH <= 2) {
+        // Variants measured at c3 (n = 64, six transforms per FD apply; profiles/round2_summary.md):
+        //   (KC 16, 2 stages, 2 CTA/SM, 64-column tiles)  0.847-0.864 ms   <- default
+        //   (KC  8, 4 stages, 2 CTA/SM)                   0.895 ms
+        //   32-column tiles, 3 CTA/SM (80 regs)           0.867 ms
+        //   1 CTA/SM, 3-4 stages                          1.08 ms
+        //   smem-staged row-wise stores                   0.98-1.06 ms
+        //   TMA bulk row loads + mbarrier (KS_FOLD_TMA=1) 0.862 ms
+        // and without the MMAs (KS_FOLD_DRY=1) the same data movement takes 0.713 ms:
+        // the kernel is bound by its memory pipeline (loads alone 4.0, stores alone 3.3 TB/s).
+        static const bool tma = [] {
+            const char* e = std::getenv("KS_FOLD_TMA");
+            return e && std::strcmp(e, "0") != 0;
+        }();
+        if (tma && M.mode == MAP_STD && M.s >= 64)
+            return launch_fold_cfg<TH, INV, 16, 2, 2, 64, true>(F, X, Y, M, st);
+        return launch_fold_cfg<TH, INV, 16, 2, 2, 64>(F, X, Y, M, st);
+    }
+    // long axes: resident halves are large -> 1 CTA/SM; 2 stages when 4 do not fit
+    constexpr int H = 16 * TH;
+    const int nkc = (F.hc + 7) / 8;
+    const size_t sm4 = (size_t)2 * nkc * 8 * (H + 4) * sizeof(double) + (size_t)2 * H * sizeof(int) +
+                       (size_t)4 * 16 * (kBN + 4) * sizeof(double);
+    if (sm4 <= 227 * 1024) return launch_fold_cfg<TH, INV, 8, 4, 1, 64>(F, X, Y, M, st);
+    return launch_fold_cfg<TH, INV, 8, 2, 1, 64>(F, X, Y, M, st);
 }
 
 ColMap make_colmap(int n, size_t s_complex, size_t outer, int layout, int nt) {
@@ -897,7 +1021,7 @@ bool fold_axis_build(const double* U, int n, double tol, FoldAxis& F) {
     if ((int)E.size() != hc) return false;
     const int th = (hc + 15) / 16;
     if (th > 5) return false;
-    const int H = 16 * th, Kp = 8 * ((hc + 7) / 8);
+    const int H = 16 * th, Kp = 16 * ((hc + 15) / 16); // stored k rows (multiple of 16)
     std::vector<double> fwd((size_t)2 * Kp * H, 0.0), inv((size_t)2 * Kp * H, 0.0);
     std::vector<int> rmap((size_t)2 * H, 0);
     const int no = n - hc;
@@ -921,6 +1045,7 @@ bool fold_axis_build(const double* U, int n, double tol, FoldAxis& F) {
     F.n = n;
     F.hc = hc;
     F.th = th;
+    F.kst = Kp;
     F.fwd.alloc(fwd.size() * sizeof(double));
     F.inv.alloc(inv.size() * sizeof(double));
     F.rmap.alloc(rmap.size() * sizeof(int));
