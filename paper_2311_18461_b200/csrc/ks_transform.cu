@@ -951,7 +951,7 @@ void launch_fold_cfg(const FoldAxis& F, const double* X, double* Y, ColMap M, cu
 template <int TH, bool INV>
 void launch_fold_th(const FoldAxis& F, const double* X, double* Y, const ColMap& M, cudaStream_t st) {
     if (TH <= 2) {
-        // Variants measured at c3 (n = 64, six transforms per FD apply; profiles/round2_summary.md):
+        // Variants measured at c3 (n = 64, six transforms per FD apply; profiles/round1_part2_summary.md):
         //   (KC 16, 2 stages, 2 CTA/SM, 64-column tiles)  0.847-0.864 ms   <- default
         //   (KC  8, 4 stages, 2 CTA/SM)                   0.895 ms
         //   32-column tiles, 3 CTA/SM (80 regs)           0.867 ms
