@@ -141,6 +141,25 @@ void launch_mode_gemm_fold(const FoldAxis& F, bool inverse, const double* X, dou
                            size_t s_complex, size_t outer, cudaStream_t st, int layout = 0, int nt = 0);
 
 // ---------------------------------------------------------------------------
+// plan-specialised fused level passes (ks_kron_jit.cu, NVRTC at plan creation)
+// ---------------------------------------------------------------------------
+struct JitContrib {
+    int in, out, factor, coeff; // coeff = index into the coefficient table
+};
+struct KronJitPair;
+// fused passes over tensors [n_outer][n_b][n_a][s_a] (axis a then axis b);
+// null when the shape is unsupported or KS_KRON_JIT=0
+KronJitPair* kron_jit_build(int nin, int nmid, int nout, int bw, const std::vector<JitContrib>& a,
+                            const std::vector<JitContrib>& b, const std::vector<int>& freal,
+                            const std::vector<double2>& coeffs, long long s_a, int n_a, int n_b, long long n_outer);
+bool kron_jit_launch(const KronJitPair& J, const double2* const* ip, double2* const* op, const double2* rb, int nmax,
+                     cudaStream_t st);
+void kron_jit_free(KronJitPair* p);
+struct KronJitDeleter {
+    void operator()(KronJitPair* p) const { kron_jit_free(p); }
+};
+
+// ---------------------------------------------------------------------------
 // banded block factor / solve (ks_fdsolve.cu)
 // ---------------------------------------------------------------------------
 struct FdBlocks {

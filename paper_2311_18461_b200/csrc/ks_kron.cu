@@ -28,6 +28,7 @@
 #include <cstring>
 #include <map>
 #include <numeric>
+#include <cstdlib>
 
 namespace ks {
 
@@ -44,6 +45,11 @@ bool launch_colsweep(int nin, int nout, int bw, const double2* const* ip, double
                      const int* in_begin, const SweepEntry* entries, const double2* rb,
                      const int* freal, size_t ncols, size_t s, int n, int nmax, cudaStream_t st,
                      int nir, int ioff, int boff, const int* ring_begin, const RingCon* ring_cons);
+
+bool launch_kron_pair(int nin, int nmid, int nout, int bw, const double2* const* ip, double2* const* op,
+                      const int* a_begin, const SweepEntry* a_ent, const int* b_begin, const SweepEntry* b_ent,
+                      const int* b_obegin, const void* b_con, const double2* rb, const int* freal, int nmax,
+                      long long s_a, int n_a, int n_b, long long n_outer, cudaStream_t st);
 
 struct KronFactor {
     int n = 0, bw = 0;
@@ -82,6 +88,8 @@ struct KronPlan {
     // slab (dims.back() rows) and writes shard_rows owned planes
     int shard_rows = 0, shard_in_off = 0, shard_band_off = 0;
     DevBuf d_rowband, d_freal; // v3: rb[f][r][dj] (width 2*bwmax+1), is_real[f]
+    // plan-specialised fused pass pairs (k, k+1), indexed by k (null = none)
+    std::vector<std::unique_ptr<KronJitPair, KronJitDeleter>> jit;
 };
 
 namespace {
@@ -443,6 +451,32 @@ KronPlan* kron_plan(const std::vector<int>& dims,
         KS_CUDA(cudaMemcpy(P->d_rowband.p, rb.data(), rb.size() * sizeof(double2), cudaMemcpyHostToDevice));
         P->d_freal.alloc(freal.size() * sizeof(int));
         KS_CUDA(cudaMemcpy(P->d_freal.p, freal.data(), freal.size() * sizeof(int), cudaMemcpyHostToDevice));
+        // fused pass pairs (0,1), (2,3), ... specialised with NVRTC
+        P->jit.resize(P->passes.size());
+        std::vector<int> frv(P->factors.size());
+        for (size_t f = 0; f < P->factors.size(); ++f) frv[f] = P->factors[f].is_real ? 1 : 0;
+        for (size_t k = 0; k + 1 < P->passes.size(); k += 2) {
+            const KronPass &pa = P->passes[k], &pb = P->passes[k + 1];
+            if (pb.axis != pa.axis + 1 || pb.n_in != pa.n_out) break;
+            std::vector<JitContrib> ca, cb;
+            std::vector<double2> co;
+            for (int o = 0; o < pa.n_out; ++o)
+                for (int ci = pa.out_begin[o]; ci < pa.out_begin[o + 1]; ++ci) {
+                    ca.push_back(JitContrib{pa.contribs[ci].in, o, pa.contribs[ci].factor, (int)co.size()});
+                    co.push_back(pa.contribs[ci].coeff);
+                }
+            for (int o = 0; o < pb.n_out; ++o)
+                for (int ci = pb.out_begin[o]; ci < pb.out_begin[o + 1]; ++ci) {
+                    cb.push_back(JitContrib{pb.contribs[ci].in, o, pb.contribs[ci].factor, (int)co.size()});
+                    co.push_back(pb.contribs[ci].coeff);
+                }
+            size_t sa = 1;
+            for (int x = 0; x < pa.axis; ++x) sa *= (size_t)P->dims[x];
+            const int na = P->dims[pa.axis], nbb = P->dims[pb.axis];
+            const long long outer = (long long)(P->N / (sa * (size_t)na * (size_t)nbb));
+            P->jit[k].reset(kron_jit_build(pa.n_in, pa.n_out, pb.n_out, P->bwmax, ca, cb, frv, co, (long long)sa, na,
+                                           nbb, outer));
+        }
     }
     for (auto& ps : P->passes) {
         std::vector<int> ib(ps.n_in + 1, 0);
@@ -520,6 +554,35 @@ void kron_apply(KronPlan& P, const double2* x, double2* y, cudaStream_t st,
         const int n = P.dims[ps.axis];
         const bool shard_last = P.shard_rows > 0 && k + 1 == P.passes.size() &&
                                 ps.axis == (int)P.dims.size() - 1;
+        // plan-specialised fused pair (NVRTC): the middle level stays on chip
+        if (k < P.jit.size() && P.jit[k] && !(P.shard_rows > 0 && k + 2 == P.passes.size())) {
+            const KronPass& nx = P.passes[k + 1];
+            auto ip = reinterpret_cast<const double2* const*>(dp + P.ptr_off[k]);
+            auto op = reinterpret_cast<double2* const*>(const_cast<void**>(dp + P.ptr_off[k + 1] + nx.n_in));
+            if (kron_jit_launch(*P.jit[k], ip, op, P.d_rowband.as<double2>(), P.nmax, st)) {
+                ++k;
+                continue;
+            }
+        }
+        // generic fused pair (opt-in, KS_KRON_PAIR=1): run-time interpreted plan
+        if (std::getenv("KS_KRON_PAIR") && k + 1 < P.passes.size() && P.passes[k + 1].axis == ps.axis + 1 &&
+            P.bwmax >= 1 && P.bwmax <= 4 && !(P.shard_rows > 0 && k + 2 == P.passes.size())) {
+            const KronPass& nx = P.passes[k + 1];
+            auto ip = reinterpret_cast<const double2* const*>(dp + P.ptr_off[k]);
+            auto op = reinterpret_cast<double2* const*>(const_cast<void**>(dp + P.ptr_off[k + 1] + nx.n_in));
+            const int nb = P.dims[ps.axis + 1];
+            const long long outer = (long long)(P.N / ((size_t)s * n * nb));
+            const bool ok = nx.n_in == ps.n_out &&
+                            launch_kron_pair(ps.n_in, ps.n_out, nx.n_out, P.bwmax, ip, op, ps.d_in_begin.as<int>(),
+                                             ps.d_entries.as<SweepEntry>(), nx.d_in_begin.as<int>(),
+                                             nx.d_entries.as<SweepEntry>(), nx.d_begin.as<int>(), nx.d_contribs.p,
+                                             P.d_rowband.as<double2>(), P.d_freal.as<int>(), P.nmax, (long long)s,
+                                             n, nb, outer, st);
+            if (ok) {
+                ++k;
+                continue;
+            }
+        }
         // element-parallel level kernel (all axes)
         if (ps.n_out <= 8 && P.bwmax >= 1 && P.bwmax <= 4) {
             auto ip = reinterpret_cast<const double2* const*>(dp + P.ptr_off[k]);
