@@ -32,11 +32,14 @@ CASES = [  # (d, p, n_el, n_el_t) -- reference unit-test shapes + config 1 + 3-D
     (2, 3, 10, 9), (2, 4, 6, 5), (2, 6, 5, 5), (3, 2, 6, 6), (3, 4, 4, 4),
 ]
 TW = [(2, 8), (3, 8), (4, 8), (2, 16), (3, 16), (4, 16)]  # Table 2: 7 / 9 / 10 +- 2
+# final-condition trial space (time basis drops its LAST function, assembly.hpp:59-62;
+# SURVEY 8(f) rank 2): same Kronecker skeleton, different time restriction
+FC_CASES = [(1, 2, 5, 4), (2, 3, 8, 7), (3, 2, 6, 6)]
 
 
-def case(d, p, n_el, n_el_t):
-    out = {}
-    R = refdrv.RefProblem(d, p, n_el, n_el_t)
+def case(d, p, n_el, n_el_t, trial=0):
+    out = {"trial": trial}
+    R = refdrv.RefProblem(d, p, n_el, n_el_t, trial=trial)
     Lt, Mt, Wt = R.time_bands()
     out.update(dims=np.array(R.dims), d=d, p=p, nu=1.0, Lt=Lt, Mt=Mt, Wt=Wt,
                lam_composite=R.composite_lambda())
@@ -65,6 +68,10 @@ def main():
     for c in CASES:
         name = "case_d%d_p%d_n%d_t%d.npz" % c
         np.savez_compressed(os.path.join(HERE, name), **case(*c))
+        print("wrote", name)
+    for c in FC_CASES:
+        name = "case_fc_d%d_p%d_n%d_t%d.npz" % c
+        np.savez_compressed(os.path.join(HERE, name), **case(*c, trial=1))
         print("wrote", name)
     for p, n_el in TW:
         R = refdrv.RefProblem(2, p, n_el, n_el)

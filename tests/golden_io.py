@@ -20,6 +20,7 @@ def load(path):
     d = int(g["dims"].size - 1)
     g["d"] = d
     g["p"] = int(g["p"])
+    g["trial"] = "final" if int(g.get("trial", 0)) == 1 else "initial"
     g["dims"] = [int(v) for v in g["dims"]]
     g["U"] = [g[f"U{l}"] for l in range(d)]
     g["lam"] = [g[f"lam{l}"] for l in range(d)]

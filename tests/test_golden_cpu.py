@@ -36,7 +36,7 @@ def test_input_generator_matches_reference(oracle):
 def test_host_setup_vs_reference(ks, oracle, path):
     g = load(path)
     d, p = g["d"], g["p"]
-    prob = ks.SpaceTimeProblem.uniform(d, p, g["dims"][1] + 2 - p, g["dims"][0] + 1 - p)
+    prob = ks.SpaceTimeProblem.uniform(d, p, g["dims"][1] + 2 - p, g["dims"][0] + 1 - p, trial=g["trial"])
     assert prob.reduced_dims() == g["dims"]
     Lt, Mt, Wt = prob.time_bands()
     for a, b in ((Lt, g["Lt"]), (Mt, g["Mt"]), (Wt, g["Wt"])):

@@ -50,3 +50,25 @@ def test_gpu_table2_traveling_wave(gpu, oracle, path):
     assert s.converged
     assert abs(s.iterations - int(g["pcg_iters"])) <= 1
     assert abs(s.iterations - {2: 7, 3: 9, 4: 10}[g["p"]]) <= 2
+
+
+FC = [p for p in cases() if "case_fc_" in p]
+
+
+@pytest.mark.parametrize("path", FC, ids=ids(FC))
+def test_gpu_final_condition_own_setup(gpu, oracle, path):
+    """Final-condition trial space (time basis drops its last function,
+    assembly.hpp:59-62) built by libks's own host setup:
+    same FD / matvec / PCG kernels, results against the reference's golden
+    outputs at the north_star tolerance."""
+    g = load(path)
+    d, p = g["d"], g["p"]
+    prob = gpu.SpaceTimeProblem.uniform(d, p, g["dims"][1] + 2 - p, g["dims"][0] + 1 - p, trial="final")
+    assert prob.reduced_dims() == g["dims"]
+    P = gpu.FDPreconditioner(prob)
+    A = gpu.assemble_system_operator(prob)
+    r = g["r"]
+    assert rel(P.apply(r), g["z"]) <= 1e-10
+    assert rel(A.apply(r), g["y"]) <= 1e-10
+    s = gpu.pcg(A, P, r, gpu.PcgOptions(1e-8, 200))
+    assert s.converged and abs(s.iterations - int(g["pcg_iters"])) <= 1
