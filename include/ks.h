@@ -100,6 +100,14 @@ int ks_fd_eigenvalues(const ks_fd* fd, double* out);
  * the BandedFactorization layout (eigensolve.hpp:36-42): ab is (3p+1) x n_t
  * complex with ldab = 3p+1, piv has n_t ints. For parity tests. */
 int ks_fd_block(const ks_fd* fd, size_t i, ks_c64* ab, int* piv);
+/* galerkin_fast_solver(prob, u) (fdsolver.hpp:76-79, fdsolver.cpp:177-191): the
+ * same spatial eigenbasis with blocks H_i = Wt + nu lambda_i Mt -- the exact
+ * inverse of the Galerkin matrix M_s x W_t - nu sum_l (..G_l^T..) x M_t.
+ * Applied with ks_fd_apply (FastDiagSolver::solve) and ks_fd_apply_adjoint
+ * (FastDiagSolver::solve_adjoint, fdsolver.cpp:65-75). */
+int ks_fd_create_galerkin(int d, const int* dims, double nu, int p_t,
+                          const double* const* U, const double* const* lambda,
+                          const double* Mt, const ks_c64* Wt, int device, ks_fd** out);
 /* Execution plan of a handle (no reference counterpart; diagnostics):
  * folded_axes bit l-1 set = axis l uses the even/odd folded transform
  * (centro-symmetric pencil); blocks = factored time blocks
@@ -276,6 +284,10 @@ int ks_setup_eig(const ks_setup* s, int l, double* U, double* lambda);
 int ks_setup_create_fd(const ks_setup* s, int device, ks_fd** out);
 /* The system operator A as the reference's term list (assembly.cpp:202-251). */
 int ks_setup_create_system(const ks_setup* s, int device, ks_kron** out);
+/* galerkin_fast_solver(prob, u) on this setup (fdsolver.cpp:177-191) */
+int ks_setup_create_galerkin_fd(const ks_setup* s, int device, ks_fd** out);
+/* assemble_galerkin_operator(prob) (assembly.cpp:273-286) */
+int ks_setup_create_galerkin_operator(const ks_setup* s, int device, ks_kron** out);
 /* The same operator sharded over nranks (ks_kronshard_*). */
 int ks_setup_create_system_sharded(const ks_setup* s, int nranks, int rank, int device,
                                    ks_kron** out);

@@ -231,24 +231,47 @@ typedef struct {
     int* piv;        /* Ns x nt */
 } ko_fd;
 
-/* W + W^H (fdsolver.cpp:95-103) and H(lam) (fdsolver.cpp:105-120) */
+/* W + W^H (fdsolver.cpp:95-103) and H(lam) (fdsolver.cpp:105-120); kind 1:
+ * galerkin_fast_solver's H(lam) = Wt + nu*lam*Mt (fdsolver.cpp:177-191) */
 static void build_block(const double* Lt, const double* Mt, const cplx* Wt, int nt, int p,
-                        double nu, double lam, cplx* H) {
+                        double nu, double lam, cplx* H, int kind) {
     const int ld = 2 * p + 1;
     memset(H, 0, (size_t)ld * nt * sizeof(cplx));
     for (int i = 0; i < nt; ++i)
         for (int j = (i - p > 0 ? i - p : 0); j <= (i + p < nt - 1 ? i + p : nt - 1); ++j) {
             const size_t ij = (size_t)(p + i - j) + (size_t)j * ld;
+            if (kind == 1) {
+                const cplx mt = Mt[ij];
+                H[ij] = band_get(Wt, nt, p, i, j) + nu * lam * mt;
+                continue;
+            }
             const cplx wsym = band_get(Wt, nt, p, i, j) + conj(band_get(Wt, nt, p, j, i));
             const cplx lt = Lt[ij], mt = Mt[ij];
             H[ij] = lt + nu * nu * lam * lam * mt + nu * lam * wsym;
         }
 }
 
+static ko_fd* fd_create(int kind, int d, const int* dims, double nu, int p, const double* const* U,
+                        const double* const* lam_axes, const double* Lt, const double* Mt,
+                        const cplx* Wt, int* status);
+
 /* FDPreconditioner(prob, u): spatial_eigenbasis (fdsolver.cpp:23-44) + FastDiagSolver ctor (:46-51) */
 ko_fd* ko_fd_create(int d, const int* dims, double nu, int p, const double* const* U,
                     const double* const* lam_axes, const double* Lt, const double* Mt,
                     const cplx* Wt, int* status) {
+    return fd_create(0, d, dims, nu, p, U, lam_axes, Lt, Mt, Wt, status);
+}
+
+/* galerkin_fast_solver(prob, u) (fdsolver.cpp:177-191) */
+ko_fd* ko_fd_create_galerkin(int d, const int* dims, double nu, int p, const double* const* U,
+                             const double* const* lam_axes, const double* Mt, const cplx* Wt,
+                             int* status) {
+    return fd_create(1, d, dims, nu, p, U, lam_axes, NULL, Mt, Wt, status);
+}
+
+static ko_fd* fd_create(int kind, int d, const int* dims, double nu, int p, const double* const* U,
+                        const double* const* lam_axes, const double* Lt, const double* Mt,
+                        const cplx* Wt, int* status) {
     ko_fd* f = (ko_fd*)calloc(1, sizeof(ko_fd));
     f->d = d;
     f->p = p;
@@ -280,7 +303,7 @@ ko_fd* ko_fd_create(int d, const int* dims, double nu, int p, const double* cons
     cplx* H = (cplx*)malloc((size_t)(2 * p + 1) * nt * sizeof(cplx));
     *status = 0;
     for (size_t i = 0; i < f->Ns; ++i) {
-        build_block(Lt, Mt, Wt, nt, p, nu, f->lambda[i], H);
+        build_block(Lt, Mt, Wt, nt, p, nu, f->lambda[i], H, kind);
         if (ko_factor_banded(H, nt, p, f->ab + i * (size_t)ldab * nt, f->piv + i * (size_t)nt)) {
             *status = 2;
             break;

@@ -52,6 +52,8 @@ def olib():
         P, I, D, S = C.c_void_p, C.c_int, C.c_double, C.c_size_t
         L.ko_fd_create.restype = P
         L.ko_fd_create.argtypes = [I, P, D, I, P, P, P, P, P, C.POINTER(I)]
+        L.ko_fd_create_galerkin.restype = P
+        L.ko_fd_create_galerkin.argtypes = [I, P, D, I, P, P, P, P, C.POINTER(I)]
         L.ko_fd_apply.argtypes = [P, P, P]
         L.ko_fd_apply_adjoint.argtypes = [P, P, P]
         L.ko_fd_destroy.argtypes = [P]
@@ -90,9 +92,10 @@ def random_vec(n: int, seed: int = 1234) -> np.ndarray:
 
 
 class OracleFD:
-    """FDPreconditioner restated in C (fdsolver.cpp); takes the setup products."""
+    """FDPreconditioner restated in C (fdsolver.cpp); takes the setup products.
+    kind="galerkin": galerkin_fast_solver (fdsolver.cpp:177-191), blocks W + nu lam Mt."""
 
-    def __init__(self, dims, nu, p, U, lam, Lt, Mt, Wt):
+    def __init__(self, dims, nu, p, U, lam, Lt, Mt, Wt, kind="ls"):
         d = len(dims) - 1
         self.dims = list(dims)
         self.p = p
@@ -105,8 +108,12 @@ class OracleFD:
         lp = (C.c_void_p * d)(*[a.ctypes.data for a in self._keep[d:]])
         cd = (C.c_int * (d + 1))(*dims)
         st = C.c_int()
-        self._h = olib().ko_fd_create(d, cd, float(nu), int(p), up, lp, _p(self._Lt), _p(self._Mt),
-                                      _p(self._Wt), C.byref(st))
+        if kind == "galerkin":
+            self._h = olib().ko_fd_create_galerkin(d, cd, float(nu), int(p), up, lp, _p(self._Mt),
+                                                   _p(self._Wt), C.byref(st))
+        else:
+            self._h = olib().ko_fd_create(d, cd, float(nu), int(p), up, lp, _p(self._Lt), _p(self._Mt),
+                                          _p(self._Wt), C.byref(st))
         if st.value != 0:
             olib().ko_fd_destroy(self._h)
             self._h = None
@@ -310,4 +317,30 @@ def system_terms(prob_bands, d, nu):
         f = wm(Wsym)
         f[l + 1] = L[l]
         terms.append((nu, f, bw))
+    return terms
+
+
+def galerkin_terms(prob_bands, d, nu):
+    """assemble_galerkin_operator (assembly.cpp:273-286) as an oracle term list:
+    1 (W x M_1 x .. x M_d) - nu sum_l (M_t x .. G_l^T on axis l ..)."""
+    p = prob_bands["p"]
+    dims = prob_bands["dims"]
+    Mt = np.asarray(prob_bands["Mt"], dtype=np.complex128)
+    W = np.asarray(prob_bands["Wt"], dtype=np.complex128)
+
+    def tr(b, n):
+        D = band_to_dense(b, n, p).T
+        out = np.zeros((2 * p + 1) * n, dtype=np.complex128)
+        for j in range(n):
+            for i in range(max(0, j - p), min(n, j + p + 1)):
+                out[p + i - j + j * (2 * p + 1)] = D[i, j]
+        return out
+    M = [np.asarray(b, dtype=np.complex128) for b in prob_bands["M"]]
+    G = [np.asarray(b, dtype=np.complex128) for b in prob_bands["G"]]
+    bw = [p] * (d + 1)
+    terms = [(1.0, [W] + [M[l] for l in range(d)], bw)]
+    for l in range(d):
+        f = [Mt] + [M[m] for m in range(d)]
+        f[l + 1] = tr(G[l], dims[l + 1])
+        terms.append((-nu, f, bw))
     return terms

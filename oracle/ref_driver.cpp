@@ -29,6 +29,8 @@ struct RefProblem {
     UnivariateSet u;
     std::unique_ptr<FDPreconditioner> P;
     std::unique_ptr<KroneckerOperator> A;
+    std::unique_ptr<FastDiagSolver> Gfd;       // galerkin_fast_solver (lazy)
+    std::unique_ptr<KroneckerOperator> Gop;    // assemble_galerkin_operator (lazy)
     SpatialEigenbasis basis;
     explicit RefProblem(SpaceTimeProblem pr) : prob(std::move(pr)) {}
 };
@@ -201,6 +203,33 @@ int ref_fd_to_dense(void* h, std::complex<double>* out) {
     } catch (const std::length_error& e) {
         g_err = e.what();
         return 6;
+    }
+}
+
+// galerkin_fast_solver(prob, u) solve / solve_adjoint (fdsolver.cpp:53-75,177-191)
+int ref_galerkin_apply(void* h, const std::complex<double>* x, std::complex<double>* y, int adjoint) {
+    auto* r = static_cast<RefProblem*>(h);
+    try {
+        if (!r->Gfd) r->Gfd = std::make_unique<FastDiagSolver>(galerkin_fast_solver(r->prob, r->u));
+        if (adjoint) r->Gfd->solve_adjoint(x, y);
+        else r->Gfd->solve(x, y);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 2;
+    }
+}
+
+// assemble_galerkin_operator(prob).apply (assembly.cpp:273-286)
+int ref_galerkin_kron_apply(void* h, const std::complex<double>* x, std::complex<double>* y) {
+    auto* r = static_cast<RefProblem*>(h);
+    try {
+        if (!r->Gop) r->Gop = std::make_unique<KroneckerOperator>(assemble_galerkin_operator(r->prob));
+        r->Gop->apply(x, y);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 2;
     }
 }
 

@@ -50,6 +50,10 @@ def rlib():
         L.ref_named_rhs.argtypes = [P, C.c_char_p, P]
         L.ref_sinsin_rhs.restype = I
         L.ref_sinsin_rhs.argtypes = [P, P, P]
+        L.ref_galerkin_apply.restype = I
+        L.ref_galerkin_apply.argtypes = [P, P, P, I]
+        L.ref_galerkin_kron_apply.restype = I
+        L.ref_galerkin_kron_apply.argtypes = [P, P, P]
         _r = L
     return _r
 
@@ -118,6 +122,22 @@ class RefProblem:
         x = np.ascontiguousarray(x, dtype=np.complex128).ravel()
         y = np.empty_like(x)
         rlib().ref_kron_apply(self._h, _p(x), _p(y))
+        return y
+
+    def galerkin_apply(self, r, adjoint=False):
+        """galerkin_fast_solver(prob, u).solve / solve_adjoint (fdsolver.cpp:53-75,177-191)."""
+        r = np.ascontiguousarray(r, dtype=np.complex128).ravel()
+        z = np.empty_like(r)
+        if rlib().ref_galerkin_apply(self._h, _p(r), _p(z), int(adjoint)):
+            raise RuntimeError(rlib().ref_last_error().decode())
+        return z
+
+    def galerkin_kron_apply(self, x):
+        """assemble_galerkin_operator(prob).apply (assembly.cpp:273-286)."""
+        x = np.ascontiguousarray(x, dtype=np.complex128).ravel()
+        y = np.empty_like(x)
+        if rlib().ref_galerkin_kron_apply(self._h, _p(x), _p(y)):
+            raise RuntimeError(rlib().ref_last_error().decode())
         return y
 
     def fd_block(self, i):

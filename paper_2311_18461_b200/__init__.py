@@ -160,6 +160,10 @@ _SIGS = {
     "ks_setup_eig": (C.c_int, [_P, C.c_int, _P, _P]),
     "ks_setup_create_fd": (C.c_int, [_P, C.c_int, C.POINTER(_P)]),
     "ks_setup_create_system": (C.c_int, [_P, C.c_int, C.POINTER(_P)]),
+    "ks_setup_create_galerkin_fd": (C.c_int, [_P, C.c_int, C.POINTER(_P)]),
+    "ks_setup_create_galerkin_operator": (C.c_int, [_P, C.c_int, C.POINTER(_P)]),
+    "ks_fd_create_galerkin": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.c_double, C.c_int, C.POINTER(_P),
+                                        C.POINTER(_P), _P, _P, C.c_int, C.POINTER(_P)]),
     "ks_setup_create_system_sharded": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),
     "ks_setup_destroy": (C.c_int, [_P]),
 }
@@ -337,6 +341,30 @@ class FDPreconditioner:
             self._h = h
             self.dims = prob.reduced_dims()
         self.device = device
+
+    @classmethod
+    def galerkin(cls, prob: "SpaceTimeProblem", device: int = 0) -> "FDPreconditioner":
+        """galerkin_fast_solver(prob, u) (fdsolver.hpp:76-79, fdsolver.cpp:177-191): exact
+        inverse of the Galerkin matrix; apply = solve, apply_adjoint = solve_adjoint."""
+        h = C.c_void_p()
+        _check(lib().ks_setup_create_galerkin_fd(prob._h, device, C.byref(h)))
+        return cls(device=device, _handle=h, _dims=prob.reduced_dims())
+
+    @classmethod
+    def galerkin_from_arrays(cls, dims: Sequence[int], nu: float, p_t: int, U: Sequence[np.ndarray],
+                             lam: Sequence[np.ndarray], Mt, Wt, device: int = 0):
+        d = len(dims) - 1
+        Us = [np.ascontiguousarray(u, dtype=np.float64).ravel() for u in U]
+        ls = [np.ascontiguousarray(v, dtype=np.float64).ravel() for v in lam]
+        Mt = np.ascontiguousarray(Mt, dtype=np.float64).ravel()
+        Wt = _cvec(Wt).ravel()
+        up = (C.c_void_p * d)(*[a.ctypes.data for a in Us])
+        lp = (C.c_void_p * d)(*[a.ctypes.data for a in ls])
+        cd = (C.c_int * (d + 1))(*dims)
+        h = C.c_void_p()
+        _check(lib().ks_fd_create_galerkin(d, cd, float(nu), int(p_t), up, lp, _ptr(Mt), _ptr(Wt), device,
+                                           C.byref(h)))
+        return cls(device=device, _handle=h, _dims=dims)
 
     @classmethod
     def from_arrays(cls, dims: Sequence[int], nu: float, p_t: int, U: Sequence[np.ndarray],
@@ -543,6 +571,13 @@ def assemble_system_operator(prob: SpaceTimeProblem, device: int = 0) -> Kroneck
     """A = M_s x L_t + nu^2 B_s x M_t + nu L_s x (W_t + W_t^*) (assembly.cpp:202-257)."""
     h = C.c_void_p()
     _check(lib().ks_setup_create_system(prob._h, device, C.byref(h)))
+    return KroneckerOperator._wrap(h, prob.reduced_dims(), device)
+
+
+def assemble_galerkin_operator(prob: SpaceTimeProblem, device: int = 0) -> KroneckerOperator:
+    """Galerkin matrix M_s x W_t - nu sum_l (..G_l^T..) x M_t (assembly.cpp:273-286)."""
+    h = C.c_void_p()
+    _check(lib().ks_setup_create_galerkin_operator(prob._h, device, C.byref(h)))
     return KroneckerOperator._wrap(h, prob.reduced_dims(), device)
 
 

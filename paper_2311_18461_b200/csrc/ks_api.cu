@@ -77,7 +77,8 @@ struct ks_fd {
     std::vector<std::vector<double>> lam_host;
     std::vector<int> fiber_block; // host copy of the block map (empty = identity)
     bool fused = false;           // outermost axis via k_fd_fused
-    DevBuf Lt, Mt, Wsym;
+    int kind = 0;                 // 0: least-squares blocks, 1: Galerkin blocks (galerkin_fast_solver)
+    DevBuf Lt, Mt, Wsym;          // Wsym: W + W^H (least squares) or W itself (Galerkin)
     FdBlocks blocks;
     DevBuf s0, s1, io;
     cudaStream_t stream = nullptr;
@@ -273,11 +274,14 @@ void ks_launch_count_reset(void) { g_launches.store(0); }
 // ---------------------------------------------------------------------------
 // FD preconditioner
 // ---------------------------------------------------------------------------
-int ks_fd_create(int d, const int* dims, double nu, int p_t, const double* const* U,
-                 const double* const* lambda, const double* Lt, const double* Mt, const ks_c64* Wt,
-                 int device, ks_fd** out) {
-    API_BEGIN
-    KS_REQUIRE(out && dims && U && lambda && Lt && Mt && Wt, KS_EINVAL, "ks_fd_create: NULL argument");
+} // extern "C"
+
+// FDPreconditioner / galerkin_fast_solver construction (kind 0 / 1)
+static void fd_create_impl(int kind, int d, const int* dims, double nu, int p_t, const double* const* U,
+                           const double* const* lambda, const double* Lt, const double* Mt, const ks_c64* Wt,
+                           int device, ks_fd** out) {
+    KS_REQUIRE(out && dims && U && lambda && (Lt || kind == 1) && Mt && Wt, KS_EINVAL,
+               "ks_fd_create: NULL argument");
     KS_REQUIRE(d >= 1 && d <= 3, KS_EINVAL, "ks_fd_create: d must be 1, 2 or 3");
     KS_REQUIRE(nu > 0, KS_EINVAL, "ks_fd_create: nu must be positive");
     KS_REQUIRE(p_t >= 1 && p_t <= 8, KS_EINVAL, "ks_fd_create: time degree must be 1..8");
@@ -328,15 +332,17 @@ int ks_fd_create(int d, const int* dims, double nu, int p_t, const double* const
         const ks_c64 v = Wt[p_t + i - j + (size_t)j * ld];
         return make_double2(v.re, v.im);
     };
+    f->kind = kind;
     for (int i = 0; i < nt; ++i)
         for (int j = std::max(0, i - p_t); j <= std::min(nt - 1, i + p_t); ++j) {
             const double2 a = wget(i, j), b = wget(j, i);
-            ws[p_t + i - j + (size_t)j * ld] = make_double2(a.x + b.x, a.y - b.y);
+            ws[p_t + i - j + (size_t)j * ld] = kind == 1 ? a : make_double2(a.x + b.x, a.y - b.y);
         }
     f->Lt.alloc((size_t)ld * nt * sizeof(double));
     f->Mt.alloc((size_t)ld * nt * sizeof(double));
     f->Wsym.alloc(ws.size() * sizeof(double2));
-    KS_CUDA(cudaMemcpy(f->Lt.p, Lt, (size_t)ld * nt * sizeof(double), cudaMemcpyHostToDevice));
+    if (Lt) KS_CUDA(cudaMemcpy(f->Lt.p, Lt, (size_t)ld * nt * sizeof(double), cudaMemcpyHostToDevice));
+    else KS_CUDA(cudaMemset(f->Lt.p, 0, (size_t)ld * nt * sizeof(double)));
     KS_CUDA(cudaMemcpy(f->Mt.p, Mt, (size_t)ld * nt * sizeof(double), cudaMemcpyHostToDevice));
     KS_CUDA(cudaMemcpy(f->Wsym.p, ws.data(), ws.size() * sizeof(double2), cudaMemcpyHostToDevice));
     // factored blocks (fdsolver.cpp:46-51): one per composite eigenvalue, or one
@@ -443,12 +449,31 @@ int ks_fd_create(int d, const int* dims, double nu, int p_t, const double* const
     B.nblk = lam_blk.size();
     B.lam_blk.alloc(B.nblk * sizeof(double));
     KS_CUDA(cudaMemcpy(B.lam_blk.p, lam_blk.data(), B.nblk * sizeof(double), cudaMemcpyHostToDevice));
+    B.kind = kind;
     fd_blocks_alloc(B);
     launch_fd_factor(B, nu, f->Lt.as<double>(), f->Mt.as<double>(), f->Wsym.as<double2>(), f->stream);
     f->s0.alloc(f->N * sizeof(double2));
     f->s1.alloc(f->N * sizeof(double2));
     KS_CUDA(cudaStreamSynchronize(f->stream));
     *out = f.release();
+}
+
+extern "C" {
+
+int ks_fd_create(int d, const int* dims, double nu, int p_t, const double* const* U,
+                 const double* const* lambda, const double* Lt, const double* Mt, const ks_c64* Wt,
+                 int device, ks_fd** out) {
+    API_BEGIN
+    KS_REQUIRE(Lt, KS_EINVAL, "ks_fd_create: NULL argument");
+    fd_create_impl(0, d, dims, nu, p_t, U, lambda, Lt, Mt, Wt, device, out);
+    API_END
+}
+
+int ks_fd_create_galerkin(int d, const int* dims, double nu, int p_t, const double* const* U,
+                          const double* const* lambda, const double* Mt, const ks_c64* Wt, int device,
+                          ks_fd** out) {
+    API_BEGIN
+    fd_create_impl(1, d, dims, nu, p_t, U, lambda, nullptr, Mt, Wt, device, out);
     API_END
 }
 

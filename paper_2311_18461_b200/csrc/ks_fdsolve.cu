@@ -79,7 +79,8 @@ __global__ void k_fd_factor(double2* __restrict__ ab, unsigned char* __restrict_
                             int* __restrict__ flag, size_t ns, int nt, int p,
                             const double* __restrict__ lam_blk, double nu,
                             const double* __restrict__ Lt, const double* __restrict__ Mt,
-                            const double2* __restrict__ Wsym, int rec, int fused_nd, long long fused_np) {
+                            const double2* __restrict__ Wsym, int rec, int fused_nd, long long fused_np,
+                            int kind) {
     const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     if (i >= ns) return; // here ns = number of factored blocks
     const int ldab = 3 * p + 1, kuf = 2 * p, bwld = 2 * p + 1;
@@ -102,11 +103,18 @@ __global__ void k_fd_factor(double2* __restrict__ ab, unsigned char* __restrict_
         for (int r = r0; r <= r1; ++r) {
             const int bi = p + r - c + c * bwld;
             const double2 w = Wsym[bi];
-            // Lt(i,j) + nu*nu*lam*lam*Mt(i,j) + nu*lam*Wsym(i,j), complex
-            double re = __dadd_rn(Lt[bi], __dmul_rn(s2, Mt[bi]));
-            double im = 0.0; // Lt, Mt have zero imaginary parts (to_complex)
-            re = __dadd_rn(re, __dmul_rn(s1, w.x));
-            im = __dadd_rn(im, __dmul_rn(s1, w.y));
+            double re, im;
+            if (kind == 1) {
+                // galerkin_fast_solver (fdsolver.cpp:177-191): Wt(i,j) + nu*lam*Mt(i,j)
+                re = __dadd_rn(w.x, __dmul_rn(s1, Mt[bi]));
+                im = __dadd_rn(w.y, __dmul_rn(s1, 0.0));
+            } else {
+                // Lt(i,j) + nu*nu*lam*lam*Mt(i,j) + nu*lam*Wsym(i,j), complex
+                re = __dadd_rn(Lt[bi], __dmul_rn(s2, Mt[bi]));
+                im = 0.0; // Lt, Mt have zero imaginary parts (to_complex)
+                re = __dadd_rn(re, __dmul_rn(s1, w.x));
+                im = __dadd_rn(im, __dmul_rn(s1, w.y));
+            }
             A(r, c) = make_double2(re, im);
         }
     }
@@ -657,7 +665,7 @@ void launch_fd_factor(FdBlocks& B, double nu, const double* Lt, const double* Mt
     const unsigned grid = (unsigned)((B.nblk + 127) / 128);
     k_fd_factor<<<grid, 128, 0, st>>>(B.ab.as<double2>(), B.piv.as<unsigned char>(),
                                       B.flag.as<int>(), B.nblk, B.nt, B.p, B.lam_blk.as<double>(), nu,
-                                      Lt, Mt, Wsym, B.rec, B.fused_nd, B.fused_np);
+                                      Lt, Mt, Wsym, B.rec, B.fused_nd, B.fused_np, B.kind);
     check_launch("k_fd_factor");
     int h = 0;
     KS_CUDA(cudaMemcpyAsync(&h, B.flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));

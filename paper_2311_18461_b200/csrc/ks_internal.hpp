@@ -181,6 +181,7 @@ struct FdBlocks {
     // pair mode (d = 3, axes 2 and 3 identical): block b = i1 + n1 * pidx over
     // pairs (i2 <= i3), solved for fibers (i1, i2, i3) and (i1, i3, i2) together
     int pair_n1 = 0, pair_n2 = 0;
+    int kind = 0;       // 0: H = Lt + nu^2 lam^2 Mt + nu lam (W + W^H); 1 (Galerkin): H = W + nu lam Mt
     DevBuf pairs;       // int2 [npairs] (i2, i3)
     int fused_nd = 0;        // > 0: per-rest-column layout for the fused axis-d kernel
     long long fused_np = 0;  //      (block i = rho + fused_np * r, r < fused_nd)

@@ -421,18 +421,34 @@ extern "C" int ks_setup_create_fd(const ks_setup* s, int device, ks_fd** out) {
                         s->Mt.a.data(), reinterpret_cast<const ks_c64*>(s->Wt.a.data()), device, out);
 }
 
-static int create_system(const ks_setup* s, int device, int nranks, int rank, ks_kron** out);
+// galerkin_fast_solver (fdsolver.cpp:177-191): same eigenbasis, H = W + nu lam Mt
+extern "C" int ks_setup_create_galerkin_fd(const ks_setup* s, int device, ks_fd** out) {
+    if (!s) return KS_EINVAL;
+    std::vector<const double*> U, lam;
+    for (int l = 0; l < s->d; ++l) {
+        U.push_back(s->U[l].data());
+        lam.push_back(s->lam[l].data());
+    }
+    return ks_fd_create_galerkin(s->d, s->dims.data(), s->nu, s->p, U.data(), lam.data(), s->Mt.a.data(),
+                                 reinterpret_cast<const ks_c64*>(s->Wt.a.data()), device, out);
+}
+
+static int create_system(const ks_setup* s, int device, int nranks, int rank, ks_kron** out, int kind);
 
 // assemble_system (assembly.cpp:202-251), restricted (rs = DropBoth) branch
 extern "C" int ks_setup_create_system(const ks_setup* s, int device, ks_kron** out) {
-    return create_system(s, device, 0, 0, out);
+    return create_system(s, device, 0, 0, out, 0);
 }
 extern "C" int ks_setup_create_system_sharded(const ks_setup* s, int nranks, int rank, int device,
                                               ks_kron** out) {
-    return create_system(s, device, nranks, rank, out);
+    return create_system(s, device, nranks, rank, out, 0);
+}
+// assemble_galerkin_operator (assembly.cpp:273-286): 1 (W x M..) - nu sum_l (Mt x .. G_l^T ..)
+extern "C" int ks_setup_create_galerkin_operator(const ks_setup* s, int device, ks_kron** out) {
+    return create_system(s, device, 0, 0, out, 1);
 }
 
-static int create_system(const ks_setup* s, int device, int nranks, int rank, ks_kron** out) {
+static int create_system(const ks_setup* s, int device, int nranks, int rank, ks_kron** out, int kind) {
     if (!s) return KS_EINVAL;
     const int d = s->d, D = d + 1;
     const double nu = s->nu;
@@ -480,13 +496,22 @@ static int create_system(const ks_setup* s, int device, int nranks, int rank, ks
         for (int l = 0; l < d; ++l) f[l + 1] = M[l];
         return f;
     };
-    terms.push_back({{1.0, 0.0}, with_masses(Lt)});
-    for (int l = 0; l < d; ++l) {
+    if (kind == 1) {
+        const Band<cplx>* W = keep(s->Wt);
+        terms.push_back({{1.0, 0.0}, with_masses(W)});
+        for (int l = 0; l < d; ++l) {
+            auto f = with_masses(Mt);
+            f[l + 1] = Gt[l];
+            terms.push_back({{-nu, 0.0}, f});
+        }
+    }
+    if (kind == 0) terms.push_back({{1.0, 0.0}, with_masses(Lt)});
+    for (int l = 0; l < d && kind == 0; ++l) {
         auto f = with_masses(Mt);
         f[l + 1] = V[l];
         terms.push_back({{nu * nu, 0.0}, f});
     }
-    for (int l = 0; l < d; ++l)
+    for (int l = 0; l < d && kind == 0; ++l)
         for (int m = 0; m < d; ++m) {
             if (l == m) continue;
             auto f = with_masses(Mt);
@@ -494,7 +519,7 @@ static int create_system(const ks_setup* s, int device, int nranks, int rank, ks
             f[m + 1] = Gt[m];
             terms.push_back({{nu * nu, 0.0}, f});
         }
-    for (int l = 0; l < d; ++l) {
+    for (int l = 0; l < d && kind == 0; ++l) {
         auto f = with_masses(Wsym);
         f[l + 1] = L[l];
         terms.push_back({{nu, 0.0}, f});

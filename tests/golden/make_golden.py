@@ -35,6 +35,8 @@ TW = [(2, 8), (3, 8), (4, 8), (2, 16), (3, 16), (4, 16)]  # Table 2: 7 / 9 / 10 
 # final-condition trial space (time basis drops its LAST function, assembly.hpp:59-62;
 # SURVEY 8(f) rank 2): same Kronecker skeleton, different time restriction
 FC_CASES = [(1, 2, 5, 4), (2, 3, 8, 7), (3, 2, 6, 6)]
+# Galerkin fast solver (fdsolver.cpp:177-191) and Galerkin operator (assembly.cpp:273-286)
+GAL_CASES = [(1, 2, 5, 4), (2, 3, 6, 5), (3, 2, 6, 6)]
 
 
 def case(d, p, n_el, n_el_t, trial=0):
@@ -64,10 +66,28 @@ def case(d, p, n_el, n_el_t, trial=0):
     return out
 
 
+def galerkin_case(d, p, n_el, n_el_t):
+    R = refdrv.RefProblem(d, p, n_el, n_el_t)
+    Lt, Mt, Wt = R.time_bands()
+    out = {"dims": np.array(R.dims), "p": p, "Lt": Lt, "Mt": Mt, "Wt": Wt}
+    for l in range(d):
+        U, lam = R.eig(l)
+        M, L, G, V = R.space_bands(l)
+        out.update({f"U{l}": U, f"lam{l}": lam, f"M{l}": M, f"L{l}": L, f"G{l}": G, f"V{l}": V})
+    r = O.random_vec(R.N, 1234)
+    refdrv.force_backend("scalar")
+    out.update(r=r, z_gal=R.galerkin_apply(r), z_gal_adj=R.galerkin_apply(r, True), y_gal=R.galerkin_kron_apply(r))
+    return out
+
+
 def main():
     for c in CASES:
         name = "case_d%d_p%d_n%d_t%d.npz" % c
         np.savez_compressed(os.path.join(HERE, name), **case(*c))
+        print("wrote", name)
+    for c in GAL_CASES:
+        name = "gal_d%d_p%d_n%d_t%d.npz" % c
+        np.savez_compressed(os.path.join(HERE, name), **galerkin_case(*c))
         print("wrote", name)
     for c in FC_CASES:
         name = "case_fc_d%d_p%d_n%d_t%d.npz" % c
