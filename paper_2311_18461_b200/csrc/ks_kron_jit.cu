@@ -100,6 +100,7 @@ struct KronJitPair {
     int nin = 0, nmid = 0, nout = 0, bw = 0, ncoef = 0;
     bool pull = true;
     int T = 0, nq = 1, no = 1, D = 2, pad = 0; // block size, point block, ring depth, ring halo
+    size_t smem = 0;                           // ring + staged axis-b bands
     long long s_a = 0, n_outer = 0;
     int n_a = 0, n_b = 0;
     unsigned grid = 0;
@@ -152,6 +153,18 @@ KronJitPair* kron_jit_build(int nin, int nmid, int nout, int bw, const std::vect
     const int minb = 1;
     const int minb_env = std::getenv("KS_KRON_JIT_MINB") ? std::atoi(std::getenv("KS_KRON_JIT_MINB")) : 0;
     auto is_real = [&](int f) { return f >= 0 && freal[f] != 0; };
+    // axis-b factor bands staged in shared memory once per CTA (they are read
+    // every plane, uniformly across the CTA)
+    std::vector<int> fbl;
+    {
+        std::set<int> t;
+        for (auto& c : b)
+            if (c.factor >= 0) t.insert(c.factor);
+        fbl.assign(t.begin(), t.end());
+    }
+    const size_t bstage = fbl.size() * (size_t)n_b * W * sizeof(double2);
+    const bool stage = smem(D) + bstage <= 200 * 1024 && !std::getenv("KS_KRON_JIT_NOSTAGE");
+    auto bidx = [&](int f) { return (int)(std::find(fbl.begin(), fbl.end(), f) - fbl.begin()); };
     std::ostringstream s;
     s << "// generated: fused level passes (ks_kron_jit.cu)\n"
       << "#define BW " << bw << "\n#define W " << W << "\n#define NIN " << nin << "\n#define T " << T
@@ -181,7 +194,14 @@ ks_pair(const double2* const* __restrict__ ip, double2* const* __restrict__ op, 
     const double2 Z = make_double2(0.0, 0.0);
     // halos (and whole rings) zero: out-of-range taps meet zero band entries
     for (int e = tid; e < D * NIN * RS; e += T) ring[e] = Z;
-    __syncthreads();
+)";
+    if (stage) {
+        s << "    double2* bsm = ring + D * NIN * RS; // [factor][row][W] axis-b bands\n";
+        for (size_t j = 0; j < fbl.size(); ++j)
+            s << "    for (int e = tid; e < n_b * W; e += T) bsm[" << j << " * n_b * W + e] = rb[(unsigned long long)"
+              << fbl[j] << " * nmax * W + e];\n";
+    }
+    s << R"(    __syncthreads();
     const double2* src[NIN];
 #pragma unroll
     for (int g = 0; g < NIN; ++g) src[g] = ip[g] + base;
@@ -261,8 +281,10 @@ ks_pair(const double2* const* __restrict__ ip, double2* const* __restrict__ op, 
         // axis-b rows at row rd (uniform across the CTA)
         for (int f : fb) {
             s << "        " << (is_real(f) ? "double" : "double2") << " B" << f << "[W];\n"
-              << "#pragma unroll\n        for (int j = 0; j < W; ++j) { const double2 t = rb[((unsigned long long)" << f
-              << " * nmax + rd) * W + j]; B" << f << "[j] = t" << (is_real(f) ? ".x" : "") << "; }\n";
+              << "#pragma unroll\n        for (int j = 0; j < W; ++j) { const double2 t = "
+              << (stage ? "bsm[(" + lit(bidx(f)) + " * n_b + rd) * W + j]"
+                        : "rb[((unsigned long long)" + lit(f) + " * nmax + rd) * W + j]")
+              << "; B" << f << "[j] = t" << (is_real(f) ? ".x" : "") << "; }\n";
         }
         // distinct (h, f) products, then outputs
         std::set<std::pair<int, int>> hf;
@@ -294,8 +316,10 @@ ks_pair(const double2* const* __restrict__ ip, double2* const* __restrict__ op, 
         // push: column ib of each axis-b factor, F(ib + j - BW, ib), uniform
         for (int f : fb) {
             s << "            " << (is_real(f) ? "double" : "double2") << " C" << f << "[W];\n"
-              << "#pragma unroll\n            for (int j = 0; j < W; ++j) { const int r = ib + j - BW; const double2 t = (r >= 0 && r < n_b) ? rb[((unsigned long long)"
-              << f << " * nmax + r) * W + (W - 1 - j)] : Z; C" << f << "[j] = t" << (is_real(f) ? ".x" : "") << "; }\n";
+              << "#pragma unroll\n            for (int j = 0; j < W; ++j) { const int r = ib + j - BW; const double2 t = (r >= 0 && r < n_b) ? "
+              << (stage ? "bsm[(" + lit(bidx(f)) + " * n_b + r) * W + (W - 1 - j)]"
+                        : "rb[((unsigned long long)" + lit(f) + " * nmax + r) * W + (W - 1 - j)]")
+              << " : Z; C" << f << "[j] = t" << (is_real(f) ? ".x" : "") << "; }\n";
         }
         // cm = sum over contributions into (o, f) of c * m_h; then win[o][j] += C_f[j] * cm
         std::set<std::pair<int, int>> of;
@@ -350,6 +374,7 @@ ks_pair(const double2* const* __restrict__ ip, double2* const* __restrict__ op, 
     P->no = no;
     P->D = D;
     P->pad = pad;
+    P->smem = smem(D) + (stage ? bstage : 0);
     P->s_a = s_a;
     P->n_a = n_a;
     P->n_b = n_b;
@@ -380,8 +405,7 @@ bool kron_jit_launch(const KronJitPair& J, const double2* const* ip, double2* co
     int n_a = J.n_a, n_b = J.n_b, nq = J.nq, no = J.no, D = J.D;
     void* args[] = {(void*)&ip, (void*)&op, (void*)&rb, (void*)&nmax, (void*)&s_a, (void*)&n_a,
                     (void*)&n_b, (void*)&n_outer, (void*)&nq, (void*)&no, (void*)&D, (void*)coef.data()};
-    const size_t sm = (size_t)D * J.nin * (J.T + 2 * J.pad) * sizeof(double2);
-    KS_CUDA(cudaLaunchKernel((const void*)J.k.fn, dim3(J.grid), dim3(J.T), args, sm, st));
+    KS_CUDA(cudaLaunchKernel((const void*)J.k.fn, dim3(J.grid), dim3(J.T), args, J.smem, st));
     check_launch("ks_pair (jit)");
     return true;
 }
