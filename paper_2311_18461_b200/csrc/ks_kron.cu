@@ -559,7 +559,9 @@ void kron_apply(KronPlan& P, const double2* x, double2* y, cudaStream_t st,
             const KronPass& nx = P.passes[k + 1];
             auto ip = reinterpret_cast<const double2* const*>(dp + P.ptr_off[k]);
             auto op = reinterpret_cast<double2* const*>(const_cast<void**>(dp + P.ptr_off[k + 1] + nx.n_in));
-            if (kron_jit_launch(*P.jit[k], ip, op, P.d_rowband.as<double2>(), P.nmax, st)) {
+            if (kron_jit_launch(*P.jit[k], ip, op, host_ptrs.data() + P.ptr_off[k],
+                                host_ptrs.data() + P.ptr_off[k + 1] + nx.n_in, P.d_rowband.as<double2>(), P.nmax,
+                                st)) {
                 ++k;
                 continue;
             }

@@ -164,12 +164,23 @@ KronJitPair* kron_jit_build(int nin, int nmid, int nout, int bw, const std::vect
     }
     const size_t bstage = fbl.size() * (size_t)n_b * W * sizeof(double2);
     const bool stage = smem(D) + bstage <= 200 * 1024 && !std::getenv("KS_KRON_JIT_NOSTAGE");
+    size_t nfa = 0;
+    {
+        std::set<int> t;
+        for (auto& c : a)
+            if (c.factor >= 0) t.insert(c.factor);
+        nfa = t.size();
+    }
+    const size_t astage = nfa * (size_t)n_a * W * sizeof(double2);
+    const bool asm_rows = std::getenv("KS_KRON_JIT_ASMEM") && std::strcmp(std::getenv("KS_KRON_JIT_ASMEM"), "1") == 0 &&
+                          smem(D) + (stage ? bstage : 0) + astage <= 200 * 1024;
     auto bidx = [&](int f) { return (int)(std::find(fbl.begin(), fbl.end(), f) - fbl.begin()); };
     std::ostringstream s;
     s << "// generated: fused level passes (ks_kron_jit.cu)\n"
       << "#define BW " << bw << "\n#define W " << W << "\n#define NIN " << nin << "\n#define T " << T
       << "\n#define RS " << RS << "\n#define PAD " << pad << "\n"
-      << "struct Coef { double2 c[" << std::max<size_t>(1, coeffs.size()) << "]; };\n"
+      << "struct Coef { double2 c[" << std::max<size_t>(1, coeffs.size()) << "]; const double2* in[" << nin
+      << "]; double2* out[" << nout << "]; };\n"
       << R"(
 __device__ __forceinline__ void cacc(double2& a, const double2 c, const double2 v) {
     a.x = fma(c.x, v.x, fma(-c.y, v.y, a.x));
@@ -201,33 +212,52 @@ ks_pair(const double2* const* __restrict__ ip, double2* const* __restrict__ op, 
             s << "    for (int e = tid; e < n_b * W; e += T) bsm[" << j << " * n_b * W + e] = rb[(unsigned long long)"
               << fbl[j] << " * nmax * W + e];\n";
     }
+    if (asm_rows) {
+        std::set<int> fa0;
+        for (auto& c : a)
+            if (c.factor >= 0) fa0.insert(c.factor);
+        int j = 0;
+        s << "    { double2* ar = ring + D * NIN * RS + " << (stage ? fbl.size() : 0) << " * n_b * W;\n";
+        for (int f : fa0)
+            s << "      for (int e = tid; e < n_a * W; e += T) ar[" << j++ << " * n_a * W + e] = rb[(unsigned long long)" << f
+              << " * nmax * W + e];\n";
+        s << "    }\n";
+    }
     s << R"(    __syncthreads();
-    const double2* src[NIN];
-#pragma unroll
-    for (int g = 0; g < NIN; ++g) src[g] = ip[g] + base;
     auto issue = [&](int ib) {
         if (ib < n_b) {
             double2* slot = ring + (ib % D) * (NIN * RS) + PAD + tid;
-            const long long off = s_b * ib;
+            const long long off = base + s_b * ib;
 #pragma unroll
             for (int g = 0; g < NIN; ++g)
-                cp16(slot + g * RS, valid ? (const void*)(src[g] + off) : (const void*)ip[0], valid);
+                cp16(slot + g * RS, valid ? (const void*)(P.in[g] + off) : (const void*)P.in[0], valid);
         }
         asm volatile("cp.async.commit_group;\n" ::);
     };
     for (int k = 0; k < D - 1; ++k) issue(k);
 )";
-    // axis-a factor rows (the thread's own row ia, constant over the sweep)
+    // axis-a factor rows (the thread's own row ia, constant over the sweep):
+    // registers, or (asm_rows) shared memory [factor][row][W]
     std::set<int> fa;
     for (auto& c : a)
         if (c.factor >= 0) fa.insert(c.factor);
-    for (int f : fa) {
-        if (is_real(f))
-            s << "    double A" << f << "[W];\n";
-        else
-            s << "    double2 A" << f << "[W];\n";
-        s << "#pragma unroll\n    for (int k = 0; k < W; ++k) { const double2 t = valid ? rb[((unsigned long long)" << f
-          << " * nmax + ia) * W + k] : Z; A" << f << "[k] = t" << (is_real(f) ? ".x" : "") << "; }\n";
+    std::vector<int> fal(fa.begin(), fa.end());
+    auto aref = [&](int f, const char* k) -> std::string {
+        if (!asm_rows) return "A" + lit(f) + "[" + k + "]";
+        const int j = (int)(std::find(fal.begin(), fal.end(), f) - fal.begin());
+        return std::string("asmr[(") + lit(j) + " * n_a + ia) * W + " + k + "]" + (is_real(f) ? ".x" : "");
+    };
+    if (asm_rows) {
+        s << "    const double2* asmr = ring + D * NIN * RS + " << (stage ? fbl.size() : 0) << " * n_b * W;\n";
+    } else {
+        for (int f : fa) {
+            if (is_real(f))
+                s << "    double A" << f << "[W];\n";
+            else
+                s << "    double2 A" << f << "[W];\n";
+            s << "#pragma unroll\n    for (int k = 0; k < W; ++k) { const double2 t = valid ? rb[((unsigned long long)" << f
+              << " * nmax + ia) * W + k] : Z; A" << f << "[k] = t" << (is_real(f) ? ".x" : "") << "; }\n";
+        }
     }
     const int nwin = pull ? nmid : nout;
     s << "    double2 win[" << nwin << "][W];\n"
@@ -260,10 +290,10 @@ ks_pair(const double2* const* __restrict__ ip, double2* const* __restrict__ op, 
             } else {
                 s << "                double2 " << v << " = Z;\n#pragma unroll\n                for (int k = 0; k < W; ++k) {";
                 if (is_real(f))
-                    s << " " << v << ".x = fma(A" << f << "[k], w[k].x, " << v << ".x); " << v << ".y = fma(A" << f
-                      << "[k], w[k].y, " << v << ".y); }\n";
+                    s << " " << v << ".x = fma(" << aref(f, "k") << ", w[k].x, " << v << ".x); " << v << ".y = fma("
+                      << aref(f, "k") << ", w[k].y, " << v << ".y); }\n";
                 else
-                    s << " cacc(" << v << ", A" << f << "[k], w[k]); }\n";
+                    s << " cacc(" << v << ", " << aref(f, "k") << ", w[k]); }\n";
             }
             for (auto* c : cs)
                 if (c->factor == f) s << "                cacc(m" << c->out << ", P.c[" << c->coeff << "], " << v << ");\n";
@@ -309,7 +339,7 @@ ks_pair(const double2* const* __restrict__ ip, double2* const* __restrict__ op, 
                 if (c.out == o)
                     s << "          cacc(acc, P.c[" << c.coeff << "], d" << c.in << "_"
                       << (c.factor < 0 ? std::string("I") : lit(c.factor)) << ");\n";
-            s << "          if (valid) op[" << o << "][base + s_b * rd] = acc; }\n";
+            s << "          if (valid) P.out[" << o << "][base + s_b * rd] = acc; }\n";
         }
         s << "    }\n";
     } else {
@@ -341,7 +371,7 @@ ks_pair(const double2* const* __restrict__ ip, double2* const* __restrict__ op, 
             }
         }
         s << "        }\n        const int rd = ib - BW;\n        if (rd >= 0 && valid) {\n";
-        for (int o = 0; o < nout; ++o) s << "            op[" << o << "][base + s_b * rd] = win[" << o << "][0];\n";
+        for (int o = 0; o < nout; ++o) s << "            P.out[" << o << "][base + s_b * rd] = win[" << o << "][0];\n";
         s << "        }\n#pragma unroll\n        for (int o = 0; o < " << nout
           << "; ++o) {\n#pragma unroll\n            for (int j = 0; j < W - 1; ++j) win[o][j] = win[o][j + 1];\n"
           << "            win[o][W - 1] = Z;\n        }\n    }\n";
@@ -374,7 +404,7 @@ ks_pair(const double2* const* __restrict__ ip, double2* const* __restrict__ op, 
     P->no = no;
     P->D = D;
     P->pad = pad;
-    P->smem = smem(D) + (stage ? bstage : 0);
+    P->smem = smem(D) + (stage ? bstage : 0) + (asm_rows ? astage : 0);
     P->s_a = s_a;
     P->n_a = n_a;
     P->n_b = n_b;
@@ -387,8 +417,8 @@ ks_pair(const double2* const* __restrict__ ip, double2* const* __restrict__ op, 
 
 // launch over the plan's tensors (geometry fixed at build); false when the
 // grid is too small to fill the GPU (the caller runs the passes separately)
-bool kron_jit_launch(const KronJitPair& J, const double2* const* ip, double2* const* op, const double2* rb, int nmax,
-                     cudaStream_t st) {
+bool kron_jit_launch(const KronJitPair& J, const double2* const* ip, double2* const* op, void* const* hin,
+                     void* const* hout, const double2* rb, int nmax, cudaStream_t st) {
     static int sms = 0;
     if (!sms) {
         int dev = 0;
@@ -399,8 +429,13 @@ bool kron_jit_launch(const KronJitPair& J, const double2* const* ip, double2* co
     // (c2: 22 CTAs, 0.23 ms vs 0.064 ms for the per-pass kernels)
     if (J.grid < (unsigned)(2 * sms)) return false;
     // by-value coefficient table (constant bank)
-    std::vector<double2> coef(std::max(1, J.ncoef));
+    // by-value parameter: coefficients, then the input and output tensor pointers
+    const size_t nc = (size_t)std::max(1, J.ncoef);
+    std::vector<double2> coef(nc + (size_t)(J.nin + J.nout + 1) / 2 + 1);
     std::copy(J.coef.begin(), J.coef.end(), coef.begin());
+    void** pp = reinterpret_cast<void**>(coef.data() + nc);
+    for (int g = 0; g < J.nin; ++g) pp[g] = hin[g];
+    for (int o = 0; o < J.nout; ++o) pp[J.nin + o] = hout[o];
     long long s_a = J.s_a, n_outer = J.n_outer;
     int n_a = J.n_a, n_b = J.n_b, nq = J.nq, no = J.no, D = J.D;
     void* args[] = {(void*)&ip, (void*)&op, (void*)&rb, (void*)&nmax, (void*)&s_a, (void*)&n_a,
