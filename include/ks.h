@@ -291,7 +291,45 @@ int ks_setup_create_galerkin_operator(const ks_setup* s, int device, ks_kron** o
 /* The same operator sharded over nranks (ks_kronshard_*). */
 int ks_setup_create_system_sharded(const ks_setup* s, int nranks, int rank, int device,
                                    ks_kron** out);
+/* unrestricted (full) tensor dims (SpaceTimeProblem::full_dims, assembly.hpp:51) */
+int ks_setup_full_dims(const ks_setup* s, int* dims /* d+1 */);
+/* element_quadrature(kv, p+1) of axis `axis` (0 = time; bspline.cpp:189-208):
+ * *nq nodes; nodes / weights may be NULL to query the size */
+int ks_setup_quad_rule(const ks_setup* s, int axis, int* nq, double* nodes, double* weights);
+/* KnotVector::greville (bspline.cpp:77-86) of axis `axis`: *n = full basis size */
+int ks_setup_greville(const ks_setup* s, int axis, int* n, double* pts);
 int ks_setup_destroy(ks_setup* s);
+
+/* ---------------------------------------------------------------------------
+ * Right-hand side, lifting and error norms on the device.
+ * The caller samples f / u / g at the points; the sum-factorised quadrature
+ * contractions, collocation solves, full-space operator and reductions run on
+ * the GPU. Quadrature grid: axis a has nq[a] nodes (ks_setup_quad_rule order),
+ * axis 0 (time) fastest; the outermost axis is processed in chunks of rows
+ * [r0, r1) inside one element (at most p+1 rows), as the reference does.
+ * ------------------------------------------------------------------------- */
+typedef struct ks_quad ks_quad;
+int ks_quad_create(const ks_setup* s, int device, ks_quad** out);
+int ks_quad_destroy(ks_quad* q);
+int ks_quad_dims(const ks_quad* q, int* nq /* d+1 */, int* chunk, int* full_dims /* d+1 */);
+/* assemble_rhs(prob, f) (assembly.cpp:390-404): reset, accumulate the moments
+ * of f chunk by chunk (f: raw samples on the chunk grid), then combine and
+ * restrict to the reduced space */
+int ks_quad_rhs_reset(ks_quad* q);
+int ks_quad_rhs_chunk(ks_quad* q, int r0, int r1, const ks_c64* f, int mem);
+int ks_quad_rhs_finish(ks_quad* q, ks_c64* rhs /* reduced */, int mem);
+/* lift_nonhomogeneous (assembly.cpp:514-570): g sampled on the full Greville
+ * grid -> boundary coefficients (full dims; zero on free indices) and the
+ * correction restrict(A_full g_h); corrected_rhs = assemble_rhs(f) - correction */
+int ks_quad_lift(ks_quad* q, const ks_c64* g_greville, int mem, ks_c64* boundary, ks_c64* correction);
+/* extend_with_boundary (assembly.cpp:468-490); boundary may be NULL (zeros) */
+int ks_quad_extend(ks_quad* q, const ks_c64* reduced, const ks_c64* boundary, int mem, ks_c64* full);
+/* error_norms (experiments.cpp:73-153): set the full coefficients, then per
+ * chunk return sum w |u - u_h|^2 and sum w |f - S u_h|^2 (S u = i u_t - nu lap u);
+ * L2 = sqrt(sum l2sq), energy = sqrt(sum l2sq + sum ressq) */
+int ks_quad_error_set(ks_quad* q, const ks_c64* full_coeffs, int mem);
+int ks_quad_error_chunk(ks_quad* q, int r0, int r1, const ks_c64* u, const ks_c64* f, int mem,
+                        double* l2sq, double* ressq);
 
 #ifdef __cplusplus
 }

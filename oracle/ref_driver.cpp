@@ -252,6 +252,84 @@ int ref_sinsin_rhs(void* h, std::complex<double>* rhs, std::complex<double>* bou
     return 0;
 }
 
+// manufactured solution by name: the reference's named problems (problems.cpp)
+// or "sinsin" (c2/c4: u = prod sin(pi x_l) e^{-i d pi^2 t}, f = d pi^2 u)
+static ManufacturedSolution solution_by_name(const RefProblem* r, const std::string& name) {
+    if (name != "sinsin") return find_problem(name);
+    const double pi = 3.14159265358979323846;
+    ManufacturedSolution s;
+    s.name = "sinsin";
+    s.d = r->prob.d;
+    s.T = r->prob.T;
+    s.nu = r->prob.nu;
+    s.homogeneous = false;
+    s.u = [pi](double t, std::span<const double> x) {
+        double v = 1.0;
+        for (double xi : x) v *= std::sin(pi * xi);
+        return v * std::exp(cplx(0, -(double)x.size() * pi * pi * t));
+    };
+    auto u = s.u;
+    s.f = [pi, u](double t, std::span<const double> x) { return (double)x.size() * pi * pi * u(t, x); };
+    return s;
+}
+
+// lift_nonhomogeneous (assembly.cpp:514-570) for a named solution: corrected rhs + boundary coefficients
+int ref_lift_named(void* h, const char* name, std::complex<double>* rhs, std::complex<double>* boundary) {
+    auto* r = static_cast<RefProblem*>(h);
+    try {
+        const ManufacturedSolution s = solution_by_name(r, name);
+        const Lifting L = lift_nonhomogeneous(r->prob, s.u, s.f);
+        std::copy(L.corrected_rhs.begin(), L.corrected_rhs.end(), rhs);
+        std::copy(L.boundary_coeffs.begin(), L.boundary_coeffs.end(), boundary);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+// assemble_rhs (assembly.cpp:390-404) of a named solution's f
+int ref_assemble_rhs_named(void* h, const char* name, std::complex<double>* rhs) {
+    auto* r = static_cast<RefProblem*>(h);
+    try {
+        const ManufacturedSolution s = solution_by_name(r, name);
+        const std::vector<cplx> b = assemble_rhs(r->prob, s.f);
+        std::copy(b.begin(), b.end(), rhs);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+// error_norms (experiments.cpp:73-153) of full coefficients against a named solution
+int ref_error_norms_named(void* h, const char* name, const std::complex<double>* full, double* l2, double* energy) {
+    auto* r = static_cast<RefProblem*>(h);
+    try {
+        const ManufacturedSolution s = solution_by_name(r, name);
+        const size_t n = CoeffTensor::total(r->prob.full_dims());
+        const std::vector<cplx> c(full, full + n);
+        const auto e = error_norms(r->prob, c, s);
+        *l2 = e.first;
+        *energy = e.second;
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+// extend_with_boundary (assembly.cpp:468-490)
+int ref_extend(void* h, const std::complex<double>* reduced, const std::complex<double>* boundary,
+               std::complex<double>* full) {
+    auto* r = static_cast<RefProblem*>(h);
+    const size_t nr = CoeffTensor::total(r->prob.reduced_dims()), nf = CoeffTensor::total(r->prob.full_dims());
+    const std::vector<cplx> red(reduced, reduced + nr), bnd(boundary, boundary + nf);
+    const std::vector<cplx> f = extend_with_boundary(r->prob, red, bnd);
+    std::copy(f.begin(), f.end(), full);
+    return 0;
+}
+
 // RHS of a named manufactured problem (problems.cpp:find_problem) exactly as
 // solve_problem builds it (experiments.cpp:34-42): assemble_rhs if
 // homogeneous, else lift_nonhomogeneous.

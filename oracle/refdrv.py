@@ -54,6 +54,14 @@ def rlib():
         L.ref_galerkin_apply.argtypes = [P, P, P, I]
         L.ref_galerkin_kron_apply.restype = I
         L.ref_galerkin_kron_apply.argtypes = [P, P, P]
+        L.ref_lift_named.restype = I
+        L.ref_lift_named.argtypes = [P, C.c_char_p, P, P]
+        L.ref_assemble_rhs_named.restype = I
+        L.ref_assemble_rhs_named.argtypes = [P, C.c_char_p, P]
+        L.ref_error_norms_named.restype = I
+        L.ref_error_norms_named.argtypes = [P, C.c_char_p, P, C.POINTER(D), C.POINTER(D)]
+        L.ref_extend.restype = I
+        L.ref_extend.argtypes = [P, P, P, P]
         _r = L
     return _r
 
@@ -139,6 +147,37 @@ class RefProblem:
         if rlib().ref_galerkin_kron_apply(self._h, _p(x), _p(y)):
             raise RuntimeError(rlib().ref_last_error().decode())
         return y
+
+    def full_size(self):
+        return int(np.prod([self.dims[0] + 1] + [n + 2 for n in self.dims[1:]]))
+
+    def lift_named(self, name):
+        """lift_nonhomogeneous (assembly.cpp:514-570): (corrected rhs, boundary coefficients)."""
+        rhs = np.zeros(self.N, dtype=np.complex128)
+        bnd = np.zeros(self.full_size(), dtype=np.complex128)
+        if rlib().ref_lift_named(self._h, name.encode(), _p(rhs), _p(bnd)):
+            raise ValueError(rlib().ref_last_error().decode())
+        return rhs, bnd
+
+    def assemble_rhs_named(self, name):
+        rhs = np.zeros(self.N, dtype=np.complex128)
+        if rlib().ref_assemble_rhs_named(self._h, name.encode(), _p(rhs)):
+            raise ValueError(rlib().ref_last_error().decode())
+        return rhs
+
+    def error_norms_named(self, name, full):
+        full = np.ascontiguousarray(full, dtype=np.complex128).ravel()
+        l2, en = C.c_double(), C.c_double()
+        if rlib().ref_error_norms_named(self._h, name.encode(), _p(full), C.byref(l2), C.byref(en)):
+            raise ValueError(rlib().ref_last_error().decode())
+        return l2.value, en.value
+
+    def extend(self, reduced, boundary):
+        out = np.zeros(self.full_size(), dtype=np.complex128)
+        reduced = np.ascontiguousarray(reduced, dtype=np.complex128)
+        boundary = np.ascontiguousarray(boundary, dtype=np.complex128)
+        rlib().ref_extend(self._h, _p(reduced), _p(boundary), _p(out))
+        return out
 
     def fd_block(self, i):
         nt, ld = self.dims[0], 3 * self.p + 1

@@ -161,6 +161,20 @@ _SIGS = {
     "ks_setup_create_fd": (C.c_int, [_P, C.c_int, C.POINTER(_P)]),
     "ks_setup_create_system": (C.c_int, [_P, C.c_int, C.POINTER(_P)]),
     "ks_setup_create_galerkin_fd": (C.c_int, [_P, C.c_int, C.POINTER(_P)]),
+    "ks_setup_full_dims": (C.c_int, [_P, _P]),
+    "ks_setup_quad_rule": (C.c_int, [_P, C.c_int, C.POINTER(C.c_int), _P, _P]),
+    "ks_setup_greville": (C.c_int, [_P, C.c_int, C.POINTER(C.c_int), _P]),
+    "ks_quad_create": (C.c_int, [_P, C.c_int, C.POINTER(_P)]),
+    "ks_quad_destroy": (C.c_int, [_P]),
+    "ks_quad_dims": (C.c_int, [_P, _P, C.POINTER(C.c_int), _P]),
+    "ks_quad_rhs_reset": (C.c_int, [_P]),
+    "ks_quad_rhs_chunk": (C.c_int, [_P, C.c_int, C.c_int, _P, C.c_int]),
+    "ks_quad_rhs_finish": (C.c_int, [_P, _P, C.c_int]),
+    "ks_quad_lift": (C.c_int, [_P, _P, C.c_int, _P, _P]),
+    "ks_quad_extend": (C.c_int, [_P, _P, _P, C.c_int, _P]),
+    "ks_quad_error_set": (C.c_int, [_P, _P, C.c_int]),
+    "ks_quad_error_chunk": (C.c_int, [_P, C.c_int, C.c_int, _P, _P, C.c_int, C.POINTER(C.c_double),
+                                      C.POINTER(C.c_double)]),
     "ks_setup_create_galerkin_operator": (C.c_int, [_P, C.c_int, C.POINTER(_P)]),
     "ks_fd_create_galerkin": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.c_double, C.c_int, C.POINTER(_P),
                                         C.POINTER(_P), _P, _P, C.c_int, C.POINTER(_P)]),
@@ -579,6 +593,111 @@ def assemble_galerkin_operator(prob: SpaceTimeProblem, device: int = 0) -> Krone
     h = C.c_void_p()
     _check(lib().ks_setup_create_galerkin_operator(prob._h, device, C.byref(h)))
     return KroneckerOperator._wrap(h, prob.reduced_dims(), device)
+
+
+# ---------------------------------------------------------------------------
+# Right-hand side, lifting, error norms
+# ---------------------------------------------------------------------------
+class Quadrature:
+    """Device-side assemble_rhs / lift_nonhomogeneous / extend_with_boundary /
+    error_norms (assembly.cpp:390-404,468-490,514-570; experiments.cpp:73-153)
+    for a SpaceTimeProblem. Functions are vectorised numpy callables
+    fn(t, x_1, ..., x_d) returning complex arrays (broadcast over the grid);
+    they are sampled on the host, chunk by chunk along the outermost axis, and
+    every contraction / solve / operator / reduction runs on the GPU."""
+
+    def __init__(self, prob: "SpaceTimeProblem", device: int = 0):
+        self.prob = prob
+        self.d = prob.d
+        h = C.c_void_p()
+        _check(lib().ks_quad_create(prob._h, device, C.byref(h)))
+        self._h = h
+        D = self.d + 1
+        nq = (C.c_int * D)()
+        fd = (C.c_int * D)()
+        ch = C.c_int()
+        _check(lib().ks_quad_dims(h, nq, C.byref(ch), fd))
+        self.nq, self.chunk, self.full_dims = list(nq), ch.value, list(fd)
+        self.nodes, self.weights, self.greville = [], [], []
+        for a in range(D):
+            n = C.c_int()
+            x = np.zeros(self.nq[a])
+            w = np.zeros(self.nq[a])
+            _check(lib().ks_setup_quad_rule(prob._h, a, C.byref(n), _ptr(x), _ptr(w)))
+            self.nodes.append(x)
+            self.weights.append(w)
+            g = np.zeros(self.full_dims[a])
+            _check(lib().ks_setup_greville(prob._h, a, C.byref(n), _ptr(g)))
+            self.greville.append(g)
+        self.N_full = int(np.prod(self.full_dims))
+
+    @staticmethod
+    def _sample(fn, coords):
+        """fn on the tensor grid of coords (axis 0 = time fastest) -> flat complex array."""
+        D = len(coords)
+        args = []
+        for a, c in enumerate(coords):
+            shape = [1] * D
+            shape[D - 1 - a] = len(c)
+            args.append(np.asarray(c, dtype=np.float64).reshape(shape))
+        v = np.asarray(fn(*args), dtype=np.complex128)
+        v = np.broadcast_to(v, tuple(len(c) for c in reversed(coords)))
+        return np.ascontiguousarray(v).ravel()
+
+    def _chunks(self):
+        last = self.nq[self.d]
+        for r0 in range(0, last, self.chunk):
+            yield r0, min(last, r0 + self.chunk)
+
+    def assemble_rhs(self, f) -> np.ndarray:
+        _check(lib().ks_quad_rhs_reset(self._h))
+        for r0, r1 in self._chunks():
+            coords = self.nodes[:self.d] + [self.nodes[self.d][r0:r1]]
+            fs = self._sample(f, coords)
+            _check(lib().ks_quad_rhs_chunk(self._h, r0, r1, _ptr(fs), KS_MEM_HOST))
+        out = np.zeros(self.prob.N_dof, dtype=np.complex128)
+        _check(lib().ks_quad_rhs_finish(self._h, _ptr(out), KS_MEM_HOST))
+        return out
+
+    def lift(self, g, f):
+        """lift_nonhomogeneous: (corrected rhs, boundary coefficients on the full space)."""
+        rhs = self.assemble_rhs(f)
+        gs = self._sample(g, self.greville)
+        bnd = np.zeros(self.N_full, dtype=np.complex128)
+        corr = np.zeros(self.prob.N_dof, dtype=np.complex128)
+        _check(lib().ks_quad_lift(self._h, _ptr(gs), KS_MEM_HOST, _ptr(bnd), _ptr(corr)))
+        return rhs - corr, bnd
+
+    def extend(self, reduced, boundary=None) -> np.ndarray:
+        reduced = _cvec(reduced).ravel()
+        out = np.zeros(self.N_full, dtype=np.complex128)
+        b = None if boundary is None else _cvec(boundary).ravel()
+        _check(lib().ks_quad_extend(self._h, _ptr(reduced), None if b is None else _ptr(b), KS_MEM_HOST,
+                                    _ptr(out)))
+        return out
+
+    def error_norms(self, full_coeffs, u, f):
+        """(L2 error, sqrt(L2^2 + ||f - S u_h||^2)) as error_norms returns."""
+        c = _cvec(full_coeffs).ravel()
+        _check(lib().ks_quad_error_set(self._h, _ptr(c), KS_MEM_HOST))
+        l2 = res = 0.0
+        for r0, r1 in self._chunks():
+            coords = self.nodes[:self.d] + [self.nodes[self.d][r0:r1]]
+            us, fs = self._sample(u, coords), self._sample(f, coords)
+            a, b = C.c_double(), C.c_double()
+            _check(lib().ks_quad_error_chunk(self._h, r0, r1, _ptr(us), _ptr(fs), KS_MEM_HOST, C.byref(a),
+                                             C.byref(b)))
+            l2 += a.value
+            res += b.value
+        return float(np.sqrt(l2)), float(np.sqrt(l2 + res))
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().ks_quad_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
 
 
 # ---------------------------------------------------------------------------

@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "../../include/ks.h"
+#include "ks_quad_host.hpp"
 
 namespace ks_host {
 
@@ -539,6 +540,146 @@ static int create_system(const ks_setup* s, int device, int nranks, int rank, ks
     if (nranks > 0)
         return ks_kronshard_create(D, s->dims.data(), (int)kt.size(), kt.data(), nranks, rank, device, out);
     return ks_kron_create(D, s->dims.data(), (int)kt.size(), kt.data(), device, out);
+}
+
+// ---------------------------------------------------------------------------
+// quadrature / collocation data for the device RHS, lifting and error norms
+// (ks_rhs.cu): element_quadrature(kv, p+1) (bspline.cpp:189-208),
+// basis_eval_matrix (assembly.cpp:288-303), KnotVector::greville
+// (bspline.cpp:77-86), the lifting's collocation factor (assembly.cpp:540-550)
+// and the unrestricted univariate factors of assemble_system_operator_full
+// (assembly.cpp:260-263)
+// ---------------------------------------------------------------------------
+namespace {
+// factor_banded (eigensolve.cpp:77-121): kl = bw, ku_f = 2 bw, ldab = 3 bw + 1
+void factor_band_host(const Band<cplx>& H, std::vector<cplx>& ab, std::vector<int>& piv) {
+    const int n = H.n, p = H.bw, ldab = 3 * p + 1, kuf = 2 * p;
+    ab.assign((size_t)ldab * n, cplx(0, 0));
+    piv.assign(n, 0);
+    auto A = [&](int r, int c) -> cplx& { return ab[(size_t)(kuf + r - c) + (size_t)c * ldab]; };
+    for (int c = 0; c < n; ++c)
+        for (int r = std::max(0, c - p); r <= std::min(n - 1, c + p); ++r) A(r, c) = H.get(r, c);
+    for (int k = 0; k < n; ++k) {
+        const int imax = std::min(k + p, n - 1);
+        int pr = k;
+        double best = std::abs(A(k, k));
+        for (int r = k + 1; r <= imax; ++r)
+            if (std::abs(A(r, k)) > best) {
+                best = std::abs(A(r, k));
+                pr = r;
+            }
+        piv[k] = pr;
+        if (best == 0.0) throw std::runtime_error("factor_banded: singular collocation matrix");
+        const int jmax = std::min(k + kuf, n - 1);
+        if (pr != k)
+            for (int c = k; c <= jmax; ++c) std::swap(A(k, c), A(pr, c));
+        const cplx pv = A(k, k);
+        for (int r = k + 1; r <= imax; ++r) {
+            const cplx m = A(r, k) / pv;
+            A(r, k) = m;
+            if (m != cplx(0, 0))
+                for (int c = k + 1; c <= jmax; ++c) A(r, c) -= m * A(k, c);
+        }
+    }
+}
+
+ks::QuadAxis quad_axis(const Knots& k) {
+    ks::QuadAxis a;
+    const int p = k.p;
+    a.n = k.dim();
+    a.npe = p + 1;
+    std::vector<double> gx, gw;
+    gauss_legendre(p + 1, gx, gw);
+    for (size_t e = 0; e + 1 < k.u.size(); ++e) {
+        const double z0 = k.u[e], z1 = k.u[e + 1];
+        if (!(z1 > z0)) continue;
+        const double mid = 0.5 * (z0 + z1), half = 0.5 * (z1 - z0);
+        for (int q = 0; q <= p; ++q) {
+            a.nodes.push_back(mid + half * gx[q]);
+            a.weights.push_back(half * gw[q]);
+        }
+    }
+    a.nq = (int)a.nodes.size();
+    for (int o = 0; o < 3; ++o) a.E[o].assign((size_t)a.nq * (p + 1), 0.0);
+    a.off.assign(a.nq, 0);
+    for (int q = 0; q < a.nq; ++q) {
+        const Basis b = basis_at(k, a.nodes[q], 2);
+        a.off[q] = b.first;
+        for (int o = 0; o < 3; ++o)
+            for (int kk = 0; kk <= p; ++kk) a.E[o][(size_t)q * (p + 1) + kk] = b.d[o][kk];
+    }
+    a.greville.assign(a.n, 0.0);
+    for (int i = 0; i < a.n; ++i) {
+        double sm = 0.0;
+        for (int kk = 1; kk <= p; ++kk) sm += k.u[i + kk];
+        a.greville[i] = sm / p;
+    }
+    Band<cplx> C(a.n, p);
+    for (int i = 0; i < a.n; ++i) {
+        const Basis b = basis_at(k, a.greville[i], 0);
+        for (int kk = 0; kk <= p; ++kk)
+            if (C.in(i, b.first + kk)) C.at(i, b.first + kk) = b.d[0][kk];
+    }
+    factor_band_host(C, a.colloc_ab, a.colloc_piv);
+    return a;
+}
+} // namespace
+
+namespace ks {
+QuadData setup_quad_data(const ks_setup* s) {
+    if (!s) throw std::invalid_argument("ks_quad_create: NULL setup");
+    QuadData q;
+    q.d = s->d;
+    q.p = s->p;
+    q.trial = s->trial;
+    q.nu = s->nu;
+    q.red_dims = s->dims;
+    q.full_dims.push_back(s->tk.dim());
+    for (int l = 0; l < s->d; ++l) q.full_dims.push_back(s->sk[l].dim());
+    q.axes.push_back(quad_axis(s->tk));
+    for (int l = 0; l < s->d; ++l) q.axes.push_back(quad_axis(s->sk[l]));
+    q.Lt = univariate(Stiff, s->tk, None).a;
+    q.Mt = univariate(Mass, s->tk, None).a;
+    q.Wt = univariate(TimeDer, s->tk, None).a;
+    for (int l = 0; l < s->d; ++l) {
+        q.M.push_back(univariate(Mass, s->sk[l], None).a);
+        q.L.push_back(univariate(Stiff, s->sk[l], None).a);
+        q.G.push_back(univariate(Second, s->sk[l], None).a);
+        q.V.push_back(univariate(Bilap, s->sk[l], None).a);
+    }
+    return q;
+}
+} // namespace ks
+
+extern "C" int ks_setup_full_dims(const ks_setup* s, int* dims) {
+    if (!s || !dims) return KS_EINVAL;
+    dims[0] = s->tk.dim();
+    for (int l = 0; l < s->d; ++l) dims[l + 1] = s->sk[l].dim();
+    return KS_OK;
+}
+
+// element_quadrature(kv, p+1) of axis `axis` (0 = time): nq nodes / weights
+extern "C" int ks_setup_quad_rule(const ks_setup* s, int axis, int* nq, double* nodes, double* weights) {
+    if (!s || !nq || axis < 0 || axis > s->d) return KS_EINVAL;
+    const ks::QuadAxis a = quad_axis(axis == 0 ? s->tk : s->sk[axis - 1]);
+    *nq = a.nq;
+    if (nodes) std::copy(a.nodes.begin(), a.nodes.end(), nodes);
+    if (weights) std::copy(a.weights.begin(), a.weights.end(), weights);
+    return KS_OK;
+}
+
+// KnotVector::greville (bspline.cpp:77-86) of axis `axis`: n = full basis size
+extern "C" int ks_setup_greville(const ks_setup* s, int axis, int* n, double* pts) {
+    if (!s || !n || axis < 0 || axis > s->d) return KS_EINVAL;
+    const Knots& k = axis == 0 ? s->tk : s->sk[axis - 1];
+    *n = k.dim();
+    if (pts)
+        for (int i = 0; i < k.dim(); ++i) {
+            double sm = 0.0;
+            for (int kk = 1; kk <= k.p; ++kk) sm += k.u[i + kk];
+            pts[i] = sm / k.p;
+        }
+    return KS_OK;
 }
 
 extern "C" int ks_setup_destroy(ks_setup* s) {

@@ -37,6 +37,9 @@ TW = [(2, 8), (3, 8), (4, 8), (2, 16), (3, 16), (4, 16)]  # Table 2: 7 / 9 / 10 
 FC_CASES = [(1, 2, 5, 4), (2, 3, 8, 7), (3, 2, 6, 6)]
 # Galerkin fast solver (fdsolver.cpp:177-191) and Galerkin operator (assembly.cpp:273-286)
 GAL_CASES = [(1, 2, 5, 4), (2, 3, 6, 5), (3, 2, 6, 6)]
+# right-hand side, lifting, solution and error norms of manufactured solutions
+# (assembly.cpp:390-404,514-570; experiments.cpp:73-153): (d, p, n_el, name)
+RHS_CASES = [(1, 3, 8, "sinsin"), (2, 2, 6, "sinsin"), (2, 3, 6, "traveling_wave_2d"), (3, 2, 4, "sinsin")]
 
 
 def case(d, p, n_el, n_el_t, trial=0):
@@ -80,6 +83,18 @@ def galerkin_case(d, p, n_el, n_el_t):
     return out
 
 
+def rhs_case(d, p, n_el, name):
+    R = refdrv.RefProblem(d, p, n_el, n_el)
+    refdrv.force_backend("scalar")
+    b0 = R.assemble_rhs_named(name)
+    rhs, bnd = R.lift_named(name)
+    sol = R.pcg(rhs, 1e-10, 400)
+    full = R.extend(sol["x"], bnd)
+    l2, en = R.error_norms_named(name, full)
+    return {"d": d, "p": p, "n_el": n_el, "name": name, "dims": np.array(R.dims), "rhs_f": b0, "rhs": rhs,
+            "boundary": bnd, "x": sol["x"], "full": full, "l2": l2, "energy": en}
+
+
 def main():
     for c in CASES:
         name = "case_d%d_p%d_n%d_t%d.npz" % c
@@ -88,6 +103,10 @@ def main():
     for c in GAL_CASES:
         name = "gal_d%d_p%d_n%d_t%d.npz" % c
         np.savez_compressed(os.path.join(HERE, name), **galerkin_case(*c))
+        print("wrote", name)
+    for c in RHS_CASES:
+        name = "rhs_d%d_p%d_n%d_%s.npz" % c
+        np.savez_compressed(os.path.join(HERE, name), **rhs_case(*c))
         print("wrote", name)
     for c in FC_CASES:
         name = "case_fc_d%d_p%d_n%d_t%d.npz" % c
