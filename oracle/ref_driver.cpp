@@ -233,7 +233,7 @@ int ref_galerkin_kron_apply(void* h, const std::complex<double>* x, std::complex
     }
 }
 
-// c2/c4 manufactured solution u = sin(pi x) sin(pi y) e^{-i 2 pi^2 t}, f = S u = 4 pi^2 u
+// c2/c4 manufactured solution u = sin(pi x) sin(pi y) e^{-i 2 pi^2 t}, f = S u = (1+nu) d pi^2 u (4 pi^2 u at d=2, nu=1)
 // (SURVEY G2), lifted with lift_nonhomogeneous (assembly.cpp:514-570)
 int ref_sinsin_rhs(void* h, std::complex<double>* rhs, std::complex<double>* boundary) {
     auto* r = static_cast<RefProblem*>(h);
@@ -243,8 +243,9 @@ int ref_sinsin_rhs(void* h, std::complex<double>* rhs, std::complex<double>* bou
         for (double xi : x) s *= std::sin(pi * xi);
         return s * std::exp(cplx(0, -(double)x.size() * pi * pi * t));
     };
-    SpaceTimeFn f = [pi, u](double t, std::span<const double> x) {
-        return (double)x.size() * pi * pi * u(t, x);
+    const double nu = r->prob.nu;
+    SpaceTimeFn f = [pi, u, nu](double t, std::span<const double> x) { // S u = i u_t - nu lap u
+        return (1.0 + nu) * (double)x.size() * pi * pi * u(t, x);
     };
     const Lifting L = lift_nonhomogeneous(r->prob, u, f);
     std::copy(L.corrected_rhs.begin(), L.corrected_rhs.end(), rhs);
@@ -253,7 +254,7 @@ int ref_sinsin_rhs(void* h, std::complex<double>* rhs, std::complex<double>* bou
 }
 
 // manufactured solution by name: the reference's named problems (problems.cpp)
-// or "sinsin" (c2/c4: u = prod sin(pi x_l) e^{-i d pi^2 t}, f = d pi^2 u)
+// or "sinsin" (c2/c4: u = prod sin(pi x_l) e^{-i d pi^2 t}, f = S u = (1+nu) d pi^2 u)
 static ManufacturedSolution solution_by_name(const RefProblem* r, const std::string& name) {
     if (name != "sinsin") return find_problem(name);
     const double pi = 3.14159265358979323846;
@@ -269,7 +270,10 @@ static ManufacturedSolution solution_by_name(const RefProblem* r, const std::str
         return v * std::exp(cplx(0, -(double)x.size() * pi * pi * t));
     };
     auto u = s.u;
-    s.f = [pi, u](double t, std::span<const double> x) { return (double)x.size() * pi * pi * u(t, x); };
+    const double nu = s.nu;
+    s.f = [pi, u, nu](double t, std::span<const double> x) { // S u = i u_t - nu lap u
+        return (1.0 + nu) * (double)x.size() * pi * pi * u(t, x);
+    };
     return s;
 }
 

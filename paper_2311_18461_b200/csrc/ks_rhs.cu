@@ -469,11 +469,24 @@ int ks_quad_create(const ks_setup* s, int device, ks_quad** out) {
                 f[m + 1] = &Gt[m];
                 terms.push_back({{Q.nu * Q.nu, 0.0}, f});
             }
-        for (int l = 0; l < d; ++l) {
-            auto f = wm(&ws);
-            f[l + 1] = &Q.L[l];
-            terms.push_back({{Q.nu, 0.0}, f});
+        // unrestricted coupling -nu [G^T x W^H + G x W] (assemble_system, rs == None branch,
+        // assembly.cpp:226-240); on the Dirichlet space it collapses to nu L x (W + W^H)
+        std::vector<cplx> Wh(Q.Wt.size(), cplx(0, 0));
+        {
+            const int n = Q.full_dims[0], ld = 2 * p + 1;
+            for (int j = 0; j < n; ++j)
+                for (int i = std::max(0, j - p); i <= std::min(n - 1, j + p); ++i)
+                    Wh[(size_t)(p + i - j) + (size_t)j * ld] = std::conj(Q.Wt[(size_t)(p + j - i) + (size_t)i * ld]);
         }
+        for (int l = 0; l < d; ++l) {
+            auto f = wm(&Wh);
+            f[l + 1] = &Gt[l];
+            terms.push_back({{-Q.nu, 0.0}, f});
+            f = wm(&Q.Wt);
+            f[l + 1] = &Q.G[l];
+            terms.push_back({{-Q.nu, 0.0}, f});
+        }
+        (void)ws;
         std::vector<std::vector<const ks_c64*>> fp(terms.size());
         std::vector<std::vector<int>> bw(terms.size());
         std::vector<ks_term> kt(terms.size());

@@ -2,7 +2,8 @@
 callables fn(t, x_1, ..., x_d) for Quadrature (restating the closed forms of
 the reference's problems.cpp and the c2/c4 solution of SURVEY 8(d), G2):
 
-    sinsin             u = prod_l sin(pi x_l) exp(-i d pi^2 t),  f = i u_t - nu lap u = d pi^2 u (nu = 1)
+    sinsin             u = prod_l sin(pi x_l) exp(-i d pi^2 t),  f = i u_t - nu lap u = (1 + nu) d pi^2 u
+                       (4 pi^2 u at d = 2, nu = 1: SURVEY 8(d) c2/c4)
     traveling_wave_2d  u = a exp(-i (|x|^2 + t^2) / w^2), w = 0.2, a = (2 / w^2)^(1/4)  (problems.cpp:95-117)
 """
 import numpy as np
@@ -10,7 +11,7 @@ import numpy as np
 PI = 3.14159265358979323846
 
 
-def sinsin(d):
+def sinsin(d, nu=1.0):
     def u(t, *x):
         v = np.exp(-1j * d * PI * PI * t)
         for xi in x:
@@ -18,7 +19,7 @@ def sinsin(d):
         return v
 
     def f(t, *x):
-        return d * PI * PI * u(t, *x)
+        return (1.0 + nu) * d * PI * PI * u(t, *x)
     return u, f
 
 
