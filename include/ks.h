@@ -315,6 +315,11 @@ int ks_quad_dims(const ks_quad* q, int* nq /* d+1 */, int* chunk, int* full_dims
 /* assemble_rhs(prob, f) (assembly.cpp:390-404): reset, accumulate the moments
  * of f chunk by chunk (f: raw samples on the chunk grid), then combine and
  * restrict to the reduced space */
+/* built-in manufactured solutions ("sinsin": SURVEY 8(d) c2/c4; "traveling_wave_2d":
+ * problems.cpp:95-117) sampled on the device: what 0 = u, 1 = f = S u; grid 0 =
+ * quadrature rows [r0, r1) of the outermost axis, grid 1 = the full Greville grid.
+ * out is a device buffer. */
+int ks_quad_sample_named(ks_quad* q, const char* name, int what, int grid, int r0, int r1, ks_c64* out);
 int ks_quad_rhs_reset(ks_quad* q);
 int ks_quad_rhs_chunk(ks_quad* q, int r0, int r1, const ks_c64* f, int mem);
 int ks_quad_rhs_finish(ks_quad* q, ks_c64* rhs /* reduced */, int mem);

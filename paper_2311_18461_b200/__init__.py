@@ -168,6 +168,7 @@ _SIGS = {
     "ks_quad_destroy": (C.c_int, [_P]),
     "ks_quad_dims": (C.c_int, [_P, _P, C.POINTER(C.c_int), _P]),
     "ks_quad_rhs_reset": (C.c_int, [_P]),
+    "ks_quad_sample_named": (C.c_int, [_P, C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, _P]),
     "ks_quad_rhs_chunk": (C.c_int, [_P, C.c_int, C.c_int, _P, C.c_int]),
     "ks_quad_rhs_finish": (C.c_int, [_P, _P, C.c_int]),
     "ks_quad_lift": (C.c_int, [_P, _P, C.c_int, _P, _P]),
@@ -649,12 +650,26 @@ class Quadrature:
         for r0 in range(0, last, self.chunk):
             yield r0, min(last, r0 + self.chunk)
 
+    def _chunk_buf(self):
+        if getattr(self, "_cbuf", None) is None:
+            n = int(np.prod(self.nq[:self.d])) * self.chunk
+            self._cbuf = DeviceVector(n)
+            self._cbuf2 = DeviceVector(n)
+        return self._cbuf, self._cbuf2
+
     def assemble_rhs(self, f) -> np.ndarray:
+        """f: vectorised callable (host sampling), or the name of a built-in
+        manufactured solution ("sinsin", "traveling_wave_2d": device sampling)."""
         _check(lib().ks_quad_rhs_reset(self._h))
         for r0, r1 in self._chunks():
-            coords = self.nodes[:self.d] + [self.nodes[self.d][r0:r1]]
-            fs = self._sample(f, coords)
-            _check(lib().ks_quad_rhs_chunk(self._h, r0, r1, _ptr(fs), KS_MEM_HOST))
+            if isinstance(f, str):
+                b, _ = self._chunk_buf()
+                _check(lib().ks_quad_sample_named(self._h, f.encode(), 1, 0, r0, r1, b.ptr))
+                _check(lib().ks_quad_rhs_chunk(self._h, r0, r1, b.ptr, KS_MEM_DEVICE))
+            else:
+                coords = self.nodes[:self.d] + [self.nodes[self.d][r0:r1]]
+                fs = self._sample(f, coords)
+                _check(lib().ks_quad_rhs_chunk(self._h, r0, r1, _ptr(fs), KS_MEM_HOST))
         out = np.zeros(self.prob.N_dof, dtype=np.complex128)
         _check(lib().ks_quad_rhs_finish(self._h, _ptr(out), KS_MEM_HOST))
         return out
@@ -662,10 +677,17 @@ class Quadrature:
     def lift(self, g, f):
         """lift_nonhomogeneous: (corrected rhs, boundary coefficients on the full space)."""
         rhs = self.assemble_rhs(f)
-        gs = self._sample(g, self.greville)
         bnd = np.zeros(self.N_full, dtype=np.complex128)
         corr = np.zeros(self.prob.N_dof, dtype=np.complex128)
-        _check(lib().ks_quad_lift(self._h, _ptr(gs), KS_MEM_HOST, _ptr(bnd), _ptr(corr)))
+        if isinstance(g, str):
+            gd = DeviceVector(self.N_full)
+            _check(lib().ks_quad_sample_named(self._h, g.encode(), 0, 1, 0, 0, gd.ptr))
+            bd, cd = DeviceVector(self.N_full), DeviceVector(self.prob.N_dof)
+            _check(lib().ks_quad_lift(self._h, gd.ptr, KS_MEM_DEVICE, bd.ptr, cd.ptr))
+            bnd, corr = bd.to_host(), cd.to_host()
+        else:
+            gs = self._sample(g, self.greville)
+            _check(lib().ks_quad_lift(self._h, _ptr(gs), KS_MEM_HOST, _ptr(bnd), _ptr(corr)))
         return rhs - corr, bnd
 
     def extend(self, reduced, boundary=None) -> np.ndarray:
@@ -682,11 +704,18 @@ class Quadrature:
         _check(lib().ks_quad_error_set(self._h, _ptr(c), KS_MEM_HOST))
         l2 = res = 0.0
         for r0, r1 in self._chunks():
-            coords = self.nodes[:self.d] + [self.nodes[self.d][r0:r1]]
-            us, fs = self._sample(u, coords), self._sample(f, coords)
             a, b = C.c_double(), C.c_double()
-            _check(lib().ks_quad_error_chunk(self._h, r0, r1, _ptr(us), _ptr(fs), KS_MEM_HOST, C.byref(a),
-                                             C.byref(b)))
+            if isinstance(u, str):
+                bu, bf = self._chunk_buf()
+                _check(lib().ks_quad_sample_named(self._h, u.encode(), 0, 0, r0, r1, bu.ptr))
+                _check(lib().ks_quad_sample_named(self._h, u.encode(), 1, 0, r0, r1, bf.ptr))
+                _check(lib().ks_quad_error_chunk(self._h, r0, r1, bu.ptr, bf.ptr, KS_MEM_DEVICE, C.byref(a),
+                                                 C.byref(b)))
+            else:
+                coords = self.nodes[:self.d] + [self.nodes[self.d][r0:r1]]
+                us, fs = self._sample(u, coords), self._sample(f, coords)
+                _check(lib().ks_quad_error_chunk(self._h, r0, r1, _ptr(us), _ptr(fs), KS_MEM_HOST, C.byref(a),
+                                                 C.byref(b)))
             l2 += a.value
             res += b.value
         return float(np.sqrt(l2)), float(np.sqrt(l2 + res))

@@ -40,7 +40,7 @@ struct ks_quad {
     std::vector<int> full, red, nq;
     size_t Nfull = 0, Nred = 0, chunk_max = 0, work = 0;
     struct Axis {
-        DevBuf E[3], off, qb, qe, w, ab, piv;
+        DevBuf E[3], off, qb, qe, w, ab, piv, nodes, grev;
     };
     std::vector<Axis> ax;
     std::vector<std::vector<double>> w_host;
@@ -281,6 +281,44 @@ __global__ void k_wnorm(const double2* __restrict__ a, const double2* __restrict
     if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
 }
 
+// built-in manufactured solutions sampled on a tensor grid (axis 0 = time fastest):
+// 0 "sinsin": u = prod sin(pi x_l) e^{-i d pi^2 t}, f = (1 + nu) d pi^2 u
+// 1 "traveling_wave_2d" (problems.cpp:95-117)
+__global__ void k_sample(int which, int what, size_t n, int ndim, int4 dims, const double* c0, const double* c1,
+                         const double* c2, const double* c3, int r0, double nu, double2* __restrict__ out) {
+    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int dd[4] = {dims.x, dims.y, dims.z, dims.w};
+    const double* cs[4] = {c0, c1, c2, c3};
+    double v[4] = {0, 0, 0, 0};
+    size_t t = i;
+    for (int a = 0; a < ndim; ++a) {
+        const int ia = (int)(t % (size_t)dd[a]);
+        t /= (size_t)dd[a];
+        v[a] = cs[a][(a == ndim - 1 ? r0 : 0) + ia];
+    }
+    const double pi = 3.14159265358979323846;
+    const int d = ndim - 1;
+    double2 u;
+    double2 fac = make_double2(1.0, 0.0);
+    if (which == 0) {
+        double sp = 1.0;
+        for (int l = 1; l <= d; ++l) sp *= sin(pi * v[l]);
+        double sn, cn;
+        sincos(-(double)d * pi * pi * v[0], &sn, &cn);
+        u = make_double2(sp * cn, sp * sn);
+        fac = make_double2((1.0 + nu) * d * pi * pi, 0.0);
+    } else {
+        const double w = 0.2, iw2 = 1.0 / (w * w), a = pow(2.0 / (w * w), 0.25);
+        const double r2 = v[1] * v[1] + v[2] * v[2];
+        double sn, cn;
+        sincos(-(r2 + v[0] * v[0]) * iw2, &sn, &cn);
+        u = make_double2(a * cn, a * sn);
+        fac = make_double2(4.0 * r2 * iw2 * iw2 + 2.0 * v[0] * iw2, 4.0 * iw2);
+    }
+    out[i] = what == 0 ? u : make_double2(u.x * fac.x - u.y * fac.y, u.x * fac.y + u.y * fac.x);
+}
+
 inline unsigned blocks(size_t n) { return (unsigned)((n + 255) / 256); }
 
 size_t prod(const std::vector<int>& v) {
@@ -410,6 +448,10 @@ int ks_quad_create(const ks_setup* s, int device, ks_quad** out) {
         X.w.alloc(A.weights.size() * sizeof(double));
         KS_CUDA(cudaMemcpy(X.w.p, A.weights.data(), A.weights.size() * sizeof(double), cudaMemcpyHostToDevice));
         q->w_host.push_back(A.weights);
+        X.nodes.alloc(A.nodes.size() * sizeof(double));
+        KS_CUDA(cudaMemcpy(X.nodes.p, A.nodes.data(), A.nodes.size() * sizeof(double), cudaMemcpyHostToDevice));
+        X.grev.alloc(A.greville.size() * sizeof(double));
+        KS_CUDA(cudaMemcpy(X.grev.p, A.greville.data(), A.greville.size() * sizeof(double), cudaMemcpyHostToDevice));
         X.ab.alloc(A.colloc_ab.size() * sizeof(double2));
         KS_CUDA(cudaMemcpy(X.ab.p, A.colloc_ab.data(), A.colloc_ab.size() * sizeof(double2), cudaMemcpyHostToDevice));
         X.piv.alloc(A.colloc_piv.size() * sizeof(int));
@@ -522,6 +564,36 @@ int ks_quad_dims(const ks_quad* q, int* nq, int* chunk, int* full_dims) {
         if (full_dims) full_dims[a] = q->full[a];
     }
     if (chunk) *chunk = q->p + 1;
+    API_END
+}
+
+int ks_quad_sample_named(ks_quad* q, const char* name, int what, int grid, int r0, int r1, ks_c64* out) {
+    API_BEGIN
+    KS_REQUIRE(q && name && out, KS_EINVAL, "ks_quad_sample_named: NULL argument");
+    int which = -1;
+    if (std::strcmp(name, "sinsin") == 0) which = 0;
+    if (std::strcmp(name, "traveling_wave_2d") == 0 && q->d == 2) which = 1;
+    KS_REQUIRE(which >= 0, KS_EINVAL, std::string("ks_quad_sample_named: unknown problem ") + name);
+    std::lock_guard<std::mutex> lk(q->mu);
+    ensure_device(q->device);
+    const int D = q->d + 1;
+    std::vector<int> dims;
+    const double* c[4] = {nullptr, nullptr, nullptr, nullptr};
+    if (grid == 0) {
+        KS_REQUIRE(r0 >= 0 && r1 > r0 && r1 <= q->nq[q->d], KS_EINVAL, "ks_quad_sample_named: bad rows");
+        chunk_dims(q, r0, r1, dims);
+        for (int a = 0; a < D; ++a) c[a] = q->ax[a].nodes.as<double>();
+    } else {
+        dims = q->full;
+        r0 = 0;
+        for (int a = 0; a < D; ++a) c[a] = q->ax[a].grev.as<double>();
+    }
+    const size_t n = prod(dims);
+    int4 dm = make_int4(dims[0], D > 1 ? dims[1] : 1, D > 2 ? dims[2] : 1, D > 3 ? dims[3] : 1);
+    k_sample<<<blocks(n), 256, 0, q->stream>>>(which, what, n, D, dm, c[0], c[1], c[2], c[3], r0, q->nu,
+                                                 reinterpret_cast<double2*>(out));
+    check_launch("k_sample");
+    KS_CUDA(cudaStreamSynchronize(q->stream));
     API_END
 }
 

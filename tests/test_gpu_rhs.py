@@ -52,3 +52,17 @@ def test_c2_manufactured_solve_converges(gpu):
         assert s.converged
         errs.append(Q.error_norms(Q.extend(s.x, bnd), u, f)[0])
     assert errs[1] < errs[0] / 4
+
+
+@pytest.mark.parametrize("path", RHS, ids=[os.path.basename(p)[:-4] for p in RHS])
+def test_device_sampled_named_solutions(gpu, path):
+    """Same pipeline with the built-in device samplers (ks_quad_sample_named)."""
+    g = np.load(path)
+    d, p, n_el, name = int(g["d"]), int(g["p"]), int(g["n_el"]), str(g["name"])
+    Q = gpu.Quadrature(gpu.SpaceTimeProblem.uniform(d, p, n_el, n_el))
+    assert rel(Q.assemble_rhs(name), g["rhs_f"]) <= 1e-10
+    rhs, bnd = Q.lift(name, name)
+    assert rel(rhs, g["rhs"]) <= 1e-10 and rel(bnd, g["boundary"]) <= 1e-10
+    l2, en = Q.error_norms(g["full"], name, name)
+    assert abs(l2 - float(g["l2"])) <= 1e-10 * float(g["l2"])
+    assert abs(en - float(g["energy"])) <= 1e-10 * float(g["energy"])
