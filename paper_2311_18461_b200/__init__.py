@@ -691,6 +691,8 @@ class Quadrature:
         return rhs - corr, bnd
 
     def extend(self, reduced, boundary=None) -> np.ndarray:
+        if isinstance(reduced, DeviceVector):
+            reduced = reduced.to_host()
         reduced = _cvec(reduced).ravel()
         out = np.zeros(self.N_full, dtype=np.complex128)
         b = None if boundary is None else _cvec(boundary).ravel()
@@ -700,8 +702,11 @@ class Quadrature:
 
     def error_norms(self, full_coeffs, u, f):
         """(L2 error, sqrt(L2^2 + ||f - S u_h||^2)) as error_norms returns."""
-        c = _cvec(full_coeffs).ravel()
-        _check(lib().ks_quad_error_set(self._h, _ptr(c), KS_MEM_HOST))
+        if isinstance(full_coeffs, DeviceVector):
+            _check(lib().ks_quad_error_set(self._h, full_coeffs.ptr, KS_MEM_DEVICE))
+        else:
+            c = _cvec(full_coeffs).ravel()
+            _check(lib().ks_quad_error_set(self._h, _ptr(c), KS_MEM_HOST))
         l2 = res = 0.0
         for r0, r1 in self._chunks():
             a, b = C.c_double(), C.c_double()
