@@ -321,6 +321,8 @@ int ks_quad_dims(const ks_quad* q, int* nq /* d+1 */, int* chunk, int* full_dims
  * out is a device buffer. */
 int ks_quad_sample_named(ks_quad* q, const char* name, int what, int grid, int r0, int r1, ks_c64* out);
 int ks_quad_rhs_reset(ks_quad* q);
+/* assemble_rhs of a built-in problem's f with every chunk sampled on the device */
+int ks_quad_rhs_named(ks_quad* q, const char* name, ks_c64* rhs, int mem);
 int ks_quad_rhs_chunk(ks_quad* q, int r0, int r1, const ks_c64* f, int mem);
 int ks_quad_rhs_finish(ks_quad* q, ks_c64* rhs /* reduced */, int mem);
 /* lift_nonhomogeneous (assembly.cpp:514-570): g sampled on the full Greville

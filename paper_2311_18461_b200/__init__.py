@@ -168,6 +168,7 @@ _SIGS = {
     "ks_quad_destroy": (C.c_int, [_P]),
     "ks_quad_dims": (C.c_int, [_P, _P, C.POINTER(C.c_int), _P]),
     "ks_quad_rhs_reset": (C.c_int, [_P]),
+    "ks_quad_rhs_named": (C.c_int, [_P, C.c_char_p, _P, C.c_int]),
     "ks_quad_sample_named": (C.c_int, [_P, C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, _P]),
     "ks_quad_rhs_chunk": (C.c_int, [_P, C.c_int, C.c_int, _P, C.c_int]),
     "ks_quad_rhs_finish": (C.c_int, [_P, _P, C.c_int]),
@@ -660,6 +661,10 @@ class Quadrature:
     def assemble_rhs(self, f) -> np.ndarray:
         """f: vectorised callable (host sampling), or the name of a built-in
         manufactured solution ("sinsin", "traveling_wave_2d": device sampling)."""
+        if isinstance(f, str):
+            out = np.zeros(self.prob.N_dof, dtype=np.complex128)
+            _check(lib().ks_quad_rhs_named(self._h, f.encode(), _ptr(out), KS_MEM_HOST))
+            return out
         _check(lib().ks_quad_rhs_reset(self._h))
         for r0, r1 in self._chunks():
             if isinstance(f, str):

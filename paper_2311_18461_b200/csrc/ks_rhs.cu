@@ -399,6 +399,60 @@ using namespace ks;
     }                                                                          \
     return KS_OK;
 
+// moments of one chunk (device samples fd), accumulated into q->mom; no sync
+static void rhs_chunk_dev(ks_quad* q, int r0, int r1, const double2* fd) {
+    std::vector<int> dims;
+    chunk_dims(q, r0, r1, dims);
+    const size_t n = prod(dims);
+    const int D = q->d + 1;
+    int4 dm = make_int4(dims[0], D > 1 ? dims[1] : 1, D > 2 ? dims[2] : 1, D > 3 ? dims[3] : 1);
+    const double* w[4] = {nullptr, nullptr, nullptr, nullptr};
+    for (int a = 0; a < D; ++a) w[a] = q->ax[a].w.as<double>();
+    double2* Fw = q->buf[0].as<double2>();
+    k_weight<<<blocks(n), 256, 0, q->stream>>>(fd, Fw, n, D, dm, w[0], w[1], w[2], w[3], r0);
+    check_launch("k_weight");
+    // order sets: time derivative, then second derivative on each spatial axis
+    for (int st = 0; st <= q->d; ++st) {
+        std::vector<int> cur = dims;
+        const double2* src = Fw;
+        int nb = 1;
+        for (int a = 0; a < q->d; ++a) {
+            const int order = a == 0 ? (st == 0 ? 1 : 0) : (st == a ? 2 : 0);
+            double2* dst = q->buf[nb].as<double2>();
+            mode_T(q, src, dst, cur, a, order, 0, false);
+            src = dst;
+            nb = nb == 1 ? 2 : 1;
+        }
+        const int a = q->d, order = a == 0 ? (st == 0 ? 1 : 0) : (st == a ? 2 : 0);
+        mode_T(q, src, q->mom[st].as<double2>(), cur, a, order, r0, true);
+    }
+}
+
+// built-in problem samples (what 0 = u, 1 = f) on quadrature rows [r0, r1) or the Greville grid; no sync
+static void sample_dev(ks_quad* q, int which, int what, int grid, int r0, int r1, double2* out) {
+    const int D = q->d + 1;
+    std::vector<int> dims;
+    const double* c[4] = {nullptr, nullptr, nullptr, nullptr};
+    if (grid == 0) {
+        chunk_dims(q, r0, r1, dims);
+        for (int a = 0; a < D; ++a) c[a] = q->ax[a].nodes.as<double>();
+    } else {
+        dims = q->full;
+        r0 = 0;
+        for (int a = 0; a < D; ++a) c[a] = q->ax[a].grev.as<double>();
+    }
+    const size_t n = prod(dims);
+    int4 dm = make_int4(dims[0], D > 1 ? dims[1] : 1, D > 2 ? dims[2] : 1, D > 3 ? dims[3] : 1);
+    k_sample<<<blocks(n), 256, 0, q->stream>>>(which, what, n, D, dm, c[0], c[1], c[2], c[3], r0, q->nu, out);
+    check_launch("k_sample");
+}
+
+static int problem_id(const ks_quad* q, const char* name) {
+    if (std::strcmp(name, "sinsin") == 0) return 0;
+    if (std::strcmp(name, "traveling_wave_2d") == 0 && q->d == 2) return 1;
+    return -1;
+}
+
 extern "C" {
 
 int ks_quad_create(const ks_setup* s, int device, ks_quad** out) {
@@ -570,29 +624,12 @@ int ks_quad_dims(const ks_quad* q, int* nq, int* chunk, int* full_dims) {
 int ks_quad_sample_named(ks_quad* q, const char* name, int what, int grid, int r0, int r1, ks_c64* out) {
     API_BEGIN
     KS_REQUIRE(q && name && out, KS_EINVAL, "ks_quad_sample_named: NULL argument");
-    int which = -1;
-    if (std::strcmp(name, "sinsin") == 0) which = 0;
-    if (std::strcmp(name, "traveling_wave_2d") == 0 && q->d == 2) which = 1;
+    const int which = problem_id(q, name);
     KS_REQUIRE(which >= 0, KS_EINVAL, std::string("ks_quad_sample_named: unknown problem ") + name);
+    KS_REQUIRE(grid != 0 || (r0 >= 0 && r1 > r0 && r1 <= q->nq[q->d]), KS_EINVAL, "ks_quad_sample_named: bad rows");
     std::lock_guard<std::mutex> lk(q->mu);
     ensure_device(q->device);
-    const int D = q->d + 1;
-    std::vector<int> dims;
-    const double* c[4] = {nullptr, nullptr, nullptr, nullptr};
-    if (grid == 0) {
-        KS_REQUIRE(r0 >= 0 && r1 > r0 && r1 <= q->nq[q->d], KS_EINVAL, "ks_quad_sample_named: bad rows");
-        chunk_dims(q, r0, r1, dims);
-        for (int a = 0; a < D; ++a) c[a] = q->ax[a].nodes.as<double>();
-    } else {
-        dims = q->full;
-        r0 = 0;
-        for (int a = 0; a < D; ++a) c[a] = q->ax[a].grev.as<double>();
-    }
-    const size_t n = prod(dims);
-    int4 dm = make_int4(dims[0], D > 1 ? dims[1] : 1, D > 2 ? dims[2] : 1, D > 3 ? dims[3] : 1);
-    k_sample<<<blocks(n), 256, 0, q->stream>>>(which, what, n, D, dm, c[0], c[1], c[2], c[3], r0, q->nu,
-                                                 reinterpret_cast<double2*>(out));
-    check_launch("k_sample");
+    sample_dev(q, which, what, grid, r0, r1, reinterpret_cast<double2*>(out));
     KS_CUDA(cudaStreamSynchronize(q->stream));
     API_END
 }
@@ -617,30 +654,36 @@ int ks_quad_rhs_chunk(ks_quad* q, int r0, int r1, const ks_c64* f, int mem) {
     ensure_device(q->device);
     std::vector<int> dims;
     chunk_dims(q, r0, r1, dims);
-    const size_t n = prod(dims);
-    const double2* fd = dev_in(q, f, n, mem, in_stage());
-    const int D = q->d + 1;
-    int4 dm = make_int4(dims[0], D > 1 ? dims[1] : 1, D > 2 ? dims[2] : 1, D > 3 ? dims[3] : 1);
-    const double* w[4] = {nullptr, nullptr, nullptr, nullptr};
-    for (int a = 0; a < D; ++a) w[a] = q->ax[a].w.as<double>();
-    double2* Fw = q->buf[0].as<double2>();
-    k_weight<<<blocks(n), 256, 0, q->stream>>>(fd, Fw, n, D, dm, w[0], w[1], w[2], w[3], r0);
-    check_launch("k_weight");
-    // order sets: time derivative, then second derivative on each spatial axis
-    for (int st = 0; st <= q->d; ++st) {
-        std::vector<int> cur = dims;
-        const double2* src = Fw;
-        int nb = 1;
-        for (int a = 0; a < q->d; ++a) {
-            const int order = a == 0 ? (st == 0 ? 1 : 0) : (st == a ? 2 : 0);
-            double2* dst = q->buf[nb].as<double2>();
-            mode_T(q, src, dst, cur, a, order, 0, false);
-            src = dst;
-            nb = nb == 1 ? 2 : 1;
-        }
-        const int a = q->d, order = a == 0 ? (st == 0 ? 1 : 0) : (st == a ? 2 : 0);
-        mode_T(q, src, q->mom[st].as<double2>(), cur, a, order, r0, true);
+    const double2* fd = dev_in(q, f, prod(dims), mem, in_stage());
+    rhs_chunk_dev(q, r0, r1, fd);
+    KS_CUDA(cudaStreamSynchronize(q->stream));
+    API_END
+}
+
+// assemble_rhs of a built-in problem's f, every chunk sampled and reduced on the device
+int ks_quad_rhs_named(ks_quad* q, const char* name, ks_c64* rhs, int mem) {
+    API_BEGIN
+    KS_REQUIRE(q && name && rhs, KS_EINVAL, "ks_quad_rhs_named: NULL argument");
+    const int which = problem_id(q, name);
+    KS_REQUIRE(which >= 0, KS_EINVAL, std::string("ks_quad_rhs_named: unknown problem ") + name);
+    std::lock_guard<std::mutex> lk(q->mu);
+    ensure_device(q->device);
+    for (int k = 0; k <= q->d; ++k) KS_CUDA(cudaMemsetAsync(q->mom[k].p, 0, q->Nfull * sizeof(double2), q->stream));
+    const int last = q->nq[q->d];
+    for (int r0 = 0; r0 < last; r0 += q->p + 1) {
+        const int r1 = std::min(last, r0 + q->p + 1);
+        sample_dev(q, which, 1, 0, r0, r1, q->buf[3].as<double2>());
+        rhs_chunk_dev(q, r0, r1, q->buf[3].as<double2>());
     }
+    double2* out = mem == KS_MEM_DEVICE ? reinterpret_cast<double2*>(rhs) : q->buf[0].as<double2>();
+    const int D = q->d + 1;
+    k_rhs_combine<<<blocks(q->Nred), 256, 0, q->stream>>>(
+        q->mom[0].as<double2>(), q->d >= 1 ? q->mom[1].as<double2>() : nullptr,
+        q->d >= 2 ? q->mom[2].as<double2>() : nullptr, q->d >= 3 ? q->mom[3].as<double2>() : nullptr, out, q->Nred, D,
+        d4(q->red), d4(q->full), q->trial, q->nu);
+    check_launch("k_rhs_combine");
+    if (mem != KS_MEM_DEVICE)
+        KS_CUDA(cudaMemcpyAsync(rhs, out, q->Nred * sizeof(double2), cudaMemcpyDeviceToHost, q->stream));
     KS_CUDA(cudaStreamSynchronize(q->stream));
     API_END
 }
