@@ -334,6 +334,16 @@ int ref_extend(void* h, const std::complex<double>* reduced, const std::complex<
     return 0;
 }
 
+// infsup_constant (experiments.cpp:185-232): method 0 = Galerkin, 1 = least squares
+double ref_infsup(int method, int p, int n_el, double T, double nu) {
+    try {
+        return infsup_constant(method == 0 ? InfSupMethod::Galerkin : InfSupMethod::LeastSquares, p, n_el, T, nu);
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1.0;
+    }
+}
+
 // RHS of a named manufactured problem (problems.cpp:find_problem) exactly as
 // solve_problem builds it (experiments.cpp:34-42): assemble_rhs if
 // homogeneous, else lift_nonhomogeneous.

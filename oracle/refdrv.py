@@ -60,6 +60,8 @@ def rlib():
         L.ref_assemble_rhs_named.argtypes = [P, C.c_char_p, P]
         L.ref_error_norms_named.restype = I
         L.ref_error_norms_named.argtypes = [P, C.c_char_p, P, C.POINTER(D), C.POINTER(D)]
+        L.ref_infsup.restype = D
+        L.ref_infsup.argtypes = [I, I, I, D, D]
         L.ref_extend.restype = I
         L.ref_extend.argtypes = [P, P, P, P]
         _r = L
@@ -78,6 +80,14 @@ def force_backend(name: str):
 
 def active_backend() -> str:
     return rlib().ref_active_backend().decode()
+
+
+def infsup(method, p, n_el, T=1.0, nu=1.0):
+    """infsup_constant (experiments.cpp:185-232); method "galerkin" | "ls"."""
+    v = rlib().ref_infsup(0 if method == "galerkin" else 1, p, n_el, T, nu)
+    if v < 0:
+        raise RuntimeError(rlib().ref_last_error().decode())
+    return v
 
 
 class RefProblem:

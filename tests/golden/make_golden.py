@@ -108,6 +108,14 @@ def main():
         name = "rhs_d%d_p%d_n%d_%s.npz" % c
         np.savez_compressed(os.path.join(HERE, name), **rhs_case(*c))
         print("wrote", name)
+    # inf-sup constants (experiments.cpp:185-232) on spaces small enough that
+    # 60 Lanczos steps exhaust the Krylov space
+    inf = {"cases": np.array([(p, n) for p in (2, 3) for n in (4, 6)]), "ls": [], "galerkin": []}
+    for p, n in inf["cases"]:
+        inf["ls"].append(refdrv.infsup("ls", int(p), int(n)))
+        inf["galerkin"].append(refdrv.infsup("galerkin", int(p), int(n)))
+    np.savez_compressed(os.path.join(HERE, "infsup.npz"), **inf)
+    print("wrote infsup.npz")
     for c in FC_CASES:
         name = "case_fc_d%d_p%d_n%d_t%d.npz" % c
         np.savez_compressed(os.path.join(HERE, name), **case(*c, trial=1))
