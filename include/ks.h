@@ -88,7 +88,12 @@ int ks_fd_create(int d, const int* dims, double nu, int p_t,
                  int device, ks_fd** out);
 /* z = P^-1 r. Replaces FDPreconditioner::apply(const cplx* r, cplx* z) const
  * (fdsolver.hpp:61 -> FastDiagSolver::solve, fdsolver.cpp:53-63). r and z may
- * alias. stream is a cudaStream_t (NULL = the handle's own stream). */
+ * alias. stream is a cudaStream_t (NULL = the handle's own stream, blocking).
+ * KS_MEM_HOST with a non-NULL stream is asynchronous: the H2D copy, the apply
+ * and the D2H copy are queued on the handle's copy/compute streams (two
+ * staging buffers, so consecutive applies overlap their transfers) and z is
+ * valid once `stream` is synchronised; r and z must stay untouched (and should
+ * be pinned) until then. */
 int ks_fd_apply(ks_fd* fd, const ks_c64* r, ks_c64* z, int mem, void* stream);
 /* Same as apply but with the adjoint block solves (FastDiagSolver::solve_adjoint,
  * fdsolver.cpp:65-75, eigensolve.cpp:148-170). */
@@ -190,6 +195,10 @@ int ks_memcpy(void* dst, const void* src, size_t bytes, int kind);
 int ks_host_alloc(void** ptr, size_t bytes); /* pinned host memory */
 int ks_host_free(void* ptr);
 int ks_synchronize(void);
+/* streams for asynchronous applies (cudaStream_t behind a void*) */
+int ks_stream_create(void** stream);
+int ks_stream_destroy(void* stream);
+int ks_stream_synchronize(void* stream);
 /* Overwrite `bytes` of a device scratch buffer (L2 flush between timed runs). */
 int ks_flush_l2(size_t bytes);
 /* Time `iters` back-to-back launches of the FD apply / Kron apply on device

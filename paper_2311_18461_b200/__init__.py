@@ -117,6 +117,9 @@ _SIGS = {
     "ks_host_alloc": (C.c_int, [C.POINTER(_P), C.c_size_t]),
     "ks_host_free": (C.c_int, [_P]),
     "ks_synchronize": (C.c_int, []),
+    "ks_stream_create": (C.c_int, [C.POINTER(_P)]),
+    "ks_stream_destroy": (C.c_int, [_P]),
+    "ks_stream_synchronize": (C.c_int, [_P]),
     "ks_flush_l2": (C.c_int, [C.c_size_t]),
     "ks_fd_time": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.POINTER(C.c_double),
                              C.POINTER(C.c_double)]),
@@ -338,6 +341,27 @@ class SpaceTimeProblem:
 # ---------------------------------------------------------------------------
 # FD preconditioner
 # ---------------------------------------------------------------------------
+class Stream:
+    """A CUDA stream for asynchronous applies (host-pointer applies on a stream
+    are pipelined; results are valid after synchronize())."""
+
+    def __init__(self):
+        h = C.c_void_p()
+        _check(lib().ks_stream_create(C.byref(h)))
+        self.handle = h
+
+    def synchronize(self):
+        _check(lib().ks_stream_synchronize(self.handle))
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib().ks_stream_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
 class FDPreconditioner:
     """Fast-diagonalisation preconditioner (fdsolver.hpp:56-74) on the GPU.
 
@@ -412,7 +436,8 @@ class FDPreconditioner:
         if r.size != self.vec_size():
             raise InvalidArgument("FastDiagSolver: vector length mismatch")
         out = np.empty_like(r) if z is None else z
-        _check(lib().ks_fd_apply(self._h, _ptr(r), _ptr(out), KS_MEM_HOST, None))
+        st = stream.handle if isinstance(stream, Stream) else stream
+        _check(lib().ks_fd_apply(self._h, _ptr(r), _ptr(out), KS_MEM_HOST, st))
         return out
 
     def apply_adjoint(self, r):

@@ -82,8 +82,22 @@ struct ks_fd {
     FdBlocks blocks;
     DevBuf s0, s1, io;
     cudaStream_t stream = nullptr;
+    // asynchronous host-pointer applies (caller stream given): H2D, compute and
+    // D2H on three streams, two staging buffers, so consecutive applies overlap
+    // their copies in both directions with each other and with the compute
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    DevBuf pio[2];
+    cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+    int slot = 0;
     std::mutex mu;
     ~ks_fd() {
+        for (int k = 0; k < 2; ++k) {
+            if (ev_in[k]) cudaEventDestroy(ev_in[k]);
+            if (ev_comp[k]) cudaEventDestroy(ev_comp[k]);
+            if (ev_out[k]) cudaEventDestroy(ev_out[k]);
+        }
+        if (h2d) cudaStreamDestroy(h2d);
+        if (d2h) cudaStreamDestroy(d2h);
         if (stream) cudaStreamDestroy(stream);
     }
 };
@@ -216,6 +230,35 @@ void fd_apply_any(ks_fd* f, const ks_c64* r, ks_c64* z, int mem, void* stream, b
                      st, nullptr);
         // no caller stream: behave like the reference's blocking call
         if (!stream) KS_CUDA(cudaStreamSynchronize(st));
+    } else if (stream) {
+        // pipelined: slot k's H2D waits until slot k's previous D2H has drained
+        // its staging buffer; the compute stream orders the applies (shared
+        // scratch); the caller's stream waits for this apply's D2H
+        if (!f->h2d) {
+            KS_CUDA(cudaStreamCreateWithFlags(&f->h2d, cudaStreamNonBlocking));
+            KS_CUDA(cudaStreamCreateWithFlags(&f->d2h, cudaStreamNonBlocking));
+            for (int k = 0; k < 2; ++k) {
+                KS_CUDA(cudaEventCreateWithFlags(&f->ev_in[k], cudaEventDisableTiming));
+                KS_CUDA(cudaEventCreateWithFlags(&f->ev_comp[k], cudaEventDisableTiming));
+                KS_CUDA(cudaEventCreateWithFlags(&f->ev_out[k], cudaEventDisableTiming));
+                KS_CUDA(cudaEventRecord(f->ev_out[k], f->d2h));
+                f->pio[k].alloc(bytes);
+            }
+        }
+        const int k = f->slot;
+        f->slot ^= 1;
+        cudaStream_t us = static_cast<cudaStream_t>(stream);
+        double2* buf = f->pio[k].as<double2>();
+        KS_CUDA(cudaStreamWaitEvent(f->h2d, f->ev_out[k], 0));
+        KS_CUDA(cudaMemcpyAsync(buf, r, bytes, cudaMemcpyHostToDevice, f->h2d));
+        KS_CUDA(cudaEventRecord(f->ev_in[k], f->h2d));
+        KS_CUDA(cudaStreamWaitEvent(f->stream, f->ev_in[k], 0));
+        fd_apply_dev(f, buf, buf, adjoint, f->stream, nullptr);
+        KS_CUDA(cudaEventRecord(f->ev_comp[k], f->stream));
+        KS_CUDA(cudaStreamWaitEvent(f->d2h, f->ev_comp[k], 0));
+        KS_CUDA(cudaMemcpyAsync(z, buf, bytes, cudaMemcpyDeviceToHost, f->d2h));
+        KS_CUDA(cudaEventRecord(f->ev_out[k], f->d2h));
+        KS_CUDA(cudaStreamWaitEvent(us, f->ev_out[k], 0));
     } else {
         if (!f->io.p) f->io.alloc(bytes);
         KS_CUDA(cudaMemcpyAsync(f->io.p, r, bytes, cudaMemcpyHostToDevice, st));
@@ -933,6 +976,24 @@ int ks_host_alloc(void** ptr, size_t bytes) {
 int ks_host_free(void* ptr) {
     API_BEGIN
     KS_CUDA(cudaFreeHost(ptr));
+    API_END
+}
+int ks_stream_create(void** stream) {
+    API_BEGIN
+    KS_REQUIRE(stream, KS_EINVAL, "ks_stream_create: NULL argument");
+    cudaStream_t st;
+    KS_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    *stream = st;
+    API_END
+}
+int ks_stream_destroy(void* stream) {
+    API_BEGIN
+    if (stream) KS_CUDA(cudaStreamDestroy(static_cast<cudaStream_t>(stream)));
+    API_END
+}
+int ks_stream_synchronize(void* stream) {
+    API_BEGIN
+    KS_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
     API_END
 }
 int ks_synchronize(void) {
