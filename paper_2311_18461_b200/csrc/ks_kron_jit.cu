@@ -427,7 +427,7 @@ bool kron_jit_launch(const KronJitPair& J, const double2* const* ip, double2* co
     }
     // each CTA sweeps the whole axis b serially: too few CTAs leave the GPU idle
     // (c2: 22 CTAs, 0.23 ms vs 0.064 ms for the per-pass kernels)
-    if (J.grid < (unsigned)(2 * sms)) return false;
+    if (J.grid < (unsigned)sms) return false;
     // by-value coefficient table (constant bank)
     // by-value parameter: coefficients, then the input and output tensor pointers
     const size_t nc = (size_t)std::max(1, J.ncoef);
