@@ -205,8 +205,11 @@ def run_reference_arm(args, rank, ws, dist):
 
 
 def run_sharded(args, rank, ws, local, dist):
-    """N > 1: the c3 problem slab-sharded over N GPUs (strong scaling), FD apply
-    through ShardedFDPreconditioner (two NCCL all-to-alls per apply)."""
+    """N > 1: the c3 problem slab-sharded over N GPUs (strong scaling). FD apply
+    with the peer-memory transport (PeerShardedFDPreconditioner: the axis-d
+    transform gathers / scatters its rows from / to the other GPUs' slabs over
+    NVLink) when it reproduces the NCCL all-to-all version on this box, which is
+    timed alongside (ShardedFDPreconditioner)."""
     import torch
     import paper_2311_18461_b200 as ks
     from paper_2311_18461_b200.dist import ShardedFDPreconditioner
@@ -218,29 +221,57 @@ def run_sharded(args, rank, ws, local, dist):
     n = prob.N_dof
     Lt, Mt, Wt = prob.time_bands()
     U, lam = zip(*[prob.eig(l) for l in range(d)])
-    S = ShardedFDPreconditioner(dims, 1.0, p, U, lam, Lt, Mt, Wt, device=local)
-    lo, hi = S.plan["slab"]
+    S_nccl = ShardedFDPreconditioner(dims, 1.0, p, U, lam, Lt, Mt, Wt, device=local)
+    lo, hi = S_nccl.plan["slab"]
     per = dims[0] * int(np.prod(dims[1:d]))
     r_host = rhs(n)[lo * per: hi * per]
     r = torch.from_numpy(r_host).to(f"cuda:{local}")
     z = torch.empty_like(r)
-    for _ in range(W):
-        S.apply(r, z)
-    torch.cuda.synchronize()
-    dist.barrier()
+
+    def time_fd(S):
+        for _ in range(W):
+            S.apply(r, z)
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0.record()
+        for _ in range(K):
+            S.apply(r, z)
+        e1.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+        return max_over_ranks(dist, e0.elapsed_time(e1) / K)
+
+    # transport: peer memory (the axis-d transform reads / writes the other GPUs'
+    # slabs over NVLink, no all-to-all) when it reproduces the NCCL result on
+    # this box, else the NCCL all-to-all version
+    transport, transport_note = args.transport, None
+    z_ref = S_nccl.apply(r).clone()
+    S = S_nccl
+    if transport in ("auto", "peer"):
+        S_peer, failed = None, 0.0
+        try:
+            from paper_2311_18461_b200.dist import PeerShardedFDPreconditioner
+            S_peer = PeerShardedFDPreconditioner(dims, 1.0, p, U, lam, Lt, Mt, Wt, device=local)
+        except Exception as e:  # no P2P / IPC on this box
+            failed, transport_note = 1.0, f"peer transport unavailable: {e}"
+        if max_over_ranks(dist, failed) > 0:  # every rank agrees before any peer phase runs
+            transport = "nccl"
+            transport_note = transport_note or "peer transport unavailable on another rank"
+        else:
+            zq = S_peer.apply(r)
+            err = max_over_ranks(dist, float(torch.linalg.norm(zq - z_ref) / torch.linalg.norm(z_ref)))
+            if err <= 1e-12:
+                S, transport = S_peer, "peer"
+            else:
+                transport, transport_note = "nccl", f"peer transport mismatch {err:.2e}"
+    ms_nccl = time_fd(S_nccl) if S is not S_nccl else None
     ks.reset_launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clk = ClockSampler(local).__enter__()
-    torch.cuda.synchronize()
-    dist.barrier()
-    e0.record()
-    for _ in range(K):
-        S.apply(r, z)
-    e1.record()
-    torch.cuda.synchronize()
-    dist.barrier()
-    ms = e0.elapsed_time(e1) / K
-    launches = ks.launch_count()
+    ms = time_fd(S)
+    launches = ks.launch_count() // max(1, K + W)  # per apply (time_fd runs W + K)
     # e2e: host slab in (pinned), apply, host slab out, every step
     rp = torch.from_numpy(r_host).pin_memory()
     zp = torch.empty_like(rp).pin_memory()
@@ -253,7 +284,6 @@ def run_sharded(args, rank, ws, local, dist):
         torch.cuda.synchronize()
     e2e = (time.perf_counter() - t0) / K
     clk.__exit__(None, None, None)
-    ms = max_over_ranks(dist, ms)
     e2e = max_over_ranks(dist, e2e)
     # full sharded solve to 1e-8 (sharded matvec with halo exchange + sharded FD + all-reduce dots)
     solves = {}
@@ -276,10 +306,15 @@ def run_sharded(args, rank, ws, local, dist):
             "scaling": "strong", "vs_baseline": None, "dtype": "c128 (complex FP64)",
             "data": "synthetic (seeded U[-1,1] RHS, SURVEY 8(d))",
             "config": {"workload": f"{args.config}: d={d} p={p} n_el={n_el}, one sharded FD application per step",
-                       "dims": dims, "dofs": n, "parallelism": f"slab{ws} (axis {d}) + 2x NCCL all-to-all"},
+                       "dims": dims, "dofs": n,
+                       "parallelism": f"slab{ws} (axis {d}), transport {transport}" +
+                                      (" (axis-d transform reads/writes peer slabs over NVLink)" if transport == "peer"
+                                       else " (2x NCCL all-to-all)"),
+                       "transport_note": transport_note,
+                       "nccl_all_to_all_ms_per_step": ms_nccl},
             "e2e": {"value": n / e2e, "unit": "DOF/s", "h2d_bytes_per_step": int(r_host.nbytes) * ws,
                     "d2h_bytes_per_step": int(r_host.nbytes) * ws, "ms_per_step": e2e * 1e3},
-            "gpu_launches": launches, "roofline": None, "clocks": clk.summary(), "cpu_baseline": None,
+            "gpu_launches": launches * K, "roofline": None, "clocks": clk.summary(), "cpu_baseline": None,
             "solves": solves}),
             flush=True)
     dist.destroy_process_group()
@@ -294,6 +329,8 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--transport", default="auto", choices=["auto", "peer", "nccl"],
+                    help="sharded FD exchange (N > 1): peer memory or NCCL all-to-all")
     args = ap.parse_args()
     if args.impl == "reference":
         # CPU arm: rank 0 alone runs the reference; other ranks exit without work

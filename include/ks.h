@@ -249,6 +249,22 @@ int ks_fdshard_sizes(const ks_fdshard* h, size_t* slab_n, size_t* work_n);
 int ks_fdshard_forward(ks_fdshard* h, const ks_c64* r_slab, ks_c64* sendbuf, void* stream);
 int ks_fdshard_middle(ks_fdshard* h, ks_c64* work, void* stream);
 int ks_fdshard_backward(ks_fdshard* h, const ks_c64* recvbuf, ks_c64* z_slab, void* stream);
+/* Peer-memory transport (no all-to-all): phase 1 writes the slab (n_t, N', m)
+ * after the axis 1..d-1 transforms into an exported buffer; set_peers gives
+ * every rank's exported phase-1 slab and output slab (device pointers valid in
+ * this process: own, peer-enabled or CUDA-IPC-opened); the middle phase's
+ * axis-d transform then reads its rows straight from the owners' slabs and
+ * its inverse writes them straight into the owners' output slabs over
+ * NVLink; phase 3 applies the inverse axis 1..d-1 transforms to the rank's
+ * output slab. The caller puts a barrier across ranks between the phases. */
+int ks_fdshard_forward_slab(ks_fdshard* h, const ks_c64* r_local, ks_c64* slab_out, void* stream);
+int ks_fdshard_set_peers(ks_fdshard* h, const ks_c64* const* peer_in, ks_c64* const* peer_out);
+int ks_fdshard_middle_peer(ks_fdshard* h, void* stream);
+int ks_fdshard_backward_slab(ks_fdshard* h, const ks_c64* slab_in, ks_c64* z_local, void* stream);
+/* CUDA IPC handles (64 bytes) for exporting device buffers to other processes */
+int ks_ipc_get_handle(const void* dptr, void* handle);
+int ks_ipc_open(const void* handle, void** dptr);
+int ks_ipc_close(void* dptr);
 int ks_fdshard_destroy(ks_fdshard* h);
 
 /* Sharded Kronecker operator: same slabs of the outermost axis; the input is

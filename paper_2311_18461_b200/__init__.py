@@ -143,6 +143,13 @@ _SIGS = {
     "ks_fdshard_forward": (C.c_int, [_P, _P, _P, _P]),
     "ks_fdshard_middle": (C.c_int, [_P, _P, _P]),
     "ks_fdshard_backward": (C.c_int, [_P, _P, _P, _P]),
+    "ks_fdshard_forward_slab": (C.c_int, [_P, _P, _P, _P]),
+    "ks_fdshard_set_peers": (C.c_int, [_P, _P, _P]),
+    "ks_fdshard_middle_peer": (C.c_int, [_P, _P]),
+    "ks_fdshard_backward_slab": (C.c_int, [_P, _P, _P, _P]),
+    "ks_ipc_get_handle": (C.c_int, [_P, _P]),
+    "ks_ipc_open": (C.c_int, [_P, C.POINTER(_P)]),
+    "ks_ipc_close": (C.c_int, [_P]),
     "ks_fdshard_destroy": (C.c_int, [_P]),
     "ks_kronshard_create": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.c_int, C.POINTER(ks_term),
                                       C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),

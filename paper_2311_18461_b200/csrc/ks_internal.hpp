@@ -122,8 +122,11 @@ void launch_fill_bytes(void* p, size_t bytes, cudaStream_t s);
 // ---------------------------------------------------------------------------
 // layout: 0 natural in/out; 1 natural in -> time-major out T[t][i];
 //         2 time-major in -> natural out (1/2 need outer == 1; nt = time extent)
+// rows_in / rows_out (optional, device arrays of n pointers): row j of the input
+// / output is at rows_*[j] + column offset (rows on other GPUs, peer memory)
 void launch_mode_gemm(const double* At, int n, const double* X, double* Y,
-                      size_t s_complex, size_t outer, cudaStream_t st, int layout = 0, int nt = 0);
+                      size_t s_complex, size_t outer, cudaStream_t st, int layout = 0, int nt = 0,
+                      const double* const* rows_in = nullptr, double* const* rows_out = nullptr);
 
 // folded (even/odd) transform of one axis whose eigenvectors are all even or
 // odd to relative tolerance tol (centro-symmetric pencils): two half-size
@@ -138,7 +141,8 @@ struct FoldAxis {
 // or KS_FD_FOLD=0
 bool fold_axis_build(const double* U, int n, double tol, FoldAxis& F);
 void launch_mode_gemm_fold(const FoldAxis& F, bool inverse, const double* X, double* Y,
-                           size_t s_complex, size_t outer, cudaStream_t st, int layout = 0, int nt = 0);
+                           size_t s_complex, size_t outer, cudaStream_t st, int layout = 0, int nt = 0,
+                           const double* const* rows_in = nullptr, double* const* rows_out = nullptr);
 
 // ---------------------------------------------------------------------------
 // plan-specialised fused level passes (ks_kron_jit.cu, NVRTC at plan creation)

@@ -127,7 +127,8 @@ KronJitPair* kron_jit_build(int nin, int nmid, int nout, int bw, const std::vect
     // size rounded to whole warps; pick the fullest block of at most 384 threads
     int c_best = 1, T_best = 0;
     double e_best = -1;
-    for (int c = 1; c * n_a <= 384; ++c) {
+    const int tmax = std::getenv("KS_KRON_JIT_MAXT") ? std::atoi(std::getenv("KS_KRON_JIT_MAXT")) : 384;
+    for (int c = 1; c * n_a <= tmax; ++c) {
         if (s_a > 1 && c > s_a) break;
         if (s_a == 1 && c > n_outer) break;
         const int T = (c * n_a + 31) / 32 * 32;

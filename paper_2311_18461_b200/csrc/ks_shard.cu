@@ -93,6 +93,7 @@ struct ks_fdshard {
     ks_fd* local_fd = nullptr;       // transforms on axes 1..d-1 only (dims of the slab)
     std::vector<DevBuf> At_fwd, At_inv; // per axis 1..d
     std::vector<FoldAxis> fold;         // per axis; n == 0: dense transform
+    DevBuf rows_in, rows_out;           // peer transport: axis-d row pointer tables (n_d each)
     FdBlocks blocks;                 // blocks of this rank's fibers
     DevBuf Lt, Mt, Wsym;
     DevBuf s0, s1, work2;
@@ -103,10 +104,6 @@ struct ks_fdshard {
     }
 };
 
-namespace ks {
-void launch_mode_gemm(const double* At, int n, const double* X, double* Y, size_t s_complex,
-                      size_t outer, cudaStream_t st, int layout, int nt);
-}
 
 #define API_BEGIN try {
 #define API_END                                                                \
@@ -143,11 +140,12 @@ int ks_shard_plan(int d, const int* dims, int nranks, int rank, long long* slab_
 namespace {
 // transform of axis l (1-based): folded when the axis' eigenvectors are even/odd
 void shard_gemm(const ks_fdshard* h, int l, bool inv, const double* X, double* Y, size_t s, size_t outer,
-                cudaStream_t st, int layout, int nt) {
+                cudaStream_t st, int layout, int nt, const double* const* rin = nullptr,
+                double* const* rout = nullptr) {
     const FoldAxis& F = h->fold[l - 1];
-    if (F.n) launch_mode_gemm_fold(F, inv, X, Y, s, outer, st, layout, nt);
+    if (F.n) launch_mode_gemm_fold(F, inv, X, Y, s, outer, st, layout, nt, rin, rout);
     else launch_mode_gemm((inv ? h->At_inv : h->At_fwd)[l - 1].as<double>(), h->plan.dims[l], X, Y, s, outer, st,
-                          layout, nt);
+                          layout, nt, rin, rout);
 }
 } // namespace
 
@@ -348,6 +346,139 @@ int ks_fdshard_backward(ks_fdshard* h, const ks_c64* recvbuf, ks_c64* z_local, v
         nb ^= 1;
     }
     if (!stream) KS_CUDA(cudaStreamSynchronize(st));
+    API_END
+}
+
+// ---------------------------------------------------------------------------
+// Peer-memory transport (no all-to-all): every rank exports its phase-1 slab
+// and its output slab (CUDA IPC or, for virtual ranks, plain pointers); the
+// axis-d transform of the middle phase gathers its K rows straight from the
+// owners' slabs and the inverse transform scatters its rows straight into the
+// owners' output slabs, so the exchange rides on the transform's own tile
+// loads and stores over NVLink, tile by tile. The caller separates the three
+// phases with a barrier across ranks (all slabs written before they are read).
+// ---------------------------------------------------------------------------
+
+// phase 1 (peer): local transforms on axes 1..d-1 into the exported slab (n_t, N', m)
+int ks_fdshard_forward_slab(ks_fdshard* h, const ks_c64* r_local, ks_c64* slab_out, void* stream) {
+    API_BEGIN
+    KS_REQUIRE(h && r_local && slab_out, KS_EINVAL, "ks_fdshard_forward_slab: NULL argument");
+    std::lock_guard<std::mutex> lk(h->mu);
+    ensure_device(h->device);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : h->stream;
+    const Plan& P = h->plan;
+    const int d = P.d;
+    const long long m = P.slab[P.rank].n();
+    const double* cur = reinterpret_cast<const double*>(r_local);
+    double* bufs[2] = {h->s0.as<double>(), h->s1.as<double>()};
+    int nb = 0;
+    const size_t N = (size_t)P.nt * P.Np * m;
+    for (int l = 1; l < d; ++l) {
+        size_t stride = 1;
+        for (int k = 0; k < l; ++k) stride *= (size_t)P.dims[k];
+        const size_t outer = N / (stride * (size_t)P.dims[l]);
+        double* out = l == d - 1 ? reinterpret_cast<double*>(slab_out) : bufs[nb];
+        shard_gemm(h, l, false, cur, out, stride, outer, st, 0, 0);
+        cur = out;
+        nb ^= 1;
+    }
+    if (!stream) KS_CUDA(cudaStreamSynchronize(st));
+    API_END
+}
+
+// peers: phase-1 slabs (in) and output slabs (out) of every rank, device
+// pointers valid in this process; builds the axis-d row tables of this rank
+int ks_fdshard_set_peers(ks_fdshard* h, const ks_c64* const* peer_in, ks_c64* const* peer_out) {
+    API_BEGIN
+    KS_REQUIRE(h && peer_in && peer_out, KS_EINVAL, "ks_fdshard_set_peers: NULL argument");
+    std::lock_guard<std::mutex> lk(h->mu);
+    ensure_device(h->device);
+    const Plan& P = h->plan;
+    const Range R = P.rest[P.rank];
+    std::vector<const double*> rin(P.nd);
+    std::vector<double*> rout(P.nd);
+    for (int q = 0; q < P.nranks; ++q)
+        for (long long j = P.slab[q].lo; j < P.slab[q].hi; ++j) {
+            // row j of axis d, columns (t, rest in R): slab_q + ((j - lo_q) N' + R.lo) n_t complex
+            const size_t off = 2 * ((size_t)(j - P.slab[q].lo) * P.nt * P.Np + (size_t)P.nt * R.lo);
+            rin[j] = reinterpret_cast<const double*>(peer_in[q]) + off;
+            rout[j] = reinterpret_cast<double*>(peer_out[q]) + off;
+        }
+    h->rows_in.alloc(P.nd * sizeof(double*));
+    h->rows_out.alloc(P.nd * sizeof(double*));
+    KS_CUDA(cudaMemcpy(h->rows_in.p, rin.data(), P.nd * sizeof(double*), cudaMemcpyHostToDevice));
+    KS_CUDA(cudaMemcpy(h->rows_out.p, rout.data(), P.nd * sizeof(double*), cudaMemcpyHostToDevice));
+    API_END
+}
+
+// phase 2 (peer): axis-d transform gathering rows from the peers' slabs ->
+// block solves -> inverse transform scattering rows into the peers' output slabs
+int ks_fdshard_middle_peer(ks_fdshard* h, void* stream) {
+    API_BEGIN
+    KS_REQUIRE(h && h->rows_in.p, KS_EINVAL, "ks_fdshard_middle_peer: call ks_fdshard_set_peers first");
+    std::lock_guard<std::mutex> lk(h->mu);
+    ensure_device(h->device);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : h->stream;
+    const Plan& P = h->plan;
+    const size_t s = (size_t)P.nt * P.rest[P.rank].n();
+    double* tmp = h->s0.as<double>();
+    auto rin = static_cast<const double* const*>(h->rows_in.p);
+    auto rout = static_cast<double* const*>(h->rows_out.p);
+    shard_gemm(h, P.d, false, h->s1.as<double>() /* dummy, rows come from rin */, tmp, s, 1, st, 1, P.nt, rin, nullptr);
+    launch_fd_solve(h->blocks, reinterpret_cast<double2*>(tmp), false, st, true);
+    shard_gemm(h, P.d, true, tmp, nullptr, s, 1, st, 2, P.nt, nullptr, rout);
+    if (!stream) KS_CUDA(cudaStreamSynchronize(st));
+    API_END
+}
+
+// phase 3 (peer): inverse transforms on axes 1..d-1 of this rank's output slab
+int ks_fdshard_backward_slab(ks_fdshard* h, const ks_c64* slab_in, ks_c64* z_local, void* stream) {
+    API_BEGIN
+    KS_REQUIRE(h && slab_in && z_local, KS_EINVAL, "ks_fdshard_backward_slab: NULL argument");
+    std::lock_guard<std::mutex> lk(h->mu);
+    ensure_device(h->device);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : h->stream;
+    const Plan& P = h->plan;
+    const int d = P.d;
+    const long long m = P.slab[P.rank].n();
+    const size_t N = (size_t)P.nt * P.Np * m;
+    const double* cur = reinterpret_cast<const double*>(slab_in);
+    double* bufs[2] = {h->s0.as<double>(), h->s1.as<double>()};
+    int nb = 0;
+    for (int l = 1; l < d; ++l) {
+        size_t stride = 1;
+        for (int k = 0; k < l; ++k) stride *= (size_t)P.dims[k];
+        const size_t outer = N / (stride * (size_t)P.dims[l]);
+        double* out = (l == d - 1) ? reinterpret_cast<double*>(z_local) : bufs[nb];
+        shard_gemm(h, l, true, cur, out, stride, outer, st, 0, 0);
+        cur = out;
+        nb ^= 1;
+    }
+    if (!stream) KS_CUDA(cudaStreamSynchronize(st));
+    API_END
+}
+
+// CUDA IPC plumbing for the peer transport across processes
+int ks_ipc_get_handle(const void* dptr, void* handle /* 64 bytes */) {
+    API_BEGIN
+    KS_REQUIRE(dptr && handle, KS_EINVAL, "ks_ipc_get_handle: NULL argument");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    cudaIpcMemHandle_t hd;
+    KS_CUDA(cudaIpcGetMemHandle(&hd, const_cast<void*>(dptr)));
+    std::memcpy(handle, &hd, sizeof(hd));
+    API_END
+}
+int ks_ipc_open(const void* handle, void** dptr) {
+    API_BEGIN
+    KS_REQUIRE(handle && dptr, KS_EINVAL, "ks_ipc_open: NULL argument");
+    cudaIpcMemHandle_t hd;
+    std::memcpy(&hd, handle, sizeof(hd));
+    KS_CUDA(cudaIpcOpenMemHandle(dptr, hd, cudaIpcMemLazyEnablePeerAccess));
+    API_END
+}
+int ks_ipc_close(void* dptr) {
+    API_BEGIN
+    KS_CUDA(cudaIpcCloseMemHandle(dptr));
     API_END
 }
 

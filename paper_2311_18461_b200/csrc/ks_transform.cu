@@ -332,7 +332,19 @@ struct ColMap {
     long long ntb;     // number of time blocks (T modes)
     long long ntiles;
     int tw = 64;       // complex columns per tile
+    // optional row-pointer tables (device arrays of n pointers): row j of the
+    // input / output lives at rin[j] + column offset instead of X + j*row stride
+    // (the peer-memory sharded FD: rows of axis d on other GPUs)
+    const double* const* rin = nullptr;
+    double* const* rout = nullptr;
 };
+__device__ __forceinline__ const double* in_row(const ColMap& M, const double* X, long long col, int j,
+                                               long long rs) {
+    return M.rin ? M.rin[j] + col : X + col + (long long)j * rs;
+}
+__device__ __forceinline__ double* out_row(const ColMap& M, double* Y, long long col, int r, long long rs) {
+    return M.rout ? M.rout[r] + col : Y + col + (long long)r * rs;
+}
 
 // offsets (doubles) and row strides of complex column j of tile tile
 // per-tile state: one division per tile, none per column
@@ -428,8 +440,8 @@ k_mode_gemm_dmma2(const double* __restrict__ At, int n, const double* __restrict
             for (int k = 0; k < 4; ++k) {
                 const int jj = lrow0 + 4 * k, j = kc * kBK + jj;
                 const bool v = cur_valid && j < n;
-                cp_async16(bs + jj * BNP + 2 * lcp,
-                           v ? (const void*)(X + cur_in + (long long)j * in_rs) : (const void*)X, v);
+                cp_async16(bs + jj * BNP + 2 * lcp, v ? (const void*)in_row(M, X, cur_in, j, in_rs) : (const void*)X,
+                           v);
             }
         }
         cp_async_commit();
@@ -474,12 +486,12 @@ k_mode_gemm_dmma2(const double* __restrict__ At, int n, const double* __restrict
                 const int jcol = (c_warp >> 1) + m * 4 + (lane & 3); // complex column in tile
                 long long io, oo;
                 if (colmap(M, n, tbase, jcol, io, oo)) {
-                    double* yb = Y + oo;
+                    (void)0;
 #pragma unroll
                     for (int i = 0; i < MT; ++i) {
                         const int r = r_warp + i * 8 + cr;
                         if (r < n)
-                            *reinterpret_cast<double2*>(yb + (long long)r * out_rs) =
+                            *reinterpret_cast<double2*>(out_row(M, Y, oo, r, out_rs)) =
                                 make_double2(acc[i][m][0], acc[i][m][1]);
                     }
                 }
@@ -816,8 +828,8 @@ k_mode_gemm_fold(const double* __restrict__ Af, int Kst, const int* __restrict__
                     src = v ? (jj < KC ? rE[q] : rO[q]) : 0;
                 }
                 v = v && cur_valid && dry != 3;
-                cp_async16(bs + jj * BNP + 2 * lcp,
-                           v ? (const void*)(X + cur_in + (long long)src * in_rs) : (const void*)X, v);
+                cp_async16(bs + jj * BNP + 2 * lcp, v ? (const void*)in_row(M, X, cur_in, src, in_rs) : (const void*)X,
+                           v);
             }
         }
         cp_async_commit();
@@ -877,20 +889,19 @@ k_mode_gemm_fold(const double* __restrict__ Af, int Kst, const int* __restrict__
                 const int jcol = (c_warp >> 1) + m * 4 + (lane & 3);
                 long long io, oo;
                 if (colmap(M, n, tbase, jcol, io, oo)) {
-                    double* yb = Y + oo;
 #pragma unroll
                     for (int i = 0; i < MT; ++i) {
                         const int h = r_warp + i * 8 + cr;
                         const double2 e = make_double2(acc[0][i][m][0], acc[0][i][m][1]);
                         const double2 o = make_double2(acc[1][i][m][0], acc[1][i][m][1]);
                         if (!INV) {
-                            if (h < hc) *reinterpret_cast<double2*>(yb + (long long)rE[h] * out_rs) = e;
-                            if (h < no) *reinterpret_cast<double2*>(yb + (long long)rO[h] * out_rs) = o;
+                            if (h < hc) *reinterpret_cast<double2*>(out_row(M, Y, oo, rE[h], out_rs)) = e;
+                            if (h < no) *reinterpret_cast<double2*>(out_row(M, Y, oo, rO[h], out_rs)) = o;
                         } else if (h < hc) {
-                            *reinterpret_cast<double2*>(yb + (long long)h * out_rs) =
+                            *reinterpret_cast<double2*>(out_row(M, Y, oo, h, out_rs)) =
                                 make_double2(e.x + o.x, e.y + o.y);
                             if (n - 1 - h != h)
-                                *reinterpret_cast<double2*>(yb + (long long)(n - 1 - h) * out_rs) =
+                                *reinterpret_cast<double2*>(out_row(M, Y, oo, n - 1 - h, out_rs)) =
                                     make_double2(e.x - o.x, e.y - o.y);
                         }
                     }
@@ -964,7 +975,7 @@ void launch_fold_th(const FoldAxis& F, const double* X, double* Y, const ColMap&
             const char* e = std::getenv("KS_FOLD_TMA");
             return e && std::strcmp(e, "0") != 0;
         }();
-        if (tma && M.mode == MAP_STD && M.s >= 64)
+        if (tma && M.mode == MAP_STD && M.s >= 64 && !M.rin && !M.rout)
             return launch_fold_cfg<TH, INV, 16, 2, 2, 64, true>(F, X, Y, M, st);
         return launch_fold_cfg<TH, INV, 16, 2, 2, 64>(F, X, Y, M, st);
     }
@@ -1056,9 +1067,12 @@ bool fold_axis_build(const double* U, int n, double tol, FoldAxis& F) {
 }
 
 void launch_mode_gemm_fold(const FoldAxis& F, bool inverse, const double* X, double* Y, size_t s_complex,
-                           size_t outer, cudaStream_t st, int layout, int nt) {
+                           size_t outer, cudaStream_t st, int layout, int nt, const double* const* rows_in,
+                           double* const* rows_out) {
     if (s_complex == 0 || outer == 0) return;
-    const ColMap M = make_colmap(F.n, s_complex, outer, layout, nt);
+    ColMap M = make_colmap(F.n, s_complex, outer, layout, nt);
+    M.rin = rows_in;
+    M.rout = rows_out;
 #define KS_FOLD_CASE(T)                                                                            \
     case T:                                                                                        \
         if (inverse) launch_fold_th<T, true>(F, X, Y, M, st);                                      \
@@ -1078,17 +1092,20 @@ void launch_mode_gemm_fold(const FoldAxis& F, bool inverse, const double* X, dou
 int transform_engine() { return engine_choice(); }
 
 void launch_mode_gemm(const double* At, int n, const double* X, double* Y, size_t s_complex,
-                      size_t outer, cudaStream_t st, int layout, int nt) {
+                      size_t outer, cudaStream_t st, int layout, int nt, const double* const* rows_in,
+                      double* const* rows_out) {
     const long long W2 = 2 * (long long)s_complex;
     const long long C = W2 * (long long)outer;
     if (C == 0 || n == 0) return;
     int eng = engine_choice();
-    if (layout != MAP_STD) {
-        KS_REQUIRE(outer == 1 && nt > 0 && s_complex % (size_t)nt == 0, KS_EINVAL,
+    if (layout != MAP_STD || rows_in || rows_out) {
+        KS_REQUIRE(layout == MAP_STD || (outer == 1 && nt > 0 && s_complex % (size_t)nt == 0), KS_EINVAL,
                    "time-major transform needs the outermost axis");
-        eng = 2; // only the v2 engine implements the time-major maps
+        eng = 2; // only the v2 engine implements the time-major maps and row tables
     }
     ColMap M{};
+    M.rin = rows_in;
+    M.rout = rows_out;
     M.mode = layout;
     M.s = (long long)s_complex;
     M.Q = (long long)s_complex * (long long)outer;

@@ -103,6 +103,95 @@ class ShardedFDPreconditioner:
             pass
 
 
+class PeerShardedFDPreconditioner(ShardedFDPreconditioner):
+    """Sharded FD apply without all-to-alls: the middle phase's axis-d transform
+    reads its rows straight from every rank's exported slab and its inverse
+    writes them straight into every rank's output slab (peer memory over
+    NVLink; CUDA IPC handles exchanged once through torch.distributed). Two
+    barriers per apply separate the phases.
+
+    For tests, `peers=(ins, outs)` (lists of tensors, one per rank, all in this
+    process) replaces the IPC exchange and `barrier` the process group barrier."""
+
+    def __init__(self, *args, peers=None, barrier=None, **kw):
+        from . import DeviceVector
+        super().__init__(*args, **kw)
+        self._opened = []
+        if peers is None:
+            import torch.distributed as dist
+            L = lib()
+            # exported buffers from cudaMalloc directly: an IPC handle names the
+            # whole allocation, so the buffers must start at their allocation base
+            self._vin, self._vout = DeviceVector(self.slab_n), DeviceVector(self.slab_n)
+            self.in_ptr, self.out_ptr = self._vin.ptr.value, self._vout.ptr.value
+            hs = []
+            for ptr in (self.in_ptr, self.out_ptr):
+                buf = (C.c_char * 64)()
+                _check(L.ks_ipc_get_handle(C.c_void_p(ptr), buf))
+                hs.append(bytes(buf))
+            allh = [None] * self.nranks
+            dist.all_gather_object(allh, hs)
+            ins, outs = [], []
+            for q, (hi, ho) in enumerate(allh):
+                if q == self.rank:
+                    ins.append(self.in_ptr)
+                    outs.append(self.out_ptr)
+                    continue
+                for hnd, dst in ((hi, ins), (ho, outs)):
+                    ptr = C.c_void_p()
+                    _check(L.ks_ipc_open(C.create_string_buffer(hnd, 64), C.byref(ptr)))
+                    self._opened.append(ptr)
+                    dst.append(ptr.value)
+            self._barrier = barrier or (lambda: dist.barrier())
+        else:
+            ins = [t.data_ptr() for t in peers[0]]
+            outs = [t.data_ptr() for t in peers[1]]
+            self.in_ptr, self.out_ptr = ins[self.rank], outs[self.rank]
+            self._barrier = barrier or (lambda: None)
+        pin = (C.c_void_p * self.nranks)(*ins)
+        pout = (C.c_void_p * self.nranks)(*outs)
+        _check(lib().ks_fdshard_set_peers(self._h, pin, pout))
+
+    def forward_slab(self, r_slab):
+        import torch
+        st = C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+        _check(lib().ks_fdshard_forward_slab(self._h, C.c_void_p(r_slab.data_ptr()),
+                                             C.c_void_p(self.in_ptr), st))
+
+    def middle(self):
+        import torch
+        st = C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+        _check(lib().ks_fdshard_middle_peer(self._h, st))
+
+    def backward_slab(self, z_slab):
+        import torch
+        st = C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+        _check(lib().ks_fdshard_backward_slab(self._h, C.c_void_p(self.out_ptr),
+                                              C.c_void_p(z_slab.data_ptr()), st))
+
+    def apply(self, r_slab, z_slab=None):
+        import torch
+        if z_slab is None:
+            z_slab = torch.empty_like(r_slab)
+        self.forward_slab(r_slab)
+        torch.cuda.current_stream(self.device).synchronize()
+        self._barrier()  # every rank's phase-1 slab is written
+        self.middle()
+        torch.cuda.current_stream(self.device).synchronize()
+        self._barrier()  # every rank's output slab is complete
+        self.backward_slab(z_slab)
+        return z_slab
+
+    def __del__(self):
+        try:
+            for ptr in self._opened:
+                lib().ks_ipc_close(ptr)
+            self._opened = []
+        except Exception:
+            pass
+        super().__del__()
+
+
 # ---------------------------------------------------------------------------
 # sharded Kronecker-sum matvec: halo exchange of bw planes with the neighbours
 # ---------------------------------------------------------------------------

@@ -153,3 +153,110 @@ def test_sharded_pcg_single_rank_nccl(gpu, oracle):
         assert rel(rep["x"].cpu().numpy(), ref.x) < 1e-7
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("P,d,p,n_el,n_el_t", [(2, 2, 3, 10, 9), (3, 3, 2, 8, 8), (4, 3, 4, 6, 5),
+                                               (2, 3, 2, 64, 64)])
+def test_peer_transport_virtual_ranks(gpu, oracle, P, d, p, n_el, n_el_t):
+    """Peer-memory transport (ks_fdshard_*_slab / _middle_peer): P virtual ranks
+    in this process export their slabs as plain device pointers; the middle
+    phase gathers / scatters the axis-d rows straight from / into the other
+    ranks' slabs. Phases run rank by rank (the barrier is the phase order)."""
+    import torch
+    from paper_2311_18461_b200.dist import PeerShardedFDPreconditioner
+    ks = gpu
+    a = setup_arrays(ks, d, p, n_el, n_el_t)
+    dims, nt = a["dims"], a["dims"][0]
+    Np = int(np.prod(dims[1:d]))
+    N = int(np.prod(dims))
+    r = oracle.random_vec(N, 99)
+    z_ref = ks.FDPreconditioner.from_arrays(dims, 1.0, p, a["U"], a["lam"], a["Lt"], a["Mt"], a["Wt"]).apply(r)
+    from paper_2311_18461_b200.dist import shard_plan
+    plans = [shard_plan(d, dims, P, k) for k in range(P)]
+    sizes = [(pl["slab"][1] - pl["slab"][0]) * nt * Np for pl in plans]
+    ins = [torch.empty(n, dtype=torch.complex128, device="cuda") for n in sizes]
+    outs = [torch.empty(n, dtype=torch.complex128, device="cuda") for n in sizes]
+    ranks = []
+    for k in range(P):
+        S = PeerShardedFDPreconditioner(dims, 1.0, p, a["U"], a["lam"], a["Lt"], a["Mt"], a["Wt"],
+                                        nranks=P, rank=k, device=0, peers=(ins, outs))
+        ranks.append(S)
+    rt = torch.from_numpy(r).cuda()
+    for k, S in enumerate(ranks):
+        lo, hi = plans[k]["slab"]
+        S.forward_slab(rt[lo * nt * Np: hi * nt * Np])
+    torch.cuda.synchronize()
+    for S in ranks:
+        S.middle()
+    torch.cuda.synchronize()
+    zs = []
+    for k, S in enumerate(ranks):
+        zk = torch.empty(sizes[k], dtype=torch.complex128, device="cuda")
+        S.backward_slab(zk)
+        zs.append(zk)
+    torch.cuda.synchronize()
+    z = torch.cat(zs).cpu().numpy()
+    assert rel(z, z_ref) < 1e-12
+
+
+def _ipc_worker(rank, ws, port, q):
+    import os
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    sys.path.insert(0, os.path.join(root, "tests"))
+    try:
+        import torch
+        import torch.distributed as dist
+        import paper_2311_18461_b200 as ks
+        from paper_2311_18461_b200.dist import PeerShardedFDPreconditioner, shard_plan
+        from oracle import oracle as O
+        from helpers import setup_arrays
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=ws)
+        d, p = 3, 2
+        a = setup_arrays(ks, d, p, 12, 10)
+        dims, nt = a["dims"], a["dims"][0]
+        Np = int(np.prod(dims[1:d]))
+        r = O.random_vec(int(np.prod(dims)), 5)
+        S = PeerShardedFDPreconditioner(dims, 1.0, p, a["U"], a["lam"], a["Lt"], a["Mt"], a["Wt"],
+                                        nranks=ws, rank=rank, device=0)
+        lo, hi = shard_plan(d, dims, ws, rank)["slab"]
+        zk = S.apply(torch.from_numpy(r[lo * nt * Np: hi * nt * Np].copy()).cuda())
+        torch.cuda.synchronize()
+        parts = [None] * ws
+        dist.all_gather_object(parts, zk.cpu().numpy())
+        if rank == 0:
+            z = np.concatenate(parts)
+            zr = ks.FDPreconditioner.from_arrays(dims, 1.0, p, a["U"], a["lam"], a["Lt"], a["Mt"], a["Wt"]).apply(r)
+            q.put(float(np.linalg.norm(z - zr) / np.linalg.norm(zr)))
+        dist.barrier()
+        del S
+        dist.destroy_process_group()
+    except Exception as e:
+        q.put(repr(e))
+        raise
+
+
+def test_peer_transport_cuda_ipc_two_processes(gpu):
+    """The same peer transport across two processes through CUDA IPC handles
+    (exchanged with all_gather_object; gloo barriers between the phases). Both
+    processes share the one GPU of the test box; no kernel waits on the other
+    process -- the host barriers order the phases."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(k, 2, port, q)) for k in range(2)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(timeout=300)
+    res = q.get(timeout=10)
+    assert not isinstance(res, str), res
+    assert res < 1e-12
