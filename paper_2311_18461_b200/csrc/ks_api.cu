@@ -362,7 +362,7 @@ static void fd_create_impl(int kind, int d, const int* dims, double nu, int p_t,
         // <= 1e-9 of the column max (measured effect on an FD application
         // ~1e-13 relative at c3 sizes)
         f->fold.emplace_back();
-        fold_axis_build(U[l], n, 1e-9, f->fold.back());
+        fold_axis_build(U[l], lambda[l], n, 1e-9, f->fold.back());
         f->lam.emplace_back(n * sizeof(double));
         KS_CUDA(cudaMemcpy(f->lam.back().p, lambda[l], n * sizeof(double), cudaMemcpyHostToDevice));
         f->lam_host.emplace_back(lambda[l], lambda[l] + n);

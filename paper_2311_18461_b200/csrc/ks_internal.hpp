@@ -139,7 +139,8 @@ struct FoldAxis {
 };
 // U column-major (U[j + r*n] = U(j, r)); false (F untouched) if not foldable
 // or KS_FD_FOLD=0
-bool fold_axis_build(const double* U, int n, double tol, FoldAxis& F);
+// lam: the axis eigenvalues (near-degenerate pairs are re-combined into even/odd)
+bool fold_axis_build(const double* U, const double* lam, int n, double tol, FoldAxis& F);
 void launch_mode_gemm_fold(const FoldAxis& F, bool inverse, const double* X, double* Y,
                            size_t s_complex, size_t outer, cudaStream_t st, int layout = 0, int nt = 0,
                            const double* const* rows_in = nullptr, double* const* rows_out = nullptr);

@@ -174,7 +174,7 @@ int ks_fdshard_create(int d, const int* dims, double nu, int p_t, const double* 
         KS_CUDA(cudaMemcpy(h->At_fwd.back().p, af.data(), af.size() * sizeof(double), cudaMemcpyHostToDevice));
         KS_CUDA(cudaMemcpy(h->At_inv.back().p, ai.data(), ai.size() * sizeof(double), cudaMemcpyHostToDevice));
         h->fold.emplace_back();
-        fold_axis_build(U[l], n, 1e-9, h->fold.back());
+        fold_axis_build(U[l], lambda[l], n, 1e-9, h->fold.back());
     }
     // W + W^H and the time bands
     const int nt = dims[0], ld = 2 * p_t + 1;
