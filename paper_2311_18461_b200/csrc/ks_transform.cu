@@ -338,12 +338,16 @@ struct ColMap {
     const double* const* rin = nullptr;
     double* const* rout = nullptr;
 };
+template <bool ROWS>
 __device__ __forceinline__ const double* in_row(const ColMap& M, const double* X, long long col, int j,
                                                long long rs) {
-    return M.rin ? M.rin[j] + col : X + col + (long long)j * rs;
+    if (ROWS && M.rin) return M.rin[j] + col;
+    return X + col + (long long)j * rs;
 }
+template <bool ROWS>
 __device__ __forceinline__ double* out_row(const ColMap& M, double* Y, long long col, int r, long long rs) {
-    return M.rout ? M.rout[r] + col : Y + col + (long long)r * rs;
+    if (ROWS && M.rout) return M.rout[r] + col;
+    return Y + col + (long long)r * rs;
 }
 
 // offsets (doubles) and row strides of complex column j of tile tile
@@ -394,7 +398,7 @@ __device__ __forceinline__ bool colmap(const ColMap& M, int n, const TileBase& B
     return true;
 }
 
-template <int TM, int STG = kStages>
+template <int TM, int STG = kStages, bool ROWS = false>
 __global__ void __launch_bounds__(kThreads, (TM <= 5 ? 2 : 1))
 k_mode_gemm_dmma2(const double* __restrict__ At, int n, const double* __restrict__ X,
                   double* __restrict__ Y, ColMap M) {
@@ -440,7 +444,7 @@ k_mode_gemm_dmma2(const double* __restrict__ At, int n, const double* __restrict
             for (int k = 0; k < 4; ++k) {
                 const int jj = lrow0 + 4 * k, j = kc * kBK + jj;
                 const bool v = cur_valid && j < n;
-                cp_async16(bs + jj * BNP + 2 * lcp, v ? (const void*)in_row(M, X, cur_in, j, in_rs) : (const void*)X,
+                cp_async16(bs + jj * BNP + 2 * lcp, v ? (const void*)in_row<ROWS>(M, X, cur_in, j, in_rs) : (const void*)X,
                            v);
             }
         }
@@ -491,7 +495,7 @@ k_mode_gemm_dmma2(const double* __restrict__ At, int n, const double* __restrict
                     for (int i = 0; i < MT; ++i) {
                         const int r = r_warp + i * 8 + cr;
                         if (r < n)
-                            *reinterpret_cast<double2*>(out_row(M, Y, oo, r, out_rs)) =
+                            *reinterpret_cast<double2*>(out_row<ROWS>(M, Y, oo, r, out_rs)) =
                                 make_double2(acc[i][m][0], acc[i][m][1]);
                     }
                 }
@@ -656,8 +660,22 @@ void launch_tm(int engine, const double* At, int n, const double* X, double* Y, 
         const int per_sm = (TM <= 5 && 2 * sm <= 227 * 1024) ? 2 : 1;
         ColMap M = *map;
         const unsigned g2 = (unsigned)std::min<long long>(M.ntiles, (long long)sms * per_sm);
-        if (two) k_mode_gemm_dmma2<TM, 2><<<g2, kThreads, sm, st>>>(At, n, X, Y, M);
-        else k_mode_gemm_dmma2<TM><<<g2, kThreads, sm, st>>>(At, n, X, Y, M);
+        if (M.rin || M.rout) { // peer-memory rows (sharded middle phase)
+            static bool attr_r = false;
+            if (!attr_r) {
+                KS_CUDA(cudaFuncSetAttribute(k_mode_gemm_dmma2<TM, 2, true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+                KS_CUDA(cudaFuncSetAttribute(k_mode_gemm_dmma2<TM, kStages, true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+                attr_r = true;
+            }
+            if (two) k_mode_gemm_dmma2<TM, 2, true><<<g2, kThreads, sm, st>>>(At, n, X, Y, M);
+            else k_mode_gemm_dmma2<TM, kStages, true><<<g2, kThreads, sm, st>>>(At, n, X, Y, M);
+        } else if (two) {
+            k_mode_gemm_dmma2<TM, 2><<<g2, kThreads, sm, st>>>(At, n, X, Y, M);
+        } else {
+            k_mode_gemm_dmma2<TM><<<g2, kThreads, sm, st>>>(At, n, X, Y, M);
+        }
         check_launch("k_mode_gemm_dmma2");
     } else {
         const size_t sm = (size_t)2 * kBK * (16 * TM + 4 + kBN + 4) * sizeof(double);
@@ -714,7 +732,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 // GEMMs, so the inverse unfold happens in registers.
 // Resident matrices: Af[2][kst][H] (k-major; [0] even, [1] odd, zero padded), staged as nkc*KC rows.
 // ---------------------------------------------------------------------------
-template <int TH, bool INV, int KC, int STG, int MINB, int BNC, bool TMA>
+template <int TH, bool INV, int KC, int STG, int MINB, int BNC, bool TMA, bool ROWS = false>
 __global__ void __launch_bounds__(kThreads, MINB)
 k_mode_gemm_fold(const double* __restrict__ Af, int Kst, const int* __restrict__ rmap, int n, int hc, int nkc,
                  const double* __restrict__ X, double* __restrict__ Y, ColMap M, int dry) {
@@ -828,7 +846,7 @@ k_mode_gemm_fold(const double* __restrict__ Af, int Kst, const int* __restrict__
                     src = v ? (jj < KC ? rE[q] : rO[q]) : 0;
                 }
                 v = v && cur_valid && dry != 3;
-                cp_async16(bs + jj * BNP + 2 * lcp, v ? (const void*)in_row(M, X, cur_in, src, in_rs) : (const void*)X,
+                cp_async16(bs + jj * BNP + 2 * lcp, v ? (const void*)in_row<ROWS>(M, X, cur_in, src, in_rs) : (const void*)X,
                            v);
             }
         }
@@ -895,13 +913,13 @@ k_mode_gemm_fold(const double* __restrict__ Af, int Kst, const int* __restrict__
                         const double2 e = make_double2(acc[0][i][m][0], acc[0][i][m][1]);
                         const double2 o = make_double2(acc[1][i][m][0], acc[1][i][m][1]);
                         if (!INV) {
-                            if (h < hc) *reinterpret_cast<double2*>(out_row(M, Y, oo, rE[h], out_rs)) = e;
-                            if (h < no) *reinterpret_cast<double2*>(out_row(M, Y, oo, rO[h], out_rs)) = o;
+                            if (h < hc) *reinterpret_cast<double2*>(out_row<ROWS>(M, Y, oo, rE[h], out_rs)) = e;
+                            if (h < no) *reinterpret_cast<double2*>(out_row<ROWS>(M, Y, oo, rO[h], out_rs)) = o;
                         } else if (h < hc) {
-                            *reinterpret_cast<double2*>(out_row(M, Y, oo, h, out_rs)) =
+                            *reinterpret_cast<double2*>(out_row<ROWS>(M, Y, oo, h, out_rs)) =
                                 make_double2(e.x + o.x, e.y + o.y);
                             if (n - 1 - h != h)
-                                *reinterpret_cast<double2*>(out_row(M, Y, oo, n - 1 - h, out_rs)) =
+                                *reinterpret_cast<double2*>(out_row<ROWS>(M, Y, oo, n - 1 - h, out_rs)) =
                                     make_double2(e.x - o.x, e.y - o.y);
                         }
                     }
@@ -954,8 +972,19 @@ void launch_fold_cfg(const FoldAxis& F, const double* X, double* Y, ColMap M, cu
     const int per_sm = std::max(1, std::min(MINB, (int)((227 * 1024) / sm)));
     const unsigned g = (unsigned)std::min<long long>(M.ntiles, (long long)sms * per_sm);
     const double* A = (INV ? F.inv : F.fwd).as<double>();
-    k_mode_gemm_fold<TH, INV, KC, STG, MINB, BNC, TMA><<<g, kThreads, sm, st>>>(A, F.kst, F.rmap.as<int>(), F.n,
-                                                                                F.hc, nkc, X, Y, M, dry_run());
+    if (M.rin || M.rout) { // peer-memory rows (sharded middle phase)
+        static bool attr_r = false;
+        if (!attr_r) {
+            KS_CUDA(cudaFuncSetAttribute(k_mode_gemm_fold<TH, INV, KC, STG, MINB, BNC, false, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+            attr_r = true;
+        }
+        k_mode_gemm_fold<TH, INV, KC, STG, MINB, BNC, false, true><<<g, kThreads, sm, st>>>(
+            A, F.kst, F.rmap.as<int>(), F.n, F.hc, nkc, X, Y, M, 0);
+    } else {
+        k_mode_gemm_fold<TH, INV, KC, STG, MINB, BNC, TMA><<<g, kThreads, sm, st>>>(A, F.kst, F.rmap.as<int>(), F.n,
+                                                                                    F.hc, nkc, X, Y, M, dry_run());
+    }
     check_launch("k_mode_gemm_fold");
 }
 
