@@ -112,6 +112,7 @@ struct ks_kron {
     size_t plane = 0;
     std::unique_ptr<KronPlan, KronPlanDeleter> plan;
     DevBuf io_x, io_y;
+    DevBuf pcg[6];                 // ks_pcg work vectors (x, r, z, p, q, scratch), kept across solves
     std::vector<void*> hptrs;
     cudaStream_t stream = nullptr;
     std::mutex mu;
@@ -757,7 +758,12 @@ int ks_pcg(ks_kron* A, ks_fd* P, const ks_c64* b, ks_c64* x, int mem, const ks_p
     const size_t n = A->N, bytes = n * sizeof(double2);
     const auto t_start = std::chrono::steady_clock::now();
 
-    DevBuf bb, xv(bytes), r(bytes), z(bytes), p(bytes), q(bytes), scratch(bytes);
+    // work vectors live in the operator handle: a solve allocates nothing after the first
+    for (auto& w : A->pcg)
+        if (w.bytes < bytes) w.alloc(bytes);
+    DevBuf bb;
+    DevBuf &xv = A->pcg[0], &r = A->pcg[1], &z = A->pcg[2], &p = A->pcg[3], &q = A->pcg[4],
+           &scratch = A->pcg[5];
     const double2* bd;
     if (mem == KS_MEM_DEVICE) {
         bd = reinterpret_cast<const double2*>(b);
