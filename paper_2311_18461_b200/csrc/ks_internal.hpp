@@ -160,6 +160,7 @@ KronJitPair* kron_jit_build(int nin, int nmid, int nout, int bw, const std::vect
 bool kron_jit_launch(const KronJitPair& J, const double2* const* ip, double2* const* op, void* const* hin,
                      void* const* hout, const double2* rb, int nmax, cudaStream_t st);
 void kron_jit_free(KronJitPair* p);
+bool kron_jit_runs(const KronJitPair& J); // the grid fills the GPU (else the passes run separately)
 struct KronJitDeleter {
     void operator()(KronJitPair* p) const { kron_jit_free(p); }
 };

@@ -510,8 +510,8 @@ KronPlan* kron_plan(const std::vector<int>& dims,
                                cudaMemcpyHostToDevice));
         }
     }
-    for (int pl = 0; pl < 2; ++pl)
-        if (P->pool_nodes[pl] > 0) P->pool[pl].alloc((size_t)P->pool_nodes[pl] * P->N * sizeof(double2));
+    // level pools are allocated on first use (kron_apply): with fused pass pairs
+    // the middle levels never exist in HBM (c5: 23 GB not allocated)
     // pointer tables: filled per apply (x / y change); reserve device space
     size_t total = 0;
     for (auto& ps : P->passes) {
@@ -530,19 +530,35 @@ void kron_plan_info(const KronPlan& P, int* npasses, int* nnodes, int* nproducts
 
 void kron_apply(KronPlan& P, const double2* x, double2* y, cudaStream_t st,
                 std::vector<void*>& host_ptrs) {
+    // which passes run fused (same decision as the dispatch below): allocate only
+    // the level pools that some launch reads or writes
+    auto fused_at = [&](size_t k) {
+        return k < P.jit.size() && P.jit[k] && !(P.shard_rows > 0 && k + 2 == P.passes.size()) &&
+               kron_jit_runs(*P.jit[k]);
+    };
+    bool need[2] = {false, false};
+    for (size_t k = 0; k < P.passes.size();) {
+        const bool f = fused_at(k);
+        const KronPass& a = P.passes[k];
+        const KronPass& b = P.passes[f ? k + 1 : k];
+        if (a.in_pool >= 0) need[a.in_pool] = true;
+        if (b.out_pool >= 0) need[b.out_pool] = true;
+        k += f ? 2 : 1;
+    }
+    for (int pl = 0; pl < 2; ++pl)
+        if (need[pl] && P.pool_nodes[pl] > 0 && !P.pool[pl].p)
+            P.pool[pl].alloc((size_t)P.pool_nodes[pl] * P.N * sizeof(double2));
     // pointer table (host-staged, one async copy per apply)
     size_t total = 0;
     for (auto& ps : P.passes) total += ps.n_in + ps.n_out;
     host_ptrs.resize(total);
     size_t w = 0;
+    auto pool_ptr = [&](int pl, int i) -> void* {
+        return P.pool[pl].p ? (void*)(P.pool[pl].as<double2>() + (size_t)i * P.N) : nullptr;
+    };
     for (auto& ps : P.passes) {
-        for (int i = 0; i < ps.n_in; ++i)
-            host_ptrs[w++] = ps.in_pool < 0 ? (void*)x
-                                            : (void*)(P.pool[ps.in_pool].as<double2>() + (size_t)i * P.N);
-        for (int i = 0; i < ps.n_out; ++i)
-            host_ptrs[w++] = ps.out_pool < 0
-                                 ? (void*)y
-                                 : (void*)(P.pool[ps.out_pool].as<double2>() + (size_t)i * P.N);
+        for (int i = 0; i < ps.n_in; ++i) host_ptrs[w++] = ps.in_pool < 0 ? (void*)x : pool_ptr(ps.in_pool, i);
+        for (int i = 0; i < ps.n_out; ++i) host_ptrs[w++] = ps.out_pool < 0 ? (void*)y : pool_ptr(ps.out_pool, i);
     }
     KS_CUDA(cudaMemcpyAsync(P.d_ptrs.p, host_ptrs.data(), total * sizeof(void*),
                             cudaMemcpyHostToDevice, st));
@@ -555,7 +571,7 @@ void kron_apply(KronPlan& P, const double2* x, double2* y, cudaStream_t st,
         const bool shard_last = P.shard_rows > 0 && k + 1 == P.passes.size() &&
                                 ps.axis == (int)P.dims.size() - 1;
         // plan-specialised fused pair (NVRTC): the middle level stays on chip
-        if (k < P.jit.size() && P.jit[k] && !(P.shard_rows > 0 && k + 2 == P.passes.size())) {
+        if (fused_at(k)) {
             const KronPass& nx = P.passes[k + 1];
             auto ip = reinterpret_cast<const double2* const*>(dp + P.ptr_off[k]);
             auto op = reinterpret_cast<double2* const*>(const_cast<void**>(dp + P.ptr_off[k + 1] + nx.n_in));

@@ -416,19 +416,25 @@ ks_pair(const double2* const* __restrict__ ip, double2* const* __restrict__ op, 
     return P.release();
 }
 
-// launch over the plan's tensors (geometry fixed at build); false when the
-// grid is too small to fill the GPU (the caller runs the passes separately)
-bool kron_jit_launch(const KronJitPair& J, const double2* const* ip, double2* const* op, void* const* hin,
-                     void* const* hout, const double2* rb, int nmax, cudaStream_t st) {
+static int sm_count() {
     static int sms = 0;
     if (!sms) {
         int dev = 0;
         KS_CUDA(cudaGetDevice(&dev));
         KS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     }
-    // each CTA sweeps the whole axis b serially: too few CTAs leave the GPU idle
-    // (c2: 22 CTAs, 0.23 ms vs 0.064 ms for the per-pass kernels)
-    if (J.grid < (unsigned)sms) return false;
+    return sms;
+}
+
+// each CTA sweeps the whole axis b serially: too few CTAs leave the GPU idle
+// (c2: 22 CTAs, 0.23 ms vs 0.064 ms for the per-pass kernels)
+bool kron_jit_runs(const KronJitPair& J) { return J.grid >= (unsigned)sm_count(); }
+
+// launch over the plan's tensors (geometry fixed at build); false when the
+// grid is too small to fill the GPU (the caller runs the passes separately)
+bool kron_jit_launch(const KronJitPair& J, const double2* const* ip, double2* const* op, void* const* hin,
+                     void* const* hout, const double2* rb, int nmax, cudaStream_t st) {
+    if (!kron_jit_runs(J)) return false;
     // by-value coefficient table (constant bank)
     // by-value parameter: coefficients, then the input and output tensor pointers
     const size_t nc = (size_t)std::max(1, J.ncoef);
