@@ -116,7 +116,9 @@ int ks_fd_create_galerkin(int d, const int* dims, double nu, int p_t,
 /* Execution plan of a handle (no reference counterpart; diagnostics):
  * folded_axes bit l-1 set = axis l uses the even/odd folded transform
  * (centro-symmetric pencil); blocks = factored time blocks
- * (N_s, or fewer with permutation deduplication). Either pointer may be NULL. */
+ * (N_s, or fewer with permutation deduplication); bit 16 set = axes 1 and 2
+ * run as one fused folded-transform pass (ks_fold12.cu). Either pointer may
+ * be NULL. */
 int ks_fd_info(const ks_fd* fd, int* folded_axes, size_t* blocks);
 int ks_fd_destroy(ks_fd* fd);
 
@@ -143,6 +145,10 @@ int ks_kron_apply(ks_kron* k, const ks_c64* x, ks_c64* y, int mem, void* stream)
 size_t ks_kron_vec_size(const ks_kron* k);
 /* Planner diagnostics: number of fused level passes and intermediate tensors. */
 int ks_kron_plan_info(const ks_kron* k, int* npasses, int* nnodes, int* nproducts);
+/* Which kernels apply runs (diagnostics): 0 = one launch per level pass,
+ * 1 = NVRTC fused pass pairs, 2 = d = 3 two-launch path (axis-3 pass, then
+ * axes t/1/2 fused; ks_kron3.cu). */
+int ks_kron_engine(const ks_kron* k, int* engine);
 int ks_kron_destroy(ks_kron* k);
 
 /* ---------------------------------------------------------------------------

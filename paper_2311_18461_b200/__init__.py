@@ -103,6 +103,7 @@ _SIGS = {
     "ks_kron_vec_size": (C.c_size_t, [_P]),
     "ks_kron_plan_info": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                     C.POINTER(C.c_int)]),
+    "ks_kron_engine": (C.c_int, [_P, C.POINTER(C.c_int)]),
     "ks_kron_destroy": (C.c_int, [_P]),
     "ks_pcg": (C.c_int, [_P, _P, _P, _P, C.c_int, C.POINTER(ks_pcg_opts), _P, C.c_int,
                          C.POINTER(ks_pcg_report)]),
@@ -472,7 +473,8 @@ class FDPreconditioner:
         m, nb = C.c_int(), C.c_size_t()
         _check(lib().ks_fd_info(self._h, C.byref(m), C.byref(nb)))
         d = len(self.dims) - 1
-        return {"folded_axes": [l + 1 for l in range(d) if m.value >> l & 1], "blocks": nb.value}
+        return {"folded_axes": [l + 1 for l in range(d) if m.value >> l & 1], "blocks": nb.value,
+                "fused_axes_12": bool(m.value >> 16 & 1)}
 
     def time(self, r: DeviceVector, z: DeviceVector, iters: int, flush: bool = True):
         ms, mk = C.c_double(), C.c_double()
@@ -600,7 +602,10 @@ class KroneckerOperator:
         self._build()
         a, b, c = C.c_int(), C.c_int(), C.c_int()
         _check(lib().ks_kron_plan_info(self._h, C.byref(a), C.byref(b), C.byref(c)))
-        return {"passes": a.value, "nodes": b.value, "products": c.value}
+        e = C.c_int()
+        _check(lib().ks_kron_engine(self._h, C.byref(e)))
+        return {"passes": a.value, "nodes": b.value, "products": c.value,
+                "engine": {0: "level_passes", 1: "fused_pairs", 2: "axis3_then_fused_t12"}[e.value]}
 
     def time(self, x: DeviceVector, y: DeviceVector, iters: int, flush: bool = True):
         self._build()

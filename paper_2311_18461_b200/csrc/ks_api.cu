@@ -36,6 +36,7 @@ KronPlan* kron_plan(const std::vector<int>& dims,
 void kron_apply(KronPlan& P, const double2* x, double2* y, cudaStream_t st,
                 std::vector<void*>& host_ptrs);
 void kron_plan_info(const KronPlan& P, int* npasses, int* nnodes, int* nproducts);
+int kron_plan_engine(const KronPlan& P); // 0 level passes, 1 fused pass pairs, 2 axis 3 + fused t/1/2
 void kron_plan_free(KronPlan* p);
 void kron_plan_set_shard(KronPlan& P, int rows, int in_off, int band_off);
 struct KronPlanDeleter {
@@ -77,6 +78,7 @@ struct ks_fd {
     std::vector<std::vector<double>> lam_host;
     std::vector<int> fiber_block; // host copy of the block map (empty = identity)
     bool fused = false;           // outermost axis via k_fd_fused
+    bool fuse12 = false;          // axes 1+2 via k_fold12 (KS_FD_FUSE12=1 at creation)
     int kind = 0;                 // 0: least-squares blocks, 1: Galerkin blocks (galerkin_fast_solver)
     DevBuf Lt, Mt, Wsym;          // Wsym: W + W^H (least squares) or W itself (Galerkin)
     FdBlocks blocks;
@@ -200,10 +202,34 @@ void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStre
     // to_eigen: axes 1..d with U_l^T (fdsolver.cpp:7-14). The last one (the
     // outermost axis d) writes the time-major layout T[t][fiber] so that the
     // block solves read and write coalesced.
+    // Axes 1 and 2 go through one fused kernel when both fold and fit a
+    // shared-memory slab (ks_fold12.cu; d >= 3 so that axis d stays separate).
+    const bool f12 = f->fuse12;
+    auto fused12 = [&](bool inv, const double* in, double* out) {
+        const long long outer = (long long)(f->N / ((size_t)f->dims[0] * f->dims[1] * f->dims[2]));
+        auto launch = [&]() { launch_fold12(f->fold[0], f->fold[1], inv, in, out, f->dims[0], outer, st); };
+        if (ev) {
+            cudaEvent_t a, b;
+            KS_CUDA(cudaEventCreate(&a));
+            KS_CUDA(cudaEventCreate(&b));
+            KS_CUDA(cudaEventRecord(a, st));
+            launch();
+            KS_CUDA(cudaEventRecord(b, st));
+            ev->push_back(a);
+            ev->push_back(b);
+        } else {
+            launch();
+        }
+    };
     for (int l = 1; l <= d; ++l) {
         double* out = bufs[nb];
         nb ^= 1;
-        gemm(f->At_fwd[l - 1], l, cur, out, l == d ? 1 : 0);
+        if (f12 && l == 1) {
+            fused12(false, cur, out);
+            ++l;
+        } else {
+            gemm(f->At_fwd[l - 1], l, cur, out, l == d ? 1 : 0);
+        }
         cur = out;
     }
     // N_s block solves (fdsolver.cpp:58-60), time-major
@@ -213,9 +239,16 @@ void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStre
     // commute, so only the rounding order differs.
     for (int k = 0; k < d; ++k) {
         const int l = k == 0 ? d : k;
-        double* out = (k == d - 1) ? reinterpret_cast<double*>(z) : bufs[nb];
-        if (k != d - 1) nb ^= 1;
-        gemm(f->At_inv[l - 1], l, cur, out, k == 0 ? 2 : 0);
+        const bool pair = f12 && k == 1; // axes 1 and 2 in one pass
+        const int klast = pair ? k + 1 : k;
+        double* out = (klast == d - 1) ? reinterpret_cast<double*>(z) : bufs[nb];
+        if (klast != d - 1) nb ^= 1;
+        if (pair) {
+            fused12(true, cur, out);
+            k = klast;
+        } else {
+            gemm(f->At_inv[l - 1], l, cur, out, k == 0 ? 2 : 0);
+        }
         cur = out;
     }
 }
@@ -406,6 +439,7 @@ static void fd_create_impl(int kind, int d, const int* dims, double nu, int p_t,
     if (const char* e = std::getenv("KS_FD_FUSED"))
         fused = std::strcmp(e, "1") == 0 && fd_fused_supported(nt, dims[d], p_t);
     f->fused = fused;
+    f->fuse12 = d >= 3 && fold12_supported(f->fold[0], f->fold[1]);
     if (fused) {
         B.fused_nd = dims[d];
         B.fused_np = Np_all;
@@ -567,6 +601,7 @@ int ks_fd_info(const ks_fd* fd, int* folded_axes, size_t* blocks) {
     int m = 0;
     for (size_t l = 0; l < fd->fold.size(); ++l)
         if (fd->fold[l].n) m |= 1 << l;
+    if (fd->fuse12 && !fd->fused) m |= 1 << 16;
     if (folded_axes) *folded_axes = m;
     if (blocks) *blocks = fd->blocks.nblk;
     API_END
@@ -589,6 +624,10 @@ static void kron_create_impl(int ndim, const int* dims, int nterms, const ks_ter
     KS_REQUIRE(nterms >= 0 && (nterms == 0 || terms), KS_EINVAL, "ks_kron_create: bad term list");
     for (int a = 0; a < ndim; ++a) KS_REQUIRE(dims[a] >= 1, KS_EINVAL, "CoeffTensor: dims must be positive");
     // factor dedup by content (shared prefixes need equal factors to share ids)
+    const bool merge = [] {
+        const char* e = std::getenv("KS_KRON_MERGE");
+        return !(e && std::strcmp(e, "0") == 0);
+    }();
     std::vector<std::vector<double2>> bands;
     std::vector<int> bn, bbw;
     std::vector<double2> coeffs;
@@ -596,6 +635,7 @@ static void kron_create_impl(int ndim, const int* dims, int nterms, const ks_ter
     for (int t = 0; t < nterms; ++t) {
         KS_REQUIRE(terms[t].factors, KS_EINVAL, "KroneckerOperator: wrong factor count");
         std::vector<int> ids(ndim, -1);
+        double sign = 1.0;
         for (int a = 0; a < ndim; ++a) {
             const ks_c64* f = terms[t].factors[a];
             if (!f) continue;
@@ -612,6 +652,29 @@ static void kron_create_impl(int ndim, const int* dims, int nterms, const ks_ter
                     id = (int)e;
                     break;
                 }
+            // Equal up to sign and rounding (max-norm 1e-12 relative): the C^1
+            // Dirichlet spaces have G = -L, so the cross terms' G_l, G_m^T are
+            // one factor with L (test_assembly.cpp:39-48) --
+            // fewer distinct factors, a smaller plan. KS_KRON_MERGE=0 keeps
+            // them apart (exact-content deduplication only).
+            if (id < 0 && merge) {
+                double mx = 0.0;
+                for (const double2& v : b) mx = std::max(mx, std::max(std::fabs(v.x), std::fabs(v.y)));
+                for (size_t e = 0; e < bands.size() && id < 0 && mx > 0.0; ++e) {
+                    if (bn[e] != n || bbw[e] != bw) continue;
+                    for (double sg : {1.0, -1.0}) {
+                        double dev = 0.0;
+                        for (size_t i = 0; i < b.size() && dev <= 1e-12 * mx; ++i)
+                            dev = std::max(dev, std::max(std::fabs(b[i].x - sg * bands[e][i].x),
+                                                         std::fabs(b[i].y - sg * bands[e][i].y)));
+                        if (dev <= 1e-12 * mx) {
+                            id = (int)e;
+                            sign *= sg;
+                            break;
+                        }
+                    }
+                }
+            }
             if (id < 0) {
                 id = (int)bands.size();
                 bands.push_back(std::move(b));
@@ -620,7 +683,7 @@ static void kron_create_impl(int ndim, const int* dims, int nterms, const ks_ter
             }
             ids[a] = id;
         }
-        coeffs.push_back(make_double2(terms[t].coeff.re, terms[t].coeff.im));
+        coeffs.push_back(make_double2(sign * terms[t].coeff.re, sign * terms[t].coeff.im));
         fids.push_back(ids);
     }
     ensure_device(device);
@@ -728,6 +791,13 @@ int ks_kron_plan_info(const ks_kron* k, int* npasses, int* nnodes, int* nproduct
     API_BEGIN
     KS_REQUIRE(k, KS_EINVAL, "NULL handle");
     kron_plan_info(*k->plan, npasses, nnodes, nproducts);
+    API_END
+}
+
+int ks_kron_engine(const ks_kron* k, int* engine) {
+    API_BEGIN
+    KS_REQUIRE(k && engine, KS_EINVAL, "ks_kron_engine: bad arguments");
+    *engine = kron_plan_engine(*k->plan);
     API_END
 }
 

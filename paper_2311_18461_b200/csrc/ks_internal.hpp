@@ -141,6 +141,11 @@ struct FoldAxis {
 // or KS_FD_FOLD=0
 // lam: the axis eigenvalues (near-degenerate pairs are re-combined into even/odd)
 bool fold_axis_build(const double* U, const double* lam, int n, double tol, FoldAxis& F);
+// fused folded transforms on axes 1 and 2 (ks_fold12.cu): one HBM pass for
+// both mode products; natural layout, axis 1 stride n0, outer = prod dims[3..]
+bool fold12_supported(const FoldAxis& F1, const FoldAxis& F2);
+void launch_fold12(const FoldAxis& F1, const FoldAxis& F2, bool inverse, const double* X, double* Y, int n0,
+                   long long outer, cudaStream_t st);
 void launch_mode_gemm_fold(const FoldAxis& F, bool inverse, const double* X, double* Y,
                            size_t s_complex, size_t outer, cudaStream_t st, int layout = 0, int nt = 0,
                            const double* const* rows_in = nullptr, double* const* rows_out = nullptr);
@@ -148,6 +153,17 @@ void launch_mode_gemm_fold(const FoldAxis& F, bool inverse, const double* X, dou
 // ---------------------------------------------------------------------------
 // plan-specialised fused level passes (ks_kron_jit.cu, NVRTC at plan creation)
 // ---------------------------------------------------------------------------
+// NVRTC for sm_100a, cached by source (ks_kron_jit.cu)
+cudaKernel_t nvrtc_kernel(const std::string& src, const char* name, size_t max_smem);
+// d = 3 matvec in two launches: axis 3, then axes t/1/2 fused (ks_kron3.cu)
+struct Kron3;
+Kron3* kron3_build(const std::vector<int>& dims, int bw, int nmax, const std::vector<int>& freal,
+                   const std::vector<double2>& coeffs, const std::vector<std::vector<int>>& fids);
+void kron3_apply(Kron3& K, const double2* x, double2* y, const double2* rb, cudaStream_t st);
+void kron3_free(Kron3* p);
+struct Kron3Deleter {
+    void operator()(Kron3* p) const { kron3_free(p); }
+};
 struct JitContrib {
     int in, out, factor, coeff; // coeff = index into the coefficient table
 };

@@ -90,6 +90,8 @@ struct KronPlan {
     DevBuf d_rowband, d_freal; // v3: rb[f][r][dj] (width 2*bwmax+1), is_real[f]
     // plan-specialised fused pass pairs (k, k+1), indexed by k (null = none)
     std::vector<std::unique_ptr<KronJitPair, KronJitDeleter>> jit;
+    // d = 3: axis 3 then axes t/1/2 fused (ks_kron3.cu); null = level passes
+    std::unique_ptr<Kron3, Kron3Deleter> k3;
 };
 
 namespace {
@@ -478,6 +480,12 @@ KronPlan* kron_plan(const std::vector<int>& dims,
                                            nbb, outer));
         }
     }
+    {
+        std::vector<int> frv(std::max<size_t>(P->factors.size(), 1), 1);
+        for (size_t f = 0; f < P->factors.size(); ++f) frv[f] = P->factors[f].is_real ? 1 : 0;
+        bool all_active = D == 4 && (int)ax.size() == 4;
+        if (all_active) P->k3.reset(kron3_build(dims, P->bwmax, P->nmax, frv, coeffs, fids));
+    }
     for (auto& ps : P->passes) {
         std::vector<int> ib(ps.n_in + 1, 0);
         for (auto& c : ps.contribs) ib[c.in + 1]++;
@@ -522,6 +530,13 @@ KronPlan* kron_plan(const std::vector<int>& dims,
     return P.release();
 }
 
+int kron_plan_engine(const KronPlan& P) {
+    if (P.k3 && P.shard_rows == 0) return 2;
+    for (auto& j : P.jit)
+        if (j && kron_jit_runs(*j)) return 1;
+    return 0;
+}
+
 void kron_plan_info(const KronPlan& P, int* npasses, int* nnodes, int* nproducts) {
     if (npasses) *npasses = (int)P.passes.size();
     if (nnodes) *nnodes = P.nnodes;
@@ -530,6 +545,10 @@ void kron_plan_info(const KronPlan& P, int* npasses, int* nnodes, int* nproducts
 
 void kron_apply(KronPlan& P, const double2* x, double2* y, cudaStream_t st,
                 std::vector<void*>& host_ptrs) {
+    if (P.k3 && P.shard_rows == 0) {
+        kron3_apply(*P.k3, x, y, P.d_rowband.as<double2>(), st);
+        return;
+    }
     // which passes run fused (same decision as the dispatch below): allocate only
     // the level pools that some launch reads or writes
     auto fused_at = [&](size_t k) {

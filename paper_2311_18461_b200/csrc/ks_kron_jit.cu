@@ -41,18 +41,12 @@
 namespace ks {
 
 namespace {
-
-
-struct JitKernel {
-    cudaLibrary_t lib = nullptr;
-    cudaKernel_t fn = nullptr;
-};
-
 std::mutex g_jit_mu;
-std::map<std::string, JitKernel>& jit_cache() {
-    static std::map<std::string, JitKernel> m;
+std::map<std::string, cudaKernel_t>& jit_cache() {
+    static std::map<std::string, cudaKernel_t> m;
     return m;
 }
+} // namespace
 
 #define KS_NVRTC(x)                                                                                \
     do {                                                                                           \
@@ -60,9 +54,12 @@ std::map<std::string, JitKernel>& jit_cache() {
         KS_REQUIRE(r_ == NVRTC_SUCCESS, KS_ECUDA, std::string("nvrtc: ") + nvrtcGetErrorString(r_)); \
     } while (0)
 
-JitKernel jit_compile(const std::string& src) {
+// Compile `src` for sm_100a with NVRTC (cached process-wide by source text) and
+// return kernel `name`, with its dynamic shared memory limit raised to max_smem.
+cudaKernel_t nvrtc_kernel(const std::string& src, const char* name, size_t max_smem) {
     std::lock_guard<std::mutex> lk(g_jit_mu);
-    auto it = jit_cache().find(src);
+    const std::string key = std::string(name) + "\n" + src;
+    auto it = jit_cache().find(key);
     if (it != jit_cache().end()) return it->second;
     nvrtcProgram prog;
     KS_NVRTC(nvrtcCreateProgram(&prog, src.c_str(), "ks_kron_jit.cu", 0, nullptr, nullptr));
@@ -81,13 +78,28 @@ JitKernel jit_compile(const std::string& src) {
     std::vector<char> cubin(cn);
     KS_NVRTC(nvrtcGetCUBIN(prog, cubin.data()));
     nvrtcDestroyProgram(&prog);
-    JitKernel k;
-    KS_CUDA(cudaLibraryLoadData(&k.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
-    KS_CUDA(cudaLibraryGetKernel(&k.fn, k.lib, "ks_pair"));
+    cudaLibrary_t lib = nullptr;
+    cudaKernel_t fn = nullptr;
+    KS_CUDA(cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+    KS_CUDA(cudaLibraryGetKernel(&fn, lib, name));
     int dev = 0;
     KS_CUDA(cudaGetDevice(&dev));
-    KS_CUDA(cudaKernelSetAttributeForDevice(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024, dev));
-    jit_cache()[src] = k;
+    KS_CUDA(cudaKernelSetAttributeForDevice(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_smem, dev));
+    jit_cache()[key] = fn;
+    return fn;
+}
+
+namespace {
+
+
+struct JitKernel {
+    cudaLibrary_t lib = nullptr;
+    cudaKernel_t fn = nullptr;
+};
+
+JitKernel jit_compile(const std::string& src) {
+    JitKernel k;
+    k.fn = nvrtc_kernel(src, "ks_pair", 200 * 1024);
     return k;
 }
 

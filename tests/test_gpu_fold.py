@@ -102,3 +102,17 @@ def test_folded_high_degree(gpu, oracle, d, p, n_el, n_el_t):
     assert rel(z, zo) <= TOL and maxrel(z, zo) <= TOL
     za, zao = g.apply_adjoint(r), o.apply_adjoint(r)
     assert rel(za, zao) <= TOL and maxrel(za, zao) <= TOL
+
+
+# axes 1 and 2 of length 32 / 48 / 64 run through the fused slab kernel
+# (csrc/ks_fold12.cu, opt-in KS_FD_FUSE12=1): one pass for two folded mode products
+@pytest.mark.parametrize("d,p,n_el,n_el_t", [(3, 2, 32, 5), (3, 2, 48, 3), (3, 2, 64, 2)])
+def test_fused_axes12_matches_oracle(gpu, oracle, d, p, n_el, n_el_t, monkeypatch):
+    monkeypatch.setenv("KS_FD_FUSE12", "1")
+    a, g, o = _pair(gpu, oracle, d, p, n_el, n_el_t)
+    assert g.info()["fused_axes_12"]
+    r = oracle.random_vec(o.N, 41)
+    z, zo = g.apply(r), o.apply(r)
+    assert rel(z, zo) <= TOL and maxrel(z, zo) <= TOL
+    za, zao = g.apply_adjoint(r), o.apply_adjoint(r)
+    assert rel(za, zao) <= TOL and maxrel(za, zao) <= TOL

@@ -1,0 +1,9 @@
+#!/bin/bash
+# Validation pass: GPU tests, smoke(), default bench line.
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1
+echo "rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+echo "rc=$?" >> gpurun_out/smoke.log
+timeout 600 python bench.py > gpurun_out/bench.log 2>&1
+echo "rc=$?" >> gpurun_out/bench.log
