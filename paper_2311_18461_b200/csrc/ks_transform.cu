@@ -947,6 +947,9 @@ void set_tile_width(ColMap& M, int tw) {
         M.ntiles = (M.Q + tw - 1) / tw;
     } else {
         M.tbr = M.Np >= 8 ? 8 : (M.Np >= 4 ? 4 : (M.Np >= 2 ? 2 : 1));
+        // experiment hook: spatial block width of a time-major tile (tbt * tbr = tw)
+        static const int tbr_env = std::getenv("KS_FD_TBR") ? std::atoi(std::getenv("KS_FD_TBR")) : 0;
+        if (tbr_env > 0 && tw % tbr_env == 0 && M.Np >= tbr_env) M.tbr = tbr_env;
         M.tbt = tw / M.tbr;
         M.ntb = (M.nt + M.tbt - 1) / M.tbt;
         M.ntiles = M.ntb * ((M.Np + M.tbr - 1) / M.tbr);
