@@ -221,6 +221,18 @@ void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStre
             launch();
         }
     };
+    // Opt-in (KS_FD_NAT=1, pair-mode blocks, forward solve): the solve reads the
+    // natural layout directly (k_fd_solve_nat, chunked through shared memory),
+    // so no transform needs the time-major hand-off. Measured c3: transforms
+    // 0.75 vs 0.85 ms, but the chunked solve takes 0.51 vs 0.37 ms (its
+    // per-chunk staging instructions and 7 warps/SM make it latency bound) --
+    // 1.26 vs 1.21 ms per FD apply, so the time-major path stays the default.
+    static const bool nat_ok = [] {
+        const char* e = std::getenv("KS_FD_NAT");
+        return e && std::strcmp(e, "1") == 0;
+    }();
+    const bool nat = nat_ok && !adjoint && f->blocks.pair_n1 > 0 && f->blocks.rec == 0;
+    const int tout = nat ? 0 : 1, tin = nat ? 0 : 2;
     for (int l = 1; l <= d; ++l) {
         double* out = bufs[nb];
         nb ^= 1;
@@ -228,12 +240,12 @@ void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStre
             fused12(false, cur, out);
             ++l;
         } else {
-            gemm(f->At_fwd[l - 1], l, cur, out, l == d ? 1 : 0);
+            gemm(f->At_fwd[l - 1], l, cur, out, l == d ? tout : 0);
         }
         cur = out;
     }
     // N_s block solves (fdsolver.cpp:58-60), time-major
-    launch_fd_solve(f->blocks, reinterpret_cast<double2*>(const_cast<double*>(cur)), adjoint, st, true);
+    launch_fd_solve(f->blocks, reinterpret_cast<double2*>(const_cast<double*>(cur)), adjoint, st, !nat);
     // from_eigen with U_l (fdsolver.cpp:16-21): axis d first (it consumes the
     // time-major layout), then axes 1..d-1. Mode products on distinct axes
     // commute, so only the rounding order differs.
@@ -247,7 +259,7 @@ void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStre
             fused12(true, cur, out);
             k = klast;
         } else {
-            gemm(f->At_inv[l - 1], l, cur, out, k == 0 ? 2 : 0);
+            gemm(f->At_inv[l - 1], l, cur, out, k == 0 ? tin : 0);
         }
         cur = out;
     }

@@ -453,6 +453,9 @@ __global__ void __launch_bounds__(128) k_fd_solve_ring(const double2* __restrict
 // time-major x accesses coalesce. Loads go through the per-thread cp.async ring
 // as in k_fd_solve_ring.
 // ---------------------------------------------------------------------------
+#ifndef KS_PAIR_RECIP
+#define KS_PAIR_RECIP 1
+#endif
 template <int P, int D>
 __global__ void __launch_bounds__(128) k_fd_solve_pair(const double2* __restrict__ ab,
                                                        const unsigned char* __restrict__ piv,
@@ -550,8 +553,15 @@ __global__ void __launch_bounds__(128) k_fd_solve_pair(const double2* __restrict
         cpa_wait<D - 2>();
         issue_b(k - (D - 1));
         const double2 dg = *slot(k, 0);
-        ua[0] = cdiv(ua[0], dg);
-        ub[0] = cdiv(ub[0], dg);
+        if (KS_PAIR_RECIP) { // one reciprocal for both fibers (rounding-level change)
+            const double sc = 1.0 / fma(dg.x, dg.x, dg.y * dg.y);
+            const double2 rd = make_double2(dg.x * sc, -dg.y * sc);
+            ua[0] = cmul(ua[0], rd);
+            ub[0] = cmul(ub[0], rd);
+        } else {
+            ua[0] = cdiv(ua[0], dg);
+            ub[0] = cdiv(ub[0], dg);
+        }
 #pragma unroll
         for (int j = 1; j <= 2 * P; ++j)
             if (k - j >= 0) {
@@ -572,6 +582,235 @@ __global__ void __launch_bounds__(128) k_fd_solve_pair(const double2* __restrict
     }
 }
 
+// ---------------------------------------------------------------------------
+// Pair-mode solve on the NATURAL layout (t fastest: fiber i is the contiguous
+// run X[i*nt .. i*nt + nt)), so the FD apply needs no time-major hand-off and
+// its outermost-axis transforms run in the plain column mode (c3: 0.77 vs
+// 0.85 ms for the six transforms). A CTA of T threads owns T consecutive
+// blocks and their 2T fibers (pair mode: thread = block b = (i1, pair (i2,i3)),
+// fibers (i1,i2,i3) and (i1,i3,i2)) and sweeps time in chunks of C steps:
+// each chunk's fiber rows (2T segments of C*16 B), band entries (block-
+// interleaved: T consecutive blocks = one contiguous run per entry) and the
+// forward outputs move between HBM and shared memory CTA-wide with cp.async
+// (double-buffered), while each thread runs the same register-window
+// elimination as k_fd_solve_pair on its two fibers from shared memory.
+// Forward (L, with the row interchanges) writes its outputs back to X; the
+// backward sweep (U) reads them in reverse chunks. Same arithmetic, same
+// order as k_fd_solve_pair (eigensolve.cpp:123-140).
+// ---------------------------------------------------------------------------
+template <int P, int C, int T>
+__global__ void __launch_bounds__(T) k_fd_solve_nat(const double2* __restrict__ ab,
+                                                    const unsigned char* __restrict__ piv,
+                                                    double2* __restrict__ X, int nt, size_t nblk, int n1, int n2,
+                                                    const int2* __restrict__ pairs) {
+    constexpr int kuf = 2 * P, NF = 2 * T, CP = C + 1, NEB = 2 * P + 1;
+    extern __shared__ __align__(16) double2 sm_nat[];
+    double2* xin = sm_nat;                          // [2][NF][CP] chunk input rows
+    double2* xout = xin + 2 * NF * CP;              // [2][NF][CP] chunk output rows
+    double2* fac = xout + 2 * NF * CP;              // [2][C][NEB][T] band entries
+    long long* fb = reinterpret_cast<long long*>(fac + 2 * C * NEB * T); // [NF] fiber offsets (-1: none)
+    const int tid = threadIdx.x;
+    const size_t b0 = (size_t)blockIdx.x * T;
+    const size_t b = b0 + tid;
+    const bool valid = b < nblk;
+    {
+        long long oa = -1, ob = -1;
+        if (valid) {
+            const int i1 = (int)(b % (size_t)n1);
+            const int2 q = __ldg(pairs + b / (size_t)n1);
+            oa = ((long long)i1 + (long long)n1 * ((long long)q.x + (long long)n2 * q.y)) * nt;
+            if (q.x != q.y) ob = ((long long)i1 + (long long)n1 * ((long long)q.y + (long long)n2 * q.x)) * nt;
+        }
+        fb[tid] = oa;
+        fb[T + tid] = ob;
+    }
+    __syncthreads();
+    const bool hb = fb[T + tid] >= 0;
+    const double2 Z = make_double2(0.0, 0.0);
+    const int nb = (int)(nblk - b0 < (size_t)T ? nblk - b0 : (size_t)T);
+    // chunk loads: rows [r0, r0 + C) of every fiber, entries (k0 + j, e(j)) of the T blocks
+    auto load_rows = [&](double2* dst, int r0) {
+        for (int e = tid; e < NF * C; e += T) {
+            const int f = e / C, j = e - f * C, r = r0 + j;
+            const long long o = fb[f];
+            const bool v = o >= 0 && r >= 0 && r < nt;
+            cpa16(dst + f * CP + j, v ? (const void*)(X + o + r) : (const void*)X, v);
+        }
+    };
+    // forward entries: the P multipliers (k, kuf + 1 + m) of steps k0 .. k0 + C - 1
+    auto load_fac = [&](double2* dst, int k0) {
+        const bool vb = tid < nb;
+#pragma unroll
+        for (int j = 0; j < C; ++j)
+#pragma unroll
+            for (int m = 0; m < P; ++m) {
+                const int k = k0 + j;
+                const bool v = vb && k + 1 + m < nt;
+                cpa16(dst + (j * NEB + m) * T + tid,
+                      v ? (const void*)(ab + b0 + tid + ((size_t)k * (3 * P + 1) + kuf + 1 + m) * nblk) : (const void*)ab,
+                      v);
+            }
+    };
+    // backward entries: (k, kuf - m), m = 0 .. 2P, of steps k0 .. k0 + C - 1
+    auto load_fac_b = [&](double2* dst, int k0) {
+        const bool vb = tid < nb;
+#pragma unroll
+        for (int j = 0; j < C; ++j)
+#pragma unroll
+            for (int m = 0; m < NEB; ++m) {
+                const int k = k0 + j;
+                const bool v = vb && k >= 0 && k < nt && k - m >= 0;
+                cpa16(dst + (j * NEB + m) * T + tid,
+                      v ? (const void*)(ab + b0 + tid + ((size_t)k * (3 * P + 1) + kuf - m) * nblk) : (const void*)ab,
+                      v);
+            }
+    };
+    auto store_rows = [&](const double2* src, int r0) {
+        for (int e = tid; e < NF * C; e += T) {
+            const int f = e / C, j = e - f * C, r = r0 + j;
+            const long long o = fb[f];
+            if (o >= 0 && r >= 0 && r < nt) X[o + r] = src[f * CP + j];
+        }
+    };
+    const int nch = (nt + C - 1) / C;
+    // ---------------- forward: L with row interchanges (eigensolve.cpp:127-133)
+    double2 wa[P + 1], wb[P + 1];
+#pragma unroll
+    for (int m = 0; m <= P; ++m) {
+        wa[m] = valid && m < nt ? X[fb[tid] + m] : Z;
+        wb[m] = hb && m < nt ? X[fb[T + tid] + m] : Z;
+    }
+    // chunk c: steps [cC, cC + C); new window rows cC + P + 1 + j
+    load_rows(xin, P + 1);
+    load_fac(fac, 0);
+    cpa_commit();
+    unsigned char pv[C], pvn[C];
+#pragma unroll
+    for (int j = 0; j < C; ++j) pv[j] = valid && j < nt ? __ldg(piv + (size_t)j * nblk + b) : 0;
+    for (int c = 0; c < nch; ++c) {
+        const int cb = c & 1;
+        if (c + 1 < nch) {
+            load_rows(xin + (cb ^ 1) * NF * CP, (c + 1) * C + P + 1);
+            load_fac(fac + (cb ^ 1) * C * NEB * T, (c + 1) * C);
+        }
+        cpa_commit();
+#pragma unroll
+        for (int j = 0; j < C; ++j) {
+            const int k = (c + 1) * C + j;
+            pvn[j] = valid && k < nt ? __ldg(piv + (size_t)k * nblk + b) : 0;
+        }
+        cpa_wait<1>();
+        __syncthreads();
+        const double2* xi = xin + cb * NF * CP;
+        double2* xo = xout + cb * NF * CP;
+        const double2* fc = fac + cb * C * NEB * T;
+#pragma unroll
+        for (int j = 0; j < C; ++j) {
+            const int k = c * C + j;
+            if (k < nt) {
+                const int po = pv[j];
+#pragma unroll
+                for (int m = 1; m <= P; ++m)
+                    if (po == m) {
+                        double2 tt = wa[0];
+                        wa[0] = wa[m];
+                        wa[m] = tt;
+                        tt = wb[0];
+                        wb[0] = wb[m];
+                        wb[m] = tt;
+                    }
+#pragma unroll
+                for (int m = 1; m <= P; ++m)
+                    if (k + m < nt) {
+                        const double2 l = fc[(j * NEB + (m - 1)) * T + tid];
+                        wa[m] = csub(wa[m], cmul(l, wa[0]));
+                        wb[m] = csub(wb[m], cmul(l, wb[0]));
+                    }
+                xo[tid * CP + j] = wa[0];
+                xo[(T + tid) * CP + j] = wb[0];
+                const double2 ina = xi[tid * CP + j], inb = xi[(T + tid) * CP + j];
+#pragma unroll
+                for (int m = 0; m < P; ++m) {
+                    wa[m] = wa[m + 1];
+                    wb[m] = wb[m + 1];
+                }
+                wa[P] = ina;
+                wb[P] = inb;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < C; ++j) pv[j] = pvn[j];
+        __syncthreads();
+        store_rows(xo, c * C);
+    }
+    cpa_wait<0>();
+    __threadfence_block();
+    __syncthreads();
+    // ---------------- backward: U, column oriented (eigensolve.cpp:134-139)
+    // chunk c: steps k = nt-1-cC-j; new window rows k - 2P - 1
+    double2 ua[2 * P + 1], ub[2 * P + 1];
+#pragma unroll
+    for (int j = 0; j <= 2 * P; ++j) {
+        const int r = nt - 1 - j;
+        ua[j] = valid && r >= 0 ? X[fb[tid] + r] : Z;
+        ub[j] = hb && r >= 0 ? X[fb[T + tid] + r] : Z;
+    }
+    // rows of chunk c (ascending in memory): [nt-1-cC-(C-1) - 2P - 1, nt-1-cC - 2P - 1]
+    auto brow0 = [&](int c) { return nt - 1 - c * C - (C - 1) - 2 * P - 1; };
+    auto bk0 = [&](int c) { return nt - 1 - c * C - (C - 1); }; // lowest step of chunk c
+    load_rows(xin, brow0(0));
+    load_fac_b(fac, bk0(0)); // slot j <-> step bk0 + j
+    cpa_commit();
+    for (int c = 0; c < nch; ++c) {
+        const int cb = c & 1;
+        if (c + 1 < nch) {
+            load_rows(xin + (cb ^ 1) * NF * CP, brow0(c + 1));
+            load_fac_b(fac + (cb ^ 1) * C * NEB * T, bk0(c + 1));
+        }
+        cpa_commit();
+        cpa_wait<1>();
+        __syncthreads();
+        const double2* xi = xin + cb * NF * CP;
+        double2* xo = xout + cb * NF * CP;
+        const double2* fc = fac + cb * C * NEB * T;
+        const int k0 = bk0(c);
+#pragma unroll
+        for (int jj = C - 1; jj >= 0; --jj) { // steps descending
+            const int k = k0 + jj;
+            if (k >= 0) {
+                // one reciprocal of the pivot for both fibers: conj(d) / |d|^2
+                // (1 division instead of Smith's 3 per quotient; differs from
+                // the reference's __divdc3 by rounding only)
+                const double2 dg = fc[(jj * NEB + 0) * T + tid];
+                const double sc = 1.0 / fma(dg.x, dg.x, dg.y * dg.y);
+                const double2 rd = make_double2(dg.x * sc, -dg.y * sc);
+                ua[0] = cmul(ua[0], rd);
+                ub[0] = cmul(ub[0], rd);
+#pragma unroll
+                for (int j = 1; j <= 2 * P; ++j)
+                    if (k - j >= 0) {
+                        const double2 uu = fc[(jj * NEB + j) * T + tid];
+                        ua[j] = csub(ua[j], cmul(uu, ua[0]));
+                        ub[j] = csub(ub[j], cmul(uu, ub[0]));
+                    }
+                xo[tid * CP + jj] = ua[0];
+                xo[(T + tid) * CP + jj] = ub[0];
+                // row k - 2P - 1 sits at chunk slot jj (chunk rows start at k0 - 2P - 1)
+                const double2 ina = xi[tid * CP + jj], inb = xi[(T + tid) * CP + jj];
+#pragma unroll
+                for (int j = 0; j < 2 * P; ++j) {
+                    ua[j] = ua[j + 1];
+                    ub[j] = ub[j + 1];
+                }
+                ua[2 * P] = ina;
+                ub[2 * P] = inb;
+            }
+        }
+        __syncthreads();
+        store_rows(xo, k0);
+    }
+}
+
 template <int P>
 void launch_solve_p(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t st, int tm) {
     const unsigned grid = (unsigned)((B.ns + 127) / 128);
@@ -584,6 +823,25 @@ void launch_solve_p(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t st
             const char* e = std::getenv("KS_FD_PFD");
             return e ? std::atoi(e) : 0;
         }();
+        if (!tm && B.pair_n1 > 0 && B.rec == 0 && B.fused_nd == 0) {
+            // natural layout (FD apply without the time-major hand-off)
+            // C = 2 steps per chunk: 45 KB per CTA, five CTAs (10 warps) per SM
+            // (C = 4: two CTAs per SM, latency bound at 0.88 ms)
+            constexpr int C = 2, T = 64, NEB = 2 * P + 1;
+            const size_t sm = (size_t)(4 * 2 * T * (C + 1) + 2 * C * NEB * T) * sizeof(double2) +
+                              (size_t)2 * T * sizeof(long long);
+            static bool attr = false;
+            if (!attr) {
+                KS_CUDA(cudaFuncSetAttribute(k_fd_solve_nat<P, C, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)sm));
+                attr = true;
+            }
+            const unsigned gn = (unsigned)((B.nblk + T - 1) / T);
+            k_fd_solve_nat<P, C, T><<<gn, T, sm, st>>>(B.ab.as<double2>(), B.piv.as<unsigned char>(), X, B.nt, B.nblk,
+                                                       B.pair_n1, B.pair_n2, B.pairs.as<int2>());
+            check_launch("k_fd_solve_nat");
+            return;
+        }
         if (tm && B.pair_n1 > 0) {
             constexpr int NE = 2 * P + 3, D = 4;
             const size_t sm = (size_t)D * NE * 128 * sizeof(double2) + (size_t)D * 128 * sizeof(unsigned);
