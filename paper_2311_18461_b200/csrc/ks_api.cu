@@ -115,6 +115,7 @@ struct ks_kron {
     std::unique_ptr<KronPlan, KronPlanDeleter> plan;
     DevBuf io_x, io_y;
     DevBuf pcg[6];                 // ks_pcg work vectors (x, r, z, p, q, scratch), kept across solves
+    std::unique_ptr<Reducer> pcg_red[5]; // ks_pcg reducers (pinned host words), kept across solves
     std::vector<void*> hptrs;
     cudaStream_t stream = nullptr;
     std::mutex mu;
@@ -855,37 +856,43 @@ int ks_pcg(ks_kron* A, ks_fd* P, const ks_c64* b, ks_c64* x, int mem, const ks_p
         bd = bb.as<double2>();
     }
     KS_CUDA(cudaMemsetAsync(xv.p, 0, bytes, st));
-    Reducer red;
-    cudaEvent_t e0, e1;
-    KS_CUDA(cudaEventCreate(&e0));
-    KS_CUDA(cudaEventCreate(&e1));
+    // Scalars stay on the device: alpha and beta are formed by the update
+    // kernels from the reducers' results, so an iteration has one host round
+    // trip (curvature + ||r||^2, read together for the breakdown and
+    // convergence tests). Operator timers: event pairs, summed at the end.
+    for (auto& rp : A->pcg_red)
+        if (!rp) rp.reset(new Reducer());
+    Reducer &red = *A->pcg_red[0], &red_c = *A->pcg_red[1], &red_u = *A->pcg_red[2];
+    Reducer* red_rho[2] = {A->pcg_red[3].get(), A->pcg_red[4].get()};
+    int ra = 0; // red_rho[ra] holds the current rho
+    std::vector<cudaEvent_t> evs;
     struct EvGuard {
-        cudaEvent_t a, b;
-        ~EvGuard() { cudaEventDestroy(a); cudaEventDestroy(b); }
-    } evg{e0, e1};
-    double t_mv = 0, t_pc = 0;
+        std::vector<cudaEvent_t>& v;
+        ~EvGuard() {
+            for (auto e : v) cudaEventDestroy(e);
+        }
+    } evg{evs};
+    std::vector<std::pair<int, int>> mv_ev, pc_ev; // indices into evs
+    auto ev_pair = [&](std::vector<std::pair<int, int>>& dst, auto&& body) {
+        cudaEvent_t a, b2;
+        KS_CUDA(cudaEventCreate(&a));
+        evs.push_back(a);
+        KS_CUDA(cudaEventCreate(&b2));
+        evs.push_back(b2);
+        KS_CUDA(cudaEventRecord(a, st));
+        body();
+        KS_CUDA(cudaEventRecord(b2, st));
+        dst.push_back({(int)evs.size() - 2, (int)evs.size() - 1});
+    };
     auto matvec = [&](const double2* in, double2* outv) {
-        KS_CUDA(cudaEventRecord(e0, st));
-        kron_apply(*A->plan, in, outv, st, A->hptrs);
-        KS_CUDA(cudaEventRecord(e1, st));
-        KS_CUDA(cudaEventSynchronize(e1));
-        t_mv += elapsed(e0, e1) * 1e-3;
+        ev_pair(mv_ev, [&]() { kron_apply(*A->plan, in, outv, st, A->hptrs); });
     };
     auto precond = [&](const double2* rin, double2* zout) {
         if (P) {
-            KS_CUDA(cudaEventRecord(e0, st));
-            fd_apply_dev(P, rin, zout, false, st, nullptr);
-            KS_CUDA(cudaEventRecord(e1, st));
-            KS_CUDA(cudaEventSynchronize(e1));
-            t_pc += elapsed(e0, e1) * 1e-3;
+            ev_pair(pc_ev, [&]() { fd_apply_dev(P, rin, zout, false, st, nullptr); });
         } else {
             KS_CUDA(cudaMemcpyAsync(zout, rin, bytes, cudaMemcpyDeviceToDevice, st));
         }
-    };
-    auto dotc_re = [&](const double2* a, const double2* c) {
-        launch_dotc(red, a, c, n, st);
-        fetch(red, st, 2);
-        return red.host[0];
     };
     auto norm2 = [&](const double2* a) {
         launch_norm2sq(red, a, n, st);
@@ -897,6 +904,9 @@ int ks_pcg(ks_kron* A, ks_fd* P, const ks_c64* b, ks_c64* x, int mem, const ks_p
                                 mem == KS_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                                 st));
         KS_CUDA(cudaStreamSynchronize(st));
+        double t_mv = 0, t_pc = 0;
+        for (auto& e : mv_ev) t_mv += elapsed(evs[e.first], evs[e.second]) * 1e-3;
+        for (auto& e : pc_ev) t_pc += elapsed(evs[e.first], evs[e.second]) * 1e-3;
         report->matvec_seconds = t_mv;
         report->precond_seconds = t_pc;
         report->solve_seconds =
@@ -925,21 +935,22 @@ int ks_pcg(ks_kron* A, ks_fd* P, const ks_c64* b, ks_c64* x, int mem, const ks_p
     KS_CUDA(cudaMemcpyAsync(r.p, bd, bytes, cudaMemcpyDeviceToDevice, st));
     precond(r.as<double2>(), z.as<double2>());
     KS_CUDA(cudaMemcpyAsync(p.p, z.p, bytes, cudaMemcpyDeviceToDevice, st));
-    double rho = dotc_re(r.as<double2>(), z.as<double2>());
+    launch_dotc(*red_rho[ra], r.as<double2>(), z.as<double2>(), n, st); // rho = Re <r, z>
     int restarts = 0;
     for (int k = 0; k < opts->maxit; ++k) {
         matvec(p.as<double2>(), q.as<double2>());
-        const double curvature = dotc_re(p.as<double2>(), q.as<double2>());
-        if (curvature <= 0.0) {
+        launch_dotc(red_c, p.as<double2>(), q.as<double2>(), n, st); // curvature Re <p, Ap>
+        launch_cg_update_dev(red_u, red_rho[ra]->result.as<double>(), red_c.result.as<double>(), p.as<double2>(),
+                             q.as<double2>(), xv.as<double2>(), r.as<double2>(), n, st);
+        KS_CUDA(cudaMemcpyAsync(red_c.host, red_c.result.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+        KS_CUDA(cudaMemcpyAsync(red_u.host, red_u.result.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+        KS_CUDA(cudaStreamSynchronize(st));
+        if (red_c.host[0] <= 0.0) { // x, r untouched by the update kernel
             report->breakdown = 1;
             break;
         }
-        const double alpha = rho / curvature;
-        launch_cg_update(red, alpha, p.as<double2>(), q.as<double2>(), xv.as<double2>(),
-                         r.as<double2>(), n, st);
-        fetch(red, st, 1);
         report->iterations++;
-        double relres = std::sqrt(red.host[0]) / bnorm;
+        double relres = std::sqrt(red_u.host[0]) / bnorm;
         if (opts->strict_residual) relres = true_relres();
         push_hist(relres);
         if (relres <= opts->tol) {
@@ -951,7 +962,7 @@ int ks_pcg(ks_kron* A, ks_fd* P, const ks_c64* b, ks_c64* x, int mem, const ks_p
                     launch_neg_copy(scratch.as<double2>(), r.as<double2>(), n, st);
                     precond(r.as<double2>(), z.as<double2>());
                     KS_CUDA(cudaMemcpyAsync(p.p, z.p, bytes, cudaMemcpyDeviceToDevice, st));
-                    rho = dotc_re(r.as<double2>(), z.as<double2>());
+                    launch_dotc(*red_rho[ra], r.as<double2>(), z.as<double2>(), n, st);
                     continue;
                 }
             }
@@ -959,10 +970,10 @@ int ks_pcg(ks_kron* A, ks_fd* P, const ks_c64* b, ks_c64* x, int mem, const ks_p
             break;
         }
         precond(r.as<double2>(), z.as<double2>());
-        const double rho_new = dotc_re(r.as<double2>(), z.as<double2>());
-        const double beta = rho_new / rho;
-        rho = rho_new;
-        launch_xpby(z.as<double2>(), beta, p.as<double2>(), n, st);
+        launch_dotc(*red_rho[ra ^ 1], r.as<double2>(), z.as<double2>(), n, st); // rho_new
+        launch_xpby_dev(z.as<double2>(), red_rho[ra ^ 1]->result.as<double>(), red_rho[ra]->result.as<double>(),
+                        p.as<double2>(), n, st);
+        ra ^= 1;
     }
     report->restarts = restarts;
     report->hist_len = hist_len < hist_cap ? hist_len : hist_cap;

@@ -125,6 +125,49 @@ __global__ void __launch_bounds__(kT) k_cg_update(double alpha, const double2* _
     finish<1>(v, partial, counter, result);
 }
 
+// Device-scalar variant: alpha = rho / curv read from the reducers' results
+// (same double division as krylov.cpp:73); curv <= 0 (breakdown,
+// krylov.cpp:68-72) leaves x and r untouched so the host can stop exactly
+// where the reference does.
+__global__ void __launch_bounds__(kT) k_cg_update_dev(const double* __restrict__ rho, const double* __restrict__ curv,
+                                                      const double2* __restrict__ p, const double2* __restrict__ q,
+                                                      double2* __restrict__ x, double2* __restrict__ r, size_t n,
+                                                      double* partial, unsigned* counter, double* result) {
+    const double c = *curv;
+    const bool live = c > 0.0;
+    const double alpha = live ? *rho / c : 0.0;
+    double v[1] = {0.0};
+    for (size_t i = blockIdx.x * (size_t)kT + threadIdx.x; i < n; i += (size_t)gridDim.x * kT) {
+        double2 ri = r[i];
+        if (live) {
+            const double2 pi = __ldg(p + i), qi = __ldg(q + i);
+            double2 xi = x[i];
+            xi.x += alpha * pi.x;
+            xi.y += alpha * pi.y;
+            ri.x += -alpha * qi.x;
+            ri.y += -alpha * qi.y;
+            x[i] = xi;
+            r[i] = ri;
+        }
+        v[0] += ri.x * ri.x + ri.y * ri.y;
+    }
+    finish<1>(v, partial, counter, result);
+}
+
+// p = z + (rho_new / rho_old) p  (krylov.cpp:105-110), beta formed on the device
+__global__ void k_xpby_dev(const double2* __restrict__ z, const double* __restrict__ rho_new,
+                           const double* __restrict__ rho_old, double2* __restrict__ p, size_t n) {
+    const double beta = *rho_new / *rho_old;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x) {
+        const double2 zi = __ldg(z + i);
+        double2 pi = p[i];
+        pi.x = zi.x + beta * pi.x;
+        pi.y = zi.y + beta * pi.y;
+        p[i] = pi;
+    }
+}
+
 __global__ void k_xpby(const double2* __restrict__ z, double beta, double2* __restrict__ p,
                        size_t n) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
@@ -207,6 +250,17 @@ void launch_cg_update(Reducer& red, double alpha, const double2* p, const double
     k_cg_update<<<kB, kT, 0, s>>>(alpha, p, q, x, r, n, red.partial.as<double>(),
                                   red.counter.as<unsigned>(), red.result.as<double>());
     check_launch("k_cg_update");
+}
+void launch_cg_update_dev(Reducer& red, const double* rho, const double* curv, const double2* p, const double2* q,
+                          double2* x, double2* r, size_t n, cudaStream_t s) {
+    k_cg_update_dev<<<kB, kT, 0, s>>>(rho, curv, p, q, x, r, n, red.partial.as<double>(), red.counter.as<unsigned>(),
+                                      red.result.as<double>());
+    check_launch("k_cg_update_dev");
+}
+void launch_xpby_dev(const double2* z, const double* rho_new, const double* rho_old, double2* p, size_t n,
+                     cudaStream_t s) {
+    k_xpby_dev<<<ew_blocks(n), 256, 0, s>>>(z, rho_new, rho_old, p, n);
+    check_launch("k_xpby_dev");
 }
 void launch_xpby(const double2* z, double beta, double2* p, size_t n, cudaStream_t s) {
     k_xpby<<<ew_blocks(n), 256, 0, s>>>(z, beta, p, n);

@@ -105,6 +105,12 @@ void launch_norm2sq(Reducer& r, const double2* x, size_t n, cudaStream_t s);
 // x += a p ; r -= a q ; result[0] = ||r||^2   (krylov.cpp:73-78)
 void launch_cg_update(Reducer& red, double alpha, const double2* p, const double2* q,
                       double2* x, double2* r, size_t n, cudaStream_t s);
+// device-scalar forms (no host round trip): alpha = *rho / *curv (no update
+// when *curv <= 0), beta = *rho_new / *rho_old
+void launch_cg_update_dev(Reducer& red, const double* rho, const double* curv, const double2* p, const double2* q,
+                          double2* x, double2* r, size_t n, cudaStream_t s);
+void launch_xpby_dev(const double2* z, const double* rho_new, const double* rho_old, double2* p, size_t n,
+                     cudaStream_t s);
 // p = z + beta p   (krylov.cpp:109-110)
 void launch_xpby(const double2* z, double beta, double2* p, size_t n, cudaStream_t s);
 // y = a*x + y (real a)
