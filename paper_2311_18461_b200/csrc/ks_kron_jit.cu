@@ -152,6 +152,7 @@ KronJitPair* kron_jit_build(int nin, int nmid, int nout, int bw, const std::vect
             T_best = T;
         }
     }
+    if (T_best == 0) return nullptr; // a line longer than the block limit: per-pass kernels
     const int T = T_best;
     const int nq = s_a > 1 ? c_best : 1, no = s_a > 1 ? 1 : c_best;
     const long long nqb = (s_a + nq - 1) / nq, nob = (n_outer + no - 1) / no;
