@@ -455,8 +455,14 @@ KronPlan* kron_plan(const std::vector<int>& dims,
         KS_CUDA(cudaMemcpy(P->d_freal.p, freal.data(), freal.size() * sizeof(int), cudaMemcpyHostToDevice));
         // fused pass pairs (0,1), (2,3), ... specialised with NVRTC
         P->jit.resize(P->passes.size());
+        // factor classes: 1 real, 2 purely imaginary (e.g. W + W^H), 0 complex
         std::vector<int> frv(P->factors.size());
-        for (size_t f = 0; f < P->factors.size(); ++f) frv[f] = P->factors[f].is_real ? 1 : 0;
+        for (size_t f = 0; f < P->factors.size(); ++f) {
+            const KronFactor& kf = P->factors[f];
+            bool imag = !kf.is_real;
+            for (size_t e = 0; e < (size_t)kf.n * (2 * kf.bw + 1) && imag; ++e) imag = pool[kf.off + e].x == 0.0;
+            frv[f] = kf.is_real ? 1 : (imag ? 2 : 0);
+        }
         for (size_t k = 0; k + 1 < P->passes.size(); k += 2) {
             const KronPass &pa = P->passes[k], &pb = P->passes[k + 1];
             if (pb.axis != pa.axis + 1 || pb.n_in != pa.n_out) break;
@@ -481,10 +487,16 @@ KronPlan* kron_plan(const std::vector<int>& dims,
         }
     }
     {
-        std::vector<int> frv(std::max<size_t>(P->factors.size(), 1), 1);
-        for (size_t f = 0; f < P->factors.size(); ++f) frv[f] = P->factors[f].is_real ? 1 : 0;
+        // factor classes for the generated kernel: 1 real, 2 purely imaginary, 0 complex
+        std::vector<int> fcl(std::max<size_t>(P->factors.size(), 1), 1);
+        for (size_t f = 0; f < P->factors.size(); ++f) {
+            const KronFactor& kf = P->factors[f];
+            bool imag = !kf.is_real;
+            for (size_t e = 0; e < (size_t)kf.n * (2 * kf.bw + 1) && imag; ++e) imag = pool[kf.off + e].x == 0.0;
+            fcl[f] = kf.is_real ? 1 : (imag ? 2 : 0);
+        }
         bool all_active = D == 4 && (int)ax.size() == 4;
-        if (all_active) P->k3.reset(kron3_build(dims, P->bwmax, P->nmax, frv, coeffs, fids));
+        if (all_active) P->k3.reset(kron3_build(dims, P->bwmax, P->nmax, fcl, coeffs, fids));
     }
     for (auto& ps : P->passes) {
         std::vector<int> ib(ps.n_in + 1, 0);

@@ -110,14 +110,17 @@ void kron3_free(Kron3* p) { delete p; }
 
 // Build the two-launch plan for four axes (t, 1, 2, 3); null if the shape does
 // not fit (the level-pass plan is used instead) or KS_KRON3=0.
-Kron3* kron3_build(const std::vector<int>& dims, int bw, int nmax, const std::vector<int>& freal,
+Kron3* kron3_build(const std::vector<int>& dims, int bw, int nmax, const std::vector<int>& fclass,
                    const std::vector<double2>& coeffs, const std::vector<std::vector<int>>& fids) {
     if (const char* e = std::getenv("KS_KRON3"))
         if (std::strcmp(e, "0") == 0) return nullptr;
     if (dims.size() != 4 || bw < 1 || bw > 6 || coeffs.empty()) return nullptr;
     const int n0 = dims[0], n1 = dims[1], n2 = dims[2];
     const int T = (int)coeffs.size();
-    auto is_real = [&](int f) { return f >= 0 && freal[f] != 0; };
+    // factor classes: 1 real, 2 purely imaginary (W + W^H), 0 complex
+    auto is_real = [&](int f) { return f >= 0 && fclass[f] == 1; };
+    auto is_imag = [&](int f) { return f >= 0 && fclass[f] == 2; };
+    auto is_scal = [&](int f) { return is_real(f) || is_imag(f); }; // one double per entry
     std::unique_ptr<Kron3> K(new Kron3());
     K->dims = dims;
     K->N = (size_t)dims[0] * dims[1] * dims[2] * dims[3];
@@ -283,9 +286,10 @@ ks_k3(const K3P P) {
     // time factors: real rows in registers (each lane has its own row t), complex
     // rows in shared memory, k-major so that a warp's lanes read consecutive t
     for (size_t j = 0; j < f0l.size(); ++j) {
-        if (is_real(f0l[j]))
+        if (is_scal(f0l[j]))
             s << "    double R0_" << j << "[W];\n#pragma unroll\n    for (int k = 0; k < W; ++k) R0_" << j
-              << "[k] = act ? P.rb[((long long)" << f0l[j] << " * NMAX + t) * W + k].x : 0.0;\n";
+              << "[k] = act ? P.rb[((long long)" << f0l[j] << " * NMAX + t) * W + k]." << (is_imag(f0l[j]) ? "y" : "x")
+              << " : 0.0;\n";
         else
             s << "    for (int e = tid; e < N0 * W; e += NT) { const int tt = e / W, k = e - tt * W; ft[" << j
               << " * N0 * W + k * N0 + tt] = P.rb[(long long)" << f0l[j] << " * NMAX * W + e]; }\n";
@@ -305,9 +309,10 @@ ks_k3(const K3P P) {
         // two partial sums (even / odd taps) per component: shorter dependent
         // DFMA chains
         std::string fk;
-        if (!axis1 && is_real(f)) fk = "R0_" + lit(j) + "[K]";
-        else if (axis1) fk = std::string("fat[") + lit(j) + " * TX * W + K]" + (is_real(f) ? ".x" : "");
-        else fk = std::string("ftt[") + lit(j) + " * N0 * W + K * N0]" + (is_real(f) ? ".x" : "");
+        const char* comp = is_real(f) ? ".x" : (is_imag(f) ? ".y" : "");
+        if (!axis1 && is_scal(f)) fk = "R0_" + lit(j) + "[K]";
+        else if (axis1) fk = std::string("fat[") + lit(j) + " * TX * W + K]" + comp;
+        else fk = std::string("ftt[") + lit(j) + " * N0 * W + K * N0]" + comp;
         auto F = [&](int k) {
             std::string r = fk;
             const size_t pos = r.find('K');
@@ -323,6 +328,9 @@ ks_k3(const K3P P) {
                 if (is_real(f))
                     s << "                  q" << par << ".x = fma(" << F(k) << ", " << tk << ".x, q" << par << ".x); q" << par
                       << ".y = fma(" << F(k) << ", " << tk << ".y, q" << par << ".y);\n";
+                else if (is_imag(f)) // (i w)(a + i b) = -w b + i w a
+                    s << "                  q" << par << ".x = fma(-" << F(k) << ", " << tk << ".y, q" << par << ".x); q" << par
+                      << ".y = fma(" << F(k) << ", " << tk << ".x, q" << par << ".y);\n";
                 else
                     s << "                  cacc(q" << par << ", " << F(k) << ", " << tk << ");\n";
             }
@@ -394,6 +402,9 @@ ks_k3(const K3P P) {
                 if (is_real(f))
                     s << "acc[" << slot << "].x = fma(cf.x, wh" << h << ".x, acc[" << slot << "].x); acc[" << slot
                       << "].y = fma(cf.x, wh" << h << ".y, acc[" << slot << "].y); }\n";
+                else if (is_imag(f))
+                    s << "acc[" << slot << "].x = fma(-cf.y, wh" << h << ".y, acc[" << slot << "].x); acc[" << slot
+                      << "].y = fma(cf.y, wh" << h << ".x, acc[" << slot << "].y); }\n";
                 else
                     s << "cacc(acc[" << slot << "], cf, wh" << h << "); }\n";
             }

@@ -166,7 +166,28 @@ KronJitPair* kron_jit_build(int nin, int nmid, int nout, int bw, const std::vect
     // (1.98 vs 1.67 ms; KS_KRON_JIT_MINB overrides for experiments)
     const int minb = 1;
     const int minb_env = std::getenv("KS_KRON_JIT_MINB") ? std::atoi(std::getenv("KS_KRON_JIT_MINB")) : 0;
-    auto is_real = [&](int f) { return f >= 0 && freal[f] != 0; };
+    // factor classes (freal): 1 real, 2 purely imaginary (one double per entry), 0 complex
+    auto is_real = [&](int f) { return f >= 0 && freal[f] == 1; };
+    auto is_imag = [&](int f) { return f >= 0 && freal[f] == 2; };
+    auto is_scal = [&](int f) { return is_real(f) || is_imag(f); };
+    auto comp = [&](int f) -> std::string { return is_real(f) ? ".x" : (is_imag(f) ? ".y" : ""); };
+    // v += F * w for one tap, F of class f held as `fv` (double for real / imaginary)
+    auto mac = [&](int f, const std::string& v, const std::string& fv, const std::string& w) -> std::string {
+        if (is_real(f))
+            return " " + v + ".x = fma(" + fv + ", " + w + ".x, " + v + ".x); " + v + ".y = fma(" + fv + ", " + w + ".y, " + v +
+                   ".y);";
+        if (is_imag(f))
+            return " " + v + ".x = fma(-" + fv + ", " + w + ".y, " + v + ".x); " + v + ".y = fma(" + fv + ", " + w + ".x, " + v +
+                   ".y);";
+        return " cacc(" + v + ", " + fv + ", " + w + ");";
+    };
+    // acc += c * v with the contribution coefficient (real coefficients: 2 DFMA)
+    auto cmac = [&](const std::string& acc, int ci, const std::string& v) -> std::string {
+        if (coeffs[ci].y == 0.0)
+            return acc + ".x = fma(P.c[" + lit(ci) + "].x, " + v + ".x, " + acc + ".x); " + acc + ".y = fma(P.c[" + lit(ci) +
+                   "].x, " + v + ".y, " + acc + ".y);";
+        return "cacc(" + acc + ", P.c[" + lit(ci) + "], " + v + ");";
+    };
     // axis-b factor bands staged in shared memory once per CTA (they are read
     // every plane, uniformly across the CTA)
     std::vector<int> fbl;
@@ -259,18 +280,18 @@ ks_pair(const double2* const* __restrict__ ip, double2* const* __restrict__ op, 
     auto aref = [&](int f, const char* k) -> std::string {
         if (!asm_rows) return "A" + lit(f) + "[" + k + "]";
         const int j = (int)(std::find(fal.begin(), fal.end(), f) - fal.begin());
-        return std::string("asmr[(") + lit(j) + " * n_a + ia) * W + " + k + "]" + (is_real(f) ? ".x" : "");
+        return std::string("asmr[(") + lit(j) + " * n_a + ia) * W + " + k + "]" + comp(f);
     };
     if (asm_rows) {
         s << "    const double2* asmr = ring + D * NIN * RS + " << (stage ? fbl.size() : 0) << " * n_b * W;\n";
     } else {
         for (int f : fa) {
-            if (is_real(f))
+            if (is_scal(f))
                 s << "    double A" << f << "[W];\n";
             else
                 s << "    double2 A" << f << "[W];\n";
             s << "#pragma unroll\n    for (int k = 0; k < W; ++k) { const double2 t = valid ? rb[((unsigned long long)" << f
-              << " * nmax + ia) * W + k] : Z; A" << f << "[k] = t" << (is_real(f) ? ".x" : "") << "; }\n";
+              << " * nmax + ia) * W + k] : Z; A" << f << "[k] = t" << comp(f) << "; }\n";
         }
     }
     const int nwin = pull ? nmid : nout;
@@ -302,15 +323,11 @@ ks_pair(const double2* const* __restrict__ ip, double2* const* __restrict__ op, 
             if (f < 0) {
                 s << "                const double2 vI = w[BW];\n";
             } else {
-                s << "                double2 " << v << " = Z;\n#pragma unroll\n                for (int k = 0; k < W; ++k) {";
-                if (is_real(f))
-                    s << " " << v << ".x = fma(" << aref(f, "k") << ", w[k].x, " << v << ".x); " << v << ".y = fma("
-                      << aref(f, "k") << ", w[k].y, " << v << ".y); }\n";
-                else
-                    s << " cacc(" << v << ", " << aref(f, "k") << ", w[k]); }\n";
+                s << "                double2 " << v << " = Z;\n#pragma unroll\n                for (int k = 0; k < W; ++k) {"
+                  << mac(f, v, aref(f, "k"), "w[k]") << " }\n";
             }
             for (auto* c : cs)
-                if (c->factor == f) s << "                cacc(m" << c->out << ", P.c[" << c->coeff << "], " << v << ");\n";
+                if (c->factor == f) s << "                " << cmac("m" + lit(c->out), c->coeff, v) << "\n";
         }
         s << "            }\n";
     }
@@ -324,11 +341,11 @@ ks_pair(const double2* const* __restrict__ ip, double2* const* __restrict__ op, 
         s << "        }\n        const int rd = ib - BW;\n        if (rd < 0) continue;\n";
         // axis-b rows at row rd (uniform across the CTA)
         for (int f : fb) {
-            s << "        " << (is_real(f) ? "double" : "double2") << " B" << f << "[W];\n"
+            s << "        " << (is_scal(f) ? "double" : "double2") << " B" << f << "[W];\n"
               << "#pragma unroll\n        for (int j = 0; j < W; ++j) { const double2 t = "
               << (stage ? "bsm[(" + lit(bidx(f)) + " * n_b + rd) * W + j]"
                         : "rb[((unsigned long long)" + lit(f) + " * nmax + rd) * W + j]")
-              << "; B" << f << "[j] = t" << (is_real(f) ? ".x" : "") << "; }\n";
+              << "; B" << f << "[j] = t" << comp(f) << "; }\n";
         }
         // distinct (h, f) products, then outputs
         std::set<std::pair<int, int>> hf;
@@ -339,31 +356,27 @@ ks_pair(const double2* const* __restrict__ ip, double2* const* __restrict__ op, 
             if (f < 0) {
                 s << "        const double2 " << v << " = win[" << h << "][BW];\n";
             } else {
-                s << "        double2 " << v << " = Z;\n#pragma unroll\n        for (int j = 0; j < W; ++j) {";
-                if (is_real(f))
-                    s << " " << v << ".x = fma(B" << f << "[j], win[" << h << "][j].x, " << v << ".x); " << v
-                      << ".y = fma(B" << f << "[j], win[" << h << "][j].y, " << v << ".y); }\n";
-                else
-                    s << " cacc(" << v << ", B" << f << "[j], win[" << h << "][j]); }\n";
+                s << "        double2 " << v << " = Z;\n#pragma unroll\n        for (int j = 0; j < W; ++j) {"
+                  << mac(f, v, "B" + lit(f) + "[j]", "win[" + lit(h) + "][j]") << " }\n";
             }
         }
         for (int o = 0; o < nout; ++o) {
             s << "        { double2 acc = Z;\n";
             for (auto& c : b)
                 if (c.out == o)
-                    s << "          cacc(acc, P.c[" << c.coeff << "], d" << c.in << "_"
-                      << (c.factor < 0 ? std::string("I") : lit(c.factor)) << ");\n";
+                    s << "          " << cmac("acc", c.coeff, "d" + lit(c.in) + "_" + (c.factor < 0 ? std::string("I") : lit(c.factor)))
+                      << "\n";
             s << "          if (valid) P.out[" << o << "][base + s_b * rd] = acc; }\n";
         }
         s << "    }\n";
     } else {
         // push: column ib of each axis-b factor, F(ib + j - BW, ib), uniform
         for (int f : fb) {
-            s << "            " << (is_real(f) ? "double" : "double2") << " C" << f << "[W];\n"
+            s << "            " << (is_scal(f) ? "double" : "double2") << " C" << f << "[W];\n"
               << "#pragma unroll\n            for (int j = 0; j < W; ++j) { const int r = ib + j - BW; const double2 t = (r >= 0 && r < n_b) ? "
               << (stage ? "bsm[(" + lit(bidx(f)) + " * n_b + r) * W + (W - 1 - j)]"
                         : "rb[((unsigned long long)" + lit(f) + " * nmax + r) * W + (W - 1 - j)]")
-              << " : Z; C" << f << "[j] = t" << (is_real(f) ? ".x" : "") << "; }\n";
+              << " : Z; C" << f << "[j] = t" << comp(f) << "; }\n";
         }
         // cm = sum over contributions into (o, f) of c * m_h; then win[o][j] += C_f[j] * cm
         std::set<std::pair<int, int>> of;
@@ -372,13 +385,12 @@ ks_pair(const double2* const* __restrict__ ip, double2* const* __restrict__ op, 
             const int o = pr.first, f = pr.second;
             s << "            { double2 cm = Z;\n";
             for (auto& c : b)
-                if (c.out == o && c.factor == f) s << "              cacc(cm, P.c[" << c.coeff << "], m" << c.in << ");\n";
+                if (c.out == o && c.factor == f) s << "              " << cmac("cm", c.coeff, "m" + lit(c.in)) << "\n";
             if (f < 0) {
                 s << "              win[" << o << "][BW].x += cm.x; win[" << o << "][BW].y += cm.y; }\n";
-            } else if (is_real(f)) {
-                s << "#pragma unroll\n              for (int j = 0; j < W; ++j) { win[" << o << "][j].x = fma(C" << f
-                  << "[j], cm.x, win[" << o << "][j].x); win[" << o << "][j].y = fma(C" << f << "[j], cm.y, win[" << o
-                  << "][j].y); } }\n";
+            } else if (is_scal(f)) {
+                s << "#pragma unroll\n              for (int j = 0; j < W; ++j) {"
+                  << mac(f, "win[" + lit(o) + "][j]", "C" + lit(f) + "[j]", "cm") << " } }\n";
             } else {
                 s << "#pragma unroll\n              for (int j = 0; j < W; ++j) cacc(win[" << o << "][j], C" << f
                   << "[j], cm); }\n";

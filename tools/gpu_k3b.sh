@@ -1,0 +1,5 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_kron3.py tests/test_gpu_parity.py -q -x > gpurun_out/k3_pytest.log 2>&1
+echo "rc=$?" >> gpurun_out/k3_pytest.log
+timeout 600 python tools/kron_sweep.py 'KS_KRON3=0' 'KS_KRON3=1' 'KS_KRON3_TX=4' > gpurun_out/k3_sweep.log 2>&1
