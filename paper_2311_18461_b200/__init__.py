@@ -25,7 +25,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libks.so")
+LIB_PATH = os.environ.get("KS_LIB_PATH") or os.path.join(_HERE, "libks.so")  # override: experiment builds
 
 KS_OK, KS_EINVAL, KS_ESINGULAR, KS_ECUDA, KS_ENOMEM, KS_ENCCL, KS_ELENGTH = range(7)
 KS_MEM_HOST, KS_MEM_DEVICE = 0, 1

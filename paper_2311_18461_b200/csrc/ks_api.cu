@@ -85,15 +85,18 @@ struct ks_fd {
     DevBuf s0, s1, io;
     cudaStream_t stream = nullptr;
     // asynchronous host-pointer applies (caller stream given): H2D, compute and
-    // D2H on three streams, two staging buffers, so consecutive applies overlap
-    // their copies in both directions with each other and with the compute
+    // D2H on three streams, kNSlot staging buffers, so consecutive applies
+    // overlap their copies in both directions with each other and with the
+    // compute. Three slots let the H2D of apply i+2 start while apply i's D2H
+    // still drains (two slots serialise H2D(i+2) behind D2H(i)).
+    static constexpr int kNSlot = 3;
     cudaStream_t h2d = nullptr, d2h = nullptr;
-    DevBuf pio[2];
-    cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+    DevBuf pio[kNSlot];
+    cudaEvent_t ev_in[kNSlot] = {}, ev_comp[kNSlot] = {}, ev_out[kNSlot] = {};
     int slot = 0;
     std::mutex mu;
     ~ks_fd() {
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < kNSlot; ++k) {
             if (ev_in[k]) cudaEventDestroy(ev_in[k]);
             if (ev_comp[k]) cudaEventDestroy(ev_comp[k]);
             if (ev_out[k]) cudaEventDestroy(ev_out[k]);
@@ -284,7 +287,7 @@ void fd_apply_any(ks_fd* f, const ks_c64* r, ks_c64* z, int mem, void* stream, b
         if (!f->h2d) {
             KS_CUDA(cudaStreamCreateWithFlags(&f->h2d, cudaStreamNonBlocking));
             KS_CUDA(cudaStreamCreateWithFlags(&f->d2h, cudaStreamNonBlocking));
-            for (int k = 0; k < 2; ++k) {
+            for (int k = 0; k < ks_fd::kNSlot; ++k) {
                 KS_CUDA(cudaEventCreateWithFlags(&f->ev_in[k], cudaEventDisableTiming));
                 KS_CUDA(cudaEventCreateWithFlags(&f->ev_comp[k], cudaEventDisableTiming));
                 KS_CUDA(cudaEventCreateWithFlags(&f->ev_out[k], cudaEventDisableTiming));
@@ -293,7 +296,7 @@ void fd_apply_any(ks_fd* f, const ks_c64* r, ks_c64* z, int mem, void* stream, b
             }
         }
         const int k = f->slot;
-        f->slot ^= 1;
+        f->slot = (f->slot + 1) % ks_fd::kNSlot;
         cudaStream_t us = static_cast<cudaStream_t>(stream);
         double2* buf = f->pio[k].as<double2>();
         KS_CUDA(cudaStreamWaitEvent(f->h2d, f->ev_out[k], 0));

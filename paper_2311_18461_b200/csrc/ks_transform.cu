@@ -305,6 +305,8 @@ constexpr int kStages = 4;
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, bool valid) {
     const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
     const int sz = valid ? 16 : 0; // src-size 0 -> zero fill
+    // .cg: measured faster than .ca (c3 transforms 0.849 vs 0.886 ms) although
+    // .ca removes the duplicate L2 sector reads of the misaligned rows
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gsrc), "r"(sz));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
