@@ -28,6 +28,7 @@
 #include <cstring>
 #include <map>
 #include <numeric>
+#include <cmath>
 #include <cstdlib>
 
 namespace ks {
@@ -349,15 +350,94 @@ KronPlan* kron_plan(const std::vector<int>& dims,
         }
         return (int)m.size();
     };
+    // Rank-revealing merge of the boundary after the switch pass s: the suffix
+    // nodes q there receive sum_{(in, f)} C[q][(in, f)] F_f(in) from pass s.
+    // Nodes whose rows C[q] are proportional (C[q] = scale_q * R_g) become one
+    // intermediate U_g = sum R_g[(in, f)] F_f(in), and the pass after the
+    // switch reads scale_q * U_g. For the system operator at d = 3 the 6
+    // suffix classes (f2, f3) collapse to 3 (rank of C; e.g. (L,M) and (M,L)
+    // get the same row from the W and the cross terms), so the fused pass
+    // pairs write / read 3 intermediate tensors instead of 6.
+    const bool merge_rows = [] {
+        const char* e = std::getenv("KS_KRON_RANK");
+        return !(e && std::strcmp(e, "0") == 0);
+    }();
+    auto merge_boundary = [&](int s, const std::vector<int>& nin, const std::vector<int>& nout, int nq,
+                              std::vector<int>& grp, std::vector<double2>& scale, std::vector<char>& is_rep) -> int {
+        grp.resize(nq);
+        scale.assign(nq, make_double2(1.0, 0.0));
+        is_rep.assign(nq, 1);
+        for (int q = 0; q < nq; ++q) grp[q] = q;
+        if (!merge_rows || s + 1 >= L || nq <= 1) return nq;
+        std::vector<std::map<std::pair<int, int>, double2>> row(nq);
+        for (int t = 0; t < T; ++t) {
+            auto& e = row[nout[t]][std::make_pair(nin[t], fids[t][ax[s]])];
+            e.x += coeffs[t].x;
+            e.y += coeffs[t].y;
+        }
+        auto cdivd = [](double2 a, double2 b) {
+            const double den = b.x * b.x + b.y * b.y;
+            return make_double2((a.x * b.x + a.y * b.y) / den, (a.y * b.x - a.x * b.y) / den);
+        };
+        std::vector<int> rep; // representative node of each group
+        int ng = 0;
+        for (int q = 0; q < nq; ++q) {
+            if (row[q].empty()) continue;
+            const double2 lead = row[q].begin()->second;
+            if (lead.x == 0.0 && lead.y == 0.0) continue;
+            int found = -1;
+            for (int g = 0; g < ng && found < 0; ++g) {
+                const auto& r0 = row[rep[g]];
+                if (r0.size() != row[q].size()) continue;
+                const double2 l0 = r0.begin()->second;
+                const double2 sc = cdivd(lead, l0); // row q = sc * row rep
+                bool same = true;
+                const auto& rq = row[q];
+                auto jt = r0.begin();
+                for (auto it = rq.begin(); it != rq.end() && same; ++it, ++jt) {
+                    if (it->first != jt->first) {
+                        same = false;
+                        break;
+                    }
+                    const double2 v = jt->second;
+                    const double2 pr = make_double2(sc.x * v.x - sc.y * v.y, sc.x * v.y + sc.y * v.x);
+                    const double mag = std::max(std::hypot(it->second.x, it->second.y), std::hypot(pr.x, pr.y));
+                    same = std::hypot(it->second.x - pr.x, it->second.y - pr.y) <= 1e-12 * mag;
+                }
+                if (same) {
+                    found = g;
+                    scale[q] = sc;
+                    is_rep[q] = 0;
+                }
+            }
+            if (found < 0) {
+                rep.push_back(q);
+                found = ng++;
+            }
+            grp[q] = found;
+        }
+        // nodes with an all-zero row keep their own group (nothing flows in)
+        for (int q = 0; q < nq; ++q)
+            if (row[q].empty() || (row[q].begin()->second.x == 0.0 && row[q].begin()->second.y == 0.0)) grp[q] = ng++;
+        return ng;
+    };
     int best_s = 0;
     long best_cost = -1;
     for (int s = 0; s < L; ++s) {
         long cost = 0;
         std::vector<int> tmp;
         std::vector<int> cnt(L + 1);
-        for (int b = 0; b <= L; ++b) cnt[b] = boundary_nodes(s, b, tmp);
+        std::vector<std::vector<int>> nb(L + 1);
+        for (int b = 0; b <= L; ++b) cnt[b] = boundary_nodes(s, b, nb[b]);
         cnt[0] = 1;
         cnt[L] = 1;
+        if (s + 1 < L) {
+            std::vector<int> g;
+            std::vector<double2> sc;
+            std::vector<char> rp;
+            std::vector<int> n0(T, 0);
+            cnt[s + 1] = merge_boundary(s, s == 0 ? n0 : nb[s], nb[s + 1], cnt[s + 1], g, sc, rp);
+        }
         for (int k = 0; k < L; ++k) cost += cnt[k] + cnt[k + 1];
         if (best_cost < 0 || cost < best_cost) {
             best_cost = cost;
@@ -374,6 +454,21 @@ KronPlan* kron_plan(const std::vector<int>& dims,
         node_of[0][t] = 0;
         node_of[L][t] = 0;
     }
+    // merged boundary after the switch pass: node -> group, with the scale the
+    // following pass applies
+    std::vector<double2> tscale(T, make_double2(1.0, 0.0));
+    std::vector<char> tsrc(T, 1); // term feeds its merged node in the switch pass (representative rows only)
+    if (s + 1 < L) {
+        std::vector<int> g;
+        std::vector<double2> sc;
+        std::vector<char> rp;
+        cnt[s + 1] = merge_boundary(s, node_of[s], node_of[s + 1], cnt[s + 1], g, sc, rp);
+        for (int t = 0; t < T; ++t) {
+            tscale[t] = sc[node_of[s + 1][t]];
+            tsrc[t] = rp[node_of[s + 1][t]];
+            node_of[s + 1][t] = g[node_of[s + 1][t]];
+        }
+    }
     P->nnodes = 0;
     for (int b = 1; b < L; ++b) P->nnodes += cnt[b];
 
@@ -385,8 +480,18 @@ KronPlan* kron_plan(const std::vector<int>& dims,
         // (out, in, factor) -> coeff
         std::map<std::tuple<int, int, int>, double2> acc;
         for (int t = 0; t < T; ++t) {
+            if (k == s && !tsrc[t]) continue; // merged node: defined by its representative's row
             const int in = node_of[k][t], out = node_of[k + 1][t], f = fids[t][ax[k]];
-            double2 c = (k == s) ? coeffs[t] : make_double2(1.0, 0.0);
+            // switch pass: the term's coefficient over its merged node's scale;
+            // the pass after it: the scale (one value per (out, in, f): see above)
+            double2 c = make_double2(1.0, 0.0);
+            if (k == s) {
+                const double2 a = coeffs[t], b = tscale[t];
+                const double den = b.x * b.x + b.y * b.y;
+                c = make_double2((a.x * b.x + a.y * b.y) / den, (a.y * b.x - a.x * b.y) / den);
+            } else if (k == s + 1) {
+                c = tscale[t];
+            }
             auto key = std::make_tuple(out, in, f);
             auto it = acc.find(key);
             if (it == acc.end()) {

@@ -14,6 +14,12 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-10
 
 
+@pytest.fixture(autouse=True)
+def _two_launch_path(monkeypatch):
+    # the two-launch path is opt-in (the rank-merged pass pairs are faster at c3)
+    monkeypatch.setenv("KS_KRON3", "1")
+
+
 @pytest.mark.parametrize("p,n_el,n_el_t", [(2, 5, 5), (2, 9, 3), (3, 6, 7), (4, 5, 4), (2, 17, 2), (5, 6, 3)])
 def test_system_matvec_two_launch_path(gpu, oracle, p, n_el, n_el_t):
     a = setup_arrays(gpu, 3, p, n_el, n_el_t)
@@ -46,6 +52,7 @@ def test_equals_level_pass_plan(gpu, oracle, monkeypatch):
     y3 = gpu.assemble_system_operator(a["prob"]).apply(x)
     monkeypatch.setenv("KS_KRON3", "0")
     monkeypatch.setenv("KS_KRON_MERGE", "0")
+    monkeypatch.setenv("KS_KRON_RANK", "0")
     A0 = gpu.assemble_system_operator(a["prob"])
     assert A0.plan_info()["engine"] != "axis3_then_fused_t12"
     assert rel(y3, A0.apply(x)) <= 1e-13
@@ -93,6 +100,51 @@ def test_sign_merged_factors(gpu, oracle):
     K = gpu.KroneckerOperator(dims)
     for c, fs, bw in terms:
         K.add_term(c, [None if f is None else gpu.Banded(dims[k], bw[k], f.astype(complex)) for k, f in enumerate(fs)])
+    x = rng.standard_normal(np.prod(dims)) + 1j * rng.standard_normal(np.prod(dims))
+    yd = oracle.kron_to_dense(dims, terms) @ x
+    assert np.max(np.abs(K.apply(x) - yd)) <= 1e-12 * np.max(np.abs(yd))
+
+
+def test_rank_merged_plan_matches_oracle(gpu, oracle, monkeypatch):
+    """Default matvec plan (fused pass pairs over the rank-merged boundary:
+    proportional coefficient rows share one intermediate) against the oracle,
+    and against the plan without the merge."""
+    monkeypatch.setenv("KS_KRON3", "0")
+    for p, n_el, n_el_t in [(2, 9, 5), (3, 6, 4), (4, 5, 3)]:
+        a = setup_arrays(gpu, 3, p, n_el, n_el_t)
+        A = gpu.assemble_system_operator(a["prob"])
+        info = A.plan_info()
+        assert info["nodes"] == 9 and info["engine"] != "axis3_then_fused_t12"
+        K = oracle.OracleKron(a["dims"], oracle.system_terms(a, 3, a["nu"]))
+        x = oracle.random_vec(K.N, 13)
+        y, yo = A.apply(x), K.apply(x)
+        assert rel(y, yo) <= TOL and maxrel(y, yo) <= TOL
+    monkeypatch.setenv("KS_KRON_RANK", "0")
+    A0 = gpu.assemble_system_operator(a["prob"])
+    assert A0.plan_info()["nodes"] == 12
+    assert rel(A0.apply(x), y) <= 1e-13
+
+
+def test_rank_merge_complex_scales_vs_dense(gpu, oracle, monkeypatch):
+    """Generic term list whose middle-boundary rows are proportional with
+    complex ratios (and one that is not): the merged plan must equal the dense
+    Kronecker sum (tensorops.cpp:277-301)."""
+    monkeypatch.setenv("KS_KRON3", "0")
+    rng = np.random.default_rng(21)
+    dims = [4, 5, 3, 6]
+
+    def band(n, bw):
+        return rng.standard_normal((2 * bw + 1) * n) + 1j * rng.standard_normal((2 * bw + 1) * n)
+    A0, B0, B1 = band(4, 1), band(5, 2), band(5, 1)
+    C0, D0, C1, D1, C2 = band(3, 1), band(6, 2), band(3, 0), band(6, 1), band(3, 1)
+    terms = [(1.5, [A0, B0, C0, D0], [1, 2, 1, 2]),
+             (0.5 - 1.0j, [A0, B1, C0, D0], [1, 1, 1, 2]),
+             (3.0j, [A0, B0, C1, D1], [1, 2, 0, 1]),           # row of (C1, D1) = 2j * row of (C0, D0)
+             ((0.5 - 1.0j) * 2.0j, [A0, B1, C1, D1], [1, 1, 0, 1]),
+             (-2.0, [None, B0, C2, None], [0, 2, 1, 0])]      # not proportional
+    K = gpu.KroneckerOperator(dims)
+    for c, fs, bw in terms:
+        K.add_term(c, [None if f is None else gpu.Banded(dims[k], bw[k], f) for k, f in enumerate(fs)])
     x = rng.standard_normal(np.prod(dims)) + 1j * rng.standard_normal(np.prod(dims))
     yd = oracle.kron_to_dense(dims, terms) @ x
     assert np.max(np.abs(K.apply(x) - yd)) <= 1e-12 * np.max(np.abs(yd))
