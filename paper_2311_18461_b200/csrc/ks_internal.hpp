@@ -178,7 +178,9 @@ struct KronJitPair;
 // null when the shape is unsupported or KS_KRON_JIT=0
 KronJitPair* kron_jit_build(int nin, int nmid, int nout, int bw, const std::vector<JitContrib>& a,
                             const std::vector<JitContrib>& b, const std::vector<int>& freal,
-                            const std::vector<double2>& coeffs, long long s_a, int n_a, int n_b, long long n_outer);
+                            const std::vector<double2>& coeffs, long long s_a, int n_a, int n_b, long long n_outer,
+                            int tmax_default = 384);
+bool kron_jit_same_shape(const KronJitPair& A, const KronJitPair& B);
 bool kron_jit_launch(const KronJitPair& J, const double2* const* ip, double2* const* op, void* const* hin,
                      void* const* hout, const double2* rb, int nmax, cudaStream_t st);
 void kron_jit_free(KronJitPair* p);

@@ -91,6 +91,10 @@ struct KronPlan {
     DevBuf d_rowband, d_freal; // v3: rb[f][r][dj] (width 2*bwmax+1), is_real[f]
     // plan-specialised fused pass pairs (k, k+1), indexed by k (null = none)
     std::vector<std::unique_ptr<KronJitPair, KronJitDeleter>> jit;
+    // alternative block shapes of each fused pair, timed once on the first
+    // apply (the faster one replaces jit[k]); the best shape differs between
+    // sizes (c3: 160-thread blocks 0.81 ms vs 352 0.87; c5: 288 beats 160)
+    std::vector<std::vector<std::unique_ptr<KronJitPair, KronJitDeleter>>> jit_alt;
     // d = 3: axis 3 then axes t/1/2 fused (ks_kron3.cu); null = level passes
     std::unique_ptr<Kron3, Kron3Deleter> k3;
 };
@@ -560,6 +564,7 @@ KronPlan* kron_plan(const std::vector<int>& dims,
         KS_CUDA(cudaMemcpy(P->d_freal.p, freal.data(), freal.size() * sizeof(int), cudaMemcpyHostToDevice));
         // fused pass pairs (0,1), (2,3), ... specialised with NVRTC
         P->jit.resize(P->passes.size());
+        P->jit_alt.resize(P->passes.size());
         // factor classes: 1 real, 2 purely imaginary (e.g. W + W^H), 0 complex
         std::vector<int> frv(P->factors.size());
         for (size_t f = 0; f < P->factors.size(); ++f) {
@@ -589,6 +594,14 @@ KronPlan* kron_plan(const std::vector<int>& dims,
             const long long outer = (long long)(P->N / (sa * (size_t)na * (size_t)nbb));
             P->jit[k].reset(kron_jit_build(pa.n_in, pa.n_out, pb.n_out, P->bwmax, ca, cb, frv, co, (long long)sa, na,
                                            nbb, outer));
+            if (P->jit[k] && !std::getenv("KS_KRON_JIT_MAXT"))
+                for (int tm : {192, 128}) {
+                    std::unique_ptr<KronJitPair, KronJitDeleter> alt(kron_jit_build(
+                        pa.n_in, pa.n_out, pb.n_out, P->bwmax, ca, cb, frv, co, (long long)sa, na, nbb, outer, tm));
+                    bool dup = !alt || kron_jit_same_shape(*alt, *P->jit[k]);
+                    for (auto& o : P->jit_alt[k]) dup = dup || kron_jit_same_shape(*alt, *o);
+                    if (!dup) P->jit_alt[k].push_back(std::move(alt));
+                }
         }
     }
     {
@@ -711,6 +724,36 @@ void kron_apply(KronPlan& P, const double2* x, double2* y, cudaStream_t st,
             const KronPass& nx = P.passes[k + 1];
             auto ip = reinterpret_cast<const double2* const*>(dp + P.ptr_off[k]);
             auto op = reinterpret_cast<double2* const*>(const_cast<void**>(dp + P.ptr_off[k + 1] + nx.n_in));
+            if (k < P.jit_alt.size() && !P.jit_alt[k].empty()) {
+                // first apply: time the current shape and the alternatives once, keep the fastest
+                auto time_one = [&](KronJitPair& J) {
+                    cudaEvent_t a, b;
+                    KS_CUDA(cudaEventCreate(&a));
+                    KS_CUDA(cudaEventCreate(&b));
+                    KS_CUDA(cudaEventRecord(a, st));
+                    const bool ok = kron_jit_launch(J, ip, op, host_ptrs.data() + P.ptr_off[k],
+                                                    host_ptrs.data() + P.ptr_off[k + 1] + nx.n_in,
+                                                    P.d_rowband.as<double2>(), P.nmax, st);
+                    KS_CUDA(cudaEventRecord(b, st));
+                    KS_CUDA(cudaEventSynchronize(b));
+                    float ms = 0.f;
+                    KS_CUDA(cudaEventElapsedTime(&ms, a, b));
+                    cudaEventDestroy(a);
+                    cudaEventDestroy(b);
+                    return ok ? ms : 1e30f;
+                };
+                time_one(*P.jit[k]); // warm-up launches (lazy module loading, L2)
+                for (auto& alt : P.jit_alt[k]) time_one(*alt);
+                float best = time_one(*P.jit[k]);
+                for (auto& alt : P.jit_alt[k]) {
+                    const float t = time_one(*alt);
+                    if (t < best) {
+                        best = t;
+                        std::swap(P.jit[k], alt);
+                    }
+                }
+                P.jit_alt[k].clear();
+            }
             if (kron_jit_launch(*P.jit[k], ip, op, host_ptrs.data() + P.ptr_off[k],
                                 host_ptrs.data() + P.ptr_off[k + 1] + nx.n_in, P.d_rowband.as<double2>(), P.nmax,
                                 st)) {

@@ -126,7 +126,8 @@ void kron_jit_free(KronJitPair* p) { delete p; }
 // the order a then b (indices in JitContrib::coeff).
 KronJitPair* kron_jit_build(int nin, int nmid, int nout, int bw, const std::vector<JitContrib>& a,
                             const std::vector<JitContrib>& b, const std::vector<int>& freal,
-                            const std::vector<double2>& coeffs, long long s_a, int n_a, int n_b, long long n_outer) {
+                            const std::vector<double2>& coeffs, long long s_a, int n_a, int n_b, long long n_outer,
+                            int tmax_default) {
     if (const char* e = std::getenv("KS_KRON_JIT"))
         if (std::strcmp(e, "0") == 0) return nullptr;
     if (nin < 1 || nmid < 1 || nout < 1 || bw < 1 || bw > 6 || nin > 16 || nmid > 16 || nout > 16) return nullptr;
@@ -139,7 +140,7 @@ KronJitPair* kron_jit_build(int nin, int nmid, int nout, int bw, const std::vect
     // size rounded to whole warps; pick the fullest block of at most 384 threads
     int c_best = 1, T_best = 0;
     double e_best = -1;
-    const int tmax = std::getenv("KS_KRON_JIT_MAXT") ? std::atoi(std::getenv("KS_KRON_JIT_MAXT")) : 384;
+    const int tmax = std::getenv("KS_KRON_JIT_MAXT") ? std::atoi(std::getenv("KS_KRON_JIT_MAXT")) : tmax_default;
     for (int c = 1; c * n_a <= tmax; ++c) {
         if (s_a > 1 && c > s_a) break;
         if (s_a == 1 && c > n_outer) break;
@@ -454,6 +455,9 @@ static int sm_count() {
 // each CTA sweeps the whole axis b serially: too few CTAs leave the GPU idle
 // (c2: 22 CTAs, 0.23 ms vs 0.064 ms for the per-pass kernels)
 bool kron_jit_runs(const KronJitPair& J) { return J.grid >= (unsigned)sm_count(); }
+bool kron_jit_same_shape(const KronJitPair& A, const KronJitPair& B) {
+    return A.T == B.T && A.nq == B.nq && A.no == B.no && A.D == B.D;
+}
 
 // launch over the plan's tensors (geometry fixed at build); false when the
 // grid is too small to fill the GPU (the caller runs the passes separately)
