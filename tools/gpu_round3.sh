@@ -12,6 +12,6 @@ python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-solve > gpurun_out/b
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-solve > gpurun_out/ncu_launch.log 2>&1
 python tools/prof_c3.py c3 > gpurun_out/prof_plain.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_mode_gemm_fold|k_fd_solve_pair|ks_k3|k_axis3" -c 10 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_mode_gemm_fold|k_fd_solve_pair|ks_pair" -c 12 \
     -o gpurun_out/prof_top python tools/prof_c3.py c3 > gpurun_out/ncu_top.log 2>&1
 echo "done" >> gpurun_out/ncu_top.log
