@@ -95,6 +95,8 @@ struct KronPlan {
     // apply (the faster one replaces jit[k]); the best shape differs between
     // sizes (c3: 160-thread blocks 0.81 ms vs 352 0.87; c5: 288 beats 160)
     std::vector<std::vector<std::unique_ptr<KronJitPair, KronJitDeleter>>> jit_alt;
+    // device pointer tables per (x, y) pair (kron_apply)
+    std::map<std::pair<const void*, void*>, DevBuf> ptr_tables;
     // d = 3: axis 3 then axes t/1/2 fused (ks_kron3.cu); null = level passes
     std::unique_ptr<Kron3, Kron3Deleter> k3;
 };
@@ -709,9 +711,20 @@ void kron_apply(KronPlan& P, const double2* x, double2* y, cudaStream_t st,
         for (int i = 0; i < ps.n_in; ++i) host_ptrs[w++] = ps.in_pool < 0 ? (void*)x : pool_ptr(ps.in_pool, i);
         for (int i = 0; i < ps.n_out; ++i) host_ptrs[w++] = ps.out_pool < 0 ? (void*)y : pool_ptr(ps.out_pool, i);
     }
-    KS_CUDA(cudaMemcpyAsync(P.d_ptrs.p, host_ptrs.data(), total * sizeof(void*),
-                            cudaMemcpyHostToDevice, st));
-    const void* const* dp = static_cast<const void* const*>(P.d_ptrs.p);
+    // one device copy of the table per (x, y) pair, uploaded on first use: later
+    // applies with the same vectors issue no host->device copy (so a CUDA graph
+    // can capture them, ks_pcg)
+    auto key = std::make_pair((const void*)x, (void*)y);
+    auto it = P.ptr_tables.find(key);
+    if (it == P.ptr_tables.end()) {
+        if (P.ptr_tables.size() >= 4096) { // bounded: callers cycling through many vectors
+            KS_CUDA(cudaStreamSynchronize(st));
+            P.ptr_tables.clear();
+        }
+        it = P.ptr_tables.emplace(key, DevBuf(std::max<size_t>(total, 1) * sizeof(void*))).first;
+        KS_CUDA(cudaMemcpyAsync(it->second.p, host_ptrs.data(), total * sizeof(void*), cudaMemcpyHostToDevice, st));
+    }
+    const void* const* dp = static_cast<const void* const*>(it->second.p);
     for (size_t k = 0; k < P.passes.size(); ++k) {
         const KronPass& ps = P.passes[k];
         size_t s = 1;
@@ -837,6 +850,10 @@ void kron_apply(KronPlan& P, const double2* x, double2* y, cudaStream_t st,
 }
 
 void kron_plan_free(KronPlan* p) { delete p; }
+
+bool kron_has_table(const KronPlan& P, const void* x, const void* y) {
+    return P.ptr_tables.count(std::make_pair(x, const_cast<void*>(y))) > 0 || (P.k3 && P.shard_rows == 0);
+}
 
 void kron_plan_set_shard(KronPlan& P, int rows, int in_off, int band_off) {
     P.shard_rows = rows;

@@ -234,3 +234,19 @@ def test_c3_full_size_properties(gpu, oracle):
     PAu = P.apply(gpu.DeviceVector.from_host(Au)).to_host()
     ratio = np.vdot(uh, PAu).real / np.vdot(uh, uh).real
     assert 0.1 < ratio < 10
+
+
+def test_pcg_graph_replay_matches_eager(gpu, oracle, monkeypatch):
+    """Iteration phases replayed as CUDA graphs (KS_PCG_GRAPH=1) run the same
+    kernels in the same order: identical iterates, counts and histories."""
+    a = setup_arrays(gpu, 3, 2, 6, 5)
+    b = oracle.random_vec(a["prob"].N_dof, 17)
+    reps = []
+    for g in ("0", "1"):
+        monkeypatch.setenv("KS_PCG_GRAPH", g)
+        A = gpu.assemble_system_operator(a["prob"])
+        P = gpu.FDPreconditioner(a["prob"])
+        reps.append(gpu.pcg(A, P, b, gpu.PcgOptions(1e-10, 100)))
+    assert reps[0].iterations == reps[1].iterations and reps[0].converged and reps[1].converged
+    assert np.array_equal(np.asarray(reps[0].x), np.asarray(reps[1].x))
+    assert list(reps[0].res_history) == list(reps[1].res_history)
