@@ -350,22 +350,22 @@ __device__ __forceinline__ void cpa4(void* sdst, const void* g, bool v) {
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N> __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-template <int P, int D>
-__global__ void __launch_bounds__(128) k_fd_solve_ring(const double2* __restrict__ ab,
+template <int P, int D, int TB = 128>
+__global__ void __launch_bounds__(TB) k_fd_solve_ring(const double2* __restrict__ ab,
                                                        const unsigned char* __restrict__ piv,
                                                        double2* __restrict__ X, size_t ns, int nt, size_t nblk,
                                                        const int* __restrict__ fblk, int rec, int fnd,
                                                        long long fnp) {
     constexpr int ldab = 3 * P + 1, kuf = 2 * P, NE = 2 * P + 2;
-    extern __shared__ __align__(16) double2 ring[]; // [D][NE][128], then int [D][128]
-    unsigned* pr = reinterpret_cast<unsigned*>(ring + (size_t)D * NE * 128);
+    extern __shared__ __align__(16) double2 ring[]; // [D][NE][TB], then int [D][TB]
+    unsigned* pr = reinterpret_cast<unsigned*>(ring + (size_t)D * NE * TB);
     const int t = threadIdx.x;
-    const size_t f = blockIdx.x * (size_t)128 + t;
+    const size_t f = blockIdx.x * (size_t)TB + t;
     if (f >= ns) return;
     double2* x = X + f; // x[k * ns]
     const size_t i = fblk ? (size_t)__ldg(fblk + f) : f;
     const BandIndex bx = fd_band_index(i, nt, ldab, nblk, rec, fnd, fnp);
-    auto slot = [&](int k, int e) -> double2* { return ring + ((size_t)((k % D) * NE + e) * 128 + t); };
+    auto slot = [&](int k, int e) -> double2* { return ring + ((size_t)((k % D) * NE + e) * TB + t); };
     auto baddr = [&](int k, int e) -> const double2* { return ab + bx.fb + (size_t)k * bx.fk + (size_t)e * bx.fe; };
     // pivot of step k: byte (or record slot) -> 4 B word in the ring
     auto issue_f = [&](int k) {
@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(128) k_fd_solve_ring(const double2* __restrict
                 cpa16(slot(k, P + 1), baddr(k, ldab), true);
             } else {
                 const size_t o = bx.pb + (size_t)k * bx.pk;
-                cpa4(pr + (k % D) * 128 + t, piv + (o & ~(size_t)3), true);
+                cpa4(pr + (k % D) * TB + t, piv + (o & ~(size_t)3), true);
             }
         }
         cpa_commit();
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(128) k_fd_solve_ring(const double2* __restrict
     auto pivot_of = [&](int k) -> int {
         if (rec > 0) return (int)slot(k, P + 1)->x;
         const size_t o = bx.pb + (size_t)k * bx.pk;
-        return (int)((pr[(k % D) * 128 + t] >> (8 * (unsigned)(o & 3))) & 0xffu);
+        return (int)((pr[(k % D) * TB + t] >> (8 * (unsigned)(o & 3))) & 0xffu);
     };
     // forward: L with row interchanges (eigensolve.cpp:127-133); w[m] = x[k+m]
     double2 w[P + 1];
@@ -433,7 +433,11 @@ __global__ void __launch_bounds__(128) k_fd_solve_ring(const double2* __restrict
         cpa_wait<D - 2>();
         issue_b(k - (D - 1));
         // slot index of step k: use (nt-1-k) so the ring advances monotonically
-        u[0] = cdiv(u[0], *slot(k, 0));
+        { // reciprocal conj(d)/|d|^2: one division on the step's latency chain instead of Smith's three
+            const double2 dg = *slot(k, 0);
+            const double sc = 1.0 / fma(dg.x, dg.x, dg.y * dg.y);
+            u[0] = cmul(u[0], make_double2(dg.x * sc, -dg.y * sc));
+        }
 #pragma unroll
         for (int j = 1; j <= 2 * P; ++j)
             if (k - j >= 0) u[j] = csub(u[j], cmul(*slot(k, j), u[0]));
@@ -863,14 +867,24 @@ void launch_solve_p(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t st
         }();
         if (tm && (ring == 4 || ring == 8)) {
             constexpr int NE = 2 * P + 2;
-            auto go = [&](auto kern, int D) {
-                const size_t sm = (size_t)D * NE * 128 * sizeof(double2) + (size_t)D * 128 * sizeof(unsigned);
+            auto go = [&](auto kern, int D, int tb) {
+                const size_t sm = (size_t)D * NE * tb * sizeof(double2) + (size_t)D * tb * sizeof(unsigned);
                 KS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-                kern<<<grid, 128, sm, st>>>(B.ab.as<double2>(), B.piv.as<unsigned char>(), X, B.ns, B.nt, B.nblk,
-                                            B.fiber_block.as<int>(), B.rec, B.fused_nd, B.fused_np);
+                const unsigned g = (unsigned)((B.ns + tb - 1) / tb);
+                kern<<<g, tb, sm, st>>>(B.ab.as<double2>(), B.piv.as<unsigned char>(), X, B.ns, B.nt, B.nblk,
+                                        B.fiber_block.as<int>(), B.rec, B.fused_nd, B.fused_np);
             };
-            if (ring == 8) go(k_fd_solve_ring<P, 8>, 8);
-            else go(k_fd_solve_ring<P, 4>, 4);
+            // few fibers (c1, c2: < 2 x 148 CTAs of 128): one warp per CTA spreads
+            // them over all SMs, and an 8-deep ring keeps more steps in flight
+            static int sms = 0;
+            if (!sms) {
+                int dev = 0;
+                KS_CUDA(cudaGetDevice(&dev));
+                KS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            }
+            if (grid < (unsigned)(2 * sms)) go(k_fd_solve_ring<P, 8, 32>, 8, 32);
+            else if (ring == 8) go(k_fd_solve_ring<P, 8>, 8, 128);
+            else go(k_fd_solve_ring<P, 4>, 4, 128);
             check_launch("k_fd_solve_ring");
             return;
         }

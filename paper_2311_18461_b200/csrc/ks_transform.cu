@@ -1013,6 +1013,23 @@ void launch_fold_th(const FoldAxis& F, const double* X, double* Y, const ColMap&
             return launch_fold_cfg<TH, INV, 16, 2, 2, 64, true>(F, X, Y, M, st);
         return launch_fold_cfg<TH, INV, 16, 2, 2, 64>(F, X, Y, M, st);
     }
+    // small problems (c1, c2: fewer 64-column tiles than SMs): 32-column tiles
+    // give twice the CTAs
+    {
+        static int sms = 0;
+        if (!sms) {
+            int dev = 0;
+            KS_CUDA(cudaGetDevice(&dev));
+            KS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        }
+        if (M.mode == MAP_STD && !M.rin && !M.rout && (M.Q + 63) / 64 < sms) {
+            constexpr int Hs = 16 * TH;
+            const int nkc8 = (F.hc + 7) / 8;
+            const size_t sm32 = (size_t)2 * nkc8 * 8 * (Hs + 4) * sizeof(double) + (size_t)2 * Hs * sizeof(int) +
+                                (size_t)4 * 16 * (64 + 4) * sizeof(double);
+            if (sm32 <= 227 * 1024) return launch_fold_cfg<TH, INV, 8, 4, 1, 32>(F, X, Y, M, st);
+        }
+    }
     // long axes: resident halves are large -> 1 CTA/SM; 2 stages when 4 do not fit
     constexpr int H = 16 * TH;
     const int nkc = (F.hc + 7) / 8;
