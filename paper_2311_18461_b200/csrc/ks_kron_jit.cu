@@ -215,6 +215,11 @@ KronJitPair* kron_jit_build(int nin, int nmid, int nout, int bw, const std::vect
     s << "// generated: fused level passes (ks_kron_jit.cu)\n"
       << "#define BW " << bw << "\n#define W " << W << "\n#define NIN " << nin << "\n#define T " << T
       << "\n#define RS " << RS << "\n#define PAD " << pad << "\n"
+      // the plan's geometry as literals: the sweep's ring index, plane strides and
+      // output offsets become constant arithmetic (the run-time values are only
+      // kept in the signature; ncu showed IMAD / I2F division sequences per plane)
+      << "#define s_a " << s_a << "LL\n#define n_a " << n_a << "\n#define n_b " << n_b << "\n#define n_outer " << n_outer
+      << "LL\n#define nq " << nq << "\n#define no " << no << "\n#define D " << D << "\n"
       << "struct Coef { double2 c[" << std::max<size_t>(1, coeffs.size()) << "]; const double2* in[" << nin
       << "]; double2* out[" << nout << "]; };\n"
       << R"(
@@ -228,7 +233,8 @@ __device__ __forceinline__ void cp16(void* sdst, const void* g, bool v) {
 }
 extern "C" __global__ void __launch_bounds__(T, )" << (minb_env > 0 ? minb_env : minb) << R"()
 ks_pair(const double2* const* __restrict__ ip, double2* const* __restrict__ op, const double2* __restrict__ rb,
-        int nmax, long long s_a, int n_a, int n_b, long long n_outer, int nq, int no, int D, const Coef P) {
+        int nmax, long long s_a_rt, int n_a_rt, int n_b_rt, long long n_outer_rt, int nq_rt, int no_rt, int D_rt,
+        const Coef P) {
     extern __shared__ __align__(16) double2 ring[]; // [D][NIN][RS]: halo | T points | halo
     const int tid = threadIdx.x;
     const long long nqb = (s_a + nq - 1) / nq;
