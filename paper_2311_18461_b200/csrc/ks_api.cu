@@ -80,6 +80,7 @@ struct ks_fd {
     std::vector<int> fiber_block; // host copy of the block map (empty = identity)
     bool fused = false;           // outermost axis via k_fd_fused
     bool fuse12 = false;          // axes 1+2 via k_fold12 (KS_FD_FUSE12=1 at creation)
+    bool tm1 = false;             // time-major hand-off on axis 1 (pair mode, folded axis 1)
     int kind = 0;                 // 0: least-squares blocks, 1: Galerkin blocks (galerkin_fast_solver)
     DevBuf Lt, Mt, Wsym;          // Wsym: W + W^H (least squares) or W itself (Galerkin)
     FdBlocks blocks;
@@ -236,8 +237,26 @@ void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStre
         const char* e = std::getenv("KS_FD_NAT");
         return e && std::strcmp(e, "1") == 0;
     }();
-    const bool nat = nat_ok && !adjoint && f->blocks.pair_n1 > 0 && f->blocks.rec == 0;
+    const bool nat = nat_ok && !adjoint && f->blocks.pair_n1 > 0 && f->blocks.rec == 0 && !f->tm1;
     const int tout = nat ? 0 : 1, tin = nat ? 0 : 2;
+    if (f->tm1) {
+        // forward axes d..1, the axis-1 transform writes the position-ordered
+        // time-major layout; solves; inverse axis 1 first, then 2..d
+        for (int l = d; l >= 1; --l) {
+            double* out = bufs[nb];
+            nb ^= 1;
+            gemm(f->At_fwd[l - 1], l, cur, out, l == 1 ? 3 : 0);
+            cur = out;
+        }
+        launch_fd_solve(f->blocks, reinterpret_cast<double2*>(const_cast<double*>(cur)), adjoint, st, true);
+        for (int l = 1; l <= d; ++l) {
+            double* out = l == d ? reinterpret_cast<double*>(z) : bufs[nb];
+            if (l != d) nb ^= 1;
+            gemm(f->At_inv[l - 1], l, cur, out, l == 1 ? 4 : 0);
+            cur = out;
+        }
+        return;
+    }
     for (int l = 1; l <= d; ++l) {
         double* out = bufs[nb];
         nb ^= 1;
@@ -479,8 +498,23 @@ static void fd_create_impl(int kind, int d, const int* dims, double nu, int p_t,
     bool pair = d == 3 && !fused && dims[2] == dims[3] &&
                 std::memcmp(lambda[1], lambda[2], sizeof(double) * dims[2]) == 0;
     if (const char* e = std::getenv("KS_FD_PAIR")) pair = pair && std::strcmp(e, "0") != 0;
+    // time-major hand-off on axis 1 (default for pair mode with a folded axis 1;
+    // KS_FD_TM1=0 off): forward transforms run axes d..1, the last one writes
+    // T[t][pos(i1) + n1*(i2 + n2*i3)] with the even eigen-indices of axis 1 at
+    // positions 0..hc-1 and the odd ones after them (FoldAxis::perm), so both
+    // time-major transforms move whole 1 KB rows; the blocks are numbered by
+    // position. NAT mode (natural-layout solve) and the fused paths keep the
+    // eigen-index order.
+    bool tm1 = pair && f->fold[0].n > 0 && !f->fuse12 && (int)f->fold[0].perm.size() == dims[1];
+    if (const char* e = std::getenv("KS_FD_TM1")) tm1 = tm1 && std::strcmp(e, "0") != 0;
+    if (const char* e = std::getenv("KS_FD_NAT")) tm1 = tm1 && std::strcmp(e, "1") != 0;
+    f->tm1 = tm1;
     if (pair) {
         const int n1 = dims[1], n2 = dims[2];
+        // position -> eigen-index of axis 1 (identity unless tm1), and its inverse
+        std::vector<int> perm1(n1), pos1(n1);
+        for (int p = 0; p < n1; ++p) perm1[p] = tm1 ? f->fold[0].perm[p] : p;
+        for (int p = 0; p < n1; ++p) pos1[perm1[p]] = p;
         std::vector<int2> prs;
         std::vector<int> pidx((size_t)n2 * n2);
         for (int i3 = 0; i3 < n2; ++i3)
@@ -490,17 +524,22 @@ static void fd_create_impl(int kind, int d, const int* dims, double nu, int p_t,
             }
         lam_blk.resize((size_t)n1 * prs.size());
         for (size_t pp = 0; pp < prs.size(); ++pp)
-            for (int i1 = 0; i1 < n1; ++i1) {
-                const int id[3] = {i1, prs[pp].x, prs[pp].y};
-                lam_blk[(size_t)i1 + (size_t)n1 * pp] = ref_sum(id);
+            for (int p1 = 0; p1 < n1; ++p1) {
+                const int id[3] = {perm1[p1], prs[pp].x, prs[pp].y};
+                lam_blk[(size_t)p1 + (size_t)n1 * pp] = ref_sum(id);
             }
+        // host map by natural fiber index (ks_fd_block); device map by layout
+        // position (time-major adjoint solves; natural order unless tm1)
         f->fiber_block.resize(f->Ns);
+        std::vector<int> fb_dev(f->Ns);
         for (size_t i = 0; i < f->Ns; ++i) {
             const int i1 = (int)(i % n1), i2 = (int)((i / n1) % n2), i3 = (int)(i / ((size_t)n1 * n2));
-            f->fiber_block[i] = i1 + n1 * pidx[(size_t)i2 * n2 + i3];
+            const int pb = n1 * pidx[(size_t)i2 * n2 + i3];
+            f->fiber_block[i] = pos1[i1] + pb;
+            fb_dev[i] = i1 + pb;
         }
         B.fiber_block.alloc(f->Ns * sizeof(int)); // adjoint / non-time-major solves
-        KS_CUDA(cudaMemcpy(B.fiber_block.p, f->fiber_block.data(), f->Ns * sizeof(int), cudaMemcpyHostToDevice));
+        KS_CUDA(cudaMemcpy(B.fiber_block.p, fb_dev.data(), f->Ns * sizeof(int), cudaMemcpyHostToDevice));
         B.pair_n1 = n1;
         B.pair_n2 = n2;
         B.pairs.alloc(prs.size() * sizeof(int2));
@@ -619,6 +658,7 @@ int ks_fd_info(const ks_fd* fd, int* folded_axes, size_t* blocks) {
     for (size_t l = 0; l < fd->fold.size(); ++l)
         if (fd->fold[l].n) m |= 1 << l;
     if (fd->fuse12 && !fd->fused) m |= 1 << 16;
+    if (fd->tm1) m |= 1 << 17;
     if (folded_axes) *folded_axes = m;
     if (blocks) *blocks = fd->blocks.nblk;
     API_END

@@ -127,7 +127,9 @@ void launch_fill_bytes(void* p, size_t bytes, cudaStream_t s);
 // At is A stored k-major: At[j*n + r] = A[r][j].
 // ---------------------------------------------------------------------------
 // layout: 0 natural in/out; 1 natural in -> time-major out T[t][i];
-//         2 time-major in -> natural out (1/2 need outer == 1; nt = time extent)
+//         2 time-major in -> natural out (1/2 need outer == 1; nt = time extent);
+//         3 / 4: the same hand-off on axis 1 (folded axes only, rows stored by
+//         position: FoldAxis::perm)
 // rows_in / rows_out (optional, device arrays of n pointers): row j of the input
 // / output is at rows_*[j] + column offset (rows on other GPUs, peer memory)
 void launch_mode_gemm(const double* At, int n, const double* X, double* Y,
@@ -142,6 +144,8 @@ struct FoldAxis {
     int kst = 0;               // stored k rows of each half matrix (zero padded)
     DevBuf fwd, inv;           // [2][Kp][16*th] symmetrised half matrices (even, odd), k-major
     DevBuf rmap;               // int [2][16*th]: even eigen-indices, odd eigen-indices
+    DevBuf rpos;               // int [2][16*th]: positions 0..hc-1, hc..n-1 (axis-1 time-major rows)
+    std::vector<int> perm;     // eigen-index stored at position p of the axis-1 time-major layout
 };
 // U column-major (U[j + r*n] = U(j, r)); false (F untouched) if not foldable
 // or KS_FD_FOLD=0
@@ -179,7 +183,7 @@ struct KronJitPair;
 KronJitPair* kron_jit_build(int nin, int nmid, int nout, int bw, const std::vector<JitContrib>& a,
                             const std::vector<JitContrib>& b, const std::vector<int>& freal,
                             const std::vector<double2>& coeffs, long long s_a, int n_a, int n_b, long long n_outer,
-                            int tmax_default = 384);
+                            int tmax_default = 384, int dmax = 4);
 bool kron_jit_same_shape(const KronJitPair& A, const KronJitPair& B);
 bool kron_jit_launch(const KronJitPair& J, const double2* const* ip, double2* const* op, void* const* hin,
                      void* const* hout, const double2* rb, int nmax, cudaStream_t st);

@@ -127,7 +127,7 @@ void kron_jit_free(KronJitPair* p) { delete p; }
 KronJitPair* kron_jit_build(int nin, int nmid, int nout, int bw, const std::vector<JitContrib>& a,
                             const std::vector<JitContrib>& b, const std::vector<int>& freal,
                             const std::vector<double2>& coeffs, long long s_a, int n_a, int n_b, long long n_outer,
-                            int tmax_default) {
+                            int tmax_default, int dmax) {
     if (const char* e = std::getenv("KS_KRON_JIT"))
         if (std::strcmp(e, "0") == 0) return nullptr;
     if (nin < 1 || nmid < 1 || nout < 1 || bw < 1 || bw > 6 || nin > 16 || nmid > 16 || nout > 16) return nullptr;
@@ -159,7 +159,8 @@ KronJitPair* kron_jit_build(int nin, int nmid, int nout, int bw, const std::vect
     const long long nqb = (s_a + nq - 1) / nq, nob = (n_outer + no - 1) / no;
     const int pad = bw * nq;
     const int RS = T + 2 * pad; // ring row: halo | T points | halo
-    int D = 4;
+    // ring depth: planes in flight per CTA (KS_KRON_JIT_D overrides for experiments)
+    int D = std::getenv("KS_KRON_JIT_D") ? std::max(2, std::min(12, std::atoi(std::getenv("KS_KRON_JIT_D")))) : dmax;
     auto smem = [&](int d) { return (size_t)d * nin * RS * sizeof(double2); };
     while (D > 2 && smem(D) > 110 * 1024) --D;
     if (smem(D) > 200 * 1024) return nullptr;
@@ -309,9 +310,7 @@ ks_pair(const double2* const* __restrict__ ip, double2* const* __restrict__ op, 
         s << "#pragma unroll\n        for (int h = 0; h < " << nmid
           << "; ++h)\n#pragma unroll\n            for (int j = 0; j < W - 1; ++j) win[h][j] = win[h][j + 1];\n";
     s << "        if (ib < n_b) {\n"
-      << "            if (D == 2) asm volatile(\"cp.async.wait_group 0;\\n\" ::);\n"
-      << "            else if (D == 3) asm volatile(\"cp.async.wait_group 1;\\n\" ::);\n"
-      << "            else asm volatile(\"cp.async.wait_group 2;\\n\" ::);\n"
+      << "            asm volatile(\"cp.async.wait_group " << (D - 2) << ";\\n\" ::);\n"
       << "            __syncthreads();\n            issue(ib + D - 1);\n"
       << "            const double2* sl = ring + (ib % D) * (NIN * RS) + PAD + tid;\n";
     for (int h = 0; h < nmid; ++h) s << "            double2 m" << h << " = Z;\n";

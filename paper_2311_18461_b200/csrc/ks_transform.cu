@@ -322,7 +322,13 @@ template <int N> __device__ __forceinline__ void cp_async_wait() {
 // tiles are tbt (time) x tbr (lower spatial index) blocks of 64 columns, so
 // both the natural side (consecutive t) and the time-major side (consecutive
 // i) move 64-128 B segments.
-enum { MAP_STD = 0, MAP_TOUT = 1, MAP_TIN = 2 };
+//
+// MAP_TOUT1 / MAP_TIN1 hand the time-major layout over on AXIS 1 instead
+// (d = 3 pair-mode FD apply: forward axes d..2 natural, axis 1 last). Columns
+// are enumerated as in MAP_STD (q = t + nt*o, o = the axes above 1), so the
+// natural side moves whole 1 KB rows; on the time-major side a column's rows
+// (i1) are contiguous: T[t][i1 + n1*o], row stride one complex (Np = 1).
+enum { MAP_STD = 0, MAP_TOUT = 1, MAP_TIN = 2, MAP_TOUT1 = 3, MAP_TIN1 = 4 };
 struct ColMap {
     int mode;
     int nt;            // time extent (T modes)
@@ -360,7 +366,7 @@ struct TileBase {
 };
 __device__ __forceinline__ TileBase tile_base(const ColMap& M, long long tile) {
     TileBase b;
-    if (M.mode == MAP_STD) {
+    if (M.mode == MAP_STD || M.mode >= MAP_TOUT1) {
         b.q0 = tile * M.tw;
         b.o0 = b.q0 / M.s;
         b.r0 = b.q0 - b.o0 * M.s;
@@ -382,6 +388,18 @@ __device__ __forceinline__ bool colmap(const ColMap& M, int n, const TileBase& B
             ++o;
         }
         in_off = out_off = 2 * (o * (long long)n * M.s + qq);
+        return true;
+    }
+    if (M.mode >= MAP_TOUT1) { // STD columns, axis-1 time-major side
+        if (B.q0 + j >= M.Q) return false;
+        long long o = B.o0, qq = B.r0 + j;
+        while (qq >= M.s) {
+            qq -= M.s;
+            ++o;
+        }
+        const long long nat = 2 * (o * (long long)n * M.s + qq), tm = 2 * (qq * M.Ns + (long long)n * o);
+        in_off = M.mode == MAP_TIN1 ? tm : nat;
+        out_off = M.mode == MAP_TOUT1 ? tm : nat;
         return true;
     }
     const long long tb = B.tb, rb = B.rb;
@@ -412,8 +430,8 @@ k_mode_gemm_dmma2(const double* __restrict__ At, int n, const double* __restrict
     const int nk = (n + kBK - 1) / kBK;
     double* As = smem;                          // [nk*kBK][BMP]
     double* Bs = smem + (size_t)nk * kBK * BMP; // [STG][kBK][BNP]
-    const long long in_rs = M.mode == MAP_TIN ? 2 * M.Np : 2 * M.s;
-    const long long out_rs = M.mode == MAP_TOUT ? 2 * M.Np : 2 * M.s;
+    const long long in_rs = (M.mode == MAP_TIN || M.mode == MAP_TIN1) ? 2 * M.Np : 2 * M.s;
+    const long long out_rs = (M.mode == MAP_TOUT || M.mode == MAP_TOUT1) ? 2 * M.Np : 2 * M.s;
     const long long ntiles = M.ntiles;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -530,8 +548,8 @@ k_mode_gemm_dmma3(const double* __restrict__ At, int n, const double* __restrict
     const int kpad = nk * kBK;
     double* As = smem;                           // [KMAX][BMP]
     double* Bs = smem + (size_t)KMAX * BMP;      // [2][KMAX][BNP]
-    const long long in_rs = M.mode == MAP_TIN ? 2 * M.Np : 2 * M.s;
-    const long long out_rs = M.mode == MAP_TOUT ? 2 * M.Np : 2 * M.s;
+    const long long in_rs = (M.mode == MAP_TIN || M.mode == MAP_TIN1) ? 2 * M.Np : 2 * M.s;
+    const long long out_rs = (M.mode == MAP_TOUT || M.mode == MAP_TOUT1) ? 2 * M.Np : 2 * M.s;
     const long long ntiles = M.ntiles;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wr = warp & 1, wc = warp >> 1;
@@ -734,7 +752,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 // GEMMs, so the inverse unfold happens in registers.
 // Resident matrices: Af[2][kst][H] (k-major; [0] even, [1] odd, zero padded), staged as nkc*KC rows.
 // ---------------------------------------------------------------------------
-template <int TH, bool INV, int KC, int STG, int MINB, int BNC, bool TMA, bool ROWS = false>
+// RL: loader lanes along rows instead of columns (MAP_TIN1: a column's rows
+// are contiguous on the time-major side, so a warp reads 2 x 256 B runs)
+template <int TH, bool INV, int KC, int STG, int MINB, int BNC, bool TMA, bool ROWS = false, bool RL = false>
 __global__ void __launch_bounds__(kThreads, MINB)
 k_mode_gemm_fold(const double* __restrict__ Af, int Kst, const int* __restrict__ rmap, int n, int hc, int nkc,
                  const double* __restrict__ X, double* __restrict__ Y, ColMap M, int dry) {
@@ -746,18 +766,26 @@ k_mode_gemm_fold(const double* __restrict__ Af, int Kst, const int* __restrict__
     constexpr int NF = BND / 32;     // 8-column fragments per warp
     constexpr int RPP = kThreads / BNC; // smem rows per loader pass
     constexpr int SR = 2 * KC; // smem rows per stage: KC top + KC bottom
+    static_assert(!RL || (kThreads % SR == 0 && BNC % (kThreads / SR) == 0 && BNC / (kThreads / SR) <= 32),
+                  "row-lane loader geometry");
+    // RL keeps a stage column-major, [complex column][row (SRP)][re, im]: a warp's
+    // 32 rows of one column land contiguously (row-major staging would split every
+    // 32 B sector over two smem rows and fetch it twice); SRP == 4 (mod 8) keeps
+    // the B-fragment loads at two wavefronts
+    constexpr int SRP = SR + 4;
+    constexpr int STAGE_D = RL ? BNC * SRP * 2 : SR * BNP; // doubles per stage
     extern __shared__ __align__(16) double smem[];
     const int Kp = nkc * KC;
     double* Ae = smem;                        // [Kp][BMP]
     double* Ao = Ae + (size_t)Kp * BMP;       // [Kp][BMP]
     double* Bs = Ao + (size_t)Kp * BMP;       // [STG][SR][BNP]
-    int* rE = reinterpret_cast<int*>(Bs + (size_t)STG * SR * BNP); // [H] even eigen-indices
+    int* rE = reinterpret_cast<int*>(Bs + (size_t)STG * STAGE_D); // [H] even eigen-indices
     int* rO = rE + H;                                               // [H] odd eigen-indices
     // TMA: one mbarrier per stage (8 B aligned: rE/rO hold 2H ints)
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(rO + H);
     const int no = n - hc;
-    const long long in_rs = M.mode == MAP_TIN ? 2 * M.Np : 2 * M.s;
-    const long long out_rs = M.mode == MAP_TOUT ? 2 * M.Np : 2 * M.s;
+    const long long in_rs = (M.mode == MAP_TIN || M.mode == MAP_TIN1) ? 2 * M.Np : 2 * M.s;
+    const long long out_rs = (M.mode == MAP_TOUT || M.mode == MAP_TOUT1) ? 2 * M.Np : 2 * M.s;
     const long long ntiles = M.ntiles;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wr = warp & 1, wc = warp >> 1;
@@ -819,9 +847,51 @@ k_mode_gemm_fold(const double* __restrict__ Af, int Kst, const int* __restrict__
                          (unsigned)((ncol - seg1) * 16), b);
         }
     };
+    // RL loader state: the thread's row and the column offsets of its NPASS columns
+    constexpr int CPP = kThreads / SR, NPASS = RL ? BNC / CPP : 1;
+    long long rl_in[NPASS];
+    unsigned rl_valid = 0;
     auto issue = [&](int w) {
         if (TMA) {
             issue_tma(w);
+            return;
+        }
+        if (RL) {
+            if (w < nwork) {
+                const int wt = w / nkc;
+                const long long tile = (long long)blockIdx.x + (long long)wt * gridDim.x;
+                const int kc = w - wt * nkc;
+                if (tile != cur_tile) {
+                    const TileBase tb = tile_base(M, tile);
+                    rl_valid = 0;
+#pragma unroll
+                    for (int c = 0; c < NPASS; ++c) {
+                        long long dummy;
+                        if (colmap(M, n, tb, tid / SR + CPP * c, rl_in[c], dummy)) rl_valid |= 1u << c;
+                    }
+                    cur_tile = tile;
+                }
+                double* bs = Bs + (size_t)(w % STG) * STAGE_D;
+                const int jj = tid % SR;
+                const int q = kc * KC + (jj % KC);
+                int src;
+                bool v;
+                if (!INV) {
+                    src = jj < KC ? q : n - 1 - q;
+                    v = jj < KC ? q < hc : q < n - hc;
+                } else {
+                    v = jj < KC ? q < hc : q < no;
+                    src = v ? (jj < KC ? rE[q] : rO[q]) : 0;
+                }
+#pragma unroll
+                for (int c = 0; c < NPASS; ++c) {
+                    const bool vc = v && ((rl_valid >> c) & 1u) && dry != 3;
+                    const int col = tid / SR + CPP * c;
+                    cp_async16(bs + 2 * (col * SRP + jj), vc ? (const void*)in_row<ROWS>(M, X, rl_in[c], src, in_rs) : (const void*)X,
+                               vc);
+                }
+            }
+            cp_async_commit();
             return;
         }
         if (w < nwork) {
@@ -875,7 +945,7 @@ k_mode_gemm_fold(const double* __restrict__ Af, int Kst, const int* __restrict__
         __syncthreads();
         issue(w + STG - 1);
         const int kc = w % nkc;
-        const double* bs = Bs + (size_t)(w % STG) * SR * BNP;
+        const double* bs = Bs + (size_t)(w % STG) * STAGE_D;
         if (!dry)
 #pragma unroll
         for (int k4 = 0; k4 < KC; k4 += 4) {
@@ -888,8 +958,9 @@ k_mode_gemm_fold(const double* __restrict__ Af, int Kst, const int* __restrict__
             }
 #pragma unroll
             for (int m = 0; m < NF; ++m) {
-                const double t = bs[(k4 + ak) * BNP + c_warp + m * 8 + ar];
-                const double b = bs[(KC + k4 + ak) * BNP + c_warp + m * 8 + ar];
+                const int dc = c_warp + m * 8 + ar; // double column
+                const double t = RL ? bs[2 * ((dc >> 1) * SRP + k4 + ak) + (dc & 1)] : bs[(k4 + ak) * BNP + dc];
+                const double b = RL ? bs[2 * ((dc >> 1) * SRP + KC + k4 + ak) + (dc & 1)] : bs[(KC + k4 + ak) * BNP + dc];
                 be[m] = INV ? t : t + b;
                 bo[m] = INV ? b : t - b;
             }
@@ -945,7 +1016,7 @@ int dry_run() {
 // tile width (complex columns) of a column map; T modes block it as tbt x tbr
 void set_tile_width(ColMap& M, int tw) {
     M.tw = tw;
-    if (M.mode == MAP_STD) {
+    if (M.mode == MAP_STD || M.mode >= MAP_TOUT1) {
         M.ntiles = (M.Q + tw - 1) / tw;
     } else {
         M.tbr = M.Np >= 8 ? 8 : (M.Np >= 4 ? 4 : (M.Np >= 2 ? 2 : 1));
@@ -962,8 +1033,10 @@ template <int TH, bool INV, int KC, int STG, int MINB, int BNC, bool TMA = false
 void launch_fold_cfg(const FoldAxis& F, const double* X, double* Y, ColMap M, cudaStream_t st) {
     constexpr int H = 16 * TH;
     const int nkc = (F.hc + KC - 1) / KC;
+    const bool rl = M.mode == MAP_TIN1 && !M.rin && !M.rout; // column-major stages (row-lane loader)
+    const size_t stage_d = rl ? (size_t)BNC * (2 * KC + 4) * 2 : (size_t)2 * KC * (2 * BNC + 4);
     const size_t sm = (size_t)2 * nkc * KC * (H + 4) * sizeof(double) + (size_t)2 * H * sizeof(int) +
-                      (size_t)STG * 2 * KC * (2 * BNC + 4) * sizeof(double) + (size_t)STG * 8;
+                      (size_t)STG * stage_d * sizeof(double) + (size_t)STG * 8;
     KS_REQUIRE(sm <= 227 * 1024, KS_EINVAL, "folded mode product: axis too long");
     static int sms = 0;
     if (!sms) {
@@ -986,6 +1059,23 @@ void launch_fold_cfg(const FoldAxis& F, const double* X, double* Y, ColMap M, cu
         }
         k_mode_gemm_fold<TH, INV, KC, STG, MINB, BNC, false, true><<<g, kThreads, sm, st>>>(
             A, F.kst, F.rmap.as<int>(), F.n, F.hc, nkc, X, Y, M, 0);
+    } else if (M.mode == MAP_TIN1 || M.mode == MAP_TOUT1) {
+        // axis-1 time-major side: rows are stored by position (even eigen-indices
+        // first, then odd), so the time-major row map is the position map
+        const int* rm = F.rpos.as<int>();
+        if (M.mode == MAP_TIN1) {
+            static bool attr_l = false;
+            if (!attr_l) {
+                KS_CUDA(cudaFuncSetAttribute(k_mode_gemm_fold<TH, INV, KC, STG, MINB, BNC, false, false, true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+                attr_l = true;
+            }
+            k_mode_gemm_fold<TH, INV, KC, STG, MINB, BNC, false, false, true><<<g, kThreads, sm, st>>>(
+                A, F.kst, rm, F.n, F.hc, nkc, X, Y, M, dry_run());
+        } else {
+            k_mode_gemm_fold<TH, INV, KC, STG, MINB, BNC, false><<<g, kThreads, sm, st>>>(A, F.kst, rm, F.n, F.hc,
+                                                                                          nkc, X, Y, M, dry_run());
+        }
     } else {
         k_mode_gemm_fold<TH, INV, KC, STG, MINB, BNC, TMA><<<g, kThreads, sm, st>>>(A, F.kst, F.rmap.as<int>(), F.n,
                                                                                     F.hc, nkc, X, Y, M, dry_run());
@@ -1045,6 +1135,12 @@ ColMap make_colmap(int n, size_t s_complex, size_t outer, int layout, int nt) {
     M.s = (long long)s_complex;
     M.Q = (long long)s_complex * (long long)outer;
     if (layout == MAP_STD) {
+        M.ntiles = (M.Q + 63) / 64;
+    } else if (layout >= MAP_TOUT1) {
+        KS_REQUIRE(nt > 0 && s_complex == (size_t)nt, KS_EINVAL, "axis-1 time-major transform needs axis 1");
+        M.nt = nt;
+        M.Np = 1;
+        M.Ns = (long long)n * (long long)outer;
         M.ntiles = (M.Q + 63) / 64;
     } else {
         KS_REQUIRE(outer == 1 && nt > 0 && s_complex % (size_t)nt == 0, KS_EINVAL,
@@ -1183,6 +1279,13 @@ bool fold_axis_build(const double* U_in, const double* lam, int n, double tol, F
     F.fwd.alloc(fwd.size() * sizeof(double));
     F.inv.alloc(inv.size() * sizeof(double));
     F.rmap.alloc(rmap.size() * sizeof(int));
+    // position map of the axis-1 time-major layout: even eigenvectors at 0..hc-1, odd at hc..n-1
+    std::vector<int> rpos((size_t)2 * H, 0);
+    F.perm.assign(n, 0);
+    for (int m = 0; m < hc; ++m) rpos[m] = m, F.perm[m] = E[m];
+    for (int m = 0; m < no; ++m) rpos[H + m] = hc + m, F.perm[hc + m] = O[m];
+    F.rpos.alloc(rpos.size() * sizeof(int));
+    KS_CUDA(cudaMemcpy(F.rpos.p, rpos.data(), rpos.size() * sizeof(int), cudaMemcpyHostToDevice));
     KS_CUDA(cudaMemcpy(F.fwd.p, fwd.data(), fwd.size() * sizeof(double), cudaMemcpyHostToDevice));
     KS_CUDA(cudaMemcpy(F.inv.p, inv.data(), inv.size() * sizeof(double), cudaMemcpyHostToDevice));
     KS_CUDA(cudaMemcpy(F.rmap.p, rmap.data(), rmap.size() * sizeof(int), cudaMemcpyHostToDevice));

@@ -116,3 +116,34 @@ def test_fused_axes12_matches_oracle(gpu, oracle, d, p, n_el, n_el_t, monkeypatc
     assert rel(z, zo) <= TOL and maxrel(z, zo) <= TOL
     za, zao = g.apply_adjoint(r), o.apply_adjoint(r)
     assert rel(za, zao) <= TOL and maxrel(za, zao) <= TOL
+
+
+@pytest.mark.parametrize("d,p,n_el,n_el_t", [(3, 2, 16, 8), (3, 3, 13, 5), (3, 4, 11, 4)])
+def test_axis1_time_major_handoff(gpu, oracle, d, p, n_el, n_el_t):
+    """Pair mode hands the time-major layout over on axis 1 (forward axes d..1,
+    rows stored by even/odd position, blocks numbered by position); KS_FD_TM1=0
+    keeps the outermost-axis hand-off. Both match the oracle, forward and
+    adjoint, and each other to rounding; ks_fd_block still answers by natural
+    fiber index."""
+    old = os.environ.get("KS_FD_TM1")
+    try:
+        os.environ["KS_FD_TM1"] = "0"
+        _, g0, o = _pair(gpu, oracle, d, p, n_el, n_el_t)
+        os.environ["KS_FD_TM1"] = "1"
+        a, g1, _ = _pair(gpu, oracle, d, p, n_el, n_el_t)
+    finally:
+        if old is None:
+            del os.environ["KS_FD_TM1"]
+        else:
+            os.environ["KS_FD_TM1"] = old
+    assert g0.info()["time_major_axis"] == d and g1.info()["time_major_axis"] == 1
+    r = oracle.random_vec(o.N, 17)
+    for ap in ("apply", "apply_adjoint"):
+        z0, z1 = getattr(g0, ap)(r), getattr(g1, ap)(r)
+        zo = getattr(o, ap)(r)
+        assert rel(z1, zo) <= TOL and maxrel(z1, zo) <= TOL
+        assert rel(z1, z0) <= 1e-12
+    n1 = a["dims"][1]
+    for i in (0, 1, n1 - 1, n1 + 3, o.N // a["dims"][0] - 1):
+        b0, b1 = g0.block(i, p), g1.block(i, p)
+        assert np.array_equal(b0[0], b1[0]) and np.array_equal(b0[1], b1[1])

@@ -12,7 +12,7 @@ A, P = ks.assemble_system_operator(prob), ks.FDPreconditioner(prob)
 g = np.random.default_rng(1234)
 b = ks.DeviceVector.from_host(g.uniform(-1, 1, prob.N_dof) + 1j * g.uniform(-1, 1, prob.N_dof))
 ts = []
-for k in range(8):
+for k in range(int(os.environ.get("SOLVE_N", "8"))):
     t0 = time.perf_counter()
     rep = ks.pcg(A, P, b, ks.PcgOptions(1e-8, 200))
     ts.append((time.perf_counter() - t0, rep.solve_seconds, rep.iterations))
