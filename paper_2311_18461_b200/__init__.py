@@ -474,7 +474,8 @@ class FDPreconditioner:
         _check(lib().ks_fd_info(self._h, C.byref(m), C.byref(nb)))
         d = len(self.dims) - 1
         return {"folded_axes": [l + 1 for l in range(d) if m.value >> l & 1], "blocks": nb.value,
-                "fused_axes_12": bool(m.value >> 16 & 1), "time_major_axis": 1 if m.value >> 17 & 1 else d}
+                "fused_axes_12": bool(m.value >> 16 & 1), "time_major_axis": 1 if m.value >> 17 & 1 else d,
+                "no_pivoting": bool(m.value >> 18 & 1)}
 
     def time(self, r: DeviceVector, z: DeviceVector, iters: int, flush: bool = True):
         ms, mk = C.c_double(), C.c_double()

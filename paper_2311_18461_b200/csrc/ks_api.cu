@@ -659,6 +659,7 @@ int ks_fd_info(const ks_fd* fd, int* folded_axes, size_t* blocks) {
         if (fd->fold[l].n) m |= 1 << l;
     if (fd->fuse12 && !fd->fused) m |= 1 << 16;
     if (fd->tm1) m |= 1 << 17;
+    if (fd->blocks.nopiv) m |= 1 << 18;
     if (folded_axes) *folded_axes = m;
     if (blocks) *blocks = fd->blocks.nblk;
     API_END
@@ -962,11 +963,32 @@ int ks_pcg(ks_kron* A, ks_fd* P, const ks_c64* b, ks_c64* x, int mem, const ks_p
         ~Graphs() { reset(); }
     } graphs;
     bool use_graph = graphs_ok, seen[2] = {false, false};
+    // Deferred solution update (default; KS_PCG_XDEFER=0 off): phase A updates
+    // only r, and x += alpha_k p_k rides along the p update of phase B (which
+    // reads p_k anyway) -- or runs alone before a true residual and at exit.
+    // Same arithmetic on the same operands: bit-identical iterates, 48 B per
+    // element less vector traffic per iteration. In strict mode x is needed
+    // every iteration, so it is updated right after phase A.
+    const bool xdefer = [] {
+        const char* e = std::getenv("KS_PCG_XDEFER");
+        return !(e && std::strcmp(e, "0") == 0);
+    }();
+    bool pending = false; // x += alpha_k p_k not yet applied
+    auto apply_x = [&]() {
+        if (!pending) return;
+        launch_x_update_dev(rho_old.result.as<double>(), red_c.result.as<double>(), p.as<double2>(), xv.as<double2>(),
+                            n, st);
+        pending = false;
+    };
     auto phase_a = [&]() {
         kron_apply(*A->plan, p.as<double2>(), q.as<double2>(), st, A->hptrs);
         launch_dotc(red_c, p.as<double2>(), q.as<double2>(), n, st); // curvature Re <p, Ap>
-        launch_cg_update_dev(red_u, rho_old.result.as<double>(), red_c.result.as<double>(), p.as<double2>(),
-                             q.as<double2>(), xv.as<double2>(), r.as<double2>(), n, st);
+        if (xdefer)
+            launch_cg_update_r_dev(red_u, rho_old.result.as<double>(), red_c.result.as<double>(), q.as<double2>(),
+                                   r.as<double2>(), n, st);
+        else
+            launch_cg_update_dev(red_u, rho_old.result.as<double>(), red_c.result.as<double>(), p.as<double2>(),
+                                 q.as<double2>(), xv.as<double2>(), r.as<double2>(), n, st);
         KS_CUDA(cudaMemcpyAsync(red_c.host, red_c.result.p, sizeof(double), cudaMemcpyDeviceToHost, st));
         KS_CUDA(cudaMemcpyAsync(red_u.host, red_u.result.p, sizeof(double), cudaMemcpyDeviceToHost, st));
     };
@@ -974,8 +996,13 @@ int ks_pcg(ks_kron* A, ks_fd* P, const ks_c64* b, ks_c64* x, int mem, const ks_p
         if (P) fd_apply_dev(P, r.as<double2>(), z.as<double2>(), false, st, nullptr);
         else KS_CUDA(cudaMemcpyAsync(z.p, r.p, bytes, cudaMemcpyDeviceToDevice, st));
         launch_dotc(rho_new, r.as<double2>(), z.as<double2>(), n, st); // rho'
-        launch_xpby_dev(z.as<double2>(), rho_new.result.as<double>(), rho_old.result.as<double>(), p.as<double2>(),
-                        n, st);
+        if (pending) { // (the caller clears pending: a replayed graph does not run this body)
+            launch_xpby_x_dev(z.as<double2>(), rho_new.result.as<double>(), rho_old.result.as<double>(),
+                              red_c.result.as<double>(), p.as<double2>(), xv.as<double2>(), n, st);
+        } else {
+            launch_xpby_dev(z.as<double2>(), rho_new.result.as<double>(), rho_old.result.as<double>(),
+                            p.as<double2>(), n, st);
+        }
         KS_CUDA(cudaMemcpyAsync(rho_old.result.p, rho_new.result.p, sizeof(double), cudaMemcpyDeviceToDevice, st));
     };
     auto run_phase = [&](int which, auto&& body, std::vector<std::pair<int, int>>& tim) {
@@ -1055,11 +1082,16 @@ int ks_pcg(ks_kron* A, ks_fd* P, const ks_c64* b, ks_c64* x, int mem, const ks_p
             break;
         }
         report->iterations++;
+        pending = xdefer;
         double relres = std::sqrt(red_u.host[0]) / bnorm;
-        if (opts->strict_residual) relres = true_relres();
+        if (opts->strict_residual) {
+            apply_x();
+            relres = true_relres();
+        }
         push_hist(relres);
         if (relres <= opts->tol) {
             if (!opts->strict_residual) {
+                apply_x();
                 const double tr = true_relres();
                 set_last_hist(tr);
                 if (tr > opts->tol) {
@@ -1075,7 +1107,9 @@ int ks_pcg(ks_kron* A, ks_fd* P, const ks_c64* b, ks_c64* x, int mem, const ks_p
             break;
         }
         run_phase(1, phase_b, pc_ev);
+        pending = false;
     }
+    apply_x(); // maxit reached with the last update pending
     report->restarts = restarts;
     report->hist_len = hist_len < hist_cap ? hist_len : hist_cap;
     if (!res_hist) report->hist_len = 0;

@@ -154,6 +154,62 @@ __global__ void __launch_bounds__(kT) k_cg_update_dev(const double* __restrict__
     finish<1>(v, partial, counter, result);
 }
 
+// Deferred-x variant: the same r update and ||r||^2, x left for the p update
+// (x += alpha p_k is applied by k_xpby_x_dev, which reads p_k anyway, or by
+// k_x_update_dev before a true residual / at exit): 48 instead of 96 B per
+// element here, +32 B there -- the iterates are bit-identical.
+__global__ void __launch_bounds__(kT) k_cg_update_r_dev(const double* __restrict__ rho, const double* __restrict__ curv,
+                                                        const double2* __restrict__ q, double2* __restrict__ r, size_t n,
+                                                        double* partial, unsigned* counter, double* result) {
+    const double c = *curv;
+    const bool live = c > 0.0;
+    const double alpha = live ? *rho / c : 0.0;
+    double v[1] = {0.0};
+    for (size_t i = blockIdx.x * (size_t)kT + threadIdx.x; i < n; i += (size_t)gridDim.x * kT) {
+        double2 ri = r[i];
+        if (live) {
+            const double2 qi = __ldg(q + i);
+            ri.x += -alpha * qi.x;
+            ri.y += -alpha * qi.y;
+            r[i] = ri;
+        }
+        v[0] += ri.x * ri.x + ri.y * ri.y;
+    }
+    finish<1>(v, partial, counter, result);
+}
+
+// x += alpha_k p_k (alpha_k = rho_old / curv, krylov.cpp:73-75) and
+// p = z + (rho_new / rho_old) p_k (krylov.cpp:105-110) in one pass
+__global__ void k_xpby_x_dev(const double2* __restrict__ z, const double* __restrict__ rho_new,
+                             const double* __restrict__ rho_old, const double* __restrict__ curv,
+                             double2* __restrict__ p, double2* __restrict__ x, size_t n) {
+    const double beta = *rho_new / *rho_old, alpha = *rho_old / *curv;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x) {
+        const double2 zi = __ldg(z + i);
+        double2 pi = p[i], xi = x[i];
+        xi.x += alpha * pi.x;
+        xi.y += alpha * pi.y;
+        pi.x = zi.x + beta * pi.x;
+        pi.y = zi.y + beta * pi.y;
+        x[i] = xi;
+        p[i] = pi;
+    }
+}
+
+__global__ void k_x_update_dev(const double* __restrict__ rho, const double* __restrict__ curv,
+                               const double2* __restrict__ p, double2* __restrict__ x, size_t n) {
+    const double alpha = *rho / *curv;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x) {
+        const double2 pi = __ldg(p + i);
+        double2 xi = x[i];
+        xi.x += alpha * pi.x;
+        xi.y += alpha * pi.y;
+        x[i] = xi;
+    }
+}
+
 // p = z + (rho_new / rho_old) p  (krylov.cpp:105-110), beta formed on the device
 __global__ void k_xpby_dev(const double2* __restrict__ z, const double* __restrict__ rho_new,
                            const double* __restrict__ rho_old, double2* __restrict__ p, size_t n) {
@@ -256,6 +312,22 @@ void launch_cg_update_dev(Reducer& red, const double* rho, const double* curv, c
     k_cg_update_dev<<<kB, kT, 0, s>>>(rho, curv, p, q, x, r, n, red.partial.as<double>(), red.counter.as<unsigned>(),
                                       red.result.as<double>());
     check_launch("k_cg_update_dev");
+}
+void launch_cg_update_r_dev(Reducer& red, const double* rho, const double* curv, const double2* q, double2* r,
+                            size_t n, cudaStream_t s) {
+    k_cg_update_r_dev<<<kB, kT, 0, s>>>(rho, curv, q, r, n, red.partial.as<double>(), red.counter.as<unsigned>(),
+                                        red.result.as<double>());
+    check_launch("k_cg_update_r_dev");
+}
+void launch_xpby_x_dev(const double2* z, const double* rho_new, const double* rho_old, const double* curv,
+                       double2* p, double2* x, size_t n, cudaStream_t s) {
+    k_xpby_x_dev<<<ew_blocks(n), 256, 0, s>>>(z, rho_new, rho_old, curv, p, x, n);
+    check_launch("k_xpby_x_dev");
+}
+void launch_x_update_dev(const double* rho, const double* curv, const double2* p, double2* x, size_t n,
+                         cudaStream_t s) {
+    k_x_update_dev<<<ew_blocks(n), 256, 0, s>>>(rho, curv, p, x, n);
+    check_launch("k_x_update_dev");
 }
 void launch_xpby_dev(const double2* z, const double* rho_new, const double* rho_old, double2* p, size_t n,
                      cudaStream_t s) {

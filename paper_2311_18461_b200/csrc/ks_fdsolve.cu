@@ -76,7 +76,7 @@ __device__ __forceinline__ double cabs_(double2 a) { return hypot(a.x, a.y); }
 // and eliminates in place.
 // ---------------------------------------------------------------------------
 __global__ void k_fd_factor(double2* __restrict__ ab, unsigned char* __restrict__ piv,
-                            int* __restrict__ flag, size_t ns, int nt, int p,
+                            int* __restrict__ flag, unsigned char* __restrict__ wpiv, size_t ns, int nt, int p,
                             const double* __restrict__ lam_blk, double nu,
                             const double* __restrict__ Lt, const double* __restrict__ Mt,
                             const double2* __restrict__ Wsym, int rec, int fused_nd, long long fused_np,
@@ -119,6 +119,19 @@ __global__ void k_fd_factor(double2* __restrict__ ab, unsigned char* __restrict_
         }
     }
     // partial-pivot banded LU (eigensolve.cpp:93-119)
+    bool swapped = false; // any row interchange: flag bit 1 (the solves then read the fill-in rows)
+    struct SwapFlag {
+        bool& s;
+        int* f;
+        unsigned char* w;
+        size_t i;
+        __device__ ~SwapFlag() {
+            if (s) {
+                atomicOr(f, 2);
+                w[i >> 5] = 1; // every writer stores 1
+            }
+        }
+    } swap_flag{swapped, flag, wpiv, i};
     for (int k = 0; k < nt; ++k) {
         const int imax = k + p < nt - 1 ? k + p : nt - 1;
         int pr = k;
@@ -133,9 +146,10 @@ __global__ void k_fd_factor(double2* __restrict__ ab, unsigned char* __restrict_
         if (rec > 0) ab[base + (size_t)k * kstr + ldab] = make_double2((double)(pr - k), 0.0);
         else piv[bx.pb + (size_t)k * bx.pk] = (unsigned char)(pr - k);
         if (best == 0.0) {
-            atomicExch(flag, 1);
+            atomicOr(flag, 1);
             return;
         }
+        swapped |= pr != k;
         const int jmax = k + kuf < nt - 1 ? k + kuf : nt - 1;
         if (pr != k)
             for (int c = k; c <= jmax; ++c) {
@@ -460,17 +474,16 @@ __global__ void __launch_bounds__(TB) k_fd_solve_ring(const double2* __restrict_
 #ifndef KS_PAIR_RECIP
 #define KS_PAIR_RECIP 1
 #endif
-template <int P, int D>
-__global__ void __launch_bounds__(128) k_fd_solve_pair(const double2* __restrict__ ab,
-                                                       const unsigned char* __restrict__ piv,
-                                                       double2* __restrict__ X, size_t ns, int nt, size_t nblk,
-                                                       int n1, int n2, const int2* __restrict__ pairs) {
+// NP: no block pivoted (FdBlocks::nopiv): pivot offsets not read, and the
+// backward sweep reads U's p+1 rows instead of the 2p+1 of the fill-in band --
+// the skipped entries are exact zeros, so the result is bit-identical
+template <int P, int D, bool NP>
+__device__ __forceinline__ void fd_pair_body(const double2* __restrict__ ab, const unsigned char* __restrict__ piv,
+                                             double2* __restrict__ X, size_t ns, int nt, size_t nblk, int n1, int n2,
+                                             const int2* __restrict__ pairs, double2* ring, size_t b) {
     constexpr int kuf = 2 * P, NE = 2 * P + 3;
-    extern __shared__ __align__(16) double2 ring[]; // [D][NE][128], then unsigned [D][128]
     unsigned* pr = reinterpret_cast<unsigned*>(ring + (size_t)D * NE * 128);
     const int t = threadIdx.x;
-    const size_t b = blockIdx.x * (size_t)128 + t;
-    if (b >= nblk) return;
     const int i1 = (int)(b % (size_t)n1);
     const int2 q = __ldg(pairs + b / (size_t)n1);
     const bool hb = q.x != q.y;
@@ -485,8 +498,10 @@ __global__ void __launch_bounds__(128) k_fd_solve_pair(const double2* __restrict
             const int kx = k + P + 1;
             cpa16(slot(k, P), kx < nt ? xa + (size_t)kx * ns : X, kx < nt);
             cpa16(slot(k, P + 1), kx < nt && hb ? xb + (size_t)kx * ns : X, kx < nt && hb);
-            const size_t o = (size_t)k * nblk + b;
-            cpa4(pr + (k % D) * 128 + t, piv + (o & ~(size_t)3), true);
+            if (!NP) {
+                const size_t o = (size_t)k * nblk + b;
+                cpa4(pr + (k % D) * 128 + t, piv + (o & ~(size_t)3), true);
+            }
         }
         cpa_commit();
     };
@@ -503,7 +518,7 @@ __global__ void __launch_bounds__(128) k_fd_solve_pair(const double2* __restrict
         cpa_wait<D - 2>();
         issue_f(k + D - 1);
         const size_t o = (size_t)k * nblk + b;
-        const int po = (int)((pr[(k % D) * 128 + t] >> (8 * (unsigned)(o & 3))) & 0xffu);
+        const int po = NP ? 0 : (int)((pr[(k % D) * 128 + t] >> (8 * (unsigned)(o & 3))) & 0xffu);
 #pragma unroll
         for (int m = 1; m <= P; ++m)
             if (po == m) {
@@ -537,7 +552,7 @@ __global__ void __launch_bounds__(128) k_fd_solve_pair(const double2* __restrict
     auto issue_b = [&](int k) {
         if (k >= 0) {
 #pragma unroll
-            for (int j = 0; j <= 2 * P; ++j) cpa16(slot(k, j), k - j >= 0 ? baddr(k, kuf - j) : ab, k - j >= 0);
+            for (int j = 0; j <= (NP ? P : 2 * P); ++j) cpa16(slot(k, j), k - j >= 0 ? baddr(k, kuf - j) : ab, k - j >= 0);
             const int kx = k - 2 * P - 1;
             cpa16(slot(k, 2 * P + 1), kx >= 0 ? xa + (size_t)kx * ns : X, kx >= 0);
             cpa16(slot(k, 2 * P + 2), kx >= 0 && hb ? xb + (size_t)kx * ns : X, kx >= 0 && hb);
@@ -567,7 +582,7 @@ __global__ void __launch_bounds__(128) k_fd_solve_pair(const double2* __restrict
             ub[0] = cdiv(ub[0], dg);
         }
 #pragma unroll
-        for (int j = 1; j <= 2 * P; ++j)
+        for (int j = 1; j <= (NP ? P : 2 * P); ++j)
             if (k - j >= 0) {
                 const double2 uu = *slot(k, j);
                 ua[j] = csub(ua[j], cmul(uu, ua[0]));
@@ -584,6 +599,25 @@ __global__ void __launch_bounds__(128) k_fd_solve_pair(const double2* __restrict
         ua[2 * P] = ina;
         ub[2 * P] = inb;
     }
+}
+
+// Warp-uniform choice per group of 32 blocks: wpiv[b / 32] != 0 when one of
+// them pivoted (factor kernel). Only the smallest-eigenvalue blocks pivot
+// (c3: the first ~0.01%), so nearly every warp takes the NP body. wpiv null:
+// full band everywhere (KS_FD_NOPIV=0).
+template <int P, int D>
+__global__ void __launch_bounds__(128) k_fd_solve_pair(const double2* __restrict__ ab,
+                                                       const unsigned char* __restrict__ piv,
+                                                       double2* __restrict__ X, size_t ns, int nt, size_t nblk,
+                                                       int n1, int n2, const int2* __restrict__ pairs,
+                                                       const unsigned char* __restrict__ wpiv) {
+    extern __shared__ __align__(16) double2 ring[]; // [D][NE][128], then unsigned [D][128]
+    const size_t b = blockIdx.x * (size_t)128 + threadIdx.x;
+    if (b >= nblk) return;
+    if (wpiv && __ldg(wpiv + (b >> 5)) == 0)
+        fd_pair_body<P, D, true>(ab, piv, X, ns, nt, nblk, n1, n2, pairs, ring, b);
+    else
+        fd_pair_body<P, D, false>(ab, piv, X, ns, nt, nblk, n1, n2, pairs, ring, b);
 }
 
 // ---------------------------------------------------------------------------
@@ -857,7 +891,8 @@ void launch_solve_p(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t st
             }
             const unsigned gp = (unsigned)((B.nblk + 127) / 128);
             k_fd_solve_pair<P, D><<<gp, 128, sm, st>>>(B.ab.as<double2>(), B.piv.as<unsigned char>(), X, B.ns,
-                                                       B.nt, B.nblk, B.pair_n1, B.pair_n2, B.pairs.as<int2>());
+                                                       B.nt, B.nblk, B.pair_n1, B.pair_n2, B.pairs.as<int2>(),
+                                                       B.nopiv_off ? nullptr : B.wpiv.as<unsigned char>());
             check_launch("k_fd_solve_pair");
             return;
         }
@@ -910,6 +945,7 @@ void fd_blocks_alloc(FdBlocks& B) {
     B.ab.alloc((size_t)B.nt * per * B.nblk * sizeof(double2));
     if (B.rec == 0) B.piv.alloc((size_t)B.nt * B.nblk + 4); // +4: 4 B cp.async words
     B.flag.alloc(sizeof(int));
+    B.wpiv.alloc((B.nblk + 31) / 32 + 1);
 }
 
 void fd_block_to_host(const FdBlocks& B, size_t b, ks_c64* ab, int* piv) {
@@ -934,15 +970,22 @@ void fd_block_to_host(const FdBlocks& B, size_t b, ks_c64* ab, int* piv) {
 void launch_fd_factor(FdBlocks& B, double nu, const double* Lt, const double* Mt,
                       const double2* Wsym, cudaStream_t st) {
     KS_CUDA(cudaMemsetAsync(B.flag.p, 0, sizeof(int), st));
+    KS_CUDA(cudaMemsetAsync(B.wpiv.p, 0, B.wpiv.bytes, st));
     const unsigned grid = (unsigned)((B.nblk + 127) / 128);
     k_fd_factor<<<grid, 128, 0, st>>>(B.ab.as<double2>(), B.piv.as<unsigned char>(),
-                                      B.flag.as<int>(), B.nblk, B.nt, B.p, B.lam_blk.as<double>(), nu,
+                                      B.flag.as<int>(), B.wpiv.as<unsigned char>(), B.nblk, B.nt, B.p, B.lam_blk.as<double>(), nu,
                                       Lt, Mt, Wsym, B.rec, B.fused_nd, B.fused_np, B.kind);
     check_launch("k_fd_factor");
     int h = 0;
     KS_CUDA(cudaMemcpyAsync(&h, B.flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     KS_CUDA(cudaStreamSynchronize(st));
-    KS_REQUIRE(h == 0, KS_ESINGULAR, "factor_banded: numerically singular pivot");
+    KS_REQUIRE((h & 1) == 0, KS_ESINGULAR, "factor_banded: numerically singular pivot");
+    // no row interchange in any block: U has bandwidth p, the 2p-row fill-in
+    // band stays exactly zero, and the pair solve skips it (and the pivots)
+    B.nopiv = (h & 2) == 0;
+    B.nopiv_off = false;
+    if (const char* e = std::getenv("KS_FD_NOPIV"))
+        if (std::strcmp(e, "0") == 0) B.nopiv_off = true;
 }
 
 void launch_fd_solve(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t st, bool time_major) {

@@ -109,6 +109,14 @@ void launch_cg_update(Reducer& red, double alpha, const double2* p, const double
 // when *curv <= 0), beta = *rho_new / *rho_old
 void launch_cg_update_dev(Reducer& red, const double* rho, const double* curv, const double2* p, const double2* q,
                           double2* x, double2* r, size_t n, cudaStream_t s);
+// deferred solution update (PCG): r -= alpha q and ||r||^2 only (x untouched) ...
+void launch_cg_update_r_dev(Reducer& red, const double* rho, const double* curv, const double2* q, double2* r,
+                            size_t n, cudaStream_t s);
+// ... then x += alpha p_k fused into p = z + beta p_k (one pass over p), or alone
+void launch_xpby_x_dev(const double2* z, const double* rho_new, const double* rho_old, const double* curv,
+                       double2* p, double2* x, size_t n, cudaStream_t s);
+void launch_x_update_dev(const double* rho, const double* curv, const double2* p, double2* x, size_t n,
+                         cudaStream_t s);
 void launch_xpby_dev(const double2* z, const double* rho_new, const double* rho_old, double2* p, size_t n,
                      cudaStream_t s);
 // p = z + beta p   (krylov.cpp:109-110)
@@ -209,7 +217,11 @@ struct FdBlocks {
     DevBuf ab;
     DevBuf piv;         // uint8 pivot offsets piv[k]-k in 0..p (not used with rec)
     int rec = 0;
-    DevBuf flag;        // int: singular-pivot flag set by the factor kernel
+    DevBuf flag;        // int: bit 0 singular pivot, bit 1 some row interchange (factor kernel)
+    bool nopiv = false; // no block pivoted at all
+    DevBuf wpiv;        // uint8 per 32 consecutive blocks: some block pivoted (pair solve takes
+                        // the fill-in-free body for warps whose blocks did not)
+    bool nopiv_off = false; // KS_FD_NOPIV=0 at factor time: full band everywhere
     DevBuf lam_blk;     // double [nblk] composite eigenvalue of each block
     DevBuf fiber_block; // int [ns] block of each fiber (empty = identity)
     // pair mode (d = 3, axes 2 and 3 identical): block b = i1 + n1 * pidx over

@@ -755,16 +755,19 @@ void kron_apply(KronPlan& P, const double2* x, double2* y, cudaStream_t st,
                     cudaEventDestroy(b);
                     return ok ? ms : 1e30f;
                 };
+                // three interleaved rounds, best of each candidate (single launches
+                // of ~0.3 ms differ by a few percent from run to run)
                 time_one(*P.jit[k]); // warm-up launches (lazy module loading, L2)
                 for (auto& alt : P.jit_alt[k]) time_one(*alt);
-                float best = time_one(*P.jit[k]);
-                for (auto& alt : P.jit_alt[k]) {
-                    const float t = time_one(*alt);
-                    if (t < best) {
-                        best = t;
-                        std::swap(P.jit[k], alt);
-                    }
+                std::vector<float> tb(P.jit_alt[k].size() + 1, 1e30f);
+                for (int round = 0; round < 3; ++round) {
+                    tb[0] = std::min(tb[0], time_one(*P.jit[k]));
+                    for (size_t a = 0; a < P.jit_alt[k].size(); ++a) tb[a + 1] = std::min(tb[a + 1], time_one(*P.jit_alt[k][a]));
                 }
+                size_t bi = 0;
+                for (size_t a = 1; a < tb.size(); ++a)
+                    if (tb[a] < tb[bi]) bi = a;
+                if (bi > 0) std::swap(P.jit[k], P.jit_alt[k][bi - 1]);
                 P.jit_alt[k].clear();
             }
             if (kron_jit_launch(*P.jit[k], ip, op, host_ptrs.data() + P.ptr_off[k],

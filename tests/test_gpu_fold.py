@@ -147,3 +147,19 @@ def test_axis1_time_major_handoff(gpu, oracle, d, p, n_el, n_el_t):
     for i in (0, 1, n1 - 1, n1 + 3, o.N // a["dims"][0] - 1):
         b0, b1 = g0.block(i, p), g1.block(i, p)
         assert np.array_equal(b0[0], b1[0]) and np.array_equal(b0[1], b1[1])
+
+
+@pytest.mark.parametrize("d,p,n_el,n_el_t", [(3, 2, 16, 8), (3, 4, 11, 4)])
+def test_no_pivot_pair_solve_bitexact(gpu, oracle, d, p, n_el, n_el_t, monkeypatch):
+    """Warps whose 32 blocks did not pivot (all but the smallest-eigenvalue
+    blocks) skip the fill-in band and the pivots in the pair solve; the
+    skipped entries are exact zeros, so the application is bit-identical to
+    the full band read (KS_FD_NOPIV=0)."""
+    monkeypatch.setenv("KS_FD_NOPIV", "0")
+    _, g0, o = _pair(gpu, oracle, d, p, n_el, n_el_t)
+    monkeypatch.setenv("KS_FD_NOPIV", "1")
+    _, g1, _ = _pair(gpu, oracle, d, p, n_el, n_el_t)
+    r = oracle.random_vec(o.N, 29)
+    z0, z1 = g0.apply(r), g1.apply(r)
+    assert np.array_equal(z0, z1)
+    assert rel(z1, o.apply(r)) <= TOL

@@ -250,3 +250,23 @@ def test_pcg_graph_replay_matches_eager(gpu, oracle, monkeypatch):
     assert reps[0].iterations == reps[1].iterations and reps[0].converged and reps[1].converged
     assert np.array_equal(np.asarray(reps[0].x), np.asarray(reps[1].x))
     assert list(reps[0].res_history) == list(reps[1].res_history)
+
+
+@pytest.mark.parametrize("strict,maxit", [(False, 100), (True, 100), (False, 3)])
+def test_pcg_deferred_x_update_bitexact(gpu, oracle, monkeypatch, strict, maxit):
+    """x += alpha_k p_k deferred into the p update (default) vs applied with
+    the r update (KS_PCG_XDEFER=0): same arithmetic on the same operands, so
+    identical bits -- also when the solve stops at maxit with the last update
+    pending, and in strict mode (x needed every iteration)."""
+    a = setup_arrays(gpu, 3, 2, 6, 5)
+    b = oracle.random_vec(a["prob"].N_dof, 23)
+    reps = []
+    for v in ("0", "1"):
+        monkeypatch.setenv("KS_PCG_XDEFER", v)
+        A = gpu.assemble_system_operator(a["prob"])
+        P = gpu.FDPreconditioner(a["prob"])
+        reps.append(gpu.pcg(A, P, b, gpu.PcgOptions(1e-10, maxit, strict)))
+    assert reps[0].iterations == reps[1].iterations
+    assert reps[0].converged == reps[1].converged == (maxit == 100)
+    assert np.array_equal(np.asarray(reps[0].x), np.asarray(reps[1].x))
+    assert list(reps[0].res_history) == list(reps[1].res_history)
