@@ -303,10 +303,22 @@ ks_pair(const double2* const* __restrict__ ip, double2* const* __restrict__ op, 
         }
     }
     const int nwin = pull ? nmid : nout;
+    // Rotating windows (default; KS_KRON_JIT_ROT=0 shifts them): the sweep is
+    // unrolled by W planes, so window position j of plane ib lives in the static
+    // register slot (ib + 1 + j) % W (pull) / (ib + j) % W (push) instead of
+    // being shifted every plane -- ncu showed the shifts as ~20% of the pass-1
+    // instructions (IMAD.MOV).
+    const bool rot = !(std::getenv("KS_KRON_JIT_ROT") && std::strcmp(std::getenv("KS_KRON_JIT_ROT"), "0") == 0);
+    auto WP = [&](const std::string& j) { return rot ? "(ph + 1 + (" + j + ")) % W" : j; };
+    auto WQ = [&](const std::string& j) { return rot ? "(ph + (" + j + ")) % W" : j; };
     s << "    double2 win[" << nwin << "][W];\n"
-      << "#pragma unroll\n    for (int h = 0; h < " << nwin << "; ++h)\n#pragma unroll\n        for (int j = 0; j < W; ++j) win[h][j] = Z;\n"
-      << "    for (int ib = 0; ib < n_b + BW; ++ib) {\n";
-    if (pull)
+      << "#pragma unroll\n    for (int h = 0; h < " << nwin << "; ++h)\n#pragma unroll\n        for (int j = 0; j < W; ++j) win[h][j] = Z;\n";
+    if (rot)
+        s << "    for (int ib0 = 0; ib0 < n_b + BW; ib0 += W) {\n#pragma unroll\n    for (int ph = 0; ph < W; ++ph) {\n"
+          << "        const int ib = ib0 + ph;\n        if (ib >= n_b + BW) break;\n";
+    else
+        s << "    for (int ib = 0; ib < n_b + BW; ++ib) {\n";
+    if (pull && !rot)
         s << "#pragma unroll\n        for (int h = 0; h < " << nmid
           << "; ++h)\n#pragma unroll\n            for (int j = 0; j < W - 1; ++j) win[h][j] = win[h][j + 1];\n";
     s << "        if (ib < n_b) {\n"
@@ -341,9 +353,10 @@ ks_pair(const double2* const* __restrict__ ip, double2* const* __restrict__ op, 
     for (auto& c : b)
         if (c.factor >= 0) fb.insert(c.factor);
     if (pull) {
-        for (int h = 0; h < nmid; ++h) s << "            win[" << h << "][W - 1] = m" << h << ";\n";
+        const std::string newest = rot ? "ph" : "W - 1";
+        for (int h = 0; h < nmid; ++h) s << "            win[" << h << "][" << newest << "] = m" << h << ";\n";
         s << "        } else {\n";
-        for (int h = 0; h < nmid; ++h) s << "            win[" << h << "][W - 1] = Z;\n";
+        for (int h = 0; h < nmid; ++h) s << "            win[" << h << "][" << newest << "] = Z;\n";
         s << "        }\n        const int rd = ib - BW;\n        if (rd < 0) continue;\n";
         // axis-b rows at row rd (uniform across the CTA)
         for (int f : fb) {
@@ -360,10 +373,10 @@ ks_pair(const double2* const* __restrict__ ip, double2* const* __restrict__ op, 
             const int h = pr.first, f = pr.second;
             const std::string v = "d" + lit(h) + "_" + (f < 0 ? std::string("I") : lit(f));
             if (f < 0) {
-                s << "        const double2 " << v << " = win[" << h << "][BW];\n";
+                s << "        const double2 " << v << " = win[" << h << "][" << WP("BW") << "];\n";
             } else {
                 s << "        double2 " << v << " = Z;\n#pragma unroll\n        for (int j = 0; j < W; ++j) {"
-                  << mac(f, v, "B" + lit(f) + "[j]", "win[" + lit(h) + "][j]") << " }\n";
+                  << mac(f, v, "B" + lit(f) + "[j]", "win[" + lit(h) + "][" + WP("j") + "]") << " }\n";
             }
         }
         for (int o = 0; o < nout; ++o) {
@@ -374,7 +387,7 @@ ks_pair(const double2* const* __restrict__ ip, double2* const* __restrict__ op, 
                       << "\n";
             s << "          if (valid) P.out[" << o << "][base + s_b * rd] = acc; }\n";
         }
-        s << "    }\n";
+        s << (rot ? "    }\n    }\n" : "    }\n");
     } else {
         // push: column ib of each axis-b factor, F(ib + j - BW, ib), uniform
         for (int f : fb) {
@@ -393,20 +406,27 @@ ks_pair(const double2* const* __restrict__ ip, double2* const* __restrict__ op, 
             for (auto& c : b)
                 if (c.out == o && c.factor == f) s << "              " << cmac("cm", c.coeff, "m" + lit(c.in)) << "\n";
             if (f < 0) {
-                s << "              win[" << o << "][BW].x += cm.x; win[" << o << "][BW].y += cm.y; }\n";
+                s << "              win[" << o << "][" << WQ("BW") << "].x += cm.x; win[" << o << "][" << WQ("BW")
+                  << "].y += cm.y; }\n";
             } else if (is_scal(f)) {
                 s << "#pragma unroll\n              for (int j = 0; j < W; ++j) {"
-                  << mac(f, "win[" + lit(o) + "][j]", "C" + lit(f) + "[j]", "cm") << " } }\n";
+                  << mac(f, "win[" + lit(o) + "][" + WQ("j") + "]", "C" + lit(f) + "[j]", "cm") << " } }\n";
             } else {
-                s << "#pragma unroll\n              for (int j = 0; j < W; ++j) cacc(win[" << o << "][j], C" << f
+                s << "#pragma unroll\n              for (int j = 0; j < W; ++j) cacc(win[" << o << "][" << WQ("j") << "], C" << f
                   << "[j], cm); }\n";
             }
         }
         s << "        }\n        const int rd = ib - BW;\n        if (rd >= 0 && valid) {\n";
-        for (int o = 0; o < nout; ++o) s << "            P.out[" << o << "][base + s_b * rd] = win[" << o << "][0];\n";
-        s << "        }\n#pragma unroll\n        for (int o = 0; o < " << nout
-          << "; ++o) {\n#pragma unroll\n            for (int j = 0; j < W - 1; ++j) win[o][j] = win[o][j + 1];\n"
-          << "            win[o][W - 1] = Z;\n        }\n    }\n";
+        for (int o = 0; o < nout; ++o)
+            s << "            P.out[" << o << "][base + s_b * rd] = win[" << o << "][" << WQ("0") << "];\n";
+        if (rot) {
+            // the stored slot becomes the newest position of the next plane
+            s << "        }\n#pragma unroll\n        for (int o = 0; o < " << nout << "; ++o) win[o][ph] = Z;\n    }\n    }\n";
+        } else {
+            s << "        }\n#pragma unroll\n        for (int o = 0; o < " << nout
+              << "; ++o) {\n#pragma unroll\n            for (int j = 0; j < W - 1; ++j) win[o][j] = win[o][j + 1];\n"
+              << "            win[o][W - 1] = Z;\n        }\n    }\n";
+        }
     }
     s << "    asm volatile(\"cp.async.wait_group 0;\\n\" ::);\n}\n";
     if (const char* dump = std::getenv("KS_KRON_JIT_DUMP")) { // debugging: append the generated source
