@@ -183,8 +183,20 @@ KronJitPair* kron_jit_build(int nin, int nmid, int nout, int bw, const std::vect
                    ".y);";
         return " cacc(" + v + ", " + fv + ", " + w + ");";
     };
-    // acc += c * v with the contribution coefficient (real coefficients: 2 DFMA)
+    // acc += c * v with the contribution coefficient (real coefficients: 2 DFMA).
+    // Unit coefficients (exactly +-1, the common case: nu = 1 and the plan's
+    // merged rows) become a copy / an add, and the first contribution into a
+    // still-zero accumulator a plain assignment -- bit-identical (1*v = v,
+    // 0 + v = v) and up to 2 DFMA less per contribution (KS_KRON_JIT_UNIT=0 off).
+    const bool unit_ok = !(std::getenv("KS_KRON_JIT_UNIT") && std::strcmp(std::getenv("KS_KRON_JIT_UNIT"), "0") == 0);
+    std::set<std::string> live; // accumulators already holding a contribution
     auto cmac = [&](const std::string& acc, int ci, const std::string& v) -> std::string {
+        const bool fresh = live.insert(acc).second;
+        if (unit_ok && coeffs[ci].y == 0.0 && (coeffs[ci].x == 1.0 || coeffs[ci].x == -1.0)) {
+            const bool neg = coeffs[ci].x == -1.0;
+            if (fresh) return acc + ".x = " + (neg ? "-" : "") + v + ".x; " + acc + ".y = " + (neg ? "-" : "") + v + ".y;";
+            return acc + ".x " + (neg ? "-" : "+") + "= " + v + ".x; " + acc + ".y " + (neg ? "-" : "+") + "= " + v + ".y;";
+        }
         if (coeffs[ci].y == 0.0)
             return acc + ".x = fma(P.c[" + lit(ci) + "].x, " + v + ".x, " + acc + ".x); " + acc + ".y = fma(P.c[" + lit(ci) +
                    "].x, " + v + ".y, " + acc + ".y);";
@@ -326,6 +338,7 @@ ks_pair(const double2* const* __restrict__ ip, double2* const* __restrict__ op, 
       << "            __syncthreads();\n            issue(ib + D - 1);\n"
       << "            const double2* sl = ring + (ib % D) * (NIN * RS) + PAD + tid;\n";
     for (int h = 0; h < nmid; ++h) s << "            double2 m" << h << " = Z;\n";
+    live.clear();
     // axis a: per input g, taps once, per distinct factor one product, then the coefficients
     for (int g = 0; g < nin; ++g) {
         std::vector<const JitContrib*> cs;
@@ -381,6 +394,7 @@ ks_pair(const double2* const* __restrict__ ip, double2* const* __restrict__ op, 
         }
         for (int o = 0; o < nout; ++o) {
             s << "        { double2 acc = Z;\n";
+            live.erase("acc");
             for (auto& c : b)
                 if (c.out == o)
                     s << "          " << cmac("acc", c.coeff, "d" + lit(c.in) + "_" + (c.factor < 0 ? std::string("I") : lit(c.factor)))
@@ -403,6 +417,7 @@ ks_pair(const double2* const* __restrict__ ip, double2* const* __restrict__ op, 
         for (auto& pr : of) {
             const int o = pr.first, f = pr.second;
             s << "            { double2 cm = Z;\n";
+            live.erase("cm");
             for (auto& c : b)
                 if (c.out == o && c.factor == f) s << "              " << cmac("cm", c.coeff, "m" + lit(c.in)) << "\n";
             if (f < 0) {
