@@ -137,14 +137,21 @@ inline cudaStream_t pick(void* user, cudaStream_t own) {
 
 // FD apply on device pointers (Algorithm 1 steps 2-4; fdsolver.cpp:53-63).
 // ev (optional): start/stop event pairs recorded around each transform kernel.
+// dot (optional): also leave Re <r, z> in dot->result[0] -- fused into the last
+// inverse transform on the axis-1 time-major path, a separate reduction otherwise
 void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStream_t st,
-                  std::vector<cudaEvent_t>* ev) {
+                  std::vector<cudaEvent_t>* ev, Reducer* dot = nullptr) {
+    if (dot && !(f->tm1 && !f->fused && f->fold[f->d - 1].n && r != z)) {
+        fd_apply_dev(f, r, z, adjoint, st, ev, nullptr);
+        launch_dotc(*dot, r, z, f->N, st);
+        return;
+    }
     const int d = f->d;
     const double* cur = reinterpret_cast<const double*>(r);
     double* bufs[2] = {f->s0.as<double>(), f->s1.as<double>()};
     int nb = 0;
     size_t s = f->dims[0];
-    auto gemm = [&](const DevBuf& At, int l, const double* in, double* out, int layout) {
+    auto gemm = [&](const DevBuf& At, int l, const double* in, double* out, int layout, Reducer* red = nullptr) {
         const int n = f->dims[l];
         size_t stride = 1;
         for (int k = 0; k < l; ++k) stride *= (size_t)f->dims[k];
@@ -152,7 +159,9 @@ void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStre
         const FoldAxis& F = f->fold[l - 1];
         const bool inv = &At == &f->At_inv[l - 1];
         auto launch = [&]() {
-            if (F.n) launch_mode_gemm_fold(F, inv, in, out, stride, outer, st, layout, f->dims[0]);
+            if (F.n)
+                launch_mode_gemm_fold(F, inv, in, out, stride, outer, st, layout, f->dims[0], nullptr, nullptr,
+                                      reinterpret_cast<const double*>(r), red);
             else launch_mode_gemm(At.as<double>(), n, in, out, stride, outer, st, layout, f->dims[0]);
         };
         if (ev) {
@@ -252,7 +261,7 @@ void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStre
         for (int l = 1; l <= d; ++l) {
             double* out = l == d ? reinterpret_cast<double*>(z) : bufs[nb];
             if (l != d) nb ^= 1;
-            gemm(f->At_inv[l - 1], l, cur, out, l == 1 ? 4 : 0);
+            gemm(f->At_inv[l - 1], l, cur, out, l == 1 ? 4 : 0, l == d ? dot : nullptr);
             cur = out;
         }
         return;
@@ -974,6 +983,16 @@ int ks_pcg(ks_kron* A, ks_fd* P, const ks_c64* b, ks_c64* x, int mem, const ks_p
         return !(e && std::strcmp(e, "0") == 0);
     }();
     bool pending = false; // x += alpha_k p_k not yet applied
+    // rho' = Re <r, P r> reduced inside the preconditioner's last transform
+    // (opt-in KS_PCG_FUSEDOT=1; rounding-level change of rho', same counts).
+    // Measured c3: the DOT transform takes 233 us against 124 us + 91 us for
+    // the plain transform and the separate dotc -- its epilogue waits on the r
+    // loads (no register or shared-memory room to prefetch them) -- so the
+    // separate reduction stays the default.
+    const bool fuse_dot = [] {
+        const char* e = std::getenv("KS_PCG_FUSEDOT");
+        return e && std::strcmp(e, "1") == 0;
+    }();
     auto apply_x = [&]() {
         if (!pending) return;
         launch_x_update_dev(rho_old.result.as<double>(), red_c.result.as<double>(), p.as<double2>(), xv.as<double2>(),
@@ -993,9 +1012,14 @@ int ks_pcg(ks_kron* A, ks_fd* P, const ks_c64* b, ks_c64* x, int mem, const ks_p
         KS_CUDA(cudaMemcpyAsync(red_u.host, red_u.result.p, sizeof(double), cudaMemcpyDeviceToHost, st));
     };
     auto phase_b = [&]() {
-        if (P) fd_apply_dev(P, r.as<double2>(), z.as<double2>(), false, st, nullptr);
-        else KS_CUDA(cudaMemcpyAsync(z.p, r.p, bytes, cudaMemcpyDeviceToDevice, st));
-        launch_dotc(rho_new, r.as<double2>(), z.as<double2>(), n, st); // rho'
+        // z = P r and rho' = Re <r, z> (fused into the FD's last transform when it can be)
+        if (P && fuse_dot) {
+            fd_apply_dev(P, r.as<double2>(), z.as<double2>(), false, st, nullptr, &rho_new);
+        } else {
+            if (P) fd_apply_dev(P, r.as<double2>(), z.as<double2>(), false, st, nullptr);
+            else KS_CUDA(cudaMemcpyAsync(z.p, r.p, bytes, cudaMemcpyDeviceToDevice, st));
+            launch_dotc(rho_new, r.as<double2>(), z.as<double2>(), n, st); // rho'
+        }
         if (pending) { // (the caller clears pending: a replayed graph does not run this body)
             launch_xpby_x_dev(z.as<double2>(), rho_new.result.as<double>(), rho_old.result.as<double>(),
                               red_c.result.as<double>(), p.as<double2>(), xv.as<double2>(), n, st);

@@ -164,9 +164,11 @@ bool fold_axis_build(const double* U, const double* lam, int n, double tol, Fold
 bool fold12_supported(const FoldAxis& F1, const FoldAxis& F2);
 void launch_fold12(const FoldAxis& F1, const FoldAxis& F2, bool inverse, const double* X, double* Y, int n0,
                    long long outer, cudaStream_t st);
+// dot (optional, plain inverse transforms): also reduce Re <dot_x, Y> into dot->result[0]
 void launch_mode_gemm_fold(const FoldAxis& F, bool inverse, const double* X, double* Y,
                            size_t s_complex, size_t outer, cudaStream_t st, int layout = 0, int nt = 0,
-                           const double* const* rows_in = nullptr, double* const* rows_out = nullptr);
+                           const double* const* rows_in = nullptr, double* const* rows_out = nullptr,
+                           const double* dot_x = nullptr, Reducer* dot = nullptr);
 
 // ---------------------------------------------------------------------------
 // plan-specialised fused level passes (ks_kron_jit.cu, NVRTC at plan creation)

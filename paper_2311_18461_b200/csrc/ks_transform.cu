@@ -345,6 +345,13 @@ struct ColMap {
     // (the peer-memory sharded FD: rows of axis d on other GPUs)
     const double* const* rin = nullptr;
     double* const* rout = nullptr;
+    // optional fused reduction (inverse folded transform, DOT variant): Re <x, Y>
+    // over the written output, per-CTA partials + last-block sum in block order
+    // into res[0] (a Reducer's buffers: partial, counter, result)
+    const double* dx = nullptr;
+    double* dpart = nullptr;
+    unsigned* dcnt = nullptr;
+    double* dres = nullptr;
 };
 template <bool ROWS>
 __device__ __forceinline__ const double* in_row(const ColMap& M, const double* X, long long col, int j,
@@ -754,7 +761,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 // ---------------------------------------------------------------------------
 // RL: loader lanes along rows instead of columns (MAP_TIN1: a column's rows
 // are contiguous on the time-major side, so a warp reads 2 x 256 B runs)
-template <int TH, bool INV, int KC, int STG, int MINB, int BNC, bool TMA, bool ROWS = false, bool RL = false>
+// DOT: also reduce Re <M.dx, Y> over the written output (PCG: rho = Re <r, P r>)
+template <int TH, bool INV, int KC, int STG, int MINB, int BNC, bool TMA, bool ROWS = false, bool RL = false,
+          bool DOT = false>
 __global__ void __launch_bounds__(kThreads, MINB)
 k_mode_gemm_fold(const double* __restrict__ Af, int Kst, const int* __restrict__ rmap, int n, int hc, int nkc,
                  const double* __restrict__ X, double* __restrict__ Y, ColMap M, int dry) {
@@ -926,6 +935,7 @@ k_mode_gemm_fold(const double* __restrict__ Af, int Kst, const int* __restrict__
     };
 
     double acc[2][MT][NF][2];
+    double dacc = 0.0; // DOT: this thread's share of Re <x, Y>
 #pragma unroll
     for (int g = 0; g < 2; ++g)
 #pragma unroll
@@ -989,11 +999,22 @@ k_mode_gemm_fold(const double* __restrict__ Af, int Kst, const int* __restrict__
                             if (h < hc) *reinterpret_cast<double2*>(out_row<ROWS>(M, Y, oo, rE[h], out_rs)) = e;
                             if (h < no) *reinterpret_cast<double2*>(out_row<ROWS>(M, Y, oo, rO[h], out_rs)) = o;
                         } else if (h < hc) {
-                            *reinterpret_cast<double2*>(out_row<ROWS>(M, Y, oo, h, out_rs)) =
-                                make_double2(e.x + o.x, e.y + o.y);
-                            if (n - 1 - h != h)
-                                *reinterpret_cast<double2*>(out_row<ROWS>(M, Y, oo, n - 1 - h, out_rs)) =
-                                    make_double2(e.x - o.x, e.y - o.y);
+                            const double2 v1 = make_double2(e.x + o.x, e.y + o.y);
+                            *reinterpret_cast<double2*>(out_row<ROWS>(M, Y, oo, h, out_rs)) = v1;
+                            if (DOT) {
+                                const double2 x1 = __ldg(reinterpret_cast<const double2*>(
+                                    out_row<false>(M, const_cast<double*>(M.dx), oo, h, out_rs)));
+                                dacc = fma(x1.x, v1.x, fma(x1.y, v1.y, dacc));
+                            }
+                            if (n - 1 - h != h) {
+                                const double2 v2 = make_double2(e.x - o.x, e.y - o.y);
+                                *reinterpret_cast<double2*>(out_row<ROWS>(M, Y, oo, n - 1 - h, out_rs)) = v2;
+                                if (DOT) {
+                                    const double2 x2 = __ldg(reinterpret_cast<const double2*>(
+                                        out_row<false>(M, const_cast<double*>(M.dx), oo, n - 1 - h, out_rs)));
+                                    dacc = fma(x2.x, v2.x, fma(x2.y, v2.y, dacc));
+                                }
+                            }
                         }
                     }
                 }
@@ -1004,6 +1025,30 @@ k_mode_gemm_fold(const double* __restrict__ Af, int Kst, const int* __restrict__
         }
     }
     cp_async_wait<0>();
+    if (DOT) { // fixed tree per CTA, then the last CTA sums the partials in block order
+        __shared__ double red[kThreads / 32];
+        __shared__ bool last;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) dacc += __shfl_down_sync(0xffffffffu, dacc, o);
+        if (lane == 0) red[warp] = dacc;
+        __syncthreads();
+        if (tid == 0) {
+            double sum = 0.0;
+            for (int q = 0; q < kThreads / 32; ++q) sum += red[q];
+            M.dpart[blockIdx.x] = sum;
+            __threadfence();
+            last = atomicAdd(M.dcnt, 1u) == gridDim.x - 1;
+        }
+        __syncthreads();
+        if (last && tid == 0) {
+            __threadfence();
+            double sum = 0.0;
+            for (unsigned q = 0; q < gridDim.x; ++q) sum += ((volatile double*)M.dpart)[q];
+            M.dres[0] = sum;
+            M.dres[1] = 0.0;
+            *M.dcnt = 0u;
+        }
+    }
 }
 
 // fold kernel configuration: pair rows per stage (KC), ring stages, CTAs per SM
@@ -1075,6 +1120,20 @@ void launch_fold_cfg(const FoldAxis& F, const double* X, double* Y, ColMap M, cu
         } else {
             k_mode_gemm_fold<TH, INV, KC, STG, MINB, BNC, false><<<g, kThreads, sm, st>>>(A, F.kst, rm, F.n, F.hc,
                                                                                           nkc, X, Y, M, dry_run());
+        }
+    } else if (M.dx) {
+        if constexpr (INV) {
+            static bool attr_d = false;
+            if (!attr_d) {
+                // (the DOT variant has ~80 B of static shared memory)
+                KS_CUDA(cudaFuncSetAttribute(k_mode_gemm_fold<TH, INV, KC, STG, MINB, BNC, false, false, false, true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
+                attr_d = true;
+            }
+            k_mode_gemm_fold<TH, INV, KC, STG, MINB, BNC, false, false, false, true><<<g, kThreads, sm, st>>>(
+                A, F.kst, F.rmap.as<int>(), F.n, F.hc, nkc, X, Y, M, dry_run());
+        } else {
+            throw Error(KS_EINVAL, "fused dot: inverse transforms only");
         }
     } else {
         k_mode_gemm_fold<TH, INV, KC, STG, MINB, BNC, TMA><<<g, kThreads, sm, st>>>(A, F.kst, F.rmap.as<int>(), F.n,
@@ -1294,11 +1353,19 @@ bool fold_axis_build(const double* U_in, const double* lam, int n, double tol, F
 
 void launch_mode_gemm_fold(const FoldAxis& F, bool inverse, const double* X, double* Y, size_t s_complex,
                            size_t outer, cudaStream_t st, int layout, int nt, const double* const* rows_in,
-                           double* const* rows_out) {
+                           double* const* rows_out, const double* dot_x, Reducer* dot) {
     if (s_complex == 0 || outer == 0) return;
     ColMap M = make_colmap(F.n, s_complex, outer, layout, nt);
     M.rin = rows_in;
     M.rout = rows_out;
+    if (dot) {
+        KS_REQUIRE(inverse && layout == MAP_STD && !rows_in && !rows_out && dot_x, KS_EINVAL,
+                   "fused dot: plain inverse transform only");
+        M.dx = dot_x;
+        M.dpart = dot->partial.as<double>();
+        M.dcnt = dot->counter.as<unsigned>();
+        M.dres = dot->result.as<double>();
+    }
 #define KS_FOLD_CASE(T)                                                                            \
     case T:                                                                                        \
         if (inverse) launch_fold_th<T, true>(F, X, Y, M, st);                                      \

@@ -270,3 +270,28 @@ def test_pcg_deferred_x_update_bitexact(gpu, oracle, monkeypatch, strict, maxit)
     assert reps[0].converged == reps[1].converged == (maxit == 100)
     assert np.array_equal(np.asarray(reps[0].x), np.asarray(reps[1].x))
     assert list(reps[0].res_history) == list(reps[1].res_history)
+
+
+@pytest.mark.parametrize("d,p,n_el", [(3, 2, 8), (3, 3, 7)])
+def test_pcg_fused_rho_matches_separate_dot(gpu, oracle, monkeypatch, d, p, n_el):
+    """rho' = Re <r, P r> reduced inside the preconditioner's last inverse
+    transform (opt-in KS_PCG_FUSEDOT=1, pair-mode path) vs the separate dotc
+    (default): only the summation order differs -- same iteration
+    count, iterates equal to rounding, and both match the oracle's solve."""
+    a = setup_arrays(gpu, d, p, n_el, n_el)
+    b = oracle.random_vec(a["prob"].N_dof, 31)
+    reps = []
+    for v in ("0", "1"):
+        monkeypatch.setenv("KS_PCG_FUSEDOT", v)
+        A = gpu.assemble_system_operator(a["prob"])
+        P = gpu.FDPreconditioner(a["prob"])
+        assert P.info()["time_major_axis"] == 1
+        reps.append(gpu.pcg(A, P, b, gpu.PcgOptions(1e-10, 100)))
+    assert reps[0].converged and reps[1].converged
+    assert reps[0].iterations == reps[1].iterations
+    assert rel(reps[1].x, reps[0].x) < 1e-11
+    K = oracle.OracleKron(a["dims"], oracle.system_terms(a, d, a["nu"]))
+    F = oracle.OracleFD(a["dims"], a["nu"], a["p"], a["U"], a["lam"], a["Lt"], a["Mt"], a["Wt"])
+    ro = oracle.oracle_pcg(K.apply, F.apply, b, 1e-10, 100)
+    assert abs(reps[1].iterations - ro["iterations"]) <= 1
+    assert rel(reps[1].x, ro["x"]) < 1e-8
