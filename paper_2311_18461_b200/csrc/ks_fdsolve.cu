@@ -76,7 +76,8 @@ __device__ __forceinline__ double cabs_(double2 a) { return hypot(a.x, a.y); }
 // and eliminates in place.
 // ---------------------------------------------------------------------------
 __global__ void k_fd_factor(double2* __restrict__ ab, unsigned char* __restrict__ piv,
-                            int* __restrict__ flag, unsigned char* __restrict__ wpiv, size_t ns, int nt, int p,
+                            int* __restrict__ flag, unsigned char* __restrict__ wpiv,
+                            unsigned char* __restrict__ bpiv, size_t ns, int nt, int p,
                             const double* __restrict__ lam_blk, double nu,
                             const double* __restrict__ Lt, const double* __restrict__ Mt,
                             const double2* __restrict__ Wsym, int rec, int fused_nd, long long fused_np,
@@ -124,14 +125,16 @@ __global__ void k_fd_factor(double2* __restrict__ ab, unsigned char* __restrict_
         bool& s;
         int* f;
         unsigned char* w;
+        unsigned char* bp;
         size_t i;
         __device__ ~SwapFlag() {
             if (s) {
                 atomicOr(f, 2);
                 w[i >> 5] = 1; // every writer stores 1
             }
+            bp[i] = s ? 1 : 0;
         }
-    } swap_flag{swapped, flag, wpiv, i};
+    } swap_flag{swapped, flag, wpiv, bpiv, i};
     for (int k = 0; k < nt; ++k) {
         const int imax = k + p < nt - 1 ? k + p : nt - 1;
         int pr = k;
@@ -364,18 +367,15 @@ __device__ __forceinline__ void cpa4(void* sdst, const void* g, bool v) {
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N> __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-template <int P, int D, int TB = 128>
-__global__ void __launch_bounds__(TB) k_fd_solve_ring(const double2* __restrict__ ab,
-                                                       const unsigned char* __restrict__ piv,
-                                                       double2* __restrict__ X, size_t ns, int nt, size_t nblk,
-                                                       const int* __restrict__ fblk, int rec, int fnd,
-                                                       long long fnp) {
+// NP: this warp's fibers' blocks did not pivot (see k_fd_solve_pair)
+template <int P, int D, int TB, bool NP>
+__device__ __forceinline__ void fd_ring_body(const double2* __restrict__ ab, const unsigned char* __restrict__ piv,
+                                             double2* __restrict__ X, size_t ns, int nt, size_t nblk,
+                                             const int* __restrict__ fblk, int rec, int fnd, long long fnp,
+                                             double2* ring, size_t f) {
     constexpr int ldab = 3 * P + 1, kuf = 2 * P, NE = 2 * P + 2;
-    extern __shared__ __align__(16) double2 ring[]; // [D][NE][TB], then int [D][TB]
     unsigned* pr = reinterpret_cast<unsigned*>(ring + (size_t)D * NE * TB);
     const int t = threadIdx.x;
-    const size_t f = blockIdx.x * (size_t)TB + t;
-    if (f >= ns) return;
     double2* x = X + f; // x[k * ns]
     const size_t i = fblk ? (size_t)__ldg(fblk + f) : f;
     const BandIndex bx = fd_band_index(i, nt, ldab, nblk, rec, fnd, fnp);
@@ -387,7 +387,8 @@ __global__ void __launch_bounds__(TB) k_fd_solve_ring(const double2* __restrict_
 #pragma unroll
             for (int m = 1; m <= P; ++m) cpa16(slot(k, m - 1), k + m < nt ? baddr(k, kuf + m) : ab, k + m < nt);
             cpa16(slot(k, P), k + P + 1 < nt ? x + (size_t)(k + P + 1) * ns : X, k + P + 1 < nt);
-            if (rec > 0) {
+            if (NP) {
+            } else if (rec > 0) {
                 cpa16(slot(k, P + 1), baddr(k, ldab), true);
             } else {
                 const size_t o = bx.pb + (size_t)k * bx.pk;
@@ -397,6 +398,7 @@ __global__ void __launch_bounds__(TB) k_fd_solve_ring(const double2* __restrict_
         cpa_commit();
     };
     auto pivot_of = [&](int k) -> int {
+        if (NP) return 0;
         if (rec > 0) return (int)slot(k, P + 1)->x;
         const size_t o = bx.pb + (size_t)k * bx.pk;
         return (int)((pr[(k % D) * TB + t] >> (8 * (unsigned)(o & 3))) & 0xffu);
@@ -432,7 +434,7 @@ __global__ void __launch_bounds__(TB) k_fd_solve_ring(const double2* __restrict_
     auto issue_b = [&](int k) {
         if (k >= 0) {
 #pragma unroll
-            for (int j = 0; j <= 2 * P; ++j) cpa16(slot(k, j), k - j >= 0 ? baddr(k, kuf - j) : ab, k - j >= 0);
+            for (int j = 0; j <= (NP ? P : 2 * P); ++j) cpa16(slot(k, j), k - j >= 0 ? baddr(k, kuf - j) : ab, k - j >= 0);
             const int kx = k - 2 * P - 1;
             cpa16(slot(k, 2 * P + 1), kx >= 0 ? x + (size_t)kx * ns : X, kx >= 0);
         }
@@ -453,7 +455,7 @@ __global__ void __launch_bounds__(TB) k_fd_solve_ring(const double2* __restrict_
             u[0] = cmul(u[0], make_double2(dg.x * sc, -dg.y * sc));
         }
 #pragma unroll
-        for (int j = 1; j <= 2 * P; ++j)
+        for (int j = 1; j <= (NP ? P : 2 * P); ++j)
             if (k - j >= 0) u[j] = csub(u[j], cmul(*slot(k, j), u[0]));
         x[(size_t)k * ns] = u[0];
         const double2 xin = *slot(k, 2 * P + 1);
@@ -461,6 +463,32 @@ __global__ void __launch_bounds__(TB) k_fd_solve_ring(const double2* __restrict_
         for (int j = 0; j < 2 * P; ++j) u[j] = u[j + 1];
         u[2 * P] = xin;
     }
+}
+
+// wpivf[f / 32] != 0: one of the 32 fibers' blocks pivoted (built after the
+// factorisation); null: full band everywhere
+template <int P, int D, int TB = 128>
+__global__ void __launch_bounds__(TB) k_fd_solve_ring(const double2* __restrict__ ab,
+                                                       const unsigned char* __restrict__ piv,
+                                                       double2* __restrict__ X, size_t ns, int nt, size_t nblk,
+                                                       const int* __restrict__ fblk, int rec, int fnd,
+                                                       long long fnp, const unsigned char* __restrict__ wpivf) {
+    extern __shared__ __align__(16) double2 ring[]; // [D][NE][TB], then int [D][TB]
+    const size_t f = blockIdx.x * (size_t)TB + threadIdx.x;
+    if (f >= ns) return;
+    if (wpivf && __ldg(wpivf + (f >> 5)) == 0)
+        fd_ring_body<P, D, TB, true>(ab, piv, X, ns, nt, nblk, fblk, rec, fnd, fnp, ring, f);
+    else
+        fd_ring_body<P, D, TB, false>(ab, piv, X, ns, nt, nblk, fblk, rec, fnd, fnp, ring, f);
+}
+
+// per-fiber-group pivot flags for the ring solve from the per-block flags
+__global__ void k_fiber_piv(const unsigned char* __restrict__ bpiv, const int* __restrict__ fblk, size_t ns,
+                            unsigned char* __restrict__ wpivf) {
+    const size_t f = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (f >= ns) return;
+    const size_t i = fblk ? (size_t)fblk[f] : f;
+    if (bpiv[i]) wpivf[f >> 5] = 1;
 }
 
 // ---------------------------------------------------------------------------
@@ -907,7 +935,8 @@ void launch_solve_p(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t st
                 KS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
                 const unsigned g = (unsigned)((B.ns + tb - 1) / tb);
                 kern<<<g, tb, sm, st>>>(B.ab.as<double2>(), B.piv.as<unsigned char>(), X, B.ns, B.nt, B.nblk,
-                                        B.fiber_block.as<int>(), B.rec, B.fused_nd, B.fused_np);
+                                        B.fiber_block.as<int>(), B.rec, B.fused_nd, B.fused_np,
+                                        B.nopiv_off ? nullptr : B.wpivf.as<unsigned char>());
             };
             // few fibers (c1, c2: < 2 x 148 CTAs of 128): one warp per CTA spreads
             // them over all SMs, and an 8-deep ring keeps more steps in flight
@@ -946,6 +975,8 @@ void fd_blocks_alloc(FdBlocks& B) {
     if (B.rec == 0) B.piv.alloc((size_t)B.nt * B.nblk + 4); // +4: 4 B cp.async words
     B.flag.alloc(sizeof(int));
     B.wpiv.alloc((B.nblk + 31) / 32 + 1);
+    B.bpiv.alloc(B.nblk + 1);
+    B.wpivf.alloc((B.ns + 31) / 32 + 1);
 }
 
 void fd_block_to_host(const FdBlocks& B, size_t b, ks_c64* ab, int* piv) {
@@ -973,7 +1004,7 @@ void launch_fd_factor(FdBlocks& B, double nu, const double* Lt, const double* Mt
     KS_CUDA(cudaMemsetAsync(B.wpiv.p, 0, B.wpiv.bytes, st));
     const unsigned grid = (unsigned)((B.nblk + 127) / 128);
     k_fd_factor<<<grid, 128, 0, st>>>(B.ab.as<double2>(), B.piv.as<unsigned char>(),
-                                      B.flag.as<int>(), B.wpiv.as<unsigned char>(), B.nblk, B.nt, B.p, B.lam_blk.as<double>(), nu,
+                                      B.flag.as<int>(), B.wpiv.as<unsigned char>(), B.bpiv.as<unsigned char>(), B.nblk, B.nt, B.p, B.lam_blk.as<double>(), nu,
                                       Lt, Mt, Wsym, B.rec, B.fused_nd, B.fused_np, B.kind);
     check_launch("k_fd_factor");
     int h = 0;
@@ -983,6 +1014,15 @@ void launch_fd_factor(FdBlocks& B, double nu, const double* Lt, const double* Mt
     // no row interchange in any block: U has bandwidth p, the 2p-row fill-in
     // band stays exactly zero, and the pair solve skips it (and the pivots)
     B.nopiv = (h & 2) == 0;
+    // fiber-group flags for the ring solve (fibers map to blocks through fiber_block)
+    KS_CUDA(cudaMemsetAsync(B.wpivf.p, 0, B.wpivf.bytes, st));
+    if (B.ns > 0) {
+        k_fiber_piv<<<(unsigned)((B.ns + 255) / 256), 256, 0, st>>>(
+            B.bpiv.as<unsigned char>(), B.fiber_block.bytes ? B.fiber_block.as<int>() : nullptr, B.ns,
+            B.wpivf.as<unsigned char>());
+        check_launch("k_fiber_piv");
+        KS_CUDA(cudaStreamSynchronize(st));
+    }
     B.nopiv_off = false;
     if (const char* e = std::getenv("KS_FD_NOPIV"))
         if (std::strcmp(e, "0") == 0) B.nopiv_off = true;

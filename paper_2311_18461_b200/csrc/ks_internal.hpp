@@ -224,6 +224,8 @@ struct FdBlocks {
     DevBuf wpiv;        // uint8 per 32 consecutive blocks: some block pivoted (pair solve takes
                         // the fill-in-free body for warps whose blocks did not)
     bool nopiv_off = false; // KS_FD_NOPIV=0 at factor time: full band everywhere
+    DevBuf bpiv;        // uint8 per block: pivoted
+    DevBuf wpivf;       // uint8 per 32 consecutive fibers: some fiber's block pivoted (ring solve)
     DevBuf lam_blk;     // double [nblk] composite eigenvalue of each block
     DevBuf fiber_block; // int [ns] block of each fiber (empty = identity)
     // pair mode (d = 3, axes 2 and 3 identical): block b = i1 + n1 * pidx over

@@ -149,10 +149,12 @@ def test_axis1_time_major_handoff(gpu, oracle, d, p, n_el, n_el_t):
         assert np.array_equal(b0[0], b1[0]) and np.array_equal(b0[1], b1[1])
 
 
-@pytest.mark.parametrize("d,p,n_el,n_el_t", [(3, 2, 16, 8), (3, 4, 11, 4)])
+@pytest.mark.parametrize("d,p,n_el,n_el_t", [(3, 2, 16, 8), (3, 4, 11, 4), (2, 3, 16, 8), (2, 2, 12, 6),
+                                            (1, 3, 16, 16)])
 def test_no_pivot_pair_solve_bitexact(gpu, oracle, d, p, n_el, n_el_t, monkeypatch):
-    """Warps whose 32 blocks did not pivot (all but the smallest-eigenvalue
-    blocks) skip the fill-in band and the pivots in the pair solve; the
+    """Warps whose 32 blocks (pair solve) or whose 32 fibers' blocks (ring
+    solve, d = 1, 2) did not pivot -- all but the smallest-eigenvalue ones --
+    skip the fill-in band and the pivots; the
     skipped entries are exact zeros, so the application is bit-identical to
     the full band read (KS_FD_NOPIV=0)."""
     monkeypatch.setenv("KS_FD_NOPIV", "0")
