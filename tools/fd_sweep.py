@@ -11,7 +11,7 @@ import sys, numpy as np
 sys.path.insert(0, %r)
 import paper_2311_18461_b200 as ks
 cfg = %r
-d, p, n_el = {"c3": (3, 2, 64), "c2": (2, 3, 64), "c5s": (3, 4, 64), "c4p2": (2, 2, 128), "c4p3": (2, 3, 128), "c5": (3, 4, 128)}[cfg]
+d, p, n_el = {"c3": (3, 2, 64), "c2": (2, 3, 64), "c5s": (3, 4, 64), "c4p2": (2, 2, 128), "c4p3": (2, 3, 128), "c4p4": (2, 4, 128), "c4p5": (2, 5, 128), "c4p6": (2, 6, 128), "c5": (3, 4, 128)}[cfg]
 prob = ks.SpaceTimeProblem.uniform(d, p, n_el, n_el)
 P = ks.FDPreconditioner(prob)
 n = prob.N_dof
