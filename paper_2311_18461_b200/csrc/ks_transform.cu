@@ -1160,6 +1160,12 @@ void launch_fold_th(const FoldAxis& F, const double* X, double* Y, const ColMap&
         }();
         if (tma && M.mode == MAP_STD && M.s >= 64 && !M.rin && !M.rout)
             return launch_fold_cfg<TH, INV, 16, 2, 2, 64, true>(F, X, Y, M, st);
+        // experiment hook (KS_FOLD_CFG): 1 = 32-column tiles, 4 stages, 2 CTA/SM;
+        // 2 = 32-column tiles, 3 stages, 3 CTA/SM. Measured c3 (part 5): six
+        // transforms 0.808 / 0.817 ms vs 0.770 ms for the default.
+        static const int cfg = std::getenv("KS_FOLD_CFG") ? std::atoi(std::getenv("KS_FOLD_CFG")) : 0;
+        if (cfg == 1) return launch_fold_cfg<TH, INV, 16, 4, 2, 32>(F, X, Y, M, st);
+        if (cfg == 2) return launch_fold_cfg<TH, INV, 16, 3, 3, 32>(F, X, Y, M, st);
         return launch_fold_cfg<TH, INV, 16, 2, 2, 64>(F, X, Y, M, st);
     }
     // small problems (c1, c2: fewer 64-column tiles than SMs): 32-column tiles
