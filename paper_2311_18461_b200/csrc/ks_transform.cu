@@ -996,11 +996,11 @@ k_mode_gemm_fold(const double* __restrict__ Af, int Kst, const int* __restrict__
                         const double2 e = make_double2(acc[0][i][m][0], acc[0][i][m][1]);
                         const double2 o = make_double2(acc[1][i][m][0], acc[1][i][m][1]);
                         if (!INV) {
-                            if (h < hc) *reinterpret_cast<double2*>(out_row<ROWS>(M, Y, oo, rE[h], out_rs)) = e;
-                            if (h < no) *reinterpret_cast<double2*>(out_row<ROWS>(M, Y, oo, rO[h], out_rs)) = o;
+                            if (h < hc) __stcs(reinterpret_cast<double2*>(out_row<ROWS>(M, Y, oo, rE[h], out_rs)), e);
+                            if (h < no) __stcs(reinterpret_cast<double2*>(out_row<ROWS>(M, Y, oo, rO[h], out_rs)), o);
                         } else if (h < hc) {
                             const double2 v1 = make_double2(e.x + o.x, e.y + o.y);
-                            *reinterpret_cast<double2*>(out_row<ROWS>(M, Y, oo, h, out_rs)) = v1;
+                            __stcs(reinterpret_cast<double2*>(out_row<ROWS>(M, Y, oo, h, out_rs)), v1);
                             if (DOT) {
                                 const double2 x1 = __ldg(reinterpret_cast<const double2*>(
                                     out_row<false>(M, const_cast<double*>(M.dx), oo, h, out_rs)));
@@ -1008,7 +1008,7 @@ k_mode_gemm_fold(const double* __restrict__ Af, int Kst, const int* __restrict__
                             }
                             if (n - 1 - h != h) {
                                 const double2 v2 = make_double2(e.x - o.x, e.y - o.y);
-                                *reinterpret_cast<double2*>(out_row<ROWS>(M, Y, oo, n - 1 - h, out_rs)) = v2;
+                                __stcs(reinterpret_cast<double2*>(out_row<ROWS>(M, Y, oo, n - 1 - h, out_rs)), v2);
                                 if (DOT) {
                                     const double2 x2 = __ldg(reinterpret_cast<const double2*>(
                                         out_row<false>(M, const_cast<double*>(M.dx), oo, n - 1 - h, out_rs)));

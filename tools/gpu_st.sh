@@ -1,3 +1,5 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 600 python tools/fd_sweep.py KS_FOLD_ST=0 KS_FOLD_ST=1 KS_FOLD_ST=2 KS_FOLD_ST=0 KS_FOLD_ST=1 > gpurun_out/st.log 2>&1
+timeout 600 python tools/fd_sweep.py KS_FD_TM1=1 KS_FD_TM1=1 > gpurun_out/st.log 2>&1
+SWEEP_CFG=c5 timeout 600 python tools/fd_sweep.py KS_FD_TM1=1 >> gpurun_out/st.log 2>&1
+SWEEP_CFG=c4p3 timeout 600 python tools/fd_sweep.py KS_FD_TM1=1 >> gpurun_out/st.log 2>&1
