@@ -388,7 +388,7 @@ __device__ __forceinline__ TileBase tile_base(const ColMap& M, long long tile) {
 __device__ __forceinline__ bool colmap(const ColMap& M, int n, const TileBase& B, int j,
                                        long long& in_off, long long& out_off) {
     if (M.mode == MAP_STD) {
-        if (j >= M.tw || B.q0 + j >= M.Q) return false; // balanced tiles may be narrower than the kernel's
+        if (B.q0 + j >= M.Q) return false;
         long long o = B.o0, qq = B.r0 + j;
         while (qq >= M.s) { // s >= 1; a 64-column tile crosses at most ceil(64/s) slabs
             qq -= M.s;
@@ -398,7 +398,7 @@ __device__ __forceinline__ bool colmap(const ColMap& M, int n, const TileBase& B
         return true;
     }
     if (M.mode >= MAP_TOUT1) { // STD columns, axis-1 time-major side
-        if (j >= M.tw || B.q0 + j >= M.Q) return false;
+        if (B.q0 + j >= M.Q) return false;
         long long o = B.o0, qq = B.r0 + j;
         while (qq >= M.s) {
             qq -= M.s;
@@ -829,7 +829,7 @@ k_mode_gemm_fold(const double* __restrict__ Af, int Kst, const int* __restrict__
         const long long tile = (long long)blockIdx.x + (long long)wt * gridDim.x;
         const int kc = w - wt * nkc;
         const TileBase tb = tile_base(M, tile);
-        const long long ncol = M.Q - tb.q0 < M.tw ? M.Q - tb.q0 : M.tw;
+        const long long ncol = M.Q - tb.q0 < BNC ? M.Q - tb.q0 : BNC;
         const long long seg1 = M.s - tb.r0 < ncol ? M.s - tb.r0 : ncol;
         const int jj = lane;
         const int q = kc * KC + (jj % KC);
@@ -1051,11 +1051,6 @@ k_mode_gemm_fold(const double* __restrict__ Af, int Kst, const int* __restrict__
     }
 }
 
-int fold_balance() {
-    static const int b = std::getenv("KS_FOLD_BAL") ? std::atoi(std::getenv("KS_FOLD_BAL")) : 0;
-    return b;
-}
-
 // fold kernel configuration: pair rows per stage (KC), ring stages, CTAs per SM
 // KS_FOLD_DRY=1: skip the MMAs (memory-pipeline ceiling experiment; wrong results)
 int dry_run() {
@@ -1096,26 +1091,8 @@ void launch_fold_cfg(const FoldAxis& F, const double* X, double* Y, ColMap M, cu
         KS_CUDA(cudaFuncSetAttribute(k_mode_gemm_fold<TH, INV, KC, STG, MINB, BNC, TMA>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     }
+    set_tile_width(M, BNC);
     const int per_sm = std::max(1, std::min(MINB, (int)((227 * 1024) / sm)));
-    // Wave balancing (column-slab modes): with BNC-wide tiles the last
-    // round-robin wave is often nearly empty (c3: 4160 tiles on 296 CTAs = 14
-    // full waves + 16 tiles). Narrow the tiles (even width, so every tile
-    // starts on a 32 B sector) until the tiles fill the same number of waves
-    // evenly; the kernel masks the columns past M.tw. Opt-in (KS_FOLD_BAL=1):
-    // measured slower at c3 (transforms 0.817 vs 0.791 ms; a tile costs the same
-    // DMMA work and latency at 60 columns as at 64), neutral at c2 / c4 / c5.
-    int tw = BNC;
-    if (fold_balance() && (M.mode == MAP_STD || M.mode >= MAP_TOUT1)) {
-        const long long slots = (long long)sms * per_sm;
-        const long long t_full = (M.Q + BNC - 1) / BNC;
-        const long long waves = (t_full + slots - 1) / slots;
-        if (waves >= 2) {
-            long long w = (M.Q + waves * slots - 1) / (waves * slots);
-            w = (w + 1) & ~1LL;
-            if (w < BNC) tw = (int)w;
-        }
-    }
-    set_tile_width(M, tw);
     const unsigned g = (unsigned)std::min<long long>(M.ntiles, (long long)sms * per_sm);
     const double* A = (INV ? F.inv : F.fwd).as<double>();
     if (M.rin || M.rout) { // peer-memory rows (sharded middle phase)
