@@ -38,6 +38,26 @@ CONFIGS = {
 }
 
 
+def reduced_dims(cfg):
+    """SpaceTimeProblem::uniform reduced dims (assembly.hpp:29-63, initial-condition
+    trial space): n_t = n_el_t + p - 1, n_s = n_el + p - 2 -- no library needed."""
+    d, p, n_el, n_el_t = CONFIGS[cfg]
+    return [n_el_t + p - 1] + [n_el + p - 2] * d
+
+
+def bench_config(cfg, ws):
+    """The `config` object both arms print (identical dicts: the driver compares them)."""
+    d, p, n_el, n_el_t = CONFIGS[cfg]
+    dims = reduced_dims(cfg)
+    n = int(np.prod(dims))
+    return {"workload": f"{cfg}: d={d} p={p} n_el={n_el} n_el_t={n_el_t}, "
+                        "one FD preconditioner application per step",
+            "dims": dims, "dofs": n,
+            "parallelism": "single" if ws == 1 else f"slab{ws} (outermost spatial axis)",
+            "l2": (f"inputs ({n * 16 / 1e6:.0f} MB/vector) larger than the 126 MB L2; no flush"
+                   if n * 16 > 126e6 else f"inputs ({n * 16 / 1e6:.1f} MB/vector) L2-resident (latency-bound size)")}
+
+
 def fd_flops_per_dof(dims, p):
     # SURVEY 8(d): F_alg = 8 * sum_l n_l + 24 p + 8 (dense transforms + pivoted banded solve)
     return 8 * sum(dims[1:]) + 24 * p + 8
@@ -167,30 +187,34 @@ def rhs(n, seed=1234):
     return v
 
 
-def cpu_baseline_fd(cfg, r, steps=1):
-    """Reference CPU path on the host cores: oracle/_ref (reference sources) if built,
-    else the C restatement (port). Single-threaded like the reference."""
+def _ref_apply(cfg):
+    """The reference CPU FD application on the host: oracle/_ref (the reference's own
+    sources, oracle/build_ref.sh) when built, else the C restatement (`kind` "port").
+    Single-threaded, like the reference. Errors propagate."""
+    d, p, n_el, n_el_t = CONFIGS[cfg]
+    from oracle import refdrv
+    if refdrv.available():
+        ref = refdrv.RefProblem(d, p, n_el, n_el_t)
+        return "reference", ref.fd_apply, ref.N
+    # no reference build on this host (oracle/_ref is built by __graft_entry__.build()
+    # and ships with the tree): the bit-exact C restatement (oracle/ks_oracle.c), fed
+    # by libks's host-only setup restatement (pure host code, no device work)
     from oracle import oracle as O
     import paper_2311_18461_b200 as ks
-    d, p, n_el, n_el_t = CONFIGS[cfg]
-    kind = "port"
-    ref = None
-    try:
-        from oracle import refdrv
-        if refdrv.available():
-            ref = refdrv.RefProblem(d, p, n_el, n_el_t)
-            kind = "reference"
-    except Exception:
-        ref = None
-    if ref is None:
-        O.build_oracle()
-        prob = ks.SpaceTimeProblem.uniform(d, p, n_el, n_el_t)
-        Lt, Mt, Wt = prob.time_bands()
-        U, lam = zip(*[prob.eig(l) for l in range(d)])
-        fd = O.OracleFD(prob.reduced_dims(), 1.0, p, U, lam, Lt, Mt, Wt)
-        apply = fd.apply
-    else:
-        apply = ref.fd_apply
+    O.build_oracle()
+    prob = ks.SpaceTimeProblem.uniform(d, p, n_el, n_el_t)
+    Lt, Mt, Wt = prob.time_bands()
+    U, lam = zip(*[prob.eig(l) for l in range(d)])
+    fd = O.OracleFD(prob.reduced_dims(), 1.0, p, U, lam, Lt, Mt, Wt)
+    return "port", fd.apply, prob.N_dof
+
+
+def cpu_baseline_fd(cfg, r, steps=3, warmup=1):
+    """cpu_baseline leg: `warmup` excluded applications, then the
+    median of `steps` timed ones (std::chrono-equivalent perf_counter around each)."""
+    kind, apply, _ = _ref_apply(cfg)
+    for _ in range(warmup):
+        apply(r)
     times = []
     for _ in range(steps):
         t0 = time.perf_counter()
@@ -202,49 +226,58 @@ def cpu_baseline_fd(cfg, r, steps=1):
 def _ref_worker(cfg, n, steps, warm, start, q):
     """One host core's share of the reference arm: its own reference problem (the
     reference is single-threaded, so independent applications are how it uses a
-    multi-core host), warm-up, then `steps` applications after the common start."""
+    multi-core host), `warm` untimed applications, then `steps` timed ones after
+    the common start."""
     try:
+        kind, apply, nref = _ref_apply(cfg)
+        assert nref == n, (nref, n)
         r = rhs(n)
-        cpu_baseline_fd(cfg, r, steps=warm) if warm else None
+        for _ in range(warm):
+            apply(r)
         start.wait()
         t0 = time.perf_counter()
-        kind, _, used = cpu_baseline_fd(cfg, r, steps=steps)
-        q.put((kind, used, t0, time.perf_counter()))
+        for _ in range(steps):
+            apply(r)
+        q.put((kind, steps, t0, time.perf_counter()))
     except BaseException as e:  # report instead of hanging the parent
         start.abort()
         q.put(("error", repr(e), 0.0, 0.0))
 
 
-def ref_workers():
-    """Concurrent reference applications the host can hold: one per usable core,
-    capped by free memory (~3 GB per c3 reference problem + vectors)."""
+def ref_workers(K):
+    """Concurrent reference processes: the largest divisor of K that the host's
+    cores and free memory (~3 GB per c3 reference problem) can hold, so the K
+    timed applications split evenly over them."""
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     try:
         import psutil
         mem = int(psutil.virtual_memory().available // (3 << 30))
     except Exception:
         mem = cores
-    return max(1, min(cores, mem, 64))
+    cap = int(os.environ.get("KS_REF_WORKERS", "0")) or max(1, min(cores, mem, 64))
+    return max(w for w in range(1, min(cap, K) + 1) if K % w == 0)
 
 
 def run_reference_arm(args, rank, ws, dist):
+    """--impl reference: the reference's own CPU FD application (oracle/_ref) on the
+    host cores, same config / metric / steps / warm-up as our arm. The K timed
+    applications are spread evenly over concurrent single-threaded reference
+    processes (the reference never threads); value = K x N_dof / concurrent wall
+    time. libks is never loaded in this arm."""
     if rank != 0:
         return
     cfg = args.config
-    d, p, n_el, n_el_t = CONFIGS[cfg]
+    n = int(np.prod(reduced_dims(cfg)))
+    K = args.steps
+    W = max(args.warmup, 3)
+    workers = ref_workers(K)
+    per = K // workers
+    warm = -(-W // workers)  # every process warms up; >= W applications in total
     import multiprocessing as mp
-    import paper_2311_18461_b200 as ks
-    prob = ks.SpaceTimeProblem.uniform(d, p, n_el, n_el_t)
-    n = prob.N_dof
-    # bounded: one warm-up at most, steps capped so the arm ends within minutes
-    warm = min(args.warmup, 1)
-    steps = max(1, min(args.steps, 3))
-    workers = int(os.environ.get("KS_REF_WORKERS", "0")) or ref_workers()
     ctx = mp.get_context("spawn")
     start = ctx.Barrier(workers + 1)
     q = ctx.Queue()
-    procs = [ctx.Process(target=_ref_worker, args=(cfg, n, steps, warm, start, q))
-             for _ in range(workers)]
+    procs = [ctx.Process(target=_ref_worker, args=(cfg, n, per, warm, start, q)) for _ in range(workers)]
     for pr in procs:
         pr.start()
     start.wait()
@@ -255,19 +288,19 @@ def run_reference_arm(args, rank, ws, dist):
     if bad:
         raise SystemExit(f"reference worker failed: {bad[0][1]}")
     kind = res[0][0]
-    used = min(x[1] for x in res)
     wall = max(x[3] for x in res) - min(x[2] for x in res)
-    val = workers * used * n / wall        # all cores' applications / concurrent window
+    val = K * n / wall
     line = {
         "metric": "fd_apply_dof_per_s", "value": val, "unit": "DOF/s", "n_gpus": ws,
-        "steps": used, "warmup": warm, "ms_per_step": wall / used * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
-        "data": "synthetic", "impl": "reference",
-        "config": {"workload": f"{cfg}: d={d} p={p} n_el={n_el} FD apply", "dofs": n},
+        "steps": K, "warmup": W, "ms_per_step": wall / K * 1e3,
+        "higher_is_better": True, "scaling": "weak" if ws == 1 else "strong", "vs_baseline": None,
+        "dtype": "c128 (complex FP64)",
+        "data": "synthetic (seeded U[-1,1] RHS, SURVEY 8(d))", "impl": "reference",
+        "config": bench_config(cfg, ws),
         "cpu_baseline": {"value": val, "unit": "DOF/s", "cores": workers, "kind": kind,
-                         "sample": f"{workers} concurrent single-threaded reference processes "
-                                   f"(one per host core), {used} full {cfg} FD applications "
-                                   f"each; value = all applications / concurrent wall time"},
+                         "sample": f"{K} full {cfg} FD applications split over {workers} concurrent "
+                                   f"single-threaded reference processes ({per} each, after "
+                                   f"{warm} untimed each); value = K x N_dof / concurrent wall time"},
         "e2e": {"value": val, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -386,13 +419,11 @@ def run_sharded(args, rank, ws, local, dist):
             "steps": K, "warmup": W, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "c128 (complex FP64)",
             "data": "synthetic (seeded U[-1,1] RHS, SURVEY 8(d))",
-            "config": {"workload": f"{args.config}: d={d} p={p} n_el={n_el}, one sharded FD application per step",
-                       "dims": dims, "dofs": n,
-                       "parallelism": f"slab{ws} (axis {d}), transport {transport}" +
-                                      (" (axis-d transform reads/writes peer slabs over NVLink)" if transport == "peer"
-                                       else " (2x NCCL all-to-all)"),
-                       "transport_note": transport_note,
-                       "nccl_all_to_all_ms_per_step": ms_nccl},
+            "config": bench_config(args.config, ws),
+            "transport": {"kind": transport,
+                          "detail": "axis-d transform reads/writes peer slabs over NVLink" if transport == "peer"
+                                    else "2x NCCL all-to-all",
+                          "note": transport_note, "nccl_all_to_all_ms_per_step": ms_nccl},
             "e2e": {"value": n / e2e, "unit": "DOF/s", "h2d_bytes_per_step": int(r_host.nbytes) * ws,
                     "d2h_bytes_per_step": int(r_host.nbytes) * ws, "ms_per_step": e2e * 1e3},
             "gpu_launches": launches * K, "roofline": roofline, "clocks": clk.summary(), "cpu_baseline": None,
@@ -572,10 +603,10 @@ def main():
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        kind, sec, used = cpu_baseline_fd(args.config, r_host, steps=1)
+        kind, sec, used = cpu_baseline_fd(args.config, r_host, steps=3, warmup=1)
         cpu = {"value": n / sec, "unit": "DOF/s", "cores": 1, "kind": kind,
-               "sample": f"{used} full {args.config} FD application ({n} DOF), single thread, "
-                         "setup (block factorisation) excluded"}
+               "sample": f"median of {used} full {args.config} FD applications ({n} DOF) after 1 "
+                         "untimed warm-up, single thread, setup (block factorisation) excluded"}
 
     if rank == 0:
         line = {
@@ -583,13 +614,9 @@ def main():
             "steps": K, "warmup": W, "ms_per_step": ms_fd, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "c128 (complex FP64)",
             "data": "synthetic (seeded U[-1,1] RHS, SURVEY 8(d))",
-            "config": {"workload": f"{args.config}: d={d} p={p} n_el={n_el} n_el_t={n_el_t}, "
-                                   "one FD preconditioner application per step",
-                       "dims": dims, "dofs": n,
-                       "parallelism": "replicas" if ws > 1 else "single",
-                       "l2": "inputs (272 MB/vector) larger than L2; no flush",
-                       "transform_engine": {0: "dfma", 1: "dmma_v1", 2: "dmma_v2"}[ks.lib().ks_transform_engine()]
-                       + ("+fold" if P.info()["folded_axes"] else "")},
+            "config": bench_config(args.config, ws),
+            "transform_engine": {0: "dfma", 1: "dmma_v1", 2: "dmma_v2"}[ks.lib().ks_transform_engine()]
+                                + ("+fold" if P.info()["folded_axes"] else ""),
             "e2e": {"value": e2e_val, "unit": "DOF/s", "h2d_bytes_per_step": n * 16,
                     "d2h_bytes_per_step": n * 16, "ms_per_step": e2e_s * 1e3,
                     "mode": "ks_fd_apply(host pointers, pinned) on a user stream, K steps back to back, "
