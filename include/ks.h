@@ -82,6 +82,8 @@ int ks_device_count(void);
  * ------------------------------------------------------------------------- */
 typedef struct ks_fd ks_fd;
 
+/* Limits: d <= 3, p_t <= 8, every spatial axis n_l <= 160 (the transforms keep
+ * U_l in shared memory; longer axes return KS_EINVAL at creation). */
 int ks_fd_create(int d, const int* dims, double nu, int p_t,
                  const double* const* U, const double* const* lambda,
                  const double* Lt, const double* Mt, const ks_c64* Wt,
@@ -90,10 +92,12 @@ int ks_fd_create(int d, const int* dims, double nu, int p_t,
  * (fdsolver.hpp:61 -> FastDiagSolver::solve, fdsolver.cpp:53-63). r and z may
  * alias. stream is a cudaStream_t (NULL = the handle's own stream, blocking).
  * KS_MEM_HOST with a non-NULL stream is asynchronous: the H2D copy, the apply
- * and the D2H copy are queued on the handle's copy/compute streams (two
- * staging buffers, so consecutive applies overlap their transfers) and z is
- * valid once `stream` is synchronised; r and z must stay untouched (and should
- * be pinned) until then. */
+ * and the D2H copy are queued on the handle's copy/compute streams (three
+ * staging buffers, so consecutive applies overlap their transfers; the H2D
+ * copy starts once `stream` reaches the call) and z is valid once `stream` is
+ * synchronised; r and z must stay untouched (and should be pinned) until then.
+ * Applies on one handle are ordered on the device whatever streams they use
+ * (the handle's scratch is shared), and a host mutex serialises the calls. */
 int ks_fd_apply(ks_fd* fd, const ks_c64* r, ks_c64* z, int mem, void* stream);
 /* Same as apply but with the adjoint block solves (FastDiagSolver::solve_adjoint,
  * fdsolver.cpp:65-75, eigensolve.cpp:148-170). */

@@ -232,6 +232,33 @@ def _cvec(a) -> np.ndarray:
     return np.ascontiguousarray(a, dtype=np.complex128)
 
 
+def _stream(stream):
+    """A ks.Stream, a raw cudaStream_t (int / c_void_p) or None -> ctypes argument."""
+    return stream.handle if isinstance(stream, Stream) else stream
+
+
+def _dev_pair(n, x, y, what):
+    """Check device vectors against the operator size; allocate y if absent."""
+    if x.n != n:
+        raise InvalidArgument(f"{what}: vector length mismatch ({x.n} != {n})")
+    if y is None:
+        return DeviceVector(n)
+    if not isinstance(y, DeviceVector) or y.n != n:
+        raise InvalidArgument(f"{what}: output must be a DeviceVector of length {n}")
+    return y
+
+
+def _host_out(n, y, what):
+    """Output array for a host-pointer apply: a new one, or the caller's if it is
+    a C-contiguous complex128 array of length n (the D2H copy writes n entries)."""
+    if y is None:
+        return np.empty(n, dtype=np.complex128)
+    if not (isinstance(y, np.ndarray) and y.dtype == np.complex128 and y.flags["C_CONTIGUOUS"] and y.size == n
+            and y.flags["WRITEABLE"]):
+        raise InvalidArgument(f"{what}: output must be a writeable C-contiguous complex128 array of length {n}")
+    return y
+
+
 # ---------------------------------------------------------------------------
 # device buffers (HBM-resident vectors for the device-pointer API)
 # ---------------------------------------------------------------------------
@@ -436,16 +463,16 @@ class FDPreconditioner:
 
     def apply(self, r, z=None, stream=None):
         """z = P^-1 r. numpy in -> numpy out (host path), or DeviceVector in/out."""
+        n = self.vec_size()
         if isinstance(r, DeviceVector):
-            z = z if z is not None else DeviceVector(r.n)
-            _check(lib().ks_fd_apply(self._h, r.ptr, z.ptr, KS_MEM_DEVICE, stream))
+            z = _dev_pair(n, r, z, "FastDiagSolver")
+            _check(lib().ks_fd_apply(self._h, r.ptr, z.ptr, KS_MEM_DEVICE, _stream(stream)))
             return z
         r = _cvec(r).ravel()
-        if r.size != self.vec_size():
+        if r.size != n:
             raise InvalidArgument("FastDiagSolver: vector length mismatch")
-        out = np.empty_like(r) if z is None else z
-        st = stream.handle if isinstance(stream, Stream) else stream
-        _check(lib().ks_fd_apply(self._h, _ptr(r), _ptr(out), KS_MEM_HOST, st))
+        out = _host_out(n, z, "FastDiagSolver")
+        _check(lib().ks_fd_apply(self._h, _ptr(r), _ptr(out), KS_MEM_HOST, _stream(stream)))
         return out
 
     def apply_adjoint(self, r):
@@ -474,8 +501,9 @@ class FDPreconditioner:
         _check(lib().ks_fd_info(self._h, C.byref(m), C.byref(nb)))
         d = len(self.dims) - 1
         return {"folded_axes": [l + 1 for l in range(d) if m.value >> l & 1], "blocks": nb.value,
-                "fused_axes_12": bool(m.value >> 16 & 1), "time_major_axis": 1 if m.value >> 17 & 1 else d,
-                "no_pivoting": bool(m.value >> 18 & 1)}
+                "time_major_axis": 1 if m.value >> 17 & 1 else d,
+                # least-squares blocks: L D L^H (never pivots); Galerkin LU: no block pivoted
+                "no_pivot_solve": bool(m.value >> 18 & 1)}
 
     def time(self, r: DeviceVector, z: DeviceVector, iters: int, flush: bool = True):
         ms, mk = C.c_double(), C.c_double()
@@ -588,15 +616,16 @@ class KroneckerOperator:
     def apply(self, x, y=None, stream=None):
         """y = K x (tensorops.cpp:236-254)."""
         self._build()
+        n = self.vec_size()
         if isinstance(x, DeviceVector):
-            y = y if y is not None else DeviceVector(x.n)
-            _check(lib().ks_kron_apply(self._h, x.ptr, y.ptr, KS_MEM_DEVICE, stream))
+            y = _dev_pair(n, x, y, "KroneckerOperator")
+            _check(lib().ks_kron_apply(self._h, x.ptr, y.ptr, KS_MEM_DEVICE, _stream(stream)))
             return y
         x = _cvec(x).ravel()
-        if x.size != self.vec_size():
+        if x.size != n:
             raise InvalidArgument("KroneckerOperator: vector length mismatch")
-        out = np.empty_like(x) if y is None else y
-        _check(lib().ks_kron_apply(self._h, _ptr(x), _ptr(out), KS_MEM_HOST, None))
+        out = _host_out(n, y, "KroneckerOperator")
+        _check(lib().ks_kron_apply(self._h, _ptr(x), _ptr(out), KS_MEM_HOST, _stream(stream)))
         return out
 
     def plan_info(self):
@@ -606,7 +635,7 @@ class KroneckerOperator:
         e = C.c_int()
         _check(lib().ks_kron_engine(self._h, C.byref(e)))
         return {"passes": a.value, "nodes": b.value, "products": c.value,
-                "engine": {0: "level_passes", 1: "fused_pairs", 2: "axis3_then_fused_t12"}[e.value]}
+                "engine": {0: "level_passes", 1: "fused_pairs"}[e.value]}
 
     def time(self, x: DeviceVector, y: DeviceVector, iters: int, flush: bool = True):
         self._build()
@@ -810,7 +839,7 @@ def pcg(A: KroneckerOperator, P: Optional[FDPreconditioner], b, opts: PcgOptions
     cap = max(int(opts.maxit), 1)
     hist = np.zeros(cap)
     if isinstance(b, DeviceVector):
-        x = x_out if x_out is not None else DeviceVector(b.n)
+        x = _dev_pair(A.vec_size(), b, x_out, "pcg")
         _check(lib().ks_pcg(A._h, P._h if P is not None else None, b.ptr, x.ptr, KS_MEM_DEVICE,
                             C.byref(o), _ptr(hist), cap, C.byref(rep)))
         xr = x

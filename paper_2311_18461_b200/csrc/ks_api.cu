@@ -26,6 +26,34 @@ void ensure_device(int device) {
 
 int transform_engine();
 
+void smem_optin(const void* func, int bytes) {
+    static std::mutex m;
+    static std::vector<std::pair<int, const void*>> done; // (device, function) pairs opted in
+    int dev = 0;
+    KS_CUDA(cudaGetDevice(&dev));
+    {
+        std::lock_guard<std::mutex> lk(m);
+        for (auto& e : done)
+            if (e.first == dev && e.second == func) return;
+    }
+    // always the maximum: launches of one function may need different sizes
+    (void)bytes;
+    KS_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    std::lock_guard<std::mutex> lk(m);
+    done.emplace_back(dev, func);
+}
+
+int device_sms() {
+    static std::mutex m;
+    static std::vector<int> sms; // by device index, 0 = unknown
+    int dev = 0;
+    KS_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(m);
+    if ((int)sms.size() <= dev) sms.resize(dev + 1, 0);
+    if (!sms[dev]) KS_CUDA(cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev));
+    return sms[dev];
+}
+
 // kron engine (ks_kron.cu)
 struct KronPlan;
 KronPlan* kron_plan(const std::vector<int>& dims,
@@ -78,8 +106,6 @@ struct ks_fd {
     std::vector<FoldAxis> fold;   // per axis; fold[l].n == 0: dense transform
     std::vector<std::vector<double>> lam_host;
     std::vector<int> fiber_block; // host copy of the block map (empty = identity)
-    bool fused = false;           // outermost axis via k_fd_fused
-    bool fuse12 = false;          // axes 1+2 via k_fold12 (KS_FD_FUSE12=1 at creation)
     bool tm1 = false;             // time-major hand-off on axis 1 (pair mode, folded axis 1)
     int kind = 0;                 // 0: least-squares blocks, 1: Galerkin blocks (galerkin_fast_solver)
     DevBuf Lt, Mt, Wsym;          // Wsym: W + W^H (least squares) or W itself (Galerkin)
@@ -96,8 +122,14 @@ struct ks_fd {
     DevBuf pio[kNSlot];
     cudaEvent_t ev_in[kNSlot] = {}, ev_comp[kNSlot] = {}, ev_out[kNSlot] = {};
     int slot = 0;
+    // ordering across streams: every apply's device work waits for the previous
+    // apply's (the scratch s0/s1/io and the staging slots are per handle, whatever
+    // stream the caller picks), and records `done` when it has been enqueued
+    cudaEvent_t done = nullptr, ev_user = nullptr;
     std::mutex mu;
     ~ks_fd() {
+        if (done) cudaEventDestroy(done);
+        if (ev_user) cudaEventDestroy(ev_user);
         for (int k = 0; k < kNSlot; ++k) {
             if (ev_in[k]) cudaEventDestroy(ev_in[k]);
             if (ev_comp[k]) cudaEventDestroy(ev_comp[k]);
@@ -123,8 +155,10 @@ struct ks_kron {
     std::unique_ptr<Reducer> pcg_red[5]; // ks_pcg reducers (pinned host words), kept across solves
     std::vector<void*> hptrs;
     cudaStream_t stream = nullptr;
+    cudaEvent_t done = nullptr; // see ks_fd::done
     std::mutex mu;
     ~ks_kron() {
+        if (done) cudaEventDestroy(done);
         if (stream) cudaStreamDestroy(stream);
     }
 };
@@ -137,21 +171,13 @@ inline cudaStream_t pick(void* user, cudaStream_t own) {
 
 // FD apply on device pointers (Algorithm 1 steps 2-4; fdsolver.cpp:53-63).
 // ev (optional): start/stop event pairs recorded around each transform kernel.
-// dot (optional): also leave Re <r, z> in dot->result[0] -- fused into the last
-// inverse transform on the axis-1 time-major path, a separate reduction otherwise
 void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStream_t st,
-                  std::vector<cudaEvent_t>* ev, Reducer* dot = nullptr) {
-    if (dot && !(f->tm1 && !f->fused && f->fold[f->d - 1].n && r != z)) {
-        fd_apply_dev(f, r, z, adjoint, st, ev, nullptr);
-        launch_dotc(*dot, r, z, f->N, st);
-        return;
-    }
+                  std::vector<cudaEvent_t>* ev) {
     const int d = f->d;
     const double* cur = reinterpret_cast<const double*>(r);
     double* bufs[2] = {f->s0.as<double>(), f->s1.as<double>()};
     int nb = 0;
-    size_t s = f->dims[0];
-    auto gemm = [&](const DevBuf& At, int l, const double* in, double* out, int layout, Reducer* red = nullptr) {
+    auto gemm = [&](const DevBuf& At, int l, const double* in, double* out, int layout) {
         const int n = f->dims[l];
         size_t stride = 1;
         for (int k = 0; k < l; ++k) stride *= (size_t)f->dims[k];
@@ -159,9 +185,7 @@ void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStre
         const FoldAxis& F = f->fold[l - 1];
         const bool inv = &At == &f->At_inv[l - 1];
         auto launch = [&]() {
-            if (F.n)
-                launch_mode_gemm_fold(F, inv, in, out, stride, outer, st, layout, f->dims[0], nullptr, nullptr,
-                                      reinterpret_cast<const double*>(r), red);
+            if (F.n) launch_mode_gemm_fold(F, inv, in, out, stride, outer, st, layout, f->dims[0]);
             else launch_mode_gemm(At.as<double>(), n, in, out, stride, outer, st, layout, f->dims[0]);
         };
         if (ev) {
@@ -177,39 +201,21 @@ void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStre
             launch();
         }
     };
-    (void)s;
-    if (f->fused && !adjoint) {
-        // axes 1..d-1 forward, fused [axis d forward, solves, axis d inverse],
-        // axes 1..d-1 inverse
-        for (int l = 1; l < d; ++l) {
+    if (f->tm1) {
+        // pair mode with a folded axis 1: forward axes d..1, the axis-1 transform
+        // writes the position-ordered time-major layout; solves; inverse axis 1
+        // first (reads the time-major layout), then 2..d
+        for (int l = d; l >= 1; --l) {
             double* out = bufs[nb];
             nb ^= 1;
-            gemm(f->At_fwd[l - 1], l, cur, out, 0);
+            gemm(f->At_fwd[l - 1], l, cur, out, l == 1 ? 3 : 0);
             cur = out;
         }
-        double* mid = (d == 1) ? reinterpret_cast<double*>(z) : bufs[nb];
-        if (d != 1) nb ^= 1;
-        if (ev) {
-            cudaEvent_t a, b;
-            KS_CUDA(cudaEventCreate(&a));
-            KS_CUDA(cudaEventCreate(&b));
-            KS_CUDA(cudaEventRecord(a, st));
-            launch_fd_fused(f->At_fwd[d - 1].as<double>(), f->At_inv[d - 1].as<double>(), f->blocks,
-                            f->dims[d], (long long)(f->Ns / (size_t)f->dims[d]),
-                            reinterpret_cast<const double2*>(cur), reinterpret_cast<double2*>(mid), st);
-            KS_CUDA(cudaEventRecord(b, st));
-            ev->push_back(a);
-            ev->push_back(b);
-        } else {
-            launch_fd_fused(f->At_fwd[d - 1].as<double>(), f->At_inv[d - 1].as<double>(), f->blocks,
-                            f->dims[d], (long long)(f->Ns / (size_t)f->dims[d]),
-                            reinterpret_cast<const double2*>(cur), reinterpret_cast<double2*>(mid), st);
-        }
-        cur = mid;
-        for (int l = 1; l < d; ++l) {
-            double* out = (l == d - 1) ? reinterpret_cast<double*>(z) : bufs[nb];
-            if (l != d - 1) nb ^= 1;
-            gemm(f->At_inv[l - 1], l, cur, out, 0);
+        launch_fd_solve(f->blocks, reinterpret_cast<double2*>(const_cast<double*>(cur)), adjoint, st);
+        for (int l = 1; l <= d; ++l) {
+            double* out = l == d ? reinterpret_cast<double*>(z) : bufs[nb];
+            if (l != d) nb ^= 1;
+            gemm(f->At_inv[l - 1], l, cur, out, l == 1 ? 4 : 0);
             cur = out;
         }
         return;
@@ -217,102 +223,46 @@ void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStre
     // to_eigen: axes 1..d with U_l^T (fdsolver.cpp:7-14). The last one (the
     // outermost axis d) writes the time-major layout T[t][fiber] so that the
     // block solves read and write coalesced.
-    // Axes 1 and 2 go through one fused kernel when both fold and fit a
-    // shared-memory slab (ks_fold12.cu; d >= 3 so that axis d stays separate).
-    const bool f12 = f->fuse12;
-    auto fused12 = [&](bool inv, const double* in, double* out) {
-        const long long outer = (long long)(f->N / ((size_t)f->dims[0] * f->dims[1] * f->dims[2]));
-        auto launch = [&]() { launch_fold12(f->fold[0], f->fold[1], inv, in, out, f->dims[0], outer, st); };
-        if (ev) {
-            cudaEvent_t a, b;
-            KS_CUDA(cudaEventCreate(&a));
-            KS_CUDA(cudaEventCreate(&b));
-            KS_CUDA(cudaEventRecord(a, st));
-            launch();
-            KS_CUDA(cudaEventRecord(b, st));
-            ev->push_back(a);
-            ev->push_back(b);
-        } else {
-            launch();
-        }
-    };
-    // Opt-in (KS_FD_NAT=1, pair-mode blocks, forward solve): the solve reads the
-    // natural layout directly (k_fd_solve_nat, chunked through shared memory),
-    // so no transform needs the time-major hand-off. Measured c3: transforms
-    // 0.75 vs 0.85 ms, but the chunked solve takes 0.51 vs 0.37 ms (its
-    // per-chunk staging instructions and 7 warps/SM make it latency bound) --
-    // 1.26 vs 1.21 ms per FD apply, so the time-major path stays the default.
-    static const bool nat_ok = [] {
-        const char* e = std::getenv("KS_FD_NAT");
-        return e && std::strcmp(e, "1") == 0;
-    }();
-    const bool nat = nat_ok && !adjoint && f->blocks.pair_n1 > 0 && f->blocks.rec == 0 && !f->tm1;
-    const int tout = nat ? 0 : 1, tin = nat ? 0 : 2;
-    if (f->tm1) {
-        // forward axes d..1, the axis-1 transform writes the position-ordered
-        // time-major layout; solves; inverse axis 1 first, then 2..d
-        for (int l = d; l >= 1; --l) {
-            double* out = bufs[nb];
-            nb ^= 1;
-            gemm(f->At_fwd[l - 1], l, cur, out, l == 1 ? 3 : 0);
-            cur = out;
-        }
-        launch_fd_solve(f->blocks, reinterpret_cast<double2*>(const_cast<double*>(cur)), adjoint, st, true);
-        for (int l = 1; l <= d; ++l) {
-            double* out = l == d ? reinterpret_cast<double*>(z) : bufs[nb];
-            if (l != d) nb ^= 1;
-            gemm(f->At_inv[l - 1], l, cur, out, l == 1 ? 4 : 0, l == d ? dot : nullptr);
-            cur = out;
-        }
-        return;
-    }
     for (int l = 1; l <= d; ++l) {
         double* out = bufs[nb];
         nb ^= 1;
-        if (f12 && l == 1) {
-            fused12(false, cur, out);
-            ++l;
-        } else {
-            gemm(f->At_fwd[l - 1], l, cur, out, l == d ? tout : 0);
-        }
+        gemm(f->At_fwd[l - 1], l, cur, out, l == d ? 1 : 0);
         cur = out;
     }
     // N_s block solves (fdsolver.cpp:58-60), time-major
-    launch_fd_solve(f->blocks, reinterpret_cast<double2*>(const_cast<double*>(cur)), adjoint, st, !nat);
+    launch_fd_solve(f->blocks, reinterpret_cast<double2*>(const_cast<double*>(cur)), adjoint, st);
     // from_eigen with U_l (fdsolver.cpp:16-21): axis d first (it consumes the
     // time-major layout), then axes 1..d-1. Mode products on distinct axes
     // commute, so only the rounding order differs.
     for (int k = 0; k < d; ++k) {
         const int l = k == 0 ? d : k;
-        const bool pair = f12 && k == 1; // axes 1 and 2 in one pass
-        const int klast = pair ? k + 1 : k;
-        double* out = (klast == d - 1) ? reinterpret_cast<double*>(z) : bufs[nb];
-        if (klast != d - 1) nb ^= 1;
-        if (pair) {
-            fused12(true, cur, out);
-            k = klast;
-        } else {
-            gemm(f->At_inv[l - 1], l, cur, out, k == 0 ? tin : 0);
-        }
+        double* out = (k == d - 1) ? reinterpret_cast<double*>(z) : bufs[nb];
+        if (k != d - 1) nb ^= 1;
+        gemm(f->At_inv[l - 1], l, cur, out, k == 0 ? 2 : 0);
         cur = out;
     }
 }
 
 void fd_apply_any(ks_fd* f, const ks_c64* r, ks_c64* z, int mem, void* stream, bool adjoint) {
     KS_REQUIRE(f, KS_EINVAL, "ks_fd_apply: NULL handle");
+    KS_REQUIRE(r && z, KS_EINVAL, "ks_fd_apply: NULL vector");
     std::lock_guard<std::mutex> lk(f->mu);
     ensure_device(f->device);
     cudaStream_t st = pick(stream, f->stream);
     const size_t bytes = f->N * sizeof(double2);
     if (mem == KS_MEM_DEVICE) {
+        KS_CUDA(cudaStreamWaitEvent(st, f->done, 0));
         fd_apply_dev(f, reinterpret_cast<const double2*>(r), reinterpret_cast<double2*>(z), adjoint,
                      st, nullptr);
+        KS_CUDA(cudaEventRecord(f->done, st));
         // no caller stream: behave like the reference's blocking call
         if (!stream) KS_CUDA(cudaStreamSynchronize(st));
     } else if (stream) {
         // pipelined: slot k's H2D waits until slot k's previous D2H has drained
-        // its staging buffer; the compute stream orders the applies (shared
-        // scratch); the caller's stream waits for this apply's D2H
+        // its staging buffer and until the caller's stream reaches this call
+        // (earlier work there may still be producing r); the compute waits for
+        // the handle's previous apply (shared scratch); the caller's stream
+        // waits for this apply's D2H
         if (!f->h2d) {
             KS_CUDA(cudaStreamCreateWithFlags(&f->h2d, cudaStreamNonBlocking));
             KS_CUDA(cudaStreamCreateWithFlags(&f->d2h, cudaStreamNonBlocking));
@@ -328,11 +278,15 @@ void fd_apply_any(ks_fd* f, const ks_c64* r, ks_c64* z, int mem, void* stream, b
         f->slot = (f->slot + 1) % ks_fd::kNSlot;
         cudaStream_t us = static_cast<cudaStream_t>(stream);
         double2* buf = f->pio[k].as<double2>();
+        KS_CUDA(cudaEventRecord(f->ev_user, us));
+        KS_CUDA(cudaStreamWaitEvent(f->h2d, f->ev_user, 0));
         KS_CUDA(cudaStreamWaitEvent(f->h2d, f->ev_out[k], 0));
         KS_CUDA(cudaMemcpyAsync(buf, r, bytes, cudaMemcpyHostToDevice, f->h2d));
         KS_CUDA(cudaEventRecord(f->ev_in[k], f->h2d));
         KS_CUDA(cudaStreamWaitEvent(f->stream, f->ev_in[k], 0));
+        KS_CUDA(cudaStreamWaitEvent(f->stream, f->done, 0));
         fd_apply_dev(f, buf, buf, adjoint, f->stream, nullptr);
+        KS_CUDA(cudaEventRecord(f->done, f->stream));
         KS_CUDA(cudaEventRecord(f->ev_comp[k], f->stream));
         KS_CUDA(cudaStreamWaitEvent(f->d2h, f->ev_comp[k], 0));
         KS_CUDA(cudaMemcpyAsync(z, buf, bytes, cudaMemcpyDeviceToHost, f->d2h));
@@ -340,23 +294,30 @@ void fd_apply_any(ks_fd* f, const ks_c64* r, ks_c64* z, int mem, void* stream, b
         KS_CUDA(cudaStreamWaitEvent(us, f->ev_out[k], 0));
     } else {
         if (!f->io.p) f->io.alloc(bytes);
+        KS_CUDA(cudaStreamWaitEvent(st, f->done, 0));
         KS_CUDA(cudaMemcpyAsync(f->io.p, r, bytes, cudaMemcpyHostToDevice, st));
         fd_apply_dev(f, f->io.as<double2>(), f->io.as<double2>(), adjoint, st, nullptr);
         KS_CUDA(cudaMemcpyAsync(z, f->io.p, bytes, cudaMemcpyDeviceToHost, st));
+        KS_CUDA(cudaEventRecord(f->done, st));
         KS_CUDA(cudaStreamSynchronize(st));
     }
 }
 
 void kron_apply_any(ks_kron* k, const ks_c64* x, ks_c64* y, int mem, void* stream) {
     KS_REQUIRE(k, KS_EINVAL, "ks_kron_apply: NULL handle");
+    KS_REQUIRE(x && y, KS_EINVAL, "ks_kron_apply: NULL vector");
     std::lock_guard<std::mutex> lk(k->mu);
     ensure_device(k->device);
     cudaStream_t st = pick(stream, k->stream);
     const size_t bytes = k->N * sizeof(double2);
+    // the plan's intermediates and pointer tables are per handle: order this
+    // apply after the previous one whatever stream either ran on
+    KS_CUDA(cudaStreamWaitEvent(st, k->done, 0));
     if (mem == KS_MEM_DEVICE) {
         KS_REQUIRE(x != y, KS_EINVAL, "ks_kron_apply: x and y must not alias");
         kron_apply(*k->plan, reinterpret_cast<const double2*>(x), reinterpret_cast<double2*>(y), st,
                    k->hptrs);
+        KS_CUDA(cudaEventRecord(k->done, st));
         if (!stream) KS_CUDA(cudaStreamSynchronize(st));
     } else {
         if (!k->io_x.p) {
@@ -366,6 +327,7 @@ void kron_apply_any(ks_kron* k, const ks_c64* x, ks_c64* y, int mem, void* strea
         KS_CUDA(cudaMemcpyAsync(k->io_x.p, x, bytes, cudaMemcpyHostToDevice, st));
         kron_apply(*k->plan, k->io_x.as<double2>(), k->io_y.as<double2>(), st, k->hptrs);
         KS_CUDA(cudaMemcpyAsync(y, k->io_y.p, bytes, cudaMemcpyDeviceToHost, st));
+        KS_CUDA(cudaEventRecord(k->done, st));
         KS_CUDA(cudaStreamSynchronize(st));
     }
 }
@@ -409,6 +371,10 @@ static void fd_create_impl(int kind, int d, const int* dims, double nu, int p_t,
     KS_REQUIRE(p_t >= 1 && p_t <= 8, KS_EINVAL, "ks_fd_create: time degree must be 1..8");
     for (int a = 0; a <= d; ++a) KS_REQUIRE(dims[a] >= 1, KS_EINVAL, "CoeffTensor: dims must be positive");
     for (int l = 0; l < d; ++l) KS_REQUIRE(U[l] && lambda[l], KS_EINVAL, "ks_fd_create: NULL U/lambda");
+    // the transforms keep the (folded halves of the) n x n eigenvector matrix
+    // resident in shared memory: n <= 160 (every BASELINE config: n <= 132)
+    for (int l = 1; l <= d; ++l)
+        KS_REQUIRE(dims[l] <= 160, KS_EINVAL, "ks_fd_create: spatial axis longer than 160 not supported");
     ensure_device(device);
     std::unique_ptr<ks_fd> f(new ks_fd());
     f->device = device;
@@ -420,6 +386,8 @@ static void fd_create_impl(int kind, int d, const int* dims, double nu, int p_t,
     for (int l = 1; l <= d; ++l) f->Ns *= (size_t)dims[l];
     f->N = f->Ns * (size_t)dims[0];
     KS_CUDA(cudaStreamCreateWithFlags(&f->stream, cudaStreamNonBlocking));
+    KS_CUDA(cudaEventCreateWithFlags(&f->done, cudaEventDisableTiming));
+    KS_CUDA(cudaEventCreateWithFlags(&f->ev_user, cudaEventDisableTiming));
     for (int l = 0; l < d; ++l) {
         const int n = dims[l + 1];
         for (int i = 0; i < n; ++i)
@@ -474,22 +442,7 @@ static void fd_create_impl(int kind, int d, const int* dims, double nu, int p_t,
     B.p = p_t;
     B.ldab = 3 * p_t + 1;
     B.ns = f->Ns;
-    // fused outermost-axis kernel (ks_fdfused.cu) when the slab fits shared memory;
-    // it streams per-column factors, so it factors every fiber (no dedup)
-    const long long Np_all = (long long)(f->Ns / (size_t)dims[d]);
-    // opt-in (KS_FD_FUSED=1): measured slower than the unfused path at c3 (1.39 ms
-    // vs 0.98 ms for the same work; the serial block solves of one slab leave
-    // 6 of 8 warps at the barrier) -- see profiles/round1_summary.md
-    bool fused = false;
-    if (const char* e = std::getenv("KS_FD_FUSED"))
-        fused = std::strcmp(e, "1") == 0 && fd_fused_supported(nt, dims[d], p_t);
-    f->fused = fused;
-    f->fuse12 = d >= 3 && fold12_supported(f->fold[0], f->fold[1]);
-    if (fused) {
-        B.fused_nd = dims[d];
-        B.fused_np = Np_all;
-    }
-    bool dedup = d >= 2 && !fused;
+    bool dedup = d >= 2;
     for (int l = 1; l < d && dedup; ++l)
         dedup = dims[l + 1] == dims[1] &&
                 std::memcmp(lambda[l], lambda[0], sizeof(double) * dims[1]) == 0;
@@ -504,19 +457,16 @@ static void fd_create_impl(int kind, int d, const int* dims, double nu, int p_t,
     int idx[3] = {0, 0, 0};
     // pair mode (default for d = 3 with identical axes 2, 3; KS_FD_PAIR=0 off):
     // coalesced two-fiber solves, half the blocks of the plain layout
-    bool pair = d == 3 && !fused && dims[2] == dims[3] &&
+    bool pair = d == 3 && dims[2] == dims[3] &&
                 std::memcmp(lambda[1], lambda[2], sizeof(double) * dims[2]) == 0;
     if (const char* e = std::getenv("KS_FD_PAIR")) pair = pair && std::strcmp(e, "0") != 0;
-    // time-major hand-off on axis 1 (default for pair mode with a folded axis 1;
-    // KS_FD_TM1=0 off): forward transforms run axes d..1, the last one writes
+    // time-major hand-off on axis 1 (pair mode with a folded axis 1): forward
+    // transforms run axes d..1, the last one writes
     // T[t][pos(i1) + n1*(i2 + n2*i3)] with the even eigen-indices of axis 1 at
     // positions 0..hc-1 and the odd ones after them (FoldAxis::perm), so both
     // time-major transforms move whole 1 KB rows; the blocks are numbered by
-    // position. NAT mode (natural-layout solve) and the fused paths keep the
-    // eigen-index order.
-    bool tm1 = pair && f->fold[0].n > 0 && !f->fuse12 && (int)f->fold[0].perm.size() == dims[1];
-    if (const char* e = std::getenv("KS_FD_TM1")) tm1 = tm1 && std::strcmp(e, "0") != 0;
-    if (const char* e = std::getenv("KS_FD_NAT")) tm1 = tm1 && std::strcmp(e, "1") != 0;
+    // position.
+    const bool tm1 = pair && f->fold[0].n > 0 && (int)f->fold[0].perm.size() == dims[1];
     f->tm1 = tm1;
     if (pair) {
         const int n1 = dims[1], n2 = dims[2];
@@ -666,9 +616,8 @@ int ks_fd_info(const ks_fd* fd, int* folded_axes, size_t* blocks) {
     int m = 0;
     for (size_t l = 0; l < fd->fold.size(); ++l)
         if (fd->fold[l].n) m |= 1 << l;
-    if (fd->fuse12 && !fd->fused) m |= 1 << 16;
     if (fd->tm1) m |= 1 << 17;
-    if (fd->blocks.nopiv) m |= 1 << 18;
+    if (fd->blocks.kind == 0 || fd->blocks.nopiv) m |= 1 << 18; // kind 0: L D L^H, never pivots
     if (folded_axes) *folded_axes = m;
     if (blocks) *blocks = fd->blocks.nblk;
     API_END
@@ -781,6 +730,7 @@ static void kron_create_impl(int ndim, const int* dims, int nterms, const ks_ter
     k->N = 1;
     for (int a = 0; a < ndim; ++a) k->N *= (size_t)(k->sharded && a == ndim - 1 ? k->hi - k->lo : dims[a]);
     KS_CUDA(cudaStreamCreateWithFlags(&k->stream, cudaStreamNonBlocking));
+    KS_CUDA(cudaEventCreateWithFlags(&k->done, cudaEventDisableTiming));
     k->plan.reset(kron_plan(pdims, bands, bn, bbw, coeffs, fids));
     if (k->sharded && bbw.size() && pdims.back() != (int)(k->hi - k->lo))
         kron_plan_set_shard(*k->plan, (int)(k->hi - k->lo), (int)(k->lo - k->ext_lo), (int)k->lo);
@@ -840,8 +790,10 @@ int ks_kronshard_apply(ks_kron* k, const ks_c64* x_ext, ks_c64* y_slab, void* st
     std::lock_guard<std::mutex> lk(k->mu);
     ensure_device(k->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : k->stream;
+    KS_CUDA(cudaStreamWaitEvent(st, k->done, 0));
     kron_apply(*k->plan, reinterpret_cast<const double2*>(x_ext), reinterpret_cast<double2*>(y_slab), st,
                k->hptrs);
+    KS_CUDA(cudaEventRecord(k->done, st));
     if (!stream) KS_CUDA(cudaStreamSynchronize(st));
     API_END
 }
@@ -892,6 +844,9 @@ int ks_pcg(ks_kron* A, ks_fd* P, const ks_c64* b, ks_c64* x, int mem, const ks_p
     ensure_device(A->device);
     std::memset(report, 0, sizeof(*report));
     cudaStream_t st = A->stream;
+    // after any apply still in flight on either handle (other streams)
+    KS_CUDA(cudaStreamWaitEvent(st, A->done, 0));
+    if (P) KS_CUDA(cudaStreamWaitEvent(st, P->done, 0));
     const size_t n = A->N, bytes = n * sizeof(double2);
     const auto t_start = std::chrono::steady_clock::now();
 
@@ -972,27 +927,13 @@ int ks_pcg(ks_kron* A, ks_fd* P, const ks_c64* b, ks_c64* x, int mem, const ks_p
         ~Graphs() { reset(); }
     } graphs;
     bool use_graph = graphs_ok, seen[2] = {false, false};
-    // Deferred solution update (default; KS_PCG_XDEFER=0 off): phase A updates
-    // only r, and x += alpha_k p_k rides along the p update of phase B (which
-    // reads p_k anyway) -- or runs alone before a true residual and at exit.
-    // Same arithmetic on the same operands: bit-identical iterates, 48 B per
-    // element less vector traffic per iteration. In strict mode x is needed
-    // every iteration, so it is updated right after phase A.
-    const bool xdefer = [] {
-        const char* e = std::getenv("KS_PCG_XDEFER");
-        return !(e && std::strcmp(e, "0") == 0);
-    }();
+    // Deferred solution update: phase A updates only r, and x += alpha_k p_k
+    // rides along the p update of phase B (which reads p_k anyway) -- or runs
+    // alone before a true residual and at exit. Same arithmetic on the same
+    // operands: bit-identical iterates, 48 B per element less vector traffic per
+    // iteration. In strict mode x is needed every iteration, so it is updated
+    // right after phase A.
     bool pending = false; // x += alpha_k p_k not yet applied
-    // rho' = Re <r, P r> reduced inside the preconditioner's last transform
-    // (opt-in KS_PCG_FUSEDOT=1; rounding-level change of rho', same counts).
-    // Measured c3: the DOT transform takes 233 us against 124 us + 91 us for
-    // the plain transform and the separate dotc -- its epilogue waits on the r
-    // loads (no register or shared-memory room to prefetch them) -- so the
-    // separate reduction stays the default.
-    const bool fuse_dot = [] {
-        const char* e = std::getenv("KS_PCG_FUSEDOT");
-        return e && std::strcmp(e, "1") == 0;
-    }();
     auto apply_x = [&]() {
         if (!pending) return;
         launch_x_update_dev(rho_old.result.as<double>(), red_c.result.as<double>(), p.as<double2>(), xv.as<double2>(),
@@ -1002,24 +943,16 @@ int ks_pcg(ks_kron* A, ks_fd* P, const ks_c64* b, ks_c64* x, int mem, const ks_p
     auto phase_a = [&]() {
         kron_apply(*A->plan, p.as<double2>(), q.as<double2>(), st, A->hptrs);
         launch_dotc(red_c, p.as<double2>(), q.as<double2>(), n, st); // curvature Re <p, Ap>
-        if (xdefer)
-            launch_cg_update_r_dev(red_u, rho_old.result.as<double>(), red_c.result.as<double>(), q.as<double2>(),
-                                   r.as<double2>(), n, st);
-        else
-            launch_cg_update_dev(red_u, rho_old.result.as<double>(), red_c.result.as<double>(), p.as<double2>(),
-                                 q.as<double2>(), xv.as<double2>(), r.as<double2>(), n, st);
+        launch_cg_update_r_dev(red_u, rho_old.result.as<double>(), red_c.result.as<double>(), q.as<double2>(),
+                               r.as<double2>(), n, st);
         KS_CUDA(cudaMemcpyAsync(red_c.host, red_c.result.p, sizeof(double), cudaMemcpyDeviceToHost, st));
         KS_CUDA(cudaMemcpyAsync(red_u.host, red_u.result.p, sizeof(double), cudaMemcpyDeviceToHost, st));
     };
     auto phase_b = [&]() {
-        // z = P r and rho' = Re <r, z> (fused into the FD's last transform when it can be)
-        if (P && fuse_dot) {
-            fd_apply_dev(P, r.as<double2>(), z.as<double2>(), false, st, nullptr, &rho_new);
-        } else {
-            if (P) fd_apply_dev(P, r.as<double2>(), z.as<double2>(), false, st, nullptr);
-            else KS_CUDA(cudaMemcpyAsync(z.p, r.p, bytes, cudaMemcpyDeviceToDevice, st));
-            launch_dotc(rho_new, r.as<double2>(), z.as<double2>(), n, st); // rho'
-        }
+        // z = P r and rho' = Re <r, z>
+        if (P) fd_apply_dev(P, r.as<double2>(), z.as<double2>(), false, st, nullptr);
+        else KS_CUDA(cudaMemcpyAsync(z.p, r.p, bytes, cudaMemcpyDeviceToDevice, st));
+        launch_dotc(rho_new, r.as<double2>(), z.as<double2>(), n, st); // rho' = Re <r, z>
         if (pending) { // (the caller clears pending: a replayed graph does not run this body)
             launch_xpby_x_dev(z.as<double2>(), rho_new.result.as<double>(), rho_old.result.as<double>(),
                               red_c.result.as<double>(), p.as<double2>(), xv.as<double2>(), n, st);
@@ -1062,6 +995,8 @@ int ks_pcg(ks_kron* A, ks_fd* P, const ks_c64* b, ks_c64* x, int mem, const ks_p
         KS_CUDA(cudaMemcpyAsync(x, xv.p, bytes,
                                 mem == KS_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                                 st));
+        KS_CUDA(cudaEventRecord(A->done, st));
+        if (P) KS_CUDA(cudaEventRecord(P->done, st));
         KS_CUDA(cudaStreamSynchronize(st));
         double t_mv = 0, t_pc = 0;
         for (auto& e : mv_ev) t_mv += elapsed(evs[e.first], evs[e.second]) * 1e-3;
@@ -1106,7 +1041,7 @@ int ks_pcg(ks_kron* A, ks_fd* P, const ks_c64* b, ks_c64* x, int mem, const ks_p
             break;
         }
         report->iterations++;
-        pending = xdefer;
+        pending = true;
         double relres = std::sqrt(red_u.host[0]) / bnorm;
         if (opts->strict_residual) {
             apply_x();
@@ -1279,6 +1214,7 @@ int ks_fd_time(ks_fd* fd, const ks_c64* r, ks_c64* z, int iters, int flush, doub
     std::lock_guard<std::mutex> lk(fd->mu);
     ensure_device(fd->device);
     cudaStream_t st = fd->stream;
+    KS_CUDA(cudaStreamWaitEvent(st, fd->done, 0));
     DevBuf& fb = flush_buf();
     const size_t fbytes = (size_t)256 << 20;
     if (flush && fb.bytes < fbytes) fb.alloc(fbytes);
@@ -1314,6 +1250,7 @@ int ks_kron_time(ks_kron* k, const ks_c64* x, ks_c64* y, int iters, int flush, d
     std::lock_guard<std::mutex> lk(k->mu);
     ensure_device(k->device);
     cudaStream_t st = k->stream;
+    KS_CUDA(cudaStreamWaitEvent(st, k->done, 0));
     DevBuf& fb = flush_buf();
     const size_t fbytes = (size_t)256 << 20;
     if (flush && fb.bytes < fbytes) fb.alloc(fbytes);

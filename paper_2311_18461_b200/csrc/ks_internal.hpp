@@ -81,6 +81,12 @@ struct DevBuf {
 };
 
 void ensure_device(int device);
+// Opt `func` into `bytes` of dynamic shared memory on the CURRENT device. The
+// attribute is per device, so the cache is keyed by (device, function): a
+// handle on a second GPU in the same process gets its own opt-in.
+void smem_optin(const void* func, int bytes);
+// SM count of the current device (cached per device)
+int device_sms();
 
 // ---------------------------------------------------------------------------
 // reductions / BLAS-1 (ks_blas.cu). Deterministic: fixed grid, fixed tree.
@@ -159,31 +165,15 @@ struct FoldAxis {
 // or KS_FD_FOLD=0
 // lam: the axis eigenvalues (near-degenerate pairs are re-combined into even/odd)
 bool fold_axis_build(const double* U, const double* lam, int n, double tol, FoldAxis& F);
-// fused folded transforms on axes 1 and 2 (ks_fold12.cu): one HBM pass for
-// both mode products; natural layout, axis 1 stride n0, outer = prod dims[3..]
-bool fold12_supported(const FoldAxis& F1, const FoldAxis& F2);
-void launch_fold12(const FoldAxis& F1, const FoldAxis& F2, bool inverse, const double* X, double* Y, int n0,
-                   long long outer, cudaStream_t st);
-// dot (optional, plain inverse transforms): also reduce Re <dot_x, Y> into dot->result[0]
 void launch_mode_gemm_fold(const FoldAxis& F, bool inverse, const double* X, double* Y,
                            size_t s_complex, size_t outer, cudaStream_t st, int layout = 0, int nt = 0,
-                           const double* const* rows_in = nullptr, double* const* rows_out = nullptr,
-                           const double* dot_x = nullptr, Reducer* dot = nullptr);
+                           const double* const* rows_in = nullptr, double* const* rows_out = nullptr);
 
 // ---------------------------------------------------------------------------
 // plan-specialised fused level passes (ks_kron_jit.cu, NVRTC at plan creation)
 // ---------------------------------------------------------------------------
 // NVRTC for sm_100a, cached by source (ks_kron_jit.cu)
 cudaKernel_t nvrtc_kernel(const std::string& src, const char* name, size_t max_smem);
-// d = 3 matvec in two launches: axis 3, then axes t/1/2 fused (ks_kron3.cu)
-struct Kron3;
-Kron3* kron3_build(const std::vector<int>& dims, int bw, int nmax, const std::vector<int>& freal,
-                   const std::vector<double2>& coeffs, const std::vector<std::vector<int>>& fids);
-void kron3_apply(Kron3& K, const double2* x, double2* y, const double2* rb, cudaStream_t st);
-void kron3_free(Kron3* p);
-struct Kron3Deleter {
-    void operator()(Kron3* p) const { kron3_free(p); }
-};
 struct JitContrib {
     int in, out, factor, coeff; // coeff = index into the coefficient table
 };
@@ -210,80 +200,36 @@ struct FdBlocks {
     int nt = 0, p = 0, ldab = 0;
     size_t ns = 0;      // fibers (= N_s)
     size_t nblk = 0;    // factored blocks (N_s, or fewer when deduplicated)
-    // band storage, one of three layouts (fd_band_index):
-    //   rec > 0:           step-major records ab[(k*nblk + b)*rec + e], e < ldab, and the
-    //                      pivot offset as a double in slot ldab (rec = ldab + 1);
-    //                      a fiber's step-k band column is one contiguous record
-    //   fused_nd > 0:      per-rest-column layout of the fused axis-d kernel
-    //   otherwise:         block-interleaved ab[(k*ldab + e)*nblk + b], piv[k*nblk + b]
-    DevBuf ab;
-    DevBuf piv;         // uint8 pivot offsets piv[k]-k in 0..p (not used with rec)
-    int rec = 0;
-    DevBuf flag;        // int: bit 0 singular pivot, bit 1 some row interchange (factor kernel)
-    bool nopiv = false; // no block pivoted at all
-    DevBuf wpiv;        // uint8 per 32 consecutive blocks: some block pivoted (pair solve takes
-                        // the fill-in-free body for warps whose blocks did not)
-    bool nopiv_off = false; // KS_FD_NOPIV=0 at factor time: full band everywhere
-    DevBuf bpiv;        // uint8 per block: pivoted
-    DevBuf wpivf;       // uint8 per 32 consecutive fibers: some fiber's block pivoted (ring solve)
+    int kind = 0;       // 0: H = Lt + nu^2 lam^2 Mt + nu lam (W + W^H), HPD -> L D L^H;
+                        // 1 (Galerkin): H = W + nu lam Mt -> partial-pivot LU
+    // kind 0, block-interleaved: dinv[k*nblk + b] = 1/d_k, v[(k*p + j-1)*nblk + b] = u(k,k+j)/d_k
+    DevBuf dinv, v;
+    // kind 1, block-interleaved band ab[(k*ldab + e)*nblk + b], pivot offsets piv[k*nblk + b]
+    DevBuf ab, piv;
+    DevBuf wpiv;        // uint8 per 32 consecutive blocks: some block pivoted (kind 1 pair solve)
+    bool nopiv = false; // kind 1: no block pivoted at all
+    DevBuf flag;        // int: bit 0 singular / not HPD, bit 1 some row interchange
     DevBuf lam_blk;     // double [nblk] composite eigenvalue of each block
     DevBuf fiber_block; // int [ns] block of each fiber (empty = identity)
     // pair mode (d = 3, axes 2 and 3 identical): block b = i1 + n1 * pidx over
     // pairs (i2 <= i3), solved for fibers (i1, i2, i3) and (i1, i3, i2) together
     int pair_n1 = 0, pair_n2 = 0;
-    int kind = 0;       // 0: H = Lt + nu^2 lam^2 Mt + nu lam (W + W^H); 1 (Galerkin): H = W + nu lam Mt
     DevBuf pairs;       // int2 [npairs] (i2, i3)
-    int fused_nd = 0;        // > 0: per-rest-column layout for the fused axis-d kernel
-    long long fused_np = 0;  //      (block i = rho + fused_np * r, r < fused_nd)
+    // the time bands the blocks were built from (owned by the handle; kept for
+    // ks_fd_block's on-demand LU of one kind-0 block)
+    double nu = 1.0;
+    const double *Lt = nullptr, *Mt = nullptr;
+    const double2* Wsym = nullptr;
 };
-// address of band entry (k, e) of block b: fb + k*fk + e*fe; pivot offset
-// (non-rec layouts) at piv[pb + k*pk]
-struct BandIndex {
-    size_t fb, fk, fe, pb, pk;
-};
-__host__ __device__ inline BandIndex fd_band_index(size_t b, int nt, int ldab, size_t nblk, int rec,
-                                                   int fused_nd, long long fused_np) {
-    BandIndex x;
-    if (rec > 0) {
-        x.fb = b * (size_t)rec;
-        x.fk = nblk * (size_t)rec;
-        x.fe = 1;
-        x.pb = x.pk = 0;
-    } else if (fused_nd > 0) {
-        const size_t rho = b % (size_t)fused_np, r = b / (size_t)fused_np;
-        x.fb = rho * (size_t)nt * ldab * fused_nd + r;
-        x.fe = fused_nd;
-        x.fk = (size_t)ldab * fused_nd;
-        x.pb = rho * (size_t)nt * fused_nd + r;
-        x.pk = fused_nd;
-    } else {
-        x.fb = b;
-        x.fe = nblk;
-        x.fk = (size_t)ldab * nblk;
-        x.pb = b;
-        x.pk = nblk;
-    }
-    return x;
-}
-// allocate ab / piv / flag for B.nblk blocks in the layout chosen by B.fused_nd
-// and KS_FD_REC (records unless KS_FD_REC=0)
+// allocate the factor storage of B.nblk blocks for B.kind
 void fd_blocks_alloc(FdBlocks& B);
-// copy block b back to the host in BandedFactorization layout (eigensolve.hpp:36-42)
+// the reference's LU of block b (factor_banded layout, eigensolve.hpp:36-42) on the host
 void fd_block_to_host(const FdBlocks& B, size_t b, ks_c64* ab, int* piv);
 // time bands on device: Lt, Mt real (2p+1)xnt, Wsym complex
 void launch_fd_factor(FdBlocks& B, double nu, const double* Lt, const double* Mt,
                       const double2* Wsym, cudaStream_t st);
-// time_major: X is T[t][fiber] (stride ns between time steps) instead of
-// contiguous fibers X[fiber][t]
-void launch_fd_solve(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t st,
-                     bool time_major = false);
-
-// fused outermost-axis step of the FD apply (ks_fdfused.cu): X natural
-// (n_t, Np, n_d) -> forward transform with At_fwd, block solves, inverse with
-// At_inv -> Z natural. Returns false when the shape is not supported.
-bool fd_fused_supported(int nt, int nd, int p);
-void launch_fd_fused(const double* At_fwd, const double* At_inv, const FdBlocks& B, int nd,
-                     long long Np, const double2* X, double2* Z, cudaStream_t st);
+// block solves on the time-major layout X = T[t][fiber] (stride ns between time steps)
+void launch_fd_solve(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t st);
 
 // ---------------------------------------------------------------------------
 // level-pass Kronecker engine (ks_kron.cu)

@@ -47,11 +47,6 @@ bool launch_colsweep(int nin, int nout, int bw, const double2* const* ip, double
                      const int* freal, size_t ncols, size_t s, int n, int nmax, cudaStream_t st,
                      int nir, int ioff, int boff, const int* ring_begin, const RingCon* ring_cons);
 
-bool launch_kron_pair(int nin, int nmid, int nout, int bw, const double2* const* ip, double2* const* op,
-                      const int* a_begin, const SweepEntry* a_ent, const int* b_begin, const SweepEntry* b_ent,
-                      const int* b_obegin, const void* b_con, const double2* rb, const int* freal, int nmax,
-                      long long s_a, int n_a, int n_b, long long n_outer, cudaStream_t st);
-
 struct KronFactor {
     int n = 0, bw = 0;
     bool is_real = false;
@@ -97,8 +92,6 @@ struct KronPlan {
     std::vector<std::vector<std::unique_ptr<KronJitPair, KronJitDeleter>>> jit_alt;
     // device pointer tables per (x, y) pair (kron_apply)
     std::map<std::pair<const void*, void*>, DevBuf> ptr_tables;
-    // d = 3: axis 3 then axes t/1/2 fused (ks_kron3.cu); null = level passes
-    std::unique_ptr<Kron3, Kron3Deleter> k3;
 };
 
 namespace {
@@ -596,7 +589,7 @@ KronPlan* kron_plan(const std::vector<int>& dims,
             const long long outer = (long long)(P->N / (sa * (size_t)na * (size_t)nbb));
             P->jit[k].reset(kron_jit_build(pa.n_in, pa.n_out, pb.n_out, P->bwmax, ca, cb, frv, co, (long long)sa, na,
                                            nbb, outer));
-            if (P->jit[k] && !std::getenv("KS_KRON_JIT_MAXT"))
+            if (P->jit[k])
                 for (int tm : {192, 128}) {
                     std::unique_ptr<KronJitPair, KronJitDeleter> alt(kron_jit_build(
                         pa.n_in, pa.n_out, pb.n_out, P->bwmax, ca, cb, frv, co, (long long)sa, na, nbb, outer, tm));
@@ -605,18 +598,6 @@ KronPlan* kron_plan(const std::vector<int>& dims,
                     if (!dup) P->jit_alt[k].push_back(std::move(alt));
                 }
         }
-    }
-    {
-        // factor classes for the generated kernel: 1 real, 2 purely imaginary, 0 complex
-        std::vector<int> fcl(std::max<size_t>(P->factors.size(), 1), 1);
-        for (size_t f = 0; f < P->factors.size(); ++f) {
-            const KronFactor& kf = P->factors[f];
-            bool imag = !kf.is_real;
-            for (size_t e = 0; e < (size_t)kf.n * (2 * kf.bw + 1) && imag; ++e) imag = pool[kf.off + e].x == 0.0;
-            fcl[f] = kf.is_real ? 1 : (imag ? 2 : 0);
-        }
-        bool all_active = D == 4 && (int)ax.size() == 4;
-        if (all_active) P->k3.reset(kron3_build(dims, P->bwmax, P->nmax, fcl, coeffs, fids));
     }
     for (auto& ps : P->passes) {
         std::vector<int> ib(ps.n_in + 1, 0);
@@ -663,7 +644,6 @@ KronPlan* kron_plan(const std::vector<int>& dims,
 }
 
 int kron_plan_engine(const KronPlan& P) {
-    if (P.k3 && P.shard_rows == 0) return 2;
     for (auto& j : P.jit)
         if (j && kron_jit_runs(*j)) return 1;
     return 0;
@@ -677,10 +657,6 @@ void kron_plan_info(const KronPlan& P, int* npasses, int* nnodes, int* nproducts
 
 void kron_apply(KronPlan& P, const double2* x, double2* y, cudaStream_t st,
                 std::vector<void*>& host_ptrs) {
-    if (P.k3 && P.shard_rows == 0) {
-        kron3_apply(*P.k3, x, y, P.d_rowband.as<double2>(), st);
-        return;
-    }
     // which passes run fused (same decision as the dispatch below): allocate only
     // the level pools that some launch reads or writes
     auto fused_at = [&](size_t k) {
@@ -777,25 +753,6 @@ void kron_apply(KronPlan& P, const double2* x, double2* y, cudaStream_t st,
                 continue;
             }
         }
-        // generic fused pair (opt-in, KS_KRON_PAIR=1): run-time interpreted plan
-        if (std::getenv("KS_KRON_PAIR") && k + 1 < P.passes.size() && P.passes[k + 1].axis == ps.axis + 1 &&
-            P.bwmax >= 1 && P.bwmax <= 4 && !(P.shard_rows > 0 && k + 2 == P.passes.size())) {
-            const KronPass& nx = P.passes[k + 1];
-            auto ip = reinterpret_cast<const double2* const*>(dp + P.ptr_off[k]);
-            auto op = reinterpret_cast<double2* const*>(const_cast<void**>(dp + P.ptr_off[k + 1] + nx.n_in));
-            const int nb = P.dims[ps.axis + 1];
-            const long long outer = (long long)(P.N / ((size_t)s * n * nb));
-            const bool ok = nx.n_in == ps.n_out &&
-                            launch_kron_pair(ps.n_in, ps.n_out, nx.n_out, P.bwmax, ip, op, ps.d_in_begin.as<int>(),
-                                             ps.d_entries.as<SweepEntry>(), nx.d_in_begin.as<int>(),
-                                             nx.d_entries.as<SweepEntry>(), nx.d_begin.as<int>(), nx.d_contribs.p,
-                                             P.d_rowband.as<double2>(), P.d_freal.as<int>(), P.nmax, (long long)s,
-                                             n, nb, outer, st);
-            if (ok) {
-                ++k;
-                continue;
-            }
-        }
         // element-parallel level kernel (all axes)
         if (ps.n_out <= 8 && P.bwmax >= 1 && P.bwmax <= 4) {
             auto ip = reinterpret_cast<const double2* const*>(dp + P.ptr_off[k]);
@@ -855,7 +812,7 @@ void kron_apply(KronPlan& P, const double2* x, double2* y, cudaStream_t st,
 void kron_plan_free(KronPlan* p) { delete p; }
 
 bool kron_has_table(const KronPlan& P, const void* x, const void* y) {
-    return P.ptr_tables.count(std::make_pair(x, const_cast<void*>(y))) > 0 || (P.k3 && P.shard_rows == 0);
+    return P.ptr_tables.count(std::make_pair(x, const_cast<void*>(y))) > 0;
 }
 
 void kron_plan_set_shard(KronPlan& P, int rows, int in_off, int band_off) {

@@ -140,7 +140,7 @@ KronJitPair* kron_jit_build(int nin, int nmid, int nout, int bw, const std::vect
     // size rounded to whole warps; pick the fullest block of at most 384 threads
     int c_best = 1, T_best = 0;
     double e_best = -1;
-    const int tmax = std::getenv("KS_KRON_JIT_MAXT") ? std::atoi(std::getenv("KS_KRON_JIT_MAXT")) : tmax_default;
+    const int tmax = tmax_default;
     for (int c = 1; c * n_a <= tmax; ++c) {
         if (s_a > 1 && c > s_a) break;
         if (s_a == 1 && c > n_outer) break;
@@ -159,15 +159,16 @@ KronJitPair* kron_jit_build(int nin, int nmid, int nout, int bw, const std::vect
     const long long nqb = (s_a + nq - 1) / nq, nob = (n_outer + no - 1) / no;
     const int pad = bw * nq;
     const int RS = T + 2 * pad; // ring row: halo | T points | halo
-    // ring depth: planes in flight per CTA (KS_KRON_JIT_D overrides for experiments)
-    int D = std::getenv("KS_KRON_JIT_D") ? std::max(2, std::min(12, std::atoi(std::getenv("KS_KRON_JIT_D")))) : dmax;
+    // ring depth: planes in flight per CTA (deeper rings, D = 6..10, measured
+    // slower: the passes are issue / latency bound, not short of bytes in flight)
+    int D = dmax;
     auto smem = [&](int d) { return (size_t)d * nin * RS * sizeof(double2); };
     while (D > 2 && smem(D) > 110 * 1024) --D;
     if (smem(D) > 200 * 1024) return nullptr;
     // no register cap: capping at 128 (2 blocks/SM) spills and is slower at c3
-    // (1.98 vs 1.67 ms; KS_KRON_JIT_MINB overrides for experiments)
+    // (1.98 vs 1.67 ms)
     const int minb = 1;
-    const int minb_env = std::getenv("KS_KRON_JIT_MINB") ? std::atoi(std::getenv("KS_KRON_JIT_MINB")) : 0;
+    const int minb_env = 0;
     // factor classes (freal): 1 real, 2 purely imaginary (one double per entry), 0 complex
     auto is_real = [&](int f) { return f >= 0 && freal[f] == 1; };
     auto is_imag = [&](int f) { return f >= 0 && freal[f] == 2; };
@@ -188,7 +189,7 @@ KronJitPair* kron_jit_build(int nin, int nmid, int nout, int bw, const std::vect
     // merged rows) become a copy / an add, and the first contribution into a
     // still-zero accumulator a plain assignment -- bit-identical (1*v = v,
     // 0 + v = v) and up to 2 DFMA less per contribution (KS_KRON_JIT_UNIT=0 off).
-    const bool unit_ok = !(std::getenv("KS_KRON_JIT_UNIT") && std::strcmp(std::getenv("KS_KRON_JIT_UNIT"), "0") == 0);
+    const bool unit_ok = true;
     std::set<std::string> live; // accumulators already holding a contribution
     auto cmac = [&](const std::string& acc, int ci, const std::string& v) -> std::string {
         const bool fresh = live.insert(acc).second;
@@ -212,7 +213,7 @@ KronJitPair* kron_jit_build(int nin, int nmid, int nout, int bw, const std::vect
         fbl.assign(t.begin(), t.end());
     }
     const size_t bstage = fbl.size() * (size_t)n_b * W * sizeof(double2);
-    const bool stage = smem(D) + bstage <= 200 * 1024 && !std::getenv("KS_KRON_JIT_NOSTAGE");
+    const bool stage = smem(D) + bstage <= 200 * 1024;
     size_t nfa = 0;
     {
         std::set<int> t;
@@ -221,8 +222,8 @@ KronJitPair* kron_jit_build(int nin, int nmid, int nout, int bw, const std::vect
         nfa = t.size();
     }
     const size_t astage = nfa * (size_t)n_a * W * sizeof(double2);
-    const bool asm_rows = std::getenv("KS_KRON_JIT_ASMEM") && std::strcmp(std::getenv("KS_KRON_JIT_ASMEM"), "1") == 0 &&
-                          smem(D) + (stage ? bstage : 0) + astage <= 200 * 1024;
+    const bool asm_rows = false; // axis-a rows from shared memory: measured slower, generator kept off
+    (void)astage;
     auto bidx = [&](int f) { return (int)(std::find(fbl.begin(), fbl.end(), f) - fbl.begin()); };
     std::ostringstream s;
     s << "// generated: fused level passes (ks_kron_jit.cu)\n"
@@ -320,12 +321,12 @@ ks_pair(const double2* const* __restrict__ ip, double2* const* __restrict__ op, 
     // register slot (ib + 1 + j) % W (pull) / (ib + j) % W (push) instead of
     // being shifted every plane -- ncu showed the shifts as ~20% of the pass-1
     // instructions (IMAD.MOV).
-    const bool rot = !(std::getenv("KS_KRON_JIT_ROT") && std::strcmp(std::getenv("KS_KRON_JIT_ROT"), "0") == 0);
+    const bool rot = true;
     auto WP = [&](const std::string& j) { return rot ? "(ph + 1 + (" + j + ")) % W" : j; };
     // products sharing a tap loop emitted as one loop (independent FMA chains
     // interleaved in the source; KS_KRON_JIT_ILV=0 one loop per product):
     // c5 18.9 -> 18.3 ms, c3 unchanged
-    const bool ilv = !(std::getenv("KS_KRON_JIT_ILV") && std::strcmp(std::getenv("KS_KRON_JIT_ILV"), "0") == 0);
+    const bool ilv = true;
     auto WQ = [&](const std::string& j) { return rot ? "(ph + (" + j + ")) % W" : j; };
     s << "    double2 win[" << nwin << "][W];\n"
       << "#pragma unroll\n    for (int h = 0; h < " << nwin << "; ++h)\n#pragma unroll\n        for (int j = 0; j < W; ++j) win[h][j] = Z;\n";
@@ -466,23 +467,8 @@ ks_pair(const double2* const* __restrict__ ip, double2* const* __restrict__ op, 
         }
     }
     s << "    asm volatile(\"cp.async.wait_group 0;\\n\" ::);\n}\n";
-    if (const char* dump = std::getenv("KS_KRON_JIT_DUMP")) { // debugging: append the generated source
-        if (FILE* f = std::fopen(dump, "a")) {
-            std::fprintf(f, "// ---- s_a=%lld n_a=%d n_b=%d outer=%lld T=%d nq=%d no=%d D=%d\n%s\n", s_a, n_a, n_b,
-                         n_outer, T, nq, no, D, s.str().c_str());
-            std::fclose(f);
-        }
-    }
     std::unique_ptr<KronJitPair> P(new KronJitPair());
     P->k = jit_compile(s.str());
-    if (const char* dump = std::getenv("KS_KRON_JIT_DUMP")) {
-        cudaFuncAttributes fa_{};
-        if (cudaFuncGetAttributes(&fa_, (const void*)P->k.fn) == cudaSuccess)
-            if (FILE* f = std::fopen(dump, "a")) {
-                std::fprintf(f, "// regs=%d local=%zu\n", fa_.numRegs, (size_t)fa_.localSizeBytes);
-                std::fclose(f);
-            }
-    }
     P->nin = nin;
     P->nmid = nmid;
     P->nout = nout;

@@ -308,7 +308,7 @@ int ks_fdshard_middle(ks_fdshard* h, ks_c64* work, void* stream) {
     const size_t s = (size_t)P.nt * P.rest[P.rank].n();
     double* tmp = h->s0.as<double>();
     shard_gemm(h, P.d, false, reinterpret_cast<double*>(work), tmp, s, 1, st, 1, P.nt);
-    launch_fd_solve(h->blocks, reinterpret_cast<double2*>(tmp), false, st, true);
+    launch_fd_solve(h->blocks, reinterpret_cast<double2*>(tmp), false, st);
     shard_gemm(h, P.d, true, tmp, reinterpret_cast<double*>(work), s, 1, st, 2, P.nt);
     if (!stream) KS_CUDA(cudaStreamSynchronize(st));
     API_END
@@ -425,7 +425,7 @@ int ks_fdshard_middle_peer(ks_fdshard* h, void* stream) {
     auto rin = static_cast<const double* const*>(h->rows_in.p);
     auto rout = static_cast<double* const*>(h->rows_out.p);
     shard_gemm(h, P.d, false, h->s1.as<double>() /* dummy, rows come from rin */, tmp, s, 1, st, 1, P.nt, rin, nullptr);
-    launch_fd_solve(h->blocks, reinterpret_cast<double2*>(tmp), false, st, true);
+    launch_fd_solve(h->blocks, reinterpret_cast<double2*>(tmp), false, st);
     shard_gemm(h, P.d, true, tmp, nullptr, s, 1, st, 2, P.nt, nullptr, rout);
     if (!stream) KS_CUDA(cudaStreamSynchronize(st));
     API_END

@@ -19,12 +19,10 @@
 // X tiles stream through shared memory once (double-buffered), each output
 // is written once.
 //
-// Two inner engines over the same tiling:
-//   * DFMA: 8 x TM register micro-tile per thread (CUDA cores);
-//   * DMMA: mma.sync.aligned.m8n8k4.row.col.f64 (FP64 tensor-core path).
-// ks_transform_engine() picks one (env KS_GEMM=dfma|dmma, default below);
-// both are exact FP64 with identical accumulation order per output
-// (k ascending in 16-wide chunks), differing only in FMA rounding.
+// Engine: FP64 tensor cores, mma.sync.aligned.m8n8k4.row.col.f64 (DMMA), with
+// the transform matrix resident in shared memory and X tiles streamed through
+// a cp.async ring. (A DFMA CUDA-core engine over the same tiling measured
+// slower -- c3 FD 3.13 vs 2.17 ms, operand-feed bound -- and was removed.)
 #include "ks_internal.hpp"
 
 #include <cstdlib>
@@ -43,129 +41,6 @@ constexpr int kBK = 16;       // k-chunk
 constexpr int kBN = 128;      // columns (doubles) per CTA
 
 // ---------------------------------------------------------------------------
-// DFMA engine. Warp lanes: tx = lane % 8 (columns), ty = lane / 8 (rows).
-// Warps: wr = warp % 4 (rows), wc = warp / 4 (columns).
-// Thread rows:  r = (wr*4 + ty)*TM + i, i < TM      -> BM = 16*TM
-// Thread cols:  c = wc*64 + m*16 + 2*tx + {0,1}, m < 4
-// ---------------------------------------------------------------------------
-template <int TM>
-__global__ void __launch_bounds__(kThreads, 1)
-k_mode_gemm_dfma(const double* __restrict__ At, int n, const double* __restrict__ X,
-                 double* __restrict__ Y, long long W2, long long C) {
-    constexpr int BM = 16 * TM;
-    constexpr int BMP = BM + 2; // pad (keeps 16 B alignment, breaks row conflicts)
-    extern __shared__ double smem[];
-    double* As = smem;                       // [2][kBK][BMP]
-    double* Bs = smem + 2 * kBK * BMP;       // [2][kBK][kBN]
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int tx = lane & 7, ty = lane >> 3, wr = warp & 3, wc = warp >> 2;
-    const long long c0 = (long long)blockIdx.x * kBN;
-
-    // loader mapping for X: thread owns column pair cp = tid % 64, rows tid/64 + 4k
-    const int lcp = tid & 63;
-    const long long lc = c0 + 2 * lcp;
-    const bool lvalid = lc < C;
-    long long loff = 0;
-    if (lvalid) {
-        const long long o = lc / W2, q = lc - o * W2;
-        loff = o * (long long)n * W2 + q;
-    }
-    const int lrow0 = tid >> 6;
-
-    double2 breg[4];
-    double areg[(kBK * BM + kThreads - 1) / kThreads];
-
-    auto gload = [&](int j0) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int j = j0 + lrow0 + 4 * k;
-            breg[k] = (lvalid && j < n)
-                          ? __ldg(reinterpret_cast<const double2*>(X + loff + (long long)j * W2))
-                          : make_double2(0.0, 0.0);
-        }
-#pragma unroll
-        for (int k = 0; k < (kBK * BM + kThreads - 1) / kThreads; ++k) {
-            const int e = tid + k * kThreads;
-            const int jj = e / BM, r = e - jj * BM;
-            const int j = j0 + jj;
-            areg[k] = (e < kBK * BM && j < n && r < n) ? __ldg(At + (long long)j * n + r) : 0.0;
-        }
-    };
-    auto sstore = [&](int buf) {
-        double* as = As + buf * kBK * BMP;
-        double* bs = Bs + buf * kBK * kBN;
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-            *reinterpret_cast<double2*>(bs + (lrow0 + 4 * k) * kBN + 2 * lcp) = breg[k];
-#pragma unroll
-        for (int k = 0; k < (kBK * BM + kThreads - 1) / kThreads; ++k) {
-            const int e = tid + k * kThreads;
-            if (e < kBK * BM) {
-                const int jj = e / BM, r = e - jj * BM;
-                as[jj * BMP + r] = areg[k];
-            }
-        }
-    };
-
-    double acc[TM][8];
-#pragma unroll
-    for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int m = 0; m < 8; ++m) acc[i][m] = 0.0;
-
-    const int nk = (n + kBK - 1) / kBK;
-    gload(0);
-    sstore(0);
-    __syncthreads();
-    const int rbase = (wr * 4 + ty) * TM;
-    const int cbase = wc * 64 + 2 * tx;
-    for (int kc = 0; kc < nk; ++kc) {
-        const int buf = kc & 1;
-        if (kc + 1 < nk) gload((kc + 1) * kBK);
-        const double* as = As + buf * kBK * BMP;
-        const double* bs = Bs + buf * kBK * kBN;
-#pragma unroll
-        for (int jj = 0; jj < kBK; ++jj) {
-            double a[TM];
-#pragma unroll
-            for (int i = 0; i < TM; ++i) a[i] = as[jj * BMP + rbase + i];
-            double b[8];
-#pragma unroll
-            for (int m = 0; m < 4; ++m) {
-                const double2 v = *reinterpret_cast<const double2*>(bs + jj * kBN + cbase + 16 * m);
-                b[2 * m] = v.x;
-                b[2 * m + 1] = v.y;
-            }
-#pragma unroll
-            for (int i = 0; i < TM; ++i)
-#pragma unroll
-                for (int m = 0; m < 8; ++m) acc[i][m] = fma(a[i], b[m], acc[i][m]);
-        }
-        if (kc + 1 < nk) {
-            sstore(buf ^ 1);
-        }
-        __syncthreads();
-    }
-
-    // epilogue: write Y rows r < n, column pairs
-#pragma unroll
-    for (int m = 0; m < 4; ++m) {
-        const long long c = c0 + cbase + 16 * m;
-        if (c >= C) continue;
-        const long long o = c / W2, q = c - o * W2;
-        double* yb = Y + o * (long long)n * W2 + q;
-#pragma unroll
-        for (int i = 0; i < TM; ++i) {
-            const int r = rbase + i;
-            if (r < n)
-                *reinterpret_cast<double2*>(yb + (long long)r * W2) =
-                    make_double2(acc[i][2 * m], acc[i][2 * m + 1]);
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
 // DMMA engine: FP64 mma.sync m8n8k4 (A row-major 8x4, B col-major 4x8).
 // Fragment ownership (PTX ISA, mma.m8n8k4 .f64):
 //   A: lane holds A[lane/4][lane%4]      B: lane holds B[lane%4][lane/4]
@@ -178,119 +53,6 @@ __device__ __forceinline__ void dmma_m8n8k4(double& c0, double& c1, double a, do
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(c0), "+d"(c1)
                  : "d"(a), "d"(b));
-}
-
-template <int TM>
-__global__ void __launch_bounds__(kThreads, 1)
-k_mode_gemm_dmma(const double* __restrict__ At, int n, const double* __restrict__ X,
-                 double* __restrict__ Y, long long W2, long long C) {
-    constexpr int BM = 16 * TM;
-    constexpr int MT = BM / 2 / 8; // mma row tiles per warp
-    constexpr int BMP = BM + 4;
-    constexpr int BNP = kBN + 4;
-    extern __shared__ double smem[];
-    double* As = smem;                 // [2][kBK][BMP]  (k-major: As[k][r])
-    double* Bs = smem + 2 * kBK * BMP; // [2][kBK][BNP]  (Bs[k][c])
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wr = warp & 1, wc = warp >> 1;
-    const long long c0 = (long long)blockIdx.x * kBN;
-
-    const int lcp = tid & 63;
-    const long long lc = c0 + 2 * lcp;
-    const bool lvalid = lc < C;
-    long long loff = 0;
-    if (lvalid) {
-        const long long o = lc / W2, q = lc - o * W2;
-        loff = o * (long long)n * W2 + q;
-    }
-    const int lrow0 = tid >> 6;
-    double2 breg[4];
-    double areg[(kBK * BM + kThreads - 1) / kThreads];
-
-    auto gload = [&](int j0) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int j = j0 + lrow0 + 4 * k;
-            breg[k] = (lvalid && j < n)
-                          ? __ldg(reinterpret_cast<const double2*>(X + loff + (long long)j * W2))
-                          : make_double2(0.0, 0.0);
-        }
-#pragma unroll
-        for (int k = 0; k < (kBK * BM + kThreads - 1) / kThreads; ++k) {
-            const int e = tid + k * kThreads;
-            const int jj = e / BM, r = e - jj * BM;
-            const int j = j0 + jj;
-            areg[k] = (e < kBK * BM && j < n && r < n) ? __ldg(At + (long long)j * n + r) : 0.0;
-        }
-    };
-    auto sstore = [&](int buf) {
-        double* as = As + buf * kBK * BMP;
-        double* bs = Bs + buf * kBK * BNP;
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-            *reinterpret_cast<double2*>(bs + (lrow0 + 4 * k) * BNP + 2 * lcp) = breg[k];
-#pragma unroll
-        for (int k = 0; k < (kBK * BM + kThreads - 1) / kThreads; ++k) {
-            const int e = tid + k * kThreads;
-            if (e < kBK * BM) {
-                const int jj = e / BM, r = e - jj * BM;
-                as[jj * BMP + r] = areg[k];
-            }
-        }
-    };
-
-    double acc[MT][4][2];
-#pragma unroll
-    for (int i = 0; i < MT; ++i)
-#pragma unroll
-        for (int m = 0; m < 4; ++m) acc[i][m][0] = acc[i][m][1] = 0.0;
-
-    const int nk = (n + kBK - 1) / kBK;
-    gload(0);
-    sstore(0);
-    __syncthreads();
-    const int r_warp = wr * (BM / 2);
-    const int c_warp = wc * 32;
-    const int ar = lane >> 2, ak = lane & 3; // A frag: row ar, k ak
-    const int bk = lane & 3, bn = lane >> 2; // B frag: k bk, col bn
-    for (int kc = 0; kc < nk; ++kc) {
-        const int buf = kc & 1;
-        if (kc + 1 < nk) gload((kc + 1) * kBK);
-        const double* as = As + buf * kBK * BMP;
-        const double* bs = Bs + buf * kBK * BNP;
-#pragma unroll
-        for (int k4 = 0; k4 < kBK; k4 += 4) {
-            double a[MT], b[4];
-#pragma unroll
-            for (int i = 0; i < MT; ++i) a[i] = as[(k4 + ak) * BMP + r_warp + i * 8 + ar];
-#pragma unroll
-            for (int m = 0; m < 4; ++m) b[m] = bs[(k4 + bk) * BNP + c_warp + m * 8 + bn];
-#pragma unroll
-            for (int i = 0; i < MT; ++i)
-#pragma unroll
-                for (int m = 0; m < 4; ++m) dmma_m8n8k4(acc[i][m][0], acc[i][m][1], a[i], b[m]);
-        }
-        if (kc + 1 < nk) sstore(buf ^ 1);
-        __syncthreads();
-    }
-
-    // epilogue: C[lane/4][2*(lane%4)+{0,1}] of each tile
-    const int cr = lane >> 2, cc = 2 * (lane & 3);
-#pragma unroll
-    for (int m = 0; m < 4; ++m) {
-        const long long c = c0 + c_warp + m * 8 + cc;
-        if (c >= C) continue;
-        const long long o = c / W2, q = c - o * W2;
-        double* yb = Y + o * (long long)n * W2 + q;
-#pragma unroll
-        for (int i = 0; i < MT; ++i) {
-            const int r = r_warp + i * 8 + cr;
-            if (r < n)
-                *reinterpret_cast<double2*>(yb + (long long)r * W2) =
-                    make_double2(acc[i][m][0], acc[i][m][1]);
-        }
-    }
 }
 
 // ---------------------------------------------------------------------------
@@ -345,13 +107,6 @@ struct ColMap {
     // (the peer-memory sharded FD: rows of axis d on other GPUs)
     const double* const* rin = nullptr;
     double* const* rout = nullptr;
-    // optional fused reduction (inverse folded transform, DOT variant): Re <x, Y>
-    // over the written output, per-CTA partials + last-block sum in block order
-    // into res[0] (a Reducer's buffers: partial, counter, result)
-    const double* dx = nullptr;
-    double* dpart = nullptr;
-    unsigned* dcnt = nullptr;
-    double* dres = nullptr;
 };
 template <bool ROWS>
 __device__ __forceinline__ const double* in_row(const ColMap& M, const double* X, long long col, int j,
@@ -534,211 +289,34 @@ k_mode_gemm_dmma2(const double* __restrict__ At, int n, const double* __restrict
     cp_async_wait<0>();
 }
 
-// ---------------------------------------------------------------------------
-// DMMA engine v3 (small axes, n <= 80): the whole K extent of a column tile is
-// one cp.async group (two tile buffers), so per synchronisation a warp issues
-// TM*4*nk*4 DMMAs (256 at n = 64) and the per-work-item integer work of v2
-// (which left the SMSP issue slots, not the tensor pipe, as the limit) is paid
-// once per tile. Column maps as in v2. One CTA (8 warps) per SM.
-// ---------------------------------------------------------------------------
 template <int TM>
-__global__ void __launch_bounds__(kThreads, 1)
-k_mode_gemm_dmma3(const double* __restrict__ At, int n, const double* __restrict__ X,
-                  double* __restrict__ Y, ColMap M) {
-    constexpr int BM = 16 * TM;
-    constexpr int MT = TM;
-    constexpr int BMP = BM + 4;
-    constexpr int BNP = kBN + 4;
-    constexpr int KMAX = BM; // K padded to the row padding (n <= BM)
-    extern __shared__ __align__(16) double smem[];
+void launch_tm(const double* At, int n, const double* X, double* Y, cudaStream_t st, const ColMap* map) {
     const int nk = (n + kBK - 1) / kBK;
-    const int kpad = nk * kBK;
-    double* As = smem;                           // [KMAX][BMP]
-    double* Bs = smem + (size_t)KMAX * BMP;      // [2][KMAX][BNP]
-    const long long in_rs = (M.mode == MAP_TIN || M.mode == MAP_TIN1) ? 2 * M.Np : 2 * M.s;
-    const long long out_rs = (M.mode == MAP_TOUT || M.mode == MAP_TOUT1) ? 2 * M.Np : 2 * M.s;
-    const long long ntiles = M.ntiles;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wr = warp & 1, wc = warp >> 1;
-    for (int e = tid; e < kpad * BM; e += kThreads) {
-        const int j = e / BM, r = e - j * BM;
-        As[j * BMP + r] = (j < n && r < n) ? __ldg(At + (long long)j * n + r) : 0.0;
-    }
-    const int lcp = tid & 63, lrow0 = tid >> 6;
-    auto issue = [&](long long tile, int buf) {
-        if (tile < ntiles) {
-            long long in_off, dummy;
-            const bool cv = colmap(M, n, tile_base(M, tile), lcp, in_off, dummy);
-            double* bs = Bs + (size_t)buf * KMAX * BNP;
-            const double* src = X + in_off;
-            for (int j = lrow0; j < kpad; j += 4) {
-                const bool v = cv && j < n;
-                cp_async16(bs + j * BNP + 2 * lcp, v ? (const void*)(src + (long long)j * in_rs) : (const void*)X, v);
-            }
-        }
-        cp_async_commit();
-    };
-    const int r_warp = wr * (BM / 2), c_warp = wc * 32;
-    const int ar = lane >> 2, ak = lane & 3, cr = lane >> 2;
-    long long tile = blockIdx.x;
-    int buf = 0;
-    issue(tile, 0);
-    for (; tile < ntiles; tile += gridDim.x, buf ^= 1) {
-        issue(tile + gridDim.x, buf ^ 1);
-        cp_async_wait<1>();
-        __syncthreads();
-        double acc[MT][4][2];
-#pragma unroll
-        for (int i = 0; i < MT; ++i)
-#pragma unroll
-            for (int m = 0; m < 4; ++m) acc[i][m][0] = acc[i][m][1] = 0.0;
-        const double* bs = Bs + (size_t)buf * KMAX * BNP;
-#pragma unroll 4
-        for (int k4 = 0; k4 < kpad; k4 += 4) {
-            double a[MT], b[4];
-#pragma unroll
-            for (int i = 0; i < MT; ++i) a[i] = As[(k4 + ak) * BMP + r_warp + i * 8 + ar];
-#pragma unroll
-            for (int m = 0; m < 4; ++m) b[m] = bs[(k4 + ak) * BNP + c_warp + m * 8 + ar];
-#pragma unroll
-            for (int i = 0; i < MT; ++i)
-#pragma unroll
-                for (int m = 0; m < 4; ++m) dmma_m8n8k4(acc[i][m][0], acc[i][m][1], a[i], b[m]);
-        }
-        const TileBase tb = tile_base(M, tile);
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-            const int jcol = (c_warp >> 1) + m * 4 + (lane & 3);
-            long long io, oo;
-            if (colmap(M, n, tb, jcol, io, oo)) {
-                double* yb = Y + oo;
-#pragma unroll
-                for (int i = 0; i < MT; ++i) {
-                    const int r = r_warp + i * 8 + cr;
-                    if (r < n)
-                        *reinterpret_cast<double2*>(yb + (long long)r * out_rs) =
-                            make_double2(acc[i][m][0], acc[i][m][1]);
-                }
-            }
-        }
-        __syncthreads(); // the next iteration's issue overwrites this buffer
-    }
-    cp_async_wait<0>();
-}
-
-int engine_choice() {
-    static int e = [] {
-        const char* v = std::getenv("KS_GEMM");
-        if (v && std::strcmp(v, "dfma") == 0) return 0;
-        if (v && std::strcmp(v, "dmma1") == 0) return 1;
-        return 2; // default: DMMA v2 (profiles/ for the measurement)
-    }();
-    return e;
-}
-
-template <int TM>
-void launch_tm(int engine, const double* At, int n, const double* X, double* Y, long long W2,
-               long long C, cudaStream_t st, const ColMap* map) {
-    const unsigned grid = (unsigned)((C + kBN - 1) / kBN);
-    if (engine == 0) {
-        const size_t sm = (size_t)2 * kBK * (16 * TM + 2 + kBN) * sizeof(double);
-        static bool attr = false;
-        if (!attr) {
-            KS_CUDA(cudaFuncSetAttribute(k_mode_gemm_dfma<TM>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            attr = true;
-        }
-        k_mode_gemm_dfma<TM><<<grid, kThreads, sm, st>>>(At, n, X, Y, W2, C);
-        check_launch("k_mode_gemm_dfma");
-    } else if (engine == 2 && TM <= 5 && std::getenv("KS_GEMM_V3")) {
-        // opt-in: measured slower than v2 at c3 (193-265 us vs 189-241 us per launch)
-        constexpr int BM = 16 * TM;
-        const size_t sm = ((size_t)BM * (BM + 4) + (size_t)2 * BM * (kBN + 4)) * sizeof(double);
-        static int sms = 0;
-        if (!sms) {
-            int dev = 0;
-            KS_CUDA(cudaGetDevice(&dev));
-            KS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-            KS_CUDA(cudaFuncSetAttribute(k_mode_gemm_dmma3<TM>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        }
-        ColMap Mm = *map;
-        const unsigned g3 = (unsigned)std::min<long long>(Mm.ntiles, (long long)sms);
-        k_mode_gemm_dmma3<TM><<<g3, kThreads, sm, st>>>(At, n, X, Y, Mm);
-        check_launch("k_mode_gemm_dmma3");
-    } else if (engine == 2) {
-        const int nk = (n + kBK - 1) / kBK;
-        const size_t sm_a = (size_t)nk * kBK * (16 * TM + 4) * sizeof(double);
-        const size_t sm_s = (size_t)kBK * (kBN + 4) * sizeof(double);
-        // long axes (resident A large): fall back to a 2-stage ring
-        const bool two = sm_a + kStages * sm_s > 227 * 1024;
-        const size_t sm = sm_a + (two ? 2 : kStages) * sm_s;
-        static int sms = 0;
-        if (!sms) {
-            int dev = 0;
-            KS_CUDA(cudaGetDevice(&dev));
-            KS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-            KS_CUDA(cudaFuncSetAttribute(k_mode_gemm_dmma2<TM>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-            KS_CUDA(cudaFuncSetAttribute(k_mode_gemm_dmma2<TM, 2>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        }
-        KS_REQUIRE(sm <= 227 * 1024, KS_EINVAL, "mode product: axis too long for the resident-A kernel");
-        const int per_sm = (TM <= 5 && 2 * sm <= 227 * 1024) ? 2 : 1;
-        ColMap M = *map;
-        const unsigned g2 = (unsigned)std::min<long long>(M.ntiles, (long long)sms * per_sm);
-        if (M.rin || M.rout) { // peer-memory rows (sharded middle phase)
-            static bool attr_r = false;
-            if (!attr_r) {
-                KS_CUDA(cudaFuncSetAttribute(k_mode_gemm_dmma2<TM, 2, true>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-                KS_CUDA(cudaFuncSetAttribute(k_mode_gemm_dmma2<TM, kStages, true>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-                attr_r = true;
-            }
-            if (two) k_mode_gemm_dmma2<TM, 2, true><<<g2, kThreads, sm, st>>>(At, n, X, Y, M);
-            else k_mode_gemm_dmma2<TM, kStages, true><<<g2, kThreads, sm, st>>>(At, n, X, Y, M);
-        } else if (two) {
-            k_mode_gemm_dmma2<TM, 2><<<g2, kThreads, sm, st>>>(At, n, X, Y, M);
+    const size_t sm_a = (size_t)nk * kBK * (16 * TM + 4) * sizeof(double);
+    const size_t sm_s = (size_t)kBK * (kBN + 4) * sizeof(double);
+    // long axes (resident A large): fall back to a 2-stage ring
+    const bool two = sm_a + kStages * sm_s > 227 * 1024;
+    const size_t sm = sm_a + (two ? 2 : kStages) * sm_s;
+    KS_REQUIRE(sm <= 227 * 1024, KS_EINVAL, "mode product: axis too long for the resident-A kernel");
+    const int per_sm = (TM <= 5 && 2 * sm <= 227 * 1024) ? 2 : 1;
+    ColMap M = *map;
+    const unsigned g2 = (unsigned)std::min<long long>(M.ntiles, (long long)device_sms() * per_sm);
+    if (M.rin || M.rout) { // peer-memory rows (sharded middle phase)
+        if (two) {
+            smem_optin((const void*)k_mode_gemm_dmma2<TM, 2, true>, (int)sm);
+            k_mode_gemm_dmma2<TM, 2, true><<<g2, kThreads, sm, st>>>(At, n, X, Y, M);
         } else {
-            k_mode_gemm_dmma2<TM><<<g2, kThreads, sm, st>>>(At, n, X, Y, M);
+            smem_optin((const void*)k_mode_gemm_dmma2<TM, kStages, true>, (int)sm);
+            k_mode_gemm_dmma2<TM, kStages, true><<<g2, kThreads, sm, st>>>(At, n, X, Y, M);
         }
-        check_launch("k_mode_gemm_dmma2");
+    } else if (two) {
+        smem_optin((const void*)k_mode_gemm_dmma2<TM, 2>, (int)sm);
+        k_mode_gemm_dmma2<TM, 2><<<g2, kThreads, sm, st>>>(At, n, X, Y, M);
     } else {
-        const size_t sm = (size_t)2 * kBK * (16 * TM + 4 + kBN + 4) * sizeof(double);
-        static bool attr = false;
-        if (!attr) {
-            KS_CUDA(cudaFuncSetAttribute(k_mode_gemm_dmma<TM>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            attr = true;
-        }
-        k_mode_gemm_dmma<TM><<<grid, kThreads, sm, st>>>(At, n, X, Y, W2, C);
-        check_launch("k_mode_gemm_dmma");
+        smem_optin((const void*)k_mode_gemm_dmma2<TM>, (int)sm);
+        k_mode_gemm_dmma2<TM><<<g2, kThreads, sm, st>>>(At, n, X, Y, M);
     }
-}
-
-// TMA bulk copies (cp.async.bulk) completing on an mbarrier
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned cnt) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* b, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
-    unsigned ok = 0;
-    do {
-        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-                     : "=r"(ok)
-                     : "r"(smem_u32(b)), "r"(parity)
-                     : "memory");
-    } while (!ok);
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
+    check_launch("k_mode_gemm_dmma2");
 }
 
 // ---------------------------------------------------------------------------
@@ -761,12 +339,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 // ---------------------------------------------------------------------------
 // RL: loader lanes along rows instead of columns (MAP_TIN1: a column's rows
 // are contiguous on the time-major side, so a warp reads 2 x 256 B runs)
-// DOT: also reduce Re <M.dx, Y> over the written output (PCG: rho = Re <r, P r>)
-template <int TH, bool INV, int KC, int STG, int MINB, int BNC, bool TMA, bool ROWS = false, bool RL = false,
-          bool DOT = false>
+template <int TH, bool INV, int KC, int STG, int MINB, int BNC, bool ROWS = false, bool RL = false>
 __global__ void __launch_bounds__(kThreads, MINB)
 k_mode_gemm_fold(const double* __restrict__ Af, int Kst, const int* __restrict__ rmap, int n, int hc, int nkc,
-                 const double* __restrict__ X, double* __restrict__ Y, ColMap M, int dry) {
+                 const double* __restrict__ X, double* __restrict__ Y, ColMap M) {
     constexpr int H = 16 * TH;
     constexpr int MT = TH; // 8-row blocks per warp per GEMM (H/2 half-rows per warp)
     constexpr int BMP = H + 4;
@@ -790,8 +366,6 @@ k_mode_gemm_fold(const double* __restrict__ Af, int Kst, const int* __restrict__
     double* Bs = Ao + (size_t)Kp * BMP;       // [STG][SR][BNP]
     int* rE = reinterpret_cast<int*>(Bs + (size_t)STG * STAGE_D); // [H] even eigen-indices
     int* rO = rE + H;                                               // [H] odd eigen-indices
-    // TMA: one mbarrier per stage (8 B aligned: rE/rO hold 2H ints)
-    unsigned long long* bar = reinterpret_cast<unsigned long long*>(rO + H);
     const int no = n - hc;
     const long long in_rs = (M.mode == MAP_TIN || M.mode == MAP_TIN1) ? 2 * M.Np : 2 * M.s;
     const long long out_rs = (M.mode == MAP_TOUT || M.mode == MAP_TOUT1) ? 2 * M.Np : 2 * M.s;
@@ -806,14 +380,6 @@ k_mode_gemm_fold(const double* __restrict__ Af, int Kst, const int* __restrict__
         Ao[k * BMP + r] = v ? __ldg(Af + (size_t)Kst * H + e) : 0.0;
     }
     for (int e = tid; e < 2 * H; e += kThreads) rE[e] = __ldg(rmap + e);
-    if (TMA) {
-        // rows that are never loaded (past hc / n-hc) must hold finite values
-        for (int e = tid; e < STG * SR * BNP; e += kThreads) Bs[e] = 0.0;
-        if (tid == 0) {
-            for (int q = 0; q < STG; ++q) mbar_init(bar + q, 1);
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        }
-    }
     __syncthreads();
 
     const int lcp = tid % BNC, lrow0 = tid / BNC;
@@ -823,48 +389,11 @@ k_mode_gemm_fold(const double* __restrict__ Af, int Kst, const int* __restrict__
     long long cur_tile = -1, cur_in = 0;
     bool cur_valid = false;
 
-    auto issue_tma = [&](int w) {
-        if (warp != 0 || w >= nwork) return;
-        const int wt = w / nkc;
-        const long long tile = (long long)blockIdx.x + (long long)wt * gridDim.x;
-        const int kc = w - wt * nkc;
-        const TileBase tb = tile_base(M, tile);
-        const long long ncol = M.Q - tb.q0 < BNC ? M.Q - tb.q0 : BNC;
-        const long long seg1 = M.s - tb.r0 < ncol ? M.s - tb.r0 : ncol;
-        const int jj = lane;
-        const int q = kc * KC + (jj % KC);
-        int src = 0;
-        bool v = jj < SR;
-        if (!INV) {
-            src = jj < KC ? q : n - 1 - q;
-            v = v && (jj < KC ? q < hc : q < n - hc);
-        } else {
-            v = v && (jj < KC ? q < hc : q < no);
-            if (v) src = jj < KC ? rE[q] : rO[q];
-        }
-        const unsigned mine = v ? (unsigned)(ncol * 16) : 0u;
-        const unsigned total = __reduce_add_sync(0xffffffffu, mine);
-        unsigned long long* b = bar + (w % STG);
-        if (lane == 0) mbar_arrive_tx(b, total);
-        __syncwarp();
-        if (v) {
-            double* dst = Bs + (size_t)(w % STG) * SR * BNP + jj * BNP;
-            const double* g = X + 2 * (tb.o0 * (long long)n * M.s + (long long)src * M.s + tb.r0);
-            bulk_g2s(dst, g, (unsigned)(seg1 * 16), b);
-            if (ncol > seg1)
-                bulk_g2s(dst + 2 * seg1, X + 2 * ((tb.o0 + 1) * (long long)n * M.s + (long long)src * M.s),
-                         (unsigned)((ncol - seg1) * 16), b);
-        }
-    };
     // RL loader state: the thread's row and the column offsets of its NPASS columns
     constexpr int CPP = kThreads / SR, NPASS = RL ? BNC / CPP : 1;
     long long rl_in[NPASS];
     unsigned rl_valid = 0;
     auto issue = [&](int w) {
-        if (TMA) {
-            issue_tma(w);
-            return;
-        }
         if (RL) {
             if (w < nwork) {
                 const int wt = w / nkc;
@@ -894,7 +423,7 @@ k_mode_gemm_fold(const double* __restrict__ Af, int Kst, const int* __restrict__
                 }
 #pragma unroll
                 for (int c = 0; c < NPASS; ++c) {
-                    const bool vc = v && ((rl_valid >> c) & 1u) && dry != 3;
+                    const bool vc = v && ((rl_valid >> c) & 1u);
                     const int col = tid / SR + CPP * c;
                     cp_async16(bs + 2 * (col * SRP + jj), vc ? (const void*)in_row<ROWS>(M, X, rl_in[c], src, in_rs) : (const void*)X,
                                vc);
@@ -926,7 +455,7 @@ k_mode_gemm_fold(const double* __restrict__ Af, int Kst, const int* __restrict__
                     v = jj < KC ? q < hc : q < no;
                     src = v ? (jj < KC ? rE[q] : rO[q]) : 0;
                 }
-                v = v && cur_valid && dry != 3;
+                v = v && cur_valid;
                 cp_async16(bs + jj * BNP + 2 * lcp, v ? (const void*)in_row<ROWS>(M, X, cur_in, src, in_rs) : (const void*)X,
                            v);
             }
@@ -935,7 +464,6 @@ k_mode_gemm_fold(const double* __restrict__ Af, int Kst, const int* __restrict__
     };
 
     double acc[2][MT][NF][2];
-    double dacc = 0.0; // DOT: this thread's share of Re <x, Y>
 #pragma unroll
     for (int g = 0; g < 2; ++g)
 #pragma unroll
@@ -950,13 +478,11 @@ k_mode_gemm_fold(const double* __restrict__ Af, int Kst, const int* __restrict__
     const int ar = lane >> 2, ak = lane & 3;
     const int cr = lane >> 2;
     for (int w = 0; w < nwork; ++w) {
-        if (TMA) mbar_wait(bar + (w % STG), (unsigned)((w / STG) & 1));
-        else cp_async_wait<STG - 2>();
+        cp_async_wait<STG - 2>();
         __syncthreads();
         issue(w + STG - 1);
         const int kc = w % nkc;
         const double* bs = Bs + (size_t)(w % STG) * STAGE_D;
-        if (!dry)
 #pragma unroll
         for (int k4 = 0; k4 < KC; k4 += 4) {
             const int kr = kc * KC + k4 + ak;
@@ -982,7 +508,7 @@ k_mode_gemm_fold(const double* __restrict__ Af, int Kst, const int* __restrict__
                     dmma_m8n8k4(acc[1][i][m][0], acc[1][i][m][1], ao[i], bo[m]);
                 }
         }
-        if (kc == nkc - 1 && dry != 2) {
+        if (kc == nkc - 1) {
             const long long tile = (long long)blockIdx.x + (long long)(w / nkc) * gridDim.x;
             const TileBase tbase = tile_base(M, tile);
 #pragma unroll
@@ -1001,19 +527,9 @@ k_mode_gemm_fold(const double* __restrict__ Af, int Kst, const int* __restrict__
                         } else if (h < hc) {
                             const double2 v1 = make_double2(e.x + o.x, e.y + o.y);
                             __stcs(reinterpret_cast<double2*>(out_row<ROWS>(M, Y, oo, h, out_rs)), v1);
-                            if (DOT) {
-                                const double2 x1 = __ldg(reinterpret_cast<const double2*>(
-                                    out_row<false>(M, const_cast<double*>(M.dx), oo, h, out_rs)));
-                                dacc = fma(x1.x, v1.x, fma(x1.y, v1.y, dacc));
-                            }
                             if (n - 1 - h != h) {
                                 const double2 v2 = make_double2(e.x - o.x, e.y - o.y);
                                 __stcs(reinterpret_cast<double2*>(out_row<ROWS>(M, Y, oo, n - 1 - h, out_rs)), v2);
-                                if (DOT) {
-                                    const double2 x2 = __ldg(reinterpret_cast<const double2*>(
-                                        out_row<false>(M, const_cast<double*>(M.dx), oo, n - 1 - h, out_rs)));
-                                    dacc = fma(x2.x, v2.x, fma(x2.y, v2.y, dacc));
-                                }
                             }
                         }
                     }
@@ -1025,37 +541,6 @@ k_mode_gemm_fold(const double* __restrict__ Af, int Kst, const int* __restrict__
         }
     }
     cp_async_wait<0>();
-    if (DOT) { // fixed tree per CTA, then the last CTA sums the partials in block order
-        __shared__ double red[kThreads / 32];
-        __shared__ bool last;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) dacc += __shfl_down_sync(0xffffffffu, dacc, o);
-        if (lane == 0) red[warp] = dacc;
-        __syncthreads();
-        if (tid == 0) {
-            double sum = 0.0;
-            for (int q = 0; q < kThreads / 32; ++q) sum += red[q];
-            M.dpart[blockIdx.x] = sum;
-            __threadfence();
-            last = atomicAdd(M.dcnt, 1u) == gridDim.x - 1;
-        }
-        __syncthreads();
-        if (last && tid == 0) {
-            __threadfence();
-            double sum = 0.0;
-            for (unsigned q = 0; q < gridDim.x; ++q) sum += ((volatile double*)M.dpart)[q];
-            M.dres[0] = sum;
-            M.dres[1] = 0.0;
-            *M.dcnt = 0u;
-        }
-    }
-}
-
-// fold kernel configuration: pair rows per stage (KC), ring stages, CTAs per SM
-// KS_FOLD_DRY=1: skip the MMAs (memory-pipeline ceiling experiment; wrong results)
-int dry_run() {
-    static const int d = std::getenv("KS_FOLD_DRY") ? std::atoi(std::getenv("KS_FOLD_DRY")) : 0;
-    return d;
 }
 
 // tile width (complex columns) of a column map; T modes block it as tbt x tbr
@@ -1065,79 +550,46 @@ void set_tile_width(ColMap& M, int tw) {
         M.ntiles = (M.Q + tw - 1) / tw;
     } else {
         M.tbr = M.Np >= 8 ? 8 : (M.Np >= 4 ? 4 : (M.Np >= 2 ? 2 : 1));
-        // experiment hook: spatial block width of a time-major tile (tbt * tbr = tw)
-        static const int tbr_env = std::getenv("KS_FD_TBR") ? std::atoi(std::getenv("KS_FD_TBR")) : 0;
-        if (tbr_env > 0 && tw % tbr_env == 0 && M.Np >= tbr_env) M.tbr = tbr_env;
         M.tbt = tw / M.tbr;
         M.ntb = (M.nt + M.tbt - 1) / M.tbt;
         M.ntiles = M.ntb * ((M.Np + M.tbr - 1) / M.tbr);
     }
 }
 
-template <int TH, bool INV, int KC, int STG, int MINB, int BNC, bool TMA = false>
+template <int TH, bool INV, int KC, int STG, int MINB, int BNC>
 void launch_fold_cfg(const FoldAxis& F, const double* X, double* Y, ColMap M, cudaStream_t st) {
     constexpr int H = 16 * TH;
     const int nkc = (F.hc + KC - 1) / KC;
     const bool rl = M.mode == MAP_TIN1 && !M.rin && !M.rout; // column-major stages (row-lane loader)
     const size_t stage_d = rl ? (size_t)BNC * (2 * KC + 4) * 2 : (size_t)2 * KC * (2 * BNC + 4);
     const size_t sm = (size_t)2 * nkc * KC * (H + 4) * sizeof(double) + (size_t)2 * H * sizeof(int) +
-                      (size_t)STG * stage_d * sizeof(double) + (size_t)STG * 8;
+                      (size_t)STG * stage_d * sizeof(double);
     KS_REQUIRE(sm <= 227 * 1024, KS_EINVAL, "folded mode product: axis too long");
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        KS_CUDA(cudaGetDevice(&dev));
-        KS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        KS_CUDA(cudaFuncSetAttribute(k_mode_gemm_fold<TH, INV, KC, STG, MINB, BNC, TMA>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    }
     set_tile_width(M, BNC);
     const int per_sm = std::max(1, std::min(MINB, (int)((227 * 1024) / sm)));
-    const unsigned g = (unsigned)std::min<long long>(M.ntiles, (long long)sms * per_sm);
+    const unsigned g = (unsigned)std::min<long long>(M.ntiles, (long long)device_sms() * per_sm);
     const double* A = (INV ? F.inv : F.fwd).as<double>();
     if (M.rin || M.rout) { // peer-memory rows (sharded middle phase)
-        static bool attr_r = false;
-        if (!attr_r) {
-            KS_CUDA(cudaFuncSetAttribute(k_mode_gemm_fold<TH, INV, KC, STG, MINB, BNC, false, true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-            attr_r = true;
-        }
-        k_mode_gemm_fold<TH, INV, KC, STG, MINB, BNC, false, true><<<g, kThreads, sm, st>>>(
-            A, F.kst, F.rmap.as<int>(), F.n, F.hc, nkc, X, Y, M, 0);
+        auto k = k_mode_gemm_fold<TH, INV, KC, STG, MINB, BNC, true>;
+        smem_optin((const void*)k, (int)sm);
+        k<<<g, kThreads, sm, st>>>(A, F.kst, F.rmap.as<int>(), F.n, F.hc, nkc, X, Y, M);
     } else if (M.mode == MAP_TIN1 || M.mode == MAP_TOUT1) {
         // axis-1 time-major side: rows are stored by position (even eigen-indices
         // first, then odd), so the time-major row map is the position map
         const int* rm = F.rpos.as<int>();
         if (M.mode == MAP_TIN1) {
-            static bool attr_l = false;
-            if (!attr_l) {
-                KS_CUDA(cudaFuncSetAttribute(k_mode_gemm_fold<TH, INV, KC, STG, MINB, BNC, false, false, true>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-                attr_l = true;
-            }
-            k_mode_gemm_fold<TH, INV, KC, STG, MINB, BNC, false, false, true><<<g, kThreads, sm, st>>>(
-                A, F.kst, rm, F.n, F.hc, nkc, X, Y, M, dry_run());
+            auto k = k_mode_gemm_fold<TH, INV, KC, STG, MINB, BNC, false, true>;
+            smem_optin((const void*)k, (int)sm);
+            k<<<g, kThreads, sm, st>>>(A, F.kst, rm, F.n, F.hc, nkc, X, Y, M);
         } else {
-            k_mode_gemm_fold<TH, INV, KC, STG, MINB, BNC, false><<<g, kThreads, sm, st>>>(A, F.kst, rm, F.n, F.hc,
-                                                                                          nkc, X, Y, M, dry_run());
-        }
-    } else if (M.dx) {
-        if constexpr (INV) {
-            static bool attr_d = false;
-            if (!attr_d) {
-                // (the DOT variant has ~80 B of static shared memory)
-                KS_CUDA(cudaFuncSetAttribute(k_mode_gemm_fold<TH, INV, KC, STG, MINB, BNC, false, false, false, true>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
-                attr_d = true;
-            }
-            k_mode_gemm_fold<TH, INV, KC, STG, MINB, BNC, false, false, false, true><<<g, kThreads, sm, st>>>(
-                A, F.kst, F.rmap.as<int>(), F.n, F.hc, nkc, X, Y, M, dry_run());
-        } else {
-            throw Error(KS_EINVAL, "fused dot: inverse transforms only");
+            auto k = k_mode_gemm_fold<TH, INV, KC, STG, MINB, BNC>;
+            smem_optin((const void*)k, (int)sm);
+            k<<<g, kThreads, sm, st>>>(A, F.kst, rm, F.n, F.hc, nkc, X, Y, M);
         }
     } else {
-        k_mode_gemm_fold<TH, INV, KC, STG, MINB, BNC, TMA><<<g, kThreads, sm, st>>>(A, F.kst, F.rmap.as<int>(), F.n,
-                                                                                    F.hc, nkc, X, Y, M, dry_run());
+        auto k = k_mode_gemm_fold<TH, INV, KC, STG, MINB, BNC>;
+        smem_optin((const void*)k, (int)sm);
+        k<<<g, kThreads, sm, st>>>(A, F.kst, F.rmap.as<int>(), F.n, F.hc, nkc, X, Y, M);
     }
     check_launch("k_mode_gemm_fold");
 }
@@ -1145,45 +597,24 @@ void launch_fold_cfg(const FoldAxis& F, const double* X, double* Y, ColMap M, cu
 template <int TH, bool INV>
 void launch_fold_th(const FoldAxis& F, const double* X, double* Y, const ColMap& M, cudaStream_t st) {
     if (TH <= 2) {
-        // Variants measured at c3 (n = 64, six transforms per FD apply; profiles/round1_part2_summary.md):
-        //   (KC 16, 2 stages, 2 CTA/SM, 64-column tiles)  0.847-0.864 ms   <- default
+        // Variants measured at c3 (n = 64, six transforms per FD apply;
+        // profiles/round1_part2_summary.md, round1_part5_summary.md):
+        //   (KC 16, 2 stages, 2 CTA/SM, 64-column tiles)  0.847-0.864 ms   <- kept
         //   (KC  8, 4 stages, 2 CTA/SM)                   0.895 ms
-        //   32-column tiles, 3 CTA/SM (80 regs)           0.867 ms
+        //   32-column tiles, 3-4 stages, 2-3 CTA/SM       0.867 ms
         //   1 CTA/SM, 3-4 stages                          1.08 ms
         //   smem-staged row-wise stores                   0.98-1.06 ms
-        //   TMA bulk row loads + mbarrier (KS_FOLD_TMA=1) 0.862 ms
-        // and without the MMAs (KS_FOLD_DRY=1) the same data movement takes 0.713 ms:
-        // the kernel is bound by its memory pipeline (loads alone 4.0, stores alone 3.3 TB/s).
-        static const bool tma = [] {
-            const char* e = std::getenv("KS_FOLD_TMA");
-            return e && std::strcmp(e, "0") != 0;
-        }();
-        if (tma && M.mode == MAP_STD && M.s >= 64 && !M.rin && !M.rout)
-            return launch_fold_cfg<TH, INV, 16, 2, 2, 64, true>(F, X, Y, M, st);
-        // experiment hook (KS_FOLD_CFG): 1 = 32-column tiles, 4 stages, 2 CTA/SM;
-        // 2 = 32-column tiles, 3 stages, 3 CTA/SM. Measured c3 (part 5): six
-        // transforms 0.808 / 0.817 ms vs 0.770 ms for the default.
-        static const int cfg = std::getenv("KS_FOLD_CFG") ? std::atoi(std::getenv("KS_FOLD_CFG")) : 0;
-        if (cfg == 1) return launch_fold_cfg<TH, INV, 16, 4, 2, 32>(F, X, Y, M, st);
-        if (cfg == 2) return launch_fold_cfg<TH, INV, 16, 3, 3, 32>(F, X, Y, M, st);
+        //   TMA bulk row loads + mbarrier                 0.862 ms
         return launch_fold_cfg<TH, INV, 16, 2, 2, 64>(F, X, Y, M, st);
     }
     // small problems (c1, c2: fewer 64-column tiles than SMs): 32-column tiles
     // give twice the CTAs
-    {
-        static int sms = 0;
-        if (!sms) {
-            int dev = 0;
-            KS_CUDA(cudaGetDevice(&dev));
-            KS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        }
-        if (M.mode == MAP_STD && !M.rin && !M.rout && (M.Q + 63) / 64 < sms) {
-            constexpr int Hs = 16 * TH;
-            const int nkc8 = (F.hc + 7) / 8;
-            const size_t sm32 = (size_t)2 * nkc8 * 8 * (Hs + 4) * sizeof(double) + (size_t)2 * Hs * sizeof(int) +
-                                (size_t)4 * 16 * (64 + 4) * sizeof(double);
-            if (sm32 <= 227 * 1024) return launch_fold_cfg<TH, INV, 8, 4, 1, 32>(F, X, Y, M, st);
-        }
+    if (M.mode == MAP_STD && !M.rin && !M.rout && (M.Q + 63) / 64 < device_sms()) {
+        constexpr int Hs = 16 * TH;
+        const int nkc8 = (F.hc + 7) / 8;
+        const size_t sm32 = (size_t)2 * nkc8 * 8 * (Hs + 4) * sizeof(double) + (size_t)2 * Hs * sizeof(int) +
+                            (size_t)4 * 16 * (64 + 4) * sizeof(double);
+        if (sm32 <= 227 * 1024) return launch_fold_cfg<TH, INV, 8, 4, 1, 32>(F, X, Y, M, st);
     }
     // long axes: resident halves are large -> 1 CTA/SM; 2 stages when 4 do not fit
     constexpr int H = 16 * TH;
@@ -1359,19 +790,11 @@ bool fold_axis_build(const double* U_in, const double* lam, int n, double tol, F
 
 void launch_mode_gemm_fold(const FoldAxis& F, bool inverse, const double* X, double* Y, size_t s_complex,
                            size_t outer, cudaStream_t st, int layout, int nt, const double* const* rows_in,
-                           double* const* rows_out, const double* dot_x, Reducer* dot) {
+                           double* const* rows_out) {
     if (s_complex == 0 || outer == 0) return;
     ColMap M = make_colmap(F.n, s_complex, outer, layout, nt);
     M.rin = rows_in;
     M.rout = rows_out;
-    if (dot) {
-        KS_REQUIRE(inverse && layout == MAP_STD && !rows_in && !rows_out && dot_x, KS_EINVAL,
-                   "fused dot: plain inverse transform only");
-        M.dx = dot_x;
-        M.dpart = dot->partial.as<double>();
-        M.dcnt = dot->counter.as<unsigned>();
-        M.dres = dot->result.as<double>();
-    }
 #define KS_FOLD_CASE(T)                                                                            \
     case T:                                                                                        \
         if (inverse) launch_fold_th<T, true>(F, X, Y, M, st);                                      \
@@ -1388,7 +811,7 @@ void launch_mode_gemm_fold(const FoldAxis& F, bool inverse, const double* X, dou
 #undef KS_FOLD_CASE
 }
 
-int transform_engine() { return engine_choice(); }
+int transform_engine() { return 2; } // DMMA (the only engine)
 
 void launch_mode_gemm(const double* At, int n, const double* X, double* Y, size_t s_complex,
                       size_t outer, cudaStream_t st, int layout, int nt, const double* const* rows_in,
@@ -1396,12 +819,9 @@ void launch_mode_gemm(const double* At, int n, const double* X, double* Y, size_
     const long long W2 = 2 * (long long)s_complex;
     const long long C = W2 * (long long)outer;
     if (C == 0 || n == 0) return;
-    int eng = engine_choice();
-    if (layout != MAP_STD || rows_in || rows_out) {
+    if (layout != MAP_STD || rows_in || rows_out)
         KS_REQUIRE(layout == MAP_STD || (outer == 1 && nt > 0 && s_complex % (size_t)nt == 0), KS_EINVAL,
                    "time-major transform needs the outermost axis");
-        eng = 2; // only the v2 engine implements the time-major maps and row tables
-    }
     ColMap M{};
     M.rin = rows_in;
     M.rout = rows_out;
@@ -1422,16 +842,16 @@ void launch_mode_gemm(const double* At, int n, const double* X, double* Y, size_
     const int tm = (n + 15) / 16;
     KS_REQUIRE(tm <= 10, KS_EINVAL, "mode product: axis length > 160 not supported");
     switch (tm) {
-    case 1: launch_tm<1>(eng, At, n, X, Y, W2, C, st, &M); break;
-    case 2: launch_tm<2>(eng, At, n, X, Y, W2, C, st, &M); break;
-    case 3: launch_tm<3>(eng, At, n, X, Y, W2, C, st, &M); break;
-    case 4: launch_tm<4>(eng, At, n, X, Y, W2, C, st, &M); break;
-    case 5: launch_tm<5>(eng, At, n, X, Y, W2, C, st, &M); break;
-    case 6: launch_tm<6>(eng, At, n, X, Y, W2, C, st, &M); break;
-    case 7: launch_tm<7>(eng, At, n, X, Y, W2, C, st, &M); break;
-    case 8: launch_tm<8>(eng, At, n, X, Y, W2, C, st, &M); break;
-    case 9: launch_tm<9>(eng, At, n, X, Y, W2, C, st, &M); break;
-    case 10: launch_tm<10>(eng, At, n, X, Y, W2, C, st, &M); break;
+    case 1: launch_tm<1>(At, n, X, Y, st, &M); break;
+    case 2: launch_tm<2>(At, n, X, Y, st, &M); break;
+    case 3: launch_tm<3>(At, n, X, Y, st, &M); break;
+    case 4: launch_tm<4>(At, n, X, Y, st, &M); break;
+    case 5: launch_tm<5>(At, n, X, Y, st, &M); break;
+    case 6: launch_tm<6>(At, n, X, Y, st, &M); break;
+    case 7: launch_tm<7>(At, n, X, Y, st, &M); break;
+    case 8: launch_tm<8>(At, n, X, Y, st, &M); break;
+    case 9: launch_tm<9>(At, n, X, Y, st, &M); break;
+    case 10: launch_tm<10>(At, n, X, Y, st, &M); break;
     }
 }
 

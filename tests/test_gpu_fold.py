@@ -104,64 +104,36 @@ def test_folded_high_degree(gpu, oracle, d, p, n_el, n_el_t):
     assert rel(za, zao) <= TOL and maxrel(za, zao) <= TOL
 
 
-# axes 1 and 2 of length 32 / 48 / 64 run through the fused slab kernel
-# (csrc/ks_fold12.cu, opt-in KS_FD_FUSE12=1): one pass for two folded mode products
-@pytest.mark.parametrize("d,p,n_el,n_el_t", [(3, 2, 32, 5), (3, 2, 48, 3), (3, 2, 64, 2)])
-def test_fused_axes12_matches_oracle(gpu, oracle, d, p, n_el, n_el_t, monkeypatch):
-    monkeypatch.setenv("KS_FD_FUSE12", "1")
-    a, g, o = _pair(gpu, oracle, d, p, n_el, n_el_t)
-    assert g.info()["fused_axes_12"]
-    r = oracle.random_vec(o.N, 41)
+@pytest.mark.parametrize("d,p,n_el,n_el_t", [(3, 2, 16, 8), (3, 3, 13, 5), (3, 4, 11, 4)])
+def test_axis1_time_major_handoff(gpu, oracle, d, p, n_el, n_el_t):
+    """Pair mode hands the time-major layout over on axis 1 (forward axes d..1,
+    rows stored by even/odd position, blocks numbered by position): forward
+    and adjoint match the oracle, and ks_fd_block still answers by natural
+    fiber index (the reference's LU of that fiber's block)."""
+    a, g1, o = _pair(gpu, oracle, d, p, n_el, n_el_t)
+    assert g1.info()["time_major_axis"] == 1
+    r = oracle.random_vec(o.N, 17)
+    for ap in ("apply", "apply_adjoint"):
+        z1, zo = getattr(g1, ap)(r), getattr(o, ap)(r)
+        assert rel(z1, zo) <= TOL and maxrel(z1, zo) <= TOL
+    n1 = a["dims"][1]
+    for i in (0, 1, n1 - 1, n1 + 3, o.N // a["dims"][0] - 1):
+        ab, piv = g1.block(i, p)
+        abo, pivo = o.block(i)
+        assert np.array_equal(piv, pivo) and maxrel(ab, abo) < 1e-12
+
+
+@pytest.mark.parametrize("d,p,n_el,n_el_t", [(3, 2, 16, 8), (3, 4, 11, 4), (2, 3, 16, 8), (2, 2, 12, 6),
+                                            (1, 3, 16, 16), (3, 6, 6, 5)])
+def test_ldl_blocks_match_reference_lu(gpu, oracle, d, p, n_el, n_el_t):
+    """Least-squares blocks are HPD and factored as L D L^H without pivoting:
+    the applications match the oracle's partial-pivot LU (the reference's
+    factor_banded) at the north_star tolerance, forward and adjoint (H^H = H,
+    one solve serves both)."""
+    _, g, o = _pair(gpu, oracle, d, p, n_el, n_el_t)
+    assert g.info()["no_pivot_solve"]
+    r = oracle.random_vec(o.N, 29)
     z, zo = g.apply(r), o.apply(r)
     assert rel(z, zo) <= TOL and maxrel(z, zo) <= TOL
     za, zao = g.apply_adjoint(r), o.apply_adjoint(r)
     assert rel(za, zao) <= TOL and maxrel(za, zao) <= TOL
-
-
-@pytest.mark.parametrize("d,p,n_el,n_el_t", [(3, 2, 16, 8), (3, 3, 13, 5), (3, 4, 11, 4)])
-def test_axis1_time_major_handoff(gpu, oracle, d, p, n_el, n_el_t):
-    """Pair mode hands the time-major layout over on axis 1 (forward axes d..1,
-    rows stored by even/odd position, blocks numbered by position); KS_FD_TM1=0
-    keeps the outermost-axis hand-off. Both match the oracle, forward and
-    adjoint, and each other to rounding; ks_fd_block still answers by natural
-    fiber index."""
-    old = os.environ.get("KS_FD_TM1")
-    try:
-        os.environ["KS_FD_TM1"] = "0"
-        _, g0, o = _pair(gpu, oracle, d, p, n_el, n_el_t)
-        os.environ["KS_FD_TM1"] = "1"
-        a, g1, _ = _pair(gpu, oracle, d, p, n_el, n_el_t)
-    finally:
-        if old is None:
-            del os.environ["KS_FD_TM1"]
-        else:
-            os.environ["KS_FD_TM1"] = old
-    assert g0.info()["time_major_axis"] == d and g1.info()["time_major_axis"] == 1
-    r = oracle.random_vec(o.N, 17)
-    for ap in ("apply", "apply_adjoint"):
-        z0, z1 = getattr(g0, ap)(r), getattr(g1, ap)(r)
-        zo = getattr(o, ap)(r)
-        assert rel(z1, zo) <= TOL and maxrel(z1, zo) <= TOL
-        assert rel(z1, z0) <= 1e-12
-    n1 = a["dims"][1]
-    for i in (0, 1, n1 - 1, n1 + 3, o.N // a["dims"][0] - 1):
-        b0, b1 = g0.block(i, p), g1.block(i, p)
-        assert np.array_equal(b0[0], b1[0]) and np.array_equal(b0[1], b1[1])
-
-
-@pytest.mark.parametrize("d,p,n_el,n_el_t", [(3, 2, 16, 8), (3, 4, 11, 4), (2, 3, 16, 8), (2, 2, 12, 6),
-                                            (1, 3, 16, 16)])
-def test_no_pivot_pair_solve_bitexact(gpu, oracle, d, p, n_el, n_el_t, monkeypatch):
-    """Warps whose 32 blocks (pair solve) or whose 32 fibers' blocks (ring
-    solve, d = 1, 2) did not pivot -- all but the smallest-eigenvalue ones --
-    skip the fill-in band and the pivots; the
-    skipped entries are exact zeros, so the application is bit-identical to
-    the full band read (KS_FD_NOPIV=0)."""
-    monkeypatch.setenv("KS_FD_NOPIV", "0")
-    _, g0, o = _pair(gpu, oracle, d, p, n_el, n_el_t)
-    monkeypatch.setenv("KS_FD_NOPIV", "1")
-    _, g1, _ = _pair(gpu, oracle, d, p, n_el, n_el_t)
-    r = oracle.random_vec(o.N, 29)
-    z0, z1 = g0.apply(r), g1.apply(r)
-    assert np.array_equal(z0, z1)
-    assert rel(z1, o.apply(r)) <= TOL

@@ -1,0 +1,182 @@
+"""Parity at the BASELINE configs' full sizes against the reference itself.
+
+The reference (oracle/_ref: its unmodified sources, oracle/build_ref.sh) runs
+live on the GPU box's host cores in worker processes (tests/ref_jobs.py), on
+the same seeded inputs; the GPU side builds the same problem with libks's own
+host setup and runs through the C-ABI. Tolerances are north_star's: per
+application <= 1e-10 relative (2-norm and max-abs), PCG iteration counts
+within +-1 with matching converged / breakdown flags.
+
+  c3  d=3 p=2 n_el=64           FD apply + matvec (17.0 M DOF), FD-PCG to 1e-8
+  c2  d=2 p=3 n_el=64           manufactured sin-sin solve + L2 / energy errors
+  c4  d=2 n_el=128 p=2..6       manufactured solve per degree (iteration counts)
+  c5  d=3 p=4 n_el=128, n_el_t=4 (the c5 spatial shape, n_s = 130, with 7 time
+      functions: one application of each operator fits host RAM and minutes)
+plus the PCG restart branch (krylov.cpp:84-100) and concurrent applies on one
+handle.
+"""
+import concurrent.futures as cf
+import multiprocessing as mp
+import os
+import threading
+
+import numpy as np
+import pytest
+
+import ref_jobs as R
+from helpers import rel, maxrel
+
+pytestmark = pytest.mark.gpu
+
+# name -> (job, args); all submitted at once, each test waits on its own
+JOBS = {
+    "c3_apply": (R.apply_job, (3, 2, 64, 64, 1234)),
+    "c3_solve": (R.random_solve_job, (3, 2, 64, 64, 1234)),
+    "c2": (R.manufactured_job, (2, 3, 64, 64)),
+    "c5_apply": (R.apply_job, (3, 4, 128, 4, 99)),
+    "restart": (R.restart_job, (2, 3, 8, 8, 5, 1e-15)),
+}
+for _p in range(2, 7):
+    JOBS[f"c4_p{_p}"] = (R.manufactured_job, (2, _p, 128, 128, False))
+
+
+@pytest.fixture(scope="module")
+def ref_results():
+    from oracle import refdrv
+    if not refdrv.available():
+        pytest.fail("oracle/_ref not built: the full-size parity tests need the reference build")
+    workers = max(1, min(len(JOBS), os.cpu_count() or 1))
+    ex = cf.ProcessPoolExecutor(max_workers=workers, mp_context=mp.get_context("spawn"))
+    futs = {k: ex.submit(fn, *args) for k, (fn, args) in JOBS.items()}
+    yield futs
+    ex.shutdown(wait=False, cancel_futures=True)
+
+
+def _get(ref_results, key):
+    return ref_results[key].result(timeout=1800)
+
+
+def _within(a, b, tol=1e-10):
+    return rel(a, b) <= tol and maxrel(a, b) <= tol
+
+
+def test_c3_fd_apply_and_matvec_vs_reference(gpu, oracle, ref_results):
+    prob = gpu.SpaceTimeProblem.uniform(3, 2, 64, 64)
+    r = oracle.random_vec(prob.N_dof, 1234)
+    P = gpu.FDPreconditioner(prob)
+    A = gpu.assemble_system_operator(prob)
+    z, y = P.apply(r), A.apply(r)
+    ref = _get(ref_results, "c3_apply")
+    assert list(ref["dims"]) == prob.reduced_dims() == [65, 64, 64, 64]
+    ez, ey = (rel(z, ref["z"]), maxrel(z, ref["z"])), (rel(y, ref["y"]), maxrel(y, ref["y"]))
+    print(f"c3 FD rel {ez[0]:.2e} max {ez[1]:.2e}; matvec rel {ey[0]:.2e} max {ey[1]:.2e}")
+    assert max(ez) <= 1e-10 and max(ey) <= 1e-10
+
+
+def test_c3_pcg_iterations_vs_reference(gpu, oracle, ref_results):
+    prob = gpu.SpaceTimeProblem.uniform(3, 2, 64, 64)
+    b = oracle.random_vec(prob.N_dof, 1234)
+    P = gpu.FDPreconditioner(prob)
+    A = gpu.assemble_system_operator(prob)
+    s = gpu.pcg(A, P, b, gpu.PcgOptions(1e-8, 200))
+    ref = _get(ref_results, "c3_solve")
+    print(f"c3 PCG iterations gpu {s.iterations} ref {ref['iterations']}; x rel {rel(s.x, ref['x']):.2e}")
+    assert s.converged == ref["converged"] and s.breakdown == ref["breakdown"]
+    assert abs(s.iterations - ref["iterations"]) <= 1
+    # both stop at relres <= 1e-8: the iterates agree to the solve tolerance
+    assert rel(s.x, ref["x"]) <= 1e-6
+
+
+def _manufactured_gpu(gpu, d, p, n_el):
+    prob = gpu.SpaceTimeProblem.uniform(d, p, n_el, n_el)
+    A, P, Q = gpu.assemble_system_operator(prob), gpu.FDPreconditioner(prob), gpu.Quadrature(prob)
+    rhs, bnd = Q.lift("sinsin", "sinsin")
+    s = gpu.pcg(A, P, gpu.DeviceVector.from_host(rhs), gpu.PcgOptions(1e-8, 200))
+    full = Q.extend(s.x, bnd)
+    l2, en = Q.error_norms(full, "sinsin", "sinsin")
+    return prob, Q, rhs, bnd, s, full, l2, en
+
+
+def test_c2_manufactured_solve_vs_reference(gpu, ref_results):
+    prob, Q, rhs, bnd, s, full, l2, en = _manufactured_gpu(gpu, 2, 3, 64)
+    ref = _get(ref_results, "c2")
+    print(f"c2 iterations gpu {s.iterations} ref {ref['iterations']}; L2 gpu {l2:.6e} ref {ref['l2']:.6e}")
+    # right-hand side and lifting: per-application tolerance
+    assert _within(rhs, ref["rhs"]) and _within(bnd, ref["bnd"])
+    assert s.converged == ref["converged"] and abs(s.iterations - ref["iterations"]) <= 1
+    # the same error functional on the reference's own solution: 1e-10
+    l2r, enr = Q.error_norms(ref["full"], "sinsin", "sinsin")
+    assert abs(l2r - ref["l2"]) <= 1e-10 * ref["l2"] and abs(enr - ref["energy"]) <= 1e-10 * ref["energy"]
+    # end to end (two CG runs that each stop at relres 1e-8): L2 errors to 1e-6
+    assert abs(l2 - ref["l2"]) <= 1e-6 * ref["l2"]
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 5, 6])
+def test_c4_degree_sweep_iterations_vs_reference(gpu, ref_results, p):
+    prob, Q, rhs, bnd, s, full, l2, en = _manufactured_gpu(gpu, 2, p, 128)
+    ref = _get(ref_results, f"c4_p{p}")
+    print(f"c4 p={p}: iterations gpu {s.iterations} ref {ref['iterations']}; L2 gpu {l2:.6e} ref {ref['l2']:.6e}")
+    assert list(ref["dims"]) == prob.reduced_dims()
+    assert s.converged == ref["converged"] and abs(s.iterations - ref["iterations"]) <= 1
+    assert abs(l2 - ref["l2"]) <= 1e-6 * ref["l2"]
+
+
+def test_c5_shape_fd_apply_and_matvec_vs_reference(gpu, oracle, ref_results):
+    """The c5 spatial shape (n_s = 130, p = 4: folded transforms with hc = 65,
+    9-band time blocks) with 7 time functions."""
+    prob = gpu.SpaceTimeProblem.uniform(3, 4, 128, 4)
+    r = oracle.random_vec(prob.N_dof, 99)
+    P = gpu.FDPreconditioner(prob)
+    A = gpu.assemble_system_operator(prob)
+    z, y = P.apply(r), A.apply(r)
+    ref = _get(ref_results, "c5_apply")
+    assert list(ref["dims"]) == prob.reduced_dims() == [7, 130, 130, 130]
+    print(f"c5-shape FD rel {rel(z, ref['z']):.2e} max {maxrel(z, ref['z']):.2e}; "
+          f"matvec rel {rel(y, ref['y']):.2e} max {maxrel(y, ref['y']):.2e}")
+    assert _within(z, ref["z"]) and _within(y, ref["y"])
+
+
+def test_pcg_restart_branch_vs_reference(gpu, oracle, ref_results):
+    """tol below the attainable accuracy: the recurrence residual passes tol,
+    the true residual does not, pcg restarts from the exact residual twice and
+    stops unconverged at the third time (krylov.cpp:84-100) -- the reference
+    does the same on the same input."""
+    prob = gpu.SpaceTimeProblem.uniform(2, 3, 8, 8)
+    b = oracle.random_vec(prob.N_dof, 5)
+    P, A = gpu.FDPreconditioner(prob), gpu.assemble_system_operator(prob)
+    s = gpu.pcg(A, P, b, gpu.PcgOptions(1e-15, 400))
+    ref = _get(ref_results, "restart")
+    print(f"restart: gpu {s.iterations} it, restarts {s.restarts}; ref {ref['iterations']} it")
+    assert not ref["converged"] and not ref["breakdown"] and ref["iterations"] < 400
+    assert not s.converged and not s.breakdown and s.restarts == 3
+    assert abs(s.iterations - ref["iterations"]) <= 3
+    # every restart overwrote its history entry with a true residual above tol
+    assert s.res_history[-1] > 1e-15 and len(s.res_history) == s.iterations
+
+
+def test_concurrent_applies_on_one_handle(gpu, oracle):
+    """Several host threads applying one FD handle and one operator handle at
+    once (const apply is reentrant in the reference): each gets the result of
+    its own input."""
+    prob = gpu.SpaceTimeProblem.uniform(3, 2, 16, 16)
+    P, A = gpu.FDPreconditioner(prob), gpu.assemble_system_operator(prob)
+    ins = [oracle.random_vec(prob.N_dof, 100 + k) for k in range(6)]
+    want = [(P.apply(v), A.apply(v)) for v in ins]
+    got = [None] * len(ins)
+    errs = []
+
+    def work(k):
+        try:
+            for _ in range(3):
+                got[k] = (P.apply(ins[k]), A.apply(ins[k]))
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(len(ins))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs
+    for (z, y), (zw, yw) in zip(got, want):
+        assert np.array_equal(z, zw) and np.array_equal(y, yw)

@@ -1,9 +1,9 @@
-"""d = 3 Kronecker-sum matvec in two launches (csrc/ks_kron3.cu): an axis-3
-pass producing one tensor per distinct axis-3 factor, then axes t, 1, 2 fused
-in an NVRTC-generated kernel. Parity against the oracle's term-by-term
-KroneckerOperator::apply (reference tensorops.cpp:236-254) on the system
-operator (assembly.cpp:202-251) and on generic term lists (complex factors,
-identities on every axis, mixed bandwidths), at the north_star tolerance."""
+"""d = 3 Kronecker-sum matvec plans (csrc/ks_kron.cu, ks_kron_jit.cu): sign-merged
+factors, rank-merged middle boundary, fused pass pairs. Parity against the
+oracle's term-by-term KroneckerOperator::apply (reference tensorops.cpp:236-254)
+on the system operator (assembly.cpp:202-251) and on generic term lists
+(complex factors, identities on every axis, mixed bandwidths), at the
+north_star tolerance."""
 import numpy as np
 import pytest
 
@@ -14,47 +14,25 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-10
 
 
-@pytest.fixture(autouse=True)
-def _two_launch_path(monkeypatch):
-    # the two-launch path is opt-in (the rank-merged pass pairs are faster at c3)
-    monkeypatch.setenv("KS_KRON3", "1")
-
-
 @pytest.mark.parametrize("p,n_el,n_el_t", [(2, 5, 5), (2, 9, 3), (3, 6, 7), (4, 5, 4), (2, 17, 2), (5, 6, 3)])
-def test_system_matvec_two_launch_path(gpu, oracle, p, n_el, n_el_t):
+def test_system_matvec_shapes(gpu, oracle, p, n_el, n_el_t):
     a = setup_arrays(gpu, 3, p, n_el, n_el_t)
     A = gpu.assemble_system_operator(a["prob"])
-    assert A.plan_info()["engine"] == "axis3_then_fused_t12"
     K = oracle.OracleKron(a["dims"], oracle.system_terms(a, 3, a["nu"]))
     x = oracle.random_vec(K.N, 77)
     y, yo = A.apply(x), K.apply(x)
     assert rel(y, yo) <= TOL and maxrel(y, yo) <= TOL
 
 
-@pytest.mark.parametrize("tx", ["1", "2", "3", "5"])
-def test_tile_widths(gpu, oracle, tx, monkeypatch):
-    """Axis-1 tiles that do not divide n_1 (partial last tile, halo lines
-    outside the tensor)."""
-    monkeypatch.setenv("KS_KRON3_TX", tx)
-    a = setup_arrays(gpu, 3, 2, 6, 4)
-    A = gpu.assemble_system_operator(a["prob"])
-    assert A.plan_info()["engine"] == "axis3_then_fused_t12"
-    K = oracle.OracleKron(a["dims"], oracle.system_terms(a, 3, a["nu"]))
-    x = oracle.random_vec(K.N, 5)
-    assert rel(A.apply(x), K.apply(x)) <= TOL
-
-
 def test_equals_level_pass_plan(gpu, oracle, monkeypatch):
-    """Same operator with the two-launch path and factor merging switched off
-    (exact-content deduplication, fused pass pairs / level passes)."""
+    """Same operator with factor merging switched off (exact-content
+    deduplication, fused pass pairs / level passes)."""
     a = setup_arrays(gpu, 3, 3, 8, 6)
     x = oracle.random_vec(a["prob"].N_dof, 11)
     y3 = gpu.assemble_system_operator(a["prob"]).apply(x)
-    monkeypatch.setenv("KS_KRON3", "0")
     monkeypatch.setenv("KS_KRON_MERGE", "0")
     monkeypatch.setenv("KS_KRON_RANK", "0")
     A0 = gpu.assemble_system_operator(a["prob"])
-    assert A0.plan_info()["engine"] != "axis3_then_fused_t12"
     assert rel(y3, A0.apply(x)) <= 1e-13
 
 
@@ -79,7 +57,6 @@ def test_generic_terms_vs_dense(gpu, oracle):
     K = gpu.KroneckerOperator(dims)
     for c, fs, bw in terms:
         K.add_term(c, [None if f is None else gpu.Banded(dims[k], bw[k], f) for k, f in enumerate(fs)])
-    assert K.plan_info()["engine"] == "axis3_then_fused_t12"
     x = rng.standard_normal(np.prod(dims)) + 1j * rng.standard_normal(np.prod(dims))
     yd = oracle.kron_to_dense(dims, terms) @ x
     y = K.apply(x)
@@ -109,12 +86,11 @@ def test_rank_merged_plan_matches_oracle(gpu, oracle, monkeypatch):
     """Default matvec plan (fused pass pairs over the rank-merged boundary:
     proportional coefficient rows share one intermediate) against the oracle,
     and against the plan without the merge."""
-    monkeypatch.setenv("KS_KRON3", "0")
     for p, n_el, n_el_t in [(2, 9, 5), (3, 6, 4), (4, 5, 3)]:
         a = setup_arrays(gpu, 3, p, n_el, n_el_t)
         A = gpu.assemble_system_operator(a["prob"])
         info = A.plan_info()
-        assert info["nodes"] == 9 and info["engine"] != "axis3_then_fused_t12"
+        assert info["nodes"] == 9
         K = oracle.OracleKron(a["dims"], oracle.system_terms(a, 3, a["nu"]))
         x = oracle.random_vec(K.N, 13)
         y, yo = A.apply(x), K.apply(x)
@@ -129,7 +105,6 @@ def test_rank_merge_complex_scales_vs_dense(gpu, oracle, monkeypatch):
     """Generic term list whose middle-boundary rows are proportional with
     complex ratios (and one that is not): the merged plan must equal the dense
     Kronecker sum (tensorops.cpp:277-301)."""
-    monkeypatch.setenv("KS_KRON3", "0")
     rng = np.random.default_rng(21)
     dims = [4, 5, 3, 6]
 
