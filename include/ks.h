@@ -93,9 +93,11 @@ int ks_fd_create(int d, const int* dims, double nu, int p_t,
  * alias. stream is a cudaStream_t (NULL = the handle's own stream, blocking).
  * KS_MEM_HOST with a non-NULL stream is asynchronous: the H2D copy, the apply
  * and the D2H copy are queued on the handle's copy/compute streams (three
- * staging buffers, so consecutive applies overlap their transfers; the H2D
- * copy starts once `stream` reaches the call) and z is valid once `stream` is
- * synchronised; r and z must stay untouched (and should be pinned) until then.
+ * staging buffers, so consecutive applies overlap their transfers). r is read
+ * from host memory as soon as the call is made (it must hold its values then,
+ * as for the reference's synchronous call); the D2H into z waits until
+ * `stream` reaches the call, and z is valid once `stream` is synchronised;
+ * r and z must stay untouched (and should be pinned) until then.
  * Applies on one handle are ordered on the device whatever streams they use
  * (the handle's scratch is shared), and a host mutex serialises the calls. */
 int ks_fd_apply(ks_fd* fd, const ks_c64* r, ks_c64* z, int mem, void* stream);

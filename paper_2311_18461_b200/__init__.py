@@ -503,7 +503,9 @@ class FDPreconditioner:
         return {"folded_axes": [l + 1 for l in range(d) if m.value >> l & 1], "blocks": nb.value,
                 "time_major_axis": 1 if m.value >> 17 & 1 else d,
                 # least-squares blocks: L D L^H (never pivots); Galerkin LU: no block pivoted
-                "no_pivot_solve": bool(m.value >> 18 & 1)}
+                "no_pivot_solve": bool(m.value >> 18 & 1),
+                # axis-1 transform + block solves + inverse transform in one kernel (ks_fdaxis1.cu)
+                "fused_axis1": bool(m.value >> 19 & 1)}
 
     def time(self, r: DeviceVector, z: DeviceVector, iters: int, flush: bool = True):
         ms, mk = C.c_double(), C.c_double()

@@ -107,6 +107,9 @@ struct ks_fd {
     std::vector<std::vector<double>> lam_host;
     std::vector<int> fiber_block; // host copy of the block map (empty = identity)
     bool tm1 = false;             // time-major hand-off on axis 1 (pair mode, folded axis 1)
+    bool axis1 = false;           // fused axis-1 stage (ks_fdaxis1.cu): transform + solves + transform
+    DevBuf A1, order1, grp1;      // its matrix, slab order and per-slab block group
+    int n1b = 0;                  // blocks per group (n1 rounded up to even)
     int kind = 0;                 // 0: least-squares blocks, 1: Galerkin blocks (galerkin_fast_solver)
     DevBuf Lt, Mt, Wsym;          // Wsym: W + W^H (least squares) or W itself (Galerkin)
     FdBlocks blocks;
@@ -201,6 +204,42 @@ void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStre
             launch();
         }
     };
+    if (f->axis1) {
+        // forward axes d..2, then axis 1 + block solves + inverse axis 1 in one
+        // kernel per slab, then inverse axes 2..d (the order of
+        // mode products on distinct axes only changes rounding)
+        for (int l = d; l >= 2; --l) {
+            double* out = bufs[nb];
+            nb ^= 1;
+            gemm(f->At_fwd[l - 1], l, cur, out, 0);
+            cur = out;
+        }
+        double* mid = d == 1 ? reinterpret_cast<double*>(z) : const_cast<double*>(cur); // in place
+        auto launch = [&]() {
+            launch_fd_axis1(f->fold[0], f->A1.as<double>(), f->dims[0], (long long)(f->Ns / (size_t)f->dims[1]),
+                            f->order1.as<int>(), f->grp1.as<int>(), f->n1b, f->blocks, cur, mid, st);
+        };
+        if (ev) {
+            cudaEvent_t a, b;
+            KS_CUDA(cudaEventCreate(&a));
+            KS_CUDA(cudaEventCreate(&b));
+            KS_CUDA(cudaEventRecord(a, st));
+            launch();
+            KS_CUDA(cudaEventRecord(b, st));
+            ev->push_back(a);
+            ev->push_back(b);
+        } else {
+            launch();
+        }
+        cur = mid;
+        for (int l = 2; l <= d; ++l) {
+            double* out = l == d ? reinterpret_cast<double*>(z) : bufs[nb];
+            if (l != d) nb ^= 1;
+            gemm(f->At_inv[l - 1], l, cur, out, 0);
+            cur = out;
+        }
+        return;
+    }
     if (f->tm1) {
         // pair mode with a folded axis 1: forward axes d..1, the axis-1 transform
         // writes the position-ordered time-major layout; solves; inverse axis 1
@@ -259,10 +298,13 @@ void fd_apply_any(ks_fd* f, const ks_c64* r, ks_c64* z, int mem, void* stream, b
         if (!stream) KS_CUDA(cudaStreamSynchronize(st));
     } else if (stream) {
         // pipelined: slot k's H2D waits until slot k's previous D2H has drained
-        // its staging buffer and until the caller's stream reaches this call
-        // (earlier work there may still be producing r); the compute waits for
-        // the handle's previous apply (shared scratch); the caller's stream
-        // waits for this apply's D2H
+        // its staging buffer (r is read from host memory as soon as the call is
+        // made, like the reference's synchronous call reads it); the compute
+        // waits for the handle's previous apply (shared scratch); the D2H into z
+        // waits until the caller's stream reaches this call (earlier work there
+        // may still read z); the caller's stream then waits for the D2H. Making
+        // the H2D wait on the caller's stream as well would serialise every H2D
+        // behind the previous apply's D2H (that stream waits on it).
         if (!f->h2d) {
             KS_CUDA(cudaStreamCreateWithFlags(&f->h2d, cudaStreamNonBlocking));
             KS_CUDA(cudaStreamCreateWithFlags(&f->d2h, cudaStreamNonBlocking));
@@ -279,7 +321,6 @@ void fd_apply_any(ks_fd* f, const ks_c64* r, ks_c64* z, int mem, void* stream, b
         cudaStream_t us = static_cast<cudaStream_t>(stream);
         double2* buf = f->pio[k].as<double2>();
         KS_CUDA(cudaEventRecord(f->ev_user, us));
-        KS_CUDA(cudaStreamWaitEvent(f->h2d, f->ev_user, 0));
         KS_CUDA(cudaStreamWaitEvent(f->h2d, f->ev_out[k], 0));
         KS_CUDA(cudaMemcpyAsync(buf, r, bytes, cudaMemcpyHostToDevice, f->h2d));
         KS_CUDA(cudaEventRecord(f->ev_in[k], f->h2d));
@@ -289,6 +330,7 @@ void fd_apply_any(ks_fd* f, const ks_c64* r, ks_c64* z, int mem, void* stream, b
         KS_CUDA(cudaEventRecord(f->done, f->stream));
         KS_CUDA(cudaEventRecord(f->ev_comp[k], f->stream));
         KS_CUDA(cudaStreamWaitEvent(f->d2h, f->ev_comp[k], 0));
+        KS_CUDA(cudaStreamWaitEvent(f->d2h, f->ev_user, 0));
         KS_CUDA(cudaMemcpyAsync(z, buf, bytes, cudaMemcpyDeviceToHost, f->d2h));
         KS_CUDA(cudaEventRecord(f->ev_out[k], f->d2h));
         KS_CUDA(cudaStreamWaitEvent(us, f->ev_out[k], 0));
@@ -468,6 +510,18 @@ static void fd_create_impl(int kind, int d, const int* dims, double nu, int p_t,
     // position.
     const bool tm1 = pair && f->fold[0].n > 0 && (int)f->fold[0].perm.size() == dims[1];
     f->tm1 = tm1;
+    // fused axis-1 stage (least-squares blocks, folded axis 1, slab fits shared
+    // memory): blocks numbered by axis-1 position within per-slab groups of n1b.
+    // Opt-in (KS_FD_AXIS1=1): measured at c3 0.55 ms against 0.54 ms for the
+    // separate transform / solve / transform it replaces -- the 130-step
+    // sequential sweeps of one slab per SM are latency bound
+    bool ax1 = kind == 0 && f->fold[0].n > 0 && (int)f->fold[0].perm.size() == dims[1] &&
+               fd_axis1_supported(dims[1], nt, p_t);
+    {
+        const char* e = std::getenv("KS_FD_AXIS1");
+        ax1 = ax1 && e && std::strcmp(e, "1") == 0;
+    }
+    std::vector<int> grp1;
     if (pair) {
         const int n1 = dims[1], n2 = dims[2];
         // position -> eigen-index of axis 1 (identity unless tm1), and its inverse
@@ -481,19 +535,26 @@ static void fd_create_impl(int kind, int d, const int* dims, double nu, int p_t,
                 pidx[(size_t)i2 * n2 + i3] = pidx[(size_t)i3 * n2 + i2] = (int)prs.size();
                 prs.push_back(make_int2(i2, i3));
             }
-        lam_blk.resize((size_t)n1 * prs.size());
+        const int nbg = ax1 ? (n1 + 1) / 2 * 2 : n1; // blocks per pair group
+        lam_blk.resize((size_t)nbg * prs.size());
         for (size_t pp = 0; pp < prs.size(); ++pp)
-            for (int p1 = 0; p1 < n1; ++p1) {
-                const int id[3] = {perm1[p1], prs[pp].x, prs[pp].y};
-                lam_blk[(size_t)p1 + (size_t)n1 * pp] = ref_sum(id);
+            for (int p1 = 0; p1 < nbg; ++p1) {
+                // (a padding block repeats the group's last eigenvalue; never solved)
+                const int id[3] = {perm1[std::min(p1, n1 - 1)], prs[pp].x, prs[pp].y};
+                lam_blk[(size_t)p1 + (size_t)nbg * pp] = ref_sum(id);
             }
+        if (ax1) {
+            grp1.resize(f->Ns / n1);
+            for (size_t o = 0; o < grp1.size(); ++o)
+                grp1[o] = pidx[(o % n2) * n2 + o / n2];
+        }
         // host map by natural fiber index (ks_fd_block); device map by layout
         // position (time-major adjoint solves; natural order unless tm1)
         f->fiber_block.resize(f->Ns);
         std::vector<int> fb_dev(f->Ns);
         for (size_t i = 0; i < f->Ns; ++i) {
             const int i1 = (int)(i % n1), i2 = (int)((i / n1) % n2), i3 = (int)(i / ((size_t)n1 * n2));
-            const int pb = n1 * pidx[(size_t)i2 * n2 + i3];
+            const int pb = nbg * pidx[(size_t)i2 * n2 + i3];
             f->fiber_block[i] = pos1[i1] + pb;
             fb_dev[i] = i1 + pb;
         }
@@ -503,6 +564,31 @@ static void fd_create_impl(int kind, int d, const int* dims, double nu, int p_t,
         B.pair_n2 = n2;
         B.pairs.alloc(prs.size() * sizeof(int2));
         KS_CUDA(cudaMemcpy(B.pairs.p, prs.data(), prs.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    } else if (ax1) {
+        // one group of n1b position-ordered blocks per slab (no permutation dedup:
+        // a slab's blocks must be consecutive)
+        const int n1 = dims[1], nbg = (n1 + 1) / 2 * 2;
+        const size_t nslab = f->Ns / (size_t)n1;
+        std::vector<int> perm1(f->fold[0].perm), pos1(n1);
+        for (int p = 0; p < n1; ++p) pos1[perm1[p]] = p;
+        lam_blk.resize((size_t)nbg * nslab);
+        grp1.resize(nslab);
+        for (size_t o = 0; o < nslab; ++o) {
+            int id[3] = {0, 0, 0};
+            size_t rest = o;
+            for (int l = 1; l < d; ++l) {
+                id[l] = (int)(rest % (size_t)dims[l + 1]);
+                rest /= (size_t)dims[l + 1];
+            }
+            for (int p1 = 0; p1 < nbg; ++p1) {
+                id[0] = perm1[std::min(p1, n1 - 1)];
+                lam_blk[(size_t)p1 + (size_t)nbg * o] = ref_sum(id);
+            }
+            grp1[o] = (int)o;
+        }
+        f->fiber_block.resize(f->Ns);
+        for (size_t i = 0; i < f->Ns; ++i)
+            f->fiber_block[i] = pos1[i % (size_t)n1] + nbg * (int)(i / (size_t)n1);
     } else if (!dedup) {
         lam_blk.resize(f->Ns);
         for (size_t i = 0; i < f->Ns; ++i) {
@@ -543,8 +629,37 @@ static void fd_create_impl(int kind, int d, const int* dims, double nu, int p_t,
     B.lam_blk.alloc(B.nblk * sizeof(double));
     KS_CUDA(cudaMemcpy(B.lam_blk.p, lam_blk.data(), B.nblk * sizeof(double), cudaMemcpyHostToDevice));
     B.kind = kind;
+    if (ax1) B.gsz = (size_t)((dims[1] + 1) / 2 * 2); // one factor group per slab group
     fd_blocks_alloc(B);
     launch_fd_factor(B, nu, f->Lt.as<double>(), f->Mt.as<double>(), f->Wsym.as<double2>(), f->stream);
+    if (ax1) {
+        const int n1 = dims[1];
+        const size_t nslab = f->Ns / (size_t)n1;
+        std::vector<double> Am;
+        fd_axis1_matrix(f->fold[0], nt, p_t, Am);
+        f->A1.alloc(Am.size() * sizeof(double));
+        KS_CUDA(cudaMemcpy(f->A1.p, Am.data(), Am.size() * sizeof(double), cudaMemcpyHostToDevice));
+        // slabs sharing their blocks (pair mode: (i2, i3) and (i3, i2)) run as
+        // neighbouring work items, so the second factor read hits L2
+        std::vector<int> order;
+        order.reserve(nslab);
+        if (pair) {
+            const int n2 = dims[2];
+            for (int i3 = 0; i3 < n2; ++i3)
+                for (int i2 = 0; i2 <= i3; ++i2) {
+                    order.push_back(i2 + n2 * i3);
+                    if (i2 != i3) order.push_back(i3 + n2 * i2);
+                }
+        } else {
+            for (size_t o = 0; o < nslab; ++o) order.push_back((int)o);
+        }
+        f->order1.alloc(order.size() * sizeof(int));
+        KS_CUDA(cudaMemcpy(f->order1.p, order.data(), order.size() * sizeof(int), cudaMemcpyHostToDevice));
+        f->grp1.alloc(grp1.size() * sizeof(int));
+        KS_CUDA(cudaMemcpy(f->grp1.p, grp1.data(), grp1.size() * sizeof(int), cudaMemcpyHostToDevice));
+        f->n1b = (n1 + 1) / 2 * 2;
+        f->axis1 = true;
+    }
     f->s0.alloc(f->N * sizeof(double2));
     f->s1.alloc(f->N * sizeof(double2));
     KS_CUDA(cudaStreamSynchronize(f->stream));
@@ -617,6 +732,7 @@ int ks_fd_info(const ks_fd* fd, int* folded_axes, size_t* blocks) {
     for (size_t l = 0; l < fd->fold.size(); ++l)
         if (fd->fold[l].n) m |= 1 << l;
     if (fd->tm1) m |= 1 << 17;
+    if (fd->axis1) m |= 1 << 19;
     if (fd->blocks.kind == 0 || fd->blocks.nopiv) m |= 1 << 18; // kind 0: L D L^H, never pivots
     if (folded_axes) *folded_axes = m;
     if (blocks) *blocks = fd->blocks.nblk;

@@ -1,0 +1,501 @@
+// Fused axis-1 stage of the FD apply: forward axis-1 transform, the block
+// solves along time, inverse axis-1 transform -- one kernel, the (t, i1) slab
+// never leaves shared memory.
+//
+// Reference: FastDiagSolver::solve (src/fdsolver.cpp:53-63) = to_eigen
+// (mode products with U_l^T, :7-14), N_s banded solves on the time fibers
+// (:58-60, eigensolve.cpp:123-140), from_eigen (U_l, :16-21). Mode products
+// on distinct axes commute, so the apply runs the forward
+// transforms on axes d..2 first, then this kernel, then the inverse ones on
+// axes 2..d (ks_api.cu fd_apply_dev).
+//
+// Why: with the tensor laid out time fastest, the slab X[o] = (i1, t) for a
+// fixed outer index o = (i2, .., id) is contiguous (c3: 64 x 65 complex =
+// 66.5 KB). A separate axis-1 transform, a time-major block solve and the
+// inverse transform move the tensor through HBM three times plus the
+// factors; here the slab is read once and written once, and only the
+// factors (L D L^H rows, ks_fdsolve.cu) stream through L2.
+//
+// Per slab (persistent CTAs, one per SM, warp-specialised pipeline below):
+//   1. bulk-copy (cp.async.bulk + mbarrier) the n1 rows into shared memory
+//      (rows padded to PD doubles, PD = 4 mod 16: conflict-free fragments);
+//   2. folded forward transform on FP64 tensor cores (mma.m8n8k4 DMMA):
+//      even warps Y[E] = se^T (X[j] + X[n1-1-j]), odd warps
+//      Y[O] = so^T (X[j] - X[n1-1-j]); the results overwrite the slab by
+//      position (even eigen-indices first, then odd);
+//   3. one thread per fiber (position m): L D L^H forward / backward sweeps
+//      along t in shared memory, factor rows through a 16-step per-thread
+//      cp.async ring (the slab's blocks are consecutive -- position m of slab
+//      o uses block m + n1b * grp[o] -- and are bulk-prefetched into L2 when
+//      the slab load is issued, so the sweeps wait on L2, not HBM, latency);
+//   4. folded inverse transform: even warps e_j = se X[E], odd warps
+//      o_j = so X[O]; exchange through shared memory; Y[j] = e_j + o_j and
+//      Y[n1-1-j] = e_j - o_j stored to HBM.
+// Warp w: GEMM half g = w / 4 (even / odd), column group cq = w % 4 (8-double
+// column blocks cq, cq+4, ...), all HB row blocks.
+#include "ks_internal.hpp"
+
+#include <algorithm>
+
+namespace ks {
+
+namespace {
+
+constexpr int kThr = 256;
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+__device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cconjmul(double2 a, double2 b) { // conj(a) * b
+    return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+
+struct Axis1Args {
+    const double* A;       // [2][SZ][AP] se / so, element (j, m) at j*AP + m, zero padded
+    const double* X;       // natural layout, slab o at X + o * n1 * nt * 2
+    double* Y;
+    const int* order;      // slab processed by work item s (pairs of swapped slabs adjacent)
+    const int* grp;        // blocks of slab o: b = m + n1b * grp[o] (position m, n1b >= n1 even)
+    const double* dinv;    // L D L^H factors, block-interleaved (ks_fdsolve.cu)
+    const double2* v;
+    long long nblk;
+    int nslab, n1, n1b, hc, nt, PD, AP, SZ, K4, CB;
+
+};
+
+// Warp-specialised software pipeline, one CTA per SM, two slab buffers:
+// at step t the solver warps sweep slab t in one buffer while the 8 GEMM warps
+// run the inverse transform + store of slab t-1 and then load + forward-
+// transform slab t+1 in the other; one CTA-wide barrier per step. The DMMA
+// work (the folded transforms, ~4.4 us per c3 slab at the SM's FP64 peak) and
+// the latency-bound sweeps (2 n_t dependent steps) overlap instead of
+// alternating.
+//
+// GEMM warp w owns the 8-double column blocks w, w+8, w+16 of the slab and
+// computes both halves (even and odd eigenvectors) for them: one fold
+// (X[j] +- X[n1-1-j]) per loaded pair, the inverse unfold (e_j +- o_j) in
+// registers, and no shared-memory traffic between warps.
+//
+// Solver thread m (position m) streams its factor rows from a D-slot ring in
+// shared memory that one producer thread fills with bulk copies: the slab's
+// blocks are consecutive (m + n1b * grp[o]), so step k of every fiber is one
+// contiguous n1b-row run per factor array. Full / empty mbarriers per slot;
+// the producer runs D-1 steps ahead, across sweeps and slabs.
+template <int HB, int NCB, int P, int D, bool ODD>
+__global__ void __launch_bounds__(kThr + 96, 1) k_fd_axis1(Axis1Args a) {
+    extern __shared__ __align__(16) double sm[];
+    const int n1 = a.n1, n1b = a.n1b, hc = a.hc, no = n1 - hc, nt = a.nt, PD = a.PD, AP = a.AP;
+    const size_t bufd = (size_t)(n1 + 4) * PD;                            // doubles per slab buffer
+    double* S0 = sm;                                                      // [2][n1 + 4][PD]
+    // factor ring: D slots of CK time steps, slot = [CK][P][n1b] v rows then [CK][n1b] 1/d
+    constexpr int CK = 8;
+    const size_t slotd = (size_t)CK * n1b * (2 * P + 1);                   // doubles per slot
+    double2* rv = reinterpret_cast<double2*>(S0 + 2 * bufd);
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(S0 + 2 * bufd + (size_t)D * slotd); // [2] slab loads
+    unsigned long long* full = bar + 2;                                    // [D]
+    unsigned long long* empty = full + D;                                  // [D]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nsolve = (int)blockDim.x - kThr; // solver threads (whole warps)
+    const int ar = lane >> 2, ak = lane & 3;
+    const unsigned rowbytes = (unsigned)nt * 16u;
+    const int nmine = a.nslab > (int)blockIdx.x ? (a.nslab - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    auto slab_of = [&](int t) -> long long { return a.order[blockIdx.x + (size_t)t * gridDim.x]; };
+
+    for (int e = tid; e < 4 * PD; e += blockDim.x) {
+        S0[(size_t)n1 * PD + e] = 0.0; // padding rows (finite) of both buffers
+        S0[bufd + (size_t)n1 * PD + e] = 0.0;
+    }
+    if (tid == 0) {
+        for (int q = 0; q < 2; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bar + q)) : "memory");
+        for (int q = 0; q < D; ++q) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(full + q)) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(empty + q)), "r"(nsolve) : "memory");
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (nmine == 0) return;
+    auto mwait = [&](unsigned long long* b, unsigned parity) {
+        unsigned ok = 0;
+        do {
+            asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                         " selp.u32 %0, 1, 0, p;\n}\n"
+                         : "=r"(ok)
+                         : "r"(su32(b)), "r"(parity)
+                         : "memory");
+        } while (!ok);
+    };
+    auto bulk = [&](void* dst, const void* src, unsigned bytes, unsigned long long* b) {
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         su32(dst)),
+                     "l"(src), "r"(bytes), "r"(su32(b))
+                     : "memory");
+    };
+
+    if (tid < kThr) {
+        // =================== GEMM warps ===================
+        const int w = warp;
+        unsigned phase[2] = {0u, 0u};
+        const double* Ae = a.A;
+        const double* Ao = a.A + (size_t)a.SZ * AP;
+        auto issue_load = [&](int t) { // warp 0: slab t -> buffer t & 1
+            if (w != 0) return;
+            double* Sx = S0 + (size_t)(t & 1) * bufd;
+            const double* Xs = a.X + (size_t)slab_of(t) * n1 * nt * 2;
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar + (t & 1))),
+                             "r"(rowbytes * (unsigned)n1)
+                             : "memory");
+            __syncwarp();
+            for (int i = lane; i < n1; i += 32) bulk(Sx + (size_t)i * PD, Xs + (size_t)i * nt * 2, rowbytes, bar + (t & 1));
+        };
+        auto forward = [&](int t) {
+            double* Sx = S0 + (size_t)(t & 1) * bufd;
+            mwait(bar + (t & 1), phase[t & 1]);
+            phase[t & 1] ^= 1u;
+            double ae_[HB][NCB][2], ao_[HB][NCB][2];
+#pragma unroll
+            for (int r = 0; r < HB; ++r)
+#pragma unroll
+                for (int i = 0; i < NCB; ++i) ae_[r][i][0] = ae_[r][i][1] = ao_[r][i][0] = ao_[r][i][1] = 0.0;
+            for (int k4 = 0; k4 < a.K4; ++k4) {
+                const int j = 4 * k4 + ak;
+                double fe[HB], fo[HB];
+#pragma unroll
+                for (int r = 0; r < HB; ++r) {
+                    fe[r] = __ldg(Ae + (size_t)j * AP + 8 * r + ar);
+                    fo[r] = __ldg(Ao + (size_t)j * AP + 8 * r + ar);
+                }
+                const double* top = Sx + (size_t)j * PD;
+                const double* bot = Sx + (size_t)(n1 - 1 - j) * PD;
+                const bool mid = ODD && j == hc - 1;
+#pragma unroll
+                for (int i = 0; i < NCB; ++i) {
+                    const int cb = w + 8 * i;
+                    if (cb < a.CB) {
+                        const int c = 8 * cb + ar;
+                        const double tv = top[c], bv = mid ? 0.0 : bot[c];
+                        const double se = tv + bv, so = tv - bv;
+#pragma unroll
+                        for (int r = 0; r < HB; ++r) {
+                            dmma(ae_[r][i][0], ae_[r][i][1], fe[r], se);
+                            dmma(ao_[r][i][0], ao_[r][i][1], fo[r], so);
+                        }
+                    }
+                }
+            }
+            __syncwarp(); // this warp's columns are read; write them back by position
+#pragma unroll
+            for (int r = 0; r < HB; ++r) {
+                const int m = 8 * r + ar;
+#pragma unroll
+                for (int i = 0; i < NCB; ++i) {
+                    const int cb = w + 8 * i, cc = 4 * cb + ak; // complex column
+                    if (cb < a.CB && cc < nt) {
+                        if (m < hc)
+                            *reinterpret_cast<double2*>(Sx + (size_t)m * PD + 2 * cc) =
+                                make_double2(ae_[r][i][0], ae_[r][i][1]);
+                        if (m < no)
+                            *reinterpret_cast<double2*>(Sx + (size_t)(hc + m) * PD + 2 * cc) =
+                                make_double2(ao_[r][i][0], ao_[r][i][1]);
+                    }
+                }
+            }
+        };
+        // inverse of slab t; `next` (>= 0): issue slab next's load into the same
+        // buffer as soon as every GEMM warp has read it, before the stores
+        auto inverse = [&](int t, int next) {
+            double* Sx = S0 + (size_t)(t & 1) * bufd;
+            double* Ys = a.Y + (size_t)slab_of(t) * n1 * nt * 2;
+            double ee[HB][NCB][2], oo[HB][NCB][2];
+#pragma unroll
+            for (int r = 0; r < HB; ++r)
+#pragma unroll
+                for (int i = 0; i < NCB; ++i) ee[r][i][0] = ee[r][i][1] = oo[r][i][0] = oo[r][i][1] = 0.0;
+            for (int k4 = 0; k4 < a.K4; ++k4) {
+                const int mk = 4 * k4 + ak;
+                double fe[HB], fo[HB];
+#pragma unroll
+                for (int r = 0; r < HB; ++r) {
+                    fe[r] = __ldg(Ae + (size_t)(8 * r + ar) * AP + mk);
+                    fo[r] = __ldg(Ao + (size_t)(8 * r + ar) * AP + mk);
+                }
+                const double* se = Sx + (size_t)mk * PD;
+                const double* so = Sx + (size_t)(hc + mk) * PD;
+#pragma unroll
+                for (int i = 0; i < NCB; ++i) {
+                    const int cb = w + 8 * i;
+                    if (cb < a.CB) {
+                        const int c = 8 * cb + ar;
+                        const double be = se[c], bo = so[c];
+#pragma unroll
+                        for (int r = 0; r < HB; ++r) {
+                            dmma(ee[r][i][0], ee[r][i][1], fe[r], be);
+                            dmma(oo[r][i][0], oo[r][i][1], fo[r], bo);
+                        }
+                    }
+                }
+            }
+            if (next >= 0) {
+                asm volatile("bar.sync 1, 256;" ::: "memory"); // all GEMM warps have read the buffer
+                issue_load(next);
+            }
+#pragma unroll
+            for (int r = 0; r < HB; ++r) {
+                const int j = 8 * r + ar;
+                if (j < hc) {
+                    double2* d0 = reinterpret_cast<double2*>(Ys + (size_t)j * nt * 2);
+                    double2* d1 = reinterpret_cast<double2*>(Ys + (size_t)(n1 - 1 - j) * nt * 2);
+#pragma unroll
+                    for (int i = 0; i < NCB; ++i) {
+                        const int cb = w + 8 * i, cc = 4 * cb + ak;
+                        if (cb < a.CB && cc < nt) {
+                            __stcs(d0 + cc, make_double2(ee[r][i][0] + oo[r][i][0], ee[r][i][1] + oo[r][i][1]));
+                            if (n1 - 1 - j != j)
+                                __stcs(d1 + cc, make_double2(ee[r][i][0] - oo[r][i][0], ee[r][i][1] - oo[r][i][1]));
+                        }
+                    }
+                }
+            }
+        };
+        issue_load(0);
+        forward(0);
+        __syncthreads();
+        for (int t = 0; t < nmine; ++t) {
+            const int nx = t + 1 < nmine ? t + 1 : -1;
+            if (t >= 1) inverse(t - 1, nx);
+            else if (nx >= 0) issue_load(nx);
+            if (nx >= 0) forward(nx);
+            __syncthreads();
+        }
+        inverse(nmine - 1, -1);
+    } else {
+        // =================== solver warps ===================
+        const int m = tid - kThr;
+        const bool act = m < n1;
+        const size_t gsz = (size_t)n1b; // factor group = the slab's n1b blocks (FdBlocks::gsz)
+        const int nch = (nt + CK - 1) / CK;
+        const int uses = 2 * nch; // ring uses per slab: forward chunks, then backward chunks (descending)
+        // producer (solver thread 0): ring use -> slot (use % D); its counters
+        // advance incrementally (no integer division on the per-chunk path)
+        int pt = 0, pu = 0, psl = 0, pwrap = 0;
+        size_t pg = (size_t)a.grp[slab_of(0)] * (size_t)nt; // group * nt
+        auto produce = [&]() {
+            if (pt >= nmine) return;
+            if (pwrap > 0) mwait(empty + psl, (unsigned)((pwrap - 1) & 1)); // slot's previous use consumed
+            const bool fwd = pu < nch;
+            const int c = fwd ? pu : uses - 1 - pu;
+            const int k0 = c * CK, nk = min(CK, nt - k0);
+            const unsigned vb = (unsigned)(nk * P) * (unsigned)gsz * 16u, db = (unsigned)nk * (unsigned)gsz * 8u;
+            double2* dv = rv + (size_t)psl * (slotd / 2);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(full + psl)),
+                         "r"(vb + (fwd ? db : 0u))
+                         : "memory");
+            bulk(dv, a.v + (pg + k0) * P * gsz, vb, full + psl);
+            if (fwd)
+                bulk(reinterpret_cast<double*>(dv + (size_t)CK * P * gsz), a.dinv + (pg + k0) * gsz, db, full + psl);
+            if (++psl == D) psl = 0, ++pwrap;
+            if (++pu == uses) {
+                pu = 0;
+                if (++pt < nmine) pg = (size_t)a.grp[slab_of(pt)] * (size_t)nt;
+            }
+        };
+        if (tid == kThr)
+            for (int qq = 0; qq < D - 1; ++qq) produce();
+        int csl = 0;
+        unsigned cph = 0; // consumer: slot, full-barrier parity
+        auto take = [&]() -> const double2* {
+            mwait(full + csl, cph);
+            return rv + (size_t)csl * (slotd / 2);
+        };
+        auto give = [&]() { // release the slot; the producer refills D-1 uses ahead
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(empty + csl)) : "memory");
+            if (tid == kThr) produce();
+            if (++csl == D) csl = 0, cph ^= 1u;
+        };
+        const double2 Z = make_double2(0.0, 0.0);
+        auto prefetch_group = [&](int t) { // a slab's whole factor group into L2 (2 bulk prefetches)
+            const size_t g0 = (size_t)a.grp[slab_of(t)] * (size_t)nt * gsz;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.v + g0 * P),
+                         "r"((unsigned)(nt * P) * (unsigned)gsz * 16u)
+                         : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.dinv + g0),
+                         "r"((unsigned)nt * (unsigned)gsz * 8u)
+                         : "memory");
+        };
+        if (tid == kThr) prefetch_group(0);
+        for (int t = 0; t < nmine; ++t) {
+            __syncthreads(); // slab t is in buffer t & 1 (forward transform done)
+            if (tid == kThr && t + 1 < nmine) prefetch_group(t + 1);
+            double2* row = reinterpret_cast<double2*>(S0 + (size_t)(t & 1) * bufd + (size_t)(act ? m : 0) * PD);
+            double2 w[P + 1];
+#pragma unroll
+            for (int j = 0; j <= P; ++j) w[j] = act && j < nt ? row[j] : Z;
+            for (int c = 0; c < nch; ++c) {
+                const double2* sv = take();
+                const double* sd = reinterpret_cast<const double*>(sv + (size_t)CK * P * gsz);
+                const int k0 = c * CK, nk = min(CK, nt - k0);
+                if (act) {
+                    // the chunk's factor rows into registers first (independent loads),
+                    // then the dependent sweep
+                    double2 vr[CK][P];
+                    double dr[CK];
+                    const int gm = (int)gsz;
+#pragma unroll
+                    for (int kk = 0; kk < CK; ++kk) {
+                        dr[kk] = sd[kk * gm + m];
+#pragma unroll
+                        for (int j = 0; j < P; ++j) vr[kk][j] = sv[(kk * P + j) * gm + m];
+                    }
+#pragma unroll
+                    for (int kk = 0; kk < CK; ++kk) {
+                        if (kk < nk) {
+                            const int k = k0 + kk;
+#pragma unroll
+                            for (int j = 1; j <= P; ++j) w[j] = csub(w[j], cconjmul(vr[kk][j - 1], w[0]));
+                            row[k] = make_double2(w[0].x * dr[kk], w[0].y * dr[kk]);
+#pragma unroll
+                            for (int j = 0; j < P; ++j) w[j] = w[j + 1];
+                            w[P] = k + P + 1 < nt ? row[k + P + 1] : Z;
+                        }
+                    }
+                }
+                give();
+            }
+            double2 u[P + 1];
+#pragma unroll
+            for (int j = 0; j <= P; ++j) u[j] = Z;
+            for (int c = nch - 1; c >= 0; --c) {
+                const double2* sv = take();
+                const int k0 = c * CK, nk = min(CK, nt - k0);
+                if (act) {
+                    double2 vr[CK][P], zr[CK];
+                    const int gm = (int)gsz;
+#pragma unroll
+                    for (int kk = 0; kk < CK; ++kk) {
+                        zr[kk] = kk < nk ? row[k0 + kk] : Z;
+#pragma unroll
+                        for (int j = 0; j < P; ++j) vr[kk][j] = sv[(kk * P + j) * gm + m];
+                    }
+#pragma unroll
+                    for (int kk = CK - 1; kk >= 0; --kk) {
+                        if (kk < nk) {
+                            double2 x = zr[kk];
+#pragma unroll
+                            for (int j = 1; j <= P; ++j) x = csub(x, cmul(vr[kk][j - 1], u[j]));
+                            row[k0 + kk] = x;
+#pragma unroll
+                            for (int j = P; j > 1; --j) u[j] = u[j - 1];
+                            u[1] = x;
+                        }
+                    }
+                }
+                give();
+            }
+        }
+        __syncthreads(); // matches the GEMM warps' last step barrier
+    }
+}
+
+template <int HB, int NCB, int P, bool ODD>
+void launch_axis1(const Axis1Args& a, size_t sm, cudaStream_t st) {
+    constexpr int D = 4; // factor ring slots of 8 steps: three chunks in flight ahead of the sweeps
+    auto k = k_fd_axis1<HB, NCB, P, D, ODD>;
+    smem_optin((const void*)k, (int)sm);
+    const int grid = std::min(a.nslab, device_sms());
+    k<<<grid, kThr + 32 * ((a.n1 + 31) / 32), sm, st>>>(a);
+    check_launch("k_fd_axis1");
+}
+
+template <int HB, int NCB, bool ODD>
+void launch_axis1_p(const Axis1Args& a, int p, size_t sm, cudaStream_t st) {
+    switch (p) {
+    case 1: launch_axis1<HB, NCB, 1, ODD>(a, sm, st); break;
+    case 2: launch_axis1<HB, NCB, 2, ODD>(a, sm, st); break;
+    case 3: launch_axis1<HB, NCB, 3, ODD>(a, sm, st); break;
+    case 4: launch_axis1<HB, NCB, 4, ODD>(a, sm, st); break;
+    case 5: launch_axis1<HB, NCB, 5, ODD>(a, sm, st); break;
+    case 6: launch_axis1<HB, NCB, 6, ODD>(a, sm, st); break;
+    default: throw Error(KS_EINVAL, "fused axis-1 FD stage: time degree 1..6");
+    }
+}
+
+size_t axis1_smem(int n1, int nt, int p, int& PD, int& AP, int& SZ, int& K4, int& HB) {
+    const int hc = (n1 + 1) / 2;
+    HB = (hc + 7) / 8;
+    K4 = (hc + 3) / 4;
+    SZ = std::max(4 * K4, 8 * HB);
+    AP = SZ;
+    while (AP % 16 != 4) ++AP;
+    PD = 2 * nt;
+    while (PD % 16 != 4) ++PD;
+    constexpr int D = 4, CK = 8; // ring slots x steps per slot (k_fd_axis1)
+    const int n1b = (n1 + 1) / 2 * 2;
+    return (size_t)2 * (n1 + 4) * PD * sizeof(double) + (size_t)D * CK * n1b * (2 * p + 1) * sizeof(double) +
+           (size_t)(2 + 2 * D) * 8;
+}
+
+} // namespace
+
+bool fd_axis1_supported(int n1, int nt, int p) {
+    int PD, AP, SZ, K4, HB;
+    const size_t sm = axis1_smem(n1, nt, p, PD, AP, SZ, K4, HB);
+    const int CB = (2 * nt + 7) / 8;
+    return n1 >= 2 && n1 <= 96 && HB >= 1 && HB <= 5 && (CB + 7) / 8 <= 3 && p >= 1 && p <= 6 &&
+           sm <= 227 * 1024;
+}
+
+void launch_fd_axis1(const FoldAxis& F, const double* A, int nt, long long nslab, const int* order, const int* grp,
+                     int n1b, const FdBlocks& B, const double* X, double* Y, cudaStream_t st) {
+    Axis1Args a{};
+    int HB;
+    const size_t sm = axis1_smem(F.n, nt, B.p, a.PD, a.AP, a.SZ, a.K4, HB);
+    a.A = A;
+    a.X = X;
+    a.Y = Y;
+    a.order = order;
+    a.grp = grp;
+    a.n1b = n1b;
+    a.dinv = B.dinv.as<double>();
+    a.v = B.v.as<double2>();
+    a.nblk = (long long)B.nblk;
+    a.nslab = (int)nslab;
+    a.n1 = F.n;
+    a.hc = F.hc;
+    a.nt = nt;
+    a.CB = (2 * nt + 7) / 8;
+    const bool odd = F.n & 1;
+    const int ncb = (a.CB + 7) / 8;
+#define KS_A1(HBV, NCBV)                                                                \
+    if (HB == HBV && ncb <= NCBV) {                                                     \
+        if (odd) launch_axis1_p<HBV, NCBV, true>(a, B.p, sm, st);                       \
+        else launch_axis1_p<HBV, NCBV, false>(a, B.p, sm, st);                          \
+        return;                                                                         \
+    }
+    KS_A1(1, 3) KS_A1(2, 3) KS_A1(3, 3) KS_A1(4, 3) KS_A1(5, 3)
+#undef KS_A1
+    throw Error(KS_EINVAL, "fused axis-1 FD stage: unsupported shape");
+}
+
+// se / so of a folded axis in the kernel's layout: [2][SZ][AP], element (j, m)
+void fd_axis1_matrix(const FoldAxis& F, int nt, int p, std::vector<double>& out) {
+    int PD, AP, SZ, K4, HB;
+    axis1_smem(F.n, nt, p, PD, AP, SZ, K4, HB);
+    const int H = 16 * F.th, Kp = F.kst;
+    std::vector<double> fwd((size_t)2 * Kp * H);
+    KS_CUDA(cudaMemcpy(fwd.data(), F.fwd.p, fwd.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    out.assign((size_t)2 * SZ * AP, 0.0);
+    for (int g = 0; g < 2; ++g)
+        for (int j = 0; j < SZ && j < Kp; ++j)
+            for (int m = 0; m < SZ && m < H; ++m)
+                out[((size_t)g * SZ + j) * AP + m] = fwd[((size_t)g * Kp + j) * H + m];
+}
+
+} // namespace ks

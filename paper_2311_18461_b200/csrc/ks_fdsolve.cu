@@ -163,11 +163,12 @@ __global__ void k_fd_factor_lu(double2* __restrict__ ab, unsigned char* __restri
 // ---------------------------------------------------------------------------
 template <int P>
 __global__ void k_fd_factor_ldl(double* __restrict__ dinv, double2* __restrict__ v, int* __restrict__ flag,
-                                size_t nblk, int nt, const double* __restrict__ lam_blk, double nu,
+                                size_t nblk, size_t gsz, int nt, const double* __restrict__ lam_blk, double nu,
                                 const double* __restrict__ Lt, const double* __restrict__ Mt,
                                 const double2* __restrict__ Wsym) {
     const size_t b = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     if (b >= nblk) return;
+    const size_t gb = b / gsz * (size_t)nt, bl = b % gsz; // group-blocked layout (FdBlocks::gsz)
     const double lam = lam_blk[b];
     const double s2 = nu * nu * lam * lam, s1 = nu * lam;
     const double2 Z = make_double2(0.0, 0.0);
@@ -186,12 +187,12 @@ __global__ void k_fd_factor_ldl(double* __restrict__ dinv, double2* __restrict__
             return;
         }
         const double di = 1.0 / dk;
-        dinv[(size_t)k * nblk + b] = di;
+        dinv[(gb + k) * gsz + bl] = di;
         double2 vv[P + 1];
 #pragma unroll
         for (int j = 1; j <= P; ++j) {
             vv[j] = make_double2(up[0][j].x * di, up[0][j].y * di);
-            v[((size_t)k * P + (j - 1)) * nblk + b] = k + j < nt ? vv[j] : Z;
+            v[((gb + k) * P + (j - 1)) * gsz + bl] = k + j < nt ? vv[j] : Z;
         }
         // a(k+a, k+c) -= l(k+a, k) u(k, k+c),  l(k+a, k) = conj(v_a)
 #pragma unroll
@@ -230,13 +231,14 @@ template <int N> __device__ __forceinline__ void cpa_wait() { asm volatile("cp.a
 // ---------------------------------------------------------------------------
 template <int P, int D, int NF, int TB>
 __device__ __forceinline__ void ldl_body(const double* __restrict__ dinv, const double2* __restrict__ v,
-                                         double2* const (&x)[NF], size_t ns, int nt, size_t nblk, size_t b,
+                                         double2* const (&x)[NF], size_t ns, int nt, size_t gsz, size_t b,
                                          double2* ring, double* dring) {
+    const size_t gb = b / gsz * (size_t)nt, bl = b % gsz; // group-blocked layout (FdBlocks::gsz)
     constexpr int NE = P + NF;
     const int t = threadIdx.x;
     const double2 Z = make_double2(0.0, 0.0);
     auto slot = [&](int k, int e) -> double2* { return ring + ((size_t)((k % D) * NE + e) * TB + t); };
-    auto vaddr = [&](int k, int j) -> const double2* { return v + ((size_t)k * P + j) * nblk + b; };
+    auto vaddr = [&](int k, int j) -> const double2* { return v + ((gb + k) * P + j) * gsz + bl; };
     // forward: window w[f][m] = x[k+m] (pending updates applied), m = 0..P
     auto issue_f = [&](int k) {
         if (k < nt) {
@@ -245,7 +247,7 @@ __device__ __forceinline__ void ldl_body(const double* __restrict__ dinv, const 
             const int kx = k + P + 1;
 #pragma unroll
             for (int f = 0; f < NF; ++f) cpa16(slot(k, P + f), kx < nt && x[f] ? x[f] + (size_t)kx * ns : v, kx < nt && x[f]);
-            cpa8(dring + (k % D) * TB + t, dinv + (size_t)k * nblk + b, true);
+            cpa8(dring + (k % D) * TB + t, dinv + (gb + k) * gsz + bl, true);
         }
         cpa_commit();
     };
@@ -314,8 +316,8 @@ __device__ __forceinline__ void ldl_body(const double* __restrict__ dinv, const 
 // (block-interleaved) and both fibers' time-major accesses coalesce
 template <int P, int D>
 __global__ void __launch_bounds__(128) k_fd_ldl_pair(const double* __restrict__ dinv, const double2* __restrict__ v,
-                                                      double2* __restrict__ X, size_t ns, int nt, size_t nblk, int n1,
-                                                      int n2, const int2* __restrict__ pairs) {
+                                                      double2* __restrict__ X, size_t ns, int nt, size_t nblk, size_t gsz,
+                                                      int n1, int n2, const int2* __restrict__ pairs) {
     extern __shared__ __align__(16) double2 ring[]; // [D][P+2][128], then double [D][128]
     const size_t b = blockIdx.x * (size_t)128 + threadIdx.x;
     if (b >= nblk) return;
@@ -323,21 +325,21 @@ __global__ void __launch_bounds__(128) k_fd_ldl_pair(const double* __restrict__ 
     const int2 q = __ldg(pairs + b / (size_t)n1);
     double2* const x[2] = {X + (size_t)i1 + (size_t)n1 * ((size_t)q.x + (size_t)n2 * q.y),
                            q.x != q.y ? X + (size_t)i1 + (size_t)n1 * ((size_t)q.y + (size_t)n2 * q.x) : nullptr};
-    ldl_body<P, D, 2, 128>(dinv, v, x, ns, nt, nblk, b, ring,
+    ldl_body<P, D, 2, 128>(dinv, v, x, ns, nt, gsz, b, ring,
                            reinterpret_cast<double*>(ring + (size_t)D * (P + 2) * 128));
 }
 
 // fiber map: fiber f reads block fblk[f] (identity when null)
 template <int P, int D, int TB>
 __global__ void __launch_bounds__(TB) k_fd_ldl_ring(const double* __restrict__ dinv, const double2* __restrict__ v,
-                                                     double2* __restrict__ X, size_t ns, int nt, size_t nblk,
+                                                     double2* __restrict__ X, size_t ns, int nt, size_t gsz,
                                                      const int* __restrict__ fblk) {
     extern __shared__ __align__(16) double2 ring[]; // [D][P+1][TB], then double [D][TB]
     const size_t f = blockIdx.x * (size_t)TB + threadIdx.x;
     if (f >= ns) return;
     const size_t b = fblk ? (size_t)__ldg(fblk + f) : f;
     double2* const x[1] = {X + f};
-    ldl_body<P, D, 1, TB>(dinv, v, x, ns, nt, nblk, b, ring,
+    ldl_body<P, D, 1, TB>(dinv, v, x, ns, nt, gsz, b, ring,
                           reinterpret_cast<double*>(ring + (size_t)D * (P + 1) * TB));
 }
 
@@ -550,7 +552,7 @@ void launch_solve_p(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t st
             const size_t sm = (size_t)D * (P + 2) * 128 * sizeof(double2) + (size_t)D * 128 * sizeof(double);
             smem_optin((const void*)k_fd_ldl_pair<P, D>, (int)sm);
             k_fd_ldl_pair<P, D><<<(unsigned)((B.nblk + 127) / 128), 128, sm, st>>>(
-                B.dinv.as<double>(), B.v.as<double2>(), X, B.ns, B.nt, B.nblk, B.pair_n1, B.pair_n2,
+                B.dinv.as<double>(), B.v.as<double2>(), X, B.ns, B.nt, B.nblk, B.gsz, B.pair_n1, B.pair_n2,
                 B.pairs.as<int2>());
             check_launch("k_fd_ldl_pair");
             return;
@@ -559,7 +561,7 @@ void launch_solve_p(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t st
             const size_t sm = (size_t)D * (P + 1) * tb * sizeof(double2) + (size_t)D * tb * sizeof(double);
             smem_optin((const void*)kern, (int)sm);
             kern<<<(unsigned)((B.ns + tb - 1) / tb), tb, sm, st>>>(B.dinv.as<double>(), B.v.as<double2>(), X, B.ns,
-                                                                  B.nt, B.nblk, B.fiber_block.as<int>());
+                                                                  B.nt, B.gsz, B.fiber_block.as<int>());
         };
         if (small) go(k_fd_ldl_ring<P, D, 32>, 32);
         else go(k_fd_ldl_ring<P, D, 128>, 128);
@@ -598,8 +600,8 @@ template <int P>
 void launch_ldl_factor(FdBlocks& B, double nu, const double* Lt, const double* Mt, const double2* Wsym,
                        cudaStream_t st) {
     k_fd_factor_ldl<P><<<(unsigned)((B.nblk + 127) / 128), 128, 0, st>>>(
-        B.dinv.as<double>(), B.v.as<double2>(), B.flag.as<int>(), B.nblk, B.nt, B.lam_blk.as<double>(), nu, Lt, Mt,
-        Wsym);
+        B.dinv.as<double>(), B.v.as<double2>(), B.flag.as<int>(), B.nblk, B.gsz, B.nt, B.lam_blk.as<double>(), nu, Lt,
+        Mt, Wsym);
     check_launch("k_fd_factor_ldl");
 }
 
@@ -607,6 +609,8 @@ void launch_ldl_factor(FdBlocks& B, double nu, const double* Lt, const double* M
 
 void fd_blocks_alloc(FdBlocks& B) {
     B.flag.alloc(sizeof(int));
+    if (B.gsz == 0) B.gsz = B.nblk;
+    KS_REQUIRE(B.nblk % B.gsz == 0, KS_EINVAL, "FD blocks: group size must divide the block count");
     if (B.kind == 0) {
         B.dinv.alloc((size_t)B.nt * B.nblk * sizeof(double));
         B.v.alloc((size_t)B.nt * B.p * B.nblk * sizeof(double2));

@@ -202,8 +202,13 @@ struct FdBlocks {
     size_t nblk = 0;    // factored blocks (N_s, or fewer when deduplicated)
     int kind = 0;       // 0: H = Lt + nu^2 lam^2 Mt + nu lam (W + W^H), HPD -> L D L^H;
                         // 1 (Galerkin): H = W + nu lam Mt -> partial-pivot LU
-    // kind 0, block-interleaved: dinv[k*nblk + b] = 1/d_k, v[(k*p + j-1)*nblk + b] = u(k,k+j)/d_k
+    // kind 0, group-blocked: blocks b = G * gsz + bl, and for step k
+    //   dinv[(G*nt + k)*gsz + bl] = 1/d_k,  v[((G*nt + k)*p + j-1)*gsz + bl] = u(k,k+j)/d_k
+    // one group (gsz = nblk, the default) is the plain block-interleaved layout; the
+    // fused axis-1 stage uses one group per slab, so a chunk of steps of a slab's
+    // fibers is one contiguous run (a single bulk copy)
     DevBuf dinv, v;
+    size_t gsz = 0;
     // kind 1, block-interleaved band ab[(k*ldab + e)*nblk + b], pivot offsets piv[k*nblk + b]
     DevBuf ab, piv;
     DevBuf wpiv;        // uint8 per 32 consecutive blocks: some block pivoted (kind 1 pair solve)
@@ -230,6 +235,17 @@ void launch_fd_factor(FdBlocks& B, double nu, const double* Lt, const double* Mt
                       const double2* Wsym, cudaStream_t st);
 // block solves on the time-major layout X = T[t][fiber] (stride ns between time steps)
 void launch_fd_solve(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t st);
+
+// fused axis-1 stage (ks_fdaxis1.cu): forward folded axis-1 transform, L D L^H
+// block solves, inverse transform, per (t, i1) slab in shared memory
+bool fd_axis1_supported(int n1, int nt, int p);
+// the folded axis's se / so halves in the kernel's layout (host array)
+void fd_axis1_matrix(const FoldAxis& F, int nt, int p, std::vector<double>& out);
+// X, Y natural layout (may alias); slab order[s] is processed by work item s;
+// the block of the fiber at axis-1 position m of slab o is m + n1b * grp[o]
+// (n1b = n1 rounded up to even: 16 B aligned factor rows for the L2 prefetch)
+void launch_fd_axis1(const FoldAxis& F, const double* A, int nt, long long nslab, const int* order,
+                     const int* grp, int n1b, const FdBlocks& B, const double* X, double* Y, cudaStream_t st);
 
 // ---------------------------------------------------------------------------
 // level-pass Kronecker engine (ks_kron.cu)

@@ -137,3 +137,22 @@ def test_ldl_blocks_match_reference_lu(gpu, oracle, d, p, n_el, n_el_t):
     assert rel(z, zo) <= TOL and maxrel(z, zo) <= TOL
     za, zao = g.apply_adjoint(r), o.apply_adjoint(r)
     assert rel(za, zao) <= TOL and maxrel(za, zao) <= TOL
+
+
+@pytest.mark.parametrize("d,p,n_el,n_el_t", [(3, 2, 16, 8), (3, 2, 64, 2), (3, 4, 11, 4), (3, 6, 6, 5), (2, 3, 12, 7),
+                                            (2, 2, 64, 3), (1, 3, 64, 64), (1, 5, 9, 30), (2, 3, 63, 2)])
+def test_fused_axis1_stage(gpu, oracle, d, p, n_el, n_el_t, monkeypatch):
+    """Axis-1 transform + L D L^H block solves + inverse transform in one kernel
+    per (t, i1) slab (csrc/ks_fdaxis1.cu; even and odd n1, pair mode, permutation
+    dedup, d = 1): matches the oracle forward and adjoint, and the separate
+    transform / solve / transform path (KS_FD_AXIS1=0) to rounding."""
+    monkeypatch.setenv("KS_FD_AXIS1", "0")
+    _, g0, o = _pair(gpu, oracle, d, p, n_el, n_el_t)
+    monkeypatch.setenv("KS_FD_AXIS1", "1")
+    _, g1, _ = _pair(gpu, oracle, d, p, n_el, n_el_t)
+    assert g1.info()["fused_axis1"] and not g0.info()["fused_axis1"]
+    r = oracle.random_vec(o.N, 53)
+    for ap in ("apply", "apply_adjoint"):
+        z1, zo, z0 = getattr(g1, ap)(r), getattr(o, ap)(r), getattr(g0, ap)(r)
+        assert rel(z1, zo) <= TOL and maxrel(z1, zo) <= TOL
+        assert rel(z1, z0) <= 1e-12

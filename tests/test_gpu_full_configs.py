@@ -37,7 +37,7 @@ JOBS = {
     "restart": (R.restart_job, (2, 3, 8, 8, 5, 1e-15)),
 }
 for _p in range(2, 7):
-    JOBS[f"c4_p{_p}"] = (R.manufactured_job, (2, _p, 128, 128, False))
+    JOBS[f"c4_p{_p}"] = (R.manufactured_job, (2, _p, 128, 128))
 
 
 @pytest.fixture(scope="module")
@@ -107,8 +107,8 @@ def test_c2_manufactured_solve_vs_reference(gpu, ref_results):
     # the same error functional on the reference's own solution: 1e-10
     l2r, enr = Q.error_norms(ref["full"], "sinsin", "sinsin")
     assert abs(l2r - ref["l2"]) <= 1e-10 * ref["l2"] and abs(enr - ref["energy"]) <= 1e-10 * ref["energy"]
-    # end to end (two CG runs that each stop at relres 1e-8): L2 errors to 1e-6
-    assert abs(l2 - ref["l2"]) <= 1e-6 * ref["l2"]
+    # end to end (two CG runs that each stop at relres 1e-8): same discretisation error
+    assert abs(l2 - ref["l2"]) <= 1e-3 * ref["l2"]
 
 
 @pytest.mark.parametrize("p", [2, 3, 4, 5, 6])
@@ -117,8 +117,14 @@ def test_c4_degree_sweep_iterations_vs_reference(gpu, ref_results, p):
     ref = _get(ref_results, f"c4_p{p}")
     print(f"c4 p={p}: iterations gpu {s.iterations} ref {ref['iterations']}; L2 gpu {l2:.6e} ref {ref['l2']:.6e}")
     assert list(ref["dims"]) == prob.reduced_dims()
+    assert _within(rhs, ref["rhs"]) and _within(bnd, ref["bnd"])
     assert s.converged == ref["converged"] and abs(s.iterations - ref["iterations"]) <= 1
-    assert abs(l2 - ref["l2"]) <= 1e-6 * ref["l2"]
+    # the error functional on the reference's own solution: 1e-10
+    l2r, enr = Q.error_norms(ref["full"], "sinsin", "sinsin")
+    assert abs(l2r - ref["l2"]) <= 1e-10 * ref["l2"] and abs(enr - ref["energy"]) <= 1e-10 * ref["energy"]
+    # end to end: two CG runs stopping at relres 1e-8 differ by up to ~1e-8 ||u||,
+    # which at the high degrees' L2 errors (~1e-7) is a 1e-5..1e-3 relative change
+    assert abs(l2 - ref["l2"]) <= 1e-3 * ref["l2"]
 
 
 def test_c5_shape_fd_apply_and_matvec_vs_reference(gpu, oracle, ref_results):
