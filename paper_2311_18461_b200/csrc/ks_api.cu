@@ -107,6 +107,7 @@ struct ks_fd {
     std::vector<std::vector<double>> lam_host;
     std::vector<int> fiber_block; // host copy of the block map (empty = identity)
     bool tm1 = false;             // time-major hand-off on axis 1 (pair mode, folded axis 1)
+    bool posall = false;          // tm1 with position-ordered rows on axes 2..d (ks_xform.cu transforms)
     bool axis1 = false;           // fused axis-1 stage (ks_fdaxis1.cu): transform + solves + transform
     DevBuf A1, order1, grp1;      // its matrix, slab order and per-slab block group
     int n1b = 0;                  // blocks per group (n1 rounded up to even)
@@ -204,6 +205,26 @@ void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStre
             launch();
         }
     };
+    // (posall: axes 2..d on the bulk-copy fed transform, eigen rows by position)
+    auto std_gemm = [&](int l, bool inv, const double* in, double* out) {
+        if (!f->posall) return gemm(inv ? f->At_inv[l - 1] : f->At_fwd[l - 1], l, in, out, 0);
+        size_t stride = 1;
+        for (int k = 0; k < l; ++k) stride *= (size_t)f->dims[k];
+        const size_t outer = f->N / (stride * (size_t)f->dims[l]);
+        auto launch = [&]() { launch_xfold(f->fold[l - 1], inv, in, out, stride, outer, st); };
+        if (ev) {
+            cudaEvent_t a, b;
+            KS_CUDA(cudaEventCreate(&a));
+            KS_CUDA(cudaEventCreate(&b));
+            KS_CUDA(cudaEventRecord(a, st));
+            launch();
+            KS_CUDA(cudaEventRecord(b, st));
+            ev->push_back(a);
+            ev->push_back(b);
+        } else {
+            launch();
+        }
+    };
     if (f->axis1) {
         // forward axes d..2, then axis 1 + block solves + inverse axis 1 in one
         // kernel per slab, then inverse axes 2..d (the order of
@@ -211,7 +232,7 @@ void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStre
         for (int l = d; l >= 2; --l) {
             double* out = bufs[nb];
             nb ^= 1;
-            gemm(f->At_fwd[l - 1], l, cur, out, 0);
+            std_gemm(l, false, cur, out);
             cur = out;
         }
         double* mid = d == 1 ? reinterpret_cast<double*>(z) : const_cast<double*>(cur); // in place
@@ -235,7 +256,7 @@ void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStre
         for (int l = 2; l <= d; ++l) {
             double* out = l == d ? reinterpret_cast<double*>(z) : bufs[nb];
             if (l != d) nb ^= 1;
-            gemm(f->At_inv[l - 1], l, cur, out, 0);
+            std_gemm(l, true, cur, out);
             cur = out;
         }
         return;
@@ -247,14 +268,16 @@ void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStre
         for (int l = d; l >= 1; --l) {
             double* out = bufs[nb];
             nb ^= 1;
-            gemm(f->At_fwd[l - 1], l, cur, out, l == 1 ? 3 : 0);
+            if (l == 1) gemm(f->At_fwd[0], 1, cur, out, 3);
+            else std_gemm(l, false, cur, out);
             cur = out;
         }
         launch_fd_solve(f->blocks, reinterpret_cast<double2*>(const_cast<double*>(cur)), adjoint, st);
         for (int l = 1; l <= d; ++l) {
             double* out = l == d ? reinterpret_cast<double*>(z) : bufs[nb];
             if (l != d) nb ^= 1;
-            gemm(f->At_inv[l - 1], l, cur, out, l == 1 ? 4 : 0);
+            if (l == 1) gemm(f->At_inv[0], 1, cur, out, 4);
+            else std_gemm(l, true, cur, out);
             cur = out;
         }
         return;
@@ -510,6 +533,15 @@ static void fd_create_impl(int kind, int d, const int* dims, double nu, int p_t,
     // position.
     const bool tm1 = pair && f->fold[0].n > 0 && (int)f->fold[0].perm.size() == dims[1];
     f->tm1 = tm1;
+    // tm1 with every spatial axis folded: the transforms on axes 2..d keep their
+    // eigen rows by position too (ks_xform.cu), so the pair blocks are keyed by
+    // (position 2, position 3); needs identical position maps on axes 2 and 3
+    bool posall = tm1 && d == 3;
+    for (int l = 1; l < d && posall; ++l)
+        posall = f->fold[l].n > 0 && (int)f->fold[l].perm.size() == dims[l + 1] && xfold_supported(f->fold[l]);
+    posall = posall && f->fold[1].perm == f->fold[2].perm;
+    if (const char* e = std::getenv("KS_FD_XFOLD")) posall = posall && std::strcmp(e, "0") != 0;
+    f->posall = posall;
     // fused axis-1 stage (least-squares blocks, folded axis 1, slab fits shared
     // memory): blocks numbered by axis-1 position within per-slab groups of n1b.
     // Opt-in (KS_FD_AXIS1=1): measured at c3 0.55 ms against 0.54 ms for the
@@ -536,11 +568,15 @@ static void fd_create_impl(int kind, int d, const int* dims, double nu, int p_t,
                 prs.push_back(make_int2(i2, i3));
             }
         const int nbg = ax1 ? (n1 + 1) / 2 * 2 : n1; // blocks per pair group
+        // position -> eigen-index on axes 2, 3 (identity unless posall), and inverse
+        std::vector<int> perm2(n2), pos2(n2);
+        for (int q = 0; q < n2; ++q) perm2[q] = posall ? f->fold[1].perm[q] : q;
+        for (int q = 0; q < n2; ++q) pos2[perm2[q]] = q;
         lam_blk.resize((size_t)nbg * prs.size());
         for (size_t pp = 0; pp < prs.size(); ++pp)
             for (int p1 = 0; p1 < nbg; ++p1) {
                 // (a padding block repeats the group's last eigenvalue; never solved)
-                const int id[3] = {perm1[std::min(p1, n1 - 1)], prs[pp].x, prs[pp].y};
+                const int id[3] = {perm1[std::min(p1, n1 - 1)], perm2[prs[pp].x], perm2[prs[pp].y]};
                 lam_blk[(size_t)p1 + (size_t)nbg * pp] = ref_sum(id);
             }
         if (ax1) {
@@ -554,8 +590,8 @@ static void fd_create_impl(int kind, int d, const int* dims, double nu, int p_t,
         std::vector<int> fb_dev(f->Ns);
         for (size_t i = 0; i < f->Ns; ++i) {
             const int i1 = (int)(i % n1), i2 = (int)((i / n1) % n2), i3 = (int)(i / ((size_t)n1 * n2));
+            f->fiber_block[i] = pos1[i1] + nbg * pidx[(size_t)pos2[i2] * n2 + pos2[i3]];
             const int pb = nbg * pidx[(size_t)i2 * n2 + i3];
-            f->fiber_block[i] = pos1[i1] + pb;
             fb_dev[i] = i1 + pb;
         }
         B.fiber_block.alloc(f->Ns * sizeof(int)); // adjoint / non-time-major solves

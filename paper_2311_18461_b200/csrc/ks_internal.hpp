@@ -236,6 +236,12 @@ void launch_fd_factor(FdBlocks& B, double nu, const double* Lt, const double* Mt
 // block solves on the time-major layout X = T[t][fiber] (stride ns between time steps)
 void launch_fd_solve(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t st);
 
+// folded transform on the natural layout with POSITION-ordered eigen rows (even
+// eigenvectors first), bulk-copy fed (ks_xform.cu)
+bool xfold_supported(const FoldAxis& F);
+void launch_xfold(const FoldAxis& F, bool inverse, const double* X, double* Y, size_t s_complex, size_t outer,
+                  cudaStream_t st);
+
 // fused axis-1 stage (ks_fdaxis1.cu): forward folded axis-1 transform, L D L^H
 // block solves, inverse transform, per (t, i1) slab in shared memory
 bool fd_axis1_supported(int n1, int nt, int p);
