@@ -206,12 +206,13 @@ void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStre
         }
     };
     // (posall: axes 2..d on the bulk-copy fed transform, eigen rows by position)
-    auto std_gemm = [&](int l, bool inv, const double* in, double* out) {
-        if (!f->posall) return gemm(inv ? f->At_inv[l - 1] : f->At_fwd[l - 1], l, in, out, 0);
+    // mode: 0 natural, 1 / 2 the axis-1 time-major hand-off (forward / inverse)
+    auto std_gemm = [&](int l, bool inv, const double* in, double* out, int mode = 0) {
+        if (!f->posall) return gemm(inv ? f->At_inv[l - 1] : f->At_fwd[l - 1], l, in, out, mode == 0 ? 0 : mode + 2);
         size_t stride = 1;
         for (int k = 0; k < l; ++k) stride *= (size_t)f->dims[k];
         const size_t outer = f->N / (stride * (size_t)f->dims[l]);
-        auto launch = [&]() { launch_xfold(f->fold[l - 1], inv, in, out, stride, outer, st); };
+        auto launch = [&]() { launch_xfold(f->fold[l - 1], inv, in, out, stride, outer, st, mode); };
         if (ev) {
             cudaEvent_t a, b;
             KS_CUDA(cudaEventCreate(&a));
@@ -268,16 +269,14 @@ void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStre
         for (int l = d; l >= 1; --l) {
             double* out = bufs[nb];
             nb ^= 1;
-            if (l == 1) gemm(f->At_fwd[0], 1, cur, out, 3);
-            else std_gemm(l, false, cur, out);
+            std_gemm(l, false, cur, out, l == 1 ? 1 : 0);
             cur = out;
         }
         launch_fd_solve(f->blocks, reinterpret_cast<double2*>(const_cast<double*>(cur)), adjoint, st);
         for (int l = 1; l <= d; ++l) {
             double* out = l == d ? reinterpret_cast<double*>(z) : bufs[nb];
             if (l != d) nb ^= 1;
-            if (l == 1) gemm(f->At_inv[0], 1, cur, out, 4);
-            else std_gemm(l, true, cur, out);
+            std_gemm(l, true, cur, out, l == 1 ? 2 : 0);
             cur = out;
         }
         return;
@@ -536,7 +535,7 @@ static void fd_create_impl(int kind, int d, const int* dims, double nu, int p_t,
     // tm1 with every spatial axis folded: the transforms on axes 2..d keep their
     // eigen rows by position too (ks_xform.cu), so the pair blocks are keyed by
     // (position 2, position 3); needs identical position maps on axes 2 and 3
-    bool posall = tm1 && d == 3;
+    bool posall = tm1 && d == 3 && xfold_supported(f->fold[0]);
     for (int l = 1; l < d && posall; ++l)
         posall = f->fold[l].n > 0 && (int)f->fold[l].perm.size() == dims[l + 1] && xfold_supported(f->fold[l]);
     posall = posall && f->fold[1].perm == f->fold[2].perm;

@@ -239,8 +239,10 @@ void launch_fd_solve(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t s
 // folded transform on the natural layout with POSITION-ordered eigen rows (even
 // eigenvectors first), bulk-copy fed (ks_xform.cu)
 bool xfold_supported(const FoldAxis& F);
+// mode 0: natural in / out; 1 (axis 1, forward): time-major out T[t][pos + n1*o];
+// 2 (axis 1, inverse): time-major in (s_complex = n_t, outer = N_s / n1)
 void launch_xfold(const FoldAxis& F, bool inverse, const double* X, double* Y, size_t s_complex, size_t outer,
-                  cudaStream_t st);
+                  cudaStream_t st, int mode = 0);
 
 // fused axis-1 stage (ks_fdaxis1.cu): forward folded axis-1 transform, L D L^H
 // block solves, inverse transform, per (t, i1) slab in shared memory

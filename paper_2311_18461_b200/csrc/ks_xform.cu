@@ -62,8 +62,13 @@ struct XArgs {
     const double* X;
     double* Y;
     long long s, outer, Q, ntiles;
+    long long Ns;    // MODE 1 / 2: spatial size of the time-major layout T[t][pos + n * o]
     int n, hc, Kst, H, K4, AP;
 };
+// MODE 0: natural in / out. MODE 1 (axis 1, forward): natural in, time-major
+// out T[t][pos + n1 * o]. MODE 2 (axis 1, inverse): time-major in, natural out
+// (rows are contiguous per column there, so the stages load with per-thread
+// 16 B cp.async completing on the stage mbarrier instead of row bulk copies).
 
 // NF 8-double column fragments per consumer warp: 2 (8 consumer warps) for
 // short axes, 1 (16 warps) for long ones (HB > 5: 2 x HB x NF accumulators).
@@ -74,7 +79,7 @@ template <int NF> struct XCfg {
     static constexpr int kCons = 16 / NF;
     static constexpr int kThr = kCons * 32;
 };
-template <int HB, int KS, bool INV, bool ODD, int NF>
+template <int HB, int KS, bool INV, bool ODD, int NF, int MODE>
 __global__ void __launch_bounds__(XCfg<NF>::kThr, NF == 2 ? 2 : 1) k_xfold(XArgs a) {
     constexpr int kCons = XCfg<NF>::kCons, kXThr = XCfg<NF>::kThr;
     constexpr int SR = 8 * KS;   // stage rows: 4 KS top + 4 KS bottom
@@ -96,7 +101,8 @@ __global__ void __launch_bounds__(XCfg<NF>::kThr, NF == 2 ? 2 : 1) k_xfold(XArgs
     for (int e = tid; e < NST * SR * kBP; e += kXThr) Bs[e] = 0.0; // rows never loaded stay finite
     if (tid == 0) {
         for (int q = 0; q < NST; ++q) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(full + q)), "r"(kCons < SR ? kCons : SR)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(full + q)),
+                         "r"(MODE == 2 ? kXThr : (kCons < SR ? kCons : SR))
                          : "memory");
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(empty + q)), "r"(kCons) : "memory");
         }
@@ -116,7 +122,47 @@ __global__ void __launch_bounds__(XCfg<NF>::kThr, NF == 2 ? 2 : 1) k_xfold(XArgs
     unsigned plap = 0;
     unsigned pq0 = blockIdx.x * (unsigned)kTC;
     const unsigned su = (unsigned)s, Qu = (unsigned)a.Q;
+    // MODE 2: every thread loads 16 B elements (row e % SR, column e / SR) of
+    // the stage; its columns' (o, t) are fixed per tile
+    constexpr int EPT = MODE == 2 ? SR * kTC / kXThr : 1;
+    unsigned tin_off[EPT];
+    bool tin_ok[EPT];
+    int tin_tile = -1;
+    auto produce_tin = [&]() {
+        if (pit >= my_tiles) return;
+        if (plap > 0) mwait(empty + pst, (plap - 1) & 1u);
+        if (tin_tile != pit) {
+#pragma unroll
+            for (int j = 0; j < EPT; ++j) {
+                const int col = (tid + kXThr * j) / SR;
+                const unsigned q = pq0 + (unsigned)col;
+                tin_ok[j] = q < Qu;
+                const unsigned o = q / su, t = q - o * su;
+                // T offset of (t, pos 0, o) in complex units (fits 32 bits: N < 2^31)
+                tin_off[j] = tin_ok[j] ? (unsigned)((size_t)t * (size_t)a.Ns + (size_t)n * o) : 0u;
+            }
+            tin_tile = pit;
+        }
+#pragma unroll
+        for (int j = 0; j < EPT; ++j) {
+            const int e = tid + kXThr * j, row = e % SR, col = e / SR;
+            const int pos = row < 4 * KS ? pg * 4 * KS + row : hc + pg * 4 * KS + (row - 4 * KS);
+            const bool v = tin_ok[j] && pos < n;
+            const double* src = v ? a.X + 2 * ((size_t)tin_off[j] + pos) : a.X;
+            const unsigned dst = su32(Bs + ((size_t)pst * SR + row) * kBP + 2 * col);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 16 : 0)
+                         : "memory");
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(su32(full + pst)) : "memory");
+        if (++pst == NST) pst = 0, ++plap;
+        if (++pg == nstg) {
+            pg = 0;
+            ++pit;
+            pq0 += gridDim.x * (unsigned)kTC;
+        }
+    };
     auto produce = [&]() {
+        if (MODE == 2) return produce_tin();
         if (warp >= PW || pit >= my_tiles) return;
         if (plap > 0) mwait(empty + pst, (plap - 1) & 1u);
         const unsigned ncol = min((unsigned)kTC, Qu - pq0);
@@ -221,6 +267,17 @@ __global__ void __launch_bounds__(XCfg<NF>::kThr, NF == 2 ? 2 : 1) k_xfold(XArgs
             const unsigned q = (unsigned)q0 + (unsigned)cc;
             if (q >= (unsigned)a.Q) continue;
             const unsigned o = q / (unsigned)s, rr = q - o * (unsigned)s;
+            if (MODE == 1) { // T[t = rr][pos + n * o]
+                double* tb = a.Y + 2 * ((size_t)rr * (size_t)a.Ns + (size_t)n * o);
+#pragma unroll
+                for (int r = 0; r < HB; ++r) {
+                    const int m = 8 * r + ar;
+                    if (m < hc) __stcs(reinterpret_cast<double2*>(tb + 2 * m), make_double2(ce[r][f][0], ce[r][f][1]));
+                    if (m < no)
+                        __stcs(reinterpret_cast<double2*>(tb + 2 * (hc + m)), make_double2(co[r][f][0], co[r][f][1]));
+                }
+                continue;
+            }
             double* yb = a.Y + 2 * ((size_t)o * n * s + rr);
 #pragma unroll
             for (int r = 0; r < HB; ++r) {
@@ -243,7 +300,7 @@ __global__ void __launch_bounds__(XCfg<NF>::kThr, NF == 2 ? 2 : 1) k_xfold(XArgs
     }
 }
 
-template <int HB, int KS, bool INV, bool ODD>
+template <int HB, int KS, bool INV, bool ODD, int MODE>
 void launch_x(const XArgs& a, cudaStream_t st) {
     constexpr int NF = HB <= 5 ? 2 : 1, kXThr = XCfg<NF>::kThr;
     constexpr int SR = 8 * KS, NST = KS == 2 ? 4 : 8;
@@ -251,7 +308,7 @@ void launch_x(const XArgs& a, cudaStream_t st) {
     const size_t sm = ((size_t)2 * kpad * a.AP + (size_t)NST * SR * kBP) * sizeof(double) + (size_t)2 * NST * 8;
     KS_REQUIRE(sm <= 227 * 1024, KS_EINVAL, "folded transform: axis too long");
     KS_REQUIRE(a.Q < (1LL << 31), KS_EINVAL, "folded transform: more than 2^31 columns");
-    auto k = k_xfold<HB, KS, INV, ODD, NF>;
+    auto k = k_xfold<HB, KS, INV, ODD, NF, MODE>;
     smem_optin((const void*)k, (int)sm);
     const int per_sm = 2 * sm <= 227 * 1024 ? 2 : 1;
     const unsigned g = (unsigned)std::min<long long>(a.ntiles, (long long)device_sms() * per_sm);
@@ -259,16 +316,16 @@ void launch_x(const XArgs& a, cudaStream_t st) {
     check_launch("k_xfold");
 }
 
-template <int HB, bool INV>
+template <int HB, bool INV, int MODE>
 void launch_x_hb(const XArgs& a, cudaStream_t st) {
     // short axes: 8-row stages (two k4 steps); long ones: 4-row stages (less padding)
     const bool odd = a.n & 1;
     if (HB <= 4) {
-        if (odd) launch_x<HB, 2, INV, true>(a, st);
-        else launch_x<HB, 2, INV, false>(a, st);
+        if (odd) launch_x<HB, 2, INV, true, MODE>(a, st);
+        else launch_x<HB, 2, INV, false, MODE>(a, st);
     } else {
-        if (odd) launch_x<HB, 1, INV, true>(a, st);
-        else launch_x<HB, 1, INV, false>(a, st);
+        if (odd) launch_x<HB, 1, INV, true, MODE>(a, st);
+        else launch_x<HB, 1, INV, false, MODE>(a, st);
     }
 }
 
@@ -277,7 +334,7 @@ void launch_x_hb(const XArgs& a, cudaStream_t st) {
 bool xfold_supported(const FoldAxis& F) { return F.n >= 2 && (F.hc + 7) / 8 <= 10; }
 
 void launch_xfold(const FoldAxis& F, bool inverse, const double* X, double* Y, size_t s_complex, size_t outer,
-                  cudaStream_t st) {
+                  cudaStream_t st, int mode) {
     if (s_complex == 0 || outer == 0) return;
     XArgs a{};
     a.A = (inverse ? F.inv : F.fwd).as<double>();
@@ -295,10 +352,15 @@ void launch_xfold(const FoldAxis& F, bool inverse, const double* X, double* Y, s
     const int HB = (F.hc + 7) / 8;
     a.AP = 8 * HB + 4;
     while (a.AP % 16 != 4) ++a.AP;
+    a.Ns = (long long)F.n * a.outer;
+    KS_REQUIRE(mode == 0 || (mode == 1 && !inverse) || (mode == 2 && inverse), KS_EINVAL,
+               "folded transform: time-major output is forward-only, input inverse-only");
 #define KS_XB(V)                                                                 \
     case V:                                                                      \
-        if (inverse) launch_x_hb<V, true>(a, st);                                \
-        else launch_x_hb<V, false>(a, st);                                       \
+        if (mode == 2) launch_x_hb<V, true, 2>(a, st);                           \
+        else if (mode == 1) launch_x_hb<V, false, 1>(a, st);                     \
+        else if (inverse) launch_x_hb<V, true, 0>(a, st);                        \
+        else launch_x_hb<V, false, 0>(a, st);                                    \
         break;
     switch (HB) {
         KS_XB(1) KS_XB(2) KS_XB(3) KS_XB(4) KS_XB(5) KS_XB(6) KS_XB(7) KS_XB(8) KS_XB(9) KS_XB(10)
