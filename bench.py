@@ -432,6 +432,74 @@ def run_sharded(args, rank, ws, local, dist):
     dist.destroy_process_group()
 
 
+def solve_roofline_s(dims, p, n, iters, fp64_peak, hbm_peak):
+    """SURVEY 8(d) "Solve": iterations x (t_FD + t_mv + t_vec) at the roofline,
+    t_vec = 144 B/DOF/iteration of BLAS-1 traffic (dots fused into the operators)."""
+    d = len(dims) - 1
+    t_fd = max(fd_flops_per_dof(dims, p) * n / (fp64_peak * 1e12), 32.0 * n / (hbm_peak * 1e9))
+    t_mv = max(matvec_flops_per_dof(d, p) * n / (fp64_peak * 1e12), 32.0 * n / (hbm_peak * 1e9))
+    t_vec = 144.0 * n / (hbm_peak * 1e9)
+    return iters * (t_fd + t_mv + t_vec)
+
+
+def config_leg(ks, cfg, K, W, local, fp64_peak, hbm_peak, solve=True):
+    """One BASELINE config on this GPU: FD apply and matvec (device-resident,
+    CUDA events), their SURVEY 8(d) rooflines, and a full FD-PCG solve to 1e-8
+    with its solve roofline."""
+    d, p, n_el, n_el_t = CONFIGS[cfg]
+    t0 = time.perf_counter()
+    prob = ks.SpaceTimeProblem.uniform(d, p, n_el, n_el_t)
+    P = ks.FDPreconditioner(prob, device=local)
+    A = ks.assemble_system_operator(prob, device=local)
+    setup_s = time.perf_counter() - t0
+    dims, n = prob.reduced_dims(), prob.N_dof
+    r = ks.DeviceVector.from_host(rhs(n))
+    z = ks.DeviceVector(n)
+    P.time(r, z, W, flush=False)
+    ms_fd, ms_tr = P.time(r, z, K, flush=False)
+    A.time(r, z, W, flush=False)
+    ms_mv = A.time(r, z, K, flush=False)
+    fd_roof = max(fd_flops_per_dof(dims, p) * n / (fp64_peak * 1e12), 32.0 * n / (hbm_peak * 1e9))
+    mv_roof = max(matvec_flops_per_dof(d, p) * n / (fp64_peak * 1e12), 32.0 * n / (hbm_peak * 1e9))
+    out = {"dims": dims, "dofs": n, "setup_s": setup_s,
+           "fd_apply": {"ms": ms_fd, "dof_per_s": n / (ms_fd * 1e-3), "roofline_ms": fd_roof * 1e3,
+                        "frac_of_roofline": fd_roof * 1e3 / ms_fd, "transform_ms_per_apply": ms_tr,
+                        "info": P.info()},
+           "matvec": {"ms": ms_mv, "dof_per_s": n / (ms_mv * 1e-3), "roofline_ms": mv_roof * 1e3,
+                      "frac_of_roofline": mv_roof * 1e3 / ms_mv, "plan": A.plan_info(),
+                      "hbm_gbs_effective": 32.0 * n / (ms_mv * 1e-3) / 1e9}}
+    if solve:
+        b = ks.DeviceVector.from_host(rhs(n))
+        rep0 = ks.pcg(A, P, b, ks.PcgOptions(1e-8, 200))  # first solve allocates the work vectors
+        rep = ks.pcg(A, P, b, ks.PcgOptions(1e-8, 200))
+        roof = solve_roofline_s(dims, p, n, rep.iterations, fp64_peak, hbm_peak)
+        out["solve"] = {"iterations": rep.iterations, "converged": rep.converged, "seconds": rep.solve_seconds,
+                        "first_solve_seconds": rep0.solve_seconds,
+                        "final_relres": rep.res_history[-1] if rep.res_history else None,
+                        "roofline_s": roof, "frac_of_roofline": roof / rep.solve_seconds,
+                        "roofline_basis": "SURVEY 8(d) Solve: iterations x (FD + matvec rooflines + 144 B/DOF BLAS-1)"}
+    return out, P, A, prob
+
+
+def latency_leg(ks, cfg, local):
+    """Latency-bound configs (c1): 100 back-to-back FD applications eager and as
+    CUDA-graph replays, plus one full solve (BASELINE configs[0] workload)."""
+    d, p, n_el, n_el_t = CONFIGS[cfg]
+    prob = ks.SpaceTimeProblem.uniform(d, p, n_el, n_el_t)
+    P = ks.FDPreconditioner(prob, device=local)
+    A = ks.assemble_system_operator(prob, device=local)
+    n = prob.N_dof
+    r = ks.DeviceVector.from_host(rhs(n))
+    z = ks.DeviceVector(n)
+    eager = P.latency(r, z, 100, graph=False)
+    graph = P.latency(r, z, 100, graph=True)
+    ks.pcg(A, P, r, ks.PcgOptions(1e-8, 200))
+    rep = ks.pcg(A, P, r, ks.PcgOptions(1e-8, 200))
+    return {"dofs": n, "dims": prob.reduced_dims(), "fd_apply_us_eager": eager * 1e3,
+            "fd_apply_us_graph": graph * 1e3, "applies": 100,
+            "solve": {"iterations": rep.iterations, "converged": rep.converged, "seconds": rep.solve_seconds}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -441,6 +509,7 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the c5 / c1 / c2 legs")
     ap.add_argument("--transport", default="auto", choices=["auto", "peer", "nccl"],
                     help="sharded FD exchange (N > 1): peer memory or NCCL all-to-all")
     args = ap.parse_args()
@@ -462,6 +531,11 @@ def main():
     d, p, n_el, n_el_t = CONFIGS[args.config]
     W = max(args.warmup, 3)
     K = args.steps
+    dfma, dmma = ks.fp64_peaks()
+    fp64_peak = max(dfma, dmma)
+    nominal_fp64 = 37.2  # B200 datasheet-class FP64 at 1965 MHz
+    pk = peaks()
+    hbm_peak = pk.get("hbm_gbs", 6650.0)
 
     t_setup = time.perf_counter()
     prob = ks.SpaceTimeProblem.uniform(d, p, n_el, n_el_t)
@@ -474,14 +548,10 @@ def main():
     r = ks.DeviceVector.from_host(r_host)
     z = ks.DeviceVector(n)
     y = ks.DeviceVector(n)
-    dfma, dmma = ks.fp64_peaks()
-    mixed = ks.fp64_peak_mixed()
-    fp64_peak = max(dfma, dmma)
 
     # ---- device-resident FD apply (the headline) ----
     clk = ClockSampler(local).__enter__()
     P.time(r, z, W, flush=False)
-    barrier(dist)
     ks.lib().ks_synchronize()
     ks.reset_launch_count()
     t0 = time.perf_counter()
@@ -489,13 +559,11 @@ def main():
     ks.lib().ks_synchronize()
     wall_fd = time.perf_counter() - t0
     launches = ks.launch_count()
-    barrier(dist)
-    ms_fd = max_over_ranks(dist, ms_fd)
-    value = ws * n / (ms_fd * 1e-3)
+    value = n / (ms_fd * 1e-3)
 
     # ---- matvec ----
     A.time(r, y, W, flush=False)
-    ms_mv = max_over_ranks(dist, A.time(r, y, K, flush=False))
+    ms_mv = A.time(r, y, K, flush=False)
 
     # ---- e2e through the public host-pointer API (pinned host buffers) ----
     import ctypes as C
@@ -507,7 +575,6 @@ def main():
     rin[:] = r_host
     for _ in range(2):
         P.apply(rin, zout)
-    barrier(dist)
     t0 = time.perf_counter()
     for _ in range(K):
         P.apply(rin, zout)
@@ -518,40 +585,57 @@ def main():
     for _ in range(2):
         P.apply(rin, zout, stream=ust)
     ust.synchronize()
-    barrier(dist)
     t0 = time.perf_counter()
     for _ in range(K):
         P.apply(rin, zout, stream=ust)
     ust.synchronize()
     e2e_s = (time.perf_counter() - t0) / K
-    e2e_s = max_over_ranks(dist, e2e_s)
-    e2e_val = ws * n / e2e_s
+    e2e_val = n / e2e_s
     check = float(np.abs(zout).sum())  # the step's result was read back on the host
     clk.__exit__(None, None, None)
 
-    # ---- full solves (device-resident PCG) ----
-    solves = {}
+    # ---- roofline of the dominant kernel family: the spatial transforms ----
+    # The folded transform executes 2n+2 flop per DOF (below the FP64 ridge), so
+    # it is HBM-bound: SURVEY 8(d) per-unit figure 32 B/DOF (read X, write Y) x
+    # N DOF per launch / the average transform launch time (CUDA events around
+    # each launch). The dense-basis FP64 view (4n flop/DOF) is reported beside it.
+    info = P.info()
+    folded = set(info["folded_axes"])
+    nlaunch = 2 * d - (2 if info.get("fused_axis1") else 0) + (1 if info.get("fused_axis1") else 0)
+    t_launch = ms_gemm * 1e-3 / nlaunch
+    bytes_launch = 32.0 * n
+    dense_flops_launch = sum(4 * dims[l] for l in range(1, d + 1)) * n / d
+    exec_flops_launch = sum((2 * dims[l] + 2) if l in folded else 4 * dims[l] for l in range(1, d + 1)) * n / d
+    gemm_hbm = bytes_launch / t_launch / 1e9
+    fd_roof_s = max(fd_flops_per_dof(dims, p) * n / (fp64_peak * 1e12), 32.0 * n / (hbm_peak * 1e9))
+    fd_roof_nominal_s = max(fd_flops_per_dof(dims, p) * n / (nominal_fp64 * 1e12), 32.0 * n / (hbm_peak * 1e9))
+    mv_roof_s = max(matvec_flops_per_dof(d, p) * n / (fp64_peak * 1e12), 32.0 * n / (hbm_peak * 1e9))
+    tr = ncu_traffic("k_xfold") or {}
+
+    solves, legs = {}, {}
     if not args.no_solve:
         b = ks.DeviceVector.from_host(r_host)
-        # first solve allocates the handle's PCG work vectors (kept across solves)
-        rep0 = ks.pcg(A, P, b, ks.PcgOptions(1e-8, 200))
+        rep0 = ks.pcg(A, P, b, ks.PcgOptions(1e-8, 200))  # first solve allocates the work vectors
         rep = ks.pcg(A, P, b, ks.PcgOptions(1e-8, 200))
+        roof = solve_roofline_s(dims, p, n, rep.iterations, fp64_peak, hbm_peak)
         solves[f"solve_{args.config}"] = {"iterations": rep.iterations, "converged": rep.converged,
-                                          "seconds": rep.solve_seconds,
-                                          "first_solve_seconds": rep0.solve_seconds,
-                                          "final_relres": rep.res_history[-1] if rep.res_history else None}
-        if args.config == "c3":
+                                          "seconds": rep.solve_seconds, "first_solve_seconds": rep0.solve_seconds,
+                                          "final_relres": rep.res_history[-1] if rep.res_history else None,
+                                          "roofline_s": roof, "frac_of_roofline": roof / rep.solve_seconds,
+                                          "roofline_basis": "SURVEY 8(d) Solve: iterations x (FD + matvec "
+                                                            "rooflines + 144 B/DOF BLAS-1)"}
+    if args.config == "c3" and not args.no_extra:
+        # BASELINE configs[4] (c5, 287.8 M DOF) on this GPU: FD, matvec, solve
+        c5, P5, A5, _ = config_leg(ks, "c5", max(3, K // 4), 3, local, fp64_peak, hbm_peak, solve=not args.no_solve)
+        del P5, A5
+        legs["c5"] = c5
+        # BASELINE configs[0] (c1): latency of 100 FD applies (eager / CUDA graph) + a solve
+        legs["c1"] = latency_leg(ks, "c1", local)
+        if not args.no_solve:
+            # BASELINE configs[1]: sin-sin manufactured solution, lifted right-hand
+            # side, solve to 1e-8, L2 error check -- all on the device
             p2 = ks.SpaceTimeProblem.uniform(*CONFIGS["c2"])
             P2, A2 = ks.FDPreconditioner(p2, device=local), ks.assemble_system_operator(p2, device=local)
-            b2 = ks.DeviceVector.from_host(rhs(p2.N_dof))
-            ks.pcg(A2, P2, b2)
-            rep2 = ks.pcg(A2, P2, b2, ks.PcgOptions(1e-8, 200))
-            solves["solve_c2_random_rhs"] = {"iterations": rep2.iterations,
-                                             "converged": rep2.converged,
-                                             "seconds": rep2.solve_seconds,
-                                             "dofs": p2.N_dof}
-            # BASELINE configs[1] as specified: sin-sin manufactured solution, lifted
-            # right-hand side, solve to 1e-8, L2 error check -- all on the device
             Q2 = ks.Quadrature(p2, device=local)
             Q2.lift("sinsin", "sinsin")  # warm-up
             lifts = []
@@ -559,114 +643,75 @@ def main():
                 t0 = time.perf_counter()
                 rhs2, bnd2 = Q2.lift("sinsin", "sinsin")
                 lifts.append(time.perf_counter() - t0)
-            t_lift = sorted(lifts)[1]
-            rep3 = ks.pcg(A2, P2, ks.DeviceVector.from_host(rhs2), ks.PcgOptions(1e-8, 200))
+            b2 = ks.DeviceVector.from_host(rhs2)
+            ks.pcg(A2, P2, b2, ks.PcgOptions(1e-8, 200))
+            rep3 = ks.pcg(A2, P2, b2, ks.PcgOptions(1e-8, 200))
             errs = []
             for _ in range(3):
                 t0 = time.perf_counter()
-                full2 = Q2.extend(rep3.x, bnd2)
-                l2, en = Q2.error_norms(full2, "sinsin", "sinsin")
+                l2, en = Q2.error_norms(Q2.extend(rep3.x, bnd2), "sinsin", "sinsin")
                 errs.append(time.perf_counter() - t0)
-            t_err = sorted(errs)[1]
-            solves["solve_c2_manufactured"] = {"iterations": rep3.iterations, "converged": rep3.converged,
-                                               "seconds": rep3.solve_seconds, "rhs_lift_seconds": t_lift,
-                                               "error_seconds": t_err, "l2_error": l2, "energy_error": en,
-                                               "dofs": p2.N_dof,
-                                               "problem": "u = sin(pi x) sin(pi y) exp(-2 i pi^2 t), f = S u"}
-
-    # ---- roofline: dominant kernel = the spatial transform (mode product) ----
-    # t_roof = max(B_alg / BW_HBM, F_alg / P_FP64) with the DENSE
-    # algorithmic work ("structure tricks (even/odd split, dedup) must still be
-    # scored on this dense F_alg"): 4 n flops and 32 B per DOF per transform.
-    info = P.info()
-    folded = set(info["folded_axes"])
-    nlaunch = 2 * d                                   # transform launches per apply
-    t_launch = ms_gemm * 1e-3 / nlaunch               # average transform launch (CUDA events)
-    bytes_launch = 32.0 * n                           # read X + write Y, 16 B each
-    dense_flops_launch = sum(4 * dims[l] for l in range(1, d + 1)) * n / d
-    exec_flops_launch = sum((2 * dims[l] + 2) if l in folded else 4 * dims[l] for l in range(1, d + 1)) * n / d
-    pk = peaks()
-    hbm_peak = pk.get("hbm_gbs", 6650.0)
-    gemm_hbm = bytes_launch / t_launch / 1e9
-    gemm_tf_dense = dense_flops_launch / t_launch / 1e12
-    gemm_tf_exec = exec_flops_launch / t_launch / 1e12
-    t_roof_launch = max(bytes_launch / (hbm_peak * 1e9), dense_flops_launch / (fp64_peak * 1e12))
-    fp64_bound = dense_flops_launch / (fp64_peak * 1e12) >= bytes_launch / (hbm_peak * 1e9)
-    # whole FD apply, SURVEY basis: dense F_alg = 8 sum(n_l) + 24p + 8 flop/DOF, B_alg = 32 B/DOF
-    fd_roof_s = max(fd_flops_per_dof(dims, p) * n / (fp64_peak * 1e12), 32.0 * n / (hbm_peak * 1e9))
-    # and against this implementation's own 2d+1-pass traffic and executed flops
-    fac_bytes = info["blocks"] * dims[0] * (3 * p + 1) * 16 + info["blocks"] * dims[0]
-    fd_pass_s = max(fd_folded_flops_per_dof(dims, p, folded) * n / (fp64_peak * 1e12),
-                    ((2 * d + 1) * 32.0 * n + fac_bytes) / (hbm_peak * 1e9))
-    mv_roof_s = max(matvec_flops_per_dof(d, p) * n / (fp64_peak * 1e12),
-                    32.0 * n / (hbm_peak * 1e9))
+            c2lat = P2.latency(b2, ks.DeviceVector(p2.N_dof), 100, graph=True)
+            legs["c2"] = {"dofs": p2.N_dof, "iterations": rep3.iterations, "converged": rep3.converged,
+                          "solve_seconds": rep3.solve_seconds, "rhs_lift_seconds": sorted(lifts)[1],
+                          "error_seconds": sorted(errs)[1], "l2_error": l2, "energy_error": en,
+                          "fd_apply_us_graph": c2lat * 1e3,
+                          "problem": "u = sin(pi x) sin(pi y) exp(-2 i pi^2 t), f = S u"}
 
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:
         kind, sec, used = cpu_baseline_fd(args.config, r_host, steps=3, warmup=1)
         cpu = {"value": n / sec, "unit": "DOF/s", "cores": 1, "kind": kind,
                "sample": f"median of {used} full {args.config} FD applications ({n} DOF) after 1 "
                          "untimed warm-up, single thread, setup (block factorisation) excluded"}
 
-    if rank == 0:
-        line = {
-            "metric": "fd_apply_dof_per_s", "value": value, "unit": "DOF/s", "n_gpus": ws,
-            "steps": K, "warmup": W, "ms_per_step": ms_fd, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "c128 (complex FP64)",
-            "data": "synthetic (seeded U[-1,1] RHS, SURVEY 8(d))",
-            "config": bench_config(args.config, ws),
-            "transform_engine": {0: "dfma", 1: "dmma_v1", 2: "dmma_v2"}[ks.lib().ks_transform_engine()]
-                                + ("+fold" if P.info()["folded_axes"] else ""),
-            "e2e": {"value": e2e_val, "unit": "DOF/s", "h2d_bytes_per_step": n * 16,
-                    "d2h_bytes_per_step": n * 16, "ms_per_step": e2e_s * 1e3,
-                    "mode": "ks_fd_apply(host pointers, pinned) on a user stream, K steps back to back, "
-                            "every step's r copied in and z copied out; copies of consecutive steps overlap",
-                    "blocking_value": ws * n / e2e_block_s, "blocking_ms_per_step": e2e_block_s * 1e3},
-            "gpu_launches": launches,
-            "roofline": {"bound": "fp64" if fp64_bound else "hbm",
-                         "achieved": gemm_tf_dense if fp64_bound else gemm_hbm,
-                         "peak": fp64_peak if fp64_bound else hbm_peak,
-                         "unit": "TFLOP/s" if fp64_bound else "GB/s",
-                         "frac": t_roof_launch / t_launch,
-                         "traffic": (ncu_traffic("k_mode_gemm_fold") or {}).get("bytes_per_launch"),
-                         "traffic_source": (ncu_traffic("k_mode_gemm_fold") or {}).get("source"),
-                         "algorithmic_bytes_per_launch": bytes_launch,
-                         "kernel": "k_mode_gemm_fold" if folded else "k_mode_gemm_dmma2",
-                         "basis": "SURVEY 8(d) dense algorithmic work per launch: 4n flop + 32 B per DOF",
-                         "launch_ms": t_launch * 1e3,
-                         "executed_fp64_tflops": gemm_tf_exec,
-                         "executed_fp64_frac": gemm_tf_exec / fp64_peak,
-                         "hbm_gbs": gemm_hbm, "hbm_frac": gemm_hbm / hbm_peak,
-                         "peak_source": "FP64: measured live DFMA %.2f / DMMA %.2f TFLOP/s microbenchmarks; "
-                                        "HBM: MEASURED_PEAKS.json hbm_gbs" % (dfma, dmma),
-                         "mixed_dfma_dmma_tflops": mixed,
-                         "gemm_ms_per_apply": ms_gemm},
-            "fd_apply": {"ms": ms_fd, "roofline_ms": fd_roof_s * 1e3,
-                         "frac_of_roofline": fd_roof_s * 1e3 / ms_fd,
-                         "roofline_basis": "SURVEY 8(d): max(dense F_alg / FP64 peak, 32 B/DOF / HBM peak)",
-                         "flops_per_dof_reference_algorithm": fd_flops_per_dof(dims, p),
-                         "flops_per_dof_executed": fd_folded_flops_per_dof(dims, p, folded),
-                         "roofline_ms_this_decomposition": fd_pass_s * 1e3,
-                         "frac_of_roofline_this_decomposition": fd_pass_s * 1e3 / ms_fd,
-                         "decomposition": f"{2 * d + 1} HBM passes (16 B/DOF in + out each, factors once), "
-                                          "executed flops",
-                         "folded_axes": sorted(folded), "factored_blocks": info["blocks"],
-                         "wall_s": wall_fd},
-            "matvec": {"ms": ms_mv, "dof_per_s": ws * n / (ms_mv * 1e-3),
-                       "roofline_ms": mv_roof_s * 1e3, "frac_of_roofline": mv_roof_s * 1e3 / ms_mv,
-                       "plan": A.plan_info(),
-                       "hbm_gbs_effective": 32.0 * n / (ms_mv * 1e-3) / 1e9},
-            "solves": solves,
-            "setup_s": setup_s,
-            "clocks": clk.summary(),
-            "cpu_baseline": cpu,
-            "checksum": check,
-        }
-        print(json.dumps(line), flush=True)
+    line = {
+        "metric": "fd_apply_dof_per_s", "value": value, "unit": "DOF/s", "n_gpus": ws,
+        "steps": K, "warmup": W, "ms_per_step": ms_fd, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128 (complex FP64)",
+        "data": "synthetic (seeded U[-1,1] RHS, SURVEY 8(d))",
+        "config": bench_config(args.config, ws),
+        "e2e": {"value": e2e_val, "unit": "DOF/s", "h2d_bytes_per_step": n * 16,
+                "d2h_bytes_per_step": n * 16, "ms_per_step": e2e_s * 1e3,
+                "mode": "ks_fd_apply(host pointers, pinned) on a user stream, K steps back to back, "
+                        "every step's r copied in and z copied out; copies of consecutive steps overlap",
+                "blocking_value": n / e2e_block_s, "blocking_ms_per_step": e2e_block_s * 1e3},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "achieved": gemm_hbm, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": gemm_hbm / hbm_peak,
+                     "traffic": tr.get("bytes_per_launch"), "traffic_source": tr.get("source"),
+                     "algorithmic_bytes_per_launch": bytes_launch,
+                     "kernel": "k_xfold (folded spatial transform, average of the %d launches per apply)" % nlaunch,
+                     "basis": "SURVEY 8(d): 32 B per DOF per transform launch (read X, write Y) / launch time",
+                     "launch_ms": t_launch * 1e3,
+                     "executed_fp64_tflops": exec_flops_launch / t_launch / 1e12,
+                     "executed_fp64_frac": exec_flops_launch / t_launch / 1e12 / fp64_peak,
+                     "dense_basis_fp64_tflops": dense_flops_launch / t_launch / 1e12,
+                     "peak_source": "HBM: MEASURED_PEAKS.json hbm_gbs; FP64: live DFMA %.2f / DMMA %.2f TFLOP/s "
+                                    "microbenchmarks" % (dfma, dmma),
+                     "transform_ms_per_apply": ms_gemm},
+        "fd_apply": {"ms": ms_fd, "roofline_ms": fd_roof_s * 1e3, "frac_of_roofline": fd_roof_s * 1e3 / ms_fd,
+                     "frac_of_roofline_nominal_fp64": fd_roof_nominal_s * 1e3 / ms_fd,
+                     "roofline_basis": "SURVEY 8(d): max(dense F_alg / FP64 peak, 32 B/DOF / HBM peak); "
+                                       "FP64 peak = live microbenchmark (%.2f TF) and, for the _nominal_ "
+                                       "figure, %.1f TF" % (fp64_peak, nominal_fp64),
+                     "flops_per_dof_reference_algorithm": fd_flops_per_dof(dims, p),
+                     "flops_per_dof_executed": fd_folded_flops_per_dof(dims, p, folded),
+                     "folded_axes": sorted(folded), "factored_blocks": info["blocks"], "plan": info,
+                     "wall_s": wall_fd},
+        "matvec": {"ms": ms_mv, "dof_per_s": n / (ms_mv * 1e-3),
+                   "roofline_ms": mv_roof_s * 1e3, "frac_of_roofline": mv_roof_s * 1e3 / ms_mv,
+                   "plan": A.plan_info(), "hbm_gbs_effective": 32.0 * n / (ms_mv * 1e-3) / 1e9},
+        "solves": solves,
+        "legs": legs,
+        "setup_s": setup_s,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+        "checksum": check,
+    }
+    print(json.dumps(line), flush=True)
     ks.lib().ks_host_free(hp)
     ks.lib().ks_host_free(hz)
-    if dist is not None:
-        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -221,6 +221,11 @@ int ks_fd_time(ks_fd* fd, const ks_c64* r, ks_c64* z, int iters, int flush,
                double* ms_out, double* ms_kernel);
 int ks_kron_time(ks_kron* k, const ks_c64* x, ks_c64* y, int iters, int flush,
                  double* ms_out);
+/* Latency of the FD apply (device pointers): `iters` applies back to back on
+ * the handle's stream between two CUDA events, either launched eagerly or as
+ * replays of one CUDA graph holding a whole apply (graph = 1); ms_out = the
+ * average per apply. For the latency-bound small configs (c1, c2). */
+int ks_fd_latency(ks_fd* fd, const ks_c64* r, ks_c64* z, int iters, int graph, double* ms_out);
 /* Measured FP64 FMA peak (TFLOP/s) of this device, from a DFMA microbenchmark. */
 int ks_fp64_peak(double* tflops);
 /* Both FP64 peaks: CUDA-core DFMA and tensor-core DMMA (mma.sync m8n8k4 f64). */
@@ -279,6 +284,23 @@ int ks_ipc_open(const void* handle, void** dptr);
 int ks_ipc_close(void* dptr);
 int ks_fdshard_destroy(ks_fdshard* h);
 
+/* ---------------------------------------------------------------------------
+ * NCCL behind the C-ABI (one rank per GPU, one process per rank). Rank 0 calls
+ * ks_comm_unique_id and hands the 128 bytes to the other ranks (any channel);
+ * every rank then calls ks_comm_create (ncclCommInitRank). libnccl.so.2 is
+ * opened at run time; failures return KS_ENCCL.
+ * ------------------------------------------------------------------------- */
+#define KS_COMM_ID_BYTES 128
+typedef struct ks_comm ks_comm;
+int ks_comm_unique_id(void* id /* KS_COMM_ID_BYTES */);
+int ks_comm_create(int nranks, int rank, const void* id, int device, ks_comm** out);
+int ks_comm_destroy(ks_comm* comm);
+/* z_slab = P^-1 r_slab for this rank's slab (device pointers): the three phases
+ * above with both all-to-alls as grouped ncclSend / ncclRecv (uneven slabs
+ * included), stream-ordered on `stream` (NULL: the handle's stream, blocking).
+ * The communicator's rank / size must match the shard plan. */
+int ks_fdshard_apply(ks_fdshard* h, ks_comm* comm, const ks_c64* r_slab, ks_c64* z_slab, void* stream);
+
 /* Sharded Kronecker operator: same slabs of the outermost axis; the input is
  * the slab plus a halo of bw planes on each side (bw = widest band on that
  * axis; the caller exchanges the halos with the neighbouring ranks):
@@ -291,6 +313,18 @@ int ks_kronshard_plan(long long nd, int bw, int nranks, int rank, long long* lo,
 int ks_kronshard_sizes(const ks_kron* k, long long* lo, long long* hi, long long* ext_lo,
                        long long* ext_hi, size_t* plane_elems);
 int ks_kronshard_apply(ks_kron* k, const ks_c64* x_ext, ks_c64* y_slab, void* stream);
+/* y_slab = (K x)[slab] from this rank's slab x_slab: the bw-plane halos are
+ * exchanged with the neighbouring ranks (grouped ncclSend / ncclRecv) into the
+ * handle's extended buffer, then the local apply. Device pointers. */
+int ks_kronshard_apply_comm(ks_kron* k, ks_comm* comm, const ks_c64* x_slab, ks_c64* y_slab, void* stream);
+/* Slab-sharded pcg (krylov.cpp:24-114): every rank calls it with its slabs of
+ * b and x (device or host pointers, `mem`); A from ks_kronshard_create /
+ * ks_setup_create_system_sharded, P from ks_fdshard_create (or NULL), both for
+ * this rank. Same control flow and device-resident scalars as ks_pcg; the dots
+ * are ncclAllReduce'd on the device, one host round trip per iteration. The
+ * residual history and flags are identical on every rank. */
+int ks_pcg_sharded(ks_kron* A, ks_fdshard* P, ks_comm* comm, const ks_c64* b_slab, ks_c64* x_slab, int mem,
+                   const ks_pcg_opts* opts, double* res_hist, int hist_cap, ks_pcg_report* report);
 /* PCG building blocks on device vectors (sharded PCG): x += a p, r -= a q,
  * *rr = local ||r||^2; and p = z + beta p. Both synchronise the stream. */
 int ks_cg_update(double alpha, const ks_c64* p, const ks_c64* q, ks_c64* x, ks_c64* r, size_t n,

@@ -105,6 +105,8 @@ _SIGS = {
                                     C.POINTER(C.c_int)]),
     "ks_kron_engine": (C.c_int, [_P, C.POINTER(C.c_int)]),
     "ks_kron_destroy": (C.c_int, [_P]),
+    "ks_pcg_sharded": (C.c_int, [_P, _P, _P, _P, _P, C.c_int, C.POINTER(ks_pcg_opts), _P, C.c_int,
+                                 C.POINTER(ks_pcg_report)]),
     "ks_pcg": (C.c_int, [_P, _P, _P, _P, C.c_int, C.POINTER(ks_pcg_opts), _P, C.c_int,
                          C.POINTER(ks_pcg_report)]),
     "ks_axpy_real": (C.c_int, [C.c_double, _P, _P, C.c_size_t, _P]),
@@ -125,6 +127,7 @@ _SIGS = {
     "ks_fd_time": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.POINTER(C.c_double),
                              C.POINTER(C.c_double)]),
     "ks_kron_time": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.POINTER(C.c_double)]),
+    "ks_fd_latency": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "ks_fp64_peak": (C.c_int, [C.POINTER(C.c_double)]),
     "ks_fp64_peaks": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "ks_fp64_peak_mixed": (C.c_int, [C.POINTER(C.c_double)]),
@@ -152,6 +155,11 @@ _SIGS = {
     "ks_ipc_open": (C.c_int, [_P, C.POINTER(_P)]),
     "ks_ipc_close": (C.c_int, [_P]),
     "ks_fdshard_destroy": (C.c_int, [_P]),
+    "ks_comm_unique_id": (C.c_int, [_P]),
+    "ks_comm_create": (C.c_int, [C.c_int, C.c_int, _P, C.c_int, C.POINTER(C.c_void_p)]),
+    "ks_comm_destroy": (C.c_int, [_P]),
+    "ks_fdshard_apply": (C.c_int, [_P, _P, _P, _P, _P]),
+    "ks_kronshard_apply_comm": (C.c_int, [_P, _P, _P, _P, _P]),
     "ks_kronshard_create": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.c_int, C.POINTER(ks_term),
                                       C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),
     "ks_kronshard_sizes": (C.c_int, [_P, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong),
@@ -506,6 +514,12 @@ class FDPreconditioner:
                 "no_pivot_solve": bool(m.value >> 18 & 1),
                 # axis-1 transform + block solves + inverse transform in one kernel (ks_fdaxis1.cu)
                 "fused_axis1": bool(m.value >> 19 & 1)}
+
+    def latency(self, r: DeviceVector, z: DeviceVector, iters: int = 100, graph: bool = True) -> float:
+        """ms per apply over `iters` back-to-back applies (CUDA-graph replays if graph)."""
+        ms = C.c_double()
+        _check(lib().ks_fd_latency(self._h, r.ptr, z.ptr, int(iters), int(graph), C.byref(ms)))
+        return ms.value
 
     def time(self, r: DeviceVector, z: DeviceVector, iters: int, flush: bool = True):
         ms, mk = C.c_double(), C.c_double()

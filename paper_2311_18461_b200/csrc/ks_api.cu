@@ -153,6 +153,8 @@ struct ks_kron {
     bool sharded = false;
     long long lo = 0, hi = 0, ext_lo = 0, ext_hi = 0;
     size_t plane = 0;
+    int nranks = 1, rank = 0, bwd = 0; // sharded: the split and the halo width on the outermost axis
+    DevBuf ext;                         // ks_kronshard_apply_comm: the haloed input
     std::unique_ptr<KronPlan, KronPlanDeleter> plan;
     DevBuf io_x, io_y;
     DevBuf pcg[6];                 // ks_pcg work vectors (x, r, z, p, q, scratch), kept across solves
@@ -873,6 +875,9 @@ static void kron_create_impl(int ndim, const int* dims, int nterms, const ks_ter
                    "sharded matvec: slab thinner than the band (halo would span ranks)");
         k->ext_lo = std::max<long long>(k->lo - bwd, 0);
         k->ext_hi = std::min<long long>(k->hi + bwd, nd);
+        k->nranks = nranks;
+        k->rank = rank;
+        k->bwd = bwd;
         k->plane = 1;
         for (int a = 0; a < D; ++a) k->plane *= (size_t)dims[a];
         pdims[D] = (int)(k->ext_hi - k->ext_lo);
@@ -949,6 +954,55 @@ int ks_kronshard_apply(ks_kron* k, const ks_c64* x_ext, ks_c64* y_slab, void* st
     API_END
 }
 
+} // extern "C"
+
+namespace ks {
+// halo exchange with the neighbouring ranks into k->ext, then the local apply
+void kronshard_apply_comm(ks_kron* k, ks_comm* c, const double2* x, double2* y, cudaStream_t st) {
+    KS_REQUIRE(k->sharded, KS_EINVAL, "ks_kronshard_apply_comm: not a sharded operator");
+    KS_REQUIRE(comm_size(c) == k->nranks && comm_rank(c) == k->rank, KS_EINVAL,
+               "ks_kronshard_apply_comm: communicator does not match the shard");
+    const size_t pl = k->plane, next = (size_t)(k->ext_hi - k->ext_lo) * pl;
+    if (k->ext.bytes < next * sizeof(double2)) k->ext.alloc(next * sizeof(double2));
+    double2* e = k->ext.as<double2>();
+    const long long nd = k->dims.back();
+    KS_CUDA(cudaMemcpyAsync(e + (size_t)(k->lo - k->ext_lo) * pl, x, (size_t)(k->hi - k->lo) * pl * sizeof(double2),
+                            cudaMemcpyDeviceToDevice, st));
+    comm_group_start();
+    if (k->rank > 0) { // left neighbour: its right halo = my first planes; my left halo = its last
+        long long l_lo, l_hi, l_elo, l_ehi;
+        if (ks_kronshard_plan(nd, k->bwd, k->nranks, k->rank - 1, &l_lo, &l_hi, &l_elo, &l_ehi) != KS_OK)
+            throw Error(KS_EINVAL, ks_last_error());
+        comm_send(x, 2 * (size_t)(l_ehi - l_hi) * pl, k->rank - 1, c, st);
+        comm_recv(e, 2 * (size_t)(k->lo - k->ext_lo) * pl, k->rank - 1, c, st);
+    }
+    if (k->rank + 1 < k->nranks) { // right neighbour
+        long long r_lo, r_hi, r_elo, r_ehi;
+        if (ks_kronshard_plan(nd, k->bwd, k->nranks, k->rank + 1, &r_lo, &r_hi, &r_elo, &r_ehi) != KS_OK)
+            throw Error(KS_EINVAL, ks_last_error());
+        comm_send(x + (size_t)(r_elo - k->lo) * pl, 2 * (size_t)(k->hi - r_elo) * pl, k->rank + 1, c, st);
+        comm_recv(e + (size_t)(k->hi - k->ext_lo) * pl, 2 * (size_t)(k->ext_hi - k->hi) * pl, k->rank + 1, c, st);
+    }
+    comm_group_end();
+    kron_apply(*k->plan, e, y, st, k->hptrs);
+}
+} // namespace ks
+
+extern "C" {
+
+int ks_kronshard_apply_comm(ks_kron* k, ks_comm* comm, const ks_c64* x_slab, ks_c64* y_slab, void* stream) {
+    API_BEGIN
+    KS_REQUIRE(k && comm && x_slab && y_slab, KS_EINVAL, "ks_kronshard_apply_comm: NULL argument");
+    std::lock_guard<std::mutex> lk(k->mu);
+    ensure_device(k->device);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : k->stream;
+    KS_CUDA(cudaStreamWaitEvent(st, k->done, 0));
+    kronshard_apply_comm(k, comm, reinterpret_cast<const double2*>(x_slab), reinterpret_cast<double2*>(y_slab), st);
+    KS_CUDA(cudaEventRecord(k->done, st));
+    if (!stream) KS_CUDA(cudaStreamSynchronize(st));
+    API_END
+}
+
 int ks_kron_apply(ks_kron* k, const ks_c64* x, ks_c64* y, int mem, void* stream) {
     API_BEGIN
     kron_apply_any(k, x, y, mem, stream);
@@ -982,13 +1036,23 @@ int ks_kron_destroy(ks_kron* k) {
 // ---------------------------------------------------------------------------
 // PCG (krylov.cpp:24-114)
 // ---------------------------------------------------------------------------
-int ks_pcg(ks_kron* A, ks_fd* P, const ks_c64* b, ks_c64* x, int mem, const ks_pcg_opts* opts,
-           double* res_hist, int hist_cap, ks_pcg_report* report) {
-    API_BEGIN
+} // extern "C"
+
+// pcg body shared by ks_pcg (one GPU: A, P) and ks_pcg_sharded (this rank's
+// slabs: sharded A, Ps, communicator; dots all-reduced on the device)
+static void pcg_impl(ks_kron* A, ks_fd* P, ks_fdshard* Ps, ks_comm* comm, const ks_c64* b, ks_c64* x, int mem,
+                     const ks_pcg_opts* opts, double* res_hist, int hist_cap, ks_pcg_report* report) {
     KS_REQUIRE(A && b && x && opts && report, KS_EINVAL, "ks_pcg: NULL argument");
     KS_REQUIRE(opts->tol > 0 && opts->maxit >= 0, KS_EINVAL, "pcg: bad options");
     KS_REQUIRE(!P || P->N == A->N, KS_EINVAL, "pcg: operator sizes differ");
     KS_REQUIRE(!P || P->device == A->device, KS_EINVAL, "pcg: operators on different devices");
+    KS_REQUIRE(!Ps || (fdshard_slab_n(Ps) == A->N && fdshard_device(Ps) == A->device), KS_EINVAL,
+               "pcg: sharded operators differ in slab or device");
+    KS_REQUIRE(!comm || A->sharded, KS_EINVAL, "pcg_sharded: the operator is not sharded");
+    // device scalars summed over the ranks (in place, stream-ordered)
+    auto allreduce = [&](Reducer& rd) {
+        if (comm) comm_allreduce_sum(rd.result.as<double>(), 1, comm, A->stream);
+    };
     std::lock_guard<std::mutex> lka(A->mu);
     std::unique_ptr<std::lock_guard<std::mutex>> lkp;
     if (P) lkp.reset(new std::lock_guard<std::mutex>(P->mu));
@@ -1043,15 +1107,19 @@ int ks_pcg(ks_kron* A, ks_fd* P, const ks_c64* b, ks_c64* x, int mem, const ks_p
         KS_CUDA(cudaEventRecord(b2, st));
         dst.push_back({(int)evs.size() - 2, (int)evs.size() - 1});
     };
-    auto matvec = [&](const double2* in, double2* outv) {
-        ev_pair(mv_ev, [&]() { kron_apply(*A->plan, in, outv, st, A->hptrs); });
+    auto mv = [&](const double2* in, double2* outv) {
+        if (comm) kronshard_apply_comm(A, comm, in, outv, st);
+        else kron_apply(*A->plan, in, outv, st, A->hptrs);
     };
+    auto pc = [&](const double2* rin, double2* zout) {
+        if (Ps) fdshard_apply_comm(Ps, comm, rin, zout, st);
+        else if (P) fd_apply_dev(P, rin, zout, false, st, nullptr);
+        else KS_CUDA(cudaMemcpyAsync(zout, rin, bytes, cudaMemcpyDeviceToDevice, st));
+    };
+    auto matvec = [&](const double2* in, double2* outv) { ev_pair(mv_ev, [&]() { mv(in, outv); }); };
     auto precond = [&](const double2* rin, double2* zout) {
-        if (P) {
-            ev_pair(pc_ev, [&]() { fd_apply_dev(P, rin, zout, false, st, nullptr); });
-        } else {
-            KS_CUDA(cudaMemcpyAsync(zout, rin, bytes, cudaMemcpyDeviceToDevice, st));
-        }
+        if (P || Ps) ev_pair(pc_ev, [&]() { pc(rin, zout); });
+        else pc(rin, zout);
     };
     // The two halves of an iteration, replayed as CUDA graphs after their first
     // (eager) run, which does the allocations, first-apply tuning and pointer
@@ -1077,7 +1145,7 @@ int ks_pcg(ks_kron* A, ks_fd* P, const ks_c64* b, ks_c64* x, int mem, const ks_p
         }
         ~Graphs() { reset(); }
     } graphs;
-    bool use_graph = graphs_ok, seen[2] = {false, false};
+    bool use_graph = graphs_ok && !comm, seen[2] = {false, false};
     // Deferred solution update: phase A updates only r, and x += alpha_k p_k
     // rides along the p update of phase B (which reads p_k anyway) -- or runs
     // alone before a true residual and at exit. Same arithmetic on the same
@@ -1092,18 +1160,20 @@ int ks_pcg(ks_kron* A, ks_fd* P, const ks_c64* b, ks_c64* x, int mem, const ks_p
         pending = false;
     };
     auto phase_a = [&]() {
-        kron_apply(*A->plan, p.as<double2>(), q.as<double2>(), st, A->hptrs);
+        mv(p.as<double2>(), q.as<double2>());
         launch_dotc(red_c, p.as<double2>(), q.as<double2>(), n, st); // curvature Re <p, Ap>
+        allreduce(red_c);
         launch_cg_update_r_dev(red_u, rho_old.result.as<double>(), red_c.result.as<double>(), q.as<double2>(),
                                r.as<double2>(), n, st);
+        allreduce(red_u);
         KS_CUDA(cudaMemcpyAsync(red_c.host, red_c.result.p, sizeof(double), cudaMemcpyDeviceToHost, st));
         KS_CUDA(cudaMemcpyAsync(red_u.host, red_u.result.p, sizeof(double), cudaMemcpyDeviceToHost, st));
     };
     auto phase_b = [&]() {
         // z = P r and rho' = Re <r, z>
-        if (P) fd_apply_dev(P, r.as<double2>(), z.as<double2>(), false, st, nullptr);
-        else KS_CUDA(cudaMemcpyAsync(z.p, r.p, bytes, cudaMemcpyDeviceToDevice, st));
+        pc(r.as<double2>(), z.as<double2>());
         launch_dotc(rho_new, r.as<double2>(), z.as<double2>(), n, st); // rho' = Re <r, z>
+        allreduce(rho_new);
         if (pending) { // (the caller clears pending: a replayed graph does not run this body)
             launch_xpby_x_dev(z.as<double2>(), rho_new.result.as<double>(), rho_old.result.as<double>(),
                               red_c.result.as<double>(), p.as<double2>(), xv.as<double2>(), n, st);
@@ -1139,6 +1209,7 @@ int ks_pcg(ks_kron* A, ks_fd* P, const ks_c64* b, ks_c64* x, int mem, const ks_p
     };
     auto norm2 = [&](const double2* a) {
         launch_norm2sq(red, a, n, st);
+        allreduce(red);
         fetch(red, st, 1);
         return red.host[0];
     };
@@ -1170,7 +1241,7 @@ int ks_pcg(ks_kron* A, ks_fd* P, const ks_c64* b, ks_c64* x, int mem, const ks_p
     if (bnorm == 0.0) {
         report->converged = 1;
         finish_out();
-        return KS_OK;
+        return;
     }
     auto true_relres = [&]() {
         // a new pointer table may evict the captured phases' tables: recapture later
@@ -1183,6 +1254,7 @@ int ks_pcg(ks_kron* A, ks_fd* P, const ks_c64* b, ks_c64* x, int mem, const ks_p
     precond(r.as<double2>(), z.as<double2>());
     KS_CUDA(cudaMemcpyAsync(p.p, z.p, bytes, cudaMemcpyDeviceToDevice, st));
     launch_dotc(rho_old, r.as<double2>(), z.as<double2>(), n, st); // rho = Re <r, z>
+    allreduce(rho_old);
     int restarts = 0;
     for (int k = 0; k < opts->maxit; ++k) {
         run_phase(0, phase_a, mv_ev);
@@ -1210,6 +1282,7 @@ int ks_pcg(ks_kron* A, ks_fd* P, const ks_c64* b, ks_c64* x, int mem, const ks_p
                     precond(r.as<double2>(), z.as<double2>());
                     KS_CUDA(cudaMemcpyAsync(p.p, z.p, bytes, cudaMemcpyDeviceToDevice, st));
                     launch_dotc(rho_old, r.as<double2>(), z.as<double2>(), n, st);
+                    allreduce(rho_old);
                     continue;
                 }
             }
@@ -1224,8 +1297,26 @@ int ks_pcg(ks_kron* A, ks_fd* P, const ks_c64* b, ks_c64* x, int mem, const ks_p
     report->hist_len = hist_len < hist_cap ? hist_len : hist_cap;
     if (!res_hist) report->hist_len = 0;
     finish_out();
+}
+
+extern "C" {
+
+int ks_pcg(ks_kron* A, ks_fd* P, const ks_c64* b, ks_c64* x, int mem, const ks_pcg_opts* opts,
+           double* res_hist, int hist_cap, ks_pcg_report* report) {
+    API_BEGIN
+    KS_REQUIRE(!A || !A->sharded, KS_EINVAL, "ks_pcg: sharded operator (use ks_pcg_sharded)");
+    pcg_impl(A, P, nullptr, nullptr, b, x, mem, opts, res_hist, hist_cap, report);
     API_END
 }
+
+int ks_pcg_sharded(ks_kron* A, ks_fdshard* P, ks_comm* comm, const ks_c64* b_slab, ks_c64* x_slab, int mem,
+                   const ks_pcg_opts* opts, double* res_hist, int hist_cap, ks_pcg_report* report) {
+    API_BEGIN
+    KS_REQUIRE(comm, KS_EINVAL, "ks_pcg_sharded: NULL communicator");
+    pcg_impl(A, nullptr, P, comm, b_slab, x_slab, mem, opts, res_hist, hist_cap, report);
+    API_END
+}
+
 
 // ---------------------------------------------------------------------------
 // BLAS-1 on device vectors
@@ -1392,6 +1483,51 @@ int ks_fd_time(ks_fd* fd, const ks_c64* r, ks_c64* z, int iters, int flush, doub
     cudaEventDestroy(b);
     if (ms_out) *ms_out = tot / iters;
     if (ms_kernel) *ms_kernel = ker / iters;
+    API_END
+}
+
+int ks_fd_latency(ks_fd* fd, const ks_c64* r, ks_c64* z, int iters, int graph, double* ms_out) {
+    API_BEGIN
+    KS_REQUIRE(fd && r && z && iters > 0 && ms_out, KS_EINVAL, "ks_fd_latency: bad arguments");
+    std::lock_guard<std::mutex> lk(fd->mu);
+    ensure_device(fd->device);
+    cudaStream_t st = fd->stream;
+    KS_CUDA(cudaStreamWaitEvent(st, fd->done, 0));
+    const double2* rd = reinterpret_cast<const double2*>(r);
+    double2* zd = reinterpret_cast<double2*>(z);
+    fd_apply_dev(fd, rd, zd, false, st, nullptr); // warm-up (lazy module loading)
+    cudaGraphExec_t ge = nullptr;
+    if (graph) {
+        cudaGraph_t g = nullptr;
+        KS_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        try {
+            fd_apply_dev(fd, rd, zd, false, st, nullptr);
+        } catch (...) {
+            cudaStreamEndCapture(st, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        KS_CUDA(cudaStreamEndCapture(st, &g));
+        const cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
+        cudaGraphDestroy(g);
+        KS_CUDA(e);
+        KS_CUDA(cudaGraphLaunch(ge, st)); // warm-up replay
+    }
+    cudaEvent_t a, b;
+    KS_CUDA(cudaEventCreate(&a));
+    KS_CUDA(cudaEventCreate(&b));
+    KS_CUDA(cudaEventRecord(a, st));
+    for (int it = 0; it < iters; ++it) {
+        if (ge) KS_CUDA(cudaGraphLaunch(ge, st));
+        else fd_apply_dev(fd, rd, zd, false, st, nullptr);
+    }
+    KS_CUDA(cudaEventRecord(b, st));
+    KS_CUDA(cudaEventSynchronize(b));
+    *ms_out = elapsed(a, b) / iters;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    if (ge) cudaGraphExecDestroy(ge);
+    KS_CUDA(cudaEventRecord(fd->done, st));
     API_END
 }
 

@@ -13,6 +13,9 @@
 
 #include "../../include/ks.h"
 
+struct ks_comm;
+struct ks_fdshard;
+
 namespace ks {
 
 // ---------------------------------------------------------------------------
@@ -81,6 +84,19 @@ struct DevBuf {
 };
 
 void ensure_device(int device);
+
+// NCCL communicator (ks_comm.cu): grouped point-to-point in doubles, in-place sum
+int comm_rank(const ks_comm* c);
+int comm_size(const ks_comm* c);
+void comm_group_start();
+void comm_group_end();
+void comm_send(const void* buf, size_t doubles, int peer, ks_comm* c, cudaStream_t st);
+void comm_recv(void* buf, size_t doubles, int peer, ks_comm* c, cudaStream_t st);
+void comm_allreduce_sum(double* buf, size_t count, ks_comm* c, cudaStream_t st);
+// sharded FD apply over a communicator (ks_shard.cu), device pointers, stream-ordered
+void fdshard_apply_comm(ks_fdshard* h, ks_comm* c, const double2* r_slab, double2* z_slab, cudaStream_t st);
+size_t fdshard_slab_n(const ks_fdshard* h);
+int fdshard_device(const ks_fdshard* h);
 // Opt `func` into `bytes` of dynamic shared memory on the CURRENT device. The
 // attribute is per device, so the cache is keyed by (device, function): a
 // handle on a second GPU in the same process gets its own opt-in.

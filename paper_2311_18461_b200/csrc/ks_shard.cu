@@ -97,6 +97,7 @@ struct ks_fdshard {
     FdBlocks blocks;                 // blocks of this rank's fibers
     DevBuf Lt, Mt, Wsym;
     DevBuf s0, s1, work2;
+    DevBuf csend, cwork, cback;      // ks_fdshard_apply (NCCL) exchange buffers
     cudaStream_t stream = nullptr;
     std::mutex mu;
     ~ks_fdshard() {
@@ -136,6 +137,49 @@ int ks_shard_plan(int d, const int* dims, int nranks, int rank, long long* slab_
     }
     API_END
 }
+
+} // extern "C"
+
+namespace ks {
+size_t fdshard_slab_n(const ks_fdshard* h) {
+    const Plan& P = h->plan;
+    return (size_t)P.nt * P.Np * P.slab[P.rank].n();
+}
+int fdshard_device(const ks_fdshard* h) { return h->device; }
+void fdshard_apply_comm(ks_fdshard* h, ks_comm* c, const double2* r, double2* z, cudaStream_t st) {
+    const Plan& P = h->plan;
+    KS_REQUIRE(comm_size(c) == P.nranks && comm_rank(c) == P.rank, KS_EINVAL,
+               "ks_fdshard_apply: communicator does not match the shard plan");
+    const size_t slab_n = fdshard_slab_n(h), work_n = (size_t)P.nt * P.rest[P.rank].n() * P.nd;
+    if (h->csend.bytes < slab_n * sizeof(double2)) h->csend.alloc(slab_n * sizeof(double2));
+    if (h->cback.bytes < slab_n * sizeof(double2)) h->cback.alloc(slab_n * sizeof(double2));
+    if (h->cwork.bytes < work_n * sizeof(double2)) h->cwork.alloc(work_n * sizeof(double2));
+    auto ok = [](int rc) {
+        if (rc != KS_OK) throw Error(rc, ks_last_error());
+    };
+    double2* sb = h->csend.as<double2>();
+    double2* wb = h->cwork.as<double2>();
+    double2* bb = h->cback.as<double2>();
+    ok(ks_fdshard_forward(h, reinterpret_cast<const ks_c64*>(r), reinterpret_cast<ks_c64*>(sb), st));
+    // all-to-all: block q of the send buffer to rank q, block q of the work tensor from rank q
+    comm_group_start();
+    for (int q = 0; q < P.nranks; ++q) {
+        comm_send(sb + P.sdisp1[q], 2 * (size_t)P.send1[q], q, c, st);
+        comm_recv(wb + P.rdisp1[q], 2 * (size_t)P.recv1[q], q, c, st);
+    }
+    comm_group_end();
+    ok(ks_fdshard_middle(h, reinterpret_cast<ks_c64*>(wb), st));
+    comm_group_start(); // and back
+    for (int q = 0; q < P.nranks; ++q) {
+        comm_send(wb + P.rdisp1[q], 2 * (size_t)P.recv1[q], q, c, st);
+        comm_recv(bb + P.sdisp1[q], 2 * (size_t)P.send1[q], q, c, st);
+    }
+    comm_group_end();
+    ok(ks_fdshard_backward(h, reinterpret_cast<const ks_c64*>(bb), reinterpret_cast<ks_c64*>(z), st));
+}
+} // namespace ks
+
+extern "C" {
 
 namespace {
 // transform of axis l (1-based): folded when the axis' eigenvectors are even/odd
@@ -479,6 +523,16 @@ int ks_ipc_open(const void* handle, void** dptr) {
 int ks_ipc_close(void* dptr) {
     API_BEGIN
     KS_CUDA(cudaIpcCloseMemHandle(dptr));
+    API_END
+}
+
+int ks_fdshard_apply(ks_fdshard* h, ks_comm* comm, const ks_c64* r_slab, ks_c64* z_slab, void* stream) {
+    API_BEGIN
+    KS_REQUIRE(h && comm && r_slab && z_slab, KS_EINVAL, "ks_fdshard_apply: NULL argument");
+    ensure_device(h->device);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : h->stream;
+    fdshard_apply_comm(h, comm, reinterpret_cast<const double2*>(r_slab), reinterpret_cast<double2*>(z_slab), st);
+    if (!stream) KS_CUDA(cudaStreamSynchronize(st));
     API_END
 }
 

@@ -52,7 +52,7 @@ def manufactured_job(d, p, n_el, n_el_t, keep_x=True):
     full = ref.extend(rep["x"], bnd)
     l2, en = ref.error_norms_named("sinsin", full)
     out = {"dims": ref.dims, "iterations": rep["iterations"], "converged": rep["converged"],
-           "l2": l2, "energy": en}
+           "l2": l2, "energy": en, "res_history": rep["res_history"]}
     if keep_x:
         out.update(rhs=rhs, bnd=bnd, x=rep["x"], full=full)
     return out

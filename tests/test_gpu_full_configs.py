@@ -115,16 +115,18 @@ def test_c2_manufactured_solve_vs_reference(gpu, ref_results):
 def test_c4_degree_sweep_iterations_vs_reference(gpu, ref_results, p):
     prob, Q, rhs, bnd, s, full, l2, en = _manufactured_gpu(gpu, 2, p, 128)
     ref = _get(ref_results, f"c4_p{p}")
-    print(f"c4 p={p}: iterations gpu {s.iterations} ref {ref['iterations']}; L2 gpu {l2:.6e} ref {ref['l2']:.6e}")
+    print(f"c4 p={p}: iterations gpu {s.iterations} ref {ref['iterations']}; L2 gpu {l2:.6e} ref {ref['l2']:.6e}; "
+          f"relres gpu {list(s.res_history)} ref {ref['res_history']}")
     assert list(ref["dims"]) == prob.reduced_dims()
     assert _within(rhs, ref["rhs"]) and _within(bnd, ref["bnd"])
     assert s.converged == ref["converged"] and abs(s.iterations - ref["iterations"]) <= 1
-    # the error functional on the reference's own solution: 1e-10
+    # the error functional on the reference's own solution: 1e-10 relative to
+    # the solution's scale (the error itself is ~1e-10 at p = 5: cancellation)
     l2r, enr = Q.error_norms(ref["full"], "sinsin", "sinsin")
-    assert abs(l2r - ref["l2"]) <= 1e-10 * ref["l2"] and abs(enr - ref["energy"]) <= 1e-10 * ref["energy"]
-    # end to end: two CG runs stopping at relres 1e-8 differ by up to ~1e-8 ||u||,
-    # which at the high degrees' L2 errors (~1e-7) is a 1e-5..1e-3 relative change
-    assert abs(l2 - ref["l2"]) <= 1e-3 * ref["l2"]
+    assert abs(l2r - ref["l2"]) <= 1e-10 * max(ref["l2"], 1e-3) and abs(enr - ref["energy"]) <= 1e-10 * max(ref["energy"], 1e-3)
+    # end to end: two CG runs stopping at relres 1e-8 differ by up to ~1e-8 ||u||
+    # (||u||_L2 = 1/2), which at p >= 4 is the size of the discretisation error
+    assert abs(l2 - ref["l2"]) <= 1e-3 * ref["l2"] + 1e-8
 
 
 def test_c5_shape_fd_apply_and_matvec_vs_reference(gpu, oracle, ref_results):
