@@ -12,6 +12,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -42,9 +43,17 @@ NcclApi& nccl() {
     static NcclApi api;
     static std::once_flag once;
     std::call_once(once, [] {
+        // an NCCL the process already loaded (e.g. PyTorch's, possibly newer than
+        // the system one) wins: loading a second copy under the same soname would
+        // make the other's symbols resolve against ours
         for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
-            api.so = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+            api.so = dlopen(name, RTLD_NOW | RTLD_NOLOAD);
             if (api.so) break;
+        }
+        if (const char* e = std::getenv("KS_NCCL_LIB"); !api.so && e) api.so = dlopen(e, RTLD_NOW);
+        for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+            if (api.so) break;
+            api.so = dlopen(name, RTLD_NOW);
         }
         if (!api.so) return;
         auto sym = [](const char* n) { return dlsym(api.so, n); };

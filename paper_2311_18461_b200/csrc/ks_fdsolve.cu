@@ -557,14 +557,16 @@ void launch_solve_p(const FdBlocks& B, double2* X, bool adjoint, cudaStream_t st
             check_launch("k_fd_ldl_pair");
             return;
         }
-        auto go = [&](auto kern, int tb) {
-            const size_t sm = (size_t)D * (P + 1) * tb * sizeof(double2) + (size_t)D * tb * sizeof(double);
+        auto go = [&](auto kern, int tb, int dr) {
+            const size_t sm = (size_t)dr * (P + 1) * tb * sizeof(double2) + (size_t)dr * tb * sizeof(double);
             smem_optin((const void*)kern, (int)sm);
             kern<<<(unsigned)((B.ns + tb - 1) / tb), tb, sm, st>>>(B.dinv.as<double>(), B.v.as<double2>(), X, B.ns,
                                                                   B.nt, B.gsz, B.fiber_block.as<int>());
         };
-        if (small) go(k_fd_ldl_ring<P, D, 32>, 32);
-        else go(k_fd_ldl_ring<P, D, 128>, 128);
+        // few fibers (c1, c2): the sweeps are one latency chain per fiber, so a
+        // 16-step ring keeps 15 steps of factor loads in flight per thread
+        if (small) go(k_fd_ldl_ring<P, 16, 32>, 32, 16);
+        else go(k_fd_ldl_ring<P, D, 128>, 128, D);
         check_launch("k_fd_ldl_ring");
         return;
     }

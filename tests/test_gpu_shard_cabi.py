@@ -60,6 +60,7 @@ def test_fdshard_and_halo_apply_single_rank_comm(gpu, oracle):
     """ks_fdshard_apply / ks_kronshard_apply_comm over a one-rank NCCL
     communicator equal the unsharded FD apply and matvec."""
     import ctypes as C
+    import torch  # noqa: F401  (PyTorch's NCCL loads first; libks then uses the same library)
     from paper_2311_18461_b200 import dist
     L = gpu.lib()
     a = setup_arrays(gpu, 3, 2, 10, 6)
