@@ -402,6 +402,13 @@ int ks_quad_rhs_finish(ks_quad* q, ks_c64* rhs /* reduced */, int mem);
 int ks_quad_lift(ks_quad* q, const ks_c64* g_greville, int mem, ks_c64* boundary, ks_c64* correction);
 /* extend_with_boundary (assembly.cpp:468-490); boundary may be NULL (zeros) */
 int ks_quad_extend(ks_quad* q, const ks_c64* reduced, const ks_c64* boundary, int mem, ks_c64* full);
+/* assemble_ultraweak's initial-datum term (assembly.cpp:572-640): rhs += i (u0, B_jt(0) phi_js)
+ * for the final-condition trial space (KS_EINVAL otherwise, as the reference's
+ * invalid_argument). u0: samples of the initial datum on the spatial quadrature
+ * grid (axis 1 fastest, ks_setup_quad_rule nodes), `mem`; rhs: the reduced load
+ * vector of f (ks_quad_rhs_*), updated in place, `rhs_mem`. The system operator
+ * of the ultraweak pair is the least-squares one (ks_setup_create_system). */
+int ks_quad_initial_term(ks_quad* q, const ks_c64* u0, int mem, ks_c64* rhs, int rhs_mem);
 /* error_norms (experiments.cpp:73-153): set the full coefficients, then per
  * chunk return sum w |u - u_h|^2 and sum w |f - S u_h|^2 (S u = i u_t - nu lap u);
  * L2 = sqrt(sum l2sq), energy = sqrt(sum l2sq + sum ressq) */

@@ -306,6 +306,23 @@ int ref_assemble_rhs_named(void* h, const char* name, std::complex<double>* rhs)
     }
 }
 
+// assemble_ultraweak (assembly.cpp:572-640) for a named solution: f and u0 = u(0, .)
+// (final-condition trial space; the reference throws otherwise)
+int ref_ultraweak_named(void* h, const char* name, std::complex<double>* rhs) {
+    auto* r = static_cast<RefProblem*>(h);
+    try {
+        const ManufacturedSolution s = solution_by_name(r, name);
+        auto u = s.u;
+        const SpaceFn u0 = [u](std::span<const double> x) { return u(0.0, x); };
+        const auto [A, b] = assemble_ultraweak(r->prob, s.f, u0);
+        std::copy(b.begin(), b.end(), rhs);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
 // error_norms (experiments.cpp:73-153) of full coefficients against a named solution
 int ref_error_norms_named(void* h, const char* name, const std::complex<double>* full, double* l2, double* energy) {
     auto* r = static_cast<RefProblem*>(h);

@@ -58,6 +58,8 @@ def rlib():
         L.ref_lift_named.argtypes = [P, C.c_char_p, P, P]
         L.ref_assemble_rhs_named.restype = I
         L.ref_assemble_rhs_named.argtypes = [P, C.c_char_p, P]
+        L.ref_ultraweak_named.restype = I
+        L.ref_ultraweak_named.argtypes = [P, C.c_char_p, P]
         L.ref_error_norms_named.restype = I
         L.ref_error_norms_named.argtypes = [P, C.c_char_p, P, C.POINTER(D), C.POINTER(D)]
         L.ref_infsup.restype = D
@@ -172,6 +174,14 @@ class RefProblem:
     def assemble_rhs_named(self, name):
         rhs = np.zeros(self.N, dtype=np.complex128)
         if rlib().ref_assemble_rhs_named(self._h, name.encode(), _p(rhs)):
+            raise ValueError(rlib().ref_last_error().decode())
+        return rhs
+
+    def ultraweak_named(self, name):
+        """assemble_ultraweak (assembly.cpp:572-640): the load vector of f plus the
+        initial-datum term i (u0, B(., 0)) for a named solution (u0 = u(0, .))."""
+        rhs = np.zeros(self.N, dtype=np.complex128)
+        if rlib().ref_ultraweak_named(self._h, name.encode(), _p(rhs)):
             raise ValueError(rlib().ref_last_error().decode())
         return rhs
 

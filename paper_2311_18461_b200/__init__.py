@@ -193,6 +193,7 @@ _SIGS = {
     "ks_quad_rhs_finish": (C.c_int, [_P, _P, C.c_int]),
     "ks_quad_lift": (C.c_int, [_P, _P, C.c_int, _P, _P]),
     "ks_quad_extend": (C.c_int, [_P, _P, _P, C.c_int, _P]),
+    "ks_quad_initial_term": (C.c_int, [_P, _P, C.c_int, _P, C.c_int]),
     "ks_quad_error_set": (C.c_int, [_P, _P, C.c_int]),
     "ks_quad_error_chunk": (C.c_int, [_P, C.c_int, C.c_int, _P, _P, C.c_int, C.POINTER(C.c_double),
                                       C.POINTER(C.c_double)]),
@@ -761,6 +762,20 @@ class Quadrature:
         out = np.zeros(self.prob.N_dof, dtype=np.complex128)
         _check(lib().ks_quad_rhs_finish(self._h, _ptr(out), KS_MEM_HOST))
         return out
+
+    def ultraweak(self, f, u0, device: int = 0):
+        """assemble_ultraweak (assembly.cpp:572-640) -> (A, rhs): the system
+        operator and the load vector of f plus the initial-datum term
+        i (u0, B_jt(0) phi_js); final-condition trial space only (InvalidArgument
+        otherwise, as the reference's invalid_argument). u0: vectorised callable
+        u0(x_1, .., x_d), sampled on the spatial quadrature grid."""
+        if self.prob.trial != "final":
+            raise InvalidArgument("assemble_ultraweak: problem must use the final-condition space")
+        A = assemble_system_operator(self.prob, device=device)
+        rhs = np.ascontiguousarray(self.assemble_rhs(f))
+        u0s = self._sample(lambda *x: u0(*x), self.nodes[1:])
+        _check(lib().ks_quad_initial_term(self._h, _ptr(u0s), KS_MEM_HOST, _ptr(rhs), KS_MEM_HOST))
+        return A, rhs
 
     def lift(self, g, f):
         """lift_nonhomogeneous: (corrected rhs, boundary coefficients on the full space)."""

@@ -706,6 +706,29 @@ int ks_quad_rhs_finish(ks_quad* q, ks_c64* rhs, int mem) {
     API_END
 }
 
+// interior of the spatial moments (full spatial dims fd -> reduced rd, axes 0..d-1)
+// added into the reduced space-time rhs at time index 0: rhs[js * nt] += i * bt0 * mom[js]
+__global__ void k_add_initial(const double2* __restrict__ mom, double2* __restrict__ rhs, size_t ns, int d, int4 rd,
+                              int4 fd, int nt, double bt0) {
+    const size_t js = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (js >= ns) return;
+    const int r[3] = {rd.x, rd.y, rd.z}, f[3] = {fd.x, fd.y, fd.z};
+    size_t t = js, full = 0, stride = 1;
+    for (int a = 0; a < d; ++a) {
+        const int ia = (int)(t % (size_t)r[a]);
+        t /= (size_t)r[a];
+        full += (size_t)(ia + 1) * stride; // drop the boundary index 0 on every spatial axis
+        stride *= (size_t)f[a];
+    }
+    const double2 m = mom[full];
+    double2 v = rhs[js * (size_t)nt];
+    // cplx(0, 1) * bt0[0] * mom: (0 + i) * bt0 = (0, bt0); times mom
+    const double2 c = make_double2(0.0 * bt0, 1.0 * bt0);
+    v.x += c.x * m.x - c.y * m.y;
+    v.y += c.x * m.y + c.y * m.x;
+    rhs[js * (size_t)nt] = v;
+}
+
 int ks_quad_lift(ks_quad* q, const ks_c64* g_grev, int mem, ks_c64* boundary, ks_c64* correction) {
     API_BEGIN
     KS_REQUIRE(q && g_grev && boundary && correction, KS_EINVAL, "ks_quad_lift: NULL argument");
@@ -742,6 +765,81 @@ int ks_quad_lift(ks_quad* q, const ks_c64* g_grev, int mem, ks_c64* boundary, ks
         KS_CUDA(cudaMemcpyAsync(correction, corr, q->Nred * sizeof(double2), cudaMemcpyDeviceToHost, q->stream));
     }
     KS_CUDA(cudaStreamSynchronize(q->stream));
+    API_END
+}
+
+// assemble_ultraweak's initial-datum term (assembly.cpp:580-637): rhs += i (u0, B_jt(0) phi_js)
+int ks_quad_initial_term(ks_quad* q, const ks_c64* u0, int mem, ks_c64* rhs, int rhs_mem) {
+    API_BEGIN
+    KS_REQUIRE(q && u0 && rhs, KS_EINVAL, "ks_quad_initial_term: NULL argument");
+    KS_REQUIRE(q->trial == 1, KS_EINVAL, "assemble_ultraweak: problem must use the final-condition space");
+    std::lock_guard<std::mutex> lk(q->mu);
+    ensure_device(q->device);
+    const int d = q->d;
+    // spatial quadrature samples: weights (reference order: w *= w_l for l = 0..d-1), then
+    // mode_product_transpose with each spatial evaluation matrix (order 0)
+    std::vector<int> dims(q->nq.begin() + 1, q->nq.end());
+    size_t n = 1, nfull = 1, nmax = 1;
+    for (int l = 0; l < d; ++l) {
+        n *= (size_t)dims[l];
+        nfull *= (size_t)q->full[l + 1];
+    }
+    {
+        size_t cur = n;
+        std::vector<int> dd = dims;
+        for (int l = 0; l < d; ++l) {
+            cur = cur / (size_t)dd[l] * (size_t)q->full[l + 1];
+            dd[l] = q->full[l + 1];
+            nmax = std::max(nmax, cur);
+        }
+        nmax = std::max(nmax, n);
+    }
+    DevBuf b0(nmax * sizeof(double2)), b1(nmax * sizeof(double2)), stage;
+    const double2* src = dev_in(q, u0, n, mem, stage);
+    int4 dm = make_int4(dims[0], d > 1 ? dims[1] : 1, d > 2 ? dims[2] : 1, 1);
+    const double* w[4] = {nullptr, nullptr, nullptr, nullptr};
+    for (int l = 0; l < d; ++l) w[l] = q->ax[l + 1].w.as<double>();
+    k_weight<<<blocks(n), 256, 0, q->stream>>>(src, b0.as<double2>(), n, d, dm, w[0], w[1], w[2], w[3], 0);
+    check_launch("k_weight");
+    double2* bufs[2] = {b0.as<double2>(), b1.as<double2>()};
+    int cb = 0;
+    for (int l = 0; l < d; ++l) {
+        const int nin = dims[l], nout = q->full[l + 1];
+        size_t sl = 1;
+        for (int k = 0; k < l; ++k) sl *= (size_t)dims[k];
+        size_t tot = 1;
+        for (int k = 0; k < d; ++k) tot *= (size_t)dims[k];
+        const size_t outer = tot / (sl * (size_t)nin);
+        auto& A = q->ax[l + 1];
+        k_mode_T<<<blocks(outer * (size_t)nout * sl), 256, 0, q->stream>>>(
+            bufs[cb], bufs[cb ^ 1], sl, nin, nout, outer, A.E[0].as<double>(), A.off.as<int>(), A.qb.as<int>(),
+            A.qe.as<int>(), q->p, 0, 0);
+        check_launch("k_mode_T");
+        dims[l] = nout;
+        cb ^= 1;
+    }
+    // add into the reduced rhs (final-condition space: time index 0 is kept, and
+    // on open knots only B_0 is nonzero at t = 0, with value 1)
+    const int nt = q->red[0];
+    size_t ns = 1;
+    for (int l = 0; l < d; ++l) ns *= (size_t)q->red[l + 1];
+    double2* out;
+    DevBuf ostage;
+    if (rhs_mem == KS_MEM_DEVICE) {
+        out = reinterpret_cast<double2*>(rhs);
+    } else {
+        ostage.alloc(q->Nred * sizeof(double2));
+        KS_CUDA(cudaMemcpyAsync(ostage.p, rhs, q->Nred * sizeof(double2), cudaMemcpyHostToDevice, q->stream));
+        out = ostage.as<double2>();
+    }
+    const int4 rd = make_int4(q->red[1], d > 1 ? q->red[2] : 1, d > 2 ? q->red[3] : 1, 1);
+    const int4 fd = make_int4(q->full[1], d > 1 ? q->full[2] : 1, d > 2 ? q->full[3] : 1, 1);
+    k_add_initial<<<blocks(ns), 256, 0, q->stream>>>(bufs[cb], out, ns, d, rd, fd, nt, 1.0);
+    check_launch("k_add_initial");
+    if (rhs_mem != KS_MEM_DEVICE)
+        KS_CUDA(cudaMemcpyAsync(rhs, out, q->Nred * sizeof(double2), cudaMemcpyDeviceToHost, q->stream));
+    KS_CUDA(cudaStreamSynchronize(q->stream));
+    (void)nfull;
     API_END
 }
 
