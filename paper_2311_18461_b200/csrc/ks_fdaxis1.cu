@@ -89,7 +89,7 @@ struct Axis1Args {
 // contiguous n1b-row run per factor array. Full / empty mbarriers per slot;
 // the producer runs D-1 steps ahead, across sweeps and slabs.
 template <int HB, int NCB, int P, int D, bool ODD>
-__global__ void __launch_bounds__(kThr + 96, 1) k_fd_axis1(Axis1Args a) {
+__global__ void __launch_bounds__(kThr + 128, 1) k_fd_axis1(Axis1Args a) {
     extern __shared__ __align__(16) double sm[];
     const int n1 = a.n1, n1b = a.n1b, hc = a.hc, no = n1 - hc, nt = a.nt, PD = a.PD, AP = a.AP;
     const size_t bufd = (size_t)(n1 + 4) * PD;                            // doubles per slab buffer
@@ -102,7 +102,11 @@ __global__ void __launch_bounds__(kThr + 96, 1) k_fd_axis1(Axis1Args a) {
     unsigned long long* full = bar + 2;                                    // [D]
     unsigned long long* empty = full + D;                                  // [D]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int nsolve = (int)blockDim.x - kThr; // solver threads (whole warps)
+    const int nsolve = 32 * ((n1 + 31) / 32);  // solver threads (whole warps), then one producer warp
+    const int pwarp = (kThr + nsolve) / 32;
+    // GEMM and solver warps meet once per step (named barrier 2; the producer
+    // warp runs ahead of both and never joins it)
+    auto step_bar = [&]() { asm volatile("bar.sync 2, %0;" ::"r"(kThr + nsolve) : "memory"); };
     const int ar = lane >> 2, ak = lane & 3;
     const unsigned rowbytes = (unsigned)nt * 16u;
     const int nmine = a.nslab > (int)blockIdx.x ? (a.nslab - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
@@ -267,60 +271,21 @@ __global__ void __launch_bounds__(kThr + 96, 1) k_fd_axis1(Axis1Args a) {
         };
         issue_load(0);
         forward(0);
-        __syncthreads();
+        step_bar();
         for (int t = 0; t < nmine; ++t) {
             const int nx = t + 1 < nmine ? t + 1 : -1;
             if (t >= 1) inverse(t - 1, nx);
             else if (nx >= 0) issue_load(nx);
             if (nx >= 0) forward(nx);
-            __syncthreads();
+            step_bar();
         }
         inverse(nmine - 1, -1);
-    } else {
-        // =================== solver warps ===================
-        const int m = tid - kThr;
-        const bool act = m < n1;
-        const size_t gsz = (size_t)n1b; // factor group = the slab's n1b blocks (FdBlocks::gsz)
+    } else if (warp == pwarp) {
+        // =================== producer warp (lane 0) ===================
+        if (lane != 0) return;
+        const size_t gsz = (size_t)n1b;
         const int nch = (nt + CK - 1) / CK;
         const int uses = 2 * nch; // ring uses per slab: forward chunks, then backward chunks (descending)
-        // producer (solver thread 0): ring use -> slot (use % D); its counters
-        // advance incrementally (no integer division on the per-chunk path)
-        int pt = 0, pu = 0, psl = 0, pwrap = 0;
-        size_t pg = (size_t)a.grp[slab_of(0)] * (size_t)nt; // group * nt
-        auto produce = [&]() {
-            if (pt >= nmine) return;
-            if (pwrap > 0) mwait(empty + psl, (unsigned)((pwrap - 1) & 1)); // slot's previous use consumed
-            const bool fwd = pu < nch;
-            const int c = fwd ? pu : uses - 1 - pu;
-            const int k0 = c * CK, nk = min(CK, nt - k0);
-            const unsigned vb = (unsigned)(nk * P) * (unsigned)gsz * 16u, db = (unsigned)nk * (unsigned)gsz * 8u;
-            double2* dv = rv + (size_t)psl * (slotd / 2);
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(full + psl)),
-                         "r"(vb + (fwd ? db : 0u))
-                         : "memory");
-            bulk(dv, a.v + (pg + k0) * P * gsz, vb, full + psl);
-            if (fwd)
-                bulk(reinterpret_cast<double*>(dv + (size_t)CK * P * gsz), a.dinv + (pg + k0) * gsz, db, full + psl);
-            if (++psl == D) psl = 0, ++pwrap;
-            if (++pu == uses) {
-                pu = 0;
-                if (++pt < nmine) pg = (size_t)a.grp[slab_of(pt)] * (size_t)nt;
-            }
-        };
-        if (tid == kThr)
-            for (int qq = 0; qq < D - 1; ++qq) produce();
-        int csl = 0;
-        unsigned cph = 0; // consumer: slot, full-barrier parity
-        auto take = [&]() -> const double2* {
-            mwait(full + csl, cph);
-            return rv + (size_t)csl * (slotd / 2);
-        };
-        auto give = [&]() { // release the slot; the producer refills D-1 uses ahead
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(empty + csl)) : "memory");
-            if (tid == kThr) produce();
-            if (++csl == D) csl = 0, cph ^= 1u;
-        };
-        const double2 Z = make_double2(0.0, 0.0);
         auto prefetch_group = [&](int t) { // a slab's whole factor group into L2 (2 bulk prefetches)
             const size_t g0 = (size_t)a.grp[slab_of(t)] * (size_t)nt * gsz;
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.v + g0 * P),
@@ -330,10 +295,48 @@ __global__ void __launch_bounds__(kThr + 96, 1) k_fd_axis1(Axis1Args a) {
                          "r"((unsigned)nt * (unsigned)gsz * 8u)
                          : "memory");
         };
-        if (tid == kThr) prefetch_group(0);
+        int psl = 0, pwrap = 0;
+        prefetch_group(0);
+        for (int pt = 0; pt < nmine; ++pt) {
+            if (pt + 1 < nmine) prefetch_group(pt + 1);
+            const size_t pg = (size_t)a.grp[slab_of(pt)] * (size_t)nt; // group * nt
+            for (int pu = 0; pu < uses; ++pu) {
+                if (pwrap > 0) mwait(empty + psl, (unsigned)((pwrap - 1) & 1)); // slot's previous use consumed
+                const bool fwd = pu < nch;
+                const int c = fwd ? pu : uses - 1 - pu;
+                const int k0 = c * CK, nk = min(CK, nt - k0);
+                const unsigned vb = (unsigned)(nk * P) * (unsigned)gsz * 16u, db = (unsigned)nk * (unsigned)gsz * 8u;
+                double2* dv = rv + (size_t)psl * (slotd / 2);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(full + psl)),
+                             "r"(vb + (fwd ? db : 0u))
+                             : "memory");
+                bulk(dv, a.v + (pg + k0) * P * gsz, vb, full + psl);
+                if (fwd)
+                    bulk(reinterpret_cast<double*>(dv + (size_t)CK * P * gsz), a.dinv + (pg + k0) * gsz, db,
+                         full + psl);
+                if (++psl == D) psl = 0, ++pwrap;
+            }
+        }
+    } else {
+        // =================== solver warps ===================
+        const int m = tid - kThr;
+        const bool act = m < n1;
+        const size_t gsz = (size_t)n1b; // factor group = the slab's n1b blocks (FdBlocks::gsz)
+        const int nch = (nt + CK - 1) / CK;
+        const int uses = 2 * nch; // ring uses per slab: forward chunks, then backward chunks (descending)
+        int csl = 0;
+        unsigned cph = 0; // consumer: slot, full-barrier parity
+        auto take = [&]() -> const double2* {
+            mwait(full + csl, cph);
+            return rv + (size_t)csl * (slotd / 2);
+        };
+        auto give = [&]() { // release the slot to the producer warp
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(empty + csl)) : "memory");
+            if (++csl == D) csl = 0, cph ^= 1u;
+        };
+        const double2 Z = make_double2(0.0, 0.0);
         for (int t = 0; t < nmine; ++t) {
-            __syncthreads(); // slab t is in buffer t & 1 (forward transform done)
-            if (tid == kThr && t + 1 < nmine) prefetch_group(t + 1);
+            step_bar(); // slab t is in buffer t & 1 (forward transform done)
             double2* row = reinterpret_cast<double2*>(S0 + (size_t)(t & 1) * bufd + (size_t)(act ? m : 0) * PD);
             double2 w[P + 1];
 #pragma unroll
@@ -343,9 +346,11 @@ __global__ void __launch_bounds__(kThr + 96, 1) k_fd_axis1(Axis1Args a) {
                 const double* sd = reinterpret_cast<const double*>(sv + (size_t)CK * P * gsz);
                 const int k0 = c * CK, nk = min(CK, nt - k0);
                 if (act) {
-                    // the chunk's factor rows into registers first (independent loads),
-                    // then the dependent sweep
-                    double2 vr[CK][P];
+                    // the chunk's factor rows and incoming x values into registers
+                    // first (independent loads), then the dependent sweep purely in
+                    // registers (the chain is two FP64 ops per step), then the
+                    // chunk's outputs back to the slab
+                    double2 vr[CK][P], xin[CK], zo[CK];
                     double dr[CK];
                     const int gm = (int)gsz;
 #pragma unroll
@@ -353,19 +358,21 @@ __global__ void __launch_bounds__(kThr + 96, 1) k_fd_axis1(Axis1Args a) {
                         dr[kk] = sd[kk * gm + m];
 #pragma unroll
                         for (int j = 0; j < P; ++j) vr[kk][j] = sv[(kk * P + j) * gm + m];
+                        const int ki = k0 + P + 1 + kk;
+                        xin[kk] = ki < nt ? row[ki] : Z;
                     }
 #pragma unroll
                     for (int kk = 0; kk < CK; ++kk) {
-                        if (kk < nk) {
-                            const int k = k0 + kk;
 #pragma unroll
-                            for (int j = 1; j <= P; ++j) w[j] = csub(w[j], cconjmul(vr[kk][j - 1], w[0]));
-                            row[k] = make_double2(w[0].x * dr[kk], w[0].y * dr[kk]);
+                        for (int j = 1; j <= P; ++j) w[j] = csub(w[j], cconjmul(vr[kk][j - 1], w[0]));
+                        zo[kk] = make_double2(w[0].x * dr[kk], w[0].y * dr[kk]);
 #pragma unroll
-                            for (int j = 0; j < P; ++j) w[j] = w[j + 1];
-                            w[P] = k + P + 1 < nt ? row[k + P + 1] : Z;
-                        }
+                        for (int j = 0; j < P; ++j) w[j] = w[j + 1];
+                        w[P] = xin[kk];
                     }
+#pragma unroll
+                    for (int kk = 0; kk < CK; ++kk)
+                        if (kk < nk) row[k0 + kk] = zo[kk];
                 }
                 give();
             }
@@ -386,21 +393,24 @@ __global__ void __launch_bounds__(kThr + 96, 1) k_fd_axis1(Axis1Args a) {
                     }
 #pragma unroll
                     for (int kk = CK - 1; kk >= 0; --kk) {
-                        if (kk < nk) {
+                        if (kk < nk) { // (steps past n_t only in the last chunk)
                             double2 x = zr[kk];
 #pragma unroll
                             for (int j = 1; j <= P; ++j) x = csub(x, cmul(vr[kk][j - 1], u[j]));
-                            row[k0 + kk] = x;
 #pragma unroll
                             for (int j = P; j > 1; --j) u[j] = u[j - 1];
                             u[1] = x;
+                            zr[kk] = x;
                         }
                     }
+#pragma unroll
+                    for (int kk = 0; kk < CK; ++kk)
+                        if (kk < nk) row[k0 + kk] = zr[kk];
                 }
                 give();
             }
         }
-        __syncthreads(); // matches the GEMM warps' last step barrier
+        step_bar(); // matches the GEMM warps' last step barrier
     }
 }
 
@@ -410,7 +420,7 @@ void launch_axis1(const Axis1Args& a, size_t sm, cudaStream_t st) {
     auto k = k_fd_axis1<HB, NCB, P, D, ODD>;
     smem_optin((const void*)k, (int)sm);
     const int grid = std::min(a.nslab, device_sms());
-    k<<<grid, kThr + 32 * ((a.n1 + 31) / 32), sm, st>>>(a);
+    k<<<grid, kThr + 32 * ((a.n1 + 31) / 32) + 32, sm, st>>>(a); // GEMM + solver + producer warps
     check_launch("k_fd_axis1");
 }
 
