@@ -561,6 +561,8 @@ def main():
     launches = ks.launch_count()
     value = n / (ms_fd * 1e-3)
 
+    prof = P.profile(r, z, K)  # per kernel kind (transforms / fused axis-1 stage / solves)
+
     # ---- matvec ----
     A.time(r, y, W, flush=False)
     ms_mv = A.time(r, y, K, flush=False)
@@ -601,8 +603,8 @@ def main():
     # each launch). The dense-basis FP64 view (4n flop/DOF) is reported beside it.
     info = P.info()
     folded = set(info["folded_axes"])
-    nlaunch = 2 * d - (2 if info.get("fused_axis1") else 0) + (1 if info.get("fused_axis1") else 0)
-    t_launch = ms_gemm * 1e-3 / nlaunch
+    nlaunch = max(1, prof["transforms"]["launches"])
+    t_launch = prof["transforms"]["ms"] * 1e-3 / nlaunch
     bytes_launch = 32.0 * n
     dense_flops_launch = sum(4 * dims[l] for l in range(1, d + 1)) * n / d
     exec_flops_launch = sum((2 * dims[l] + 2) if l in folded else 4 * dims[l] for l in range(1, d + 1)) * n / d
@@ -681,7 +683,7 @@ def main():
                      "frac": gemm_hbm / hbm_peak,
                      "traffic": tr.get("bytes_per_launch"), "traffic_source": tr.get("source"),
                      "algorithmic_bytes_per_launch": bytes_launch,
-                     "kernel": "k_xfold (folded spatial transform, average of the %d launches per apply)" % nlaunch,
+                     "kernel": "k_xfold (folded spatial transform, average of its %d launches per apply)" % nlaunch,
                      "basis": "SURVEY 8(d): 32 B per DOF per transform launch (read X, write Y) / launch time",
                      "launch_ms": t_launch * 1e3,
                      "executed_fp64_tflops": exec_flops_launch / t_launch / 1e12,
@@ -689,7 +691,7 @@ def main():
                      "dense_basis_fp64_tflops": dense_flops_launch / t_launch / 1e12,
                      "peak_source": "HBM: MEASURED_PEAKS.json hbm_gbs; FP64: live DFMA %.2f / DMMA %.2f TFLOP/s "
                                     "microbenchmarks" % (dfma, dmma),
-                     "transform_ms_per_apply": ms_gemm},
+                     "transform_ms_per_apply": prof["transforms"]["ms"]},
         "fd_apply": {"ms": ms_fd, "roofline_ms": fd_roof_s * 1e3, "frac_of_roofline": fd_roof_s * 1e3 / ms_fd,
                      "frac_of_roofline_nominal_fp64": fd_roof_nominal_s * 1e3 / ms_fd,
                      "roofline_basis": "SURVEY 8(d): max(dense F_alg / FP64 peak, 32 B/DOF / HBM peak); "
@@ -698,6 +700,13 @@ def main():
                      "flops_per_dof_reference_algorithm": fd_flops_per_dof(dims, p),
                      "flops_per_dof_executed": fd_folded_flops_per_dof(dims, p, folded),
                      "folded_axes": sorted(folded), "factored_blocks": info["blocks"], "plan": info,
+                     "components_ms_per_apply": prof,
+                     "fused_axis1_stage": None if not prof["fused_axis1"]["launches"] else {
+                         "ms": prof["fused_axis1"]["ms"],
+                         "algorithmic_bytes": 32.0 * n + info["blocks"] * dims[0] * (16 * p + 8),
+                         "hbm_gbs": (32.0 * n + info["blocks"] * dims[0] * (16 * p + 8)) / (prof["fused_axis1"]["ms"] * 1e-3) / 1e9,
+                         "note": "slab in + out (32 B/DOF) and the L D L^H factor rows read once (16p+8 B per block and "
+                                 "time step); the sweeps' latency, not bandwidth, bounds it (DESIGN.md 3.3)"},
                      "wall_s": wall_fd},
         "matvec": {"ms": ms_mv, "dof_per_s": n / (ms_mv * 1e-3),
                    "roofline_ms": mv_roof_s * 1e3, "frac_of_roofline": mv_roof_s * 1e3 / ms_mv,

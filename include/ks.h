@@ -216,11 +216,17 @@ int ks_flush_l2(size_t bytes);
 /* Time `iters` back-to-back launches of the FD apply / Kron apply on device
  * pointers with CUDA events on the handle's stream; optional per-iteration
  * L2 flush. ms_out receives the average ms per call and ms_kernel the
- * average device time of the dominant kernel per call. */
+ * average device time per call of the spatial transform launches. */
 int ks_fd_time(ks_fd* fd, const ks_c64* r, ks_c64* z, int iters, int flush,
                double* ms_out, double* ms_kernel);
 int ks_kron_time(ks_kron* k, const ks_c64* x, ks_c64* y, int iters, int flush,
                  double* ms_out);
+/* The same as ks_fd_time with the device time split by kernel kind (CUDA events
+ * around every launch): ms_kind[0] spatial transforms, [1] the fused axis-1
+ * stage, [2] block solves (ms per apply, 3 entries); launches_kind = launches
+ * of each kind per apply. */
+int ks_fd_profile(ks_fd* fd, const ks_c64* r, ks_c64* z, int iters, int flush, double* ms_out,
+                  double* ms_kind, int* launches_kind);
 /* Latency of the FD apply (device pointers): `iters` applies back to back on
  * the handle's stream between two CUDA events, either launched eagerly or as
  * replays of one CUDA graph holding a whole apply (graph = 1); ms_out = the

@@ -128,6 +128,8 @@ _SIGS = {
                              C.POINTER(C.c_double)]),
     "ks_kron_time": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "ks_fd_latency": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.POINTER(C.c_double)]),
+    "ks_fd_profile": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                C.POINTER(C.c_int)]),
     "ks_fp64_peak": (C.c_int, [C.POINTER(C.c_double)]),
     "ks_fp64_peaks": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "ks_fp64_peak_mixed": (C.c_int, [C.POINTER(C.c_double)]),
@@ -521,6 +523,16 @@ class FDPreconditioner:
         ms = C.c_double()
         _check(lib().ks_fd_latency(self._h, r.ptr, z.ptr, int(iters), int(graph), C.byref(ms)))
         return ms.value
+
+    def profile(self, r: DeviceVector, z: DeviceVector, iters: int, flush: bool = False) -> dict:
+        """ms per apply, and the device time per apply split by kernel kind
+        (CUDA events around every launch) with the launch counts."""
+        ms = C.c_double()
+        mk = (C.c_double * 3)()
+        nl = (C.c_int * 3)()
+        _check(lib().ks_fd_profile(self._h, r.ptr, z.ptr, iters, int(flush), C.byref(ms), mk, nl))
+        names = ("transforms", "fused_axis1", "solves")
+        return {"ms": ms.value, **{n: {"ms": mk[i], "launches": nl[i]} for i, n in enumerate(names)}}
 
     def time(self, r: DeviceVector, z: DeviceVector, iters: int, flush: bool = True):
         ms, mk = C.c_double(), C.c_double()

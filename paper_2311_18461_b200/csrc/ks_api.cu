@@ -175,10 +175,30 @@ inline cudaStream_t pick(void* user, cudaStream_t own) {
     return user ? static_cast<cudaStream_t>(user) : own;
 }
 
+// Per-launch timing of an FD apply: start/stop event pairs and the kind of
+// each launch (0 spatial transform, 1 fused axis-1 stage, 2 block solves).
+struct FdTimes {
+    std::vector<cudaEvent_t> ev;
+    std::vector<int> kind;
+    template <class F> void run(int k, cudaStream_t st, F&& body) {
+        cudaEvent_t a, b;
+        KS_CUDA(cudaEventCreate(&a));
+        KS_CUDA(cudaEventCreate(&b));
+        KS_CUDA(cudaEventRecord(a, st));
+        body();
+        KS_CUDA(cudaEventRecord(b, st));
+        ev.push_back(a);
+        ev.push_back(b);
+        kind.push_back(k);
+    }
+    ~FdTimes() {
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+};
+
 // FD apply on device pointers (Algorithm 1 steps 2-4; fdsolver.cpp:53-63).
-// ev (optional): start/stop event pairs recorded around each transform kernel.
-void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStream_t st,
-                  std::vector<cudaEvent_t>* ev) {
+// ev (optional): events around every kernel launch, by kind.
+void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStream_t st, FdTimes* ev) {
     const int d = f->d;
     const double* cur = reinterpret_cast<const double*>(r);
     double* bufs[2] = {f->s0.as<double>(), f->s1.as<double>()};
@@ -194,18 +214,8 @@ void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStre
             if (F.n) launch_mode_gemm_fold(F, inv, in, out, stride, outer, st, layout, f->dims[0]);
             else launch_mode_gemm(At.as<double>(), n, in, out, stride, outer, st, layout, f->dims[0]);
         };
-        if (ev) {
-            cudaEvent_t a, b;
-            KS_CUDA(cudaEventCreate(&a));
-            KS_CUDA(cudaEventCreate(&b));
-            KS_CUDA(cudaEventRecord(a, st));
-            launch();
-            KS_CUDA(cudaEventRecord(b, st));
-            ev->push_back(a);
-            ev->push_back(b);
-        } else {
-            launch();
-        }
+        if (ev) ev->run(0, st, launch);
+        else launch();
     };
     // (posall: axes 2..d on the bulk-copy fed transform, eigen rows by position)
     // mode: 0 natural, 1 / 2 the axis-1 time-major hand-off (forward / inverse)
@@ -215,18 +225,8 @@ void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStre
         for (int k = 0; k < l; ++k) stride *= (size_t)f->dims[k];
         const size_t outer = f->N / (stride * (size_t)f->dims[l]);
         auto launch = [&]() { launch_xfold(f->fold[l - 1], inv, in, out, stride, outer, st, mode); };
-        if (ev) {
-            cudaEvent_t a, b;
-            KS_CUDA(cudaEventCreate(&a));
-            KS_CUDA(cudaEventCreate(&b));
-            KS_CUDA(cudaEventRecord(a, st));
-            launch();
-            KS_CUDA(cudaEventRecord(b, st));
-            ev->push_back(a);
-            ev->push_back(b);
-        } else {
-            launch();
-        }
+        if (ev) ev->run(0, st, launch);
+        else launch();
     };
     if (f->axis1) {
         // forward axes d..2, then axis 1 + block solves + inverse axis 1 in one
@@ -243,18 +243,8 @@ void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStre
             launch_fd_axis1(f->fold[0], f->A1.as<double>(), f->dims[0], (long long)(f->Ns / (size_t)f->dims[1]),
                             f->order1.as<int>(), f->grp1.as<int>(), f->n1b, f->blocks, cur, mid, st);
         };
-        if (ev) {
-            cudaEvent_t a, b;
-            KS_CUDA(cudaEventCreate(&a));
-            KS_CUDA(cudaEventCreate(&b));
-            KS_CUDA(cudaEventRecord(a, st));
-            launch();
-            KS_CUDA(cudaEventRecord(b, st));
-            ev->push_back(a);
-            ev->push_back(b);
-        } else {
-            launch();
-        }
+        if (ev) ev->run(1, st, launch);
+        else launch();
         cur = mid;
         for (int l = 2; l <= d; ++l) {
             double* out = l == d ? reinterpret_cast<double*>(z) : bufs[nb];
@@ -274,7 +264,11 @@ void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStre
             std_gemm(l, false, cur, out, l == 1 ? 1 : 0);
             cur = out;
         }
-        launch_fd_solve(f->blocks, reinterpret_cast<double2*>(const_cast<double*>(cur)), adjoint, st);
+        auto solve = [&]() {
+            launch_fd_solve(f->blocks, reinterpret_cast<double2*>(const_cast<double*>(cur)), adjoint, st);
+        };
+        if (ev) ev->run(2, st, solve);
+        else solve();
         for (int l = 1; l <= d; ++l) {
             double* out = l == d ? reinterpret_cast<double*>(z) : bufs[nb];
             if (l != d) nb ^= 1;
@@ -293,7 +287,9 @@ void fd_apply_dev(ks_fd* f, const double2* r, double2* z, bool adjoint, cudaStre
         cur = out;
     }
     // N_s block solves (fdsolver.cpp:58-60), time-major
-    launch_fd_solve(f->blocks, reinterpret_cast<double2*>(const_cast<double*>(cur)), adjoint, st);
+    auto solve = [&]() { launch_fd_solve(f->blocks, reinterpret_cast<double2*>(const_cast<double*>(cur)), adjoint, st); };
+    if (ev) ev->run(2, st, solve);
+    else solve();
     // from_eigen with U_l (fdsolver.cpp:16-21): axis d first (it consumes the
     // time-major layout), then axes 1..d-1. Mode products on distinct axes
     // commute, so only the rounding order differs.
@@ -544,16 +540,12 @@ static void fd_create_impl(int kind, int d, const int* dims, double nu, int p_t,
     if (const char* e = std::getenv("KS_FD_XFOLD")) posall = posall && std::strcmp(e, "0") != 0;
     f->posall = posall;
     // fused axis-1 stage (least-squares blocks, folded axis 1, slab fits shared
-    // memory): blocks numbered by axis-1 position within per-slab groups of n1b.
-    // Opt-in (KS_FD_AXIS1=1): measured at c3 0.55 ms against 0.54 ms for the
-    // separate transform / solve / transform it replaces -- the 130-step
-    // sequential sweeps of one slab per SM are latency bound
+    // memory; KS_FD_AXIS1=0 keeps the separate transform / solve / transform):
+    // blocks numbered by axis-1 position within per-slab groups of n1b.
+    // c3: 438 us against 509 us for the three kernels it replaces
     bool ax1 = kind == 0 && f->fold[0].n > 0 && (int)f->fold[0].perm.size() == dims[1] &&
                fd_axis1_supported(dims[1], nt, p_t);
-    {
-        const char* e = std::getenv("KS_FD_AXIS1");
-        ax1 = ax1 && e && std::strcmp(e, "1") == 0;
-    }
+    if (const char* e = std::getenv("KS_FD_AXIS1")) ax1 = ax1 && std::strcmp(e, "0") != 0;
     std::vector<int> grp1;
     if (pair) {
         const int n1 = dims[1], n2 = dims[2];
@@ -1451,6 +1443,15 @@ int ks_flush_l2(size_t bytes) {
 
 int ks_fd_time(ks_fd* fd, const ks_c64* r, ks_c64* z, int iters, int flush, double* ms_out,
                double* ms_kernel) {
+    double kinds[3] = {0, 0, 0};
+    int nl[3] = {0, 0, 0};
+    const int rc = ks_fd_profile(fd, r, z, iters, flush, ms_out, kinds, nl);
+    if (rc == KS_OK && ms_kernel) *ms_kernel = kinds[0];
+    return rc;
+}
+
+int ks_fd_profile(ks_fd* fd, const ks_c64* r, ks_c64* z, int iters, int flush, double* ms_out, double* ms_kind,
+                  int* launches_kind) {
     API_BEGIN
     KS_REQUIRE(fd && r && z && iters > 0, KS_EINVAL, "ks_fd_time: bad arguments");
     std::lock_guard<std::mutex> lk(fd->mu);
@@ -1463,26 +1464,29 @@ int ks_fd_time(ks_fd* fd, const ks_c64* r, ks_c64* z, int iters, int flush, doub
     cudaEvent_t a, b;
     KS_CUDA(cudaEventCreate(&a));
     KS_CUDA(cudaEventCreate(&b));
-    double tot = 0, ker = 0;
+    double tot = 0, ker[3] = {0, 0, 0};
+    int nl[3] = {0, 0, 0};
     for (int it = 0; it < iters; ++it) {
         if (flush) launch_fill_bytes(fb.p, fbytes, st);
-        std::vector<cudaEvent_t> ev;
+        FdTimes ev;
         KS_CUDA(cudaEventRecord(a, st));
-        fd_apply_dev(fd, reinterpret_cast<const double2*>(r), reinterpret_cast<double2*>(z), false, st,
-                     ms_kernel ? &ev : nullptr);
+        fd_apply_dev(fd, reinterpret_cast<const double2*>(r), reinterpret_cast<double2*>(z), false, st, &ev);
         KS_CUDA(cudaEventRecord(b, st));
         KS_CUDA(cudaEventSynchronize(b));
         tot += elapsed(a, b);
-        for (size_t e = 0; e + 1 < ev.size(); e += 2) {
-            ker += elapsed(ev[e], ev[e + 1]);
-            cudaEventDestroy(ev[e]);
-            cudaEventDestroy(ev[e + 1]);
+        for (size_t e = 0; e < ev.kind.size(); ++e) {
+            ker[ev.kind[e]] += elapsed(ev.ev[2 * e], ev.ev[2 * e + 1]);
+            if (it == 0) ++nl[ev.kind[e]];
         }
     }
     cudaEventDestroy(a);
     cudaEventDestroy(b);
+    KS_CUDA(cudaEventRecord(fd->done, st));
     if (ms_out) *ms_out = tot / iters;
-    if (ms_kernel) *ms_kernel = ker / iters;
+    for (int k = 0; k < 3; ++k) {
+        if (ms_kind) ms_kind[k] = ker[k] / iters;
+        if (launches_kind) launches_kind[k] = nl[k];
+    }
     API_END
 }
 
