@@ -129,9 +129,12 @@ def test_c4_degree_sweep_iterations_vs_reference(gpu, ref_results, p):
         # iteration straddles the tolerance within a factor 2
         assert ref["res_history"][s.iterations - 1] <= 2 * 1e-8, (s.iterations, ref["res_history"])
     # the error functional on the reference's own solution: 1e-10 relative to
-    # the solution's scale (the error itself is ~1e-10 at p = 5: cancellation)
+    # the solution's scale (the L2 error itself is ~1e-10 at p = 5 and the energy
+    # error below 1e-3 at p = 6: the functional sums squares of differences of O(1)
+    # values, so its rounding is ~1e-13 absolute; the floors 1e-3 (L2, where
+    # ||u|| = 1/2) and 1e-2 (energy, derivative scale ~pi) bound that)
     l2r, enr = Q.error_norms(ref["full"], "sinsin", "sinsin")
-    assert abs(l2r - ref["l2"]) <= 1e-10 * max(ref["l2"], 1e-3) and abs(enr - ref["energy"]) <= 1e-10 * max(ref["energy"], 1e-3)
+    assert abs(l2r - ref["l2"]) <= 1e-10 * max(ref["l2"], 1e-3) and abs(enr - ref["energy"]) <= 1e-10 * max(ref["energy"], 1e-2)
     # end to end: two CG runs stopping at relres 1e-8 differ by up to ~1e-8 ||u||
     # (||u||_L2 = 1/2), which at p >= 4 is the size of the discretisation error
     assert abs(l2 - ref["l2"]) <= 1e-3 * ref["l2"] + 1e-8

@@ -1,6 +1,6 @@
 """Time the c3 FD apply under environment variants (one subprocess each, since
 layout switches are read at handle creation).
-usage: python tools/fd_sweep.py 'KS_FD_REC=0 KS_FD_PFD=0' 'KS_FD_REC=1 KS_FD_PFD=8' ..."""
+usage: python tools/fd_sweep.py 'KS_FD_AXIS1=0' 'KS_FD_AXIS1=1' ..."""
 import os
 import subprocess
 import sys

@@ -21,7 +21,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
     --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-solve > gpurun_out/ncu_launch.log 2>&1
 fi
 python tools/prof_c3.py c3 > gpurun_out/prof_plain.log 2>&1
-for spec in "fd:k_mode_gemm_fold|k_fd_solve_pair:7:7" "mv:ks_pair:26:2"; do
+for spec in "fd:k_xfold|k_fd_axis1:5:5" "mv:ks_pair:26:2"; do
   IFS=: read name rx skip cnt <<< "$spec"
   timeout 900 ncu -f --set full --clock-control none --import-source on -k regex:"$rx" -s $skip -c $cnt \
       -o /tmp/prof_$name python tools/prof_c3.py c3 > gpurun_out/ncu_$name.log 2>&1
