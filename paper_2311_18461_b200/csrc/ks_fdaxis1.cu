@@ -41,7 +41,10 @@ namespace ks {
 
 namespace {
 
-constexpr int kThr = 256;
+constexpr int kNG = 9;            // GEMM warps (warps with (warp & 3) != 3)
+// 12 warps (n1 <= 64: HB <= 4): 9 GEMM, solver warps 3 and 7, producer warp 11;
+// 13 warps (HB = 5): solver warps 3, 7, 11, producer warp 12
+constexpr int axis1_warps(int HB) { return HB >= 5 ? 13 : 12; }
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -49,13 +52,6 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                  : "d"(a), "d"(b));
 }
 __device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
-}
-__device__ __forceinline__ double2 cconjmul(double2 a, double2 b) { // conj(a) * b
-    return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
-}
 
 struct Axis1Args {
     const double* A;       // [2][SZ][AP] se / so, element (j, m) at j*AP + m, zero padded
@@ -67,57 +63,73 @@ struct Axis1Args {
     const double2* v;
     long long nblk;
     int nslab, n1, n1b, hc, nt, PD, AP, SZ, K4, CB;
-
+    int nbuf, padr, asm_, ring; // slab buffers (2 or 3), zero rows after the slab, se / so in shared memory, factor ring slots
 };
 
-// Warp-specialised software pipeline, one CTA per SM, two slab buffers:
-// at step t the solver warps sweep slab t in one buffer while the 8 GEMM warps
-// run the inverse transform + store of slab t-1 and then load + forward-
-// transform slab t+1 in the other; one CTA-wide barrier per step. The DMMA
-// work (the folded transforms, ~4.4 us per c3 slab at the SM's FP64 peak) and
-// the latency-bound sweeps (2 n_t dependent steps) overlap instead of
-// alternating.
+// Warp-specialised software pipeline, one CTA per SM, NB slab buffers (the
+// plan uses 2; 3 would fit c3 only without the factor ring): at step t the
+// solver warps sweep slab t in buffer t % NB while the 9 GEMM warps run the
+// inverse transform + store of slab t-1, issue the load of slab t+NB-1 into
+// the buffer that just became free, and forward-transform slab t+1; one named
+// barrier per step. The DMMA work (the folded
+// transforms) and the latency-bound sweeps (2 n_t dependent steps) overlap
+// instead of alternating.
 //
-// GEMM warp w owns the 8-double column blocks w, w+8, w+16 of the slab and
+// GEMM warp w owns the 8-double column blocks w, w+9, w+18 of the slab and
 // computes both halves (even and odd eigenvectors) for them: one fold
 // (X[j] +- X[n1-1-j]) per loaded pair, the inverse unfold (e_j +- o_j) in
-// registers, and no shared-memory traffic between warps.
+// registers, and no shared-memory traffic between warps. The half matrices
+// se / so live in shared memory when they fit (ASM), else they come through L1.
 //
 // Solver thread m (position m) streams its factor rows from a D-slot ring in
-// shared memory that one producer thread fills with bulk copies: the slab's
-// blocks are consecutive (m + n1b * grp[o]), so step k of every fiber is one
-// contiguous n1b-row run per factor array. Full / empty mbarriers per slot;
-// the producer runs D-1 steps ahead, across sweeps and slabs.
-template <int HB, int NCB, int P, int D, bool ODD>
-__global__ void __launch_bounds__(kThr + 128, 1) k_fd_axis1(Axis1Args a) {
+// shared memory that one producer thread (a scheduler-3 warp without fibers)
+// fills with bulk copies: the slab's blocks are consecutive (m + n1b * grp[o]),
+// so step k of every fiber is one contiguous n1b-row run per factor array.
+// Full / empty mbarriers per slot of 4 steps; the producer runs D-1 slots
+// ahead, across sweeps and slabs, and bulk-prefetches the next slab's factor
+// group into L2. (Reading the rows straight from global memory into registers
+// one chunk ahead was measured slower, 0.58 vs 0.43 ms at c3: a 4-step lead
+// does not cover the L2 latency and registers do not allow a longer one.) The
+// recurrences are written so that only two dependent FMAs per step sit on the
+// chain (the contribution of the newest value is applied last).
+template <int HB, int NCB, int P, bool ODD, bool ASM>
+__global__ void __launch_bounds__(32 * axis1_warps(HB), 1) k_fd_axis1(Axis1Args a) {
     extern __shared__ __align__(16) double sm[];
-    const int n1 = a.n1, n1b = a.n1b, hc = a.hc, no = n1 - hc, nt = a.nt, PD = a.PD, AP = a.AP;
-    const size_t bufd = (size_t)(n1 + 4) * PD;                            // doubles per slab buffer
-    double* S0 = sm;                                                      // [2][n1 + 4][PD]
+    const int n1 = a.n1, n1b = a.n1b, hc = a.hc, no = n1 - hc, nt = a.nt, PD = a.PD, AP = a.AP, NB = a.nbuf;
+    const size_t bufd = (size_t)(n1 + a.padr) * PD;                       // doubles per slab buffer
+    double* S0 = sm;                                                      // [NB][n1 + padr][PD]
+    double* Asm = S0 + (size_t)NB * bufd;                                 // [2][SZ][AP] (ASM)
     // factor ring: D slots of CK time steps, slot = [CK][P][n1b] v rows then [CK][n1b] 1/d
-    constexpr int CK = 8;
-    const size_t slotd = (size_t)CK * n1b * (2 * P + 1);                   // doubles per slot
-    double2* rv = reinterpret_cast<double2*>(S0 + 2 * bufd);
-    unsigned long long* bar = reinterpret_cast<unsigned long long*>(S0 + 2 * bufd + (size_t)D * slotd); // [2] slab loads
-    unsigned long long* full = bar + 2;                                    // [D]
-    unsigned long long* empty = full + D;                                  // [D]
+    constexpr int CK = 4;
+    const int D = a.ring;
+    const size_t slotd = (size_t)CK * n1b * (2 * P + 1);                  // doubles per slot
+    double2* rv = reinterpret_cast<double2*>(Asm + (ASM ? (size_t)2 * a.SZ * AP : 0));
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(reinterpret_cast<double*>(rv) + (size_t)D * slotd); // [NB]
+    unsigned long long* full = bar + NB;                                  // [D]
+    unsigned long long* empty = full + D;                                 // [D]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int nsolve = 32 * ((n1 + 31) / 32);  // solver threads (whole warps), then one producer warp
-    const int pwarp = (kThr + nsolve) / 32;
-    // GEMM and solver warps meet once per step (named barrier 2; the producer
-    // warp runs ahead of both and never joins it)
-    auto step_bar = [&]() { asm volatile("bar.sync 2, %0;" ::"r"(kThr + nsolve) : "memory"); };
+    const int nsolve = 32 * ((n1 + 31) / 32);  // solver threads (whole warps)
+    // Warp roles by scheduler: warps 3, 7, 11 (scheduler 3) run the sweeps, the
+    // other nine the DMMA transforms -- the sweeps' dependent DFMA chains do not
+    // queue behind 16-cycle DMMAs on a shared FP64 pipe (ncu: the solver warps
+    // sat in math-pipe throttle and were the step's critical path), and nine
+    // GEMM warps split the 17 column blocks of a c3 slab 2,2,..,1 instead of 3,2,..
+    constexpr int NW = axis1_warps(HB);
+    const bool producer = warp == NW - 1;
+    const bool solver = !producer && (warp & 3) == 3;
+    // GEMM and solver warps meet once per step (named barrier 2)
+    auto step_bar = [&]() { asm volatile("bar.sync 2, %0;" ::"r"(32 * kNG + nsolve) : "memory"); };
     const int ar = lane >> 2, ak = lane & 3;
     const unsigned rowbytes = (unsigned)nt * 16u;
     const int nmine = a.nslab > (int)blockIdx.x ? (a.nslab - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
     auto slab_of = [&](int t) -> long long { return a.order[blockIdx.x + (size_t)t * gridDim.x]; };
 
-    for (int e = tid; e < 4 * PD; e += blockDim.x) {
-        S0[(size_t)n1 * PD + e] = 0.0; // padding rows (finite) of both buffers
-        S0[bufd + (size_t)n1 * PD + e] = 0.0;
-    }
+    for (int b = 0; b < NB; ++b)
+        for (int e = tid; e < a.padr * PD; e += blockDim.x) S0[b * bufd + (size_t)n1 * PD + e] = 0.0; // padding rows (finite)
+    if (ASM)
+        for (int e = tid; e < 2 * a.SZ * AP; e += blockDim.x) Asm[e] = __ldg(a.A + e);
     if (tid == 0) {
-        for (int q = 0; q < 2; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bar + q)) : "memory");
+        for (int q = 0; q < NB; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bar + q)) : "memory");
         for (int q = 0; q < D; ++q) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(full + q)) : "memory");
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(empty + q)), "r"(nsolve) : "memory");
@@ -143,27 +155,66 @@ __global__ void __launch_bounds__(kThr + 128, 1) k_fd_axis1(Axis1Args a) {
                      : "memory");
     };
 
-    if (tid < kThr) {
+    if (producer) {
+        // ---- producer: lane 0 fills the factor ring ----
+        if (lane != 0) return;
+        const size_t gsz = (size_t)n1b;
+        const int nch = (nt + CK - 1) / CK;
+        const int nuse = 2 * nch; // ring uses per slab: forward chunks 0..nch-1, then backward chunks nch-1..0
+        auto prefetch_group = [&](int t) { // a slab's whole factor group into L2 (2 bulk prefetches)
+            const size_t g0 = (size_t)a.grp[slab_of(t)] * (size_t)nt * gsz;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.v + g0 * P),
+                         "r"((unsigned)(nt * P) * (unsigned)gsz * 16u)
+                         : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.dinv + g0),
+                         "r"((unsigned)nt * (unsigned)gsz * 8u)
+                         : "memory");
+        };
+        int psl = 0, pwrap = 0;
+        prefetch_group(0);
+        for (int pt = 0; pt < nmine; ++pt) {
+            if (pt + 1 < nmine) prefetch_group(pt + 1);
+            const size_t pg = (size_t)a.grp[slab_of(pt)] * (size_t)nt; // group * nt
+            for (int pu = 0; pu < nuse; ++pu) {
+                if (pwrap > 0) mwait(empty + psl, (unsigned)((pwrap - 1) & 1)); // slot's previous use consumed
+                const bool fwd = pu < nch;
+                const int c = fwd ? pu : nuse - 1 - pu;
+                const int k0 = c * CK, nk = min(CK, nt - k0);
+                const unsigned vb = (unsigned)(nk * P) * (unsigned)gsz * 16u, db = (unsigned)nk * (unsigned)gsz * 8u;
+                double2* dv = rv + (size_t)psl * (slotd / 2);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(full + psl)),
+                             "r"(vb + (fwd ? db : 0u))
+                             : "memory");
+                bulk(dv, a.v + (pg + k0) * P * gsz, vb, full + psl);
+                if (fwd)
+                    bulk(reinterpret_cast<double*>(dv + (size_t)CK * P * gsz), a.dinv + (pg + k0) * gsz, db, full + psl);
+                if (++psl == D) psl = 0, ++pwrap;
+            }
+        }
+    } else if (!solver) {
         // =================== GEMM warps ===================
-        const int w = warp;
-        unsigned phase[2] = {0u, 0u};
-        const double* Ae = a.A;
-        const double* Ao = a.A + (size_t)a.SZ * AP;
-        auto issue_load = [&](int t) { // warp 0: slab t -> buffer t & 1
-            if (w != 0) return;
-            double* Sx = S0 + (size_t)(t & 1) * bufd;
+        const int w = warp - (warp >> 2); // 0..8
+        unsigned phase = 0u; // bit b: parity of buffer b's next load completion
+        const double* Ae = ASM ? Asm : a.A;
+        const double* Ao = Ae + (size_t)a.SZ * AP;
+        auto lda = [&](const double* p) -> double { return ASM ? *p : __ldg(p); };
+        auto issue_load = [&](int t) { // warp 0: slab t -> buffer t % NB
+            if (w != 0 || t >= nmine) return;
+            const int b = t % NB;
+            double* Sx = S0 + (size_t)b * bufd;
             const double* Xs = a.X + (size_t)slab_of(t) * n1 * nt * 2;
             if (lane == 0)
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar + (t & 1))),
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar + b)),
                              "r"(rowbytes * (unsigned)n1)
                              : "memory");
             __syncwarp();
-            for (int i = lane; i < n1; i += 32) bulk(Sx + (size_t)i * PD, Xs + (size_t)i * nt * 2, rowbytes, bar + (t & 1));
+            for (int i = lane; i < n1; i += 32) bulk(Sx + (size_t)i * PD, Xs + (size_t)i * nt * 2, rowbytes, bar + b);
         };
         auto forward = [&](int t) {
-            double* Sx = S0 + (size_t)(t & 1) * bufd;
-            mwait(bar + (t & 1), phase[t & 1]);
-            phase[t & 1] ^= 1u;
+            const int b = t % NB;
+            double* Sx = S0 + (size_t)b * bufd;
+            mwait(bar + b, (phase >> b) & 1u);
+            phase ^= 1u << b;
             double ae_[HB][NCB][2], ao_[HB][NCB][2];
 #pragma unroll
             for (int r = 0; r < HB; ++r)
@@ -174,15 +225,15 @@ __global__ void __launch_bounds__(kThr + 128, 1) k_fd_axis1(Axis1Args a) {
                 double fe[HB], fo[HB];
 #pragma unroll
                 for (int r = 0; r < HB; ++r) {
-                    fe[r] = __ldg(Ae + (size_t)j * AP + 8 * r + ar);
-                    fo[r] = __ldg(Ao + (size_t)j * AP + 8 * r + ar);
+                    fe[r] = lda(Ae + (size_t)j * AP + 8 * r + ar);
+                    fo[r] = lda(Ao + (size_t)j * AP + 8 * r + ar);
                 }
                 const double* top = Sx + (size_t)j * PD;
-                const double* bot = Sx + (size_t)(n1 - 1 - j) * PD;
+                const double* bot = Sx + (size_t)max(n1 - 1 - j, 0) * PD; // (k padding: zero coefficients)
                 const bool mid = ODD && j == hc - 1;
 #pragma unroll
                 for (int i = 0; i < NCB; ++i) {
-                    const int cb = w + 8 * i;
+                    const int cb = w + kNG * i;
                     if (cb < a.CB) {
                         const int c = 8 * cb + ar;
                         const double tv = top[c], bv = mid ? 0.0 : bot[c];
@@ -201,7 +252,7 @@ __global__ void __launch_bounds__(kThr + 128, 1) k_fd_axis1(Axis1Args a) {
                 const int m = 8 * r + ar;
 #pragma unroll
                 for (int i = 0; i < NCB; ++i) {
-                    const int cb = w + 8 * i, cc = 4 * cb + ak; // complex column
+                    const int cb = w + kNG * i, cc = 4 * cb + ak; // complex column
                     if (cb < a.CB && cc < nt) {
                         if (m < hc)
                             *reinterpret_cast<double2*>(Sx + (size_t)m * PD + 2 * cc) =
@@ -213,10 +264,10 @@ __global__ void __launch_bounds__(kThr + 128, 1) k_fd_axis1(Axis1Args a) {
                 }
             }
         };
-        // inverse of slab t; `next` (>= 0): issue slab next's load into the same
-        // buffer as soon as every GEMM warp has read it, before the stores
+        // inverse of slab t; then the load of slab `next` into the same buffer is
+        // issued as soon as every GEMM warp has read it, before the stores
         auto inverse = [&](int t, int next) {
-            double* Sx = S0 + (size_t)(t & 1) * bufd;
+            double* Sx = S0 + (size_t)(t % NB) * bufd;
             double* Ys = a.Y + (size_t)slab_of(t) * n1 * nt * 2;
             double ee[HB][NCB][2], oo[HB][NCB][2];
 #pragma unroll
@@ -228,14 +279,14 @@ __global__ void __launch_bounds__(kThr + 128, 1) k_fd_axis1(Axis1Args a) {
                 double fe[HB], fo[HB];
 #pragma unroll
                 for (int r = 0; r < HB; ++r) {
-                    fe[r] = __ldg(Ae + (size_t)(8 * r + ar) * AP + mk);
-                    fo[r] = __ldg(Ao + (size_t)(8 * r + ar) * AP + mk);
+                    fe[r] = lda(Ae + (size_t)(8 * r + ar) * AP + mk);
+                    fo[r] = lda(Ao + (size_t)(8 * r + ar) * AP + mk);
                 }
                 const double* se = Sx + (size_t)mk * PD;
                 const double* so = Sx + (size_t)(hc + mk) * PD;
 #pragma unroll
                 for (int i = 0; i < NCB; ++i) {
-                    const int cb = w + 8 * i;
+                    const int cb = w + kNG * i;
                     if (cb < a.CB) {
                         const int c = 8 * cb + ar;
                         const double be = se[c], bo = so[c];
@@ -247,8 +298,8 @@ __global__ void __launch_bounds__(kThr + 128, 1) k_fd_axis1(Axis1Args a) {
                     }
                 }
             }
-            if (next >= 0) {
-                asm volatile("bar.sync 1, 256;" ::: "memory"); // all GEMM warps have read the buffer
+            if (next < nmine) {
+                asm volatile("bar.sync 1, %0;" ::"n"(32 * kNG) : "memory"); // all GEMM warps have read the buffer
                 issue_load(next);
             }
 #pragma unroll
@@ -259,7 +310,7 @@ __global__ void __launch_bounds__(kThr + 128, 1) k_fd_axis1(Axis1Args a) {
                     double2* d1 = reinterpret_cast<double2*>(Ys + (size_t)(n1 - 1 - j) * nt * 2);
 #pragma unroll
                     for (int i = 0; i < NCB; ++i) {
-                        const int cb = w + 8 * i, cc = 4 * cb + ak;
+                        const int cb = w + kNG * i, cc = 4 * cb + ak;
                         if (cb < a.CB && cc < nt) {
                             __stcs(d0 + cc, make_double2(ee[r][i][0] + oo[r][i][0], ee[r][i][1] + oo[r][i][1]));
                             if (n1 - 1 - j != j)
@@ -269,90 +320,52 @@ __global__ void __launch_bounds__(kThr + 128, 1) k_fd_axis1(Axis1Args a) {
                 }
             }
         };
-        issue_load(0);
+        for (int t = 0; t < NB - 1; ++t) issue_load(t);
         forward(0);
         step_bar();
         for (int t = 0; t < nmine; ++t) {
-            const int nx = t + 1 < nmine ? t + 1 : -1;
-            if (t >= 1) inverse(t - 1, nx);
-            else if (nx >= 0) issue_load(nx);
-            if (nx >= 0) forward(nx);
+            // buffer (t - 1) % NB is free once slab t-1 is transformed back
+            if (t >= 1) inverse(t - 1, t + NB - 1);
+            else issue_load(NB - 1);
+            if (t + 1 < nmine) forward(t + 1);
             step_bar();
         }
-        inverse(nmine - 1, -1);
-    } else if (warp == pwarp) {
-        // =================== producer warp (lane 0) ===================
-        if (lane != 0) return;
-        const size_t gsz = (size_t)n1b;
-        const int nch = (nt + CK - 1) / CK;
-        const int uses = 2 * nch; // ring uses per slab: forward chunks, then backward chunks (descending)
-        auto prefetch_group = [&](int t) { // a slab's whole factor group into L2 (2 bulk prefetches)
-            const size_t g0 = (size_t)a.grp[slab_of(t)] * (size_t)nt * gsz;
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.v + g0 * P),
-                         "r"((unsigned)(nt * P) * (unsigned)gsz * 16u)
-                         : "memory");
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.dinv + g0),
-                         "r"((unsigned)nt * (unsigned)gsz * 8u)
-                         : "memory");
-        };
-        int psl = 0, pwrap = 0;
-        prefetch_group(0);
-        for (int pt = 0; pt < nmine; ++pt) {
-            if (pt + 1 < nmine) prefetch_group(pt + 1);
-            const size_t pg = (size_t)a.grp[slab_of(pt)] * (size_t)nt; // group * nt
-            for (int pu = 0; pu < uses; ++pu) {
-                if (pwrap > 0) mwait(empty + psl, (unsigned)((pwrap - 1) & 1)); // slot's previous use consumed
-                const bool fwd = pu < nch;
-                const int c = fwd ? pu : uses - 1 - pu;
-                const int k0 = c * CK, nk = min(CK, nt - k0);
-                const unsigned vb = (unsigned)(nk * P) * (unsigned)gsz * 16u, db = (unsigned)nk * (unsigned)gsz * 8u;
-                double2* dv = rv + (size_t)psl * (slotd / 2);
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(full + psl)),
-                             "r"(vb + (fwd ? db : 0u))
-                             : "memory");
-                bulk(dv, a.v + (pg + k0) * P * gsz, vb, full + psl);
-                if (fwd)
-                    bulk(reinterpret_cast<double*>(dv + (size_t)CK * P * gsz), a.dinv + (pg + k0) * gsz, db,
-                         full + psl);
-                if (++psl == D) psl = 0, ++pwrap;
-            }
-        }
+        inverse(nmine - 1, nmine);
     } else {
         // =================== solver warps ===================
-        const int m = tid - kThr;
-        const bool act = m < n1;
+        const int m = 32 * (warp >> 2) + lane;
         const size_t gsz = (size_t)n1b; // factor group = the slab's n1b blocks (FdBlocks::gsz)
         const int nch = (nt + CK - 1) / CK;
-        const int uses = 2 * nch; // ring uses per slab: forward chunks, then backward chunks (descending)
+        if (m >= nsolve) return; // (a warp with no fibers takes no part in the step barrier)
+        const bool act = m < n1;
         int csl = 0;
         unsigned cph = 0; // consumer: slot, full-barrier parity
         auto take = [&]() -> const double2* {
             mwait(full + csl, cph);
             return rv + (size_t)csl * (slotd / 2);
         };
-        auto give = [&]() { // release the slot to the producer warp
+        auto give = [&]() { // release the slot to the producer
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(empty + csl)) : "memory");
             if (++csl == D) csl = 0, cph ^= 1u;
         };
         const double2 Z = make_double2(0.0, 0.0);
+        const int gm = (int)gsz;
         for (int t = 0; t < nmine; ++t) {
-            step_bar(); // slab t is in buffer t & 1 (forward transform done)
-            double2* row = reinterpret_cast<double2*>(S0 + (size_t)(t & 1) * bufd + (size_t)(act ? m : 0) * PD);
+            step_bar(); // slab t is in buffer t % NB (forward transform done)
+            double2* row = reinterpret_cast<double2*>(S0 + (size_t)(t % NB) * bufd + (size_t)(act ? m : 0) * PD);
             double2 w[P + 1];
 #pragma unroll
             for (int j = 0; j <= P; ++j) w[j] = act && j < nt ? row[j] : Z;
+            // L y = r, z = D^-1 y: w[j] -= conj(v_k,j) w[0]; a chunk's factor rows and
+            // incoming values go to registers first (independent loads), then the
+            // sweep runs in registers with two dependent FMAs per step on the chain
             for (int c = 0; c < nch; ++c) {
                 const double2* sv = take();
                 const double* sd = reinterpret_cast<const double*>(sv + (size_t)CK * P * gsz);
                 const int k0 = c * CK, nk = min(CK, nt - k0);
                 if (act) {
-                    // the chunk's factor rows and incoming x values into registers
-                    // first (independent loads), then the dependent sweep purely in
-                    // registers (the chain is two FP64 ops per step), then the
-                    // chunk's outputs back to the slab
                     double2 vr[CK][P], xin[CK], zo[CK];
                     double dr[CK];
-                    const int gm = (int)gsz;
 #pragma unroll
                     for (int kk = 0; kk < CK; ++kk) {
                         dr[kk] = sd[kk * gm + m];
@@ -363,9 +376,14 @@ __global__ void __launch_bounds__(kThr + 128, 1) k_fd_axis1(Axis1Args a) {
                     }
 #pragma unroll
                     for (int kk = 0; kk < CK; ++kk) {
+                        const double2 w0 = w[0];
 #pragma unroll
-                        for (int j = 1; j <= P; ++j) w[j] = csub(w[j], cconjmul(vr[kk][j - 1], w[0]));
-                        zo[kk] = make_double2(w[0].x * dr[kk], w[0].y * dr[kk]);
+                        for (int j = 1; j <= P; ++j) {
+                            const double2 v = vr[kk][j - 1];
+                            w[j].x = fma(-v.y, w0.y, fma(-v.x, w0.x, w[j].x));
+                            w[j].y = fma(v.y, w0.x, fma(-v.x, w0.y, w[j].y));
+                        }
+                        zo[kk] = make_double2(w0.x * dr[kk], w0.y * dr[kk]);
 #pragma unroll
                         for (int j = 0; j < P; ++j) w[j] = w[j + 1];
                         w[P] = xin[kk];
@@ -376,15 +394,15 @@ __global__ void __launch_bounds__(kThr + 128, 1) k_fd_axis1(Axis1Args a) {
                 }
                 give();
             }
-            double2 u[P + 1];
+            // L^H x = z: x_k = z_k - sum_j v_k,j x_k+j, the newest x applied last
+            double2 uu[P + 1];
 #pragma unroll
-            for (int j = 0; j <= P; ++j) u[j] = Z;
+            for (int j = 0; j <= P; ++j) uu[j] = Z;
             for (int c = nch - 1; c >= 0; --c) {
                 const double2* sv = take();
                 const int k0 = c * CK, nk = min(CK, nt - k0);
                 if (act) {
                     double2 vr[CK][P], zr[CK];
-                    const int gm = (int)gsz;
 #pragma unroll
                     for (int kk = 0; kk < CK; ++kk) {
                         zr[kk] = kk < nk ? row[k0 + kk] : Z;
@@ -396,10 +414,14 @@ __global__ void __launch_bounds__(kThr + 128, 1) k_fd_axis1(Axis1Args a) {
                         if (kk < nk) { // (steps past n_t only in the last chunk)
                             double2 x = zr[kk];
 #pragma unroll
-                            for (int j = 1; j <= P; ++j) x = csub(x, cmul(vr[kk][j - 1], u[j]));
+                            for (int j = P; j >= 1; --j) {
+                                const double2 v = vr[kk][j - 1];
+                                x.x = fma(v.y, uu[j].y, fma(-v.x, uu[j].x, x.x));
+                                x.y = fma(-v.y, uu[j].x, fma(-v.x, uu[j].y, x.y));
+                            }
 #pragma unroll
-                            for (int j = P; j > 1; --j) u[j] = u[j - 1];
-                            u[1] = x;
+                            for (int j = P; j > 1; --j) uu[j] = uu[j - 1];
+                            uu[1] = x;
                             zr[kk] = x;
                         }
                     }
@@ -416,11 +438,17 @@ __global__ void __launch_bounds__(kThr + 128, 1) k_fd_axis1(Axis1Args a) {
 
 template <int HB, int NCB, int P, bool ODD>
 void launch_axis1(const Axis1Args& a, size_t sm, cudaStream_t st) {
-    constexpr int D = 4; // factor ring slots of 8 steps: three chunks in flight ahead of the sweeps
-    auto k = k_fd_axis1<HB, NCB, P, D, ODD>;
-    smem_optin((const void*)k, (int)sm);
     const int grid = std::min(a.nslab, device_sms());
-    k<<<grid, kThr + 32 * ((a.n1 + 31) / 32) + 32, sm, st>>>(a); // GEMM + solver + producer warps
+    const int thr = 32 * axis1_warps(HB);
+    if (a.asm_) {
+        auto k = k_fd_axis1<HB, NCB, P, ODD, true>;
+        smem_optin((const void*)k, (int)sm);
+        k<<<grid, thr, sm, st>>>(a);
+    } else {
+        auto k = k_fd_axis1<HB, NCB, P, ODD, false>;
+        smem_optin((const void*)k, (int)sm);
+        k<<<grid, thr, sm, st>>>(a);
+    }
     check_launch("k_fd_axis1");
 }
 
@@ -437,36 +465,54 @@ void launch_axis1_p(const Axis1Args& a, int p, size_t sm, cudaStream_t st) {
     }
 }
 
-size_t axis1_smem(int n1, int nt, int p, int& PD, int& AP, int& SZ, int& K4, int& HB) {
+// Geometry and shared-memory plan: two slab buffers, the half matrices (when a
+// ring of >= 4 slots still fits beside them, else they come through L1) and as
+// many factor-ring slots as fit, up to 8 (c3: 144 + 18 + 6 x 10 KB).
+struct Axis1Plan {
+    int PD, AP, SZ, K4, HB, padr, nbuf, asm_, ring;
+    size_t smem;
+};
+Axis1Plan axis1_plan(int n1, int nt, int p) {
+    Axis1Plan q{};
     const int hc = (n1 + 1) / 2;
-    HB = (hc + 7) / 8;
-    K4 = (hc + 3) / 4;
-    SZ = std::max(4 * K4, 8 * HB);
-    AP = SZ;
-    while (AP % 16 != 4) ++AP;
-    PD = 2 * nt;
-    while (PD % 16 != 4) ++PD;
-    constexpr int D = 4, CK = 8; // ring slots x steps per slot (k_fd_axis1)
+    q.HB = (hc + 7) / 8;
+    q.K4 = (hc + 3) / 4;
+    q.SZ = std::max(4 * q.K4, 8 * q.HB);
+    q.AP = q.SZ;
+    while (q.AP % 16 != 4) ++q.AP;
+    q.PD = 2 * nt;
+    while (q.PD % 16 != 4) ++q.PD;
+    q.padr = std::max(0, hc + 4 * q.K4 - n1); // rows the k-padded loops read past the slab (kept zero)
+    const size_t buf = (size_t)(n1 + q.padr) * q.PD * sizeof(double), am = (size_t)2 * q.SZ * q.AP * sizeof(double);
+    // factor ring: slots of 4 steps x n1b blocks x (16 p + 8) B, at least 3, at most 8
     const int n1b = (n1 + 1) / 2 * 2;
-    return (size_t)2 * (n1 + 4) * PD * sizeof(double) + (size_t)D * CK * n1b * (2 * p + 1) * sizeof(double) +
-           (size_t)(2 + 2 * D) * 8;
+    const size_t slot = (size_t)4 * n1b * (2 * p + 1) * sizeof(double);
+    const size_t lim = 226 * 1024, bars = (size_t)(2 + 2 * 8) * 8;
+    q.nbuf = 2;
+    q.asm_ = 2 * buf + am + 4 * slot + bars <= lim;
+    const size_t fixed = 2 * buf + (q.asm_ ? am : 0) + bars;
+    q.ring = fixed + 3 * slot <= lim ? (int)std::min<size_t>(8, (lim - fixed) / slot) : 0;
+    q.smem = fixed + (size_t)q.ring * slot;
+    return q;
 }
 
 } // namespace
 
 bool fd_axis1_supported(int n1, int nt, int p) {
-    int PD, AP, SZ, K4, HB;
-    const size_t sm = axis1_smem(n1, nt, p, PD, AP, SZ, K4, HB);
+    const Axis1Plan q = axis1_plan(n1, nt, p);
     const int CB = (2 * nt + 7) / 8;
-    return n1 >= 2 && n1 <= 96 && HB >= 1 && HB <= 5 && (CB + 7) / 8 <= 3 && p >= 1 && p <= 6 &&
-           sm <= 227 * 1024;
+    return n1 >= 2 && n1 <= 96 && q.HB >= 1 && q.HB <= 5 && (CB + kNG - 1) / kNG <= 3 && p >= 1 && p <= 6 &&
+           q.ring >= 3 && q.smem <= 227 * 1024;
 }
 
 void launch_fd_axis1(const FoldAxis& F, const double* A, int nt, long long nslab, const int* order, const int* grp,
                      int n1b, const FdBlocks& B, const double* X, double* Y, cudaStream_t st) {
     Axis1Args a{};
-    int HB;
-    const size_t sm = axis1_smem(F.n, nt, B.p, a.PD, a.AP, a.SZ, a.K4, HB);
+    const Axis1Plan q = axis1_plan(F.n, nt, B.p);
+    const int HB = q.HB;
+    const size_t sm = q.smem;
+    a.PD = q.PD, a.AP = q.AP, a.SZ = q.SZ, a.K4 = q.K4;
+    a.nbuf = q.nbuf, a.padr = q.padr, a.asm_ = q.asm_, a.ring = q.ring;
     a.A = A;
     a.X = X;
     a.Y = Y;
@@ -482,13 +528,14 @@ void launch_fd_axis1(const FoldAxis& F, const double* A, int nt, long long nslab
     a.nt = nt;
     a.CB = (2 * nt + 7) / 8;
     const bool odd = F.n & 1;
-    const int ncb = (a.CB + 7) / 8;
+    const int ncb = (a.CB + kNG - 1) / kNG;
 #define KS_A1(HBV, NCBV)                                                                \
     if (HB == HBV && ncb <= NCBV) {                                                     \
         if (odd) launch_axis1_p<HBV, NCBV, true>(a, B.p, sm, st);                       \
         else launch_axis1_p<HBV, NCBV, false>(a, B.p, sm, st);                          \
         return;                                                                         \
     }
+    KS_A1(1, 2) KS_A1(2, 2) KS_A1(3, 2) KS_A1(4, 2) KS_A1(5, 2)
     KS_A1(1, 3) KS_A1(2, 3) KS_A1(3, 3) KS_A1(4, 3) KS_A1(5, 3)
 #undef KS_A1
     throw Error(KS_EINVAL, "fused axis-1 FD stage: unsupported shape");
@@ -496,8 +543,8 @@ void launch_fd_axis1(const FoldAxis& F, const double* A, int nt, long long nslab
 
 // se / so of a folded axis in the kernel's layout: [2][SZ][AP], element (j, m)
 void fd_axis1_matrix(const FoldAxis& F, int nt, int p, std::vector<double>& out) {
-    int PD, AP, SZ, K4, HB;
-    axis1_smem(F.n, nt, p, PD, AP, SZ, K4, HB);
+    const Axis1Plan q = axis1_plan(F.n, nt, p);
+    const int AP = q.AP, SZ = q.SZ;
     const int H = 16 * F.th, Kp = F.kst;
     std::vector<double> fwd((size_t)2 * Kp * H);
     KS_CUDA(cudaMemcpy(fwd.data(), F.fwd.p, fwd.size() * sizeof(double), cudaMemcpyDeviceToHost));
