@@ -95,7 +95,9 @@ struct Axis1Args {
 template <int HB, int NCB, int P, bool ODD, bool ASM>
 __global__ void __launch_bounds__(32 * axis1_warps(HB), 1) k_fd_axis1(Axis1Args a) {
     extern __shared__ __align__(16) double sm[];
-    const int n1 = a.n1, n1b = a.n1b, hc = a.hc, no = n1 - hc, nt = a.nt, PD = a.PD, AP = a.AP, NB = a.nbuf;
+    const int n1 = a.n1, n1b = a.n1b, hc = a.hc, no = n1 - hc, nt = a.nt, PD = a.PD, AP = a.AP;
+    constexpr int NB = 2;  // slab buffers
+    constexpr int LG = 4;  // row groups of a slab load, one mbarrier each: the forward k loop starts on the first
     const size_t bufd = (size_t)(n1 + a.padr) * PD;                       // doubles per slab buffer
     double* S0 = sm;                                                      // [NB][n1 + padr][PD]
     double* Asm = S0 + (size_t)NB * bufd;                                 // [2][SZ][AP] (ASM)
@@ -104,8 +106,8 @@ __global__ void __launch_bounds__(32 * axis1_warps(HB), 1) k_fd_axis1(Axis1Args 
     const int D = a.ring;
     const size_t slotd = (size_t)CK * n1b * (2 * P + 1);                  // doubles per slot
     double2* rv = reinterpret_cast<double2*>(Asm + (ASM ? (size_t)2 * a.SZ * AP : 0));
-    unsigned long long* bar = reinterpret_cast<unsigned long long*>(reinterpret_cast<double*>(rv) + (size_t)D * slotd); // [NB]
-    unsigned long long* full = bar + NB;                                  // [D]
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(reinterpret_cast<double*>(rv) + (size_t)D * slotd); // [NB][LG]
+    unsigned long long* full = bar + NB * LG;                             // [D]
     unsigned long long* empty = full + D;                                 // [D]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nsolve = 32 * ((n1 + 31) / 32);  // solver threads (whole warps)
@@ -129,7 +131,8 @@ __global__ void __launch_bounds__(32 * axis1_warps(HB), 1) k_fd_axis1(Axis1Args 
     if (ASM)
         for (int e = tid; e < 2 * a.SZ * AP; e += blockDim.x) Asm[e] = __ldg(a.A + e);
     if (tid == 0) {
-        for (int q = 0; q < NB; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bar + q)) : "memory");
+        for (int q = 0; q < NB * LG; ++q)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bar + q)) : "memory");
         for (int q = 0; q < D; ++q) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(full + q)) : "memory");
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(empty + q)), "r"(nsolve) : "memory");
@@ -198,22 +201,33 @@ __global__ void __launch_bounds__(32 * axis1_warps(HB), 1) k_fd_axis1(Axis1Args 
         const double* Ae = ASM ? Asm : a.A;
         const double* Ao = Ae + (size_t)a.SZ * AP;
         auto lda = [&](const double* p) -> double { return ASM ? *p : __ldg(p); };
-        auto issue_load = [&](int t) { // warp 0: slab t -> buffer t % NB
+        // k4 steps per row group: group g holds the rows j and n1-1-j of k4 in [g KG, (g+1) KG)
+        const int KG = (a.K4 + LG - 1) / LG;
+        auto issue_load = [&](int t) { // warp 0: slab t -> buffer t % NB, rows in consumption order
             if (w != 0 || t >= nmine) return;
             const int b = t % NB;
             double* Sx = S0 + (size_t)b * bufd;
             const double* Xs = a.X + (size_t)slab_of(t) * n1 * nt * 2;
-            if (lane == 0)
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar + b)),
-                             "r"(rowbytes * (unsigned)n1)
+            if (lane < LG) {
+                const int j0 = min(4 * KG * lane, hc), j1 = min(4 * KG * (lane + 1), hc);
+                int rows = 2 * (j1 - j0);
+                if (ODD && j0 < hc && j1 == hc) --rows; // the middle row has no mirror
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar + b * LG + lane)),
+                             "r"(rowbytes * (unsigned)rows)
                              : "memory");
+            }
             __syncwarp();
-            for (int i = lane; i < n1; i += 32) bulk(Sx + (size_t)i * PD, Xs + (size_t)i * nt * 2, rowbytes, bar + b);
+            for (int i = lane; i < n1; i += 32) {
+                // pair index ii = 0, 1, 2, ..: rows 0, n1-1, 1, n1-2, ..
+                const int j = i >> 1, row = (i & 1) ? n1 - 1 - j : j;
+                if ((i & 1) && row == j) continue; // (odd n1: the middle row once)
+                bulk(Sx + (size_t)row * PD, Xs + (size_t)row * nt * 2, rowbytes, bar + b * LG + j / (4 * KG));
+            }
         };
         auto forward = [&](int t) {
             const int b = t % NB;
             double* Sx = S0 + (size_t)b * bufd;
-            mwait(bar + b, (phase >> b) & 1u);
+            const unsigned par = (phase >> b) & 1u;
             phase ^= 1u << b;
             double ae_[HB][NCB][2], ao_[HB][NCB][2];
 #pragma unroll
@@ -221,6 +235,7 @@ __global__ void __launch_bounds__(32 * axis1_warps(HB), 1) k_fd_axis1(Axis1Args 
 #pragma unroll
                 for (int i = 0; i < NCB; ++i) ae_[r][i][0] = ae_[r][i][1] = ao_[r][i][0] = ao_[r][i][1] = 0.0;
             for (int k4 = 0; k4 < a.K4; ++k4) {
+                if (k4 % KG == 0) mwait(bar + b * LG + k4 / KG, par); // this row group has landed
                 const int j = 4 * k4 + ak;
                 double fe[HB], fo[HB];
 #pragma unroll
@@ -487,7 +502,7 @@ Axis1Plan axis1_plan(int n1, int nt, int p) {
     // factor ring: slots of 4 steps x n1b blocks x (16 p + 8) B, at least 3, at most 8
     const int n1b = (n1 + 1) / 2 * 2;
     const size_t slot = (size_t)4 * n1b * (2 * p + 1) * sizeof(double);
-    const size_t lim = 226 * 1024, bars = (size_t)(2 + 2 * 8) * 8;
+    const size_t lim = 226 * 1024, bars = (size_t)(2 * 4 + 2 * 8) * 8; // slab row-group + ring barriers
     q.nbuf = 2;
     q.asm_ = 2 * buf + am + 4 * slot + bars <= lim;
     const size_t fixed = 2 * buf + (q.asm_ ? am : 0) + bars;
