@@ -355,96 +355,123 @@ __global__ void __launch_bounds__(32 * axis1_warps(HB), 1) k_fd_axis1(Axis1Args 
         const bool act = m < n1;
         int csl = 0;
         unsigned cph = 0; // consumer: slot, full-barrier parity
-        auto take = [&]() -> const double2* {
-            mwait(full + csl, cph);
-            return rv + (size_t)csl * (slotd / 2);
-        };
-        auto give = [&]() { // release the slot to the producer
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(empty + csl)) : "memory");
-            if (++csl == D) csl = 0, cph ^= 1u;
-        };
         const double2 Z = make_double2(0.0, 0.0);
         const int gm = (int)gsz;
+        const double2* svm = rv + m; // this fiber's column of a ring slot
         for (int t = 0; t < nmine; ++t) {
             step_bar(); // slab t is in buffer t % NB (forward transform done)
             double2* row = reinterpret_cast<double2*>(S0 + (size_t)(t % NB) * bufd + (size_t)(act ? m : 0) * PD);
-            double2 w[P + 1];
+            // Static windows: xs[i] is position k0 + i of the chunk (i = 0..P carried
+            // from the previous chunk, i = P+1..CK+P loaded), no per-step shifts.
+            // L y = r, z = D^-1 y: xs[kk + j] -= conj(v_kk,j) xs[kk]; the chunk's factor
+            // rows and incoming values go to registers first (independent loads), then
+            // the sweep runs in registers with two dependent FMAs per step on the chain.
+            double2 xs[CK + P + 1];
 #pragma unroll
-            for (int j = 0; j <= P; ++j) w[j] = act && j < nt ? row[j] : Z;
-            // L y = r, z = D^-1 y: w[j] -= conj(v_k,j) w[0]; a chunk's factor rows and
-            // incoming values go to registers first (independent loads), then the
-            // sweep runs in registers with two dependent FMAs per step on the chain
+            for (int j = 0; j <= P; ++j) xs[j] = act && j < nt ? row[j] : Z;
             for (int c = 0; c < nch; ++c) {
-                const double2* sv = take();
-                const double* sd = reinterpret_cast<const double*>(sv + (size_t)CK * P * gsz);
-                const int k0 = c * CK, nk = min(CK, nt - k0);
+                mwait(full + csl, cph);
+                const double2* sv = svm + (size_t)csl * (slotd / 2);
+                const double* sd = reinterpret_cast<const double*>(sv - m + (size_t)CK * P * gsz) + m;
+                const int k0 = c * CK;
                 if (act) {
-                    double2 vr[CK][P], xin[CK], zo[CK];
+                    double2 vr[CK][P];
                     double dr[CK];
+                    if (k0 + CK + P < nt) { // full chunk, every incoming position inside the fiber
 #pragma unroll
-                    for (int kk = 0; kk < CK; ++kk) {
-                        dr[kk] = sd[kk * gm + m];
+                        for (int kk = 0; kk < CK; ++kk) {
+                            dr[kk] = sd[kk * gm];
 #pragma unroll
-                        for (int j = 0; j < P; ++j) vr[kk][j] = sv[(kk * P + j) * gm + m];
-                        const int ki = k0 + P + 1 + kk;
-                        xin[kk] = ki < nt ? row[ki] : Z;
+                            for (int j = 0; j < P; ++j) vr[kk][j] = sv[(kk * P + j) * gm];
+                            xs[P + 1 + kk] = row[k0 + P + 1 + kk];
+                        }
+                    } else {
+                        const int nk = min(CK, nt - k0);
+#pragma unroll
+                        for (int kk = 0; kk < CK; ++kk) {
+                            dr[kk] = kk < nk ? sd[kk * gm] : 0.0;
+#pragma unroll
+                            for (int j = 0; j < P; ++j) vr[kk][j] = kk < nk ? sv[(kk * P + j) * gm] : Z;
+                            const int ki = k0 + P + 1 + kk;
+                            xs[P + 1 + kk] = ki < nt ? row[ki] : Z;
+                        }
                     }
 #pragma unroll
                     for (int kk = 0; kk < CK; ++kk) {
-                        const double2 w0 = w[0];
+                        const double2 w0 = xs[kk];
 #pragma unroll
                         for (int j = 1; j <= P; ++j) {
                             const double2 v = vr[kk][j - 1];
-                            w[j].x = fma(-v.y, w0.y, fma(-v.x, w0.x, w[j].x));
-                            w[j].y = fma(v.y, w0.x, fma(-v.x, w0.y, w[j].y));
+                            xs[kk + j].x = fma(-v.y, w0.y, fma(-v.x, w0.x, xs[kk + j].x));
+                            xs[kk + j].y = fma(v.y, w0.x, fma(-v.x, w0.y, xs[kk + j].y));
                         }
-                        zo[kk] = make_double2(w0.x * dr[kk], w0.y * dr[kk]);
+                        xs[kk] = make_double2(w0.x * dr[kk], w0.y * dr[kk]);
+                    }
+                    if (k0 + CK <= nt) {
 #pragma unroll
-                        for (int j = 0; j < P; ++j) w[j] = w[j + 1];
-                        w[P] = xin[kk];
+                        for (int kk = 0; kk < CK; ++kk) row[k0 + kk] = xs[kk];
+                    } else {
+#pragma unroll
+                        for (int kk = 0; kk < CK; ++kk)
+                            if (k0 + kk < nt) row[k0 + kk] = xs[kk];
                     }
 #pragma unroll
-                    for (int kk = 0; kk < CK; ++kk)
-                        if (kk < nk) row[k0 + kk] = zo[kk];
+                    for (int j = 0; j <= P; ++j) xs[j] = xs[CK + j];
                 }
-                give();
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(empty + csl)) : "memory");
+                if (++csl == D) csl = 0, cph ^= 1u;
             }
-            // L^H x = z: x_k = z_k - sum_j v_k,j x_k+j, the newest x applied last
-            double2 uu[P + 1];
+            // L^H x = z: xb[kk] = z - sum_j v_kk,j xb[kk + j], the newest x applied last;
+            // xb[CK..CK+P-1] carried from the chunk above
+            double2 xb[CK + P];
 #pragma unroll
-            for (int j = 0; j <= P; ++j) uu[j] = Z;
+            for (int j = 0; j < CK + P; ++j) xb[j] = Z;
             for (int c = nch - 1; c >= 0; --c) {
-                const double2* sv = take();
-                const int k0 = c * CK, nk = min(CK, nt - k0);
+                mwait(full + csl, cph);
+                const double2* sv = svm + (size_t)csl * (slotd / 2);
+                const int k0 = c * CK;
                 if (act) {
-                    double2 vr[CK][P], zr[CK];
+                    double2 vr[CK][P];
+                    if (k0 + CK <= nt) {
 #pragma unroll
-                    for (int kk = 0; kk < CK; ++kk) {
-                        zr[kk] = kk < nk ? row[k0 + kk] : Z;
+                        for (int kk = 0; kk < CK; ++kk) {
+                            xb[kk] = row[k0 + kk];
 #pragma unroll
-                        for (int j = 0; j < P; ++j) vr[kk][j] = sv[(kk * P + j) * gm + m];
+                            for (int j = 0; j < P; ++j) vr[kk][j] = sv[(kk * P + j) * gm];
+                        }
+                    } else { // (steps past n_t only in the last chunk: zero rows, zero values)
+                        const int nk = nt - k0;
+#pragma unroll
+                        for (int kk = 0; kk < CK; ++kk) {
+                            xb[kk] = kk < nk ? row[k0 + kk] : Z;
+#pragma unroll
+                            for (int j = 0; j < P; ++j) vr[kk][j] = kk < nk ? sv[(kk * P + j) * gm] : Z;
+                        }
                     }
 #pragma unroll
                     for (int kk = CK - 1; kk >= 0; --kk) {
-                        if (kk < nk) { // (steps past n_t only in the last chunk)
-                            double2 x = zr[kk];
+                        double2 x = xb[kk];
 #pragma unroll
-                            for (int j = P; j >= 1; --j) {
-                                const double2 v = vr[kk][j - 1];
-                                x.x = fma(v.y, uu[j].y, fma(-v.x, uu[j].x, x.x));
-                                x.y = fma(-v.y, uu[j].x, fma(-v.x, uu[j].y, x.y));
-                            }
-#pragma unroll
-                            for (int j = P; j > 1; --j) uu[j] = uu[j - 1];
-                            uu[1] = x;
-                            zr[kk] = x;
+                        for (int j = P; j >= 1; --j) {
+                            const double2 v = vr[kk][j - 1], u = xb[kk + j];
+                            x.x = fma(v.y, u.y, fma(-v.x, u.x, x.x));
+                            x.y = fma(-v.y, u.x, fma(-v.x, u.y, x.y));
                         }
+                        xb[kk] = x;
+                    }
+                    if (k0 + CK <= nt) {
+#pragma unroll
+                        for (int kk = 0; kk < CK; ++kk) row[k0 + kk] = xb[kk];
+                    } else {
+#pragma unroll
+                        for (int kk = 0; kk < CK; ++kk)
+                            if (k0 + kk < nt) row[k0 + kk] = xb[kk];
                     }
 #pragma unroll
-                    for (int kk = 0; kk < CK; ++kk)
-                        if (kk < nk) row[k0 + kk] = zr[kk];
+                    for (int j = P - 1; j >= 0; --j) xb[CK + j] = xb[j]; // (descending: the ranges overlap when P > CK)
                 }
-                give();
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(empty + csl)) : "memory");
+                if (++csl == D) csl = 0, cph ^= 1u;
             }
         }
         step_bar(); // matches the GEMM warps' last step barrier
