@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(XCfg<NF>::kThr, NF == 2 ? 2 : 1) k_xfold(XArgs
     if (tid == 0) {
         for (int q = 0; q < NST; ++q) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(full + q)),
-                         "r"(MODE == 2 ? kXThr : (kCons < SR ? kCons : SR))
+                         "r"(MODE == 2 ? kXThr : SR)
                          : "memory");
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(empty + q)), "r"(kCons) : "memory");
         }
@@ -161,10 +161,17 @@ __global__ void __launch_bounds__(XCfg<NF>::kThr, NF == 2 ? 2 : 1) k_xfold(XArgs
             pq0 += gridDim.x * (unsigned)kTC;
         }
     };
+    unsigned po = 0, pr = 0; // slab and offset of the tile's first column (per tile, not per stage)
+    int ptile = -1;
     auto produce = [&]() {
         if (MODE == 2) return produce_tin();
         if (warp >= PW || pit >= my_tiles) return;
         if (plap > 0) mwait(empty + pst, (plap - 1) & 1u);
+        if (ptile != pit) {
+            po = pq0 / su;
+            pr = pq0 - po * su;
+            ptile = pit;
+        }
         const unsigned ncol = min((unsigned)kTC, Qu - pq0);
         const int i = warp * RPW + lane; // stage row
         int row = -1;
@@ -174,17 +181,16 @@ __global__ void __launch_bounds__(XCfg<NF>::kThr, NF == 2 ? 2 : 1) k_xfold(XArgs
             else row = i < 4 * KS ? kr : hc + kr;
             if (row < 0 || row >= n) row = -1;
         }
-        unsigned tot = row >= 0 ? ncol * 16u : 0u;
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
-        if (lane == 0)
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(full + pst)), "r"(tot)
+        // every producing lane arrives for its own row (arrival count = SR): no
+        // cross-lane reduction on the producers' path
+        if (lane < RPW)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(full + pst)),
+                         "r"(row >= 0 ? ncol * 16u : 0u)
                          : "memory");
-        __syncwarp();
         if (row >= 0) {
             // the tile's columns, split at slab boundaries
             double* dst = Bs + ((size_t)pst * SR + i) * kBP;
-            unsigned o = pq0 / su, r = pq0 - o * su, done = 0, len = min(ncol, su - r);
+            unsigned o = po, r = pr, done = 0, len = min(ncol, su - r);
             while (done < ncol) {
                 const double* src = a.X + 2 * (((size_t)o * n + row) * s + r);
                 asm volatile(
@@ -198,7 +204,6 @@ __global__ void __launch_bounds__(XCfg<NF>::kThr, NF == 2 ? 2 : 1) k_xfold(XArgs
                 len = min(ncol - done, su);
             }
         }
-        __syncwarp();
         if (++pst == NST) pst = 0, ++plap;
         if (++pg == nstg) {
             pg = 0;
