@@ -83,7 +83,7 @@ template <int HB, int KS, bool INV, bool ODD, int NF, int MODE>
 __global__ void __launch_bounds__(XCfg<NF>::kThr, NF == 2 ? 2 : 1) k_xfold(XArgs a) {
     constexpr int kCons = XCfg<NF>::kCons, kXThr = XCfg<NF>::kThr;
     constexpr int SR = 8 * KS;   // stage rows: 4 KS top + 4 KS bottom
-    constexpr int NST = KS == 2 ? 4 : 8;
+    constexpr int NST = KS == 2 ? 5 : 8;
     extern __shared__ __align__(16) double sm[];
     const int n = a.n, hc = a.hc, no = n - hc, AP = a.AP;
     const int nstg = (a.K4 + KS - 1) / KS; // stages per tile
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(XCfg<NF>::kThr, NF == 2 ? 2 : 1) k_xfold(XArgs
 
     // Producers: warps 0..PW-1, each issuing the bulk copies of RPW rows of a
     // stage (one cp.async.bulk per row segment: spreading the issue over warps
-    // keeps the copies ahead of the DMMAs), NST-1 stages ahead of consumption,
+    // keeps the copies ahead of the DMMAs), NST-2 stages ahead of consumption,
     // across tiles. A slot is refilled only after every consumer warp has
     // released its previous stage. 32-bit column arithmetic (Q < 2^31).
     constexpr int PW = kCons < SR ? kCons : SR, RPW = SR / PW;
@@ -163,45 +163,54 @@ __global__ void __launch_bounds__(XCfg<NF>::kThr, NF == 2 ? 2 : 1) k_xfold(XArgs
     };
     unsigned po = 0, pr = 0; // slab and offset of the tile's first column (per tile, not per stage)
     int ptile = -1;
+    // With more consumer warps than stage rows (NPG > 1) the warps take turns:
+    // group warp / PW produces every NPG-th stage, so no warp carries the whole
+    // producer path (ncu at n = 130: the non-producing warps sat on `full`).
+    constexpr int NPG = kCons / PW;
+    int pcnt = 0;
     auto produce = [&]() {
         if (MODE == 2) return produce_tin();
-        if (warp >= PW || pit >= my_tiles) return;
-        if (plap > 0) mwait(empty + pst, (plap - 1) & 1u);
-        if (ptile != pit) {
-            po = pq0 / su;
-            pr = pq0 - po * su;
-            ptile = pit;
-        }
-        const unsigned ncol = min((unsigned)kTC, Qu - pq0);
-        const int i = warp * RPW + lane; // stage row
-        int row = -1;
-        if (lane < RPW) {
-            const int kr = pg * 4 * KS + (i % (4 * KS));
-            if (!INV) row = i < 4 * KS ? kr : n - 1 - kr;
-            else row = i < 4 * KS ? kr : hc + kr;
-            if (row < 0 || row >= n) row = -1;
-        }
-        // every producing lane arrives for its own row (arrival count = SR): no
-        // cross-lane reduction on the producers' path
-        if (lane < RPW)
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(full + pst)),
-                         "r"(row >= 0 ? ncol * 16u : 0u)
-                         : "memory");
-        if (row >= 0) {
-            // the tile's columns, split at slab boundaries
-            double* dst = Bs + ((size_t)pst * SR + i) * kBP;
-            unsigned o = po, r = pr, done = 0, len = min(ncol, su - r);
-            while (done < ncol) {
-                const double* src = a.X + 2 * (((size_t)o * n + row) * s + r);
-                asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                        su32(dst + 2 * done)),
-                    "l"(src), "r"(len * 16u), "r"(su32(full + pst))
-                    : "memory");
-                done += len;
-                ++o;
-                r = 0;
-                len = min(ncol - done, su);
+        if (pit >= my_tiles) return;
+        const bool mine = NPG == 1 || pcnt % NPG == warp / PW;
+        ++pcnt;
+        if (mine) {
+            if (plap > 0) mwait(empty + pst, (plap - 1) & 1u);
+            if (ptile != pit) {
+                po = pq0 / su;
+                pr = pq0 - po * su;
+                ptile = pit;
+            }
+            const unsigned ncol = min((unsigned)kTC, Qu - pq0);
+            const int i = (warp % PW) * RPW + lane; // stage row
+            int row = -1;
+            if (lane < RPW) {
+                const int kr = pg * 4 * KS + (i % (4 * KS));
+                if (!INV) row = i < 4 * KS ? kr : n - 1 - kr;
+                else row = i < 4 * KS ? kr : hc + kr;
+                if (row < 0 || row >= n) row = -1;
+            }
+            // every producing lane arrives for its own row (arrival count = SR): no
+            // cross-lane reduction on the producers' path
+            if (lane < RPW)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(full + pst)),
+                             "r"(row >= 0 ? ncol * 16u : 0u)
+                             : "memory");
+            if (row >= 0) {
+                // the tile's columns, split at slab boundaries
+                double* dst = Bs + ((size_t)pst * SR + i) * kBP;
+                unsigned o = po, r = pr, done = 0, len = min(ncol, su - r);
+                while (done < ncol) {
+                    const double* src = a.X + 2 * (((size_t)o * n + row) * s + r);
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                            su32(dst + 2 * done)),
+                        "l"(src), "r"(len * 16u), "r"(su32(full + pst))
+                        : "memory");
+                    done += len;
+                    ++o;
+                    r = 0;
+                    len = min(ncol - done, su);
+                }
             }
         }
         if (++pst == NST) pst = 0, ++plap;
@@ -211,7 +220,10 @@ __global__ void __launch_bounds__(XCfg<NF>::kThr, NF == 2 ? 2 : 1) k_xfold(XArgs
             pq0 += gridDim.x * (unsigned)kTC;
         }
     };
-    for (int q = 0; q < NST - 1; ++q) produce();
+    // NST-2 stages ahead: a slot is refilled two stages after its consumption,
+    // so the producers wait for the slowest warp of the stage before last, not
+    // of the one just finished (which coupled all warps every stage)
+    for (int q = 0; q < NST - 2; ++q) produce();
     // ===================== consumers (all warps) =====================
     const int ar = lane >> 2, ak = lane & 3;
     const int cw = 8 * NF * warp; // this warp's first double column in the tile
@@ -219,6 +231,19 @@ __global__ void __launch_bounds__(XCfg<NF>::kThr, NF == 2 ? 2 : 1) k_xfold(XArgs
     const double* Ao = As + (size_t)kpad * AP;
     int st = 0;
     unsigned lap = 0;
+    // the next stage's `full` barrier is tested (non-blocking) before the current
+    // stage's DMMAs and only waited on if that test failed: the ~100-cycle
+    // barrier query overlaps the warp's own math
+    auto mtest = [&](unsigned long long* b, unsigned parity) -> unsigned {
+        unsigned ok;
+        asm volatile("{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                     " selp.u32 %0, 1, 0, p;\n}\n"
+                     : "=r"(ok)
+                     : "r"(su32(b)), "r"(parity)
+                     : "memory");
+        return ok;
+    };
+    unsigned ready = my_tiles > 0 ? mtest(full, 0u) : 0u;
     for (int it = 0; it < my_tiles; ++it) {
         const long long q0 = ((long long)blockIdx.x + (long long)it * gridDim.x) * kTC;
         double ce[HB][NF][2], co[HB][NF][2];
@@ -227,8 +252,12 @@ __global__ void __launch_bounds__(XCfg<NF>::kThr, NF == 2 ? 2 : 1) k_xfold(XArgs
 #pragma unroll
             for (int f = 0; f < NF; ++f) ce[r][f][0] = ce[r][f][1] = co[r][f][0] = co[r][f][1] = 0.0;
         for (int g = 0; g < nstg; ++g) {
-            mwait(full + st, lap & 1u);
+            if (!ready) mwait(full + st, lap & 1u);
             const double* bs = Bs + (size_t)st * SR * kBP;
+            {
+                const int sn = st + 1 == NST ? 0 : st + 1;
+                ready = mtest(full + sn, (sn == 0 ? lap + 1 : lap) & 1u);
+            }
 #pragma unroll
             for (int kk = 0; kk < KS; ++kk) {
                 const int kl = 4 * kk + ak;          // stage-local k row
@@ -263,7 +292,7 @@ __global__ void __launch_bounds__(XCfg<NF>::kThr, NF == 2 ? 2 : 1) k_xfold(XArgs
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(empty + st)) : "memory");
             if (++st == NST) st = 0, ++lap;
-            produce(); // warps 0..PW-1: their rows of the stage NST-1 ahead
+            produce(); // the producing warps: their rows of the stage NST-2 ahead
         }
         // epilogue: complex column cc of the tile -> (slab o, offset r)
 #pragma unroll
@@ -308,7 +337,7 @@ __global__ void __launch_bounds__(XCfg<NF>::kThr, NF == 2 ? 2 : 1) k_xfold(XArgs
 template <int HB, int KS, bool INV, bool ODD, int MODE>
 void launch_x(const XArgs& a, cudaStream_t st) {
     constexpr int NF = HB <= 5 ? 2 : 1, kXThr = XCfg<NF>::kThr;
-    constexpr int SR = 8 * KS, NST = KS == 2 ? 4 : 8;
+    constexpr int SR = 8 * KS, NST = KS == 2 ? 5 : 8;
     const int nstg = (a.K4 + KS - 1) / KS, kpad = nstg * 4 * KS;
     const size_t sm = ((size_t)2 * kpad * a.AP + (size_t)NST * SR * kBP) * sizeof(double) + (size_t)2 * NST * 8;
     KS_REQUIRE(sm <= 227 * 1024, KS_EINVAL, "folded transform: axis too long");
