@@ -200,6 +200,13 @@ KronJitPair* kron_jit_build(int nin, int nmid, int nout, int bw, const std::vect
                             const std::vector<JitContrib>& b, const std::vector<int>& freal,
                             const std::vector<double2>& coeffs, long long s_a, int n_a, int n_b, long long n_outer,
                             int tmax_default = 384, int dmax = 4);
+// row-blocked variant for s_a > 1 (lanes across the inner columns, R rows of axis a
+// per thread, band entries as literals); hrb = host copy of the band table
+// rb[f][nmax][2 bw + 1]; null when the factors are not Toeplitz away from the boundary
+KronJitPair* kron_jitb_build(int nin, int nmid, int nout, int bw, const std::vector<JitContrib>& a,
+                             const std::vector<JitContrib>& b, const std::vector<int>& freal,
+                             const std::vector<double2>& coeffs, long long s_a, int n_a, int n_b, long long n_outer,
+                             const double2* hrb, int nmax, int R);
 bool kron_jit_same_shape(const KronJitPair& A, const KronJitPair& B);
 bool kron_jit_launch(const KronJitPair& J, const double2* const* ip, double2* const* op, void* const* hin,
                      void* const* hout, const double2* rb, int nmax, cudaStream_t st);

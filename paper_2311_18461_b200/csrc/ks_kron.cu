@@ -597,6 +597,15 @@ KronPlan* kron_plan(const std::vector<int>& dims,
                     for (auto& o : P->jit_alt[k]) dup = dup || kron_jit_same_shape(*alt, *o);
                     if (!dup) P->jit_alt[k].push_back(std::move(alt));
                 }
+            // row-blocked candidates (inner columns across the lanes); the first
+            // apply times all candidates and keeps the fastest
+            if (P->jit[k] && sa >= 32)
+                for (int rr : {2, 4}) {
+                    std::unique_ptr<KronJitPair, KronJitDeleter> alt(kron_jitb_build(
+                        pa.n_in, pa.n_out, pb.n_out, P->bwmax, ca, cb, frv, co, (long long)sa, na, nbb, outer, rb.data(),
+                        nmax, rr));
+                    if (alt) P->jit_alt[k].push_back(std::move(alt));
+                }
         }
     }
     for (auto& ps : P->passes) {

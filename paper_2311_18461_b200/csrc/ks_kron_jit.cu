@@ -28,10 +28,12 @@
 #include <nvrtc.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <set>
 #include <sstream>
@@ -111,6 +113,7 @@ struct KronJitPair {
     JitKernel k;
     int nin = 0, nmid = 0, nout = 0, bw = 0, ncoef = 0;
     bool pull = true;
+    bool blocked = false; // row-blocked variant (kron_jitb_build): lanes across the inner columns
     int T = 0, nq = 1, no = 1, D = 2, pad = 0; // block size, point block, ring depth, ring halo
     size_t smem = 0;                           // ring + staged axis-b bands
     long long s_a = 0, n_outer = 0;
@@ -504,7 +507,7 @@ static int sm_count() {
 // (c2: 22 CTAs, 0.23 ms vs 0.064 ms for the per-pass kernels)
 bool kron_jit_runs(const KronJitPair& J) { return J.grid >= (unsigned)sm_count(); }
 bool kron_jit_same_shape(const KronJitPair& A, const KronJitPair& B) {
-    return A.T == B.T && A.nq == B.nq && A.no == B.no && A.D == B.D;
+    return A.blocked == B.blocked && A.T == B.T && A.nq == B.nq && A.no == B.no && A.D == B.D;
 }
 
 // launch over the plan's tensors (geometry fixed at build); false when the
@@ -512,6 +515,27 @@ bool kron_jit_same_shape(const KronJitPair& A, const KronJitPair& B) {
 bool kron_jit_launch(const KronJitPair& J, const double2* const* ip, double2* const* op, void* const* hin,
                      void* const* hout, const double2* rb, int nmax, cudaStream_t st) {
     if (!kron_jit_runs(J)) return false;
+    if (J.blocked) {
+        // by-value parameter: input / output tensors, band table
+        struct {
+            const void* in[4];
+            void* out[2];
+            const double2* rb;
+            int nmax;
+        } par{};
+        std::vector<unsigned char> buf((size_t)(J.nin + J.nout) * sizeof(void*) + sizeof(void*) + sizeof(int) + 8, 0);
+        unsigned char* w = buf.data();
+        for (int g = 0; g < J.nin; ++g, w += sizeof(void*)) std::memcpy(w, &hin[g], sizeof(void*));
+        for (int o = 0; o < J.nout; ++o, w += sizeof(void*)) std::memcpy(w, &hout[o], sizeof(void*));
+        std::memcpy(w, &rb, sizeof(void*));
+        w += sizeof(void*);
+        std::memcpy(w, &nmax, sizeof(int));
+        (void)par;
+        void* args[] = {(void*)buf.data()};
+        KS_CUDA(cudaLaunchKernel((const void*)J.k.fn, dim3(J.grid), dim3(J.T), args, J.smem, st));
+        check_launch("ks_pairb (jit)");
+        return true;
+    }
     // by-value coefficient table (constant bank)
     // by-value parameter: coefficients, then the input and output tensor pointers
     const size_t nc = (size_t)std::max(1, J.ncoef);
@@ -527,6 +551,350 @@ bool kron_jit_launch(const KronJitPair& J, const double2* const* ip, double2* co
     KS_CUDA(cudaLaunchKernel((const void*)J.k.fn, dim3(J.grid), dim3(J.T), args, J.smem, st));
     check_launch("ks_pair (jit)");
     return true;
+}
+
+// ---------------------------------------------------------------------------
+// Row-blocked variant of a fused pass pair for an in-plane axis a with inner
+// columns (s_a > 1; at d = 3 the (2, 3) pair): the (t, i1) columns run across
+// the lanes, a thread owns R consecutive rows of axis a, and the sweep along
+// axis b scatters ("push") into a register window of output rows.
+//
+// Why (ncu of the thread-per-point kernel, c3 pass (2, 3)): 30 LDS.128 per
+// point and plane -- 15 taps of the three inputs plus 15 band rows -- against
+// 90 DFMA, `short_scoreboard` / `mio_throttle` on top. Here
+//   * a thread loads R + 2 bw values per input for R points (R = 2: 9 LDS per
+//     point, R = 4: 6) from a [row][32 lanes] tile: conflict-free 16 B per lane;
+//   * every band entry is a literal in the generated source: the row block of
+//     a warp is uniform, so the interior (Toeplitz, uniform mesh) rows share one
+//     code path and each boundary row block gets its own, selected by a
+//     warp-uniform switch; along the sweep axis the interior planes use
+//     literals and the few boundary planes read the band table;
+//   * the contribution coefficients are folded into those literals, so a
+//     product costs exactly 2 DFMA per tap and complex value;
+//   * planes arrive through a ring of whole-plane stages filled by a producer
+//     warp with one bulk copy per (input, row) -- 512 B each -- on full / empty
+//     mbarriers; the consumer warps never meet at a CTA barrier.
+// Requires every factor of the pair to be Toeplitz away from a few boundary
+// rows (uniform knot vectors); otherwise the builder returns null and the
+// thread-per-point kernel runs.
+// ---------------------------------------------------------------------------
+namespace {
+
+std::string hexd(double v) {
+    char b[64];
+    std::snprintf(b, sizeof b, "%a", v);
+    return std::string(b);
+}
+
+// rows [lo, hi) of factor f equal to the middle row (relative 1e-13)
+void toeplitz_range(const double2* hrb, int f, int nmax, int n, int W, int& lo, int& hi) {
+    const int mid = n / 2;
+    const double2* T = hrb + ((size_t)f * nmax + mid) * W;
+    double sc = 0;
+    for (int k = 0; k < W; ++k) sc = std::max(sc, std::max(std::fabs(T[k].x), std::fabs(T[k].y)));
+    auto same = [&](int r) {
+        const double2* row = hrb + ((size_t)f * nmax + r) * W;
+        for (int k = 0; k < W; ++k)
+            if (std::fabs(row[k].x - T[k].x) > 1e-13 * sc || std::fabs(row[k].y - T[k].y) > 1e-13 * sc) return false;
+        return true;
+    };
+    lo = mid;
+    hi = mid + 1;
+    while (lo > 0 && same(lo - 1)) --lo;
+    while (hi < n && same(hi)) ++hi;
+}
+
+} // namespace
+
+KronJitPair* kron_jitb_build(int nin, int nmid, int nout, int bw, const std::vector<JitContrib>& a,
+                             const std::vector<JitContrib>& b, const std::vector<int>& freal,
+                             const std::vector<double2>& coeffs, long long s_a, int n_a, int n_b, long long n_outer,
+                             const double2* hrb, int nmax, int R) {
+    if (const char* e = std::getenv("KS_KRON_JIT"))
+        if (std::strcmp(e, "0") == 0) return nullptr;
+    if (s_a < 32 || nin < 1 || nmid < 1 || nout < 1 || nin > 4 || nmid > 6 || nout > 2 || bw < 1 || bw > 4) return nullptr;
+    if (R < 1 || R > 4 || n_a < 4 * bw + 2 || n_b < 4 * bw + 2) return nullptr;
+    const int W = 2 * bw + 1;
+    auto cls = [&](int f) { return freal[f]; }; // 1 real, 2 imaginary, 0 complex
+    std::set<int> FA, FB;
+    for (auto& c : a) {
+        if (c.factor < 0) return nullptr; // (identity factors: the other kernel)
+        FA.insert(c.factor);
+    }
+    for (auto& c : b) {
+        if (c.factor < 0) return nullptr;
+        FB.insert(c.factor);
+    }
+    int loa = 0, hia = n_a, lob = 0, hib = n_b;
+    for (int f : FA) {
+        int lo, hi;
+        toeplitz_range(hrb, f, nmax, n_a, W, lo, hi);
+        loa = std::max(loa, lo);
+        hia = std::min(hia, hi);
+    }
+    for (int f : FB) {
+        int lo, hi;
+        toeplitz_range(hrb, f, nmax, n_b, W, lo, hi);
+        lob = std::max(lob, lo);
+        hib = std::min(hib, hi);
+    }
+    if (loa > 8 || n_a - hia > 8 || lob > 8 || n_b - hib > 8) return nullptr; // not a uniform-mesh factor
+    // tile: 32 lanes x RT rows (+ halo), RT a multiple of R, at most 32 rows
+    const int nrt = (n_a + 31) / 32;
+    int RT = ((n_a + nrt - 1) / nrt + R - 1) / R * R;
+    const int NW = RT / R;
+    const int RTH = RT + 2 * bw;
+    const size_t stage = (size_t)nin * RTH * 32 * sizeof(double2);
+    int S = (int)std::min<size_t>(4, (size_t)(220 * 1024) / stage);
+    if (S < 2 || NW < 1 || NW > 16) return nullptr;
+    const int nqt = (int)((s_a + 31) / 32);
+    // boundary row blocks (global block index gb = row / R)
+    const int nblk = (n_a + R - 1) / R;
+    const int NBLO = (loa + R - 1) / R, HB0 = hia / R;
+    if (NBLO + (nblk - HB0) > 16 || HB0 < NBLO) return nullptr;
+    auto band = [&](int f, int row, int k) -> double2 { // entry k of row `row` (zero outside)
+        if (row < 0) return make_double2(0, 0);
+        return hrb[((size_t)f * nmax + row) * W + k];
+    };
+    // single-consumer products fold the contribution coefficient into the literals
+    auto cval = [&](int ci) { return coeffs[ci]; };
+    for (auto& c : a)
+        if (cval(c.coeff).y != 0.0) return nullptr; // (complex contribution coefficients: the other kernel)
+    for (auto& c : b)
+        if (cval(c.coeff).y != 0.0) return nullptr;
+    std::ostringstream s;
+    s << "// generated: row-blocked fused level passes (ks_kron_jit.cu)\n"
+      << "#define BW " << bw << "\n#define W " << W << "\n#define NIN " << nin << "\n#define NMID " << nmid << "\n#define NOUT "
+      << nout << "\n#define R " << R << "\n#define RT " << RT << "\n#define RTH " << RTH << "\n#define S " << S
+      << "\n#define NW " << NW << "\n#define s_a " << s_a << "LL\n#define n_a " << n_a << "\n#define n_b " << n_b
+      << "\n#define NQT " << nqt << "\n#define NRT " << nrt << "\n"
+      << "struct Par { const double2* in[NIN]; double2* out[NOUT]; const double2* rb; int nmax; };\n"
+      << R"(
+__device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mwait(unsigned long long* b, unsigned parity) {
+    unsigned ok = 0;
+    do {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                     " selp.u32 %0, 1, 0, p;\n}\n" : "=r"(ok) : "r"(su32(b)), "r"(parity) : "memory");
+    } while (!ok);
+}
+extern "C" __global__ void __launch_bounds__(32 * (NW + 1), 1) ks_pairb(const Par P) {
+    extern __shared__ __align__(128) unsigned char smraw[];
+    double2* ring = reinterpret_cast<double2*>(smraw); // [S][NIN][RTH][32]
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(ring + (size_t)S * NIN * RTH * 32);
+    unsigned long long* empty = full + S;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int rt = blockIdx.x % NRT, qt = (blockIdx.x / NRT) % NQT;
+    const long long oo = blockIdx.x / (NRT * NQT);
+    const long long q0 = 32LL * qt;
+    const int row0 = rt * RT;
+    const int ncol = (int)(s_a - q0 < 32 ? s_a - q0 : 32);
+    const double2 Z = make_double2(0.0, 0.0);
+    for (int e = tid; e < S * NIN * RTH * 32; e += 32 * (NW + 1)) ring[e] = Z; // halo rows / columns never loaded stay zero
+    if (tid == 0) {
+        for (int q = 0; q < S; ++q) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(full + q)) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(empty + q)), "n"(NW) : "memory");
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const long long s_b = s_a * n_a;
+    const long long obase = oo * s_b * n_b + q0;
+    if (warp == NW) {
+        // ---- producer warp: one bulk copy per (input, row) and plane ----
+        int nvalid = 0;
+        for (int rr = 0; rr < RTH; ++rr) {
+            const int row = row0 - BW + rr;
+            nvalid += row >= 0 && row < n_a;
+        }
+        for (int ib = 0; ib < n_b; ++ib) {
+            const int slot = ib % S;
+            if (ib >= S) mwait(empty + slot, (unsigned)((ib / S - 1) & 1));
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(full + slot)),
+                             "r"((unsigned)(NIN * nvalid * ncol * 16)) : "memory");
+            __syncwarp();
+            for (int idx = lane; idx < NIN * RTH; idx += 32) {
+                const int g = idx / RTH, rr = idx - g * RTH, row = row0 - BW + rr;
+                if (row >= 0 && row < n_a)
+                    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+                                 "r"(su32(ring + ((size_t)(slot * NIN + g) * RTH + rr) * 32)),
+                                 "l"(P.in[g] + obase + s_b * ib + s_a * row), "r"((unsigned)(ncol * 16)), "r"(su32(full + slot))
+                                 : "memory");
+            }
+        }
+        return;
+    }
+    // ---- consumer warps: rows grow .. grow + R - 1 of axis a, column q0 + lane ----
+    const int rl = warp * R, grow = row0 + rl, gb = grow / R;
+    const bool qok = lane < ncol;
+)";
+    s << "    int cls = 0;\n    if (grow >= n_a) cls = -1;\n    else if (gb < " << NBLO << ") cls = 1 + gb;\n    else if (gb >= " << HB0
+      << ") cls = " << (1 + NBLO) << " + (gb - " << HB0 << ");\n"
+      << "    double2 win[NOUT][R][W];\n"
+      << "#pragma unroll\n    for (int o = 0; o < NOUT; ++o)\n#pragma unroll\n        for (int r = 0; r < R; ++r)\n#pragma unroll\n"
+      << "            for (int j = 0; j < W; ++j) win[o][r][j] = Z;\n"
+      << "    int ph = 0;\n"
+      << "    for (int ib = 0; ib < n_b + BW; ++ib) {\n"
+      << "        double2 m[NMID][R];\n"
+      << "#pragma unroll\n        for (int h = 0; h < NMID; ++h)\n#pragma unroll\n            for (int r = 0; r < R; ++r) m[h][r] = Z;\n"
+      << "        if (ib < n_b) {\n"
+      << "            const int slot = ib % S;\n"
+      << "            mwait(full + slot, (unsigned)((ib / S) & 1));\n"
+      << "            const double2* sl = ring + ((size_t)slot * NIN * RTH + rl) * 32 + lane;\n"
+      << "            switch (cls) {\n";
+    // in-plane code for one row block: rows[r] = global row of r (or -1: interior Toeplitz; -2: no row)
+    auto emit_inplane = [&](const std::vector<int>& rows) {
+        for (int g = 0; g < nin; ++g) {
+            std::vector<const JitContrib*> cs;
+            for (auto& c : a)
+                if (c.in == g) cs.push_back(&c);
+            if (cs.empty()) continue;
+            s << "            {\n                double2 w[R + 2 * BW];\n#pragma unroll\n                for (int k = 0; k < R + 2 * BW; ++k) w[k] = sl[("
+              << g << " * RTH + k) * 32];\n";
+            for (auto* c : cs) {
+                const int f = c->factor;
+                const double cc = coeffs[c->coeff].x;
+                for (int r = 0; r < R; ++r) {
+                    if (rows[r] == -2) continue;
+                    const std::string acc = "m[" + lit(c->out) + "][" + lit(r) + "]";
+                    for (int k = 0; k < W; ++k) {
+                        const double2 e = rows[r] == -1 ? band(f, (loa + hia) / 2, k) : band(f, rows[r], k);
+                        const std::string wv = "w[" + lit(r + k) + "]";
+                        if (cls(f) == 1) {
+                            if (e.x == 0.0) continue;
+                            const std::string v = hexd(cc * e.x);
+                            s << "                " << acc << ".x = fma(" << v << ", " << wv << ".x, " << acc << ".x); " << acc
+                              << ".y = fma(" << v << ", " << wv << ".y, " << acc << ".y);\n";
+                        } else if (cls(f) == 2) {
+                            if (e.y == 0.0) continue;
+                            const std::string v = hexd(cc * e.y);
+                            s << "                " << acc << ".x = fma(-(" << v << "), " << wv << ".y, " << acc << ".x); " << acc
+                              << ".y = fma(" << v << ", " << wv << ".x, " << acc << ".y);\n";
+                        } else {
+                            if (e.x == 0.0 && e.y == 0.0) continue;
+                            const std::string vx = hexd(cc * e.x), vy = hexd(cc * e.y);
+                            s << "                " << acc << ".x = fma(" << vx << ", " << wv << ".x, fma(-(" << vy << "), " << wv
+                              << ".y, " << acc << ".x)); " << acc << ".y = fma(" << vx << ", " << wv << ".y, fma(" << vy << ", "
+                              << wv << ".x, " << acc << ".y));\n";
+                        }
+                    }
+                }
+            }
+            s << "            }\n";
+        }
+    };
+    {
+        s << "            case 0: {\n";
+        emit_inplane(std::vector<int>(R, -1));
+        s << "            } break;\n";
+        int ci = 1;
+        auto emit_block = [&](int gbk) {
+            std::vector<int> rows(R);
+            for (int r = 0; r < R; ++r) rows[r] = gbk * R + r < n_a ? gbk * R + r : -2;
+            s << "            case " << ci++ << ": {\n";
+            emit_inplane(rows);
+            s << "            } break;\n";
+        };
+        for (int g = 0; g < NBLO; ++g) emit_block(g);
+        for (int g = HB0; g < nblk; ++g) emit_block(g);
+    }
+    s << "            default: break;\n            }\n"
+      << "            __syncwarp();\n"
+      << "            if (lane == 0) asm volatile(\"mbarrier.arrive.shared::cta.b64 _, [%0];\" ::\"r\"(su32(empty + slot)) : \"memory\");\n"
+      << "        }\n";
+    // push + store, one case per window phase
+    const int PLO = lob + bw, PHI = hib - bw; // planes whose band columns are all interior
+    s << "        const bool litp = ib >= " << PLO << " && ib < " << PHI << ";\n"
+      << "        const int rd = ib - BW;\n"
+      << "        switch (ph) {\n";
+    for (int ph = 0; ph < W; ++ph) {
+        s << "        case " << ph << ": {\n            if (ib < n_b) {\n                if (litp) {\n";
+        auto slotj = [&](int j) { return lit((ph + j) % W); };
+        for (auto& c : b) {
+            const int f = c.factor;
+            const double cc = coeffs[c.coeff].x;
+            for (int r = 0; r < R; ++r)
+                for (int j = 0; j < W; ++j) {
+                    const double2 e = band(f, (lob + hib) / 2, W - 1 - j);
+                    const std::string acc = "win[" + lit(c.out) + "][" + lit(r) + "][" + slotj(j) + "]";
+                    const std::string mv = "m[" + lit(c.in) + "][" + lit(r) + "]";
+                    if (cls(f) == 1) {
+                        if (e.x == 0.0) continue;
+                        const std::string v = hexd(cc * e.x);
+                        s << "                    " << acc << ".x = fma(" << v << ", " << mv << ".x, " << acc << ".x); " << acc
+                          << ".y = fma(" << v << ", " << mv << ".y, " << acc << ".y);\n";
+                    } else if (cls(f) == 2) {
+                        if (e.y == 0.0) continue;
+                        const std::string v = hexd(cc * e.y);
+                        s << "                    " << acc << ".x = fma(-(" << v << "), " << mv << ".y, " << acc << ".x); " << acc
+                          << ".y = fma(" << v << ", " << mv << ".x, " << acc << ".y);\n";
+                    } else {
+                        if (e.x == 0.0 && e.y == 0.0) continue;
+                        const std::string vx = hexd(cc * e.x), vy = hexd(cc * e.y);
+                        s << "                    " << acc << ".x = fma(" << vx << ", " << mv << ".x, fma(-(" << vy << "), " << mv
+                          << ".y, " << acc << ".x)); " << acc << ".y = fma(" << vx << ", " << mv << ".y, fma(" << vy << ", " << mv
+                          << ".x, " << acc << ".y));\n";
+                    }
+                }
+        }
+        s << "                } else {\n";
+        // boundary planes: column ib of each factor from the band table, F(ib + j - BW, ib)
+        for (int f : FB) {
+            s << "                    double2 C" << f << "[W];\n#pragma unroll\n                    for (int j = 0; j < W; ++j) { const int r_ = ib + j - BW; C"
+              << f << "[j] = (r_ >= 0 && r_ < n_b) ? __ldg(P.rb + ((size_t)" << f << " * P.nmax + r_) * W + (W - 1 - j)) : Z; }\n";
+        }
+        for (auto& c : b) {
+            const int f = c.factor;
+            const double cc = coeffs[c.coeff].x;
+            for (int r = 0; r < R; ++r) {
+                const std::string mv = "m[" + lit(c.in) + "][" + lit(r) + "]";
+                s << "                    { const double2 cm = make_double2(" << hexd(cc) << " * " << mv << ".x, " << hexd(cc) << " * " << mv
+                  << ".y);\n";
+                for (int j = 0; j < W; ++j) {
+                    const std::string acc = "win[" + lit(c.out) + "][" + lit(r) + "][" + slotj(j) + "]";
+                    const std::string cf = "C" + lit(f) + "[" + lit(j) + "]";
+                    s << "                      " << acc << ".x = fma(" << cf << ".x, cm.x, fma(-" << cf << ".y, cm.y, " << acc << ".x)); " << acc
+                      << ".y = fma(" << cf << ".x, cm.y, fma(" << cf << ".y, cm.x, " << acc << ".y));\n";
+                }
+                s << "                    }\n";
+            }
+        }
+        s << "                }\n            }\n"
+          << "            if (rd >= 0 && qok) {\n";
+        for (int o = 0; o < nout; ++o)
+            for (int r = 0; r < R; ++r)
+                s << "                if (grow + " << r << " < n_a) __stcs(P.out[" << o << "] + obase + s_b * rd + s_a * (grow + " << r
+                  << ") + lane, win[" << o << "][" << r << "][" << ph << "]);\n";
+        s << "            }\n";
+        for (int o = 0; o < nout; ++o)
+            for (int r = 0; r < R; ++r) s << "            win[" << o << "][" << r << "][" << ph << "] = Z;\n";
+        s << "        } break;\n";
+    }
+    s << "        }\n        ph = ph + 1 == W ? 0 : ph + 1;\n    }\n}\n";
+    std::unique_ptr<KronJitPair> P(new KronJitPair());
+    const size_t smem = (size_t)S * stage + (size_t)2 * S * 8 + 128;
+    P->k.fn = nvrtc_kernel(s.str(), "ks_pairb", 227 * 1024);
+    P->blocked = true;
+    P->nin = nin;
+    P->nmid = nmid;
+    P->nout = nout;
+    P->bw = bw;
+    P->pull = false;
+    P->T = 32 * (NW + 1);
+    P->nq = R; // (shape key: rows per thread)
+    P->no = RT;
+    P->D = S;
+    P->smem = smem;
+    P->s_a = s_a;
+    P->n_a = n_a;
+    P->n_b = n_b;
+    P->n_outer = n_outer;
+    P->grid = (unsigned)((long long)nqt * nrt * n_outer);
+    P->coef = coeffs;
+    P->ncoef = (int)coeffs.size();
+    return P.release();
 }
 
 } // namespace ks
