@@ -208,6 +208,7 @@ KronJitPair* kron_jitb_build(int nin, int nmid, int nout, int bw, const std::vec
                              const std::vector<double2>& coeffs, long long s_a, int n_a, int n_b, long long n_outer,
                              const double2* hrb, int nmax, int R);
 bool kron_jit_same_shape(const KronJitPair& A, const KronJitPair& B);
+int kron_jit_blocked_rows(const KronJitPair& J); // rows per thread of the row-blocked variant, 0 for thread-per-point
 bool kron_jit_launch(const KronJitPair& J, const double2* const* ip, double2* const* op, void* const* hin,
                      void* const* hout, const double2* rb, int nmax, cudaStream_t st);
 void kron_jit_free(KronJitPair* p);

@@ -25,6 +25,7 @@
 #include "ks_internal.hpp"
 
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <numeric>
@@ -752,6 +753,24 @@ void kron_apply(KronPlan& P, const double2* x, double2* y, cudaStream_t st,
                 size_t bi = 0;
                 for (size_t a = 1; a < tb.size(); ++a)
                     if (tb[a] < tb[bi]) bi = a;
+                // KS_KRON_JIT=b2 / b4 / point forces a candidate (tests, profiling)
+                if (const char* e = std::getenv("KS_KRON_JIT")) {
+                    const int want = !std::strcmp(e, "b2") ? 2 : !std::strcmp(e, "b4") ? 4 : !std::strcmp(e, "point") ? 0 : -1;
+                    if (want >= 0) {
+                        std::vector<KronJitPair*> all{P.jit[k].get()};
+                        for (auto& alt : P.jit_alt[k]) all.push_back(alt.get());
+                        for (size_t a = 0; a < all.size(); ++a)
+                            if (kron_jit_blocked_rows(*all[a]) == want && tb[a] < 1e29f) {
+                                bi = a;
+                                break;
+                            }
+                    }
+                }
+                if (const char* e = std::getenv("KS_KRON_JIT"); e && std::strcmp(e, "0") != 0) // any value but 0 logs the timings
+                    for (size_t a = 0; a < tb.size(); ++a)
+                        std::fprintf(stderr, "ks_kron pass pair %zu candidate %zu (rows/thread %d): %.1f us%s\n", k, a,
+                                     kron_jit_blocked_rows(a == 0 ? *P.jit[k] : *P.jit_alt[k][a - 1]), 1e3f * tb[a],
+                                     a == bi ? " <- kept" : "");
                 if (bi > 0) std::swap(P.jit[k], P.jit_alt[k][bi - 1]);
                 P.jit_alt[k].clear();
             }

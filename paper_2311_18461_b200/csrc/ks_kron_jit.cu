@@ -25,6 +25,7 @@
 // factorised by the level plan.
 #include "ks_internal.hpp"
 
+#include <cuda.h>
 #include <nvrtc.h>
 
 #include <algorithm>
@@ -505,9 +506,45 @@ static int sm_count() {
 
 // each CTA sweeps the whole axis b serially: too few CTAs leave the GPU idle
 // (c2: 22 CTAs, 0.23 ms vs 0.064 ms for the per-pass kernels)
-bool kron_jit_runs(const KronJitPair& J) { return J.grid >= (unsigned)sm_count(); }
+bool kron_jit_runs(const KronJitPair& J) {
+    // KS_KRON_JIT=b2 / b4 / point (a forced candidate: tests, profiling) also lifts the grid-size rule
+    static const bool forced = [] {
+        const char* e = std::getenv("KS_KRON_JIT");
+        return e && (!std::strcmp(e, "b2") || !std::strcmp(e, "b4") || !std::strcmp(e, "point"));
+    }();
+    return forced || J.grid >= (unsigned)sm_count();
+}
+int kron_jit_blocked_rows(const KronJitPair& J) { return J.blocked ? J.nq : 0; }
 bool kron_jit_same_shape(const KronJitPair& A, const KronJitPair& B) {
     return A.blocked == B.blocked && A.T == B.T && A.nq == B.nq && A.no == B.no && A.D == B.D;
+}
+
+// Tensor map of one level tensor [planes][n_a][s_a] complex, seen as doubles
+// (2 s_a, n_a, planes), box = 64 doubles x `rows` x 1 plane, no swizzle, zero
+// fill outside -- the row-blocked kernel's plane loads (halo rows included).
+// cuTensorMapEncodeTiled comes through the runtime's driver entry point, so
+// libks keeps linking only cudart.
+static void encode_plane_map(void* out, const void* base, long long s_a, int n_a, long long planes, int rows) {
+    using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                            const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                            CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Fn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        KS_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        KS_REQUIRE(p && q == cudaDriverEntryPointSuccess, KS_ECUDA, "cuTensorMapEncodeTiled not available");
+        fn = reinterpret_cast<Fn>(p);
+    }
+    const cuuint64_t gdim[3] = {(cuuint64_t)(2 * s_a), (cuuint64_t)n_a, (cuuint64_t)planes};
+    const cuuint64_t gstr[2] = {(cuuint64_t)(s_a * 16), (cuuint64_t)(s_a * 16 * n_a)};
+    const cuuint32_t box[3] = {64u, (cuuint32_t)rows, 1u}, est[3] = {1u, 1u, 1u};
+    CUtensorMap m;
+    const CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), gdim, gstr, box, est,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    KS_REQUIRE(r == CUDA_SUCCESS, KS_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    std::memcpy(out, &m, sizeof m);
 }
 
 // launch over the plan's tensors (geometry fixed at build); false when the
@@ -517,21 +554,18 @@ bool kron_jit_launch(const KronJitPair& J, const double2* const* ip, double2* co
     if (!kron_jit_runs(J)) return false;
     if (J.blocked) {
         // by-value parameter: input / output tensors, band table
-        struct {
-            const void* in[4];
-            void* out[2];
-            const double2* rb;
-            int nmax;
-        } par{};
-        std::vector<unsigned char> buf((size_t)(J.nin + J.nout) * sizeof(void*) + sizeof(void*) + sizeof(int) + 8, 0);
-        unsigned char* w = buf.data();
-        for (int g = 0; g < J.nin; ++g, w += sizeof(void*)) std::memcpy(w, &hin[g], sizeof(void*));
+        // (tensor maps first: 64-byte aligned, 128 B each)
+        const size_t bytes = (size_t)J.nin * 128 + ((size_t)J.nout + 2) * sizeof(void*);
+        std::vector<unsigned char> raw(bytes + 128 + 64, 0);
+        unsigned char* w = raw.data() + (64 - reinterpret_cast<uintptr_t>(raw.data()) % 64) % 64;
+        unsigned char* const w0 = w;
+        for (int g = 0; g < J.nin; ++g, w += 128)
+            encode_plane_map(w, hin[g], J.s_a, J.n_a, (long long)J.n_b * J.n_outer, J.no + 2 * J.bw);
         for (int o = 0; o < J.nout; ++o, w += sizeof(void*)) std::memcpy(w, &hout[o], sizeof(void*));
         std::memcpy(w, &rb, sizeof(void*));
         w += sizeof(void*);
         std::memcpy(w, &nmax, sizeof(int));
-        (void)par;
-        void* args[] = {(void*)buf.data()};
+        void* args[] = {(void*)w0};
         KS_CUDA(cudaLaunchKernel((const void*)J.k.fn, dim3(J.grid), dim3(J.T), args, J.smem, st));
         check_launch("ks_pairb (jit)");
         return true;
@@ -668,7 +702,8 @@ KronJitPair* kron_jitb_build(int nin, int nmid, int nout, int bw, const std::vec
       << nout << "\n#define R " << R << "\n#define RT " << RT << "\n#define RTH " << RTH << "\n#define S " << S
       << "\n#define NW " << NW << "\n#define s_a " << s_a << "LL\n#define n_a " << n_a << "\n#define n_b " << n_b
       << "\n#define NQT " << nqt << "\n#define NRT " << nrt << "\n"
-      << "struct Par { const double2* in[NIN]; double2* out[NOUT]; const double2* rb; int nmax; };\n"
+      << "struct __align__(64) TMap { unsigned long long d[16]; };\n"
+      << "struct Par { TMap tm[NIN]; double2* out[NOUT]; const double2* rb; int nmax; };\n"
       << R"(
 __device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mwait(unsigned long long* b, unsigned parity) {
@@ -678,7 +713,7 @@ __device__ __forceinline__ void mwait(unsigned long long* b, unsigned parity) {
                      " selp.u32 %0, 1, 0, p;\n}\n" : "=r"(ok) : "r"(su32(b)), "r"(parity) : "memory");
     } while (!ok);
 }
-extern "C" __global__ void __launch_bounds__(32 * (NW + 1), 1) ks_pairb(const Par P) {
+extern "C" __global__ void __launch_bounds__(32 * (NW + 1), 1) ks_pairb(const __grid_constant__ Par P) {
     extern __shared__ __align__(128) unsigned char smraw[];
     double2* ring = reinterpret_cast<double2*>(smraw); // [S][NIN][RTH][32]
     unsigned long long* full = reinterpret_cast<unsigned long long*>(ring + (size_t)S * NIN * RTH * 32);
@@ -702,27 +737,20 @@ extern "C" __global__ void __launch_bounds__(32 * (NW + 1), 1) ks_pairb(const Pa
     const long long s_b = s_a * n_a;
     const long long obase = oo * s_b * n_b + q0;
     if (warp == NW) {
-        // ---- producer warp: one bulk copy per (input, row) and plane ----
-        int nvalid = 0;
-        for (int rr = 0; rr < RTH; ++rr) {
-            const int row = row0 - BW + rr;
-            nvalid += row >= 0 && row < n_a;
-        }
+        // ---- producer: one tensor-map TMA box (64 doubles x RTH rows) per input and
+        // plane; rows outside [0, n_a) and columns past s_a arrive as zeros ----
+        if (lane != 0) return;
         for (int ib = 0; ib < n_b; ++ib) {
             const int slot = ib % S;
             if (ib >= S) mwait(empty + slot, (unsigned)((ib / S - 1) & 1));
-            if (lane == 0)
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(full + slot)),
-                             "r"((unsigned)(NIN * nvalid * ncol * 16)) : "memory");
-            __syncwarp();
-            for (int idx = lane; idx < NIN * RTH; idx += 32) {
-                const int g = idx / RTH, rr = idx - g * RTH, row = row0 - BW + rr;
-                if (row >= 0 && row < n_a)
-                    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-                                 "r"(su32(ring + ((size_t)(slot * NIN + g) * RTH + rr) * 32)),
-                                 "l"(P.in[g] + obase + s_b * ib + s_a * row), "r"((unsigned)(ncol * 16)), "r"(su32(full + slot))
-                                 : "memory");
-            }
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(full + slot)),
+                         "r"((unsigned)(NIN * RTH * 512)) : "memory");
+#pragma unroll
+            for (int g = 0; g < NIN; ++g)
+                asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+                             "r"(su32(ring + (size_t)(slot * NIN + g) * RTH * 32)), "l"(&P.tm[g]), "r"((int)(2 * q0)),
+                             "r"(row0 - BW), "r"((int)(oo * n_b + ib)), "r"(su32(full + slot))
+                             : "memory");
         }
         return;
     }
