@@ -207,8 +207,13 @@ KronJitPair* kron_jitb_build(int nin, int nmid, int nout, int bw, const std::vec
                              const std::vector<JitContrib>& b, const std::vector<int>& freal,
                              const std::vector<double2>& coeffs, long long s_a, int n_a, int n_b, long long n_outer,
                              const double2* hrb, int nmax, int R);
+// line variant for s_a = 1 (thread per point of C whole lines, planes as tensor-map boxes)
+KronJitPair* kron_jitl_build(int nin, int nmid, int nout, int bw, const std::vector<JitContrib>& a,
+                             const std::vector<JitContrib>& b, const std::vector<int>& freal,
+                             const std::vector<double2>& coeffs, int n_a, int n_b, long long n_outer,
+                             const double2* hrb, int nmax, int C, int smax, int minb);
 bool kron_jit_same_shape(const KronJitPair& A, const KronJitPair& B);
-int kron_jit_blocked_rows(const KronJitPair& J); // rows per thread of the row-blocked variant, 0 for thread-per-point
+int kron_jit_blocked_rows(const KronJitPair& J); // rows per thread of the row-blocked variant, -(lines per CTA) of the line variant, 0 for thread-per-point
 bool kron_jit_launch(const KronJitPair& J, const double2* const* ip, double2* const* op, void* const* hin,
                      void* const* hout, const double2* rb, int nmax, cudaStream_t st);
 void kron_jit_free(KronJitPair* p);

@@ -25,6 +25,7 @@
 #include "ks_internal.hpp"
 
 #include <algorithm>
+#include <array>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -601,10 +602,18 @@ KronPlan* kron_plan(const std::vector<int>& dims,
             // row-blocked candidates (inner columns across the lanes); the first
             // apply times all candidates and keeps the fastest
             if (P->jit[k] && sa >= 32)
-                for (int rr : {2, 4}) {
+                for (int rr : {2}) { // (4 rows per thread: on par at c3, spills at bw = 4)
                     std::unique_ptr<KronJitPair, KronJitDeleter> alt(kron_jitb_build(
                         pa.n_in, pa.n_out, pb.n_out, P->bwmax, ca, cb, frv, co, (long long)sa, na, nbb, outer, rb.data(),
                         nmax, rr));
+                    if (alt) P->jit_alt[k].push_back(std::move(alt));
+                }
+            if (P->jit[k] && sa == 1)
+                // (5 lines, 16 stages, one CTA per SM; fewer lines with 2-3 CTAs per SM spill: 510-540 us vs 249 us at c3)
+                for (auto cfg : {std::array<int, 3>{5, 16, 1}}) {
+                    std::unique_ptr<KronJitPair, KronJitDeleter> alt(
+                        kron_jitl_build(pa.n_in, pa.n_out, pb.n_out, P->bwmax, ca, cb, frv, co, na, nbb, outer, rb.data(), nmax,
+                                        cfg[0], cfg[1], cfg[2]));
                     if (alt) P->jit_alt[k].push_back(std::move(alt));
                 }
         }
@@ -755,12 +764,15 @@ void kron_apply(KronPlan& P, const double2* x, double2* y, cudaStream_t st,
                     if (tb[a] < tb[bi]) bi = a;
                 // KS_KRON_JIT=b2 / b4 / point forces a candidate (tests, profiling)
                 if (const char* e = std::getenv("KS_KRON_JIT")) {
+                    // (b2 / b4: rows per thread of the row-blocked kernel; the line kernel's
+                    // candidates report their lines per CTA and are picked by timing among them)
                     const int want = !std::strcmp(e, "b2") ? 2 : !std::strcmp(e, "b4") ? 4 : !std::strcmp(e, "point") ? 0 : -1;
                     if (want >= 0) {
                         std::vector<KronJitPair*> all{P.jit[k].get()};
                         for (auto& alt : P.jit_alt[k]) all.push_back(alt.get());
                         for (size_t a = 0; a < all.size(); ++a)
-                            if (kron_jit_blocked_rows(*all[a]) == want && tb[a] < 1e29f) {
+                            if ((kron_jit_blocked_rows(*all[a]) == want || (want > 0 && kron_jit_blocked_rows(*all[a]) < 0)) &&
+                                tb[a] < 1e29f) {
                                 bi = a;
                                 break;
                             }
