@@ -442,6 +442,21 @@ def solve_roofline_s(dims, p, n, iters, fp64_peak, hbm_peak):
     return iters * (t_fd + t_mv + t_vec)
 
 
+def two_pass_floor(ks, d, n, hbm_peak):
+    """The level-pass matvec moves its rank-(d) cut through HBM once: pass 1 reads x
+    and writes d intermediates, pass 2 reads them and writes y.
+    Floors of that decomposition: at the HBM peak, and as measured by streaming
+    kernels with the same read:write mixes on this GPU (ks_bw_fan)."""
+    if d < 2:
+        return None
+    nmid = 3  # Schmidt rank of the system operator across any axis cut
+    byts = (2 + 2 * nmid) * 16.0 * n
+    g_a, g_b = ks.bw_fan(1, nmid, n), ks.bw_fan(nmid, 1, n)
+    t_a, t_b = (1 + nmid) * 16.0 * n / (g_a * 1e9), (1 + nmid) * 16.0 * n / (g_b * 1e9)
+    return {"bytes_per_dof": byts / n, "floor_ms_at_hbm_peak": byts / (hbm_peak * 1e9) * 1e3,
+            "stream_1in_3out_gbs": g_a, "stream_3in_1out_gbs": g_b, "floor_ms_streaming": (t_a + t_b) * 1e3}
+
+
 def config_leg(ks, cfg, K, W, local, fp64_peak, hbm_peak, solve=True):
     """One BASELINE config on this GPU: FD apply and matvec (device-resident,
     CUDA events), their SURVEY 8(d) rooflines, and a full FD-PCG solve to 1e-8
@@ -468,6 +483,10 @@ def config_leg(ks, cfg, K, W, local, fp64_peak, hbm_peak, solve=True):
            "matvec": {"ms": ms_mv, "dof_per_s": n / (ms_mv * 1e-3), "roofline_ms": mv_roof * 1e3,
                       "frac_of_roofline": mv_roof * 1e3 / ms_mv, "plan": A.plan_info(),
                       "hbm_gbs_effective": 32.0 * n / (ms_mv * 1e-3) / 1e9}}
+    tp = two_pass_floor(ks, d, n, hbm_peak) if d >= 3 and n < 5e7 else None
+    if tp:
+        tp["frac_of_streaming_floor"] = tp["floor_ms_streaming"] / ms_mv
+        out["matvec"]["two_pass"] = tp
     if solve:
         b = ks.DeviceVector.from_host(rhs(n))
         rep0 = ks.pcg(A, P, b, ks.PcgOptions(1e-8, 200))  # first solve allocates the work vectors
@@ -566,6 +585,9 @@ def main():
     # ---- matvec ----
     A.time(r, y, W, flush=False)
     ms_mv = A.time(r, y, K, flush=False)
+    mv_two_pass = two_pass_floor(ks, d, n, hbm_peak) if d >= 3 else None
+    if mv_two_pass:
+        mv_two_pass["frac_of_streaming_floor"] = mv_two_pass["floor_ms_streaming"] / ms_mv
 
     # ---- e2e through the public host-pointer API (pinned host buffers) ----
     import ctypes as C
@@ -710,7 +732,8 @@ def main():
                      "wall_s": wall_fd},
         "matvec": {"ms": ms_mv, "dof_per_s": n / (ms_mv * 1e-3),
                    "roofline_ms": mv_roof_s * 1e3, "frac_of_roofline": mv_roof_s * 1e3 / ms_mv,
-                   "plan": A.plan_info(), "hbm_gbs_effective": 32.0 * n / (ms_mv * 1e-3) / 1e9},
+                   "plan": A.plan_info(), "hbm_gbs_effective": 32.0 * n / (ms_mv * 1e-3) / 1e9,
+                   "two_pass": mv_two_pass},
         "solves": solves,
         "legs": legs,
         "setup_s": setup_s,

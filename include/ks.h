@@ -240,6 +240,10 @@ int ks_fp64_peaks(double* dfma_tflops, double* dmma_tflops);
 int ks_fp64_peak_mixed(double* tflops);
 /* FP64 tensor-core throughput with the sm_90+ mma.sync m16n8k16 shape. */
 int ks_fp64_peak_mma16(double* tflops);
+/* Streaming HBM throughput (GB/s) of a kernel that reads `nin` and writes `nout`
+ * complex vectors of n entries -- the traffic mixes of the matvec passes (1 in /
+ * 3 out, 3 in / 1 out at d = 3), which bound the two-pass matvec. */
+int ks_bw_fan(int nin, int nout, size_t n, double* gbs);
 /* DMMA (m8n8k4) throughput with `ctas_per_sm` CTAs of `threads` threads per SM. */
 int ks_fp64_dmma_occupancy(int ctas_per_sm, int threads, double* tflops);
 /* Which engine the spatial transforms use: 0 = DFMA, 1 = DMMA (env KS_GEMM). */

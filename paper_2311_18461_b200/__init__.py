@@ -135,6 +135,7 @@ _SIGS = {
     "ks_fp64_peak_mixed": (C.c_int, [C.POINTER(C.c_double)]),
     "ks_fp64_peak_mma16": (C.c_int, [C.POINTER(C.c_double)]),
     "ks_fp64_dmma_occupancy": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_double)]),
+    "ks_bw_fan": (C.c_int, [C.c_int, C.c_int, C.c_size_t, C.POINTER(C.c_double)]),
     "ks_transform_engine": (C.c_int, []),
     "ks_launch_count": (C.c_uint64, []),
     "ks_launch_count_reset": (None, []),
@@ -916,6 +917,13 @@ def fp64_peak_mixed():
     a = C.c_double()
     _check(lib().ks_fp64_peak_mixed(C.byref(a)))
     return a.value
+
+
+def bw_fan(nin: int, nout: int, n: int) -> float:
+    """Streaming HBM throughput (GB/s) reading `nin` and writing `nout` complex vectors of n entries."""
+    g = C.c_double()
+    _check(lib().ks_bw_fan(nin, nout, n, C.byref(g)))
+    return g.value
 
 
 def launch_count() -> int:

@@ -231,7 +231,7 @@ __global__ void k_fan(const double2* const* __restrict__ in, int nin, double2* c
             a.x += v.x;
             a.y += v.y;
         }
-        for (int k = 0; k < nout; ++k) out[k][i] = make_double2(a.x * (k + 1), a.y);
+        for (int k = 0; k < nout; ++k) __stcs(out[k] + i, make_double2(a.x * (k + 1), a.y));
     }
 }
 extern "C" int ks_bw_fan(int nin, int nout, size_t n, double* gbs) {
