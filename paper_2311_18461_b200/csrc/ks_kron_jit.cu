@@ -61,7 +61,10 @@ std::map<std::string, cudaKernel_t>& jit_cache() {
 // return kernel `name`, with its dynamic shared memory limit raised to max_smem.
 cudaKernel_t nvrtc_kernel(const std::string& src, const char* name, size_t max_smem) {
     std::lock_guard<std::mutex> lk(g_jit_mu);
-    const std::string key = std::string(name) + "\n" + src;
+    int dev0 = 0;
+    KS_CUDA(cudaGetDevice(&dev0));
+    // per device: the shared-memory opt-in below is a per-device attribute
+    const std::string key = std::to_string(dev0) + ":" + name + "\n" + src;
     auto it = jit_cache().find(key);
     if (it != jit_cache().end()) return it->second;
     nvrtcProgram prog;
@@ -525,7 +528,8 @@ bool kron_jit_same_shape(const KronJitPair& A, const KronJitPair& B) {
 // included, zero filled outside). Line kernel: (2 n_a, n_b, lines), box = one
 // line x 1 plane x C lines. cuTensorMapEncodeTiled comes through the runtime's
 // driver entry point, so libks keeps linking only cudart.
-static void encode_map3(void* out, const void* base, long long d0, long long d1, long long d2, int b0, int b1, int b2) {
+static void encode_map3(void* out, const void* base, long long d0, long long d1, long long d2, int b0, int b1, int b2,
+                        bool split = false) {
     using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
                             const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -537,12 +541,17 @@ static void encode_map3(void* out, const void* base, long long d0, long long d1,
         KS_REQUIRE(p && q == cudaDriverEntryPointSuccess, KS_ECUDA, "cuTensorMapEncodeTiled not available");
         fn = reinterpret_cast<Fn>(p);
     }
-    // a dense tensor of doubles (d0 fastest), box b0 x b1 x b2, no swizzle, zero fill outside
-    const cuuint64_t gdim[3] = {(cuuint64_t)d0, (cuuint64_t)d1, (cuuint64_t)d2};
-    const cuuint64_t gstr[2] = {(cuuint64_t)(d0 * 8), (cuuint64_t)(d0 * 8 * d1)};
-    const cuuint32_t box[3] = {(cuuint32_t)b0, (cuuint32_t)b1, (cuuint32_t)b2}, est[3] = {1u, 1u, 1u};
+    // a dense tensor of doubles (d0 fastest), box b0 x b1 x b2, no swizzle, zero fill outside;
+    // split: d0 (> 256 doubles, the box limit) as (2, d0 / 2), rank 4
+    const cuuint64_t gdim[4] = {split ? 2u : (cuuint64_t)d0, split ? (cuuint64_t)(d0 / 2) : (cuuint64_t)d1,
+                                split ? (cuuint64_t)d1 : (cuuint64_t)d2, (cuuint64_t)d2};
+    const cuuint64_t gstr[3] = {split ? 16u : (cuuint64_t)(d0 * 8), split ? (cuuint64_t)(d0 * 8) : (cuuint64_t)(d0 * 8 * d1),
+                                (cuuint64_t)(d0 * 8 * d1)};
+    const cuuint32_t box[4] = {split ? 2u : (cuuint32_t)b0, split ? (cuuint32_t)(b0 / 2) : (cuuint32_t)b1,
+                               split ? (cuuint32_t)b1 : (cuuint32_t)b2, (cuuint32_t)b2},
+                     est[4] = {1u, 1u, 1u, 1u};
     CUtensorMap m;
-    const CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), gdim, gstr, box, est,
+    const CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, split ? 4 : 3, const_cast<void*>(base), gdim, gstr, box, est,
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     KS_REQUIRE(r == CUDA_SUCCESS, KS_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
@@ -562,7 +571,7 @@ bool kron_jit_launch(const KronJitPair& J, const double2* const* ip, double2* co
         unsigned char* w = raw.data() + (64 - reinterpret_cast<uintptr_t>(raw.data()) % 64) % 64;
         unsigned char* const w0 = w;
         for (int g = 0; g < J.nin; ++g, w += 128) {
-            if (J.line) encode_map3(w, hin[g], 2LL * J.n_a, J.n_b, J.n_outer, 2 * J.n_a, 1, J.no); // lines of plane ib, C of them
+            if (J.line) encode_map3(w, hin[g], 2LL * J.n_a, J.n_b, J.n_outer, 2 * J.n_a, 1, J.no, J.n_a > 128); // lines of plane ib, C of them
             else encode_map3(w, hin[g], 2 * J.s_a, J.n_a, (long long)J.n_b * J.n_outer, 64, J.no + 2 * J.bw, 1);
         }
         for (int o = 0; o < J.nout; ++o, w += sizeof(void*)) std::memcpy(w, &hout[o], sizeof(void*));
@@ -947,7 +956,8 @@ KronJitPair* kron_jitl_build(int nin, int nmid, int nout, int bw, const std::vec
     if (const char* e = std::getenv("KS_KRON_JIT"))
         if (std::strcmp(e, "0") == 0) return nullptr;
     if (nin < 1 || nmid < 1 || nout < 1 || nin > 2 || nmid > 6 || nout > 4 || bw < 1 || bw > 4) return nullptr;
-    if (n_a > 128 || n_a < 2 * bw + 1 || n_b < 4 * bw + 2 || C < 1 || n_outer < C) return nullptr; // (box: <= 256 doubles per line)
+    if (n_a > 256 || n_a < 2 * bw + 1 || n_b < 4 * bw + 2 || C < 1 || n_outer < C) return nullptr;
+    const bool split = n_a > 128; // a box holds <= 256 doubles per dimension: lines as (2, n_a) then
     const int W = 2 * bw + 1;
     auto cls = [&](int f) { return freal[f]; };
     std::set<int> FB;
@@ -979,7 +989,7 @@ KronJitPair* kron_jitl_build(int nin, int nmid, int nout, int bw, const std::vec
     s << "// generated: line variant of the fused level passes (ks_kron_jit.cu)\n"
       << "#define BW " << bw << "\n#define W " << W << "\n#define NIN " << nin << "\n#define NMID " << nmid << "\n#define NOUT "
       << nout << "\n#define C " << C << "\n#define NP " << NP << "\n#define NW " << NW << "\n#define S " << S << "\n#define SP " << SP
-      << "\n#define MINB " << minb << "\n#define PADF " << PADF << "\n#define n_a " << n_a << "\n#define n_b " << n_b << "\n#define n_outer " << n_outer << "LL\n"
+      << "\n#define SPLIT " << (split ? 1 : 0) << "\n#define MINB " << minb << "\n#define PADF " << PADF << "\n#define n_a " << n_a << "\n#define n_b " << n_b << "\n#define n_outer " << n_outer << "LL\n"
       << "struct __align__(64) TMap { unsigned long long d[16]; };\n"
       << "struct Par { TMap tm[NIN]; double2* out[NOUT]; const double2* rb; int nmax; };\n"
       << R"(
@@ -1018,10 +1028,17 @@ extern "C" __global__ void __launch_bounds__(32 * (NW + 1), MINB) ks_pairl(const
                          "r"((unsigned)(NIN * NP * 16)) : "memory");
 #pragma unroll
             for (int g = 0; g < NIN; ++g)
+#if SPLIT
+                asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::
+                             "r"(su32(ring + (size_t)(slot * NIN + g) * SP + PADF)), "l"(&P.tm[g]), "r"(0), "r"(0), "r"(ib), "r"((int)o0),
+                             "r"(su32(full + slot))
+                             : "memory");
+#else
                 asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
                              "r"(su32(ring + (size_t)(slot * NIN + g) * SP + PADF)), "l"(&P.tm[g]), "r"(0), "r"(ib), "r"((int)o0),
                              "r"(su32(full + slot))
                              : "memory");
+#endif
         }
         return;
     }

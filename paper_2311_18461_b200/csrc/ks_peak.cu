@@ -221,17 +221,33 @@ void fp64_peak_bench_mma(double* tflops) { run_peak(true, tflops); }
 
 } // namespace ks
 
-// HBM fan-in/fan-out bandwidth: read NIN arrays, write NOUT arrays (sum / copies)
-__global__ void k_fan(const double2* const* __restrict__ in, int nin, double2* const* __restrict__ out,
-                      int nout, size_t n) {
+// HBM fan-in/fan-out bandwidth: read NIN arrays, write NOUT arrays (sum / copies),
+// fully unrolled over the arrays (the matvec passes' 1:3 and 3:1 mixes)
+struct FanPtrs {
+    const double2* in[4];
+    double2* out[4];
+};
+template <int NI, int NO>
+__global__ void __launch_bounds__(512) k_fan(FanPtrs p, size_t n) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-        double2 a = make_double2(0, 0);
-        for (int j = 0; j < nin; ++j) {
-            const double2 v = __ldg(in[j] + i);
+        double2 a = __ldg(p.in[0] + i);
+#pragma unroll
+        for (int j = 1; j < NI; ++j) {
+            const double2 v = __ldg(p.in[j] + i);
             a.x += v.x;
             a.y += v.y;
         }
-        for (int k = 0; k < nout; ++k) __stcs(out[k] + i, make_double2(a.x * (k + 1), a.y));
+#pragma unroll
+        for (int k = 0; k < NO; ++k) __stcs(p.out[k] + i, make_double2(a.x * (k + 1), a.y));
+    }
+}
+template <int NI>
+static void launch_fan(int nout, const FanPtrs& p, size_t n) {
+    switch (nout) {
+    case 1: k_fan<NI, 1><<<148 * 8, 512>>>(p, n); break;
+    case 2: k_fan<NI, 2><<<148 * 8, 512>>>(p, n); break;
+    case 3: k_fan<NI, 3><<<148 * 8, 512>>>(p, n); break;
+    default: k_fan<NI, 4><<<148 * 8, 512>>>(p, n); break;
     }
 }
 extern "C" int ks_bw_fan(int nin, int nout, size_t n, double* gbs) {
@@ -243,17 +259,22 @@ extern "C" int ks_bw_fan(int nin, int nout, size_t n, double* gbs) {
             KS_CUDA(cudaMemset(bufs.back().p, 0, n * sizeof(double2)));
             ptr.push_back(bufs.back().p);
         }
-        ks::DevBuf dp(ptr.size() * sizeof(void*));
-        KS_CUDA(cudaMemcpy(dp.p, ptr.data(), ptr.size() * sizeof(void*), cudaMemcpyHostToDevice));
-        const double2* const* ip = reinterpret_cast<const double2* const*>(dp.p);
-        double2* const* op = reinterpret_cast<double2* const*>(static_cast<void**>(dp.p) + nin);
+        if (nin < 1 || nin > 4 || nout < 1 || nout > 4) throw ks::Error(KS_EINVAL, "ks_bw_fan: 1..4 inputs and outputs");
+        FanPtrs fp{};
+        for (int j = 0; j < nin; ++j) fp.in[j] = static_cast<const double2*>(ptr[j]);
+        for (int k = 0; k < nout; ++k) fp.out[k] = static_cast<double2*>(ptr[nin + k]);
         cudaEvent_t a, b;
         KS_CUDA(cudaEventCreate(&a));
         KS_CUDA(cudaEventCreate(&b));
         float best = 1e30f;
-        for (int rep = 0; rep < 5; ++rep) {
+        for (int rep = 0; rep < 8; ++rep) {
             KS_CUDA(cudaEventRecord(a));
-            k_fan<<<148 * 16, 256>>>(ip, nin, op, nout, n);
+            switch (nin) {
+            case 1: launch_fan<1>(nout, fp, n); break;
+            case 2: launch_fan<2>(nout, fp, n); break;
+            case 3: launch_fan<3>(nout, fp, n); break;
+            default: launch_fan<4>(nout, fp, n); break;
+            }
             ks::check_launch("k_fan");
             KS_CUDA(cudaEventRecord(b));
             KS_CUDA(cudaEventSynchronize(b));
