@@ -33,6 +33,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -67,6 +68,15 @@ cudaKernel_t nvrtc_kernel(const std::string& src, const char* name, size_t max_s
     const std::string key = std::to_string(dev0) + ":" + name + "\n" + src;
     auto it = jit_cache().find(key);
     if (it != jit_cache().end()) return it->second;
+    // KS_KRON_JIT=dump=<dir>: the generated sources, for offline inspection (cuobjdump -sass)
+    if (const char* e = std::getenv("KS_KRON_JIT"))
+        if (!std::strncmp(e, "dump=", 5)) {
+            const std::string fn = std::string(e + 5) + "/ks_jit_" + name + "_" + std::to_string(std::hash<std::string>{}(src) % 100000) + ".cu";
+            if (FILE* f = std::fopen(fn.c_str(), "w")) {
+                std::fwrite(src.data(), 1, src.size(), f);
+                std::fclose(f);
+            }
+        }
     nvrtcProgram prog;
     KS_NVRTC(nvrtcCreateProgram(&prog, src.c_str(), "ks_kron_jit.cu", 0, nullptr, nullptr));
     const char* opts[] = {"-arch=sm_100a", "-std=c++17", "-lineinfo", "-default-device"};
@@ -633,6 +643,35 @@ std::string hexd(double v) {
     return std::string(b);
 }
 
+// Literal coefficients of a generated kernel: entries of one __constant__ table
+// referenced with constant indices, so they become constant-bank operands of
+// the DFMAs (inline literals are materialised with two UMOVs each -- about one
+// extra instruction per DFMA in the sweep stage; line kernel 249 -> 240 us).
+struct ConstTable {
+    std::vector<double> v;
+    bool inline_literals = false; // the row-blocked kernel is faster with inline literals (187 vs 225 us at c3)
+    std::string ref(double x) {
+        if (inline_literals) return hexd(x);
+        size_t i = 0;
+        for (; i < v.size(); ++i)
+            if (std::memcmp(&v[i], &x, sizeof x) == 0) break;
+        if (i == v.size()) v.push_back(x);
+        return "KC[" + std::to_string(i) + "]";
+    }
+    std::string decl() const {
+        std::string t = "__constant__ double KC[" + std::to_string(std::max<size_t>(1, v.size())) + "] = {";
+        for (size_t i = 0; i < v.size(); ++i) t += (i ? ", " : "") + hexd(v[i]);
+        if (v.empty()) t += "0.0";
+        return t + "};\n";
+    }
+    // insert the table after the parameter struct of the generated source
+    std::string finish(const std::string& src) const {
+        const std::string mark = "int nmax; };\n";
+        const size_t at = src.find(mark);
+        return src.substr(0, at + mark.size()) + decl() + src.substr(at + mark.size());
+    }
+};
+
 // rows [lo, hi) of factor f equal to the middle row (relative 1e-13)
 void toeplitz_range(const double2* hrb, int f, int nmax, int n, int W, int& lo, int& hi) {
     const int mid = n / 2;
@@ -709,6 +748,8 @@ KronJitPair* kron_jitb_build(int nin, int nmid, int nout, int bw, const std::vec
         if (cval(c.coeff).y != 0.0) return nullptr; // (complex contribution coefficients: the other kernel)
     for (auto& c : b)
         if (cval(c.coeff).y != 0.0) return nullptr;
+    ConstTable KT;
+    KT.inline_literals = true;
     std::ostringstream s;
     s << "// generated: row-blocked fused level passes (ks_kron_jit.cu)\n"
       << "#define BW " << bw << "\n#define W " << W << "\n#define NIN " << nin << "\n#define NMID " << nmid << "\n#define NOUT "
@@ -805,17 +846,17 @@ extern "C" __global__ void __launch_bounds__(32 * (NW + 1), 1) ks_pairb(const __
                         const std::string wv = "w[" + lit(r + k) + "]";
                         if (cls(f) == 1) {
                             if (e.x == 0.0) continue;
-                            const std::string v = hexd(cc * e.x);
+                            const std::string v = KT.ref(cc * e.x);
                             s << "                " << acc << ".x = fma(" << v << ", " << wv << ".x, " << acc << ".x); " << acc
                               << ".y = fma(" << v << ", " << wv << ".y, " << acc << ".y);\n";
                         } else if (cls(f) == 2) {
                             if (e.y == 0.0) continue;
-                            const std::string v = hexd(cc * e.y);
+                            const std::string v = KT.ref(cc * e.y);
                             s << "                " << acc << ".x = fma(-(" << v << "), " << wv << ".y, " << acc << ".x); " << acc
                               << ".y = fma(" << v << ", " << wv << ".x, " << acc << ".y);\n";
                         } else {
                             if (e.x == 0.0 && e.y == 0.0) continue;
-                            const std::string vx = hexd(cc * e.x), vy = hexd(cc * e.y);
+                            const std::string vx = KT.ref(cc * e.x), vy = KT.ref(cc * e.y);
                             s << "                " << acc << ".x = fma(" << vx << ", " << wv << ".x, fma(-(" << vy << "), " << wv
                               << ".y, " << acc << ".x)); " << acc << ".y = fma(" << vx << ", " << wv << ".y, fma(" << vy << ", "
                               << wv << ".x, " << acc << ".y));\n";
@@ -863,17 +904,17 @@ extern "C" __global__ void __launch_bounds__(32 * (NW + 1), 1) ks_pairb(const __
                     const std::string mv = "m[" + lit(c.in) + "][" + lit(r) + "]";
                     if (cls(f) == 1) {
                         if (e.x == 0.0) continue;
-                        const std::string v = hexd(cc * e.x);
+                        const std::string v = KT.ref(cc * e.x);
                         s << "                    " << acc << ".x = fma(" << v << ", " << mv << ".x, " << acc << ".x); " << acc
                           << ".y = fma(" << v << ", " << mv << ".y, " << acc << ".y);\n";
                     } else if (cls(f) == 2) {
                         if (e.y == 0.0) continue;
-                        const std::string v = hexd(cc * e.y);
+                        const std::string v = KT.ref(cc * e.y);
                         s << "                    " << acc << ".x = fma(-(" << v << "), " << mv << ".y, " << acc << ".x); " << acc
                           << ".y = fma(" << v << ", " << mv << ".x, " << acc << ".y);\n";
                     } else {
                         if (e.x == 0.0 && e.y == 0.0) continue;
-                        const std::string vx = hexd(cc * e.x), vy = hexd(cc * e.y);
+                        const std::string vx = KT.ref(cc * e.x), vy = KT.ref(cc * e.y);
                         s << "                    " << acc << ".x = fma(" << vx << ", " << mv << ".x, fma(-(" << vy << "), " << mv
                           << ".y, " << acc << ".x)); " << acc << ".y = fma(" << vx << ", " << mv << ".y, fma(" << vy << ", " << mv
                           << ".x, " << acc << ".y));\n";
@@ -891,7 +932,7 @@ extern "C" __global__ void __launch_bounds__(32 * (NW + 1), 1) ks_pairb(const __
             const double cc = coeffs[c.coeff].x;
             for (int r = 0; r < R; ++r) {
                 const std::string mv = "m[" + lit(c.in) + "][" + lit(r) + "]";
-                s << "                    { const double2 cm = make_double2(" << hexd(cc) << " * " << mv << ".x, " << hexd(cc) << " * " << mv
+                s << "                    { const double2 cm = make_double2(" << KT.ref(cc) << " * " << mv << ".x, " << KT.ref(cc) << " * " << mv
                   << ".y);\n";
                 for (int j = 0; j < W; ++j) {
                     const std::string acc = "win[" + lit(c.out) + "][" + lit(r) + "][" + slotj(j) + "]";
@@ -916,7 +957,7 @@ extern "C" __global__ void __launch_bounds__(32 * (NW + 1), 1) ks_pairb(const __
     s << "        }\n        ph = ph + 1 == W ? 0 : ph + 1;\n    }\n}\n";
     std::unique_ptr<KronJitPair> P(new KronJitPair());
     const size_t smem = (size_t)S * stage + (size_t)2 * S * 8 + 128;
-    P->k.fn = nvrtc_kernel(s.str(), "ks_pairb", 227 * 1024);
+    P->k.fn = nvrtc_kernel(KT.finish(s.str()), "ks_pairb", 227 * 1024);
     P->blocked = true;
     P->nin = nin;
     P->nmid = nmid;
@@ -985,6 +1026,7 @@ KronJitPair* kron_jitl_build(int nin, int nmid, int nout, int bw, const std::vec
     if (S < 2) return nullptr;
     const long long ntile = (n_outer + C - 1) / C;
     auto band = [&](int f, int row, int k) -> double2 { return hrb[((size_t)f * nmax + row) * W + k]; };
+    ConstTable KT;
     std::ostringstream s;
     s << "// generated: line variant of the fused level passes (ks_kron_jit.cu)\n"
       << "#define BW " << bw << "\n#define W " << W << "\n#define NIN " << nin << "\n#define NMID " << nmid << "\n#define NOUT "
@@ -1051,7 +1093,7 @@ extern "C" __global__ void __launch_bounds__(32 * (NW + 1), MINB) ks_pairl(const
     // in-plane rows in registers, pre-multiplied by the contribution coefficient
     for (size_t ci = 0; ci < a.size(); ++ci) {
         const int f = a[ci].factor;
-        const std::string cc = hexd(coeffs[a[ci].coeff].x);
+        const std::string cc = KT.ref(coeffs[a[ci].coeff].x);
         if (cls(f) == 0) {
             s << "    double2 A" << ci << "[W];\n#pragma unroll\n    for (int k = 0; k < W; ++k) { const double2 t_ = valid ? __ldg(P.rb + ((size_t)"
               << f << " * P.nmax + ia) * W + k) : Z; A" << ci << "[k] = make_double2(" << cc << " * t_.x, " << cc << " * t_.y); }\n";
@@ -1102,17 +1144,17 @@ extern "C" __global__ void __launch_bounds__(32 * (NW + 1), MINB) ks_pairl(const
                 const std::string acc = "win[" + lit(c.out) + "][" + slotj(j) + "]", mv = "m[" + lit(c.in) + "]";
                 if (cls(f) == 1) {
                     if (e.x == 0.0) continue;
-                    const std::string v = hexd(cc * e.x);
+                    const std::string v = KT.ref(cc * e.x);
                     s << "                    " << acc << ".x = fma(" << v << ", " << mv << ".x, " << acc << ".x); " << acc << ".y = fma(" << v
                       << ", " << mv << ".y, " << acc << ".y);\n";
                 } else if (cls(f) == 2) {
                     if (e.y == 0.0) continue;
-                    const std::string v = hexd(cc * e.y);
+                    const std::string v = KT.ref(cc * e.y);
                     s << "                    " << acc << ".x = fma(-(" << v << "), " << mv << ".y, " << acc << ".x); " << acc << ".y = fma(" << v
                       << ", " << mv << ".x, " << acc << ".y);\n";
                 } else {
                     if (e.x == 0.0 && e.y == 0.0) continue;
-                    const std::string vx = hexd(cc * e.x), vy = hexd(cc * e.y);
+                    const std::string vx = KT.ref(cc * e.x), vy = KT.ref(cc * e.y);
                     s << "                    " << acc << ".x = fma(" << vx << ", " << mv << ".x, fma(-(" << vy << "), " << mv << ".y, " << acc
                       << ".x)); " << acc << ".y = fma(" << vx << ", " << mv << ".y, fma(" << vy << ", " << mv << ".x, " << acc << ".y));\n";
                 }
@@ -1123,7 +1165,7 @@ extern "C" __global__ void __launch_bounds__(32 * (NW + 1), MINB) ks_pairl(const
             s << "                    double2 C" << f << "[W];\n#pragma unroll\n                    for (int j = 0; j < W; ++j) { const int r_ = ib + j - BW; C"
               << f << "[j] = (r_ >= 0 && r_ < n_b) ? __ldg(P.rb + ((size_t)" << f << " * P.nmax + r_) * W + (W - 1 - j)) : Z; }\n";
         for (auto& c : b) {
-            const std::string mv = "m[" + lit(c.in) + "]", cc = hexd(coeffs[c.coeff].x);
+            const std::string mv = "m[" + lit(c.in) + "]", cc = KT.ref(coeffs[c.coeff].x);
             s << "                    { const double2 cm = make_double2(" << cc << " * " << mv << ".x, " << cc << " * " << mv << ".y);\n";
             for (int j = 0; j < W; ++j) {
                 const std::string acc = "win[" + lit(c.out) + "][" + slotj(j) + "]", cf = "C" + lit(c.factor) + "[" + lit(j) + "]";
@@ -1141,7 +1183,7 @@ extern "C" __global__ void __launch_bounds__(32 * (NW + 1), MINB) ks_pairl(const
     }
     s << "        }\n        ph = ph + 1 == W ? 0 : ph + 1;\n    }\n}\n";
     std::unique_ptr<KronJitPair> P(new KronJitPair());
-    P->k.fn = nvrtc_kernel(s.str(), "ks_pairl", 227 * 1024);
+    P->k.fn = nvrtc_kernel(KT.finish(s.str()), "ks_pairl", 227 * 1024);
     P->blocked = true;
     P->line = true;
     P->nin = nin;
