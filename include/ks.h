@@ -82,8 +82,9 @@ int ks_device_count(void);
  * ------------------------------------------------------------------------- */
 typedef struct ks_fd ks_fd;
 
-/* Limits: d <= 3, p_t <= 8, every spatial axis n_l <= 160 (the transforms keep
- * U_l in shared memory; longer axes return KS_EINVAL at creation). */
+/* Limits: d <= 3, p_t <= 8. Spatial axes up to 160 entries run the folded
+ * transforms with U_l resident in shared memory; longer axes (no limit, as in
+ * tensorops.cpp:125-156) run a dense panel kernel. */
 int ks_fd_create(int d, const int* dims, double nu, int p_t,
                  const double* const* U, const double* const* lambda,
                  const double* Lt, const double* Mt, const ks_c64* Wt,

@@ -433,10 +433,9 @@ static void fd_create_impl(int kind, int d, const int* dims, double nu, int p_t,
     KS_REQUIRE(p_t >= 1 && p_t <= 8, KS_EINVAL, "ks_fd_create: time degree must be 1..8");
     for (int a = 0; a <= d; ++a) KS_REQUIRE(dims[a] >= 1, KS_EINVAL, "CoeffTensor: dims must be positive");
     for (int l = 0; l < d; ++l) KS_REQUIRE(U[l] && lambda[l], KS_EINVAL, "ks_fd_create: NULL U/lambda");
-    // the transforms keep the (folded halves of the) n x n eigenvector matrix
-    // resident in shared memory: n <= 160 (every BASELINE config: n <= 132)
-    for (int l = 1; l <= d; ++l)
-        KS_REQUIRE(dims[l] <= 160, KS_EINVAL, "ks_fd_create: spatial axis longer than 160 not supported");
+    // (axes up to 160 keep the folded halves of the eigenvector matrix resident in
+    // shared memory -- every BASELINE config: n <= 132; longer axes run the dense
+    // panel kernel, ks_transform.cu)
     ensure_device(device);
     std::unique_ptr<ks_fd> f(new ks_fd());
     f->device = device;

@@ -610,7 +610,8 @@ KronPlan* kron_plan(const std::vector<int>& dims,
                 }
             if (P->jit[k] && sa == 1)
                 // (5 lines, 16 stages, one CTA per SM; fewer lines with 2-3 CTAs per SM spill: 510-540 us vs 249 us at c3)
-                for (auto cfg : {std::array<int, 3>{5, 16, 1}}) {
+                // longer lines (c5: 131 entries): the most lines that fit 15 consumer warps
+                for (auto cfg : {std::array<int, 3>{std::max(1, std::min(5, 480 / na)), 16, 1}}) {
                     std::unique_ptr<KronJitPair, KronJitDeleter> alt(
                         kron_jitl_build(pa.n_in, pa.n_out, pb.n_out, P->bwmax, ca, cb, frv, co, na, nbb, outer, rb.data(), nmax,
                                         cfg[0], cfg[1], cfg[2]));

@@ -320,6 +320,150 @@ void launch_tm(const double* At, int n, const double* X, double* Y, cudaStream_t
 }
 
 // ---------------------------------------------------------------------------
+// Panel variant for long axes (n > 160: the n x n matrix no longer fits shared
+// memory): the output rows are processed in panels of 128, and the 16 x 128
+// chunk of the matrix travels through the cp.async ring beside the X chunk
+// (8-byte copies: a row of At starts at an odd double when n is odd). The X
+// tile is re-read once per panel (from L2). Same fragment layout, column maps
+// and layouts as k_mode_gemm_dmma2 with TM = 8. The reference has no length
+// limit (tensorops.cpp:125-156); SPEC uses 1-D pencils up to 256 elements.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc, bool valid) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    const int sz = valid ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(gsrc), "r"(sz));
+}
+
+template <int STG, bool ROWS>
+__global__ void __launch_bounds__(kThreads, 1)
+k_mode_gemm_panel(const double* __restrict__ At, int n, const double* __restrict__ X, double* __restrict__ Y, ColMap M) {
+    constexpr int MT = 8, BM = 16 * MT;
+    constexpr int BMP = BM + 4, BNP = kBN + 4;
+    extern __shared__ __align__(16) double smem[];
+    double* As = smem;                           // [STG][kBK][BMP]
+    double* Bs = smem + (size_t)STG * kBK * BMP; // [STG][kBK][BNP]
+    const int nk = (n + kBK - 1) / kBK, np = (n + BM - 1) / BM;
+    const long long in_rs = (M.mode == MAP_TIN || M.mode == MAP_TIN1) ? 2 * M.Np : 2 * M.s;
+    const long long out_rs = (M.mode == MAP_TOUT || M.mode == MAP_TOUT1) ? 2 * M.Np : 2 * M.s;
+    const long long ntiles = M.ntiles;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wr = warp & 1, wc = warp >> 1;
+    const int lcp = tid & 63, lrow0 = tid >> 6;
+    const int my_tiles =
+        ntiles > (long long)blockIdx.x ? (int)((ntiles - 1 - (long long)blockIdx.x) / gridDim.x + 1) : 0;
+    const long long nwork = (long long)my_tiles * np * nk;
+    long long cur_tile = -1, cur_in = 0;
+    bool cur_valid = false;
+
+    auto issue = [&](long long w) {
+        if (w < nwork) {
+            const long long wt = w / ((long long)np * nk);
+            const int rem = (int)(w - wt * np * nk), pnl = rem / nk, kc = rem - pnl * nk;
+            const long long tile = (long long)blockIdx.x + wt * gridDim.x;
+            if (tile != cur_tile) {
+                long long dummy;
+                cur_valid = colmap(M, n, tile_base(M, tile), lcp, cur_in, dummy);
+                cur_tile = tile;
+            }
+            const int slot = (int)(w % STG);
+            double* bs = Bs + (size_t)slot * kBK * BNP;
+            double* as = As + (size_t)slot * kBK * BMP;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int jj = lrow0 + 4 * k, j = kc * kBK + jj;
+                const bool v = cur_valid && j < n;
+                cp_async16(bs + jj * BNP + 2 * lcp, v ? (const void*)in_row<ROWS>(M, X, cur_in, j, in_rs) : (const void*)X,
+                           v);
+            }
+#pragma unroll
+            for (int k = 0; k < (kBK * BM) / kThreads; ++k) {
+                const int e = tid + k * kThreads, jj = e / BM, r = e - jj * BM;
+                const int j = kc * kBK + jj, row = pnl * BM + r;
+                const bool v = j < n && row < n;
+                cp_async8(as + jj * BMP + r, v ? (const void*)(At + (long long)j * n + row) : (const void*)At, v);
+            }
+        }
+        cp_async_commit();
+    };
+
+    double acc[MT][4][2];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int m = 0; m < 4; ++m) acc[i][m][0] = acc[i][m][1] = 0.0;
+#pragma unroll
+    for (int s = 0; s < STG - 1; ++s) issue(s);
+
+    const int r_warp = wr * (BM / 2), c_warp = wc * 32;
+    const int ar = lane >> 2, ak = lane & 3, cr = lane >> 2;
+    int kc = 0, pnl = 0;
+    long long wt = 0;
+    for (long long w = 0; w < nwork; ++w) {
+        cp_async_wait<STG - 2>();
+        __syncthreads();
+        issue(w + STG - 1);
+        const int slot = (int)(w % STG);
+        const double* bs = Bs + (size_t)slot * kBK * BNP;
+        const double* as = As + (size_t)slot * kBK * BMP;
+#pragma unroll
+        for (int k4 = 0; k4 < kBK; k4 += 4) {
+            double a[MT], b[4];
+#pragma unroll
+            for (int i = 0; i < MT; ++i) a[i] = as[(k4 + ak) * BMP + r_warp + i * 8 + ar];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) b[m] = bs[(k4 + ak) * BNP + c_warp + m * 8 + ar];
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int m = 0; m < 4; ++m) dmma_m8n8k4(acc[i][m][0], acc[i][m][1], a[i], b[m]);
+        }
+        if (kc == nk - 1) {
+            const long long tile = (long long)blockIdx.x + wt * gridDim.x;
+            const TileBase tbase = tile_base(M, tile);
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const int jcol = (c_warp >> 1) + m * 4 + (lane & 3); // complex column in tile
+                long long io, oo;
+                if (colmap(M, n, tbase, jcol, io, oo)) {
+#pragma unroll
+                    for (int i = 0; i < MT; ++i) {
+                        const int r = pnl * BM + r_warp + i * 8 + cr;
+                        if (r < n)
+                            *reinterpret_cast<double2*>(out_row<ROWS>(M, Y, oo, r, out_rs)) =
+                                make_double2(acc[i][m][0], acc[i][m][1]);
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < MT; ++i) acc[i][m][0] = acc[i][m][1] = 0.0;
+            }
+            kc = 0;
+            if (++pnl == np) {
+                pnl = 0;
+                ++wt;
+            }
+        } else {
+            ++kc;
+        }
+    }
+    cp_async_wait<0>();
+}
+
+void launch_panel(const double* At, int n, const double* X, double* Y, cudaStream_t st, const ColMap* map) {
+    constexpr int STG = 4;
+    const size_t sm = (size_t)STG * kBK * ((16 * 8 + 4) + (kBN + 4)) * sizeof(double);
+    ColMap M = *map;
+    const unsigned g = (unsigned)std::min<long long>(M.ntiles, (long long)device_sms());
+    if (M.rin || M.rout) {
+        smem_optin((const void*)k_mode_gemm_panel<STG, true>, (int)sm);
+        k_mode_gemm_panel<STG, true><<<g, kThreads, sm, st>>>(At, n, X, Y, M);
+    } else {
+        smem_optin((const void*)k_mode_gemm_panel<STG, false>, (int)sm);
+        k_mode_gemm_panel<STG, false><<<g, kThreads, sm, st>>>(At, n, X, Y, M);
+    }
+    check_launch("k_mode_gemm_panel");
+}
+
+// ---------------------------------------------------------------------------
 // Folded (even/odd) transform. On a uniform mesh the 1-D pencils are
 // centro-symmetric (J K J = K, J M J = M, J the flip), so every eigenvector is
 // even (u[n-1-j] = u[j]) or odd (u[n-1-j] = -u[j]); ceil(n/2) of them are even.
@@ -656,7 +800,7 @@ ColMap make_colmap(int n, size_t s_complex, size_t outer, int layout, int nt) {
 
 bool fold_axis_build(const double* U_in, const double* lam, int n, double tol, FoldAxis& F) {
     // U column-major: U(j, r) = U[j + r*n]
-    if (n < 2) return false;
+    if (n < 2 || n > 160) return false; // (long axes: the dense panel kernel)
     if (const char* e = std::getenv("KS_FD_FOLD"))
         if (std::strcmp(e, "0") == 0) return false;
     const int hc = (n + 1) / 2;
@@ -840,7 +984,7 @@ void launch_mode_gemm(const double* At, int n, const double* X, double* Y, size_
         M.ntiles = M.ntb * ((M.Np + M.tbr - 1) / M.tbr);
     }
     const int tm = (n + 15) / 16;
-    KS_REQUIRE(tm <= 10, KS_EINVAL, "mode product: axis length > 160 not supported");
+    if (tm > 10) return launch_panel(At, n, X, Y, st, &M); // long axes: matrix panels streamed beside X
     switch (tm) {
     case 1: launch_tm<1>(At, n, X, Y, st, &M); break;
     case 2: launch_tm<2>(At, n, X, Y, st, &M); break;
