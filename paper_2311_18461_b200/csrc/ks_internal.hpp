@@ -206,12 +206,16 @@ KronJitPair* kron_jit_build(int nin, int nmid, int nout, int bw, const std::vect
 KronJitPair* kron_jitb_build(int nin, int nmid, int nout, int bw, const std::vector<JitContrib>& a,
                              const std::vector<JitContrib>& b, const std::vector<int>& freal,
                              const std::vector<double2>& coeffs, long long s_a, int n_a, int n_b, long long n_outer,
-                             const double2* hrb, int nmax, int R);
+                             const double2* hrb, int nmax, int R, bool align4 = false);
 // line variant for s_a = 1 (thread per point of C whole lines, planes as tensor-map boxes)
 KronJitPair* kron_jitl_build(int nin, int nmid, int nout, int bw, const std::vector<JitContrib>& a,
                              const std::vector<JitContrib>& b, const std::vector<int>& freal,
                              const std::vector<double2>& coeffs, int n_a, int n_b, long long n_outer,
                              const double2* hrb, int nmax, int C, int smax, int minb);
+KronJitPair* kron_jitt_build(int nin, int nmid, int nout, int bw, const std::vector<JitContrib>& a,
+                             const std::vector<JitContrib>& b, const std::vector<int>& freal,
+                             const std::vector<double2>& coeffs, int n_a, int n_b, long long n_outer,
+                             const double2* hrb, int nmax, int RB, int RA, int RR, int NWARP, int minb);
 bool kron_jit_same_shape(const KronJitPair& A, const KronJitPair& B);
 int kron_jit_blocked_rows(const KronJitPair& J); // rows per thread of the row-blocked variant, -(lines per CTA) of the line variant, 0 for thread-per-point
 bool kron_jit_launch(const KronJitPair& J, const double2* const* ip, double2* const* op, void* const* hin,

@@ -607,6 +607,11 @@ KronPlan* kron_plan(const std::vector<int>& dims,
                         pa.n_in, pa.n_out, pb.n_out, P->bwmax, ca, cb, frv, co, (long long)sa, na, nbb, outer, rb.data(),
                         nmax, rr));
                     if (alt) P->jit_alt[k].push_back(std::move(alt));
+                    // the same with the warp count aligned to the register allocation unit
+                    std::unique_ptr<KronJitPair, KronJitDeleter> al4(kron_jitb_build(
+                        pa.n_in, pa.n_out, pb.n_out, P->bwmax, ca, cb, frv, co, (long long)sa, na, nbb, outer, rb.data(),
+                        nmax, rr, true));
+                    if (al4) P->jit_alt[k].push_back(std::move(al4));
                 }
             if (P->jit[k] && sa == 1)
                 // (5 lines, 16 stages, one CTA per SM; fewer lines with 2-3 CTAs per SM spill: 510-540 us vs 249 us at c3)
@@ -615,6 +620,15 @@ KronPlan* kron_plan(const std::vector<int>& dims,
                     std::unique_ptr<KronJitPair, KronJitDeleter> alt(
                         kron_jitl_build(pa.n_in, pa.n_out, pb.n_out, P->bwmax, ca, cb, frv, co, na, nbb, outer, rb.data(), nmax,
                                         cfg[0], cfg[1], cfg[2]));
+                    if (alt) P->jit_alt[k].push_back(std::move(alt));
+                }
+            if (P->jit[k] && sa == 1 && pa.n_in == 1)
+                // tile variant: {rows per tile, entries / rows per thread in phases A / B, warps, CTAs per SM}
+                for (auto cfg : {std::array<int, 5>{16, 4, 4, 8, 2}, std::array<int, 5>{16, 4, 4, 16, 1},
+                                 std::array<int, 5>{24, 4, 4, 16, 1}}) {
+                    std::unique_ptr<KronJitPair, KronJitDeleter> alt(
+                        kron_jitt_build(pa.n_in, pa.n_out, pb.n_out, P->bwmax, ca, cb, frv, co, na, nbb, outer, rb.data(), nmax,
+                                        cfg[0], cfg[1], cfg[2], cfg[3], cfg[4]));
                     if (alt) P->jit_alt[k].push_back(std::move(alt));
                 }
         }
@@ -767,12 +781,15 @@ void kron_apply(KronPlan& P, const double2* x, double2* y, cudaStream_t st,
                 if (const char* e = std::getenv("KS_KRON_JIT")) {
                     // (b2 / b4: rows per thread of the row-blocked kernel; the line kernel's
                     // candidates report their lines per CTA and are picked by timing among them)
-                    const int want = !std::strcmp(e, "b2") ? 2 : !std::strcmp(e, "b4") ? 4 : !std::strcmp(e, "point") ? 0 : -1;
+                    const bool wtile = !std::strcmp(e, "tile");
+                    const int want = !std::strcmp(e, "b2") || wtile ? 2 : !std::strcmp(e, "b4") ? 4 : !std::strcmp(e, "point") ? 0 : -1;
                     if (want >= 0) {
                         std::vector<KronJitPair*> all{P.jit[k].get()};
                         for (auto& alt : P.jit_alt[k]) all.push_back(alt.get());
                         for (size_t a = 0; a < all.size(); ++a)
-                            if ((kron_jit_blocked_rows(*all[a]) == want || (want > 0 && kron_jit_blocked_rows(*all[a]) < 0)) &&
+                            if ((kron_jit_blocked_rows(*all[a]) == want ||
+                                 (want > 0 && !wtile && kron_jit_blocked_rows(*all[a]) < 0) ||
+                                 (wtile && kron_jit_blocked_rows(*all[a]) >= 1000)) &&
                                 tb[a] < 1e29f) {
                                 bi = a;
                                 break;

@@ -62,13 +62,8 @@ std::map<std::string, cudaKernel_t>& jit_cache() {
 // return kernel `name`, with its dynamic shared memory limit raised to max_smem.
 cudaKernel_t nvrtc_kernel(const std::string& src, const char* name, size_t max_smem) {
     std::lock_guard<std::mutex> lk(g_jit_mu);
-    int dev0 = 0;
-    KS_CUDA(cudaGetDevice(&dev0));
-    // per device: the shared-memory opt-in below is a per-device attribute
-    const std::string key = std::to_string(dev0) + ":" + name + "\n" + src;
-    auto it = jit_cache().find(key);
-    if (it != jit_cache().end()) return it->second;
-    // KS_KRON_JIT=dump=<dir>: the generated sources, for offline inspection (cuobjdump -sass)
+    // KS_KRON_JIT=dump=<dir>: the generated sources, for offline inspection (cuobjdump -sass);
+    // written before any device call, so a GPU-less host can generate and compile them
     if (const char* e = std::getenv("KS_KRON_JIT"))
         if (!std::strncmp(e, "dump=", 5)) {
             const std::string fn = std::string(e + 5) + "/ks_jit_" + name + "_" + std::to_string(std::hash<std::string>{}(src) % 100000) + ".cu";
@@ -77,6 +72,12 @@ cudaKernel_t nvrtc_kernel(const std::string& src, const char* name, size_t max_s
                 std::fclose(f);
             }
         }
+    int dev0 = 0;
+    KS_CUDA(cudaGetDevice(&dev0));
+    // per device: the shared-memory opt-in below is a per-device attribute
+    const std::string key = std::to_string(dev0) + ":" + name + "\n" + src;
+    auto it = jit_cache().find(key);
+    if (it != jit_cache().end()) return it->second;
     nvrtcProgram prog;
     KS_NVRTC(nvrtcCreateProgram(&prog, src.c_str(), "ks_kron_jit.cu", 0, nullptr, nullptr));
     const char* opts[] = {"-arch=sm_100a", "-std=c++17", "-lineinfo", "-default-device"};
@@ -129,6 +130,7 @@ struct KronJitPair {
     bool pull = true;
     bool blocked = false; // tensor-map fed variants (kron_jitb_build / kron_jitl_build)
     bool line = false;    // line variant (s_a = 1): boxes of whole lines
+    bool tile = false;    // tile variant (s_a = 1): two phases over shared memory, no tensor maps
     int T = 0, nq = 1, no = 1, D = 2, pad = 0; // block size, point block, ring depth, ring halo
     size_t smem = 0;                           // ring + staged axis-b bands
     long long s_a = 0, n_outer = 0;
@@ -524,11 +526,11 @@ bool kron_jit_runs(const KronJitPair& J) {
     // KS_KRON_JIT=b2 / b4 / point (a forced candidate: tests, profiling) also lifts the grid-size rule
     static const bool forced = [] {
         const char* e = std::getenv("KS_KRON_JIT");
-        return e && (!std::strcmp(e, "b2") || !std::strcmp(e, "b4") || !std::strcmp(e, "point"));
+        return e && (!std::strcmp(e, "b2") || !std::strcmp(e, "b4") || !std::strcmp(e, "point") || !std::strcmp(e, "tile"));
     }();
     return forced || J.grid >= (unsigned)sm_count();
 }
-int kron_jit_blocked_rows(const KronJitPair& J) { return J.blocked ? (J.line ? -J.nq : J.nq) : 0; }
+int kron_jit_blocked_rows(const KronJitPair& J) { return J.blocked ? (J.tile ? 1000 + J.nq : J.line ? -J.nq : J.nq) : 0; }
 bool kron_jit_same_shape(const KronJitPair& A, const KronJitPair& B) {
     return A.blocked == B.blocked && A.T == B.T && A.nq == B.nq && A.no == B.no && A.D == B.D;
 }
@@ -573,6 +575,22 @@ static void encode_map3(void* out, const void* base, long long d0, long long d1,
 bool kron_jit_launch(const KronJitPair& J, const double2* const* ip, double2* const* op, void* const* hin,
                      void* const* hout, const double2* rb, int nmax, cudaStream_t st) {
     if (!kron_jit_runs(J)) return false;
+    if (J.tile) {
+        // by-value parameter: input, outputs, band table
+        // (the generated Par: in, out[NOUT], rb, nmax)
+        std::vector<unsigned char> raw(sizeof(void*) * (2 + (size_t)J.nout) + sizeof(int) + 8, 0);
+        unsigned char* w = raw.data();
+        std::memcpy(w, &hin[0], sizeof(void*));
+        w += sizeof(void*);
+        for (int o = 0; o < J.nout; ++o, w += sizeof(void*)) std::memcpy(w, &hout[o], sizeof(void*));
+        std::memcpy(w, &rb, sizeof(void*));
+        w += sizeof(void*);
+        std::memcpy(w, &nmax, sizeof(int));
+        void* args[] = {(void*)raw.data()};
+        KS_CUDA(cudaLaunchKernel((const void*)J.k.fn, dim3(J.grid), dim3(J.T), args, J.smem, st));
+        check_launch("ks_pairt (jit)");
+        return true;
+    }
     if (J.blocked) {
         // by-value parameter: input / output tensors, band table
         // (tensor maps first: 64-byte aligned, 128 B each)
@@ -695,7 +713,7 @@ void toeplitz_range(const double2* hrb, int f, int nmax, int n, int W, int& lo, 
 KronJitPair* kron_jitb_build(int nin, int nmid, int nout, int bw, const std::vector<JitContrib>& a,
                              const std::vector<JitContrib>& b, const std::vector<int>& freal,
                              const std::vector<double2>& coeffs, long long s_a, int n_a, int n_b, long long n_outer,
-                             const double2* hrb, int nmax, int R) {
+                             const double2* hrb, int nmax, int R, bool align4) {
     if (const char* e = std::getenv("KS_KRON_JIT"))
         if (std::strcmp(e, "0") == 0) return nullptr;
     if (s_a < 32 || nin < 1 || nmid < 1 || nout < 1 || nin > 4 || nmid > 6 || nout > 2 || bw < 1 || bw > 4) return nullptr;
@@ -726,8 +744,25 @@ KronJitPair* kron_jitb_build(int nin, int nmid, int nout, int bw, const std::vec
     }
     if (loa > 8 || n_a - hia > 8 || lob > 8 || n_b - hib > 8) return nullptr; // not a uniform-mesh factor
     // tile: 32 lanes x RT rows (+ halo), RT a multiple of R, at most 32 rows
-    const int nrt = (n_a + 31) / 32;
+    // align4: the fewest row tiles whose consumer warps + the producer warp fill
+    // whole groups of four warps -- registers are allocated per four warps, so
+    // 13 + 1 warps (c5: 26 rows, R = 2) leave 128 registers per thread and the
+    // kernel spills, while 11 + 1 warps (22 rows) get 168 and do not
+    int nrt = (n_a + 31) / 32;
     int RT = ((n_a + nrt - 1) / nrt + R - 1) / R * R;
+    if (align4) {
+        bool found = false;
+        for (int t = nrt; t <= nrt + 3 && !found; ++t) {
+            const int rt = ((n_a + t - 1) / t + R - 1) / R * R;
+            if ((rt / R + 1) % 4 == 0 && rt / R >= 3) {
+                found = (t != nrt);
+                nrt = t;
+                RT = rt;
+                break;
+            }
+        }
+        if (!found) return nullptr; // (already aligned, or no aligned shape: the default candidate covers it)
+    }
     const int NW = RT / R;
     const int RTH = RT + 2 * bw;
     const size_t stage = (size_t)nin * RTH * 32 * sizeof(double2);
@@ -1202,6 +1237,290 @@ extern "C" __global__ void __launch_bounds__(32 * (NW + 1), MINB) ks_pairl(const
     P->n_b = n_b;
     P->n_outer = n_outer;
     P->grid = (unsigned)ntile;
+    P->coef = coeffs;
+    P->ncoef = (int)coeffs.size();
+    return P.release();
+}
+
+// ---------------------------------------------------------------------------
+// Tile variant for a contiguous in-plane axis (s_a = 1; at d = 3 the (t, 1)
+// pair) with one input: no register window at all. A CTA takes tiles of RB rows
+// of axis b (+ bw halo rows on both sides) x the whole axis a, of one outer
+// index, and runs two phases over shared memory:
+//   A  axis-a products of the RB + 2 bw rows: lanes across the rows (pitch odd
+//      in 16 B units: conflict-free), a thread owns RA consecutive entries of
+//      its row and loads RA + 2 bw values for them; the axis-a rows are uniform
+//      across the warp, so every band entry is a literal (one code path for the
+//      Toeplitz interior, one per boundary block); mids go back to shared memory;
+//   B  axis-b products: lanes across axis a, a thread owns RR consecutive rows
+//      and loads RR + 2 bw values per mid for them; literal band entries by row
+//      block class; streaming stores, coalesced along axis a.
+// The halo rows' axis-a products are recomputed ((RB + 2 bw) / RB of phase A).
+// The thread-per-point kernels keep a window of (outputs x W) complex values
+// per thread -- 108 registers at bw = 4 with three outputs, beside 54 for the
+// per-lane axis-a rows: they spill at c5 (ncu: 28% FP64 pipe). Here a thread
+// holds <= (RA + 2 bw) + nmid RA values in phase A and (RR + 2 bw) + nout RR in
+// phase B. The next tile's rows arrive by one bulk copy per row while phase B
+// runs.
+// ---------------------------------------------------------------------------
+KronJitPair* kron_jitt_build(int nin, int nmid, int nout, int bw, const std::vector<JitContrib>& a,
+                             const std::vector<JitContrib>& b, const std::vector<int>& freal,
+                             const std::vector<double2>& coeffs, int n_a, int n_b, long long n_outer,
+                             const double2* hrb, int nmax, int RB, int RA, int RR, int NWARP, int minb) {
+    if (const char* e = std::getenv("KS_KRON_JIT"))
+        if (std::strcmp(e, "0") == 0) return nullptr;
+    if (nin != 1 || nmid < 1 || nmid > 4 || nout < 1 || nout > 4 || bw < 1 || bw > 4) return nullptr;
+    if (n_a < 4 * bw + 2 || n_b < 4 * bw + 2 || RA < 1 || RR < 1 || RB < RR || RB % RR != 0) return nullptr;
+    const int W = 2 * bw + 1, RBH = RB + 2 * bw;
+    if (RBH > 32) return nullptr; // phase A: one lane per row
+    auto cls = [&](int f) { return freal[f]; };
+    std::set<int> FA, FB;
+    for (auto& c : a) {
+        if (c.factor < 0 || coeffs[c.coeff].y != 0.0) return nullptr;
+        FA.insert(c.factor);
+    }
+    for (auto& c : b) {
+        if (c.factor < 0 || coeffs[c.coeff].y != 0.0) return nullptr;
+        FB.insert(c.factor);
+    }
+    int loa = 0, hia = n_a, lob = 0, hib = n_b;
+    for (int f : FA) {
+        int lo, hi;
+        toeplitz_range(hrb, f, nmax, n_a, W, lo, hi);
+        loa = std::max(loa, lo);
+        hia = std::min(hia, hi);
+    }
+    for (int f : FB) {
+        int lo, hi;
+        toeplitz_range(hrb, f, nmax, n_b, W, lo, hi);
+        lob = std::max(lob, lo);
+        hib = std::min(hib, hi);
+    }
+    if (loa > 8 || n_a - hia > 8 || lob > 8 || n_b - hib > 8) return nullptr;
+    // shared memory: x rows [RBH][PX] (bw zeros | n_a | zeros, PX odd), mids [NMID][RBH][PM] (PM odd)
+    const int PX = ((n_a + RA - 1) / RA * RA + 2 * bw) | 1, PM = n_a | 1;
+    const size_t smem = ((size_t)RBH * PX + (size_t)nmid * RBH * PM) * sizeof(double2) + 64;
+    if (smem * minb > 226 * 1024 || smem > 226 * 1024) return nullptr;
+    const int T = 32 * NWARP;
+    const int ntb = (n_b + RB - 1) / RB;
+    const long long ntile = (long long)ntb * n_outer;
+    // block classes along axis a (phase A, blocks of RA entries) and axis b (phase B, blocks of RR rows)
+    const int nblkA = (n_a + RA - 1) / RA, ALO = (loa + RA - 1) / RA, AHI = hia / RA;
+    const int nblkB = (n_b + RR - 1) / RR, BLO = (lob + RR - 1) / RR, BHI = hib / RR;
+    if (AHI < ALO || BHI < BLO || ALO + (nblkA - AHI) > 24 || BLO + (nblkB - BHI) > 24) return nullptr;
+    auto band = [&](int f, int row, int k) -> double2 { return hrb[((size_t)f * nmax + row) * W + k]; };
+    ConstTable KT;
+    KT.inline_literals = true;
+    std::ostringstream s;
+    s << "// generated: tile variant of the fused level passes (ks_kron_jit.cu)\n"
+      << "#define BW " << bw << "\n#define W " << W << "\n#define NMID " << nmid << "\n#define NOUT " << nout << "\n#define RB " << RB
+      << "\n#define RBH " << RBH << "\n#define RA " << RA << "\n#define RR " << RR << "\n#define PX " << PX << "\n#define PM " << PM
+      << "\n#define T " << T << "\n#define NWARP " << NWARP << "\n#define MINB " << minb << "\n#define n_a " << n_a << "\n#define n_b " << n_b
+      << "\n#define n_outer " << n_outer << "LL\n#define NTB " << ntb << "\n#define NTILE " << ntile << "LL\n#define NBLKA " << nblkA << "\n"
+      << "struct Par { const double2* in; double2* out[NOUT]; const double2* rb; int nmax; };\n"
+      << R"(
+__device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mwait(unsigned long long* b, unsigned parity) {
+    unsigned ok = 0;
+    do {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                     " selp.u32 %0, 1, 0, p;\n}\n" : "=r"(ok) : "r"(su32(b)), "r"(parity) : "memory");
+    } while (!ok);
+}
+extern "C" __global__ void __launch_bounds__(T, MINB) ks_pairt(const __grid_constant__ Par P) {
+    extern __shared__ __align__(128) unsigned char smraw[];
+    double2* xs = reinterpret_cast<double2*>(smraw);   // [RBH][PX]: BW zeros | n_a entries | zeros
+    double2* ms = xs + (size_t)RBH * PX;                // [NMID][RBH][PM]
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(ms + (size_t)NMID * RBH * PM);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const double2 Z = make_double2(0.0, 0.0);
+    for (int e = tid; e < RBH * PX; e += T) xs[e] = Z;
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(full)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    // rows of tile `tile` (tile = tb + NTB * outer): global rows b0 - BW + r, r < RBH
+    auto load_tile = [&](long long tile) {
+        // warp 0: lane r copies row r (n_a * 16 B) when it lies inside the axis
+        const long long o = tile / NTB;
+        const int b0 = (int)(tile - o * NTB) * RB;
+        const int row = b0 - BW + lane;
+        const bool in = lane < RBH && row >= 0 && row < n_b;
+        const unsigned nrow = __popc(__ballot_sync(0xffffffffu, in));
+        if (lane == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(full)),
+                         "r"(nrow * (unsigned)(n_a * 16)) : "memory");
+        __syncwarp();
+        if (in)
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+                         "r"(su32(xs + (size_t)lane * PX + BW)), "l"(P.in + ((size_t)o * n_b + row) * n_a), "r"((unsigned)(n_a * 16)),
+                         "r"(su32(full)) : "memory");
+    };
+    long long tile = blockIdx.x;
+    if (tile < NTILE && warp == 0) load_tile(tile);
+    unsigned par = 0;
+    for (; tile < NTILE; tile += gridDim.x, par ^= 1) {
+        const long long o = tile / NTB;
+        const int b0 = (int)(tile - o * NTB) * RB;
+        mwait(full, par);
+        // ---- phase A: axis-a products of row `lane`, blocks of RA entries ----
+        {
+            const int row = b0 - BW + lane;
+            const bool rin = row >= 0 && row < n_b;
+            if (lane < RBH) {
+                const double2* xr = xs + (size_t)lane * PX; // xr[q] = x(q - BW)
+                for (int j = warp; j < NBLKA; j += NWARP) {
+                    const int t0 = j * RA;
+                    double2 acc[NMID][RA];
+#pragma unroll
+                    for (int h = 0; h < NMID; ++h)
+#pragma unroll
+                        for (int i = 0; i < RA; ++i) acc[h][i] = Z;
+                    if (rin) {
+                        double2 w[RA + 2 * BW];
+#pragma unroll
+                        for (int q = 0; q < RA + 2 * BW; ++q) w[q] = xr[t0 + q];
+)";
+    // literal product: acc[i] += cc * F[row_i][k] * w[i + k] for the rows of one block
+    auto emit_prod = [&](const std::string& ind, int f, double cc, const std::vector<int>& rows, int mid_row,
+                         const std::function<std::string(int)>& accn) {
+        for (size_t i = 0; i < rows.size(); ++i) {
+            if (rows[i] == -2) continue;
+            for (int k = 0; k < W; ++k) {
+                const double2 e = rows[i] == -1 ? band(f, mid_row, k) : band(f, rows[i], k);
+                const std::string acc = accn((int)i), wv = "w[" + lit((int)i + k) + "]";
+                if (cls(f) == 1) {
+                    if (e.x == 0.0) continue;
+                    const std::string v = KT.ref(cc * e.x);
+                    s << ind << acc << ".x = fma(" << v << ", " << wv << ".x, " << acc << ".x); " << acc << ".y = fma(" << v << ", " << wv
+                      << ".y, " << acc << ".y);\n";
+                } else if (cls(f) == 2) {
+                    if (e.y == 0.0) continue;
+                    const std::string v = KT.ref(cc * e.y);
+                    s << ind << acc << ".x = fma(-(" << v << "), " << wv << ".y, " << acc << ".x); " << acc << ".y = fma(" << v << ", " << wv
+                      << ".x, " << acc << ".y);\n";
+                } else {
+                    if (e.x == 0.0 && e.y == 0.0) continue;
+                    const std::string vx = KT.ref(cc * e.x), vy = KT.ref(cc * e.y);
+                    s << ind << acc << ".x = fma(" << vx << ", " << wv << ".x, fma(-(" << vy << "), " << wv << ".y, " << acc << ".x)); " << acc
+                      << ".y = fma(" << vx << ", " << wv << ".y, fma(" << vy << ", " << wv << ".x, " << acc << ".y));\n";
+                }
+            }
+        }
+    };
+    // phase A classes: 0 interior, then the boundary blocks
+    {
+        s << "                        int ca = 0;\n                        if (j < " << ALO << ") ca = 1 + j; else if (j >= " << AHI
+          << ") ca = " << (1 + ALO) << " + (j - " << AHI << ");\n                        switch (ca) {\n";
+        int ci = 0;
+        auto emit_case = [&](const std::vector<int>& rows) {
+            s << "                        case " << ci++ << ": {\n";
+            for (auto& c : a)
+                emit_prod("                            ", c.factor, coeffs[c.coeff].x, rows, (loa + hia) / 2,
+                          [&](int i) { return "acc[" + lit(c.out) + "][" + lit(i) + "]"; });
+            s << "                        } break;\n";
+        };
+        emit_case(std::vector<int>(RA, -1));
+        auto blockrows = [&](int j) {
+            std::vector<int> rows(RA);
+            for (int i = 0; i < RA; ++i) rows[i] = j * RA + i < n_a ? j * RA + i : -2;
+            return rows;
+        };
+        for (int j = 0; j < ALO; ++j) emit_case(blockrows(j));
+        for (int j = AHI; j < nblkA; ++j) emit_case(blockrows(j));
+        s << "                        default: break;\n                        }\n";
+    }
+    s << R"(                    }
+#pragma unroll
+                    for (int h = 0; h < NMID; ++h)
+#pragma unroll
+                        for (int i = 0; i < RA; ++i)
+                            if (t0 + i < n_a) ms[((size_t)h * RBH + lane) * PM + t0 + i] = acc[h][i];
+                }
+            }
+        }
+        __syncthreads();
+        // the x rows are consumed: the next tile's rows arrive while phase B runs
+        if (warp == 0 && tile + gridDim.x < NTILE) load_tile(tile + gridDim.x);
+        // ---- phase B: axis-b products, RR rows per thread, lanes across axis a ----
+        {
+            const int nbt = n_b - b0 < RB ? n_b - b0 : RB; // rows of this tile
+            const int nblk = (nbt + RR - 1) / RR;
+            for (int e = tid; e < nblk * n_a; e += T) {
+                const int blk = e / n_a, t = e - blk * n_a;
+                const int gb = b0 / RR + blk; // global row block (RB is a multiple of RR)
+                const double2* mr = ms + (size_t)(blk * RR) * PM + t; // mr[(h * RBH + q) * PM] = mid h at row b0 + blk RR - BW + q
+                double2 acc[NOUT][RR];
+#pragma unroll
+                for (int o2 = 0; o2 < NOUT; ++o2)
+#pragma unroll
+                    for (int i = 0; i < RR; ++i) acc[o2][i] = Z;
+                int cb = 0;
+)";
+    s << "                if (gb < " << BLO << ") cb = 1 + gb; else if (gb >= " << BHI << ") cb = " << (1 + BLO) << " + (gb - " << BHI
+      << ");\n                switch (cb) {\n";
+    {
+        int ci = 0;
+        auto emit_case = [&](const std::vector<int>& rows) {
+            s << "                case " << ci++ << ": {\n";
+            for (int h = 0; h < nmid; ++h) {
+                bool used = false;
+                for (auto& c : b) used = used || c.in == h;
+                if (!used) continue;
+                s << "                    {\n                        double2 w[RR + 2 * BW];\n#pragma unroll\n                        for (int q = 0; q < RR + 2 * BW; ++q) w[q] = mr[((size_t)"
+                  << h << " * RBH + q) * PM];\n";
+                for (auto& c : b)
+                    if (c.in == h)
+                        emit_prod("                        ", c.factor, coeffs[c.coeff].x, rows, (lob + hib) / 2,
+                                  [&](int i) { return "acc[" + lit(c.out) + "][" + lit(i) + "]"; });
+                s << "                    }\n";
+            }
+            s << "                } break;\n";
+        };
+        emit_case(std::vector<int>(RR, -1));
+        auto blockrows = [&](int g) {
+            std::vector<int> rows(RR);
+            for (int i = 0; i < RR; ++i) rows[i] = g * RR + i < n_b ? g * RR + i : -2;
+            return rows;
+        };
+        for (int g = 0; g < BLO; ++g) emit_case(blockrows(g));
+        for (int g = BHI; g < nblkB; ++g) emit_case(blockrows(g));
+        s << "                default: break;\n                }\n";
+    }
+    s << R"(                const size_t ob = ((size_t)o * n_b + b0 + blk * RR) * n_a + t;
+#pragma unroll
+                for (int i = 0; i < RR; ++i)
+                    if (blk * RR + i < nbt) {
+#pragma unroll
+                        for (int o2 = 0; o2 < NOUT; ++o2) __stcs(P.out[o2] + ob + (size_t)i * n_a, acc[o2][i]);
+                    }
+            }
+        }
+        __syncthreads();
+    }
+}
+)";
+    std::unique_ptr<KronJitPair> P(new KronJitPair());
+    P->k.fn = nvrtc_kernel(KT.finish(s.str()), "ks_pairt", 227 * 1024);
+    P->blocked = true;
+    P->tile = true;
+    P->nin = nin;
+    P->nmid = nmid;
+    P->nout = nout;
+    P->bw = bw;
+    P->pull = true;
+    P->T = T;
+    P->nq = RB; // (shape key)
+    P->no = RA * 100 + RR;
+    P->pad = minb;
+    P->D = 1;
+    P->smem = smem;
+    P->s_a = 1;
+    P->n_a = n_a;
+    P->n_b = n_b;
+    P->n_outer = n_outer;
+    P->grid = (unsigned)std::min<long long>(ntile, (long long)sm_count() * minb);
     P->coef = coeffs;
     P->ncoef = (int)coeffs.size();
     return P.release();

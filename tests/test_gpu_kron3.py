@@ -134,7 +134,7 @@ from oracle import oracle as O
 from helpers import setup_arrays, rel, maxrel
 O.build_oracle()
 worst = 0.0
-for p, n_el, n_el_t in [(2, 20, 17), (3, 14, 9), (4, 13, 11), (2, 33, 6)]:
+for p, n_el, n_el_t in [(2, 20, 17), (3, 14, 9), (4, 13, 11), (2, 33, 6), (4, 19, 18), (3, 30, 20)]:
     a = setup_arrays(ks, 3, p, n_el, n_el_t)
     A = ks.assemble_system_operator(a["prob"])
     K = O.OracleKron(a["dims"], O.system_terms(a, 3, a["nu"]))
@@ -146,9 +146,10 @@ print("worst", worst)
 """
 
 
-@pytest.mark.parametrize("variant", ["b2", "point"])
+@pytest.mark.parametrize("variant", ["b2", "point", "tile"])
 def test_generated_variants_forced(variant):
-    """The row-blocked (ks_pairb) and line (ks_pairl) generated kernels, forced on
+    """The row-blocked (ks_pairb), line (ks_pairl) and tile (ks_pairt: partial
+    last tiles, boundary blocks of both phases) generated kernels, forced on
     problems too small for them to be picked by the grid-size rule, against the
     oracle: interior (literal Toeplitz) rows, boundary row blocks, boundary
     planes, ragged column tiles and partial row tiles (KS_KRON_JIT is read once
@@ -161,6 +162,9 @@ def test_generated_variants_forced(variant):
     assert out.returncode == 0, out.stderr[-2000:]
     worst = float(out.stdout.strip().split()[-1])
     assert worst <= TOL, (worst, out.stderr[-1500:])
+    if variant == "tile":
+        kept = [l for l in out.stderr.splitlines() if "<- kept" in l]
+        assert any("rows/thread 10" in l for l in kept), out.stderr[-1500:]  # tile kernel ran (1000 + rows per tile)
     if variant == "b2":
         kept = [l for l in out.stderr.splitlines() if "<- kept" in l]
         assert any("rows/thread 2" in l for l in kept), out.stderr[-1500:]   # row-blocked kernel ran
