@@ -9,6 +9,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <array>
 #include <vector>
 
 #include "../../include/ks.h"
@@ -215,7 +216,10 @@ KronJitPair* kron_jitl_build(int nin, int nmid, int nout, int bw, const std::vec
 KronJitPair* kron_jitt_build(int nin, int nmid, int nout, int bw, const std::vector<JitContrib>& a,
                              const std::vector<JitContrib>& b, const std::vector<int>& freal,
                              const std::vector<double2>& coeffs, int n_a, int n_b, long long n_outer,
-                             const double2* hrb, int nmax, int RB, int RA, int RR, int NWARP, int minb);
+                             const double2* hrb, int nmax, int RB, int RA, int RR, int NWARP, int minb, int NAS);
+const char* kron_jit_tag(const KronJitPair& J);
+std::vector<std::array<int, 6>> kron_jitt_candidates(int bw, int n_a, int n_b, int na_prod, int nb_prod, int nmid, int nout,
+                                                     int keep);
 bool kron_jit_same_shape(const KronJitPair& A, const KronJitPair& B);
 int kron_jit_blocked_rows(const KronJitPair& J); // rows per thread of the row-blocked variant, -(lines per CTA) of the line variant, 0 for thread-per-point
 bool kron_jit_launch(const KronJitPair& J, const double2* const* ip, double2* const* op, void* const* hin,

@@ -624,11 +624,31 @@ KronPlan* kron_plan(const std::vector<int>& dims,
                 }
             if (P->jit[k] && sa == 1 && pa.n_in == 1)
                 // tile variant: {rows per tile, entries / rows per thread in phases A / B, warps, CTAs per SM}
-                for (auto cfg : {std::array<int, 5>{16, 4, 4, 8, 2}, std::array<int, 5>{16, 4, 4, 16, 1},
-                                 std::array<int, 5>{24, 4, 4, 16, 1}}) {
+                for (auto cfg : [&] {
+                         // KS_KRON_TILE="RB,RA,RR,warps,ctas,pieces;...": explicit tile shapes (sweeps)
+                         std::vector<std::array<int, 6>> v;
+                         if (const char* e = std::getenv("KS_KRON_TILE")) {
+                             std::array<int, 6> c{};
+                             int k = 0, cur = 0;
+                             for (const char* q = e;; ++q) {
+                                 if (*q >= '0' && *q <= '9') cur = cur * 10 + (*q - '0');
+                                 else {
+                                     if (k < 6) c[k++] = cur;
+                                     cur = 0;
+                                     if (*q == ';' || *q == 0) {
+                                         if (k == 6) v.push_back(c);
+                                         k = 0;
+                                     }
+                                     if (*q == 0) break;
+                                 }
+                             }
+                             return v;
+                         }
+                         return kron_jitt_candidates(P->bwmax, na, nbb, (int)ca.size(), (int)cb.size(), pa.n_out, pb.n_out, 4);
+                     }()) {
                     std::unique_ptr<KronJitPair, KronJitDeleter> alt(
                         kron_jitt_build(pa.n_in, pa.n_out, pb.n_out, P->bwmax, ca, cb, frv, co, na, nbb, outer, rb.data(), nmax,
-                                        cfg[0], cfg[1], cfg[2], cfg[3], cfg[4]));
+                                        cfg[0], cfg[1], cfg[2], cfg[3], cfg[4], cfg[5]));
                     if (alt) P->jit_alt[k].push_back(std::move(alt));
                 }
         }
@@ -798,8 +818,10 @@ void kron_apply(KronPlan& P, const double2* x, double2* y, cudaStream_t st,
                 }
                 if (const char* e = std::getenv("KS_KRON_JIT"); e && std::strcmp(e, "0") != 0) // any value but 0 logs the timings
                     for (size_t a = 0; a < tb.size(); ++a)
-                        std::fprintf(stderr, "ks_kron pass pair %zu candidate %zu (rows/thread %d): %.1f us%s\n", k, a,
-                                     kron_jit_blocked_rows(a == 0 ? *P.jit[k] : *P.jit_alt[k][a - 1]), 1e3f * tb[a],
+                        std::fprintf(stderr, "ks_kron pass pair %zu candidate %zu (rows/thread %d%s%s): %.1f us%s\n", k, a,
+                                     kron_jit_blocked_rows(a == 0 ? *P.jit[k] : *P.jit_alt[k][a - 1]),
+                                     *kron_jit_tag(a == 0 ? *P.jit[k] : *P.jit_alt[k][a - 1]) ? ", " : "",
+                                     kron_jit_tag(a == 0 ? *P.jit[k] : *P.jit_alt[k][a - 1]), 1e3f * tb[a],
                                      a == bi ? " <- kept" : "");
                 if (bi > 0) std::swap(P.jit[k], P.jit_alt[k][bi - 1]);
                 P.jit_alt[k].clear();

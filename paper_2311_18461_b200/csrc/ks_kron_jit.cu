@@ -29,6 +29,7 @@
 #include <nvrtc.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -130,7 +131,8 @@ struct KronJitPair {
     bool pull = true;
     bool blocked = false; // tensor-map fed variants (kron_jitb_build / kron_jitl_build)
     bool line = false;    // line variant (s_a = 1): boxes of whole lines
-    bool tile = false;    // tile variant (s_a = 1): two phases over shared memory, no tensor maps
+    bool tile = false;    // tile variant (s_a = 1): two phases over shared memory
+    std::string tag;      // shape, for the candidate log
     int T = 0, nq = 1, no = 1, D = 2, pad = 0; // block size, point block, ring depth, ring halo
     size_t smem = 0;                           // ring + staged axis-b bands
     long long s_a = 0, n_outer = 0;
@@ -530,6 +532,7 @@ bool kron_jit_runs(const KronJitPair& J) {
     }();
     return forced || J.grid >= (unsigned)sm_count();
 }
+const char* kron_jit_tag(const KronJitPair& J) { return J.tag.c_str(); }
 int kron_jit_blocked_rows(const KronJitPair& J) { return J.blocked ? (J.tile ? 1000 + J.nq : J.line ? -J.nq : J.nq) : 0; }
 bool kron_jit_same_shape(const KronJitPair& A, const KronJitPair& B) {
     return A.blocked == B.blocked && A.T == B.T && A.nq == B.nq && A.no == B.no && A.D == B.D;
@@ -575,22 +578,6 @@ static void encode_map3(void* out, const void* base, long long d0, long long d1,
 bool kron_jit_launch(const KronJitPair& J, const double2* const* ip, double2* const* op, void* const* hin,
                      void* const* hout, const double2* rb, int nmax, cudaStream_t st) {
     if (!kron_jit_runs(J)) return false;
-    if (J.tile) {
-        // by-value parameter: input, outputs, band table
-        // (the generated Par: in, out[NOUT], rb, nmax)
-        std::vector<unsigned char> raw(sizeof(void*) * (2 + (size_t)J.nout) + sizeof(int) + 8, 0);
-        unsigned char* w = raw.data();
-        std::memcpy(w, &hin[0], sizeof(void*));
-        w += sizeof(void*);
-        for (int o = 0; o < J.nout; ++o, w += sizeof(void*)) std::memcpy(w, &hout[o], sizeof(void*));
-        std::memcpy(w, &rb, sizeof(void*));
-        w += sizeof(void*);
-        std::memcpy(w, &nmax, sizeof(int));
-        void* args[] = {(void*)raw.data()};
-        KS_CUDA(cudaLaunchKernel((const void*)J.k.fn, dim3(J.grid), dim3(J.T), args, J.smem, st));
-        check_launch("ks_pairt (jit)");
-        return true;
-    }
     if (J.blocked) {
         // by-value parameter: input / output tensors, band table
         // (tensor maps first: 64-byte aligned, 128 B each)
@@ -599,7 +586,8 @@ bool kron_jit_launch(const KronJitPair& J, const double2* const* ip, double2* co
         unsigned char* w = raw.data() + (64 - reinterpret_cast<uintptr_t>(raw.data()) % 64) % 64;
         unsigned char* const w0 = w;
         for (int g = 0; g < J.nin; ++g, w += 128) {
-            if (J.line) encode_map3(w, hin[g], 2LL * J.n_a, J.n_b, J.n_outer, 2 * J.n_a, 1, J.no, J.n_a > 128); // lines of plane ib, C of them
+            if (J.tile) encode_map3(w, hin[g], 2LL * J.n_a, J.n_b, J.n_outer, 2 * J.D, J.nq + 2 * J.bw, 1); // PX entries x RBH rows
+            else if (J.line) encode_map3(w, hin[g], 2LL * J.n_a, J.n_b, J.n_outer, 2 * J.n_a, 1, J.no, J.n_a > 128); // lines of plane ib, C of them
             else encode_map3(w, hin[g], 2 * J.s_a, J.n_a, (long long)J.n_b * J.n_outer, 64, J.no + 2 * J.bw, 1);
         }
         for (int o = 0; o < J.nout; ++o, w += sizeof(void*)) std::memcpy(w, &hout[o], sizeof(void*));
@@ -608,7 +596,7 @@ bool kron_jit_launch(const KronJitPair& J, const double2* const* ip, double2* co
         std::memcpy(w, &nmax, sizeof(int));
         void* args[] = {(void*)w0};
         KS_CUDA(cudaLaunchKernel((const void*)J.k.fn, dim3(J.grid), dim3(J.T), args, J.smem, st));
-        check_launch(J.line ? "ks_pairl (jit)" : "ks_pairb (jit)");
+        check_launch(J.tile ? "ks_pairt (jit)" : J.line ? "ks_pairl (jit)" : "ks_pairb (jit)");
         return true;
     }
     // by-value coefficient table (constant bank)
@@ -1266,11 +1254,11 @@ extern "C" __global__ void __launch_bounds__(32 * (NW + 1), MINB) ks_pairl(const
 KronJitPair* kron_jitt_build(int nin, int nmid, int nout, int bw, const std::vector<JitContrib>& a,
                              const std::vector<JitContrib>& b, const std::vector<int>& freal,
                              const std::vector<double2>& coeffs, int n_a, int n_b, long long n_outer,
-                             const double2* hrb, int nmax, int RB, int RA, int RR, int NWARP, int minb) {
+                             const double2* hrb, int nmax, int RB, int RA, int RR, int NWARP, int minb, int NAS) {
     if (const char* e = std::getenv("KS_KRON_JIT"))
         if (std::strcmp(e, "0") == 0) return nullptr;
     if (nin != 1 || nmid < 1 || nmid > 4 || nout < 1 || nout > 4 || bw < 1 || bw > 4) return nullptr;
-    if (n_a < 4 * bw + 2 || n_b < 4 * bw + 2 || RA < 1 || RR < 1 || RB < RR || RB % RR != 0) return nullptr;
+    if (n_a < 4 * bw + 2 || n_b < 4 * bw + 2 || RA < 1 || RR < 1 || RB < RR || RB % RR != 0 || NAS < 1) return nullptr;
     const int W = 2 * bw + 1, RBH = RB + 2 * bw;
     if (RBH > 32) return nullptr; // phase A: one lane per row
     auto cls = [&](int f) { return freal[f]; };
@@ -1298,12 +1286,16 @@ KronJitPair* kron_jitt_build(int nin, int nmid, int nout, int bw, const std::vec
     }
     if (loa > 8 || n_a - hia > 8 || lob > 8 || n_b - hib > 8) return nullptr;
     // shared memory: x rows [RBH][PX] (bw zeros | n_a | zeros, PX odd), mids [NMID][RBH][PM] (PM odd)
-    const int PX = ((n_a + RA - 1) / RA * RA + 2 * bw) | 1, PM = n_a | 1;
+    // the axis-a range of a tile: NAS pieces of AT entries (a multiple of RA); the halo along a is only loaded
+    const int AT = ((n_a + NAS - 1) / NAS + RA - 1) / RA * RA;
+    if ((long long)AT * (NAS - 1) >= n_a || AT < 2 * bw) return nullptr;
+    const int PX = (AT + 2 * bw) | 1, PM = AT | 1; // (odd pitches: conflict-free with the lanes across the rows)
+    if (2 * PX > 256) return nullptr;              // one box: <= 256 doubles per dimension
     const size_t smem = ((size_t)RBH * PX + (size_t)nmid * RBH * PM) * sizeof(double2) + 64;
     if (smem * minb > 226 * 1024 || smem > 226 * 1024) return nullptr;
     const int T = 32 * NWARP;
     const int ntb = (n_b + RB - 1) / RB;
-    const long long ntile = (long long)ntb * n_outer;
+    const long long ntile = (long long)ntb * n_outer * NAS;
     // block classes along axis a (phase A, blocks of RA entries) and axis b (phase B, blocks of RR rows)
     const int nblkA = (n_a + RA - 1) / RA, ALO = (loa + RA - 1) / RA, AHI = hia / RA;
     const int nblkB = (n_b + RR - 1) / RR, BLO = (lob + RR - 1) / RR, BHI = hib / RR;
@@ -1316,8 +1308,10 @@ KronJitPair* kron_jitt_build(int nin, int nmid, int nout, int bw, const std::vec
       << "#define BW " << bw << "\n#define W " << W << "\n#define NMID " << nmid << "\n#define NOUT " << nout << "\n#define RB " << RB
       << "\n#define RBH " << RBH << "\n#define RA " << RA << "\n#define RR " << RR << "\n#define PX " << PX << "\n#define PM " << PM
       << "\n#define T " << T << "\n#define NWARP " << NWARP << "\n#define MINB " << minb << "\n#define n_a " << n_a << "\n#define n_b " << n_b
-      << "\n#define n_outer " << n_outer << "LL\n#define NTB " << ntb << "\n#define NTILE " << ntile << "LL\n#define NBLKA " << nblkA << "\n"
-      << "struct Par { const double2* in; double2* out[NOUT]; const double2* rb; int nmax; };\n"
+      << "\n#define n_outer " << n_outer << "LL\n#define NTB " << ntb << "\n#define NTILE " << ntile << "LL\n#define NAS " << NAS
+      << "\n#define AT " << AT << "\n"
+      << "struct __align__(64) TMap { unsigned long long d[16]; };\n"
+      << "struct Par { TMap tm; double2* out[NOUT]; const double2* rb; int nmax; };\n"
       << R"(
 __device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mwait(unsigned long long* b, unsigned parity) {
@@ -1329,49 +1323,45 @@ __device__ __forceinline__ void mwait(unsigned long long* b, unsigned parity) {
 }
 extern "C" __global__ void __launch_bounds__(T, MINB) ks_pairt(const __grid_constant__ Par P) {
     extern __shared__ __align__(128) unsigned char smraw[];
-    double2* xs = reinterpret_cast<double2*>(smraw);   // [RBH][PX]: BW zeros | n_a entries | zeros
+    double2* xs = reinterpret_cast<double2*>(smraw);   // [RBH][PX]: entries a0 - BW .. a0 + AT + BW of the row
     double2* ms = xs + (size_t)RBH * PX;                // [NMID][RBH][PM]
     unsigned long long* full = reinterpret_cast<unsigned long long*>(ms + (size_t)NMID * RBH * PM);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const double2 Z = make_double2(0.0, 0.0);
-    for (int e = tid; e < RBH * PX; e += T) xs[e] = Z;
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(full)) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    // rows of tile `tile` (tile = tb + NTB * outer): global rows b0 - BW + r, r < RBH
+    // tile = as + NAS * (tb + NTB * outer): axis-a range [a0, a0 + AT), global rows b0 - BW + r, r < RBH.
+    // One tensor-map box per tile: PX entries from a0 - BW of RBH rows from b0 - BW; entries and rows
+    // outside the tensor arrive as zeros. (One bulk copy per row costs ~60 cycles each in the copy
+    // engine: with the axis split in pieces the tiles became copy-issue bound, c3 325-442 us.)
     auto load_tile = [&](long long tile) {
-        // warp 0: lane r copies row r (n_a * 16 B) when it lies inside the axis
-        const long long o = tile / NTB;
-        const int b0 = (int)(tile - o * NTB) * RB;
-        const int row = b0 - BW + lane;
-        const bool in = lane < RBH && row >= 0 && row < n_b;
-        const unsigned nrow = __popc(__ballot_sync(0xffffffffu, in));
-        if (lane == 0)
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(full)),
-                         "r"(nrow * (unsigned)(n_a * 16)) : "memory");
-        __syncwarp();
-        if (in)
-            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-                         "r"(su32(xs + (size_t)lane * PX + BW)), "l"(P.in + ((size_t)o * n_b + row) * n_a), "r"((unsigned)(n_a * 16)),
-                         "r"(su32(full)) : "memory");
+        const int as = (int)(tile % NAS);
+        const long long rest = tile / NAS, o = rest / NTB;
+        const int b0 = (int)(rest - o * NTB) * RB, a0 = as * AT;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(full)), "r"((unsigned)(RBH * PX * 16)) : "memory");
+        asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+                     "r"(su32(xs)), "l"(&P.tm), "r"(2 * (a0 - BW)), "r"(b0 - BW), "r"((int)o), "r"(su32(full)) : "memory");
     };
     long long tile = blockIdx.x;
-    if (tile < NTILE && warp == 0) load_tile(tile);
+    if (tile < NTILE && tid == 0) load_tile(tile);
     unsigned par = 0;
     for (; tile < NTILE; tile += gridDim.x, par ^= 1) {
-        const long long o = tile / NTB;
-        const int b0 = (int)(tile - o * NTB) * RB;
+        const int as = (int)(tile % NAS);
+        const long long rest = tile / NAS, o = rest / NTB;
+        const int b0 = (int)(rest - o * NTB) * RB, a0 = as * AT;
+        const int nat = n_a - a0 < AT ? n_a - a0 : AT; // entries of this tile along a
         mwait(full, par);
         // ---- phase A: axis-a products of row `lane`, blocks of RA entries ----
         {
             const int row = b0 - BW + lane;
             const bool rin = row >= 0 && row < n_b;
             if (lane < RBH) {
-                const double2* xr = xs + (size_t)lane * PX; // xr[q] = x(q - BW)
-                for (int j = warp; j < NBLKA; j += NWARP) {
-                    const int t0 = j * RA;
+                const double2* xr = xs + (size_t)lane * PX; // xr[q] = x(a0 - BW + q)
+                for (int jl = warp; jl * RA < nat; jl += NWARP) {
+                    const int t0 = jl * RA, j = a0 / RA + jl; // local offset, global block
                     double2 acc[NMID][RA];
 #pragma unroll
                     for (int h = 0; h < NMID; ++h)
@@ -1436,19 +1426,19 @@ extern "C" __global__ void __launch_bounds__(T, MINB) ks_pairt(const __grid_cons
                     for (int h = 0; h < NMID; ++h)
 #pragma unroll
                         for (int i = 0; i < RA; ++i)
-                            if (t0 + i < n_a) ms[((size_t)h * RBH + lane) * PM + t0 + i] = acc[h][i];
+                            if (t0 + i < nat) ms[((size_t)h * RBH + lane) * PM + t0 + i] = acc[h][i];
                 }
             }
         }
         __syncthreads();
         // the x rows are consumed: the next tile's rows arrive while phase B runs
-        if (warp == 0 && tile + gridDim.x < NTILE) load_tile(tile + gridDim.x);
+        if (tid == 0 && tile + gridDim.x < NTILE) load_tile(tile + gridDim.x);
         // ---- phase B: axis-b products, RR rows per thread, lanes across axis a ----
         {
             const int nbt = n_b - b0 < RB ? n_b - b0 : RB; // rows of this tile
             const int nblk = (nbt + RR - 1) / RR;
-            for (int e = tid; e < nblk * n_a; e += T) {
-                const int blk = e / n_a, t = e - blk * n_a;
+            for (int e = tid; e < nblk * nat; e += T) {
+                const int blk = e / nat, t = e - blk * nat;
                 const int gb = b0 / RR + blk; // global row block (RB is a multiple of RR)
                 const double2* mr = ms + (size_t)(blk * RR) * PM + t; // mr[(h * RBH + q) * PM] = mid h at row b0 + blk RR - BW + q
                 double2 acc[NOUT][RR];
@@ -1488,7 +1478,7 @@ extern "C" __global__ void __launch_bounds__(T, MINB) ks_pairt(const __grid_cons
         for (int g = BHI; g < nblkB; ++g) emit_case(blockrows(g));
         s << "                default: break;\n                }\n";
     }
-    s << R"(                const size_t ob = ((size_t)o * n_b + b0 + blk * RR) * n_a + t;
+    s << R"(                const size_t ob = ((size_t)o * n_b + b0 + blk * RR) * n_a + a0 + t;
 #pragma unroll
                 for (int i = 0; i < RR; ++i)
                     if (blk * RR + i < nbt) {
@@ -1513,8 +1503,9 @@ extern "C" __global__ void __launch_bounds__(T, MINB) ks_pairt(const __grid_cons
     P->T = T;
     P->nq = RB; // (shape key)
     P->no = RA * 100 + RR;
-    P->pad = minb;
-    P->D = 1;
+    P->pad = minb * 10 + NAS;
+    P->tag = "tile RB " + lit(RB) + " RA " + lit(RA) + " RR " + lit(RR) + " warps " + lit(NWARP) + " ctas/sm " + lit(minb) + " pieces " + lit(NAS);
+    P->D = PX;
     P->smem = smem;
     P->s_a = 1;
     P->n_a = n_a;
@@ -1524,6 +1515,68 @@ extern "C" __global__ void __launch_bounds__(T, MINB) ks_pairt(const __grid_cons
     P->coef = coeffs;
     P->ncoef = (int)coeffs.size();
     return P.release();
+}
+
+// Tile-variant shapes worth timing for a pass pair, best first by a simple issue model:
+// per output point, phase A costs |a| products x the halo factor x the idle-lane factor of its
+// row-per-lane mapping, phase B |b| products, each divided by how evenly its work items fill
+// the warps between the two CTA barriers; shared-memory operations (4 LSU cycles per 16 B
+// warp access against 2 FP64-pipe cycles per DFMA) bound it from below. Constraints:
+// registers per thread within the allocation unit of four warps, shared memory for `minb`
+// CTAs, one tensor-map box per tile.
+std::vector<std::array<int, 6>> kron_jitt_candidates(int bw, int n_a, int n_b, int na_prod, int nb_prod, int nmid, int nout,
+                                                     int keep) {
+    struct Cand {
+        double score;
+        std::array<int, 6> c;
+    };
+    std::vector<Cand> all;
+    const int W = 2 * bw + 1;
+    for (int RR = 2; RR <= 4; ++RR)
+        for (int RB = RR; RB + 2 * bw <= 32; RB += RR)
+            for (int RA = 2; RA <= 6; ++RA)
+                for (int NAS = 1; NAS <= 4; ++NAS)
+                    for (int NW : {4, 8, 12, 16})
+                        for (int minb = 1; minb <= 4; ++minb) {
+                            if (NW * minb > 16 || NW * minb < 8) continue;
+                            const int RBH = RB + 2 * bw;
+                            const int AT = ((n_a + NAS - 1) / NAS + RA - 1) / RA * RA;
+                            if ((long long)AT * (NAS - 1) >= n_a || AT < 2 * bw) continue;
+                            const int PX = (AT + 2 * bw) | 1, PM = AT | 1;
+                            if (2 * PX > 256) continue;
+                            const size_t smem = ((size_t)RBH * PX + (size_t)nmid * RBH * PM) * 16 + 64;
+                            if (smem * minb > 226 * 1024) continue;
+                            const int regs = std::max(4 * (RA + 2 * bw) + 4 * nmid * RA, 4 * (RR + 2 * bw) + 4 * nout * RR) + 34;
+                            if (regs > std::min(255, 65536 / (minb * NW * 32))) continue;
+                            const int ntb = (n_b + RB - 1) / RB;
+                            const double eff_rows = (double)n_b / ((double)ntb * RB);
+                            double ea = 0, eb = 0; // fill of the warps in phases A / B, averaged over the pieces of axis a
+                            for (int as = 0; as < NAS; ++as) {
+                                const int nat = std::min(AT, n_a - as * AT);
+                                const int nblk = (nat + RA - 1) / RA, items = (RB / RR) * nat;
+                                ea += (double)nat / ((double)((nblk + NW - 1) / NW) * NW * RA);
+                                eb += (double)items / ((double)((items + 32 * NW - 1) / (32 * NW)) * 32 * NW);
+                            }
+                            ea /= NAS;
+                            eb /= NAS;
+                            const double h = (double)RBH / RB;
+                            const double fp = 4.0 * W * (na_prod * h * (32.0 / RBH) / ea + nb_prod / eb);
+                            const double sm = 4.0 * (((double)(RA + 2 * bw) / RA + nmid) * h * (32.0 / RBH) + (double)nmid * (RR + 2 * bw) / RR);
+                            // barriers are hidden better by more resident CTAs
+                            const double score = std::max(fp, sm) / eff_rows * (1.0 + 0.15 / minb);
+                            all.push_back({score, {RB, RA, RR, NW, minb, NAS}});
+                        }
+    std::sort(all.begin(), all.end(), [](const Cand& x, const Cand& y) { return x.score < y.score; });
+    std::vector<std::array<int, 6>> out;
+    for (auto& c : all) {
+        if ((int)out.size() >= keep) break;
+        out.push_back(c.c);
+    }
+    if (const char* e = std::getenv("KS_KRON_JIT"); e && std::strcmp(e, "0") != 0 && std::strncmp(e, "dump", 4) != 0)
+        for (size_t i = 0; i < out.size(); ++i)
+            std::fprintf(stderr, "ks_kron tile shape %zu: RB %d RA %d RR %d warps %d ctas/sm %d pieces %d (score %.1f)\n", i, out[i][0],
+                         out[i][1], out[i][2], out[i][3], out[i][4], out[i][5], all[i].score);
+    return out;
 }
 
 } // namespace ks
