@@ -644,7 +644,7 @@ KronPlan* kron_plan(const std::vector<int>& dims,
                              }
                              return v;
                          }
-                         return kron_jitt_candidates(P->bwmax, na, nbb, (int)ca.size(), (int)cb.size(), pa.n_out, pb.n_out, 4);
+                         return kron_jitt_candidates(P->bwmax, na, nbb, (int)ca.size(), (int)cb.size(), pa.n_out, pb.n_out, 3);
                      }()) {
                     std::unique_ptr<KronJitPair, KronJitDeleter> alt(
                         kron_jitt_build(pa.n_in, pa.n_out, pb.n_out, P->bwmax, ca, cb, frv, co, na, nbb, outer, rb.data(), nmax,

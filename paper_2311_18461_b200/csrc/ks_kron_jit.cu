@@ -1562,8 +1562,9 @@ std::vector<std::array<int, 6>> kron_jitt_candidates(int bw, int n_a, int n_b, i
                             const double h = (double)RBH / RB;
                             const double fp = 4.0 * W * (na_prod * h * (32.0 / RBH) / ea + nb_prod / eb);
                             const double sm = 4.0 * (((double)(RA + 2 * bw) / RA + nmid) * h * (32.0 / RBH) + (double)nmid * (RR + 2 * bw) / RR);
-                            // barriers are hidden better by more resident CTAs
-                            const double score = std::max(fp, sm) / eff_rows * (1.0 + 0.15 / minb);
+                            // measured at c3 / c5 (tools/gpu_tile_sweep.sh): two CTAs of eight warps beat four of
+                            // four and one of sixteen at equal shapes; every extra piece of axis a costs a few percent
+                            const double score = std::max(fp, sm) / eff_rows * (NW == 8 && minb == 2 ? 1.0 : 1.06) * (1.0 + 0.03 * (NAS - 1));
                             all.push_back({score, {RB, RA, RR, NW, minb, NAS}});
                         }
     std::sort(all.begin(), all.end(), [](const Cand& x, const Cand& y) { return x.score < y.score; });

@@ -2,7 +2,7 @@
 # full captures (source page) of the tile kernel at c5 (kept by timing) and c3 (forced)
 mkdir -p gpurun_out
 for cfg in c5 c3; do
-  if [ $cfg = c5 ]; then cmd="python tools/prof_c5mv.py"; export KS_KRON_JIT=log; else cmd="python tools/prof_c3.py c3"; export KS_KRON_JIT=tile; fi
+  if [ $cfg = c5 ]; then cmd="python tools/prof_c5mv.py"; export KS_KRON_JIT=log; export KS_KRON_TILE="22,3,2,8,2,3"; else export KS_KRON_TILE="22,3,2,8,2,1"; cmd="python tools/prof_c3.py c3"; export KS_KRON_JIT=tile; fi
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"ks_pair" --csv \
       --log-file gpurun_out/${cfg}t_launches.csv $cmd > /dev/null 2>&1
   n=$(grep -c "ks_pairt" gpurun_out/${cfg}t_launches.csv)
