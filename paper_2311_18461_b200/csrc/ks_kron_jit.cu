@@ -772,7 +772,7 @@ KronJitPair* kron_jitb_build(int nin, int nmid, int nout, int bw, const std::vec
     for (auto& c : b)
         if (cval(c.coeff).y != 0.0) return nullptr;
     ConstTable KT;
-    KT.inline_literals = true;
+    KT.inline_literals = true; // (the constant table measured slower in all three tensor-map fed kernels but the line one)
     std::ostringstream s;
     s << "// generated: row-blocked fused level passes (ks_kron_jit.cu)\n"
       << "#define BW " << bw << "\n#define W " << W << "\n#define NIN " << nin << "\n#define NMID " << nmid << "\n#define NOUT "
@@ -1302,7 +1302,7 @@ KronJitPair* kron_jitt_build(int nin, int nmid, int nout, int bw, const std::vec
     if (AHI < ALO || BHI < BLO || ALO + (nblkA - AHI) > 24 || BLO + (nblkB - BHI) > 24) return nullptr;
     auto band = [&](int f, int row, int k) -> double2 { return hrb[((size_t)f * nmax + row) * W + k]; };
     ConstTable KT;
-    KT.inline_literals = true;
+    KT.inline_literals = true; // (the constant table measured slower in all three tensor-map fed kernels but the line one)
     std::ostringstream s;
     s << "// generated: tile variant of the fused level passes (ks_kron_jit.cu)\n"
       << "#define BW " << bw << "\n#define W " << W << "\n#define NMID " << nmid << "\n#define NOUT " << nout << "\n#define RB " << RB
@@ -1372,7 +1372,10 @@ extern "C" __global__ void __launch_bounds__(T, MINB) ks_pairt(const __grid_cons
 #pragma unroll
                         for (int q = 0; q < RA + 2 * BW; ++q) w[q] = xr[t0 + q];
 )";
-    // literal product: acc[i] += cc * F[row_i][k] * w[i + k] for the rows of one block
+    // literal product: acc[i] += cc * F[row_i][k] * w[i + k] for the rows of one block. The statements of
+    // a case are collected and written tap by tap (k outermost), so consecutive DFMAs belong to different
+    // accumulators: a dependent pair sits as many instructions apart as the case has chains.
+    std::vector<std::pair<int, std::string>> pend;
     auto emit_prod = [&](const std::string& ind, int f, double cc, const std::vector<int>& rows, int mid_row,
                          const std::function<std::string(int)>& accn) {
         for (size_t i = 0; i < rows.size(); ++i) {
@@ -1380,24 +1383,31 @@ extern "C" __global__ void __launch_bounds__(T, MINB) ks_pairt(const __grid_cons
             for (int k = 0; k < W; ++k) {
                 const double2 e = rows[i] == -1 ? band(f, mid_row, k) : band(f, rows[i], k);
                 const std::string acc = accn((int)i), wv = "w[" + lit((int)i + k) + "]";
+                std::ostringstream t;
                 if (cls(f) == 1) {
                     if (e.x == 0.0) continue;
                     const std::string v = KT.ref(cc * e.x);
-                    s << ind << acc << ".x = fma(" << v << ", " << wv << ".x, " << acc << ".x); " << acc << ".y = fma(" << v << ", " << wv
+                    t << ind << acc << ".x = fma(" << v << ", " << wv << ".x, " << acc << ".x); " << acc << ".y = fma(" << v << ", " << wv
                       << ".y, " << acc << ".y);\n";
                 } else if (cls(f) == 2) {
                     if (e.y == 0.0) continue;
                     const std::string v = KT.ref(cc * e.y);
-                    s << ind << acc << ".x = fma(-(" << v << "), " << wv << ".y, " << acc << ".x); " << acc << ".y = fma(" << v << ", " << wv
+                    t << ind << acc << ".x = fma(-(" << v << "), " << wv << ".y, " << acc << ".x); " << acc << ".y = fma(" << v << ", " << wv
                       << ".x, " << acc << ".y);\n";
                 } else {
                     if (e.x == 0.0 && e.y == 0.0) continue;
                     const std::string vx = KT.ref(cc * e.x), vy = KT.ref(cc * e.y);
-                    s << ind << acc << ".x = fma(" << vx << ", " << wv << ".x, fma(-(" << vy << "), " << wv << ".y, " << acc << ".x)); " << acc
+                    t << ind << acc << ".x = fma(" << vx << ", " << wv << ".x, fma(-(" << vy << "), " << wv << ".y, " << acc << ".x)); " << acc
                       << ".y = fma(" << vx << ", " << wv << ".y, fma(" << vy << ", " << wv << ".x, " << acc << ".y));\n";
                 }
+                pend.push_back({k, t.str()});
             }
         }
+    };
+    auto flush = [&] {
+        std::stable_sort(pend.begin(), pend.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+        for (auto& q : pend) s << q.second;
+        pend.clear();
     };
     // phase A classes: 0 interior, then the boundary blocks
     {
@@ -1409,6 +1419,7 @@ extern "C" __global__ void __launch_bounds__(T, MINB) ks_pairt(const __grid_cons
             for (auto& c : a)
                 emit_prod("                            ", c.factor, coeffs[c.coeff].x, rows, (loa + hia) / 2,
                           [&](int i) { return "acc[" + lit(c.out) + "][" + lit(i) + "]"; });
+            flush();
             s << "                        } break;\n";
         };
         emit_case(std::vector<int>(RA, -1));
@@ -1464,6 +1475,7 @@ extern "C" __global__ void __launch_bounds__(T, MINB) ks_pairt(const __grid_cons
                     if (c.in == h)
                         emit_prod("                        ", c.factor, coeffs[c.coeff].x, rows, (lob + hib) / 2,
                                   [&](int i) { return "acc[" + lit(c.out) + "][" + lit(i) + "]"; });
+                flush();
                 s << "                    }\n";
             }
             s << "                } break;\n";
