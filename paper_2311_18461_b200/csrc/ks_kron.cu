@@ -591,7 +591,10 @@ KronPlan* kron_plan(const std::vector<int>& dims,
             const long long outer = (long long)(P->N / (sa * (size_t)na * (size_t)nbb));
             P->jit[k].reset(kron_jit_build(pa.n_in, pa.n_out, pb.n_out, P->bwmax, ca, cb, frv, co, (long long)sa, na,
                                            nbb, outer));
-            if (P->jit[k])
+            // (alternative block shapes of the thread-per-point kernel only where neither tensor-map fed
+            // variant applies: they never won against those, and every candidate costs an NVRTC compile)
+            const bool fed = (sa >= 32 || (sa == 1 && pa.n_in == 1)) && P->bwmax <= 4;
+            if (P->jit[k] && !fed)
                 for (int tm : {192, 128}) {
                     std::unique_ptr<KronJitPair, KronJitDeleter> alt(kron_jit_build(
                         pa.n_in, pa.n_out, pb.n_out, P->bwmax, ca, cb, frv, co, (long long)sa, na, nbb, outer, tm));
@@ -612,15 +615,6 @@ KronPlan* kron_plan(const std::vector<int>& dims,
                         pa.n_in, pa.n_out, pb.n_out, P->bwmax, ca, cb, frv, co, (long long)sa, na, nbb, outer, rb.data(),
                         nmax, rr, true));
                     if (al4) P->jit_alt[k].push_back(std::move(al4));
-                }
-            if (P->jit[k] && sa == 1)
-                // (5 lines, 16 stages, one CTA per SM; fewer lines with 2-3 CTAs per SM spill: 510-540 us vs 249 us at c3)
-                // longer lines (c5: 131 entries): the most lines that fit 15 consumer warps
-                for (auto cfg : {std::array<int, 3>{std::max(1, std::min(5, 480 / na)), 16, 1}}) {
-                    std::unique_ptr<KronJitPair, KronJitDeleter> alt(
-                        kron_jitl_build(pa.n_in, pa.n_out, pb.n_out, P->bwmax, ca, cb, frv, co, na, nbb, outer, rb.data(), nmax,
-                                        cfg[0], cfg[1], cfg[2]));
-                    if (alt) P->jit_alt[k].push_back(std::move(alt));
                 }
             if (P->jit[k] && sa == 1 && pa.n_in == 1)
                 // tile variant: {rows per tile, entries / rows per thread in phases A / B, warps, CTAs per SM}
@@ -644,7 +638,7 @@ KronPlan* kron_plan(const std::vector<int>& dims,
                              }
                              return v;
                          }
-                         return kron_jitt_candidates(P->bwmax, na, nbb, (int)ca.size(), (int)cb.size(), pa.n_out, pb.n_out, 3);
+                         return kron_jitt_candidates(P->bwmax, na, nbb, (int)ca.size(), (int)cb.size(), pa.n_out, pb.n_out, 2);
                      }()) {
                     std::unique_ptr<KronJitPair, KronJitDeleter> alt(
                         kron_jitt_build(pa.n_in, pa.n_out, pb.n_out, P->bwmax, ca, cb, frv, co, na, nbb, outer, rb.data(), nmax,
@@ -799,17 +793,14 @@ void kron_apply(KronPlan& P, const double2* x, double2* y, cudaStream_t st,
                     if (tb[a] < tb[bi]) bi = a;
                 // KS_KRON_JIT=b2 / b4 / point forces a candidate (tests, profiling)
                 if (const char* e = std::getenv("KS_KRON_JIT")) {
-                    // (b2 / b4: rows per thread of the row-blocked kernel; the line kernel's
-                    // candidates report their lines per CTA and are picked by timing among them)
+                    // (b2 / b4: rows per thread of the row-blocked kernel; tile: the tile kernel too)
                     const bool wtile = !std::strcmp(e, "tile");
                     const int want = !std::strcmp(e, "b2") || wtile ? 2 : !std::strcmp(e, "b4") ? 4 : !std::strcmp(e, "point") ? 0 : -1;
                     if (want >= 0) {
                         std::vector<KronJitPair*> all{P.jit[k].get()};
                         for (auto& alt : P.jit_alt[k]) all.push_back(alt.get());
                         for (size_t a = 0; a < all.size(); ++a)
-                            if ((kron_jit_blocked_rows(*all[a]) == want ||
-                                 (want > 0 && !wtile && kron_jit_blocked_rows(*all[a]) < 0) ||
-                                 (wtile && kron_jit_blocked_rows(*all[a]) >= 1000)) &&
+                            if ((kron_jit_blocked_rows(*all[a]) == want || (wtile && kron_jit_blocked_rows(*all[a]) >= 1000)) &&
                                 tb[a] < 1e29f) {
                                 bi = a;
                                 break;

@@ -129,8 +129,7 @@ struct KronJitPair {
     JitKernel k;
     int nin = 0, nmid = 0, nout = 0, bw = 0, ncoef = 0;
     bool pull = true;
-    bool blocked = false; // tensor-map fed variants (kron_jitb_build / kron_jitl_build)
-    bool line = false;    // line variant (s_a = 1): boxes of whole lines
+    bool blocked = false; // tensor-map fed variants (kron_jitb_build / kron_jitt_build)
     bool tile = false;    // tile variant (s_a = 1): two phases over shared memory
     std::string tag;      // shape, for the candidate log
     int T = 0, nq = 1, no = 1, D = 2, pad = 0; // block size, point block, ring depth, ring halo
@@ -533,18 +532,17 @@ bool kron_jit_runs(const KronJitPair& J) {
     return forced || J.grid >= (unsigned)sm_count();
 }
 const char* kron_jit_tag(const KronJitPair& J) { return J.tag.c_str(); }
-int kron_jit_blocked_rows(const KronJitPair& J) { return J.blocked ? (J.tile ? 1000 + J.nq : J.line ? -J.nq : J.nq) : 0; }
+int kron_jit_blocked_rows(const KronJitPair& J) { return J.blocked ? (J.tile ? 1000 + J.nq : J.nq) : 0; }
 bool kron_jit_same_shape(const KronJitPair& A, const KronJitPair& B) {
     return A.blocked == B.blocked && A.T == B.T && A.nq == B.nq && A.no == B.no && A.D == B.D;
 }
 
 // Tensor maps of the level tensors seen as doubles. Row-blocked kernel:
 // (2 s_a, n_a, planes), box = 64 doubles x (RT + 2 bw) rows x 1 plane (halo rows
-// included, zero filled outside). Line kernel: (2 n_a, n_b, lines), box = one
-// line x 1 plane x C lines. cuTensorMapEncodeTiled comes through the runtime's
+// included, zero filled outside). Tile kernel: (2 n_a, n_b, outer), box = PX
+// entries x (RB + 2 bw) rows x 1. cuTensorMapEncodeTiled comes through the runtime's
 // driver entry point, so libks keeps linking only cudart.
-static void encode_map3(void* out, const void* base, long long d0, long long d1, long long d2, int b0, int b1, int b2,
-                        bool split = false) {
+static void encode_map3(void* out, const void* base, long long d0, long long d1, long long d2, int b0, int b1, int b2) {
     using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
                             const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -556,17 +554,12 @@ static void encode_map3(void* out, const void* base, long long d0, long long d1,
         KS_REQUIRE(p && q == cudaDriverEntryPointSuccess, KS_ECUDA, "cuTensorMapEncodeTiled not available");
         fn = reinterpret_cast<Fn>(p);
     }
-    // a dense tensor of doubles (d0 fastest), box b0 x b1 x b2, no swizzle, zero fill outside;
-    // split: d0 (> 256 doubles, the box limit) as (2, d0 / 2), rank 4
-    const cuuint64_t gdim[4] = {split ? 2u : (cuuint64_t)d0, split ? (cuuint64_t)(d0 / 2) : (cuuint64_t)d1,
-                                split ? (cuuint64_t)d1 : (cuuint64_t)d2, (cuuint64_t)d2};
-    const cuuint64_t gstr[3] = {split ? 16u : (cuuint64_t)(d0 * 8), split ? (cuuint64_t)(d0 * 8) : (cuuint64_t)(d0 * 8 * d1),
-                                (cuuint64_t)(d0 * 8 * d1)};
-    const cuuint32_t box[4] = {split ? 2u : (cuuint32_t)b0, split ? (cuuint32_t)(b0 / 2) : (cuuint32_t)b1,
-                               split ? (cuuint32_t)b1 : (cuuint32_t)b2, (cuuint32_t)b2},
-                     est[4] = {1u, 1u, 1u, 1u};
+    // a dense tensor of doubles (d0 fastest), box b0 x b1 x b2, no swizzle, zero fill outside
+    const cuuint64_t gdim[3] = {(cuuint64_t)d0, (cuuint64_t)d1, (cuuint64_t)d2};
+    const cuuint64_t gstr[2] = {(cuuint64_t)(d0 * 8), (cuuint64_t)(d0 * 8 * d1)};
+    const cuuint32_t box[3] = {(cuuint32_t)b0, (cuuint32_t)b1, (cuuint32_t)b2}, est[3] = {1u, 1u, 1u};
     CUtensorMap m;
-    const CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, split ? 4 : 3, const_cast<void*>(base), gdim, gstr, box, est,
+    const CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), gdim, gstr, box, est,
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     KS_REQUIRE(r == CUDA_SUCCESS, KS_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
@@ -587,7 +580,6 @@ bool kron_jit_launch(const KronJitPair& J, const double2* const* ip, double2* co
         unsigned char* const w0 = w;
         for (int g = 0; g < J.nin; ++g, w += 128) {
             if (J.tile) encode_map3(w, hin[g], 2LL * J.n_a, J.n_b, J.n_outer, 2 * J.D, J.nq + 2 * J.bw, 1); // PX entries x RBH rows
-            else if (J.line) encode_map3(w, hin[g], 2LL * J.n_a, J.n_b, J.n_outer, 2 * J.n_a, 1, J.no, J.n_a > 128); // lines of plane ib, C of them
             else encode_map3(w, hin[g], 2 * J.s_a, J.n_a, (long long)J.n_b * J.n_outer, 64, J.no + 2 * J.bw, 1);
         }
         for (int o = 0; o < J.nout; ++o, w += sizeof(void*)) std::memcpy(w, &hout[o], sizeof(void*));
@@ -596,7 +588,7 @@ bool kron_jit_launch(const KronJitPair& J, const double2* const* ip, double2* co
         std::memcpy(w, &nmax, sizeof(int));
         void* args[] = {(void*)w0};
         KS_CUDA(cudaLaunchKernel((const void*)J.k.fn, dim3(J.grid), dim3(J.T), args, J.smem, st));
-        check_launch(J.tile ? "ks_pairt (jit)" : J.line ? "ks_pairl (jit)" : "ks_pairb (jit)");
+        check_launch(J.tile ? "ks_pairt (jit)" : "ks_pairb (jit)");
         return true;
     }
     // by-value coefficient table (constant bank)
@@ -649,33 +641,13 @@ std::string hexd(double v) {
     return std::string(b);
 }
 
-// Literal coefficients of a generated kernel: entries of one __constant__ table
-// referenced with constant indices, so they become constant-bank operands of
-// the DFMAs (inline literals are materialised with two UMOVs each -- about one
-// extra instruction per DFMA in the sweep stage; line kernel 249 -> 240 us).
+// Literal coefficients of a generated kernel: hexadecimal floating-point literals in the
+// source (materialised with two UMOVs each in SASS). Entries of a __constant__ table
+// (constant-bank DFMA operands instead) measured slower in the row-blocked and tile
+// kernels: c3 tile 219 -> 223 us, row-blocked 188 -> 200 us; c5 5.45 -> 6.1 ms, 6.06 -> 6.58 ms.
 struct ConstTable {
-    std::vector<double> v;
-    bool inline_literals = false; // the row-blocked kernel is faster with inline literals (187 vs 225 us at c3)
-    std::string ref(double x) {
-        if (inline_literals) return hexd(x);
-        size_t i = 0;
-        for (; i < v.size(); ++i)
-            if (std::memcmp(&v[i], &x, sizeof x) == 0) break;
-        if (i == v.size()) v.push_back(x);
-        return "KC[" + std::to_string(i) + "]";
-    }
-    std::string decl() const {
-        std::string t = "__constant__ double KC[" + std::to_string(std::max<size_t>(1, v.size())) + "] = {";
-        for (size_t i = 0; i < v.size(); ++i) t += (i ? ", " : "") + hexd(v[i]);
-        if (v.empty()) t += "0.0";
-        return t + "};\n";
-    }
-    // insert the table after the parameter struct of the generated source
-    std::string finish(const std::string& src) const {
-        const std::string mark = "int nmax; };\n";
-        const size_t at = src.find(mark);
-        return src.substr(0, at + mark.size()) + decl() + src.substr(at + mark.size());
-    }
+    std::string ref(double x) const { return hexd(x); }
+    const std::string& finish(const std::string& src) const { return src; }
 };
 
 // rows [lo, hi) of factor f equal to the middle row (relative 1e-13)
@@ -772,7 +744,6 @@ KronJitPair* kron_jitb_build(int nin, int nmid, int nout, int bw, const std::vec
     for (auto& c : b)
         if (cval(c.coeff).y != 0.0) return nullptr;
     ConstTable KT;
-    KT.inline_literals = true; // (the constant table measured slower in all three tensor-map fed kernels but the line one)
     std::ostringstream s;
     s << "// generated: row-blocked fused level passes (ks_kron_jit.cu)\n"
       << "#define BW " << bw << "\n#define W " << W << "\n#define NIN " << nin << "\n#define NMID " << nmid << "\n#define NOUT "
@@ -1004,233 +975,6 @@ extern "C" __global__ void __launch_bounds__(32 * (NW + 1), 1) ks_pairb(const __
 
 
 // ---------------------------------------------------------------------------
-// Line variant for a contiguous in-plane axis (s_a = 1; at d = 3 the (t, 1)
-// pair): thread per point of C whole lines, taps along the line from the
-// neighbours' shared-memory entries, push sweep along axis b -- the structure
-// of the thread-per-point kernel, but the planes arrive as tensor-map TMA boxes
-// (the C lines of plane ib: one request) on full / empty mbarriers, so the
-// warps never meet at a CTA barrier; the in-plane rows (which differ per
-// lane) sit in registers pre-multiplied by their contribution coefficient;
-// the sweep-axis band entries are literals on the interior planes.
-// ---------------------------------------------------------------------------
-KronJitPair* kron_jitl_build(int nin, int nmid, int nout, int bw, const std::vector<JitContrib>& a,
-                             const std::vector<JitContrib>& b, const std::vector<int>& freal,
-                             const std::vector<double2>& coeffs, int n_a, int n_b, long long n_outer,
-                             const double2* hrb, int nmax, int C, int smax, int minb) {
-    if (const char* e = std::getenv("KS_KRON_JIT"))
-        if (std::strcmp(e, "0") == 0) return nullptr;
-    if (nin < 1 || nmid < 1 || nout < 1 || nin > 2 || nmid > 6 || nout > 4 || bw < 1 || bw > 4) return nullptr;
-    if (n_a > 256 || n_a < 2 * bw + 1 || n_b < 4 * bw + 2 || C < 1 || n_outer < C) return nullptr;
-    const bool split = n_a > 128; // a box holds <= 256 doubles per dimension: lines as (2, n_a) then
-    const int W = 2 * bw + 1;
-    auto cls = [&](int f) { return freal[f]; };
-    std::set<int> FB;
-    for (auto& c : a)
-        if (c.factor < 0 || coeffs[c.coeff].y != 0.0) return nullptr;
-    for (auto& c : b) {
-        if (c.factor < 0 || coeffs[c.coeff].y != 0.0) return nullptr;
-        FB.insert(c.factor);
-    }
-    int lob = 0, hib = n_b;
-    for (int f : FB) {
-        int lo, hi;
-        toeplitz_range(hrb, f, nmax, n_b, W, lo, hi);
-        lob = std::max(lob, lo);
-        hib = std::min(hib, hi);
-    }
-    if (lob > 8 || n_b - hib > 8) return nullptr;
-    const int NP = C * n_a;               // points per plane and CTA
-    const int NW = (NP + 31) / 32;        // consumer warps
-    if (NW > 15) return nullptr;
-    const int PADF = 8;                   // zero entries in front of a stage (128 B: the box stays aligned)
-    const int SP = ((PADF + NP + bw + 7) / 8) * 8; // stage pitch per input (complex), 128 B multiple
-    const size_t stage = (size_t)nin * SP * sizeof(double2);
-    const int S = (int)std::min<size_t>((size_t)smax, (size_t)(200 * 1024 / minb) / stage);
-    if (S < 2) return nullptr;
-    const long long ntile = (n_outer + C - 1) / C;
-    auto band = [&](int f, int row, int k) -> double2 { return hrb[((size_t)f * nmax + row) * W + k]; };
-    ConstTable KT;
-    std::ostringstream s;
-    s << "// generated: line variant of the fused level passes (ks_kron_jit.cu)\n"
-      << "#define BW " << bw << "\n#define W " << W << "\n#define NIN " << nin << "\n#define NMID " << nmid << "\n#define NOUT "
-      << nout << "\n#define C " << C << "\n#define NP " << NP << "\n#define NW " << NW << "\n#define S " << S << "\n#define SP " << SP
-      << "\n#define SPLIT " << (split ? 1 : 0) << "\n#define MINB " << minb << "\n#define PADF " << PADF << "\n#define n_a " << n_a << "\n#define n_b " << n_b << "\n#define n_outer " << n_outer << "LL\n"
-      << "struct __align__(64) TMap { unsigned long long d[16]; };\n"
-      << "struct Par { TMap tm[NIN]; double2* out[NOUT]; const double2* rb; int nmax; };\n"
-      << R"(
-__device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mwait(unsigned long long* b, unsigned parity) {
-    unsigned ok = 0;
-    do {
-        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-                     " selp.u32 %0, 1, 0, p;\n}\n" : "=r"(ok) : "r"(su32(b)), "r"(parity) : "memory");
-    } while (!ok);
-}
-extern "C" __global__ void __launch_bounds__(32 * (NW + 1), MINB) ks_pairl(const __grid_constant__ Par P) {
-    extern __shared__ __align__(128) unsigned char smraw[];
-    double2* ring = reinterpret_cast<double2*>(smraw); // [S][NIN][SP]: PADF zeros | C lines | zeros
-    unsigned long long* full = reinterpret_cast<unsigned long long*>(ring + (size_t)S * NIN * SP);
-    unsigned long long* empty = full + S;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const long long o0 = (long long)blockIdx.x * C;
-    const double2 Z = make_double2(0.0, 0.0);
-    for (int e = tid; e < S * NIN * SP; e += 32 * (NW + 1)) ring[e] = Z;
-    if (tid == 0) {
-        for (int q = 0; q < S; ++q) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(full + q)) : "memory");
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(empty + q)), "n"(NW) : "memory");
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (warp == NW) {
-        // ---- producer: per input one box (the C lines of plane ib; lines past n_outer arrive as zeros) ----
-        if (lane != 0) return;
-        for (int ib = 0; ib < n_b; ++ib) {
-            const int slot = ib % S;
-            if (ib >= S) mwait(empty + slot, (unsigned)((ib / S - 1) & 1));
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(full + slot)),
-                         "r"((unsigned)(NIN * NP * 16)) : "memory");
-#pragma unroll
-            for (int g = 0; g < NIN; ++g)
-#if SPLIT
-                asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::
-                             "r"(su32(ring + (size_t)(slot * NIN + g) * SP + PADF)), "l"(&P.tm[g]), "r"(0), "r"(0), "r"(ib), "r"((int)o0),
-                             "r"(su32(full + slot))
-                             : "memory");
-#else
-                asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
-                             "r"(su32(ring + (size_t)(slot * NIN + g) * SP + PADF)), "l"(&P.tm[g]), "r"(0), "r"(ib), "r"((int)o0),
-                             "r"(su32(full + slot))
-                             : "memory");
-#endif
-        }
-        return;
-    }
-    // ---- consumer threads: point ia of line col ----
-    const int tix = tid < NP ? tid : 0; // (threads past the last point compute on point 0 and store nothing)
-    const int col = tix / n_a, ia = tix - col * n_a;
-    const bool valid = tid < NP && o0 + col < n_outer;
-    const long long obase = (o0 + col) * (long long)n_b * n_a + ia;
-)";
-    // in-plane rows in registers, pre-multiplied by the contribution coefficient
-    for (size_t ci = 0; ci < a.size(); ++ci) {
-        const int f = a[ci].factor;
-        const std::string cc = KT.ref(coeffs[a[ci].coeff].x);
-        if (cls(f) == 0) {
-            s << "    double2 A" << ci << "[W];\n#pragma unroll\n    for (int k = 0; k < W; ++k) { const double2 t_ = valid ? __ldg(P.rb + ((size_t)"
-              << f << " * P.nmax + ia) * W + k) : Z; A" << ci << "[k] = make_double2(" << cc << " * t_.x, " << cc << " * t_.y); }\n";
-        } else {
-            s << "    double A" << ci << "[W];\n#pragma unroll\n    for (int k = 0; k < W; ++k) { const double2 t_ = valid ? __ldg(P.rb + ((size_t)"
-              << f << " * P.nmax + ia) * W + k) : Z; A" << ci << "[k] = " << cc << " * t_" << (cls(f) == 1 ? ".x" : ".y") << "; }\n";
-        }
-    }
-    s << "    double2 win[NOUT][W];\n#pragma unroll\n    for (int o = 0; o < NOUT; ++o)\n#pragma unroll\n        for (int j = 0; j < W; ++j) win[o][j] = Z;\n"
-      << "    int ph = 0;\n    for (int ib = 0; ib < n_b + BW; ++ib) {\n        double2 m[NMID];\n#pragma unroll\n        for (int h = 0; h < NMID; ++h) m[h] = Z;\n"
-      << "        if (ib < n_b) {\n            const int slot = ib % S;\n            mwait(full + slot, (unsigned)((ib / S) & 1));\n"
-      << "            const double2* sl = ring + (size_t)slot * NIN * SP + PADF + tix - BW;\n";
-    for (int g = 0; g < nin; ++g) {
-        bool used = false;
-        for (auto& c : a) used = used || c.in == g;
-        if (!used) continue;
-        s << "            {\n                double2 w[W];\n#pragma unroll\n                for (int k = 0; k < W; ++k) w[k] = sl[" << g << " * SP + k];\n"
-          << "#pragma unroll\n                for (int k = 0; k < W; ++k) {\n";
-        for (size_t ci = 0; ci < a.size(); ++ci) {
-            if (a[ci].in != g) continue;
-            const int f = a[ci].factor;
-            const std::string acc = "m[" + lit(a[ci].out) + "]", A = "A" + lit((int)ci) + "[k]";
-            if (cls(f) == 1)
-                s << "                    " << acc << ".x = fma(" << A << ", w[k].x, " << acc << ".x); " << acc << ".y = fma(" << A
-                  << ", w[k].y, " << acc << ".y);\n";
-            else if (cls(f) == 2)
-                s << "                    " << acc << ".x = fma(-" << A << ", w[k].y, " << acc << ".x); " << acc << ".y = fma(" << A
-                  << ", w[k].x, " << acc << ".y);\n";
-            else
-                s << "                    " << acc << ".x = fma(" << A << ".x, w[k].x, fma(-" << A << ".y, w[k].y, " << acc << ".x)); " << acc
-                  << ".y = fma(" << A << ".x, w[k].y, fma(" << A << ".y, w[k].x, " << acc << ".y));\n";
-        }
-        s << "                }\n            }\n";
-    }
-    s << "            __syncwarp();\n"
-      << "            if (lane == 0) asm volatile(\"mbarrier.arrive.shared::cta.b64 _, [%0];\" ::\"r\"(su32(empty + slot)) : \"memory\");\n"
-      << "        }\n";
-    const int PLO = lob + bw, PHI = hib - bw;
-    s << "        const bool litp = ib >= " << PLO << " && ib < " << PHI << ";\n        const int rd = ib - BW;\n        switch (ph) {\n";
-    for (int ph = 0; ph < W; ++ph) {
-        s << "        case " << ph << ": {\n            if (ib < n_b) {\n                if (litp) {\n";
-        auto slotj = [&](int j) { return lit((ph + j) % W); };
-        for (auto& c : b) {
-            const int f = c.factor;
-            const double cc = coeffs[c.coeff].x;
-            for (int j = 0; j < W; ++j) {
-                const double2 e = band(f, (lob + hib) / 2, W - 1 - j);
-                const std::string acc = "win[" + lit(c.out) + "][" + slotj(j) + "]", mv = "m[" + lit(c.in) + "]";
-                if (cls(f) == 1) {
-                    if (e.x == 0.0) continue;
-                    const std::string v = KT.ref(cc * e.x);
-                    s << "                    " << acc << ".x = fma(" << v << ", " << mv << ".x, " << acc << ".x); " << acc << ".y = fma(" << v
-                      << ", " << mv << ".y, " << acc << ".y);\n";
-                } else if (cls(f) == 2) {
-                    if (e.y == 0.0) continue;
-                    const std::string v = KT.ref(cc * e.y);
-                    s << "                    " << acc << ".x = fma(-(" << v << "), " << mv << ".y, " << acc << ".x); " << acc << ".y = fma(" << v
-                      << ", " << mv << ".x, " << acc << ".y);\n";
-                } else {
-                    if (e.x == 0.0 && e.y == 0.0) continue;
-                    const std::string vx = KT.ref(cc * e.x), vy = KT.ref(cc * e.y);
-                    s << "                    " << acc << ".x = fma(" << vx << ", " << mv << ".x, fma(-(" << vy << "), " << mv << ".y, " << acc
-                      << ".x)); " << acc << ".y = fma(" << vx << ", " << mv << ".y, fma(" << vy << ", " << mv << ".x, " << acc << ".y));\n";
-                }
-            }
-        }
-        s << "                } else {\n";
-        for (int f : FB)
-            s << "                    double2 C" << f << "[W];\n#pragma unroll\n                    for (int j = 0; j < W; ++j) { const int r_ = ib + j - BW; C"
-              << f << "[j] = (r_ >= 0 && r_ < n_b) ? __ldg(P.rb + ((size_t)" << f << " * P.nmax + r_) * W + (W - 1 - j)) : Z; }\n";
-        for (auto& c : b) {
-            const std::string mv = "m[" + lit(c.in) + "]", cc = KT.ref(coeffs[c.coeff].x);
-            s << "                    { const double2 cm = make_double2(" << cc << " * " << mv << ".x, " << cc << " * " << mv << ".y);\n";
-            for (int j = 0; j < W; ++j) {
-                const std::string acc = "win[" + lit(c.out) + "][" + slotj(j) + "]", cf = "C" + lit(c.factor) + "[" + lit(j) + "]";
-                s << "                      " << acc << ".x = fma(" << cf << ".x, cm.x, fma(-" << cf << ".y, cm.y, " << acc << ".x)); " << acc
-                  << ".y = fma(" << cf << ".x, cm.y, fma(" << cf << ".y, cm.x, " << acc << ".y));\n";
-            }
-            s << "                    }\n";
-        }
-        s << "                }\n            }\n            if (rd >= 0 && valid) {\n";
-        for (int o = 0; o < nout; ++o)
-            s << "                __stcs(P.out[" << o << "] + obase + (long long)rd * n_a, win[" << o << "][" << ph << "]);\n";
-        s << "            }\n";
-        for (int o = 0; o < nout; ++o) s << "            win[" << o << "][" << ph << "] = Z;\n";
-        s << "        } break;\n";
-    }
-    s << "        }\n        ph = ph + 1 == W ? 0 : ph + 1;\n    }\n}\n";
-    std::unique_ptr<KronJitPair> P(new KronJitPair());
-    P->k.fn = nvrtc_kernel(KT.finish(s.str()), "ks_pairl", 227 * 1024);
-    P->blocked = true;
-    P->line = true;
-    P->nin = nin;
-    P->nmid = nmid;
-    P->nout = nout;
-    P->bw = bw;
-    P->pull = false;
-    P->T = 32 * (NW + 1);
-    P->nq = C; // (shape key: lines per CTA, stages)
-    P->no = C;
-    P->pad = S + 100 * minb;
-    P->D = S;
-    P->smem = (size_t)S * stage + (size_t)2 * S * 8 + 128;
-    P->s_a = 1;
-    P->n_a = n_a;
-    P->n_b = n_b;
-    P->n_outer = n_outer;
-    P->grid = (unsigned)ntile;
-    P->coef = coeffs;
-    P->ncoef = (int)coeffs.size();
-    return P.release();
-}
-
-// ---------------------------------------------------------------------------
 // Tile variant for a contiguous in-plane axis (s_a = 1; at d = 3 the (t, 1)
 // pair) with one input: no register window at all. A CTA takes tiles of RB rows
 // of axis b (+ bw halo rows on both sides) x the whole axis a, of one outer
@@ -1302,7 +1046,6 @@ KronJitPair* kron_jitt_build(int nin, int nmid, int nout, int bw, const std::vec
     if (AHI < ALO || BHI < BLO || ALO + (nblkA - AHI) > 24 || BLO + (nblkB - BHI) > 24) return nullptr;
     auto band = [&](int f, int row, int k) -> double2 { return hrb[((size_t)f * nmax + row) * W + k]; };
     ConstTable KT;
-    KT.inline_literals = true; // (the constant table measured slower in all three tensor-map fed kernels but the line one)
     std::ostringstream s;
     s << "// generated: tile variant of the fused level passes (ks_kron_jit.cu)\n"
       << "#define BW " << bw << "\n#define W " << W << "\n#define NMID " << nmid << "\n#define NOUT " << nout << "\n#define RB " << RB

@@ -148,8 +148,8 @@ print("worst", worst)
 
 @pytest.mark.parametrize("variant", ["b2", "point", "tile"])
 def test_generated_variants_forced(variant):
-    """The row-blocked (ks_pairb), line (ks_pairl) and tile (ks_pairt: partial
-    last tiles, boundary blocks of both phases) generated kernels, forced on
+    """The row-blocked (ks_pairb) and tile (ks_pairt: partial last tiles,
+    boundary blocks of both phases) generated kernels, forced on
     problems too small for them to be picked by the grid-size rule, against the
     oracle: interior (literal Toeplitz) rows, boundary row blocks, boundary
     planes, ragged column tiles and partial row tiles (KS_KRON_JIT is read once
@@ -168,4 +168,3 @@ def test_generated_variants_forced(variant):
     if variant == "b2":
         kept = [l for l in out.stderr.splitlines() if "<- kept" in l]
         assert any("rows/thread 2" in l for l in kept), out.stderr[-1500:]   # row-blocked kernel ran
-        assert any("rows/thread -" in l for l in kept), out.stderr[-1500:]   # line kernel ran

@@ -2,7 +2,7 @@
 # Round-end style measurement pass: GPU tests, smoke, bench (c3 default incl. legs),
 # reference arm, c4 sweep, ncu launch list of the bench command, ncu --set full
 # captures of the FD kernels (k_xfold, k_fd_axis1) and of the matvec pass pairs
-# (ks_pairl, ks_pairb), summarised to CSV on the box (the reports exceed gpurun's
+# (ks_pairt, ks_pairb), summarised to CSV on the box (the reports exceed gpurun's
 # 64 MiB return limit). SKIP_TESTS=1 skips pytest, ONLY_NCU=1 runs only the captures.
 mkdir -p gpurun_out
 if [ -z "$ONLY_NCU" ]; then
