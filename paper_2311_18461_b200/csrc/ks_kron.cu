@@ -605,7 +605,7 @@ KronPlan* kron_plan(const std::vector<int>& dims,
             // row-blocked candidates (inner columns across the lanes); the first
             // apply times all candidates and keeps the fastest
             if (P->jit[k] && sa >= 32)
-                for (int rr : {2, 3}) { // (4 rows per thread: on par at c3, spills at bw = 4)
+                for (int rr : {2}) { // (3 rows: c3 197 vs 189 us, c5 8.2 vs 6.1 ms; 4 rows: on par at c3, spills at bw = 4)
                     std::unique_ptr<KronJitPair, KronJitDeleter> alt(kron_jitb_build(
                         pa.n_in, pa.n_out, pb.n_out, P->bwmax, ca, cb, frv, co, (long long)sa, na, nbb, outer, rb.data(),
                         nmax, rr));

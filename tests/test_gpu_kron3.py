@@ -146,7 +146,7 @@ print("worst", worst)
 """
 
 
-@pytest.mark.parametrize("variant", ["b2", "point", "tile"])
+@pytest.mark.parametrize("variant", ["b2", "point", "tile", "tile:22,3,2,8,2,3", "tile:16,4,4,8,2,2", "tile:12,2,3,4,2,4"])
 def test_generated_variants_forced(variant):
     """The row-blocked (ks_pairb) and tile (ks_pairt: partial last tiles,
     boundary blocks of both phases) generated kernels, forced on
@@ -156,7 +156,10 @@ def test_generated_variants_forced(variant):
     per process, hence the subprocess)."""
     import os, subprocess, sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, KS_KRON_JIT=variant)
+    env = dict(os.environ, KS_KRON_JIT=variant.split(":")[0])
+    if ":" in variant:  # an explicit tile shape: rows per tile, entries / rows per thread, warps, CTAs per SM, pieces of the time axis
+        env["KS_KRON_TILE"] = variant.split(":")[1]
+        variant = "tile"
     out = subprocess.run([sys.executable, "-c", _FORCED.format(root=root, tests=os.path.join(root, "tests"))],
                          env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
