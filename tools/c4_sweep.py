@@ -24,6 +24,7 @@ for p in range(2, 7):
     x = ks.DeviceVector(prob.N_dof)
     P.time(b, x, 3)  # warm-up (first launches load the kernels)
     ms_fd, _ = P.time(b, x, 20)
+    A.apply(b, x)  # (the first matvec times the generated kernel candidates)
     rep = ks.pcg(A, P, b, ks.PcgOptions(1e-8, 200))
     t0 = time.perf_counter()
     l2, en = Q.error_norms(Q.extend(rep.x, bnd), "sinsin", "sinsin")
