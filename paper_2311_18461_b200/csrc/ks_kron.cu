@@ -645,6 +645,17 @@ KronPlan* kron_plan(const std::vector<int>& dims,
                                         cfg[0], cfg[1], cfg[2], cfg[3], cfg[4], cfg[5]));
                     if (alt) P->jit_alt[k].push_back(std::move(alt));
                 }
+            // a candidate whose grid cannot fill the GPU never runs (kron_jit_runs): drop those, and let a
+            // runnable alternative take the place of a primary that is not (d = 2: the thread-per-point kernel
+            // has one CTA per two lines of axis 2 -- 65 CTAs at c4 -- while the tile kernel has 774 tiles)
+            if (P->jit[k]) {
+                auto& alts = P->jit_alt[k];
+                alts.erase(std::remove_if(alts.begin(), alts.end(), [](const auto& a) { return !kron_jit_runs(*a); }), alts.end());
+                if (!kron_jit_runs(*P->jit[k]) && !alts.empty()) {
+                    std::swap(P->jit[k], alts.back());
+                    alts.pop_back();
+                }
+            }
         }
     }
     for (auto& ps : P->passes) {

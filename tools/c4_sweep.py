@@ -25,11 +25,18 @@ for p in range(2, 7):
     P.time(b, x, 3)  # warm-up (first launches load the kernels)
     ms_fd, _ = P.time(b, x, 20)
     A.apply(b, x)  # (the first matvec times the generated kernel candidates)
+    rep0 = ks.pcg(A, P, b, ks.PcgOptions(1e-8, 200))  # (first solve: workspace allocation)
     rep = ks.pcg(A, P, b, ks.PcgOptions(1e-8, 200))
+    t0 = time.perf_counter()
+    for _ in range(20):
+        A.apply(b, x)
+    ks.lib().ks_synchronize()
+    ms_mv = (time.perf_counter() - t0) / 20 * 1e3
     t0 = time.perf_counter()
     l2, en = Q.error_norms(Q.extend(rep.x, bnd), "sinsin", "sinsin")
     t_err = time.perf_counter() - t0
     print(json.dumps({"config": "c4", "p": p, "n_el": n_el, "dofs": prob.N_dof, "iterations": rep.iterations,
-                      "converged": rep.converged, "solve_s": rep.solve_seconds, "fd_apply_ms": ms_fd,
+                      "converged": rep.converged, "solve_s": rep.solve_seconds, "first_solve_s": rep0.solve_seconds,
+                      "fd_apply_ms": ms_fd, "matvec_ms": ms_mv, "plan": A.plan_info(),
                       "setup_s": t_setup, "rhs_lift_s": t_lift, "error_s": t_err, "l2_error": l2,
                       "energy_error": en, "fd_info": P.info()}), flush=True)
