@@ -593,7 +593,7 @@ KronPlan* kron_plan(const std::vector<int>& dims,
                                            nbb, outer));
             // (alternative block shapes of the thread-per-point kernel only where neither tensor-map fed
             // variant applies: they never won against those, and every candidate costs an NVRTC compile)
-            const bool fed = (sa >= 32 || (sa == 1 && pa.n_in == 1)) && P->bwmax <= 4;
+            const bool fed = (sa >= 32 && P->bwmax <= 4) || (sa == 1 && pa.n_in == 1 && P->bwmax <= 6);
             if (P->jit[k] && !fed)
                 for (int tm : {192, 128}) {
                     std::unique_ptr<KronJitPair, KronJitDeleter> alt(kron_jit_build(

@@ -1001,7 +1001,7 @@ KronJitPair* kron_jitt_build(int nin, int nmid, int nout, int bw, const std::vec
                              const double2* hrb, int nmax, int RB, int RA, int RR, int NWARP, int minb, int NAS) {
     if (const char* e = std::getenv("KS_KRON_JIT"))
         if (std::strcmp(e, "0") == 0) return nullptr;
-    if (nin != 1 || nmid < 1 || nmid > 4 || nout < 1 || nout > 4 || bw < 1 || bw > 4) return nullptr;
+    if (nin != 1 || nmid < 1 || nmid > 4 || nout < 1 || nout > 4 || bw < 1 || bw > 6) return nullptr;
     if (n_a < 4 * bw + 2 || n_b < 4 * bw + 2 || RA < 1 || RR < 1 || RB < RR || RB % RR != 0 || NAS < 1) return nullptr;
     const int W = 2 * bw + 1, RBH = RB + 2 * bw;
     if (RBH > 32) return nullptr; // phase A: one lane per row
@@ -1028,7 +1028,7 @@ KronJitPair* kron_jitt_build(int nin, int nmid, int nout, int bw, const std::vec
         lob = std::max(lob, lo);
         hib = std::min(hib, hi);
     }
-    if (loa > 8 || n_a - hia > 8 || lob > 8 || n_b - hib > 8) return nullptr;
+    if (loa > 2 * bw + 4 || n_a - hia > 2 * bw + 4 || lob > 2 * bw + 4 || n_b - hib > 2 * bw + 4) return nullptr; // not a uniform-mesh factor
     // shared memory: x rows [RBH][PX] (bw zeros | n_a | zeros, PX odd), mids [NMID][RBH][PM] (PM odd)
     // the axis-a range of a tile: NAS pieces of AT entries (a multiple of RA); the halo along a is only loaded
     const int AT = ((n_a + NAS - 1) / NAS + RA - 1) / RA * RA;

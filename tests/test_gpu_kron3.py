@@ -134,7 +134,7 @@ from oracle import oracle as O
 from helpers import setup_arrays, rel, maxrel
 O.build_oracle()
 worst = 0.0
-for p, n_el, n_el_t in [(2, 20, 17), (3, 14, 9), (4, 13, 11), (2, 33, 6), (4, 19, 18), (3, 30, 20)]:
+for p, n_el, n_el_t in [(2, 20, 17), (3, 14, 9), (4, 13, 11), (2, 33, 6), (4, 19, 18), (3, 30, 20), (5, 20, 26), (6, 24, 30)]:
     a = setup_arrays(ks, 3, p, n_el, n_el_t)
     A = ks.assemble_system_operator(a["prob"])
     K = O.OracleKron(a["dims"], O.system_terms(a, 3, a["nu"]))

@@ -31,9 +31,7 @@ int main(int argc, char** argv) {
     std::vector<JitContrib> a = {{0, 0, 0, 0}, {0, 1, 2, 1}, {0, 2, 5, 2}};
     std::vector<JitContrib> b = {{0, 0, 1, 3}, {1, 0, 3, 4}, {2, 0, 4, 5}, {1, 1, 1, 6}, {1, 2, 4, 7}, {2, 2, 1, 8}};
     std::vector<double2> co = {{1, 0}, {1, 0}, {1, 0}, {1, 0}, {1, 0}, {-1, 0}, {1, 0}, {2, 0}, {-1, 0}};
-    const int RBm = (32 - 2 * bw) / 4 * 4;
-    for (auto cfg : {std::array<int, 6>{RBm, 4, 4, 8, 2, 2}, std::array<int, 6>{RBm, 4, 4, 8, 2, 3}, std::array<int, 6>{RBm, 4, 4, 8, 3, 3},
-                     std::array<int, 6>{RBm, 4, 4, 16, 1, 1}, std::array<int, 6>{RBm, 4, 4, 16, 1, 2}, std::array<int, 6>{16, 4, 4, 8, 2, 1}}) {
+    for (auto cfg : kron_jitt_candidates(bw, n_a, n_b, (int)a.size(), (int)b.size(), 3, 3, 3)) {
         try {
             KronJitPair* p = kron_jitt_build(1, 3, 3, bw, a, b, freal, co, n_a, n_b, 4096, rb.data(), nmax, cfg[0], cfg[1], cfg[2], cfg[3], cfg[4], cfg[5]);
             std::printf("cfg %d %d %d %d: %s\n", cfg[0], cfg[3], cfg[4], cfg[5], p ? "built" : "null");
