@@ -213,6 +213,12 @@ KronJitPair* kron_jitt_build(int nin, int nmid, int nout, int bw, const std::vec
                              const std::vector<JitContrib>& b, const std::vector<int>& freal,
                              const std::vector<double2>& coeffs, int n_a, int n_b, long long n_outer,
                              const double2* hrb, int nmax, int RB, int RA, int RR, int NWARP, int minb, int NAS);
+struct KronJitPass;
+KronJitPass* kron_jitc_build(int nin, int nout, int bw, const std::vector<JitContrib>& c, const std::vector<int>& freal,
+                             const std::vector<double2>& coeffs, long long s_a, int n_a, long long n_outer,
+                             const double2* hrb, int nmax, int RR);
+void kron_jitc_launch(const KronJitPass& J, void* const* hin, void* const* hout, cudaStream_t st);
+void kron_jitc_free(KronJitPass* p);
 const char* kron_jit_tag(const KronJitPair& J);
 std::vector<std::array<int, 6>> kron_jitt_candidates(int bw, int n_a, int n_b, int na_prod, int nb_prod, int nmid, int nout,
                                                      int keep);

@@ -92,6 +92,11 @@ struct KronPlan {
     // apply (the faster one replaces jit[k]); the best shape differs between
     // sizes (c3: 160-thread blocks 0.81 ms vs 352 0.87; c5: 288 beats 160)
     std::vector<std::vector<std::unique_ptr<KronJitPair, KronJitDeleter>>> jit_alt;
+    // generated single passes (inner-column axes not covered by a runnable fused pair), indexed by pass
+    struct PassDeleter {
+        void operator()(KronJitPass* p) const { kron_jitc_free(p); }
+    };
+    std::vector<std::unique_ptr<KronJitPass, PassDeleter>> passc;
     // device pointer tables per (x, y) pair (kron_apply)
     std::map<std::pair<const void*, void*>, DevBuf> ptr_tables;
 };
@@ -657,6 +662,29 @@ KronPlan* kron_plan(const std::vector<int>& dims,
                 }
             }
         }
+        // passes over inner columns that no runnable pair covers (d = 2: the trailing axis-2 pass): generated
+        // single-pass kernel with literal bands
+        P->passc.resize(P->passes.size());
+        std::vector<bool> covered(P->passes.size(), false);
+        for (size_t k = 0; k + 1 < P->passes.size(); ++k)
+            if (P->jit[k] && kron_jit_runs(*P->jit[k])) covered[k] = covered[k + 1] = true;
+        for (size_t k = 0; k < P->passes.size(); ++k) {
+            if (covered[k]) continue;
+            const KronPass& ps = P->passes[k];
+            size_t sa = 1;
+            for (int x = 0; x < ps.axis; ++x) sa *= (size_t)P->dims[x];
+            if (sa < 32) continue;
+            std::vector<JitContrib> cc;
+            std::vector<double2> co;
+            for (int o = 0; o < ps.n_out; ++o)
+                for (int ci = ps.out_begin[o]; ci < ps.out_begin[o + 1]; ++ci) {
+                    cc.push_back(JitContrib{ps.contribs[ci].in, o, ps.contribs[ci].factor, (int)co.size()});
+                    co.push_back(ps.contribs[ci].coeff);
+                }
+            const int na = P->dims[ps.axis];
+            P->passc[k].reset(kron_jitc_build(ps.n_in, ps.n_out, P->bwmax, cc, frv, co, (long long)sa, na,
+                                              (long long)(P->N / (sa * (size_t)na)), rb.data(), nmax, 4));
+        }
     }
     for (auto& ps : P->passes) {
         std::vector<int> ib(ps.n_in + 1, 0);
@@ -834,6 +862,11 @@ void kron_apply(KronPlan& P, const double2* x, double2* y, cudaStream_t st,
                 ++k;
                 continue;
             }
+        }
+        // generated single pass (inner columns, literal bands)
+        if (k < P.passc.size() && P.passc[k] && !shard_last && P.shard_rows == 0) {
+            kron_jitc_launch(*P.passc[k], host_ptrs.data() + P.ptr_off[k], host_ptrs.data() + P.ptr_off[k] + ps.n_in, st);
+            continue;
         }
         // element-parallel level kernel (all axes)
         if (ps.n_out <= 8 && P.bwmax >= 1 && P.bwmax <= 4) {

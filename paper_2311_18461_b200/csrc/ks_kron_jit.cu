@@ -1272,6 +1272,164 @@ extern "C" __global__ void __launch_bounds__(T, MINB) ks_pairt(const __grid_cons
     return P.release();
 }
 
+// ---------------------------------------------------------------------------
+// Generated single pass along an axis with inner columns (s_a >= 32): the trailing
+// pass of a plan with an odd number of passes (d = 2: axis 2 after the (t, 1) pair),
+// or a pass whose pair cannot run fused. Lanes across the contiguous columns, a
+// thread owns RR consecutive rows of the axis and loads RR + 2 bw values per input
+// for them straight from global memory (the level tensors of these plans sit in L2);
+// the row block is uniform across the CTA, so the band entries are literals (Toeplitz
+// interior, one code path per boundary block). The element-parallel kernel it
+// replaces loads 2 bw + 1 values and band rows per point: c4 (p = 2) axis-2 pass
+// 61 us.
+// ---------------------------------------------------------------------------
+struct KronJitPass {
+    cudaKernel_t fn = nullptr;
+    int nin = 0, nout = 0;
+    unsigned gx = 0, gy = 0;
+};
+void kron_jitc_free(KronJitPass* p) { delete p; }
+
+KronJitPass* kron_jitc_build(int nin, int nout, int bw, const std::vector<JitContrib>& c, const std::vector<int>& freal,
+                             const std::vector<double2>& coeffs, long long s_a, int n_a, long long n_outer,
+                             const double2* hrb, int nmax, int RR) {
+    if (const char* e = std::getenv("KS_KRON_JIT"))
+        if (std::strcmp(e, "0") == 0) return nullptr;
+    if (s_a < 32 || nin < 1 || nin > 6 || nout < 1 || nout > 4 || bw < 1 || bw > 6 || RR < 1 || RR > 4 || n_a < 4 * bw + 2)
+        return nullptr;
+    const int W = 2 * bw + 1;
+    auto cls = [&](int f) { return freal[f]; };
+    int lo = 0, hi = n_a;
+    for (auto& k : c) {
+        if (k.factor < 0 || coeffs[k.coeff].y != 0.0) return nullptr;
+        int l, h;
+        toeplitz_range(hrb, k.factor, nmax, n_a, W, l, h);
+        lo = std::max(lo, l);
+        hi = std::min(hi, h);
+    }
+    if (lo > 2 * bw + 4 || n_a - hi > 2 * bw + 4 || lo < bw || n_a - hi < bw) return nullptr;
+    const int nblk = (n_a + RR - 1) / RR, BLO = (lo + RR - 1) / RR, BHI = hi / RR;
+    if (BHI < BLO || BLO + (nblk - BHI) > 24) return nullptr;
+    const long long nqc = (s_a + 127) / 128;
+    if (nqc * n_outer > 0x7fffffffLL || nblk > 65535) return nullptr;
+    auto band = [&](int f, int row, int k) -> double2 { return hrb[((size_t)f * nmax + row) * W + k]; };
+    std::ostringstream s;
+    s << "// generated: single pass over inner columns (ks_kron_jit.cu)\n"
+      << "#define BW " << bw << "\n#define W " << W << "\n#define NIN " << nin << "\n#define NOUT " << nout << "\n#define RR " << RR
+      << "\n#define s_a " << s_a << "LL\n#define n_a " << n_a << "\n#define NQC " << nqc << "LL\n"
+      << "struct Par { const double2* in[NIN]; double2* out[NOUT]; };\n"
+      << R"(
+extern "C" __global__ void __launch_bounds__(128) ks_passc(const __grid_constant__ Par P) {
+    const long long o = blockIdx.x / NQC;
+    const long long q = (blockIdx.x - o * NQC) * 128 + threadIdx.x;
+    const int gb = blockIdx.y, r0 = gb * RR;
+    if (q >= s_a) return;
+    const size_t base = (size_t)o * n_a * s_a + q; // row r of this column: base + r * s_a
+    const double2 Z = make_double2(0.0, 0.0);
+    double2 acc[NOUT][RR];
+#pragma unroll
+    for (int o2 = 0; o2 < NOUT; ++o2)
+#pragma unroll
+        for (int i = 0; i < RR; ++i) acc[o2][i] = Z;
+    int cb = 0;
+)";
+    s << "    if (gb < " << BLO << ") cb = 1 + gb; else if (gb >= " << BHI << ") cb = " << (1 + BLO) << " + (gb - " << BHI << ");\n"
+      << "    switch (cb) {\n";
+    std::vector<std::pair<int, std::string>> pend;
+    auto emit = [&](const std::vector<int>& rows, bool guard) {
+        for (int g = 0; g < nin; ++g) {
+            bool used = false;
+            for (auto& k : c) used = used || k.in == g;
+            if (!used) continue;
+            s << "        {\n            double2 w[RR + 2 * BW];\n#pragma unroll\n            for (int k = 0; k < RR + 2 * BW; ++k) {";
+            if (guard)
+                s << " const int row = r0 - BW + k; w[k] = (row >= 0 && row < n_a) ? __ldg(P.in[" << g
+                  << "] + base + (size_t)row * s_a) : Z; }\n";
+            else
+                s << " w[k] = __ldg(P.in[" << g << "] + base + (size_t)(r0 - BW + k) * s_a); }\n";
+            for (auto& k : c) {
+                if (k.in != g) continue;
+                const double cc = coeffs[k.coeff].x;
+                for (size_t i = 0; i < rows.size(); ++i) {
+                    if (rows[i] == -2) continue;
+                    for (int t = 0; t < W; ++t) {
+                        const double2 e = rows[i] == -1 ? band(k.factor, (lo + hi) / 2, t) : band(k.factor, rows[i], t);
+                        const std::string acc = "acc[" + lit(k.out) + "][" + lit((int)i) + "]", wv = "w[" + lit((int)i + t) + "]";
+                        std::ostringstream u;
+                        if (cls(k.factor) == 1) {
+                            if (e.x == 0.0) continue;
+                            const std::string v = hexd(cc * e.x);
+                            u << "            " << acc << ".x = fma(" << v << ", " << wv << ".x, " << acc << ".x); " << acc << ".y = fma(" << v
+                              << ", " << wv << ".y, " << acc << ".y);\n";
+                        } else if (cls(k.factor) == 2) {
+                            if (e.y == 0.0) continue;
+                            const std::string v = hexd(cc * e.y);
+                            u << "            " << acc << ".x = fma(-(" << v << "), " << wv << ".y, " << acc << ".x); " << acc << ".y = fma(" << v
+                              << ", " << wv << ".x, " << acc << ".y);\n";
+                        } else {
+                            if (e.x == 0.0 && e.y == 0.0) continue;
+                            const std::string vx = hexd(cc * e.x), vy = hexd(cc * e.y);
+                            u << "            " << acc << ".x = fma(" << vx << ", " << wv << ".x, fma(-(" << vy << "), " << wv << ".y, " << acc
+                              << ".x)); " << acc << ".y = fma(" << vx << ", " << wv << ".y, fma(" << vy << ", " << wv << ".x, " << acc << ".y));\n";
+                        }
+                        pend.push_back({t, u.str()});
+                    }
+                }
+            }
+            std::stable_sort(pend.begin(), pend.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+            for (auto& q : pend) s << q.second;
+            pend.clear();
+            s << "        }\n";
+        }
+    };
+    {
+        int ci = 0;
+        s << "    case " << ci++ << ": {\n";
+        emit(std::vector<int>(RR, -1), false);
+        s << "    } break;\n";
+        auto blockrows = [&](int g) {
+            std::vector<int> rows(RR);
+            for (int i = 0; i < RR; ++i) rows[i] = g * RR + i < n_a ? g * RR + i : -2;
+            return rows;
+        };
+        for (int g = 0; g < BLO; ++g) {
+            s << "    case " << ci++ << ": {\n";
+            emit(blockrows(g), true);
+            s << "    } break;\n";
+        }
+        for (int g = BHI; g < nblk; ++g) {
+            s << "    case " << ci++ << ": {\n";
+            emit(blockrows(g), true);
+            s << "    } break;\n";
+        }
+        s << "    default: break;\n    }\n";
+    }
+    s << R"(#pragma unroll
+    for (int i = 0; i < RR; ++i)
+        if (r0 + i < n_a) {
+#pragma unroll
+            for (int o2 = 0; o2 < NOUT; ++o2) P.out[o2][base + (size_t)(r0 + i) * s_a] = acc[o2][i];
+        }
+}
+)";
+    std::unique_ptr<KronJitPass> P(new KronJitPass());
+    P->fn = nvrtc_kernel(s.str(), "ks_passc", 48 * 1024);
+    P->nin = nin;
+    P->nout = nout;
+    P->gx = (unsigned)(nqc * n_outer);
+    P->gy = (unsigned)nblk;
+    return P.release();
+}
+
+void kron_jitc_launch(const KronJitPass& J, void* const* hin, void* const* hout, cudaStream_t st) {
+    std::vector<void*> par((size_t)J.nin + J.nout);
+    for (int g = 0; g < J.nin; ++g) par[g] = hin[g];
+    for (int o = 0; o < J.nout; ++o) par[J.nin + o] = hout[o];
+    void* args[] = {(void*)par.data()};
+    KS_CUDA(cudaLaunchKernel((const void*)J.fn, dim3(J.gx, J.gy), dim3(128), args, 0, st));
+    check_launch("ks_passc (jit)");
+}
+
 // Tile-variant shapes worth timing for a pass pair, best first by a simple issue model:
 // per output point, phase A costs |a| products x the halo factor x the idle-lane factor of its
 // row-per-lane mapping, phase B |b| products, each divided by how evenly its work items fill

@@ -39,4 +39,9 @@ int main(int argc, char** argv) {
             std::printf("cfg %d %d %d %d: dumped\n", cfg[0], cfg[3], cfg[4], cfg[5]); (void)e;
         }
     }
+    try { // the generated single pass over inner columns (three inputs, three outputs)
+        kron_jitc_build(3, 3, bw, b, freal, co, 16641, n_b, 1, rb.data(), nmax, 4);
+    } catch (const std::exception&) {
+        std::printf("single pass: dumped\n");
+    }
 }
