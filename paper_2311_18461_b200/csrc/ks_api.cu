@@ -527,7 +527,14 @@ static void fd_create_impl(int kind, int d, const int* dims, double nu, int p_t,
     // positions 0..hc-1 and the odd ones after them (FoldAxis::perm), so both
     // time-major transforms move whole 1 KB rows; the blocks are numbered by
     // position.
-    const bool tm1 = pair && f->fold[0].n > 0 && (int)f->fold[0].perm.size() == dims[1];
+    // d = 2 (c2, c4): the same position-ordered plan without pair mode -- both axes on the bulk-copy fed
+    // transform (ks_xform.cu), the axis-1 transform hands the time-major layout to the ring solves; the
+    // block map / block order below follow the positions (KS_FD_XFOLD=0: round-1 transforms, natural order)
+    bool pos2d = d == 2;
+    for (int l = 0; l < d && pos2d; ++l)
+        pos2d = f->fold[l].n > 0 && (int)f->fold[l].perm.size() == dims[l + 1] && xfold_supported(f->fold[l]);
+    if (const char* e = std::getenv("KS_FD_XFOLD")) pos2d = pos2d && std::strcmp(e, "0") != 0;
+    const bool tm1 = (pair && f->fold[0].n > 0 && (int)f->fold[0].perm.size() == dims[1]) || pos2d;
     f->tm1 = tm1;
     // tm1 with every spatial axis folded: the transforms on axes 2..d keep their
     // eigen rows by position too (ks_xform.cu), so the pair blocks are keyed by
@@ -537,7 +544,18 @@ static void fd_create_impl(int kind, int d, const int* dims, double nu, int p_t,
         posall = f->fold[l].n > 0 && (int)f->fold[l].perm.size() == dims[l + 1] && xfold_supported(f->fold[l]);
     posall = posall && f->fold[1].perm == f->fold[2].perm;
     if (const char* e = std::getenv("KS_FD_XFOLD")) posall = posall && std::strcmp(e, "0") != 0;
+    posall = posall || pos2d;
     f->posall = posall;
+    // position <-> eigen-index of the axes of a pos2d plan
+    std::vector<int> q1, q2, ip1, ip2;
+    if (pos2d) {
+        q1 = f->fold[0].perm;
+        q2 = f->fold[1].perm;
+        ip1.resize(q1.size());
+        ip2.resize(q2.size());
+        for (size_t q = 0; q < q1.size(); ++q) ip1[q1[q]] = (int)q;
+        for (size_t q = 0; q < q2.size(); ++q) ip2[q2[q]] = (int)q;
+    }
     // fused axis-1 stage (least-squares blocks, folded axis 1, slab fits shared
     // memory; KS_FD_AXIS1=0 keeps the separate transform / solve / transform):
     // blocks numbered by axis-1 position within per-slab groups of n1b.
@@ -608,6 +626,7 @@ static void fd_create_impl(int kind, int d, const int* dims, double nu, int p_t,
                 id[l] = (int)(rest % (size_t)dims[l + 1]);
                 rest /= (size_t)dims[l + 1];
             }
+            if (pos2d) id[1] = q2[id[1]]; // slab o sits at position o of axis 2
             for (int p1 = 0; p1 < nbg; ++p1) {
                 id[0] = perm1[std::min(p1, n1 - 1)];
                 lam_blk[(size_t)p1 + (size_t)nbg * o] = ref_sum(id);
@@ -615,10 +634,22 @@ static void fd_create_impl(int kind, int d, const int* dims, double nu, int p_t,
             grp1[o] = (int)o;
         }
         f->fiber_block.resize(f->Ns);
-        for (size_t i = 0; i < f->Ns; ++i)
-            f->fiber_block[i] = pos1[i % (size_t)n1] + nbg * (int)(i / (size_t)n1);
+        for (size_t i = 0; i < f->Ns; ++i) {
+            const size_t o = i / (size_t)n1;
+            f->fiber_block[i] = pos1[i % (size_t)n1] + nbg * (int)(pos2d ? (size_t)ip2[o] : o);
+        }
     } else if (!dedup) {
         lam_blk.resize(f->Ns);
+        if (pos2d) {
+            // blocks in layout (position) order; the host map answers by natural fiber index
+            const size_t n1 = (size_t)dims[1];
+            f->fiber_block.resize(f->Ns);
+            for (size_t i = 0; i < f->Ns; ++i) {
+                const int id[3] = {q1[i % n1], q2[i / n1], 0};
+                lam_blk[i] = ref_sum(id);
+                f->fiber_block[(size_t)id[0] + n1 * (size_t)id[1]] = (int)i;
+            }
+        } else
         for (size_t i = 0; i < f->Ns; ++i) {
             lam_blk[i] = ref_sum(idx);
             for (int l = 0; l < d; ++l) {
@@ -649,9 +680,13 @@ static void fd_create_impl(int kind, int d, const int* dims, double nu, int p_t,
             }
         }
         for (size_t i = 0; i < f->Ns; ++i) f->fiber_block[i] = id_of[f->fiber_block[i]];
+        // device map by layout position (natural order unless pos2d)
+        std::vector<int> fb_dev(f->fiber_block);
+        if (pos2d)
+            for (size_t i = 0; i < f->Ns; ++i)
+                fb_dev[i] = f->fiber_block[(size_t)q1[i % n] + n * (size_t)q2[i / n]];
         B.fiber_block.alloc(f->Ns * sizeof(int));
-        KS_CUDA(cudaMemcpy(B.fiber_block.p, f->fiber_block.data(), f->Ns * sizeof(int),
-                           cudaMemcpyHostToDevice));
+        KS_CUDA(cudaMemcpy(B.fiber_block.p, fb_dev.data(), f->Ns * sizeof(int), cudaMemcpyHostToDevice));
     }
     B.nblk = lam_blk.size();
     B.lam_blk.alloc(B.nblk * sizeof(double));
