@@ -508,6 +508,15 @@ static void fd_create_impl(int kind, int d, const int* dims, double nu, int p_t,
         dedup = dims[l + 1] == dims[1] &&
                 std::memcmp(lambda[l], lambda[0], sizeof(double) * dims[1]) == 0;
     if (const char* e = std::getenv("KS_FD_DEDUP")) dedup = dedup && std::strcmp(e, "0") != 0;
+    // d = 2: the permutation map makes the solves gather their factor rows (a warp of consecutive fibers
+    // reads scattered blocks); one block per fiber in layout order reads them coalesced -- c4 FD 0.24 ->
+    // 0.21 ms at p = 2, 0.41 -> 0.32 ms at p = 6 -- for twice the factor bytes, so only while those stay
+    // small (KS_FD_DEDUP=1 keeps the deduplicated blocks)
+    if (d == 2 && dedup) {
+        const double row_bytes = kind == 0 ? 16.0 * p_t + 8.0 : (3.0 * p_t + 1.0) * 16.0 + 1.0;
+        const char* e = std::getenv("KS_FD_DEDUP");
+        if (!(e && std::strcmp(e, "1") == 0) && (double)f->Ns * dims[0] * row_bytes <= 4e9) dedup = false;
+    }
     std::vector<double> lam_blk;
     f->fiber_block.clear();
     auto ref_sum = [&](const int* idx) { // fdsolver.cpp:33-35 order

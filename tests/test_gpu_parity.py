@@ -301,6 +301,23 @@ def test_argument_checks(gpu, oracle):
     assert np.array_equal(zd.to_host(), P.apply(r)) and np.array_equal(yd.to_host(), A.apply(r))
 
 
+@pytest.mark.parametrize("dedup", ["1", None])
+def test_fd_d2_block_dedup_modes(gpu, oracle, monkeypatch, dedup):
+    """d = 2 with identical axes: one block per fiber in layout order (default while the
+    factors are small) and the deduplicated blocks of sorted multi-indices
+    (KS_FD_DEDUP=1), both on the position-ordered plan, against the oracle."""
+    if dedup:
+        monkeypatch.setenv("KS_FD_DEDUP", dedup)
+    for p, n_el, n_el_t in [(3, 16, 16), (2, 90, 7), (4, 12, 10)]:   # (90 elements: axis 1 too long for the fused stage)
+        a, g, o = _fd_pair(gpu, oracle, 2, p, n_el, n_el_t)
+        n = a["dims"][1]
+        fused = g.info()["fused_axis1"]   # (the fused axis-1 stage keeps one group of blocks per slab)
+        assert g.info()["blocks"] == ((n + 1) // 2 * 2 * n if fused else n * (n + 1) // 2 if dedup else n * n)
+        r = oracle.random_vec(o.N, 11)
+        z = o.apply(r)
+        assert rel(g.apply(r), z) <= TOL and maxrel(g.apply(r), z) <= TOL
+
+
 @pytest.mark.parametrize("d,p,n_el,n_el_t", [(1, 2, 256, 6), (1, 3, 170, 5), (2, 2, 161, 3), (2, 3, 7, 4, )])
 def test_long_axes_match_oracle(gpu, oracle, d, p, n_el, n_el_t):
     """Axes longer than 160 (SPEC's 1-D pencils go to 256 elements; the
