@@ -543,6 +543,13 @@ static void fd_create_impl(int kind, int d, const int* dims, double nu, int p_t,
     for (int l = 0; l < d && pos2d; ++l)
         pos2d = f->fold[l].n > 0 && (int)f->fold[l].perm.size() == dims[l + 1] && xfold_supported(f->fold[l]);
     if (const char* e = std::getenv("KS_FD_XFOLD")) pos2d = pos2d && std::strcmp(e, "0") != 0;
+    // (small problems -- c2: 67 column tiles per transform -- stay on the round-1 kernels: the persistent
+    // bulk-copy fed transform measured 3 us slower per launch there, c2 FD 49 -> 55 us)
+    // (KS_FD_XFOLD=1 keeps the position-ordered plan at any size: tests)
+    const char* xf_env = std::getenv("KS_FD_XFOLD");
+    if (pos2d && !(xf_env && std::strcmp(xf_env, "1") == 0) &&
+        f->N / ((size_t)std::max(dims[1], dims[2]) * 64) < (size_t)device_sms())
+        pos2d = false;
     const bool tm1 = (pair && f->fold[0].n > 0 && (int)f->fold[0].perm.size() == dims[1]) || pos2d;
     f->tm1 = tm1;
     // tm1 with every spatial axis folded: the transforms on axes 2..d keep their

@@ -308,6 +308,7 @@ def test_fd_d2_block_dedup_modes(gpu, oracle, monkeypatch, dedup):
     (KS_FD_DEDUP=1), both on the position-ordered plan, against the oracle."""
     if dedup:
         monkeypatch.setenv("KS_FD_DEDUP", dedup)
+    monkeypatch.setenv("KS_FD_XFOLD", "1")   # the position-ordered plan at these small sizes too
     for p, n_el, n_el_t in [(3, 16, 16), (2, 90, 7), (4, 12, 10)]:   # (90 elements: axis 1 too long for the fused stage)
         a, g, o = _fd_pair(gpu, oracle, 2, p, n_el, n_el_t)
         n = a["dims"][1]
@@ -316,6 +317,7 @@ def test_fd_d2_block_dedup_modes(gpu, oracle, monkeypatch, dedup):
         r = oracle.random_vec(o.N, 11)
         z = o.apply(r)
         assert rel(g.apply(r), z) <= TOL and maxrel(g.apply(r), z) <= TOL
+        assert g.info()["time_major_axis"] == 1 or g.info()["fused_axis1"]
 
 
 @pytest.mark.parametrize("d,p,n_el,n_el_t", [(1, 2, 256, 6), (1, 3, 170, 5), (2, 2, 161, 3), (2, 3, 7, 4, )])
