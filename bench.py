@@ -682,6 +682,33 @@ def main():
                           "fd_apply_us_graph": c2lat * 1e3,
                           "problem": "u = sin(pi x) sin(pi y) exp(-2 i pi^2 t), f = S u"}
 
+            # BASELINE configs[3] (c4): degree sweep p = 2..6 at 128 elements, same manufactured
+            # problem: iterations, time per FD application / matvec, steady-state solve
+            c4 = []
+            for pdeg in range(2, 7):
+                p4 = ks.SpaceTimeProblem.uniform(2, pdeg, 128, 128)
+                P4, A4 = ks.FDPreconditioner(p4, device=local), ks.assemble_system_operator(p4, device=local)
+                rhs4, _ = ks.Quadrature(p4, device=local).lift("sinsin", "sinsin")
+                b4, x4 = ks.DeviceVector.from_host(rhs4), ks.DeviceVector(p4.N_dof)
+                P4.time(b4, x4, 3)
+                ms_fd4, _ = P4.time(b4, x4, 20)
+                A4.apply(b4, x4)  # (the first matvec times the generated candidates)
+                ks.lib().ks_synchronize()
+                t0 = time.perf_counter()
+                for _ in range(20):
+                    A4.apply(b4, x4)
+                ks.lib().ks_synchronize()
+                ms_mv4 = (time.perf_counter() - t0) / 20 * 1e3
+                ks.pcg(A4, P4, b4, ks.PcgOptions(1e-8, 200))
+                rep4 = ks.pcg(A4, P4, b4, ks.PcgOptions(1e-8, 200))
+                d4 = p4.reduced_dims()
+                roof4 = max(fd_flops_per_dof(d4, pdeg) * p4.N_dof / (fp64_peak * 1e12), 32.0 * p4.N_dof / (hbm_peak * 1e9))
+                c4.append({"p": pdeg, "dofs": p4.N_dof, "iterations": rep4.iterations, "converged": rep4.converged,
+                           "solve_seconds": rep4.solve_seconds, "fd_apply_ms": ms_fd4, "matvec_ms": ms_mv4,
+                           "fd_frac_of_roofline": roof4 * 1e3 / ms_fd4})
+                del P4, A4
+            legs["c4"] = c4
+
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         kind, sec, used = cpu_baseline_fd(args.config, r_host, steps=3, warmup=1)
