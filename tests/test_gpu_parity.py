@@ -317,7 +317,8 @@ def test_fd_d2_block_dedup_modes(gpu, oracle, monkeypatch, dedup):
         r = oracle.random_vec(o.N, 11)
         z = o.apply(r)
         assert rel(g.apply(r), z) <= TOL and maxrel(g.apply(r), z) <= TOL
-        assert g.info()["time_major_axis"] == 1 or g.info()["fused_axis1"]
+        if g.info()["folded_axes"] == [1, 2]:   # (KS_FD_FOLD=0 runs have no position-ordered plan)
+            assert g.info()["time_major_axis"] == 1 or g.info()["fused_axis1"]
 
 
 @pytest.mark.parametrize("d,p,n_el,n_el_t", [(1, 2, 256, 6), (1, 3, 170, 5), (2, 2, 161, 3), (2, 3, 7, 4, )])
