@@ -668,6 +668,30 @@ void toeplitz_range(const double2* hrb, int f, int nmax, int n, int W, int& lo, 
     while (hi < n && same(hi)) ++hi;
 }
 
+// One statement `acc += (cc * e) * w` with the band entry as a literal, by factor class (1 real,
+// 2 purely imaginary, 0 complex): 2 DFMA for a real or imaginary entry, 4 for a complex one. Empty
+// when the entry is zero.
+std::string literal_fma(const std::string& ind, int fclass, double cc, double2 e, const std::string& acc, const std::string& wv) {
+    std::ostringstream t;
+    if (fclass == 1) {
+        if (e.x == 0.0) return "";
+        const std::string v = hexd(cc * e.x);
+        t << ind << acc << ".x = fma(" << v << ", " << wv << ".x, " << acc << ".x); " << acc << ".y = fma(" << v << ", " << wv << ".y, " << acc
+          << ".y);\n";
+    } else if (fclass == 2) {
+        if (e.y == 0.0) return "";
+        const std::string v = hexd(cc * e.y);
+        t << ind << acc << ".x = fma(-(" << v << "), " << wv << ".y, " << acc << ".x); " << acc << ".y = fma(" << v << ", " << wv << ".x, " << acc
+          << ".y);\n";
+    } else {
+        if (e.x == 0.0 && e.y == 0.0) return "";
+        const std::string vx = hexd(cc * e.x), vy = hexd(cc * e.y);
+        t << ind << acc << ".x = fma(" << vx << ", " << wv << ".x, fma(-(" << vy << "), " << wv << ".y, " << acc << ".x)); " << acc
+          << ".y = fma(" << vx << ", " << wv << ".y, fma(" << vy << ", " << wv << ".x, " << acc << ".y));\n";
+    }
+    return t.str();
+}
+
 } // namespace
 
 KronJitPair* kron_jitb_build(int nin, int nmid, int nout, int bw, const std::vector<JitContrib>& a,
@@ -1125,25 +1149,8 @@ extern "C" __global__ void __launch_bounds__(T, MINB) ks_pairt(const __grid_cons
             if (rows[i] == -2) continue;
             for (int k = 0; k < W; ++k) {
                 const double2 e = rows[i] == -1 ? band(f, mid_row, k) : band(f, rows[i], k);
-                const std::string acc = accn((int)i), wv = "w[" + lit((int)i + k) + "]";
-                std::ostringstream t;
-                if (cls(f) == 1) {
-                    if (e.x == 0.0) continue;
-                    const std::string v = KT.ref(cc * e.x);
-                    t << ind << acc << ".x = fma(" << v << ", " << wv << ".x, " << acc << ".x); " << acc << ".y = fma(" << v << ", " << wv
-                      << ".y, " << acc << ".y);\n";
-                } else if (cls(f) == 2) {
-                    if (e.y == 0.0) continue;
-                    const std::string v = KT.ref(cc * e.y);
-                    t << ind << acc << ".x = fma(-(" << v << "), " << wv << ".y, " << acc << ".x); " << acc << ".y = fma(" << v << ", " << wv
-                      << ".x, " << acc << ".y);\n";
-                } else {
-                    if (e.x == 0.0 && e.y == 0.0) continue;
-                    const std::string vx = KT.ref(cc * e.x), vy = KT.ref(cc * e.y);
-                    t << ind << acc << ".x = fma(" << vx << ", " << wv << ".x, fma(-(" << vy << "), " << wv << ".y, " << acc << ".x)); " << acc
-                      << ".y = fma(" << vx << ", " << wv << ".y, fma(" << vy << ", " << wv << ".x, " << acc << ".y));\n";
-                }
-                pend.push_back({k, t.str()});
+                const std::string st = literal_fma(ind, cls(f), cc, e, accn((int)i), "w[" + lit((int)i + k) + "]");
+                if (!st.empty()) pend.push_back({k, st});
             }
         }
     };
@@ -1354,25 +1361,9 @@ extern "C" __global__ void __launch_bounds__(128) ks_passc(const __grid_constant
                     if (rows[i] == -2) continue;
                     for (int t = 0; t < W; ++t) {
                         const double2 e = rows[i] == -1 ? band(k.factor, (lo + hi) / 2, t) : band(k.factor, rows[i], t);
-                        const std::string acc = "acc[" + lit(k.out) + "][" + lit((int)i) + "]", wv = "w[" + lit((int)i + t) + "]";
-                        std::ostringstream u;
-                        if (cls(k.factor) == 1) {
-                            if (e.x == 0.0) continue;
-                            const std::string v = hexd(cc * e.x);
-                            u << "            " << acc << ".x = fma(" << v << ", " << wv << ".x, " << acc << ".x); " << acc << ".y = fma(" << v
-                              << ", " << wv << ".y, " << acc << ".y);\n";
-                        } else if (cls(k.factor) == 2) {
-                            if (e.y == 0.0) continue;
-                            const std::string v = hexd(cc * e.y);
-                            u << "            " << acc << ".x = fma(-(" << v << "), " << wv << ".y, " << acc << ".x); " << acc << ".y = fma(" << v
-                              << ", " << wv << ".x, " << acc << ".y);\n";
-                        } else {
-                            if (e.x == 0.0 && e.y == 0.0) continue;
-                            const std::string vx = hexd(cc * e.x), vy = hexd(cc * e.y);
-                            u << "            " << acc << ".x = fma(" << vx << ", " << wv << ".x, fma(-(" << vy << "), " << wv << ".y, " << acc
-                              << ".x)); " << acc << ".y = fma(" << vx << ", " << wv << ".y, fma(" << vy << ", " << wv << ".x, " << acc << ".y));\n";
-                        }
-                        pend.push_back({t, u.str()});
+                        const std::string st = literal_fma("            ", cls(k.factor), cc, e, "acc[" + lit(k.out) + "][" + lit((int)i) + "]",
+                                                           "w[" + lit((int)i + t) + "]");
+                        if (!st.empty()) pend.push_back({t, st});
                     }
                 }
             }
