@@ -207,7 +207,7 @@ KronJitPair* kron_jit_build(int nin, int nmid, int nout, int bw, const std::vect
 KronJitPair* kron_jitb_build(int nin, int nmid, int nout, int bw, const std::vector<JitContrib>& a,
                              const std::vector<JitContrib>& b, const std::vector<int>& freal,
                              const std::vector<double2>& coeffs, long long s_a, int n_a, int n_b, long long n_outer,
-                             const double2* hrb, int nmax, int R, bool align4 = false);
+                             const double2* hrb, int nmax, int R, bool align4 = false, bool shift = false);
 // line variant for s_a = 1 (thread per point of C whole lines, planes as tensor-map boxes)
 KronJitPair* kron_jitt_build(int nin, int nmid, int nout, int bw, const std::vector<JitContrib>& a,
                              const std::vector<JitContrib>& b, const std::vector<int>& freal,

@@ -611,15 +611,18 @@ KronPlan* kron_plan(const std::vector<int>& dims,
             // apply times all candidates and keeps the fastest
             if (P->jit[k] && sa >= 32)
                 for (int rr : {2}) { // (3 rows: c3 197 vs 189 us, c5 8.2 vs 6.1 ms; 4 rows: on par at c3, spills at bw = 4)
-                    std::unique_ptr<KronJitPair, KronJitDeleter> alt(kron_jitb_build(
-                        pa.n_in, pa.n_out, pb.n_out, P->bwmax, ca, cb, frv, co, (long long)sa, na, nbb, outer, rb.data(),
-                        nmax, rr));
-                    if (alt) P->jit_alt[k].push_back(std::move(alt));
-                    // the same with the warp count aligned to the register allocation unit
-                    std::unique_ptr<KronJitPair, KronJitDeleter> al4(kron_jitb_build(
-                        pa.n_in, pa.n_out, pb.n_out, P->bwmax, ca, cb, frv, co, (long long)sa, na, nbb, outer, rb.data(),
-                        nmax, rr, true));
-                    if (al4) P->jit_alt[k].push_back(std::move(al4));
+                    // {warp count aligned to the register allocation unit, shifted window}: the window shifted by
+                    // register moves needs one copy of the push code instead of 2 bw + 1 rotated ones -- at bw = 4
+                    // the copies made the hot loop ~34 KB and the kernel instruction-fetch bound (c5: 6.09 ->
+                    // 4.51 ms with the shift); at bw = 2 the rotated copies are faster (c3: 189 vs 197 us)
+                    for (auto v : {std::array<bool, 2>{false, false}, std::array<bool, 2>{true, false},
+                                   std::array<bool, 2>{false, true}, std::array<bool, 2>{true, true}}) {
+                        if (P->bwmax >= 4 && !v[1]) continue;
+                        std::unique_ptr<KronJitPair, KronJitDeleter> alt(kron_jitb_build(
+                            pa.n_in, pa.n_out, pb.n_out, P->bwmax, ca, cb, frv, co, (long long)sa, na, nbb, outer, rb.data(),
+                            nmax, rr, v[0], v[1]));
+                        if (alt) P->jit_alt[k].push_back(std::move(alt));
+                    }
                 }
             if (P->jit[k] && sa == 1 && pa.n_in == 1)
                 // tile variant: {rows per tile, entries / rows per thread in phases A / B, warps, CTAs per SM}
@@ -833,13 +836,15 @@ void kron_apply(KronPlan& P, const double2* x, double2* y, cudaStream_t st,
                 // KS_KRON_JIT=b2 / b4 / point forces a candidate (tests, profiling)
                 if (const char* e = std::getenv("KS_KRON_JIT")) {
                     // (b2 / b4: rows per thread of the row-blocked kernel; tile: the tile kernel too)
-                    const bool wtile = !std::strcmp(e, "tile");
-                    const int want = !std::strcmp(e, "b2") || wtile ? 2 : !std::strcmp(e, "b4") ? 4 : !std::strcmp(e, "point") ? 0 : -1;
+                    const bool wtile = !std::strcmp(e, "tile"), wshift = !std::strcmp(e, "shift");
+                    const int want = !std::strcmp(e, "b2") || wtile || wshift ? 2 : !std::strcmp(e, "b4") ? 4 : !std::strcmp(e, "point") ? 0 : -1;
                     if (want >= 0) {
                         std::vector<KronJitPair*> all{P.jit[k].get()};
                         for (auto& alt : P.jit_alt[k]) all.push_back(alt.get());
                         for (size_t a = 0; a < all.size(); ++a)
-                            if ((kron_jit_blocked_rows(*all[a]) == want || (wtile && kron_jit_blocked_rows(*all[a]) >= 1000)) &&
+                            if (((kron_jit_blocked_rows(*all[a]) == want &&
+                                  (std::strcmp(kron_jit_tag(*all[a]), "shifted window") == 0) == wshift) ||
+                                 ((wtile || wshift) && kron_jit_blocked_rows(*all[a]) >= 1000)) &&
                                 tb[a] < 1e29f) {
                                 bi = a;
                                 break;

@@ -527,7 +527,7 @@ bool kron_jit_runs(const KronJitPair& J) {
     // KS_KRON_JIT=b2 / b4 / point (a forced candidate: tests, profiling) also lifts the grid-size rule
     static const bool forced = [] {
         const char* e = std::getenv("KS_KRON_JIT");
-        return e && (!std::strcmp(e, "b2") || !std::strcmp(e, "b4") || !std::strcmp(e, "point") || !std::strcmp(e, "tile"));
+        return e && (!std::strcmp(e, "b2") || !std::strcmp(e, "b4") || !std::strcmp(e, "point") || !std::strcmp(e, "tile") || !std::strcmp(e, "shift"));
     }();
     return forced || J.grid >= (unsigned)sm_count();
 }
@@ -697,7 +697,7 @@ std::string literal_fma(const std::string& ind, int fclass, double cc, double2 e
 KronJitPair* kron_jitb_build(int nin, int nmid, int nout, int bw, const std::vector<JitContrib>& a,
                              const std::vector<JitContrib>& b, const std::vector<int>& freal,
                              const std::vector<double2>& coeffs, long long s_a, int n_a, int n_b, long long n_outer,
-                             const double2* hrb, int nmax, int R, bool align4) {
+                             const double2* hrb, int nmax, int R, bool align4, bool shift) {
     if (const char* e = std::getenv("KS_KRON_JIT"))
         if (std::strcmp(e, "0") == 0) return nullptr;
     if (s_a < 32 || nin < 1 || nmid < 1 || nout < 1 || nin > 4 || nmid > 6 || nout > 2 || bw < 1 || bw > 4) return nullptr;
@@ -908,9 +908,12 @@ extern "C" __global__ void __launch_bounds__(32 * (NW + 1), 1) ks_pairb(const __
     const int PLO = lob + bw, PHI = hib - bw; // planes whose band columns are all interior
     s << "        const bool litp = ib >= " << PLO << " && ib < " << PHI << ";\n"
       << "        const int rd = ib - BW;\n"
-      << "        switch (ph) {\n";
-    for (int ph = 0; ph < W; ++ph) {
-        s << "        case " << ph << ": {\n            if (ib < n_b) {\n                if (litp) {\n";
+      << (shift ? "        {\n" : "        switch (ph) {\n");
+    // shift: one copy of the push with the window shifted by register moves every plane instead of W
+    // rotated copies selected by the phase (a ninth of the push code: the hot loop of the bw = 4 kernel
+    // is ~34 KB with the copies, 13% of its stall samples were instruction-cache misses)
+    for (int ph = 0; ph < (shift ? 1 : W); ++ph) {
+        s << (shift ? "        {\n" : "        case " + lit(ph) + ": {\n") << "            if (ib < n_b) {\n                if (litp) {\n";
         auto slotj = [&](int j) { return lit((ph + j) % W); };
         for (auto& c : b) {
             const int f = c.factor;
@@ -969,8 +972,15 @@ extern "C" __global__ void __launch_bounds__(32 * (NW + 1), 1) ks_pairb(const __
                   << ") + lane, win[" << o << "][" << r << "][" << ph << "]);\n";
         s << "            }\n";
         for (int o = 0; o < nout; ++o)
-            for (int r = 0; r < R; ++r) s << "            win[" << o << "][" << r << "][" << ph << "] = Z;\n";
-        s << "        } break;\n";
+            for (int r = 0; r < R; ++r) {
+                if (shift) {
+                    for (int j = 0; j + 1 < W; ++j) s << "            win[" << o << "][" << r << "][" << j << "] = win[" << o << "][" << r << "][" << j + 1 << "];\n";
+                    s << "            win[" << o << "][" << r << "][" << W - 1 << "] = Z;\n";
+                } else {
+                    s << "            win[" << o << "][" << r << "][" << ph << "] = Z;\n";
+                }
+            }
+        s << (shift ? "        }\n" : "        } break;\n");
     }
     s << "        }\n        ph = ph + 1 == W ? 0 : ph + 1;\n    }\n}\n";
     std::unique_ptr<KronJitPair> P(new KronJitPair());
@@ -984,6 +994,8 @@ extern "C" __global__ void __launch_bounds__(32 * (NW + 1), 1) ks_pairb(const __
     P->pull = false;
     P->T = 32 * (NW + 1);
     P->nq = R; // (shape key: rows per thread)
+    P->pad = shift ? 1 : 0;
+    if (shift) P->tag = "shifted window";
     P->no = RT;
     P->D = S;
     P->smem = smem;
