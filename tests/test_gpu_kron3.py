@@ -146,7 +146,7 @@ print("worst", worst)
 """
 
 
-@pytest.mark.parametrize("variant", ["b2", "shift", "point", "tile", "tile:22,3,2,8,2,3", "tile:16,4,4,8,2,2", "tile:12,2,3,4,2,4"])
+@pytest.mark.parametrize("variant", ["b2", "b4", "shift", "point", "tile", "tile:22,3,2,8,2,3", "tile:16,4,4,8,2,2", "tile:12,2,3,4,2,4"])
 def test_generated_variants_forced(variant):
     """The row-blocked (ks_pairb) and tile (ks_pairt: partial last tiles,
     boundary blocks of both phases) generated kernels, forced on
@@ -171,6 +171,9 @@ def test_generated_variants_forced(variant):
     if variant == "b2":
         kept = [l for l in out.stderr.splitlines() if "<- kept" in l]
         assert any("rows/thread 2" in l for l in kept), out.stderr[-1500:]   # row-blocked kernel ran
+    if variant == "b4":
+        kept = [l for l in out.stderr.splitlines() if "<- kept" in l]
+        assert any("rows/thread 4" in l for l in kept), out.stderr[-1500:]   # four rows per thread (p = 2 problems)
     if variant == "shift":
         kept = [l for l in out.stderr.splitlines() if "<- kept" in l]
         assert any("shifted window" in l for l in kept), out.stderr[-1500:]  # its shifted-window form ran
